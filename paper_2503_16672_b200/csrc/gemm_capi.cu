@@ -1,0 +1,233 @@
+// C-ABI entry points for the tcgen05 GEMMs (dense, 2:4 sparse, fused K1/K3)
+// plus the shared host utilities (error text, tensor maps, SM count).
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "epilogues.cuh"
+#include "gemm.cuh"
+#include "host_util.h"
+
+namespace s24 {
+
+std::string& last_error_ref() {
+  static thread_local std::string msg;
+  return msg;
+}
+
+int num_sms() {
+  static std::mutex mu;
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (!aligned16(base) || (ld * 2) % 16 != 0)
+    return fail(S24_ERR_DIMENSION, "operand base/leading dimension must be 16-byte aligned");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(S24_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return S24_OK;
+}
+
+// ---------------------------------------------------------------------------
+template <class Cfg, class Epi>
+static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
+  if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
+  CUtensorMap ma, mb;
+  int rc;
+  // A
+  if constexpr (Cfg::A_MN) {
+    rc = make_map_bf16(&ma, A, M, K, lda, 64, Cfg::BK);
+  } else if constexpr (Cfg::SPARSE) {
+    const int64_t mpad = (M + 127) / 128 * 128;
+    rc = make_map_bf16(&ma, A, K / 2, mpad, K / 2, 64, Cfg::BM);
+  } else {
+    rc = make_map_bf16(&ma, A, K, M, lda, 64, Cfg::BM);
+  }
+  if (rc) return rc;
+  // B
+  if constexpr (Cfg::B_MN) {
+    rc = make_map_bf16(&mb, B, N, K, ldb, 64, Cfg::BK);
+  } else {
+    rc = make_map_bf16(&mb, B, K, N, ldb, 64, Cfg::BN);
+  }
+  if (rc) return rc;
+
+  GemmShape sh;
+  sh.M = static_cast<int>(M);
+  sh.N = static_cast<int>(N);
+  sh.K = static_cast<int>(K);
+  sh.tiles_m = static_cast<int>((M + Cfg::BM - 1) / Cfg::BM);
+  sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
+  sh.group_m = 16;
+  sh.meta = meta;
+  const int tiles = sh.tiles_m * sh.tiles_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+
+  auto kern = gemm_kernel<Cfg, Epi>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  kern<<<grid, 256, Cfg::SMEM_BYTES, stream>>>(ma, mb, sh, ep);
+  return check_launch("gemm_kernel");
+}
+
+// tile configurations
+using DenseKN = GemmCfg<false, false, true, 256, 4, 2>;   // A K-major, B MN-major
+using DenseKK = GemmCfg<false, false, false, 256, 4, 2>;  // A K-major, B K-major
+using DenseMM = GemmCfg<false, true, true, 256, 4, 2>;    // A MN-major, B MN-major
+using DenseMK = GemmCfg<false, true, false, 256, 4, 2>;   // A MN-major, B K-major
+using SparseN = GemmCfg<true, false, true, 128, 4, 2>;    // sparse A, B MN-major
+using SparseK = GemmCfg<true, false, false, 128, 4, 2>;   // sparse A, B K-major
+
+template <class Epi>
+static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
+                          int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st) {
+  if (!a_mn && b_mn) return launch_gemm<DenseKN, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
+  if (!a_mn && !b_mn) return launch_gemm<DenseKK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
+  if (a_mn && b_mn) return launch_gemm<DenseMM, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
+  return launch_gemm<DenseMK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
+}
+
+template <class Epi>
+static int dispatch_sparse(int b_mn, const void* A, const uint8_t* meta, const void* B, int64_t ldb, int64_t M,
+                           int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st) {
+  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st);
+  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st);
+}
+
+static int check_common(int64_t M, int64_t N, int64_t K, int64_t lda, int a_mn, int64_t ldb, int b_mn) {
+  if (M < 0 || N < 0 || K < 0) return fail(S24_ERR_DIMENSION, "negative GEMM dimension");
+  if (N % 32 != 0) return fail(S24_ERR_DIMENSION, "N = %lld must be a multiple of 32", (long long)N);
+  if (lda < (a_mn ? M : K)) return fail(S24_ERR_DIMENSION, "lda too small");
+  if (ldb < (b_mn ? N : K)) return fail(S24_ERR_DIMENSION, "ldb too small");
+  return S24_OK;
+}
+
+template <class Fn>
+static int with_out(int out_dtype, Fn&& fn) {
+  if (out_dtype == S24_F32) return fn(static_cast<float*>(nullptr));
+  if (out_dtype == S24_BF16) return fn(static_cast<__nv_bfloat16*>(nullptr));
+  return fail(S24_ERR_PRECISION, "unsupported output dtype %d", out_dtype);
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+extern "C" {
+
+const char* s24_last_error(void) { return last_error_ref().c_str(); }
+const char* s24_version(void) { return "s24-b200 0.1.0 (sm_100a)"; }
+
+int64_t s24_meta_hw_bytes(int64_t rows, int64_t cols) {
+  const int64_t rp = (rows + 127) / 128 * 128;
+  return rp * cols / 8;
+}
+
+int s24_gemm(const void* A, int a_mn_major, int64_t lda, const void* B, int b_mn_major, int64_t ldb, int64_t M,
+             int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
+             int64_t d_rows_valid, void* stream) {
+  int rc = check_common(M, N, K, lda, a_mn_major, ldb, b_mn_major);
+  if (rc) return rc;
+  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
+                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid)};
+    return dispatch_dense<EpiStore<OutT>>(a_mn_major, b_mn_major, A, lda, B, ldb, M, N, K, ep,
+                                          static_cast<cudaStream_t>(stream));
+  });
+}
+
+int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
+             int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
+             int64_t d_rows_valid, void* stream) {
+  int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
+  if (rc) return rc;
+  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
+  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
+                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid)};
+    return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep,
+                                           static_cast<cudaStream_t>(stream));
+  });
+}
+
+int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
+                        int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
+                        float* y_dbg, void* stream) {
+  int rc = check_common(M, N, K, ldx, 0, ldw1, 1);
+  if (rc) return rc;
+  if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
+  EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N)};
+  return launch_gemm<DenseKN, EpiFwd1>(x, ldx, w1, ldw1, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+}
+
+int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
+                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* stream) {
+  int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
+  if (rc) return rc;
+  if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
+  EpiBwd1::Params ep{static_cast<const __nv_bfloat16*>(act_vals), act_meta, static_cast<__nv_bfloat16*>(g_vals),
+                     static_cast<int>(N)};
+  return launch_gemm<DenseKK, EpiBwd1>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+}
+
+int s24_gemm_relu2(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N, int64_t K,
+                   void* act, int64_t ld_act, void* stream) {
+  int rc = check_common(M, N, K, ldx, 0, ldw1, 1);
+  if (rc) return rc;
+  EpiRelu2::Params ep{static_cast<__nv_bfloat16*>(act), ld_act};
+  return launch_gemm<DenseKN, EpiRelu2>(x, ldx, w1, ldw1, M, N, K, nullptr, ep,
+                                        static_cast<cudaStream_t>(stream));
+}
+
+int s24_gemm_dact(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N, int64_t K,
+                  const void* act, int64_t ld_act, void* gpre, int64_t ld_g, void* stream) {
+  int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
+  if (rc) return rc;
+  EpiDact::Params ep{static_cast<const __nv_bfloat16*>(act), ld_act, static_cast<__nv_bfloat16*>(gpre), ld_g};
+  return launch_gemm<DenseKK, EpiDact>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// Host-side helpers shared by the C-ABI translation units: thread-local error
+// text, status codes, TMA tensor-map encoding through the driver entry point
+// (no link-time libcuda dependency) and device attribute caching.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "../../include/s24.h"
+
+namespace s24 {
+
+std::string& last_error_ref();
+
+inline int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  last_error_ref() = buf;
+  return code;
+}
+
+inline int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(S24_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return S24_OK;
+}
+
+int num_sms();
+
+// 2-D bf16 tensor map: inner dim (contiguous) `inner` elements, `outer` rows,
+// row pitch `ld` elements; box {box_inner, box_outer}; 128B swizzle.
+int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_inner, uint32_t box_outer);
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace s24

@@ -1,0 +1,690 @@
+// HBM-bound 2:4 kernels and their C-ABI entry points:
+//   token-wise / feature-wise sparsify, mask compression, decompress,
+//   metadata converters, row gather (token permutation), the split plan (K7)
+//   and the feature-wise transposed split (K4).
+#include <cuda_bf16.h>
+
+#include <type_traits>
+
+#include "host_util.h"
+#include "meta.cuh"
+#include "ptx.cuh"
+
+namespace s24 {
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p) {
+  if constexpr (std::is_same_v<T, float>)
+    return *p;
+  else
+    return __bfloat162float(*p);
+}
+
+template <typename T>
+__device__ __forceinline__ void stf(T* p, float v) {
+  if constexpr (std::is_same_v<T, float>)
+    *p = v;
+  else
+    *p = __float2bfloat16_rn(v);
+}
+
+__device__ __forceinline__ unsigned long long block_sum_u64_to(unsigned long long v, unsigned long long* dst) {
+  // warp reduce then one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// token-wise sparsify: each thread owns GPT consecutive groups of one row.
+template <typename T, int GPT>
+__global__ void k_sparsify_token(const T* __restrict__ a, long long rows, long long cols, long long lda,
+                                 __nv_bfloat16* __restrict__ vals, uint8_t* __restrict__ meta_ref,
+                                 uint8_t* __restrict__ meta_hw, uint8_t* __restrict__ mask,
+                                 unsigned long long* stats) {
+  const long long chunks_per_row = cols / (4 * GPT);
+  const long long total = rows * chunks_per_row;
+  unsigned long long nb = 0, na = 0;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < total;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / chunks_per_row;
+    const long long c0 = (w - r * chunks_per_row) * 4 * GPT;
+    const T* src = a + r * lda + c0;
+    uint32_t m16 = 0;
+#pragma unroll
+    for (int g = 0; g < GPT; ++g) {
+      const float x0 = ldf(src + 4 * g), x1 = ldf(src + 4 * g + 1), x2 = ldf(src + 4 * g + 2),
+                  x3 = ldf(src + 4 * g + 3);
+      nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
+      const uint32_t keep = top2_keep_mask(x0, x1, x2, x3);
+      const uint32_t nib = keep_to_nibble(keep);
+      const float v0 = sel4(x0, x1, x2, x3, nib & 3u), v1 = sel4(x0, x1, x2, x3, nib >> 2);
+      na += (v0 != 0.f) + (v1 != 0.f);
+      const long long gi = c0 / 4 + g;
+      reinterpret_cast<__nv_bfloat162*>(vals + r * (cols / 2))[gi] = __floats2bfloat162_rn(v0, v1);
+      if (meta_ref) {
+        meta_ref[(r * (cols / 4) + gi) * 2] = static_cast<uint8_t>(nib & 3u);
+        meta_ref[(r * (cols / 4) + gi) * 2 + 1] = static_cast<uint8_t>(nib >> 2);
+      }
+      if (mask) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mask[r * cols + c0 + 4 * g + i] = (keep >> i) & 1u;
+      }
+      m16 |= nib << (4 * g);
+    }
+    if constexpr (GPT == 4) {
+      if (meta_hw)
+        *reinterpret_cast<uint16_t*>(meta_hw + meta_hw_halfword_offset(r, c0 / 16, cols)) = (uint16_t)m16;
+    }
+  }
+  if (stats) {
+    block_sum_u64_to(nb, stats);
+    block_sum_u64_to(na, stats + 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// feature-wise sparsify: thread owns GPT consecutive row-groups of column j.
+template <typename T, int GPT>
+__global__ void k_sparsify_feature(const T* __restrict__ a, long long rows, long long cols, long long lda,
+                                   __nv_bfloat16* __restrict__ vals_t, uint8_t* __restrict__ meta_ref,
+                                   uint8_t* __restrict__ meta_hw, uint8_t* __restrict__ mask,
+                                   unsigned long long* stats) {
+  const long long chunks = rows / (4 * GPT);
+  const long long total = chunks * cols;
+  unsigned long long nb = 0, na = 0;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < total;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long ch = w / cols;
+    const long long j = w - ch * cols;
+    uint32_t m16 = 0;
+#pragma unroll
+    for (int g = 0; g < GPT; ++g) {
+      const long long gi = ch * GPT + g;  // row group index
+      const long long r0 = gi * 4;
+      const float x0 = ldf(a + r0 * lda + j), x1 = ldf(a + (r0 + 1) * lda + j), x2 = ldf(a + (r0 + 2) * lda + j),
+                  x3 = ldf(a + (r0 + 3) * lda + j);
+      nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
+      const uint32_t keep = top2_keep_mask(x0, x1, x2, x3);
+      const uint32_t nib = keep_to_nibble(keep);
+      const float v0 = sel4(x0, x1, x2, x3, nib & 3u), v1 = sel4(x0, x1, x2, x3, nib >> 2);
+      na += (v0 != 0.f) + (v1 != 0.f);
+      reinterpret_cast<__nv_bfloat162*>(vals_t + j * (rows / 2))[gi] = __floats2bfloat162_rn(v0, v1);
+      if (meta_ref) {
+        meta_ref[(gi * cols + j) * 2] = static_cast<uint8_t>(nib & 3u);
+        meta_ref[(gi * cols + j) * 2 + 1] = static_cast<uint8_t>(nib >> 2);
+      }
+      if (mask) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mask[(r0 + i) * cols + j] = (keep >> i) & 1u;
+      }
+      m16 |= nib << (4 * g);
+    }
+    if constexpr (GPT == 4) {
+      if (meta_hw)
+        *reinterpret_cast<uint16_t*>(meta_hw + meta_hw_halfword_offset(j, ch, rows)) = (uint16_t)m16;
+    }
+  }
+  if (stats) {
+    block_sum_u64_to(nb, stats);
+    block_sum_u64_to(na, stats + 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// compress with a given mask (exact when supp(a) is inside the mask)
+template <typename T>
+__global__ void k_compress_mask(const T* __restrict__ a, long long rows, long long cols, long long lda,
+                                const uint8_t* __restrict__ mask, __nv_bfloat16* __restrict__ vals,
+                                uint8_t* __restrict__ meta_ref, uint8_t* __restrict__ meta_hw, int* bad) {
+  const long long groups = rows * (cols / 4);
+  int my_bad = 0;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < groups;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / (cols / 4);
+    const long long gi = w - r * (cols / 4);
+    const long long c0 = gi * 4;
+    uint32_t keep = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) keep |= (mask[r * cols + c0 + i] ? 1u : 0u) << i;
+    if (__popc(keep) != 2) {
+      ++my_bad;
+      keep = 3u;
+    }
+    const uint32_t nib = keep_to_nibble(keep);
+    const T* src = a + r * lda + c0;
+    const float v0 = ldf(src + (nib & 3u)), v1 = ldf(src + (nib >> 2));
+    reinterpret_cast<__nv_bfloat162*>(vals + r * (cols / 2))[gi] = __floats2bfloat162_rn(v0, v1);
+    if (meta_ref) {
+      meta_ref[w * 2] = static_cast<uint8_t>(nib & 3u);
+      meta_ref[w * 2 + 1] = static_cast<uint8_t>(nib >> 2);
+    }
+    if (meta_hw) {
+      // nibble-granular write: 4 groups share a halfword -> atomic OR on the
+      // containing 32-bit word (caller zeroes meta_hw)
+      const uint64_t off = meta_hw_halfword_offset(r, c0 / 16, cols);
+      const uint32_t shift = 4u * (gi & 3) + 8u * (off & 2);
+      atomicOr(reinterpret_cast<unsigned int*>(meta_hw + (off & ~3ull)), nib << shift);
+    }
+  }
+  if (bad && my_bad) atomicAdd(bad, my_bad);
+}
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t read_nibble_token(const uint8_t* meta_ref, const uint8_t* meta_hw,
+                                                      long long r, long long gi, long long cols) {
+  if (meta_ref) {
+    const long long o = (r * (cols / 4) + gi) * 2;
+    return meta_ref[o] | (meta_ref[o + 1] << 2);
+  }
+  const uint16_t h = *reinterpret_cast<const uint16_t*>(meta_hw + meta_hw_halfword_offset(r, gi / 4, cols));
+  return (h >> (4 * (gi & 3))) & 0xFu;
+}
+
+template <typename OutT>
+__global__ void k_decompress_token(const __nv_bfloat16* __restrict__ vals, const uint8_t* __restrict__ meta_ref,
+                                   const uint8_t* __restrict__ meta_hw, long long rows, long long cols,
+                                   OutT* __restrict__ out, long long ldo) {
+  const long long groups = rows * (cols / 4);
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < groups;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / (cols / 4);
+    const long long gi = w - r * (cols / 4);
+    const uint32_t nib = read_nibble_token(meta_ref, meta_hw, r, gi, cols);
+    const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(vals + r * (cols / 2))[gi];
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    o[nib & 3u] = __bfloat162float(v.x);
+    o[nib >> 2] = __bfloat162float(v.y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) stf(out + r * ldo + gi * 4 + i, o[i]);
+  }
+}
+
+template <typename OutT>
+__global__ void k_decompress_feature(const __nv_bfloat16* __restrict__ vals_t, const uint8_t* __restrict__ meta_ref,
+                                     const uint8_t* __restrict__ meta_hw, long long rows, long long cols,
+                                     OutT* __restrict__ out, long long ldo) {
+  const long long groups = (rows / 4) * cols;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < groups;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long gi = w / cols;
+    const long long j = w - gi * cols;
+    uint32_t nib;
+    if (meta_ref) {
+      nib = meta_ref[(gi * cols + j) * 2] | (meta_ref[(gi * cols + j) * 2 + 1] << 2);
+    } else {
+      const uint16_t h = *reinterpret_cast<const uint16_t*>(meta_hw + meta_hw_halfword_offset(j, gi / 4, rows));
+      nib = (h >> (4 * (gi & 3))) & 0xFu;
+    }
+    const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(vals_t + j * (rows / 2))[gi];
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    o[nib & 3u] = __bfloat162float(v.x);
+    o[nib >> 2] = __bfloat162float(v.y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) stf(out + (gi * 4 + i) * ldo + j, o[i]);
+  }
+}
+
+__global__ void k_meta_hw_to_ref(const uint8_t* __restrict__ hw, long long rows, long long cols,
+                                 uint8_t* __restrict__ ref) {
+  const long long groups = rows * (cols / 4);
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < groups;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / (cols / 4);
+    const long long gi = w - r * (cols / 4);
+    const uint32_t nib = read_nibble_token(nullptr, hw, r, gi, cols);
+    ref[w * 2] = nib & 3u;
+    ref[w * 2 + 1] = nib >> 2;
+  }
+}
+
+__global__ void k_meta_ref_to_hw(const uint8_t* __restrict__ ref, long long rows, long long cols,
+                                 uint8_t* __restrict__ hw) {
+  const long long halves = rows * (cols / 16);
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < halves;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long r = w / (cols / 16);
+    const long long q = w - r * (cols / 16);
+    uint32_t h = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const long long o = (r * (cols / 4) + q * 4 + g) * 2;
+      h |= (ref[o] | (ref[o + 1] << 2)) << (4 * g);
+    }
+    *reinterpret_cast<uint16_t*>(hw + meta_hw_halfword_offset(r, q, cols)) = (uint16_t)h;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: row gather, one warp per row, 16-byte vectors
+__global__ void k_gather_rows(const uint8_t* __restrict__ in, long long rows, long long row_bytes,
+                              long long ld_in, const int* __restrict__ src, uint8_t* __restrict__ out,
+                              long long ld_out) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const long long vecs = row_bytes >> 4;
+  for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const uint4* s = reinterpret_cast<const uint4*>(in + (long long)src[r] * ld_in);
+    uint4* d = reinterpret_cast<uint4*>(out + r * ld_out);
+    for (long long v = lane; v < vecs; v += 32) d[v] = s[v];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7: split plan. One CTA of 1024 threads. Key of feature j = (count_j << 16)
+// | j (unique, orders by (count, index) exactly like the stable argsort in
+// splitgemm.py:49). An 8-bit MSB radix select finds the key of rank
+// n_sparse-1; features with key <= it are sparse. A block scan then emits the
+// ascending index lists (splitgemm.py:50-51) and the per-feature positions.
+__global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts, int h, int n_sparse,
+                                               int* __restrict__ sparse_idx, int* __restrict__ dense_idx,
+                                               int* __restrict__ feat_pos) {
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long sh_prefix;
+  __shared__ int sh_rank;
+  __shared__ int warp_tot[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (h + 1023) / 1024;
+  const int j0 = min(h, tid * per), j1 = min(h, j0 + per);
+
+  unsigned long long thr = 0;  // threshold key (inclusive); unused when n_sparse == 0
+  if (n_sparse > 0) {
+    if (tid == 0) {
+      sh_prefix = 0;
+      sh_rank = n_sparse - 1;
+    }
+    unsigned long long maskbits = 0;
+    for (int pass = 0; pass < 6; ++pass) {
+      const int shift = 40 - 8 * pass;
+      for (int b = tid; b < 256; b += 1024) hist[b] = 0;
+      __syncthreads();
+      const unsigned long long prefix = sh_prefix;
+      for (int j = j0; j < j1; ++j) {
+        const unsigned long long key = (static_cast<unsigned long long>(static_cast<unsigned>(counts[j])) << 16) | j;
+        if ((key & maskbits) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (wid == 0) {
+        unsigned int loc[8], s = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          loc[i] = hist[lane * 8 + i];
+          s += loc[i];
+        }
+        unsigned int inc = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        const unsigned int exc = inc - s;
+        const int rank = sh_rank;
+        if (static_cast<unsigned>(rank) >= exc && static_cast<unsigned>(rank) < inc) {
+          unsigned int c = exc;
+          int b = 7;
+          for (int i = 0; i < 8; ++i) {
+            if (static_cast<unsigned>(rank) < c + loc[i]) {
+              b = i;
+              break;
+            }
+            c += loc[i];
+          }
+          sh_rank = rank - static_cast<int>(c);
+          sh_prefix = prefix | (static_cast<unsigned long long>(lane * 8 + b) << shift);
+        }
+      }
+      maskbits |= 255ull << shift;
+      __syncthreads();
+    }
+    thr = sh_prefix;
+  }
+
+  // flags and block-wide exclusive scan of sparse counts in index order
+  int my_sparse = 0;
+  for (int j = j0; j < j1; ++j) {
+    const unsigned long long key = (static_cast<unsigned long long>(static_cast<unsigned>(counts[j])) << 16) | j;
+    my_sparse += (n_sparse > 0 && key <= thr) ? 1 : 0;
+  }
+  int inc = my_sparse;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = warp_tot[lane];
+    int vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, vi, o);
+      if (lane >= o) vi += t;
+    }
+    warp_tot[lane] = vi - v;
+  }
+  __syncthreads();
+  int s_off = warp_tot[wid] + inc - my_sparse;
+  int d_off = j0 - s_off;
+  for (int j = j0; j < j1; ++j) {
+    const unsigned long long key = (static_cast<unsigned long long>(static_cast<unsigned>(counts[j])) << 16) | j;
+    if (n_sparse > 0 && key <= thr) {
+      sparse_idx[s_off] = j;
+      feat_pos[j] = s_off;
+      ++s_off;
+    } else {
+      dense_idx[d_off] = j;
+      feat_pos[j] = -d_off - 1;
+      ++d_off;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: feature-wise transposed split of a token-wise compressed [n, h] matrix.
+// CTA tile: 128 tokens x 128 features. Phase 1 decompresses the tile into
+// smem (row pitch 272 B, conflict-free 16 B stores); phase 2 walks each
+// feature column in token groups of 4 and emits either the feature-wise 2:4
+// form (sparse features, K-major along tokens + hw metadata) or the dense
+// column (dense features), both transposed so the dW GEMMs read K-major A.
+constexpr int K4_PITCH = 136;  // bf16 elements per smem row (128 + 8 pad)
+
+__global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __restrict__ vals,
+                                                       const uint8_t* __restrict__ meta_hw, int n, int h,
+                                                       const int* __restrict__ feat_pos,
+                                                       __nv_bfloat16* __restrict__ vs, uint8_t* __restrict__ es,
+                                                       __nv_bfloat16* __restrict__ vd,
+                                                       unsigned long long* stats) {
+  __shared__ __align__(16) __nv_bfloat16 tile[128 * K4_PITCH];
+  const int f0 = blockIdx.x * 128, t0 = blockIdx.y * 128;
+  const int tid = threadIdx.x;
+  {
+    // phase 1: 2 threads per token row, 64 features (4 halfwords) each
+    const int tr = tid >> 1, half = tid & 1;
+    const int t = t0 + tr;
+    const __nv_bfloat16* src = vals + static_cast<long long>(t) * (h / 2) + f0 / 2 + half * 32;
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = reinterpret_cast<const uint4*>(src)[i];
+      w[4 * i] = v.x;
+      w[4 * i + 1] = v.y;
+      w[4 * i + 2] = v.z;
+      w[4 * i + 3] = v.w;
+    }
+    __nv_bfloat16* dst = tile + tr * K4_PITCH + half * 64;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t m16 = *reinterpret_cast<const uint16_t*>(
+          meta_hw + meta_hw_halfword_offset(t, (f0 + half * 64) / 16 + q, h));
+      uint32_t outw[8];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint32_t nib = (m16 >> (4 * g)) & 0xFu;
+        const uint32_t pair = w[q * 4 + g];
+        const uint32_t lo = pair & 0xFFFFu, hi = pair >> 16;
+        uint32_t e[4] = {0u, 0u, 0u, 0u};
+        e[nib & 3u] = lo;
+        e[nib >> 2] = hi;
+        outw[2 * g] = e[0] | (e[1] << 16);
+        outw[2 * g + 1] = e[2] | (e[3] << 16);
+      }
+      uint4* d4 = reinterpret_cast<uint4*>(dst + q * 16);
+      d4[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+      d4[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
+    }
+  }
+  __syncthreads();
+  // phase 2: thread = (feature j, token half); 16 groups of 4 tokens
+  const int j = tid & 127, th = tid >> 7;
+  const int pos = feat_pos[f0 + j];
+  unsigned long long nb = 0, na = 0;
+  if (pos >= 0) {
+    uint32_t packed[16];
+    uint32_t m16[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int g = 0; g < 16; ++g) {
+      const int tr = th * 64 + 4 * g;
+      const float x0 = __bfloat162float(tile[tr * K4_PITCH + j]);
+      const float x1 = __bfloat162float(tile[(tr + 1) * K4_PITCH + j]);
+      const float x2 = __bfloat162float(tile[(tr + 2) * K4_PITCH + j]);
+      const float x3 = __bfloat162float(tile[(tr + 3) * K4_PITCH + j]);
+      nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
+      const uint32_t keep = top2_keep_mask(x0, x1, x2, x3);
+      const uint32_t nib = keep_to_nibble(keep);
+      const float v0 = sel4(x0, x1, x2, x3, nib & 3u), v1 = sel4(x0, x1, x2, x3, nib >> 2);
+      na += (v0 != 0.f) + (v1 != 0.f);
+      packed[g] = pack_bf16x2(v0, v1);
+      m16[g >> 2] |= nib << (4 * (g & 3));
+    }
+    uint4* dst = reinterpret_cast<uint4*>(vs + static_cast<long long>(pos) * (n / 2) + t0 / 2 + th * 32);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint16_t*>(es + meta_hw_halfword_offset(pos, (t0 + th * 64) / 16 + q, n)) =
+          static_cast<uint16_t>(m16[q]);
+  } else {
+    const int dpos = -pos - 1;
+    uint32_t wds[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int tr = th * 64 + 2 * i;
+      const uint32_t lo = *reinterpret_cast<const uint16_t*>(&tile[tr * K4_PITCH + j]);
+      const uint32_t hi = *reinterpret_cast<const uint16_t*>(&tile[(tr + 1) * K4_PITCH + j]);
+      wds[i] = lo | (hi << 16);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(vd + static_cast<long long>(dpos) * n + t0 + th * 64);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = make_uint4(wds[4 * i], wds[4 * i + 1], wds[4 * i + 2], wds[4 * i + 3]);
+  }
+  if (stats) {
+    block_sum_u64_to(nb, stats);
+    block_sum_u64_to(na, stats + 1);
+  }
+}
+
+static int grid_for(long long work, int block) {
+  long long g = (work + block - 1) / block;
+  const long long cap = static_cast<long long>(num_sms()) * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+extern "C" {
+
+int s24_sparsify_token(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda, void* vals,
+                       uint8_t* meta_ref, uint8_t* meta_hw, uint8_t* mask, unsigned long long* stats,
+                       void* stream) {
+  if (rows < 0 || cols < 0) return fail(S24_ERR_DIMENSION, "negative shape");
+  if (cols % 4 != 0) return fail(S24_ERR_DIMENSION, "token-wise groups need cols %% 4 == 0, got %lld", (long long)cols);
+  if (lda < cols) return fail(S24_ERR_DIMENSION, "lda < cols");
+  if (meta_hw && cols % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs cols %% 128 == 0");
+  if (dtype != S24_F32 && dtype != S24_BF16) return fail(S24_ERR_PRECISION, "unsupported dtype");
+  if (rows == 0 || cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const bool q = cols % 16 == 0;
+  const long long work = rows * cols / (q ? 16 : 4);
+  const int g = grid_for(work, 256);
+  if (dtype == S24_F32) {
+    if (q)
+      k_sparsify_token<float, 4><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
+                                                     static_cast<__nv_bfloat16*>(vals), meta_ref, meta_hw, mask, stats);
+    else
+      k_sparsify_token<float, 1><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
+                                                     static_cast<__nv_bfloat16*>(vals), meta_ref, nullptr, mask, stats);
+  } else {
+    if (q)
+      k_sparsify_token<__nv_bfloat16, 4><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
+                                                             static_cast<__nv_bfloat16*>(vals), meta_ref, meta_hw,
+                                                             mask, stats);
+    else
+      k_sparsify_token<__nv_bfloat16, 1><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
+                                                             static_cast<__nv_bfloat16*>(vals), meta_ref, nullptr,
+                                                             mask, stats);
+  }
+  return check_launch("k_sparsify_token");
+}
+
+int s24_sparsify_feature(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda, void* vals_t,
+                         uint8_t* meta_ref, uint8_t* meta_hw, uint8_t* mask, unsigned long long* stats,
+                         void* stream) {
+  if (rows < 0 || cols < 0) return fail(S24_ERR_DIMENSION, "negative shape");
+  if (rows % 4 != 0) return fail(S24_ERR_DIMENSION, "feature-wise groups need rows %% 4 == 0, got %lld", (long long)rows);
+  if (lda < cols) return fail(S24_ERR_DIMENSION, "lda < cols");
+  if (meta_hw && rows % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs rows %% 128 == 0");
+  if (dtype != S24_F32 && dtype != S24_BF16) return fail(S24_ERR_PRECISION, "unsupported dtype");
+  if (rows == 0 || cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const bool q = rows % 16 == 0;
+  const long long work = rows * cols / (q ? 16 : 4);
+  const int g = grid_for(work, 256);
+  if (dtype == S24_F32) {
+    if (q)
+      k_sparsify_feature<float, 4><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
+                                                       static_cast<__nv_bfloat16*>(vals_t), meta_ref, meta_hw, mask, stats);
+    else
+      k_sparsify_feature<float, 1><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
+                                                       static_cast<__nv_bfloat16*>(vals_t), meta_ref, nullptr, mask, stats);
+  } else {
+    if (q)
+      k_sparsify_feature<__nv_bfloat16, 4><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
+                                                               static_cast<__nv_bfloat16*>(vals_t), meta_ref, meta_hw,
+                                                               mask, stats);
+    else
+      k_sparsify_feature<__nv_bfloat16, 1><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
+                                                               static_cast<__nv_bfloat16*>(vals_t), meta_ref, nullptr,
+                                                               mask, stats);
+  }
+  return check_launch("k_sparsify_feature");
+}
+
+int s24_compress_token_with_mask(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda,
+                                 const uint8_t* mask, void* vals, uint8_t* meta_ref, uint8_t* meta_hw,
+                                 int* bad_groups, void* stream) {
+  if (rows < 0 || cols < 0 || cols % 4 != 0) return fail(S24_ERR_DIMENSION, "mask/matrix shapes unusable");
+  if (meta_hw && cols % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs cols %% 128 == 0");
+  if (rows == 0 || cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  if (meta_hw) {
+    const int64_t bytes = s24_meta_hw_bytes(rows, cols);
+    cudaMemsetAsync(meta_hw, 0, bytes, st);
+  }
+  const int g = grid_for(rows * cols / 4, 256);
+  if (dtype == S24_F32)
+    k_compress_mask<float><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda, mask,
+                                              static_cast<__nv_bfloat16*>(vals), meta_ref, meta_hw, bad_groups);
+  else if (dtype == S24_BF16)
+    k_compress_mask<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda, mask,
+                                                      static_cast<__nv_bfloat16*>(vals), meta_ref, meta_hw, bad_groups);
+  else
+    return fail(S24_ERR_PRECISION, "unsupported dtype");
+  return check_launch("k_compress_mask");
+}
+
+int s24_decompress_token(const void* vals, const uint8_t* meta_ref, const uint8_t* meta_hw, int64_t rows,
+                         int64_t cols, void* out, int out_dtype, int64_t ldo, void* stream) {
+  if (rows < 0 || cols < 0 || cols % 4 != 0) return fail(S24_ERR_DIMENSION, "bad shape for decompress");
+  if ((meta_ref == nullptr) == (meta_hw == nullptr)) return fail(S24_ERR_DIMENSION, "exactly one metadata form");
+  if (meta_hw && cols % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs cols %% 128 == 0");
+  if (rows == 0 || cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(rows * cols / 4, 256);
+  auto v = static_cast<const __nv_bfloat16*>(vals);
+  if (out_dtype == S24_F32)
+    k_decompress_token<float><<<g, 256, 0, st>>>(v, meta_ref, meta_hw, rows, cols, static_cast<float*>(out), ldo);
+  else if (out_dtype == S24_BF16)
+    k_decompress_token<__nv_bfloat16><<<g, 256, 0, st>>>(v, meta_ref, meta_hw, rows, cols,
+                                                         static_cast<__nv_bfloat16*>(out), ldo);
+  else
+    return fail(S24_ERR_PRECISION, "unsupported dtype");
+  return check_launch("k_decompress_token");
+}
+
+int s24_decompress_feature(const void* vals_t, const uint8_t* meta_ref, const uint8_t* meta_hw, int64_t rows,
+                           int64_t cols, void* out, int out_dtype, int64_t ldo, void* stream) {
+  if (rows < 0 || cols < 0 || rows % 4 != 0) return fail(S24_ERR_DIMENSION, "bad shape for decompress");
+  if ((meta_ref == nullptr) == (meta_hw == nullptr)) return fail(S24_ERR_DIMENSION, "exactly one metadata form");
+  if (meta_hw && rows % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs rows %% 128 == 0");
+  if (rows == 0 || cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(rows * cols / 4, 256);
+  auto v = static_cast<const __nv_bfloat16*>(vals_t);
+  if (out_dtype == S24_F32)
+    k_decompress_feature<float><<<g, 256, 0, st>>>(v, meta_ref, meta_hw, rows, cols, static_cast<float*>(out), ldo);
+  else if (out_dtype == S24_BF16)
+    k_decompress_feature<__nv_bfloat16><<<g, 256, 0, st>>>(v, meta_ref, meta_hw, rows, cols,
+                                                           static_cast<__nv_bfloat16*>(out), ldo);
+  else
+    return fail(S24_ERR_PRECISION, "unsupported dtype");
+  return check_launch("k_decompress_feature");
+}
+
+int s24_meta_hw_to_ref(const uint8_t* meta_hw, int64_t rows, int64_t cols, uint8_t* meta_ref, void* stream) {
+  if (rows < 0 || cols % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs cols %% 128 == 0");
+  if (rows == 0 || cols == 0) return S24_OK;
+  k_meta_hw_to_ref<<<grid_for(rows * cols / 4, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(meta_hw, rows, cols,
+                                                                                                 meta_ref);
+  return check_launch("k_meta_hw_to_ref");
+}
+
+int s24_meta_ref_to_hw(const uint8_t* meta_ref, int64_t rows, int64_t cols, uint8_t* meta_hw, void* stream) {
+  if (rows < 0 || cols % 128 != 0) return fail(S24_ERR_DIMENSION, "hw metadata needs cols %% 128 == 0");
+  if (rows == 0 || cols == 0) return S24_OK;
+  k_meta_ref_to_hw<<<grid_for(rows * cols / 16, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(meta_ref, rows,
+                                                                                                  cols, meta_hw);
+  return check_launch("k_meta_ref_to_hw");
+}
+
+int s24_gather_rows(const void* in, int64_t rows, int64_t row_bytes, int64_t ld_in_bytes, const int* src,
+                    void* out, int64_t ld_out_bytes, void* stream) {
+  if (rows < 0 || row_bytes < 0) return fail(S24_ERR_DIMENSION, "negative shape");
+  if (row_bytes % 16 != 0 || ld_in_bytes % 16 != 0 || ld_out_bytes % 16 != 0 || !aligned16(in) || !aligned16(out))
+    return fail(S24_ERR_DIMENSION, "row gather needs 16-byte aligned rows");
+  if (rows == 0 || row_bytes == 0) return S24_OK;
+  const int g = grid_for(rows * 32, 256);
+  k_gather_rows<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint8_t*>(in), rows, row_bytes,
+                                                                  ld_in_bytes, src, static_cast<uint8_t*>(out),
+                                                                  ld_out_bytes);
+  return check_launch("k_gather_rows");
+}
+
+int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, int* dense_idx, int* feat_pos,
+             void* stream) {
+  if (h < 0 || h > 65536) return fail(S24_ERR_DIMENSION, "plan supports 0 <= h <= 65536");
+  if (n_sparse < 0 || n_sparse > h) return fail(S24_ERR_CONFIG, "n_sparse out of range");
+  if (h == 0) return S24_OK;
+  k_plan<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(counts, static_cast<int>(h), static_cast<int>(n_sparse),
+                                                            sparse_idx, dense_idx, feat_pos);
+  return check_launch("k_plan");
+}
+
+int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
+                      int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
+                      unsigned long long* stats, void* stream) {
+  if (n % 128 != 0 || h % 128 != 0) return fail(S24_ERR_DIMENSION, "feature split needs n, h multiples of 128");
+  if (n_sparse + n_dense != h) return fail(S24_ERR_STATE, "plan sizes do not add up to h");
+  if (n == 0 || h == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int64_t sp_pad = (n_sparse + 127) / 128 * 128, d_pad = (n_dense + 127) / 128 * 128;
+  // padding rows: zero values, valid metadata (i0=0, i1=1 -> nibble 0x4)
+  if (sp_pad > n_sparse) {
+    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vs) + n_sparse * (n / 2), 0, (sp_pad - n_sparse) * (n / 2) * 2, st);
+    cudaMemsetAsync(es + (n_sparse / 128) * (n / 128) * 2048, 0x44, (n / 128) * 2048, st);
+  }
+  if (d_pad > n_dense && vd)
+    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vd) + n_dense * n, 0, (d_pad - n_dense) * n * 2, st);
+  dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
+  k_feature_split<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n),
+                                        static_cast<int>(h), feat_pos, static_cast<__nv_bfloat16*>(vs), es,
+                                        static_cast<__nv_bfloat16*>(vd), stats);
+  return check_launch("k_feature_split");
+}
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+"""Kernel-level parity of libs24.so on the GPU, called through the C ABI.
+
+Bit-exact checks (masks, metadata, values given identical fp32 inputs, counts,
+plans, permutation gathers) use the numpy oracle; GEMMs are checked against a
+torch fp32 reference within a stated tolerance.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import srelu24_np as O
+from paper_2503_16672_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+F32, BF16 = 0, 1
+
+
+def P(t):
+    return None if t is None else t.data_ptr()
+
+
+def S():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def rel_err(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).norm() / max(b.norm(), 1e-30))
+
+
+def meta_hw_to_ref(meta_hw, rows, cols):
+    ref = torch.empty(rows, cols // 4, 2, dtype=torch.uint8, device="cuda")
+    _lib.call("s24_meta_hw_to_ref", P(meta_hw), rows, cols, P(ref), S())
+    return ref
+
+
+def gpu_sparsify_token(a, want_hw=True):
+    rows, cols = a.shape
+    rp = (rows + 127) // 128 * 128
+    vals = torch.zeros(rp, cols // 2, dtype=torch.bfloat16, device="cuda")
+    meta_ref = torch.empty(rows, cols // 4, 2, dtype=torch.uint8, device="cuda")
+    meta_hw = torch.zeros(_lib.meta_hw_bytes(rows, cols), dtype=torch.uint8, device="cuda") if want_hw else None
+    if meta_hw is not None:
+        meta_hw.fill_(0x44)
+    mask = torch.empty(rows, cols, dtype=torch.uint8, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    dt = F32 if a.dtype == torch.float32 else BF16
+    _lib.call("s24_sparsify_token", P(a), dt, rows, cols, a.stride(0), P(vals), P(meta_ref), P(meta_hw), P(mask),
+              P(stats), S())
+    return vals, meta_ref, meta_hw, mask, stats
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (320, 256, 448), (128, 288, 64)])
+def test_dense_gemm_majors(a_mn, b_mn, M, N, K):
+    torch.manual_seed(0)
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    As = A.t().contiguous() if a_mn else A
+    Bs = B if b_mn else B.t().contiguous()
+    D = torch.empty(M, N, device="cuda")
+    _lib.call("s24_gemm", P(As), a_mn, As.stride(0), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1,
+              S())
+    ref = A.float() @ B.float()
+    assert rel_err(D, ref) < 1e-5
+
+
+def test_dense_gemm_bf16_out_rowmap_transposed():
+    torch.manual_seed(1)
+    M, N, K = 200, 256, 192
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    rmap = torch.randperm(M, device="cuda").int()
+    D = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    _lib.call("s24_gemm", P(A), 0, K, P(B), 1, N, M, N, K, P(D), BF16, N, P(rmap), 0, -1, S())
+    ref = torch.empty(M, N, device="cuda")
+    ref[rmap.long()] = A.float() @ B.float()
+    assert rel_err(D.float(), ref) < 4e-3
+    Dt = torch.zeros(N, M, device="cuda")
+    _lib.call("s24_gemm", P(A), 0, K, P(B), 1, N, M, N, K, P(Dt), F32, M, P(rmap), 1, -1, S())
+    assert rel_err(Dt.t(), ref) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_sparsify_token_matches_oracle(dtype):
+    rng = np.random.Generator(np.random.PCG64(3))
+    a = ((rng.random((256, 512)) < 0.3) * rng.standard_normal((256, 512))).astype(np.float32)
+    a[0, :8] = [1, -2, 0, 0.5, 0, 0, 5, 0]  # KATs from ref tests/test_sparse24.py:43-57
+    a[1, :4] = [1, -1, 2, 0]                 # tie KAT :59-61
+    a = O.bf16_round(a)
+    ta = torch.from_numpy(a).cuda().to(dtype)
+    vals, meta_ref, meta_hw, mask, stats = gpu_sparsify_token(ta)
+    ov, om, omask, ost = O.sparsify_token(a)
+    assert np.array_equal(meta_ref.cpu().numpy(), om)
+    assert np.array_equal(mask.cpu().numpy().astype(bool), omask)
+    assert np.array_equal(vals[:256].float().cpu().numpy().reshape(256, 128, 2), ov)
+    assert stats.cpu().tolist() == [ost["nonzeros_before"], ost["nonzeros_after"]]
+    assert np.array_equal(meta_hw_to_ref(meta_hw, 256, 512).cpu().numpy(), om)
+
+
+@pytest.mark.parametrize("b_mn", [1, 0])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 512), (384, 128, 256), (200, 384, 1024)])
+def test_spmm_vs_decompressed(b_mn, M, N, K):
+    torch.manual_seed(2)
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    vals, meta_ref, meta_hw, mask, stats = gpu_sparsify_token(a)
+    dense = a.float() * mask.float()
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    Bs = B if b_mn else B.t().contiguous()
+    D = torch.empty(M, N, device="cuda")
+    _lib.call("s24_spmm", P(vals), P(meta_hw), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, S())
+    ref = dense @ B.float()
+    assert rel_err(D, ref) < 1e-5
+
+
+def test_decompress_roundtrip():
+    torch.manual_seed(4)
+    a = torch.randn(128, 256, device="cuda").bfloat16()
+    vals, meta_ref, meta_hw, mask, _ = gpu_sparsify_token(a)
+    for mr, mh in ((meta_ref, None), (None, meta_hw)):
+        out = torch.empty(128, 256, device="cuda")
+        _lib.call("s24_decompress_token", P(vals), P(mr), P(mh), 128, 256, P(out), F32, 256, S())
+        assert torch.equal(out, a.float() * mask.float())
+    hw2 = torch.zeros_like(meta_hw)
+    _lib.call("s24_meta_ref_to_hw", P(meta_ref), 128, 256, P(hw2), S())
+    assert torch.equal(hw2, meta_hw)
+
+
+def test_sparsify_feature_matches_oracle():
+    rng = np.random.Generator(np.random.PCG64(5))
+    a = O.bf16_round(((rng.random((256, 192)) < 0.3) * rng.standard_normal((256, 192))).astype(np.float32))
+    ta = torch.from_numpy(a).cuda()
+    rows, cols = a.shape
+    vals_t = torch.zeros((cols + 127) // 128 * 128, rows // 2, dtype=torch.bfloat16, device="cuda")
+    meta_ref = torch.empty(rows // 4, cols, 2, dtype=torch.uint8, device="cuda")
+    meta_hw = torch.zeros(_lib.meta_hw_bytes(cols, rows), dtype=torch.uint8, device="cuda")
+    mask = torch.empty(rows, cols, dtype=torch.uint8, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.call("s24_sparsify_feature", P(ta), F32, rows, cols, cols, P(vals_t), P(meta_ref), P(meta_hw), P(mask),
+              P(stats), S())
+    ov, om, omask, ost = O.sparsify_feature(a)
+    assert np.array_equal(meta_ref.cpu().numpy(), om)
+    assert np.array_equal(mask.cpu().numpy().astype(bool), omask)
+    # vals_t[j, 2g + s] == ov[g, j, s]
+    assert np.array_equal(vals_t[:cols].float().cpu().numpy().reshape(cols, rows // 4, 2).transpose(1, 0, 2), ov)
+    assert stats.cpu().tolist() == [ost["nonzeros_before"], ost["nonzeros_after"]]
+    out = torch.empty(rows, cols, device="cuda")
+    _lib.call("s24_decompress_feature", P(vals_t), None, P(meta_hw), rows, cols, P(out), F32, cols, S())
+    assert np.array_equal(out.cpu().numpy(), O.decompress_feature(ov, om, rows, cols))
+
+
+def test_gather_rows():
+    x = torch.randn(300, 64, device="cuda").bfloat16()
+    src = torch.randperm(300, device="cuda").int()
+    out = torch.empty_like(x)
+    _lib.call("s24_gather_rows", P(x), 300, 128, 128, P(src), P(out), 128, S())
+    assert torch.equal(out, x[src.long()])
+
+
+@pytest.mark.parametrize("h,ratio,hi", [(2048, 0.95, 4096), (8192, 0.95, 50), (16384, 0.95, 32768), (100, 0.5, 3),
+                                        (4096, 1.0, 10), (4096, 0.0, 10), (1, 0.95, 5)])
+def test_plan_matches_oracle(h, ratio, hi):
+    rng = np.random.Generator(np.random.PCG64(h))
+    counts = rng.integers(0, hi, h).astype(np.int32)
+    k = O.ceil_fraction(ratio, h)
+    c = torch.from_numpy(counts).cuda()
+    sp = torch.full((max(k, 1),), -7, dtype=torch.int32, device="cuda")
+    de = torch.full((max(h - k, 1),), -7, dtype=torch.int32, device="cuda")
+    pos = torch.empty(h, dtype=torch.int32, device="cuda")
+    _lib.call("s24_plan", P(c), h, k, P(sp), P(de), P(pos), S())
+    osp, ode = O.partition(counts, ratio)
+    assert np.array_equal(sp[:k].cpu().numpy(), osp)
+    assert np.array_equal(de[: h - k].cpu().numpy(), ode)
+    p = pos.cpu().numpy()
+    assert np.array_equal(p[osp], np.arange(k))
+    assert np.array_equal(-p[ode] - 1, np.arange(h - k))
+
+
+def _k1(x, w1, with_counts=True):
+    M, K = x.shape
+    N = w1.shape[1]
+    mp = (M + 127) // 128 * 128
+    vals = torch.zeros(mp, N // 2, dtype=torch.bfloat16, device="cuda")
+    meta = torch.full((_lib.meta_hw_bytes(M, N),), 0x44, dtype=torch.uint8, device="cuda")
+    counts = torch.zeros(N, dtype=torch.int32, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    y = torch.empty(M, N, device="cuda")
+    _lib.call("s24_fwd_gemm1_fused", P(x), K, P(w1), N, M, N, K, P(vals), P(meta), P(counts) if with_counts else None,
+              P(stats), P(y), S())
+    return vals, meta, counts, stats, y
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (4096, 2048, 512), (200, 256, 64)])
+def test_fwd_gemm1_fused_exact_given_y(M, N, K):
+    x, w1, _, _ = O.synthetic_ffn_inputs(M, K, N, sparsity=0.9, seed=M)
+    tx = torch.from_numpy(x).cuda().bfloat16()
+    tw = torch.from_numpy(w1).cuda().bfloat16()
+    vals, meta, counts, stats, y = _k1(tx, tw)
+    assert rel_err(y, tx.float() @ tw.float()) < 1e-5
+    yn = y.cpu().numpy()
+    r = np.maximum(yn, np.float32(0))
+    a = r * r
+    ov, om, omask, ost = O.sparsify_token(a)
+    assert np.array_equal(meta_hw_to_ref(meta, M, N).cpu().numpy(), om)
+    assert np.array_equal(vals[:M].float().cpu().numpy().reshape(M, N // 4, 2), O.bf16_round(ov))
+    assert np.array_equal(counts.cpu().numpy(), O.column_counts(a))
+    assert stats.cpu().tolist() == [ost["nonzeros_before"], ost["nonzeros_after"]]
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (1024, 2048, 512)])
+def test_bwd_dact_fused(M, N, K):
+    x, w1, w2, dy = O.synthetic_ffn_inputs(M, K, N, sparsity=0.8, seed=7)
+    tx, tw1, tw2, tg = (torch.from_numpy(t).cuda().bfloat16() for t in (x, w1, w2, dy))
+    vals, meta, _, _, y = _k1(tx, tw1, with_counts=False)
+    gv = torch.zeros_like(vals)
+    _lib.call("s24_bwd_dact_fused", P(tg), K, P(tw2), K, M, N, K, P(vals), P(meta), P(gv), S())
+    G = tg.float() @ tw2.float().t()  # [M, N]
+    mref = meta_hw_to_ref(meta, M, N).long()  # [M, N/4, 2]
+    Gk = torch.gather(G.view(M, N // 4, 4), 2, mref)  # [M, N/4, 2]
+    av = vals[:M].float().view(M, N // 4, 2)
+    expect = Gk * 2 * av.sqrt()
+    assert rel_err(gv[:M].float().view(M, N // 4, 2), expect) < 5e-3
+
+
+def test_feature_split_matches_oracle():
+    n, h = 512, 384
+    rng = np.random.Generator(np.random.PCG64(9))
+    a = O.bf16_round(((rng.random((n, h)) < 0.25) * rng.standard_normal((n, h))).astype(np.float32))
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    vals, meta_ref, meta_hw, mask, _ = gpu_sparsify_token(ta)
+    am = a * mask.cpu().numpy().astype(np.float32)
+    counts = O.column_counts(am)
+    ks = O.ceil_fraction(0.9, h)
+    osp, ode = O.partition(counts, 0.9)
+    pos = np.empty(h, np.int32)
+    pos[osp] = np.arange(len(osp))
+    pos[ode] = -np.arange(len(ode)) - 1
+    tpos = torch.from_numpy(pos).cuda()
+    sp_pad = (ks + 127) // 128 * 128
+    d_pad = (h - ks + 127) // 128 * 128
+    vs = torch.full((sp_pad, n // 2), 7.0, dtype=torch.bfloat16, device="cuda")
+    es = torch.zeros(_lib.meta_hw_bytes(sp_pad, n), dtype=torch.uint8, device="cuda")
+    vd = torch.full((d_pad, n), 7.0, dtype=torch.bfloat16, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.call("s24_feature_split", P(vals), P(meta_hw), n, h, P(tpos), ks, h - ks, P(vs), P(es), P(vd), P(stats), S())
+    ov, om, _, ost = O.sparsify_feature(np.ascontiguousarray(am[:, osp]))
+    got_meta = meta_hw_to_ref(es, sp_pad, n).cpu().numpy()  # [sp_pad, n/4, 2]
+    assert np.array_equal(got_meta[:ks].transpose(1, 0, 2), om)
+    got_v = vs.float().cpu().numpy().reshape(sp_pad, n // 4, 2)
+    assert np.array_equal(got_v[:ks].transpose(1, 0, 2), ov)
+    assert not got_v[ks:].any()
+    assert np.array_equal(vd[: h - ks].float().cpu().numpy(), am[:, ode].T)
+    assert not vd[h - ks:].float().any()
+    assert stats.cpu().tolist() == [ost["nonzeros_before"], ost["nonzeros_after"]]
