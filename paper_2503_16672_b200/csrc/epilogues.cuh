@@ -31,10 +31,12 @@ struct EpiStore {
     int n_rows_valid;    // rows >= this are padding (skip)
   };
   using State = NoState;
+  static constexpr bool kUnroll = false;
   __device__ static void init(const Params&, State&) {}
+  __device__ static void prefetch(const Params&, State&, int, bool, int) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, const float (&v)[32],
-                               uint32_t) {
+  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, int c,
+                               const float (&v)[32], uint32_t) {
     if (!row_ok || row >= p.n_rows_valid) return;
     const long long r = p.row_map ? p.row_map[row] : row;
     if (p.transposed) {
@@ -81,7 +83,9 @@ struct EpiFwd1 {
   struct State {
     unsigned long long before, after;
   };
+  static constexpr bool kUnroll = false;
   __device__ static void init(const Params&, State& s) { s.before = s.after = 0; }
+  __device__ static void prefetch(const Params&, State&, int, bool, int) {}
   __device__ static void finish(const Params& p, State& s, uint32_t lane) {
     const unsigned long long b = warp_sum_u64(s.before), a = warp_sum_u64(s.after);
     if (lane == 0 && p.stats) {
@@ -89,8 +93,8 @@ struct EpiFwd1 {
       atomicAdd(p.stats + 1, a);
     }
   }
-  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, const float (&v)[32],
-                               uint32_t lane) {
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int c,
+                               const float (&v)[32], uint32_t lane) {
     float a[32];
     uint32_t nz = 0;
 #pragma unroll
@@ -145,6 +149,8 @@ struct EpiFwd1 {
 //   g_pre = G * 2 * relu(y1),  relu(y1) recovered as sqrt(a) from the cached
 // compressed activation a = relu(y1)^2. Output: compressed g_pre [M, N/2] on
 // the forward metadata (which is reused as-is for the dX sparse GEMM).
+// The tile's act values (256 B / row) and metadata rows are prefetched into
+// registers before the accumulator wait, so their latency hides under the MMA.
 struct EpiBwd1 {
   struct Params {
     const __nv_bfloat16* act_vals;  // [Mpad, N/2]
@@ -152,19 +158,43 @@ struct EpiBwd1 {
     __nv_bfloat16* gvals;           // [Mpad, N/2] out
     int N;
   };
-  using State = NoState;
+  static constexpr int TILE_N = 256;
+  static constexpr bool kUnroll = true;
+  struct State {
+    uint4 act[TILE_N / 16];  // 8 bf16 kept values per uint4 = 16 logical columns
+    uint4 meta[TILE_N / 128][2];
+  };
   __device__ static void init(const Params&, State&) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, const float (&v)[32],
-                               uint32_t) {
+  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_base) {
     if (!row_ok) return;
-    const uint16_t* mh = reinterpret_cast<const uint16_t*>(p.meta);
-    const uint32_t m16[2] = {mh[meta_hw_halfword_offset(row, col0 / 16, p.N) / 2],
-                             mh[meta_hw_halfword_offset(row, col0 / 16 + 1, p.N) / 2]};
-    const long long off = static_cast<long long>(row) * (p.N / 2) + col0 / 2;
-    const uint4 av0 = *reinterpret_cast<const uint4*>(p.act_vals + off);
-    const uint4 av1 = *reinterpret_cast<const uint4*>(p.act_vals + off + 8);
-    const uint32_t aw[8] = {av0.x, av0.y, av0.z, av0.w, av1.x, av1.y, av1.z, av1.w};
+    const uint4* a = reinterpret_cast<const uint4*>(p.act_vals + static_cast<long long>(row) * (p.N / 2) + col_base / 2);
+#pragma unroll
+    for (int i = 0; i < TILE_N / 16; ++i)
+      if (col_base + 16 * i < p.N) s.act[i] = a[i];
+    const uint32_t r = static_cast<uint32_t>(row) & 127u;
+#pragma unroll
+    for (int at = 0; at < TILE_N / 128; ++at) {
+      if (col_base + 128 * at >= p.N) break;
+      const uint8_t* base = p.meta + meta_hw_halfword_offset(row, (col_base + 128 * at) / 16, p.N) -
+                            meta_atom_halfword_byte(r, 0);
+      const uint32_t row16 = 16u * (r & 7u) + 256u * (r >> 4);
+      s.meta[at][0] = *reinterpret_cast<const uint4*>(base + row16);
+      s.meta[at][1] = *reinterpret_cast<const uint4*>(base + row16 + 128);
+    }
+  }
+  __device__ static uint32_t word(const uint4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int c,
+                               const float (&v)[32], uint32_t) {
+    if (!row_ok) return;
+    const uint32_t m1 = (static_cast<uint32_t>(row) >> 3) & 1u;
+    // chunk c covers the 16-column quads 2c (k1 = 0) and 2c+1 (k1 = 1) of atom c/4, word k2 = c%4
+    const uint32_t w0 = word(s.meta[c >> 2][0], c & 3), w1 = word(s.meta[c >> 2][1], c & 3);
+    const uint32_t m16[2] = {(w0 >> (16 * m1)) & 0xFFFFu, (w1 >> (16 * m1)) & 0xFFFFu};
+    const uint32_t aw[8] = {s.act[2 * c].x, s.act[2 * c].y, s.act[2 * c].z, s.act[2 * c].w,
+                            s.act[2 * c + 1].x, s.act[2 * c + 1].y, s.act[2 * c + 1].z, s.act[2 * c + 1].w};
     uint32_t packed[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
@@ -175,7 +205,7 @@ struct EpiBwd1 {
       const float a0 = __bfloat162float(a2.x), a1 = __bfloat162float(a2.y);
       packed[g] = pack_bf16x2(g0 * (2.f * sqrtf(a0)), g1 * (2.f * sqrtf(a1)));
     }
-    __nv_bfloat16* dst = p.gvals + off;
+    __nv_bfloat16* dst = p.gvals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
     st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
     st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
   }
@@ -189,10 +219,12 @@ struct EpiRelu2 {
     long long ld;
   };
   using State = NoState;
+  static constexpr bool kUnroll = false;
   __device__ static void init(const Params&, State&) {}
+  __device__ static void prefetch(const Params&, State&, int, bool, int) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, const float (&v)[32],
-                               uint32_t) {
+  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, int c,
+                               const float (&v)[32], uint32_t) {
     if (!row_ok) return;
     float a[32];
 #pragma unroll
@@ -208,30 +240,57 @@ struct EpiRelu2 {
   }
 };
 
-// bwd: g_pre = G * 2 * sqrt(act), dense (ref ffn.py:415 with act_squared_relu_grad :172-173)
+// bwd: g_pre = G * 2 * sqrt(act), dense (ref ffn.py:415 with act_squared_relu_grad :172-173).
+// act chunks are software-pipelined 4 chunks ahead through registers.
 struct EpiDact {
   struct Params {
     const __nv_bfloat16* act;
     long long ld_act;
     __nv_bfloat16* gpre;
     long long ld_g;
+    int N;
   };
-  using State = NoState;
+  static constexpr int AHEAD = 4;
+  static constexpr bool kUnroll = true;
+  struct State {
+    uint4 buf[AHEAD][4];
+    int col_base;
+  };
   __device__ static void init(const Params&, State&) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, const float (&v)[32],
-                               uint32_t) {
+  __device__ static void load(const Params& p, State& s, int row, int c, int slot) {
+    const int col = s.col_base + 32 * c;
+    if (col >= p.N) return;
+    const uint4* src = reinterpret_cast<const uint4*>(p.act + static_cast<long long>(row) * p.ld_act + col);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s.buf[slot][i] = src[i];
+  }
+  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_base) {
+    s.col_base = col_base;
     if (!row_ok) return;
-    const __nv_bfloat16* src = p.act + static_cast<long long>(row) * p.ld_act + col0;
+#pragma unroll
+    for (int c = 0; c < AHEAD; ++c) load(p, s, row, c, c);
+  }
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int c,
+                               const float (&v)[32], uint32_t) {
+    if (!row_ok) return;
+    const int slot = c % AHEAD;
+    uint32_t ww[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ww[4 * i] = s.buf[slot][i].x;
+      ww[4 * i + 1] = s.buf[slot][i].y;
+      ww[4 * i + 2] = s.buf[slot][i].z;
+      ww[4 * i + 3] = s.buf[slot][i].w;
+    }
+    load(p, s, row, c + AHEAD, slot);
     __nv_bfloat16* dst = p.gpre + static_cast<long long>(row) * p.ld_g + col0;
 #pragma unroll
     for (int i = 0; i < 32; i += 8) {
-      const uint4 w = *reinterpret_cast<const uint4*>(src + i);
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
       uint32_t o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&ww[j]);
+        const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&ww[i / 2 + j]);
         o[j] = pack_bf16x2(v[i + 2 * j] * (2.f * sqrtf(__bfloat162float(a2.x))),
                            v[i + 2 * j + 1] * (2.f * sqrtf(__bfloat162float(a2.y))));
       }

@@ -2,22 +2,29 @@
 //
 //   D[M,N] = A[M,K] * B[K,N]      (bf16 operands, fp32 accumulation in TMEM)
 //
-// One CTA per SM (grid = min(#tiles, #SMs)), 256 threads:
-//   warp 0  : TMA producer (A/B tiles via cp.async.bulk.tensor, 2:4 metadata
-//             atoms via cp.async.bulk) into a STAGES-deep smem ring
-//   warp 1  : MMA issuer (single thread): tcgen05.cp metadata smem->TMEM, then
-//             tcgen05.mma(.sp) into one of NUM_ACC TMEM accumulators
-//   warp 2  : TMEM allocator
-//   warps 4-7: epilogue (TMEM -> registers -> fused epilogue functor -> HBM);
-//             warp w owns TMEM lanes 32*(w%4) .. +31, i.e. tile rows.
-// Tile = 128 x BN; K step per stage = 64 (dense) or 128 logical (sparse, i.e.
-// 64 stored values per row + one 2048-byte metadata atom).
+// CG = 1: one CTA per tile of 128 x BN.
+// CG = 2: a CTA pair (cluster of 2 on one TPC) per tile of 256 x BN, issued as
+//         tcgen05.mma.cta_group::2 by the leader CTA: each CTA stages its own
+//         128 rows of A and BN/2 columns of B; the pair's tensor cores read
+//         both halves of B, halving smem operand traffic per SM.
+// 256 threads per CTA:
+//   warp 0   : TMA producer (A/B tiles, 2:4 metadata atoms) into a ring of
+//              STAGES smem slots
+//   warp 1   : MMA issuer (leader CTA, one thread): tcgen05.cp metadata
+//              smem->TMEM, tcgen05.mma(.sp), tcgen05.commit
+//   warp 2   : TMEM allocator
+//   warps 4-7: epilogue; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows)
+//              chunk by chunk (32 fp32 columns) into the fused epilogue functor.
+// Accumulators: two TMEM slots. Disjoint (2*BN columns) when they fit, else
+// overlapping by one 32-column chunk (slot 1 starts at BN-32): the epilogue
+// drains the shared chunk first and releases the slot right away, so the next
+// tile's MMAs overlap the rest of the drain while the 2:4 metadata keeps its
+// own TMEM columns.
 //
-// Operand layouts (smem, SWIZZLE_128B, as TMA writes them):
+// Operand smem layouts (SWIZZLE_128B, exactly as TMA writes them):
 //   K-major  : rows of 128 bytes (64 bf16 along K), 8-row groups 1024 B apart
 //   MN-major : boxes of 64 (M or N) elements x BK rows of K, box stride BK*128 B
-// Descriptors follow the canonical tcgen05 forms: K-major SBO = 1024;
-// MN-major LBO = box stride, SBO = 1024 (8 K rows).
+// Descriptors: K-major SBO = 1024; MN-major LBO = box stride, SBO = 1024.
 #pragma once
 #include "meta.cuh"
 #include "ptx.cuh"
@@ -25,38 +32,44 @@
 namespace s24 {
 
 struct GemmShape {
-  int M, N, K;         // logical sizes (K = logical K for sparse A)
-  int tiles_m, tiles_n;
-  int group_m;         // tile rasterisation: group_m M-blocks share a B sweep
-  const uint8_t* meta; // sparse only: hw-layout metadata, rows padded to 128
+  int M, N, K;          // logical sizes (K = logical K for sparse A)
+  int tiles_m, tiles_n; // in units of (128*CG) x BN
+  int group_m;          // raster: group_m M-tiles share one sweep over N
 };
 
-template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int NUM_ACC_>
+template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_>
 struct GemmCfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr bool A_MN = A_MN_;
   static constexpr bool B_MN = B_MN_;
-  static constexpr int BM = 128;
-  static constexpr int BN = BN_;
+  static constexpr int CG = CG_;
+  static constexpr int BM = 128;                 // rows per CTA
+  static constexpr int TILE_M = BM * CG;         // rows per tile
+  static constexpr int BN = BN_;                 // columns per tile (MMA N)
+  static constexpr int BN_CTA = BN / CG;         // B columns staged per CTA
   static constexpr int STAGES = STAGES_;
-  static constexpr int NUM_ACC = NUM_ACC_;
-  static constexpr int BK = SPARSE ? 128 : 64;       // logical K per stage
-  static constexpr int A_COLS = SPARSE ? 64 : 64;    // stored A elements per row per stage
-  static constexpr int KSTEPS = 4;                   // MMAs per stage (K16 dense / K32 sparse)
+  static constexpr int BK = SPARSE ? 128 : 64;   // logical K per stage
+  static constexpr int A_COLS = 64;              // stored A elements per row per stage
+  static constexpr int KSTEPS = 4;               // MMAs per stage (K16 dense / K32 sparse)
   static constexpr uint32_t A_BYTES = BM * A_COLS * 2;
-  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t B_BYTES = BN_CTA * BK * 2;
   static constexpr uint32_t E_BYTES = SPARSE ? 2048 : 0;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
-  static constexpr uint32_t TMEM_E_COL = NUM_ACC * BN;
-  static constexpr uint32_t TMEM_NEED = NUM_ACC * BN + (SPARSE ? STAGES * 4 : 0);
+  static constexpr uint32_t E_COLS = SPARSE ? STAGES * 4 : 0;
+  static constexpr bool OVERLAP = 2 * BN + E_COLS > 512;
+  static constexpr uint32_t SLOT1_COL = OVERLAP ? BN - 32 : BN;
+  static constexpr uint32_t E_COL = SLOT1_COL + BN;
+  static constexpr uint32_t TMEM_NEED = E_COL + E_COLS;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128
                                        : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static_assert(!(SPARSE && A_MN), "sparse A must be K-major");
-  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  static_assert(BN_CTA % 64 == 0 && BN <= 256, "BN");
+  static_assert(CG == 1 || CG == 2, "CG");
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 2 * NUM_ACC) * 8 + 16 + 1024;
-  static constexpr uint32_t IDESC = make_idesc_bf16(BM, BN, A_MN, B_MN, SPARSE);
+  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr uint32_t IDESC = make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
+  static constexpr int NCHUNK = BN / 32;
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, int& nb) {
@@ -69,46 +82,69 @@ __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, 
   nb = local / gm;
 }
 
-// Epilogue contract: Epi::Params ep; per 32-column chunk of one row
-//   Epi::chunk(ep, st, row, row_ok, col0, v[32], lane)   (all 32 lanes call it)
-// and Epi::finish(ep, st, lane) once at the end (per-thread state reductions).
+template <int CG>
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  if constexpr (CG == 2)
+    tma_load_2d_cg2(dst, map, bar, c0, c1);
+  else
+    tma_load_2d(dst, map, bar, c0, c1);
+}
+
+// Epilogue contract: Epi::Params ep; per 32-column chunk c of one row
+//   Epi::chunk(ep, st, row, row_ok, col0, c, v[32], lane)  (all 32 lanes call it)
+// Epi::prefetch(ep, st, row, row_ok, col_base) once per tile before waiting
+// for the accumulator, and Epi::finish(ep, st, lane) once at the end.
 template <class Cfg, class Epi>
 __global__ void __launch_bounds__(256, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmShape shape, const typename Epi::Params ep) {
+                const __grid_constant__ CUtensorMap tmE, const GemmShape shape, const typename Epi::Params ep) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  constexpr int CG = Cfg::CG;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
-  uint64_t* tempty_bar = tfull_bar + Cfg::NUM_ACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + Cfg::NUM_ACC);
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
   const int total_tiles = shape.tiles_m * shape.tiles_n;
   const int num_kb = (shape.K + Cfg::BK - 1) / Cfg::BK;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if constexpr (Cfg::SPARSE) tma_prefetch(&tmE);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], CG);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int a = 0; a < Cfg::NUM_ACC; ++a) {
+    for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], CG * 128);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_alloc_cg2<Cfg::TMEM_COLS>(tmem_slot);
+    else
+      tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -117,38 +153,37 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         int mb, nb;
         tile_coords(shape, t, mb, nb);
-        const int m0 = mb * Cfg::BM, n0 = nb * Cfg::BN;
+        const int m0 = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
+        const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::BN_CTA;
+        const int atom_row = mb * CG + static_cast<int>(rank);  // 128-row metadata block
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          if (leader)
+            mbar_arrive_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
+          else
+            mbar_arrive_remote(&full_bar[stage], 0);
           if constexpr (Cfg::A_MN) {
-            // A stored [K][M]: two boxes of {64 M, 64 K}
-            tma_load_2d(sa, &tmA, &full_bar[stage], m0, kb * Cfg::BK);
-            tma_load_2d(sa + Cfg::A_BYTES / 2, &tmA, &full_bar[stage], m0 + 64, kb * Cfg::BK);
+            tma_load<CG>(sa, &tmA, &full_bar[stage], m0, kb * Cfg::BK);
+            tma_load<CG>(sa + Cfg::A_BYTES / 2, &tmA, &full_bar[stage], m0 + 64, kb * Cfg::BK);
           } else {
-            // A stored [M][Kstored]: one box {64, 128}
-            tma_load_2d(sa, &tmA, &full_bar[stage], kb * Cfg::A_COLS, m0);
+            tma_load<CG>(sa, &tmA, &full_bar[stage], kb * Cfg::A_COLS, m0);
           }
           if constexpr (Cfg::B_MN) {
-            // B stored [K][N]: BN/64 boxes of {64 N, BK K}
 #pragma unroll
-            for (int j = 0; j < Cfg::BN / 64; ++j)
-              tma_load_2d(sb + j * (Cfg::BK * 128), &tmB, &full_bar[stage], n0 + 64 * j, kb * Cfg::BK);
+            for (int j = 0; j < Cfg::BN_CTA / 64; ++j)
+              tma_load<CG>(sb + j * (Cfg::BK * 128), &tmB, &full_bar[stage], n0 + 64 * j, kb * Cfg::BK);
           } else {
-            // B stored [N][K]: BK/64 boxes of {64 K, BN rows}
 #pragma unroll
             for (int j = 0; j < Cfg::BK / 64; ++j)
-              tma_load_2d(sb + j * (Cfg::BN * 128), &tmB, &full_bar[stage], kb * Cfg::BK + 64 * j, n0);
+              tma_load<CG>(sb + j * (Cfg::BN_CTA * 128), &tmB, &full_bar[stage], kb * Cfg::BK + 64 * j, n0);
           }
-          if constexpr (Cfg::SPARSE) {
-            const uint8_t* src = shape.meta + (static_cast<size_t>(mb) * num_kb + kb) * 2048u;
-            bulk_load(sb + Cfg::B_BYTES, src, 2048u, &full_bar[stage]);
-          }
+          if constexpr (Cfg::SPARSE)
+            tma_load<CG>(sb + Cfg::B_BYTES, &tmE, &full_bar[stage], 0, (atom_row * num_kb + kb) * 16);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -159,16 +194,19 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (leader && lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++iter) {
-        const int acc = iter % Cfg::NUM_ACC;
-        const uint32_t acc_phase = (iter / Cfg::NUM_ACC) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++iter) {
+        const int slot = iter & 1;
+        if constexpr (Cfg::OVERLAP) {
+          if (iter > 0) mbar_wait(&tempty_bar[0], (iter - 1) & 1);
+        } else {
+          mbar_wait(&tempty_bar[slot], ((iter >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * Cfg::BN;
+        const uint32_t d_tmem = tmem_base + slot * Cfg::SLOT1_COL;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -176,8 +214,12 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t sb = sa + Cfg::A_BYTES;
           uint32_t e_tmem = 0;
           if constexpr (Cfg::SPARSE) {
-            e_tmem = tmem_base + Cfg::TMEM_E_COL + stage * 4;
-            tmem_cp_128x128b(e_tmem, make_sdesc(sb + Cfg::B_BYTES, 0, 128, kLayoutNone));
+            e_tmem = tmem_base + Cfg::E_COL + stage * 4;
+            const uint64_t edesc = make_sdesc(sb + Cfg::B_BYTES, 0, 128, kLayoutNone);
+            if constexpr (CG == 2)
+              tmem_cp_128x128b_cg2(e_tmem, edesc);
+            else
+              tmem_cp_128x128b(e_tmem, edesc);
           }
 #pragma unroll
           for (int j = 0; j < Cfg::KSTEPS; ++j) {
@@ -191,7 +233,7 @@ __global__ void __launch_bounds__(256, 1)
               // dense: 16 K rows per step; sparse: 32 K rows per step
               bdesc = make_sdesc(sb + j * (Cfg::SPARSE ? 4096 : 2048), Cfg::BK * 128, 1024, kLayoutSw128);
             } else if constexpr (Cfg::SPARSE) {
-              bdesc = make_sdesc(sb + (j >> 1) * (Cfg::BN * 128) + (j & 1) * 64, 16, 1024, kLayoutSw128);
+              bdesc = make_sdesc(sb + (j >> 1) * (Cfg::BN_CTA * 128) + (j & 1) * 64, 16, 1024, kLayoutSw128);
             } else {
               bdesc = make_sdesc(sb + j * 32, 16, 1024, kLayoutSw128);
             }
@@ -199,14 +241,26 @@ __global__ void __launch_bounds__(256, 1)
             if constexpr (Cfg::SPARSE) {
               // metadata address must be 2-column aligned; the odd column is
               // selected by the descriptor's sparse-id2 field (bits 0-1)
-              mma_sp_bf16(d_tmem, adesc, bdesc, e_tmem + (j & ~1), Cfg::IDESC | static_cast<uint32_t>(j & 1),
-                          accum);
+              const uint32_t id = Cfg::IDESC | static_cast<uint32_t>(j & 1);
+              if constexpr (CG == 2)
+                mma_sp_bf16_cg2(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
+              else
+                mma_sp_bf16(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
             } else {
-              mma_bf16(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+              if constexpr (CG == 2)
+                mma_bf16_cg2(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+              else
+                mma_bf16(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
             }
           }
-          mma_commit(&empty_bar[stage]);
-          if (kb == num_kb - 1) mma_commit(&tfull_bar[acc]);
+          uint64_t* tf = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
+          if constexpr (CG == 2) {
+            mma_commit_cg2(&empty_bar[stage], 0x3);
+            if (kb == num_kb - 1) mma_commit_cg2(tf, 0x3);
+          } else {
+            mma_commit(&empty_bar[stage]);
+            if (kb == num_kb - 1) mma_commit(tf);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -221,39 +275,68 @@ __global__ void __launch_bounds__(256, 1)
     typename Epi::State st;
     Epi::init(ep, st);
     int iter = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++iter) {
+    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++iter) {
       int mb, nb;
       tile_coords(shape, t, mb, nb);
-      const int acc = iter % Cfg::NUM_ACC;
-      const uint32_t acc_phase = (iter / Cfg::NUM_ACC) & 1;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const int row = mb * Cfg::BM + q * 32 + static_cast<int>(lane);
+      const int slot = iter & 1;
+      const int row = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 + static_cast<int>(lane);
       const bool row_ok = row < shape.M;
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * Cfg::BN;
-#pragma unroll 1
-      for (int c = 0; c < Cfg::BN / 32; ++c) {
+      Epi::prefetch(ep, st, row, row_ok, nb * Cfg::BN);
+      uint64_t* tempty = &tempty_bar[Cfg::OVERLAP ? 0 : slot];
+      if constexpr (Cfg::OVERLAP)
+        mbar_wait(&tfull_bar[0], iter & 1);
+      else
+        mbar_wait(&tfull_bar[slot], (iter >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * Cfg::SLOT1_COL;
+      // epilogues that keep per-chunk state (Epi::kUnroll) get a fully unrolled
+      // loop so that state stays in registers
+#pragma unroll(Epi::kUnroll ? Cfg::NCHUNK : 1)
+      for (int ci = 0; ci < Cfg::NCHUNK; ++ci) {
+        // overlapping slots: drain the shared chunk first
+        const int c = (Cfg::OVERLAP && slot == 0) ? (ci == 0 ? Cfg::NCHUNK - 1 : ci - 1) : ci;
         const int col0 = nb * Cfg::BN + c * 32;
-        if (col0 >= shape.N) break;  // uniform across the warp
         uint32_t r[32];
-        tmem_ld32(t_row + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
+        if (col0 < shape.N) {  // uniform across the warp
+          tmem_ld32(t_row + c * 32, r);
+          tmem_ld_wait();
+        }
+        if (Cfg::OVERLAP && ci == 0) {
+          tc_fence_before();
+          if (leader)
+            mbar_arrive(tempty);
+          else
+            mbar_arrive_remote(tempty, 0);
+        }
+        if (col0 < shape.N) {
+          float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        Epi::chunk(ep, st, row, row_ok, col0, v, lane);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          Epi::chunk(ep, st, row, row_ok, col0, c, v, lane);
+        }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if constexpr (!Cfg::OVERLAP) {
+        tc_fence_before();
+        if (leader)
+          mbar_arrive(tempty);
+        else
+          mbar_arrive_remote(tempty, 0);
+      }
     }
     Epi::finish(ep, st, lane);
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    if constexpr (CG == 2)
+      tmem_dealloc_cg2<Cfg::TMEM_COLS>(tmem_base);
+    else
+      tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
 #endif
 }

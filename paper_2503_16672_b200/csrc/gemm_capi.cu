@@ -44,21 +44,27 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                  uint32_t box_inner, uint32_t box_outer) {
+int make_map_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
   auto fn = encode_fn();
   if (!fn) return fail(S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  if (!aligned16(base) || (ld * 2) % 16 != 0)
+  if (!aligned16(base) || ld_bytes % 16 != 0)
     return fail(S24_ERR_DIMENSION, "operand base/leading dimension must be 16-byte aligned");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(S24_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return S24_OK;
+}
+
+int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_inner, uint32_t box_outer) {
+  return make_map_2d(map, base, true, inner, outer, ld * 2, box_inner, box_outer, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -83,20 +89,29 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   if constexpr (Cfg::B_MN) {
     rc = make_map_bf16(&mb, B, N, K, ldb, 64, Cfg::BK);
   } else {
-    rc = make_map_bf16(&mb, B, K, N, ldb, 64, Cfg::BN);
+    rc = make_map_bf16(&mb, B, K, N, ldb, 64, Cfg::BN_CTA);
   }
   if (rc) return rc;
+
+  CUtensorMap me;
+  std::memset(&me, 0, sizeof(me));
+  if constexpr (Cfg::SPARSE) {
+    // metadata atoms viewed as [atoms * 16 rows, 128 bytes]; one box = one atom
+    const int64_t atoms = (M + 127) / 128 * (K / 128);
+    rc = make_map_2d(&me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16, false);
+    if (rc) return rc;
+  }
 
   GemmShape sh;
   sh.M = static_cast<int>(M);
   sh.N = static_cast<int>(N);
   sh.K = static_cast<int>(K);
-  sh.tiles_m = static_cast<int>((M + Cfg::BM - 1) / Cfg::BM);
+  sh.tiles_m = static_cast<int>((M + Cfg::TILE_M - 1) / Cfg::TILE_M);
   sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
-  sh.group_m = 16;
-  sh.meta = meta;
+  sh.group_m = 16 / Cfg::CG;
   const int tiles = sh.tiles_m * sh.tiles_n;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int max_clusters = num_sms() / Cfg::CG;
+  const int clusters = tiles < max_clusters ? tiles : max_clusters;
 
   auto kern = gemm_kernel<Cfg, Epi>;
   static std::once_flag once;
@@ -105,17 +120,31 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  kern<<<grid, 256, Cfg::SMEM_BYTES, stream>>>(ma, mb, sh, ep);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CG));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = Cfg::CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, sh, ep);
+  if (e != cudaSuccess) return fail(S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return check_launch("gemm_kernel");
 }
 
 // tile configurations
-using DenseKN = GemmCfg<false, false, true, 256, 4, 2>;   // A K-major, B MN-major
-using DenseKK = GemmCfg<false, false, false, 256, 4, 2>;  // A K-major, B K-major
-using DenseMM = GemmCfg<false, true, true, 256, 4, 2>;    // A MN-major, B MN-major
-using DenseMK = GemmCfg<false, true, false, 256, 4, 2>;   // A MN-major, B K-major
-using SparseN = GemmCfg<true, false, true, 128, 4, 2>;    // sparse A, B MN-major
-using SparseK = GemmCfg<true, false, false, 128, 4, 2>;   // sparse A, B K-major
+// <sparse, A MN-major, B MN-major, BN, stages, CTA-group>
+using DenseKN = GemmCfg<false, false, true, 256, 6, 2>;   // A K-major, B MN-major
+using DenseKK = GemmCfg<false, false, false, 256, 6, 2>;  // A K-major, B K-major
+using DenseMM = GemmCfg<false, true, true, 256, 6, 2>;    // A MN-major, B MN-major
+using DenseMK = GemmCfg<false, true, false, 256, 6, 2>;   // A MN-major, B K-major
+using SparseN = GemmCfg<true, false, true, 256, 4, 2>;    // sparse A, B MN-major
+using SparseK = GemmCfg<true, false, false, 256, 4, 2>;   // sparse A, B K-major
 
 template <class Epi>
 static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
@@ -226,7 +255,8 @@ int s24_gemm_dact(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int6
                   const void* act, int64_t ld_act, void* gpre, int64_t ld_g, void* stream) {
   int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
   if (rc) return rc;
-  EpiDact::Params ep{static_cast<const __nv_bfloat16*>(act), ld_act, static_cast<__nv_bfloat16*>(gpre), ld_g};
+  EpiDact::Params ep{static_cast<const __nv_bfloat16*>(act), ld_act, static_cast<__nv_bfloat16*>(gpre), ld_g,
+                     static_cast<int>(N)};
   return launch_gemm<DenseKK, EpiDact>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 

@@ -36,6 +36,8 @@ int num_sms();
 
 // 2-D bf16 tensor map: inner dim (contiguous) `inner` elements, `outer` rows,
 // row pitch `ld` elements; box {box_inner, box_outer}; 128B swizzle.
+int make_map_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                   uint32_t box_inner, uint32_t box_outer);
 
