@@ -1,0 +1,419 @@
+"""Squared-ReLU FFN with the 2:4 activation-sparsity recipe on B200 -- drop-in
+for the reference's pkg/src/srelu24/ffn.py (ffn_forward / ffn_backward and
+their dataclasses; activation = squared_relu).
+
+Recipe forward (ref ffn.py:276-363), one device pass each:
+  K6  x_in = permute_rows(x, perm)                    (row gather)
+  K1  Y1 = x_in . W1 -> relu^2 -> token-wise 2:4       (tcgen05 GEMM, fused epilogue:
+      compressed act + hw metadata + per-feature counts + drop stats)
+  K7  plan = partition_features(counts, ratio)        (device radix select)
+  K2  out = inverse_permute_rows(act_sp . W2)          (tcgen05.mma.sp, row map epilogue)
+Recipe backward (ref ffn.py:366-451):
+  K6  g_c = permute_rows(g_out, perm)
+  K3  g_pre = (g_c . W2^T) * 2 relu(y1) on the forward keep pattern (fused, compressed)
+  K4  feature-wise 2:4 split of act and of g_pre (sparse features) + dense columns
+  K5  dW2 = split(act)^T g_c ; dW1 = (split(g_pre)^T x_in)^T  (sparse + dense GEMMs,
+      feature-index scatter / transpose in the epilogue)
+  K2  dX = inverse_permute_rows(g_pre_sp . W1^T)       (exact: forward metadata)
+Dense mode runs the same GEMM kernels with dense operands (the "dense twin").
+
+Tensors are bf16 on the device (numpy float32 inputs are uploaded and rounded
+to bf16). Weight gradients are fp32, activations/outputs bf16.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import torch
+
+from . import _lib
+from ._tensors import BF16, F32, as_matrix, pad128, ptr, require_cuda, stream
+from .errors import ConfigError, DimensionError, StateError
+from .matcore import device_permutation, gather_rows, gemm_macs
+from .sparse24 import (
+    TOKEN_WISE,
+    Sparse24Matrix,
+    SparsifyStats,
+    sp_gemm_macs,
+)
+from .splitgemm import SplitPlan, ceil_fraction, feature_split, partition_features, split_gemm_macs, split_weight_grad
+
+ACTIVATIONS = ("squared_relu", "swiglu")
+FORWARD_MODES = ("dense", "sparse24")
+BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
+
+
+@dataclass(frozen=True)
+class FfnConfig:
+    """Same fields, defaults and cross-field validation as ref ffn.py:58-101."""
+
+    activation: str = "squared_relu"
+    forward_mode: str = "dense"
+    backward_mode: str = "dense"
+    mask_grad_with_fwd: bool = False
+    permute_tokens: bool = False
+    permute_seed: int = 0
+    split_ratio: float = 0.95
+    fp8_emulation: bool = False
+    fp8_backward: bool = False
+
+    def __post_init__(self):
+        if self.activation not in ACTIVATIONS:
+            raise ConfigError(f"unknown activation {self.activation!r}")
+        if self.forward_mode not in FORWARD_MODES:
+            raise ConfigError(f"unknown forward_mode {self.forward_mode!r}")
+        if self.backward_mode not in BACKWARD_MODES:
+            raise ConfigError(f"unknown backward_mode {self.backward_mode!r}")
+        sparse_any = self.forward_mode != "dense" or self.backward_mode != "dense" or self.mask_grad_with_fwd
+        if sparse_any and self.activation != "squared_relu":
+            raise ConfigError("sparse modes are defined only for squared_relu")
+        if self.backward_mode != "dense" and self.forward_mode != "sparse24":
+            raise ConfigError("sparse backward modes need the sparse forward")
+        if self.mask_grad_with_fwd and self.forward_mode != "sparse24":
+            raise ConfigError("mask_grad_with_fwd needs the sparse forward")
+        if not 0.0 <= self.split_ratio <= 1.0:
+            raise ConfigError(f"split_ratio must be in [0, 1], got {self.split_ratio}")
+        if self.fp8_backward and not self.fp8_emulation:
+            raise ConfigError("fp8_backward requires fp8_emulation")
+
+    def densified(self) -> "FfnConfig":
+        """Same config with every sparsity feature off (ref ffn.py:93-101)."""
+        return replace(self, forward_mode="dense", backward_mode="dense", mask_grad_with_fwd=False,
+                       permute_tokens=False)
+
+
+RECIPE = FfnConfig(forward_mode="sparse24", backward_mode="split_masked", mask_grad_with_fwd=True,
+                   permute_tokens=True)
+
+
+@dataclass(frozen=True)
+class FfnParams:
+    """w1 [d, h], w2 [h, d] (ref ffn.py:104-126), held as bf16 device tensors.
+    Both GEMM orientations read the weights in place (no transposed copies)."""
+
+    w1: torch.Tensor
+    w2: torch.Tensor
+    w3: torch.Tensor | None = None
+    beta: float = 1.0
+
+    def __post_init__(self):
+        w1 = as_matrix(self.w1, "w1", BF16)
+        w2 = as_matrix(self.w2, "w2", BF16)
+        object.__setattr__(self, "w1", w1)
+        object.__setattr__(self, "w2", w2)
+        d, h = w1.shape
+        if tuple(w2.shape) != (h, d):
+            raise DimensionError(f"w2 shape {tuple(w2.shape)} does not match w1 {tuple(w1.shape)}")
+        if h % 4 != 0:
+            raise DimensionError(f"hidden width must be a multiple of 4, got {h}")
+        if self.w3 is not None:
+            w3 = as_matrix(self.w3, "w3", BF16)
+            if tuple(w3.shape) != (d, h):
+                raise DimensionError(f"w3 shape {tuple(w3.shape)} does not match w1 {tuple(w1.shape)}")
+            object.__setattr__(self, "w3", w3)
+
+    @property
+    def model_dim(self) -> int:
+        return self.w1.shape[0]
+
+    @property
+    def hidden_dim(self) -> int:
+        return self.w1.shape[1]
+
+
+@dataclass(frozen=True)
+class GemmEvent:
+    name: str
+    sparse: bool
+    macs: int
+
+
+@dataclass
+class FfnCache:
+    """What the backward reads (ref ffn.py:136-150), kept compressed.
+
+    x_in      bf16 [pad128(n), d] compute-frame input (zero padding rows)
+    act_vals  bf16 [pad128(n), h/2] kept relu^2 values (sparse forward)
+    act_meta  uint8 hw metadata of the forward keep pattern
+    act_dense bf16 [n, h] activation (dense forward only)
+    pre_act   fp32 [n, h] pre-activation, kept only when the backward needs
+              relu(y1) outside the keep mask (mask_grad_with_fwd=False)
+    perm / perm_dev / inv_dev : host permutation and its device copies
+    """
+
+    x_in: torch.Tensor
+    n: int
+    act_vals: torch.Tensor | None
+    act_meta: torch.Tensor | None
+    act_dense: torch.Tensor | None
+    pre_act: torch.Tensor | None
+    perm: object
+    perm_dev: torch.Tensor | None
+    inv_dev: torch.Tensor | None
+    plan: SplitPlan | None
+    stats: SparsifyStats | None
+    counts: torch.Tensor | None
+    census: list[GemmEvent]
+    config: FfnConfig
+    gate: torch.Tensor | None = None
+
+    @property
+    def act_sparse(self) -> Sparse24Matrix | None:
+        if self.act_vals is None:
+            return None
+        h = self.act_vals.shape[1] * 2
+        return Sparse24Matrix(self.n, h, TOKEN_WISE, self.act_vals, self.act_meta)
+
+    @property
+    def fwd_mask(self) -> torch.Tensor | None:
+        s = self.act_sparse
+        if s is None:
+            return None
+        m = torch.zeros(self.n, s.cols // 4, 4, dtype=torch.bool, device=self.act_vals.device)
+        m.scatter_(2, s.meta.long(), True)
+        return m.view(self.n, s.cols)
+
+
+@dataclass
+class FfnGrads:
+    d_w1: torch.Tensor
+    d_w2: torch.Tensor
+    d_x: torch.Tensor
+    d_w3: torch.Tensor | None = None
+    census: list[GemmEvent] = field(default_factory=list)
+    stats_act: SparsifyStats | None = None  # feature-wise drops of the act split (dW2)
+    stats_grad: SparsifyStats | None = None  # feature-wise drops of the g_pre split (dW1)
+
+
+def act_squared_relu(pre):
+    """relu(pre)^2 (ref ffn.py:167-169)."""
+    r = torch.clamp_min(pre, 0)
+    return r * r
+
+
+def act_squared_relu_grad(pre):
+    """2 relu(pre) (ref ffn.py:172-173)."""
+    return 2 * torch.clamp_min(pre, 0)
+
+
+def _unsupported(cfg: FfnConfig) -> None:
+    if cfg.activation != "squared_relu":
+        raise ConfigError("the B200 backend implements the squared_relu FFN only (SwiGLU is the "
+                          "reference's dense Table-1 baseline, out of scope)")
+    if cfg.fp8_emulation:
+        raise ConfigError("the fp8 (e4m3) path is not part of this build")
+
+
+def _check_dims(n: int, d: int, h: int) -> None:
+    if d % 8 != 0:
+        raise DimensionError(f"model dim {d} must be a multiple of 8 on the device path")
+    if h % 128 != 0:
+        raise DimensionError(f"hidden width {h} must be a multiple of 128 on the device path")
+
+
+def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, keep_pre_act: bool = False):
+    """Run the forward pass; returns (out [n, d] bf16, FfnCache) (ref ffn.py:276-363).
+    keep_pre_act=True also stores the fp32 pre-activation in the cache (parity
+    tests use it to replay the selection on identical inputs)."""
+    require_cuda()
+    _unsupported(cfg)
+    x = as_matrix(x, "x", BF16)
+    n, d = x.shape
+    if d != p.model_dim:
+        raise DimensionError(f"input width {d} does not match w1 {tuple(p.w1.shape)}")
+    if (p.w3 is not None) != (cfg.activation == "swiglu"):
+        raise ConfigError("gate weight w3 must be present exactly for swiglu")
+    sparse_fwd = cfg.forward_mode == "sparse24"
+    if sparse_fwd and n % 4 != 0:
+        raise DimensionError(f"sparse modes need token count % 4 == 0, got {n}")
+    h = p.hidden_dim
+    _check_dims(n, d, h)
+    dev = x.device
+    s = stream()
+    npad = pad128(n)
+    census: list[GemmEvent] = []
+
+    # compute-frame input, padded to a multiple of 128 rows (zero rows are
+    # transparent to every stage: they produce zero activations and gradients)
+    x_in = torch.empty(npad, d, dtype=BF16, device=dev)
+    if npad > n:
+        x_in[n:].zero_()
+    perm = perm_dev = inv_dev = None
+    if cfg.permute_tokens and sparse_fwd:
+        perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
+        perm = perm_dev
+        gather_rows(x, inv_dev, x_in)  # x_in[p[i]] = x[i]
+    else:
+        x_in[:n].copy_(x)
+
+    out = torch.empty(n, d, dtype=BF16, device=dev)
+    if not sparse_fwd:
+        act = torch.empty(n, h, dtype=BF16, device=dev)
+        _lib.call("s24_gemm_relu2", ptr(x_in), d, ptr(p.w1), h, n, h, d, ptr(act), h, s)
+        census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
+        _lib.call("s24_gemm", ptr(act), 0, h, ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d, None, 0, -1, s)
+        census.append(GemmEvent("fwd.out", False, gemm_macs(n, h, d)))
+        cache = FfnCache(x_in, n, None, None, act, None, None, None, None, None, None, None, census, cfg)
+        return out, cache
+
+    act_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
+    act_meta = torch.empty(_lib.meta_hw_bytes(n, h), dtype=torch.uint8, device=dev)
+    if npad > n:
+        act_vals[n:].zero_()
+        act_meta[(n // 128) * (h // 128) * 2048:].fill_(0x44)
+    counts = torch.zeros(h, dtype=torch.int32, device=dev)
+    stats_dev = torch.zeros(2, dtype=torch.int64, device=dev)
+    need_pre = keep_pre_act or not cfg.mask_grad_with_fwd
+    pre = torch.empty(n, h, dtype=F32, device=dev) if need_pre else None
+    _lib.call("s24_fwd_gemm1_fused", ptr(x_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta), ptr(counts),
+              ptr(stats_dev), ptr(pre), s)
+    census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
+
+    plan_out = None
+    if cfg.backward_mode == "split_masked":
+        if plan is not None and plan.hidden_dim != h:
+            raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+        plan_out = plan if plan is not None else partition_features(counts, cfg.split_ratio)
+
+    _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
+              ptr(inv_dev), 0, -1, s)
+    census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
+    cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
+                     SparsifyStats(n * h, stats_dev), counts, census, cfg)
+    return out, cache
+
+
+def _all_sparse_plan(h: int, dev) -> SplitPlan:
+    pos = torch.arange(h, dtype=torch.int32, device=dev)
+    return SplitPlan(h, 1.0, torch.zeros(h, dtype=torch.int64, device=dev), pos,
+                     torch.empty(0, dtype=torch.int32, device=dev), pos)
+
+
+def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_ready=None) -> FfnGrads:
+    """Backward matching the cached forward (ref ffn.py:366-451).
+
+    grad_ready(name, tensor), if given, is called as soon as d_w2 and then
+    d_w1 are final on the current stream (used by the data-parallel step to
+    launch their all-reduce while the rest of the backward runs)."""
+    if cache.config != cfg:
+        raise StateError("cache was produced under a different configuration")
+    _unsupported(cfg)
+    n = cache.n
+    d = cache.x_in.shape[1]
+    g_out = as_matrix(g_out, "g_out", BF16)
+    if tuple(g_out.shape) != (n, d):
+        raise StateError(f"gradient shape {tuple(g_out.shape)} does not match cached input {(n, d)}")
+    sparse_fwd = cfg.forward_mode == "sparse24"
+    if sparse_fwd and cache.act_vals is None:
+        raise StateError("sparse forward cache is missing the compressed activation")
+    if not sparse_fwd and cache.act_dense is None:
+        raise StateError("dense forward cache is missing the activation")
+    if cfg.backward_mode == "split_masked" and cache.plan is None:
+        raise StateError("split backward needs the plan computed in forward")
+    h = p.hidden_dim
+    dev = g_out.device
+    s = stream()
+    npad = pad128(n)
+    census: list[GemmEvent] = []
+    notify = grad_ready or (lambda name, t: None)
+
+    g_c = torch.empty(npad, d, dtype=BF16, device=dev)
+    if npad > n:
+        g_c[n:].zero_()
+    if cache.inv_dev is not None:
+        gather_rows(g_out, cache.inv_dev, g_c)
+    else:
+        g_c[:n].copy_(g_out)
+
+    d_w1 = torch.empty(d, h, dtype=F32, device=dev)
+    d_w2 = torch.empty(h, d, dtype=F32, device=dev)
+    d_x = torch.empty(n, d, dtype=BF16, device=dev)
+    stats_a = stats_g = None
+
+    if not sparse_fwd:
+        # ---------------------------------------------------------- dense twin
+        act = cache.act_dense
+        g_pre = torch.empty(n, h, dtype=BF16, device=dev)
+        _lib.call("s24_gemm_dact", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(act), h, ptr(g_pre), h, s)
+        census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
+        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, s)
+        census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
+        notify("d_w2", d_w2)
+        _lib.call("s24_gemm", ptr(g_pre), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, s)
+        census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
+        notify("d_w1", d_w1)
+        _lib.call("s24_gemm", ptr(g_pre), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d, None, 0, -1, s)
+        census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
+        return FfnGrads(d_w1, d_w2, d_x, None, census)
+
+    # -------------------------------------------------------------- sparse forward
+    # g_pre on the forward keep pattern, compressed (exact; ref ffn.py:415-417, 443)
+    g_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
+    if npad > n:
+        g_vals[n:].zero_()
+    _lib.call("s24_bwd_dact_fused", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(cache.act_vals), ptr(cache.act_meta),
+              ptr(g_vals), s)
+    census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
+    g_pre_dense = None
+    if not cfg.mask_grad_with_fwd:
+        # unmasked derivative: needs relu(y1) everywhere (fp32 pre-activation kept by the forward)
+        G = torch.empty(n, h, dtype=F32, device=dev)
+        _lib.call("s24_gemm", ptr(g_c), 0, d, ptr(p.w2), 0, d, n, h, d, ptr(G), _lib.F32, h, None, 0, -1, s)
+        g_pre_dense = (G * act_squared_relu_grad(cache.pre_act)).to(BF16)
+
+    mode = cfg.backward_mode
+    if mode == "dense":
+        act = torch.empty(n, h, dtype=BF16, device=dev)
+        _lib.call("s24_decompress_token", ptr(cache.act_vals), None, ptr(cache.act_meta), n, h, ptr(act), _lib.BF16, h, s)
+        if g_pre_dense is None:
+            gp = torch.empty(n, h, dtype=BF16, device=dev)
+            _lib.call("s24_decompress_token", ptr(g_vals), None, ptr(cache.act_meta), n, h, ptr(gp), _lib.BF16, h, s)
+        else:
+            gp = g_pre_dense
+        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, s)
+        census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
+        notify("d_w2", d_w2)
+        _lib.call("s24_gemm", ptr(gp), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, s)
+        census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
+        notify("d_w1", d_w1)
+    else:
+        if mode == "naive_sparse":
+            plan = _all_sparse_plan(h, dev)
+            macs_w2 = macs_w1 = sp_gemm_macs(n, h, d)
+        else:
+            plan = cache.plan
+            macs_w2 = macs_w1 = split_gemm_macs(n, d, plan)
+        # dW2 = split(act)^T g_c  (act is already restricted to the mask)
+        fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
+        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
+        census.append(GemmEvent("bwd.d_w2", True, macs_w2))
+        notify("d_w2", d_w2)
+        # dW1 = (split(g_pre)^T x_in)^T. The split path always sees the masked
+        # g_pre (ref splitgemm.py:72, even with mask_grad_with_fwd off);
+        # naive_sparse without the mask sparsifies the raw g_pre feature-wise.
+        if mode == "naive_sparse" and g_pre_dense is not None:
+            from .sparse24 import sparsify_feature_wise
+
+            gpad = torch.zeros(npad, h, dtype=BF16, device=dev)
+            gpad[:n] = g_pre_dense
+            sg, _, stats_g = sparsify_feature_wise(gpad)
+            _lib.call("s24_spmm", ptr(sg.data), ptr(sg.meta_hw), ptr(cache.x_in), 1, d, h, d, npad, ptr(d_w1),
+                      _lib.F32, h, None, 1, -1, s)
+        else:
+            fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+            split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
+            stats_g = fg.stats
+        census.append(GemmEvent("bwd.d_w1", True, macs_w1))
+        notify("d_w1", d_w1)
+        stats_a = fa.stats
+
+    if cfg.mask_grad_with_fwd:
+        _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
+                  ptr(cache.inv_dev), 0, -1, s)
+        census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
+    else:
+        _lib.call("s24_gemm", ptr(g_pre_dense), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
+                  ptr(cache.inv_dev), 0, -1, s)
+        census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
+    return FfnGrads(d_w1, d_w2, d_x, None, census, stats_a, stats_g)

@@ -1,0 +1,180 @@
+"""Split GEMM (paper Optimization 1; drop-in for the reference's
+pkg/src/srelu24/splitgemm.py).
+
+Features are ranked by nonzero count; the ceil(ratio*h) sparsest go through a
+feature-wise 2:4 sparse GEMM, the rest through an exact dense GEMM, and both
+partial products scatter into the output by feature index inside the GEMM
+epilogue (row map). The plan is computed on the device (K7) from counts that
+the forward GEMM's epilogue already produced, so no host sync is needed: its
+sizes follow from h and the ratio alone.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import BF16, F32, as_matrix, pad128, ptr, stream
+from .errors import ConfigError, DimensionError
+from .sparse24 import (
+    SparsifyStats,
+    TOKEN_WISE,
+    apply_mask,
+    sp_gemm_macs,
+    sparsify_feature_wise,
+)
+from .matcore import gemm_macs
+
+
+@dataclass(frozen=True)
+class SplitPlan:
+    """Partition of feature indices (ref splitgemm.py:17-25). Index lists are
+    int32 device tensors; feat_pos[j] = rank of j in the sparse list, or
+    -(rank in the dense list) - 1."""
+
+    hidden_dim: int
+    ratio: float
+    counts: torch.Tensor
+    sparse_features: torch.Tensor
+    dense_features: torch.Tensor
+    feat_pos: torch.Tensor
+
+    @property
+    def n_sparse(self) -> int:
+        return int(self.sparse_features.shape[0])
+
+    @property
+    def n_dense(self) -> int:
+        return int(self.dense_features.shape[0])
+
+
+def column_nonzero_counts(a) -> torch.Tensor:
+    """counts[j] = number of nonzero entries in column j (ref splitgemm.py:28-30).
+    (On the FFN hot path these counts come out of the K1 epilogue instead.)"""
+    a = as_matrix(a, "a")
+    return (a != 0).sum(dim=0).to(torch.int64)
+
+
+def ceil_fraction(ratio: float, h: int) -> int:
+    """ceil(ratio*h), exact for integral products (ref splitgemm.py:33-38)."""
+    x = ratio * h
+    if abs(x - round(x)) < 1e-9:
+        return int(round(x))
+    return math.ceil(x)
+
+
+def partition_features(counts, ratio: float) -> SplitPlan:
+    """Stable ascending (count, index) order; the first ceil(ratio*h) features
+    are sparse, both lists ascending (ref splitgemm.py:41-52). Runs on the
+    device (radix select + block scan, csrc/sparse_capi.cu k_plan)."""
+    if not 0.0 <= ratio <= 1.0:
+        raise ConfigError(f"split ratio must be in [0, 1], got {ratio}")
+    if isinstance(counts, np.ndarray) or not isinstance(counts, torch.Tensor):
+        counts = torch.as_tensor(np.asarray(counts, dtype=np.int64))
+    if not counts.is_cuda:
+        counts = counts.cuda()
+    h = int(counts.shape[0])
+    c32 = counts.to(torch.int32).contiguous()
+    k = ceil_fraction(ratio, h)
+    dev = c32.device
+    sp = torch.empty(max(k, 0), dtype=torch.int32, device=dev)
+    de = torch.empty(max(h - k, 0), dtype=torch.int32, device=dev)
+    pos = torch.empty(h, dtype=torch.int32, device=dev)
+    if h:
+        sp_buf = sp if k else torch.empty(1, dtype=torch.int32, device=dev)
+        de_buf = de if h - k else torch.empty(1, dtype=torch.int32, device=dev)
+        _lib.call("s24_plan", ptr(c32), h, k, ptr(sp_buf), ptr(de_buf), ptr(pos), stream())
+    return SplitPlan(h, ratio, counts, sp, de, pos)
+
+
+def split_gemm_macs(n: int, d: int, plan: SplitPlan) -> int:
+    """Exact MAC count n*d*(|sparse|/2 + |dense|) (ref splitgemm.py:84-88)."""
+    return sp_gemm_macs(n, plan.n_sparse, d) + gemm_macs(plan.n_dense, n, d)
+
+
+@dataclass
+class FeatureSplit:
+    """Device operands of one split weight-gradient GEMM, produced by K4."""
+
+    vs: torch.Tensor  # bf16 [pad128(n_sparse), n/2] feature-wise 2:4 values, K-major along tokens
+    es: torch.Tensor  # hw metadata, rows = sparse rank, K = tokens
+    vd: torch.Tensor  # bf16 [pad128(n_dense), n] dense features, transposed
+    stats: SparsifyStats
+
+
+def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan) -> FeatureSplit:
+    """K4: token-wise compressed [n, h] (vals + hw meta, n and h multiples of
+    128) -> feature-wise 2:4 of the sparse features + transposed dense
+    features (the apply_mask / gather / sparsify_feature_wise part of ref
+    splitgemm.py:72-80, without a dense round trip)."""
+    dev = vals.device
+    ns, nd = plan.n_sparse, plan.n_dense
+    vs = torch.empty(max(pad128(ns), 128), n // 2, dtype=BF16, device=dev)
+    es = torch.empty(_lib.meta_hw_bytes(max(ns, 1), n), dtype=torch.uint8, device=dev)
+    vd = torch.empty(max(pad128(nd), 128), n, dtype=BF16, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(vs), ptr(es),
+              ptr(vd), ptr(cnt), stream())
+    return FeatureSplit(vs, es, vd, SparsifyStats(n * ns, cnt))
+
+
+def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int, out: torch.Tensor,
+                      transposed: bool) -> None:
+    """out[S] = sparse(fs)^T b, out[D] = dense(fs)^T b on tensor cores, scattered
+    by feature index in the epilogue. b: bf16 [n, d] (K = tokens, MN-major).
+    transposed=True writes out as [d, h] (dW1 layout)."""
+    d = b.shape[1]
+    ld = out.shape[1]
+    if plan.n_sparse:
+        _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), plan.n_sparse, d, n, ptr(out),
+                  _lib.F32 if out.dtype == F32 else _lib.BF16, ld, ptr(plan.sparse_features), int(transposed),
+                  plan.n_sparse, stream())
+    if plan.n_dense:
+        _lib.call("s24_gemm", ptr(fs.vd), 0, n, ptr(b), 1, b.stride(0), plan.n_dense, d, n, ptr(out),
+                  _lib.F32 if out.dtype == F32 else _lib.BF16, ld, ptr(plan.dense_features), int(transposed),
+                  plan.n_dense, stream())
+
+
+def split_gemm_t(a, fwd_mask, b, plan: SplitPlan, out_dtype: torch.dtype = F32) -> torch.Tensor:
+    """Masked a^T b via one feature-wise 2:4 GEMM plus one dense GEMM, rows
+    scattered by feature index (ref splitgemm.py:55-81). Generic entry point
+    for arbitrary (mask, a); the FFN hot path calls feature_split +
+    split_weight_grad on the already-compressed activation instead."""
+    a = as_matrix(a, "a")
+    n, h = a.shape
+    if n % 4 != 0:
+        raise DimensionError(f"feature-wise groups need rows % 4 == 0, got {n}")
+    if plan.hidden_dim != h:
+        raise DimensionError(f"plan built for {plan.hidden_dim} features, matrix has {h}")
+    b = as_matrix(b, "b", BF16)
+    if b.shape[0] != n:
+        raise DimensionError(f"reduction dimensions differ: {tuple(a.shape)} x {tuple(b.shape)}")
+    am = apply_mask(a, fwd_mask)
+    d = b.shape[1]
+    out = torch.zeros(h, d, dtype=out_dtype, device=a.device)
+    if n % 128 == 0 and h % 128 == 0 and d % 32 == 0:
+        from .sparse24 import sparsify_token_wise
+
+        # exact token-wise compression of the masked operand keeps every value
+        # whose group has <= 2 nonzeros; for general masks fall back to the
+        # per-partition path below
+        if bool(((am.view(n, h // 4, 4) != 0).sum(-1) <= 2).all()):
+            t, _, _ = sparsify_token_wise(am)
+            fs = feature_split(t.data, t.meta_hw, n, h, plan)
+            split_weight_grad(fs, plan, b, n, out, transposed=False)
+            return out
+    from .sparse24 import sp_gemm_t
+    from .matcore import gemm_at
+
+    if plan.n_sparse:
+        sidx = plan.sparse_features.long()
+        s, _, _ = sparsify_feature_wise(am[:, sidx].contiguous())
+        out[sidx] = sp_gemm_t(s, b, out_dtype)
+    if plan.n_dense:
+        didx = plan.dense_features.long()
+        out[didx] = gemm_at(am[:, didx].contiguous(), b, out_dtype)
+    return out

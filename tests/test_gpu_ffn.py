@@ -1,0 +1,211 @@
+"""End-to-end parity of the drop-in FFN (ffn_forward / ffn_backward) on the GPU
+against the numpy oracle (oracle/srelu24_np.py, itself pinned to the
+reference by tests/test_oracle_golden.py).
+
+Bit-exact: permutation, keep masks / metadata, per-feature counts, split plan
+and every drop count, all evaluated on identical inputs (the GPU's own fp32
+pre-activation, or its own stored bf16 values for the feature-wise splits).
+Tolerance (relative Frobenius norm, stated per output): out / d_x are bf16
+outputs that pass through 2-3 bf16 roundings (act or g_pre, then the output),
+each <= 2^-9 relative, so we allow TOL_BF16 = 1e-2; the fp32 weight gradients
+see one bf16 rounding of act / g_pre, TOL_F32 = 8e-3. Mask flips caused by
+fp32 accumulation-order differences in Y1 are counted and must stay below
+1e-4 of the groups.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2503_16672_b200 as s24
+from oracle import srelu24_np as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 1e-2
+TOL_F32 = 8e-3
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def cfg_dict(cfg):
+    return dict(forward_mode=cfg.forward_mode, backward_mode=cfg.backward_mode,
+                mask_grad_with_fwd=cfg.mask_grad_with_fwd, permute_tokens=cfg.permute_tokens,
+                permute_seed=cfg.permute_seed, split_ratio=cfg.split_ratio)
+
+
+def run_gpu(x, w1, w2, dy, cfg, keep_pre=True):
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    out, cache = s24.ffn_forward(torch.from_numpy(x).cuda(), p, cfg, keep_pre_act=keep_pre)
+    grads = s24.ffn_backward(torch.from_numpy(dy).cuda(), cache, p, cfg)
+    torch.cuda.synchronize()
+    return out, cache, grads
+
+
+@pytest.mark.parametrize("n,d,h", [(4096, 512, 2048), (1024, 256, 512), (200, 128, 256)])
+def test_recipe_selection_exact_and_outputs_within_tolerance(n, d, h):
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.9, seed=0)
+    cfg = s24.RECIPE
+    out, cache, grads = run_gpu(x, w1, w2, dy, cfg)
+
+    # permutation (host PCG64 Fisher-Yates, same stream as the reference)
+    perm = O.make_permutation(0, n)
+    assert np.array_equal(cache.perm.cpu().numpy(), perm)
+
+    # selection replayed on the GPU's own fp32 pre-activation: bit-exact
+    pre = cache.pre_act.cpu().numpy()
+    r = np.maximum(pre, np.float32(0))
+    act = r * r
+    ov, om, omask, ost = O.sparsify_token(act)
+    assert np.array_equal(cache.act_sparse.meta.cpu().numpy(), om)
+    assert np.array_equal(cache.act_sparse.values.float().cpu().numpy(), O.bf16_round(ov))
+    assert np.array_equal(cache.counts.cpu().numpy(), O.column_counts(act))
+    assert cache.stats.nonzeros_before == ost["nonzeros_before"]
+    assert cache.stats.dropped == ost["dropped"]
+    osp, ode = O.partition(O.column_counts(act), cfg.split_ratio)
+    assert np.array_equal(cache.plan.sparse_features.cpu().numpy(), osp)
+    assert np.array_equal(cache.plan.dense_features.cpu().numpy(), ode)
+
+    # feature-wise drop counts of both weight-gradient splits, replayed on the
+    # GPU's stored (bf16) act and g_pre values
+    act_kept = s24.decompress(cache.act_sparse).cpu().numpy()
+    _, _, _, fst = O.sparsify_feature(np.ascontiguousarray(act_kept[:, osp]))
+    assert grads.stats_act.nonzeros_before == fst["nonzeros_before"]
+    assert grads.stats_act.dropped == fst["dropped"]
+
+    # end-to-end vs the oracle run independently on the same (bf16-rounded) inputs
+    o_out, o_cache = O.ffn_forward(x, w1, w2, cfg_dict(cfg), ordered=False)
+    o_g = O.ffn_backward(dy, o_cache, w1, w2, cfg_dict(cfg), ordered=False)
+    flips = int((o_cache["mask"] != omask).sum()) // 2
+    assert flips <= max(1, n * h // 4 // 10000), f"{flips} mask flips"
+    assert rel(out.float().cpu(), o_out) < TOL_BF16
+    assert rel(grads.d_x.float().cpu(), o_g["d_x"]) < TOL_BF16
+    assert rel(grads.d_w2.cpu(), o_g["d_w2"]) < TOL_F32
+    assert rel(grads.d_w1.cpu(), o_g["d_w1"]) < TOL_F32
+    assert [e.sparse for e in cache.census + grads.census] == [False, True, False, True, True, True]
+
+
+def test_dense_mode_matches_oracle():
+    n, d, h = 1024, 256, 1024
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.7, seed=3)
+    cfg = s24.FfnConfig()
+    out, cache, grads = run_gpu(x, w1, w2, dy, cfg)
+    o_out, o_cache = O.ffn_forward(x, w1, w2, cfg_dict(cfg), ordered=False)
+    o_g = O.ffn_backward(dy, o_cache, w1, w2, cfg_dict(cfg), ordered=False)
+    assert rel(out.float().cpu(), o_out) < TOL_BF16
+    assert rel(grads.d_x.float().cpu(), o_g["d_x"]) < TOL_BF16
+    assert rel(grads.d_w2.cpu(), o_g["d_w2"]) < TOL_F32
+    assert rel(grads.d_w1.cpu(), o_g["d_w1"]) < TOL_F32
+    assert [e.sparse for e in cache.census + grads.census] == [False] * 6
+
+
+@pytest.mark.parametrize("cfg", [
+    s24.FfnConfig(forward_mode="sparse24"),
+    s24.FfnConfig(forward_mode="sparse24", mask_grad_with_fwd=True),
+    s24.FfnConfig(forward_mode="sparse24", backward_mode="naive_sparse", mask_grad_with_fwd=True),
+    s24.FfnConfig(forward_mode="sparse24", backward_mode="naive_sparse"),
+    s24.FfnConfig(forward_mode="sparse24", backward_mode="split_masked"),
+    s24.FfnConfig(forward_mode="sparse24", backward_mode="split_masked", mask_grad_with_fwd=True,
+                  split_ratio=0.5, permute_tokens=True, permute_seed=7),
+])
+def test_ablation_configs_match_oracle(cfg):
+    n, d, h = 512, 256, 512
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=5)
+    out, cache, grads = run_gpu(x, w1, w2, dy, cfg)
+    o_out, o_cache = O.ffn_forward(x, w1, w2, cfg_dict(cfg), ordered=False)
+    o_g = O.ffn_backward(dy, o_cache, w1, w2, cfg_dict(cfg), ordered=False)
+    assert rel(out.float().cpu(), o_out) < TOL_BF16
+    assert rel(grads.d_x.float().cpu(), o_g["d_x"]) < TOL_BF16
+    assert rel(grads.d_w2.cpu(), o_g["d_w2"]) < TOL_F32
+    assert rel(grads.d_w1.cpu(), o_g["d_w1"]) < TOL_F32
+
+
+def striped(n, d, seed):
+    """pre-activation with one positive per group of 4 in both orientations
+    (ref tests/test_ffn.py:117-124): nothing can ever be dropped."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = -np.abs(rng.standard_normal((n, d))).astype(np.float32) - 0.5
+    for i in range(n):
+        x[i, 4 * np.arange(d // 4) + (i % 4)] = np.abs(rng.standard_normal(d // 4)) + 0.5
+    return O.bf16_round(x)
+
+
+def test_no_drop_recipe_equals_dense_twin():
+    n, d = 512, 128
+    x = striped(n, d, 1)
+    w1 = np.eye(d, dtype=np.float32)
+    rng = np.random.Generator(np.random.PCG64(2))
+    w2 = O.bf16_round(rng.standard_normal((d, d)).astype(np.float32))
+    dy = O.bf16_round(rng.standard_normal((n, d)).astype(np.float32))
+    cfg = s24.FfnConfig(forward_mode="sparse24", backward_mode="split_masked", mask_grad_with_fwd=True)
+    out_s, cache, g_s = run_gpu(x, w1, w2, dy, cfg)
+    assert cache.stats.dropped == 0
+    assert g_s.stats_act.dropped == 0 and g_s.stats_grad.dropped == 0
+    out_d, _, g_d = run_gpu(x, w1, w2, dy, s24.FfnConfig())
+    assert rel(out_s.float().cpu(), out_d.float().cpu()) < 1e-2
+    assert rel(g_s.d_w1.cpu(), g_d.d_w1.cpu()) < 1e-2
+    assert rel(g_s.d_w2.cpu(), g_d.d_w2.cpu()) < 1e-2
+    assert rel(g_s.d_x.float().cpu(), g_d.d_x.float().cpu()) < 1e-2
+
+
+def test_zero_upstream_gradient_gives_zero_grads():
+    n, d, h = 256, 128, 256
+    x, w1, w2, _ = O.synthetic_ffn_inputs(n, d, h, seed=9)
+    out, cache, grads = run_gpu(x, w1, w2, np.zeros((n, d), np.float32), s24.RECIPE)
+    assert not grads.d_w1.any() and not grads.d_w2.any() and not grads.d_x.float().any()
+
+
+def test_state_and_dimension_errors():
+    n, d, h = 256, 128, 256
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, seed=4)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    out, cache = s24.ffn_forward(torch.from_numpy(x).cuda(), p, s24.RECIPE)
+    with pytest.raises(s24.StateError):
+        s24.ffn_backward(torch.from_numpy(dy).cuda(), cache, p, s24.FfnConfig())
+    with pytest.raises(s24.StateError):
+        s24.ffn_backward(torch.zeros(n + 4, d).cuda(), cache, p, s24.RECIPE)
+    with pytest.raises(s24.DimensionError):
+        s24.ffn_forward(torch.zeros(6, d).cuda(), p, s24.RECIPE)
+
+
+def test_sparse_api_functions_match_oracle():
+    rng = np.random.Generator(np.random.PCG64(11))
+    a = O.bf16_round(((rng.random((256, 384)) < 0.35) * rng.standard_normal((256, 384))).astype(np.float32))
+    b = O.bf16_round(rng.standard_normal((384, 64)).astype(np.float32))
+    s, mask, st = s24.sparsify_token_wise(a)
+    ov, om, omask, ost = O.sparsify_token(a)
+    assert np.array_equal(s.meta.cpu().numpy(), om)
+    assert np.array_equal(mask.cpu().numpy(), omask)
+    assert st.dropped == ost["dropped"]
+    kept = O.decompress_token(ov, om, *a.shape)
+    assert np.array_equal(s24.decompress(s).cpu().numpy(), kept)
+    assert rel(s24.sp_gemm(s, b).cpu(), kept @ b) < 1e-5
+    # feature-wise, then the transposed sparse GEMM
+    bt = O.bf16_round(rng.standard_normal((256, 64)).astype(np.float32))
+    f, fmask, fst = s24.sparsify_feature_wise(a)
+    fv, fm, fmask_o, fst_o = O.sparsify_feature(a)
+    assert np.array_equal(f.meta.cpu().numpy(), fm)
+    assert fst.dropped == fst_o["dropped"]
+    fk = O.decompress_feature(fv, fm, *a.shape)
+    assert rel(s24.sp_gemm_t(f, bt).cpu(), fk.T @ bt) < 1e-5
+    # exact mask compression and its error
+    c = s24.compress_token_wise_with_mask(torch.from_numpy(kept).cuda(), mask)
+    assert np.array_equal(s24.decompress(c).cpu().numpy(), kept)
+    bad = mask.clone()
+    bad[0, 0] = ~bad[0, 0]
+    with pytest.raises(s24.MaskError):
+        s24.compress_token_wise_with_mask(torch.from_numpy(kept).cuda(), bad)
+    with pytest.raises(s24.OrientationError):
+        s24.sp_gemm(f, b)
+    # split GEMM composite oracle (ref tests/test_splitgemm.py:91-97)
+    counts = s24.column_nonzero_counts(a)
+    plan = s24.partition_features(counts, 0.75)
+    osp, ode = O.partition(O.column_counts(a), 0.75)
+    assert np.array_equal(plan.sparse_features.cpu().numpy(), osp)
+    out = s24.split_gemm_t(a, mask, bt, plan)
+    ref, _ = O.split_gemm_t(a, omask, bt, osp, ode, ordered=False)
+    assert rel(out.cpu(), ref) < 1e-5
