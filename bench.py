@@ -1,0 +1,453 @@
+"""Benchmark: Squared-ReLU FFN fwd+bwd with 2:4 activation sparsity on B200.
+
+Contract (one JSON line on rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU runs are launched by torchrun (one rank per GPU, NCCL); each rank
+processes its own token shard (weak scaling) and the weight gradients are
+summed with one NCCL all-reduce per tensor inside the step.
+
+Workload (BASELINE.json configs[1]): FFN d=2048, h=8192, 16384 tokens per GPU,
+bf16 operands / fp32 accumulation, synthetic activations at 90% sparsity (95%
+of features at 0.9, 5% at 0.5), recipe = sparse24 forward +
+split_masked backward + mask_grad_with_fwd + token permutation, ratio 0.95.
+A "step" is one forward + backward of the FFN over the batch. Timing: CUDA
+events on the launching stream around every step, L2 flushed (256 MiB write)
+between steps outside the events, barrier + synchronize on both sides, max
+over ranks. The dense twin (same kernels, FfnConfig() dense) is timed the
+same way for the speedup. e2e repeats the recipe step through the public API
+with pinned host buffers: H2D of x and dY, D2H of out, dX, dW1, dW2.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Squared-ReLU FFN fwd+bwd tokens/sec & speedup vs dense bf16; sparse TFLOPS"
+CONFIGS = {"c1": (4096, 512, 2048), "c2": (16384, 2048, 8192), "c3": (32768, 4096, 16384)}
+WORKLOAD = {"c1": "c1: FFN d=512 h=2048, 4096 tokens/GPU, fwd+bwd",
+            "c2": "c2: FFN d=2048 h=8192 (1.5B-class), 16384 tokens/GPU, fwd+bwd",
+            "c3": "c4: FFN d=4096 h=16384 (7B-class), 32768 tokens/GPU, fwd+bwd"}
+SPARSITY = 0.9
+CPU_SAMPLE_TOKENS = 64
+REF_SAMPLE_TOKENS = 32
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# --------------------------------------------------------------------------- CPU reference (oracle port)
+
+
+def _cpu_sample(seed: int, n: int, d: int, h: int) -> float:
+    """One bounded sample of the workload on the CPU oracle (ordered-accumulation
+    GEMMs, the reference's own arithmetic): returns wall seconds."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import srelu24_np as O
+
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=SPARSITY, seed=seed)
+    t0 = time.perf_counter()
+    out, cache = O.ffn_forward(x, w1, w2, O.RECIPE, ordered=True)
+    O.ffn_backward(dy, cache, w1, w2, O.RECIPE, ordered=True)
+    return time.perf_counter() - t0
+
+
+def _cpu_worker(args):
+    seed, n, d, h = args
+    return _cpu_sample(seed, n, d, h)
+
+
+def cpu_parallel_step(procs: int, n: int, d: int, h: int, seed0: int = 0) -> float:
+    """procs independent samples in parallel processes; returns wall seconds."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        pool.map(_cpu_worker, [(seed0 + i, n, d, h) for i in range(procs)])
+    return time.perf_counter() - t0
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_total, d, h = CONFIGS[args.config]
+    procs = max(1, min(host_cores(), 32))
+    tok = REF_SAMPLE_TOKENS
+    # the pool start-up is part of every step; warm-up steps absorb import costs
+    for i in range(args.warmup):
+        cpu_parallel_step(procs, tok, d, h, seed0=1000 * (i + 1))
+    times = [cpu_parallel_step(procs, tok, d, h, seed0=7 + 100 * i) for i in range(args.steps)]
+    total = sum(times)
+    value = procs * tok * len(times) / total
+    sample = (f"{procs} processes x {tok} tokens each per step of the {WORKLOAD[args.config]} workload "
+              f"(oracle/srelu24_np.py recipe fwd+bwd, ordered fp32 GEMMs = the reference's arithmetic)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "d": d, "h": h, "sparsity": SPARSITY},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU side
+
+
+class KernelTracer:
+    """Brackets every libs24 entry point with CUDA events on the current stream
+    and records the algorithmic work of each launch (FLOPs or bytes)."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.records = []  # (label, kind, work, start_ev, end_ev)
+        self.launches = 0
+        self._open = None
+
+    @staticmethod
+    def work(name, a):
+        if name in ("s24_gemm",):
+            return "tensor", 2.0 * a[6] * a[7] * a[8], f"gemm dense M={a[6]} N={a[7]} K={a[8]}"
+        if name == "s24_spmm":
+            return "tensor_sparse", 2.0 * a[5] * a[6] * a[7], f"spmm 2:4 M={a[5]} N={a[6]} K={a[7]}"
+        if name in ("s24_fwd_gemm1_fused",):
+            return "tensor", 2.0 * a[4] * a[5] * a[6], "K1 gemm+relu2+2:4 (fwd.pre_act)"
+        if name in ("s24_bwd_dact_fused",):
+            return "tensor", 2.0 * a[4] * a[5] * a[6], "K3 gemm+relu2'+mask (bwd.d_act)"
+        if name in ("s24_gemm_relu2",):
+            return "tensor", 2.0 * a[4] * a[5] * a[6], "dense gemm+relu2"
+        if name in ("s24_gemm_dact",):
+            return "tensor", 2.0 * a[4] * a[5] * a[6], "dense gemm+relu2'"
+        if name == "s24_feature_split":
+            n, h, ns, nd = a[2], a[3], a[5], a[6]
+            return "hbm", n * h * 1.125 + n * ns * 1.125 + n * nd * 2.0, "K4 feature split"
+        if name == "s24_gather_rows":
+            return "hbm", 2.0 * a[1] * a[2], "K6 row gather"
+        if name == "s24_plan":
+            return "hbm", 4.0 * a[1] * 3, "K7 plan"
+        return "other", 0.0, name
+
+    def before(self, name, args):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self._open = (name, args, ev)
+
+    def after(self, name):
+        nm, args, s = self._open
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        kind, work, label = self.work(nm, args)
+        self.records.append((label, kind, work, s, e))
+        self.launches += 1
+
+    def summary(self):
+        agg = {}
+        for label, kind, work, s, e in self.records:
+            ms = s.elapsed_time(e)
+            a = agg.setdefault(label, {"kind": kind, "launches": 0, "ms": 0.0, "work": 0.0})
+            a["launches"] += 1
+            a["ms"] += ms
+            a["work"] += work
+        return agg
+
+
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sms, maxs, reasons = [], [], set()
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm, mx = float(f[0]), float(f[1])
+            except ValueError:
+                continue
+            sms.append(sm)
+            maxs.append(mx)
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        load = [s for s in sms if s > 0.5 * (max(sms) if sms else 1)]
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def synthetic_device_inputs(torch, n, d, h, seed, device):
+    """SURVEY 8d generator on the device (bf16): x ~ N(0,1) with a bias-carrier
+    last column; W1 ~ N(0, 1/(d-1)) with last row = Phi^-1(1 - s_j)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    bf = torch.bfloat16
+    x = torch.randn(n, d, generator=g, device=device)
+    x[:, -1] = 1.0
+    w1 = torch.randn(d, h, generator=g, device=device) / math.sqrt(d - 1)
+    s = torch.full((h,), SPARSITY, device=device)
+    dense_idx = torch.randperm(h, generator=g, device=device)[: int(round(0.05 * h))]
+    s[dense_idx] = 0.5
+    w1[-1] = torch.special.ndtri(1.0 - s)
+    w2 = torch.randn(h, d, generator=g, device=device) / math.sqrt(h)
+    dy = torch.randn(n, d, generator=g, device=device)
+    return x.to(bf), w1.to(bf), w2.to(bf), dy.to(bf)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2503_16672_b200 as s24
+    from paper_2503_16672_b200 import _lib
+    from paper_2503_16672_b200.dp import GradAllReducer
+
+    n, d, h = CONFIGS[args.config]
+    pk = peaks()
+    x, w1, w2, dy = synthetic_device_inputs(torch, n, d, h, seed=1234 + rank, device=dev)
+    params = s24.FfnParams(w1=w1, w2=w2)
+    recipe = s24.RECIPE
+    dense = s24.FfnConfig()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(cfg, xx, gg):
+        out, cache = s24.ffn_forward(xx, params, cfg)
+        if world > 1:
+            red = GradAllReducer()
+            grads = s24.ffn_backward(gg, cache, params, cfg, grad_ready=red)
+            red.wait()
+        else:
+            grads = s24.ffn_backward(gg, cache, params, cfg)
+        return out, cache, grads
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(cfg, k, tracer=None):
+        evs = []
+        barrier()
+        for _ in range(k):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            _lib.set_tracer(tracer)
+            s.record()
+            step(cfg, x, dy)
+            e.record()
+            _lib.set_tracer(None)
+            evs.append((s, e))
+        barrier()
+        return max_over_ranks(sum(s.elapsed_time(e) for s, e in evs))
+
+    # warm-up (also JIT-free: kernels are precompiled in libs24.so)
+    for _ in range(max(args.warmup, 3)):
+        step(recipe, x, dy)
+    if not args.no_dense:
+        for _ in range(max(args.warmup, 3)):
+            step(dense, x, dy)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    tracer = KernelTracer(torch)
+    t_recipe = timed(recipe, args.steps, tracer)
+    clk = clocks.stop()
+    t_dense = timed(dense, args.steps) if not args.no_dense else None
+
+    # drop statistics of one recipe step (reported, not timed)
+    out, cache, grads = step(recipe, x, dy)
+    torch.cuda.synchronize()
+    drops = {"fwd_token_wise_dropped_fraction": cache.stats.dropped_fraction_of_nonzeros,
+             "fwd_activation_sparsity": cache.stats.sparsity_before,
+             "bwd_act_feature_wise_dropped_fraction": grads.stats_act.dropped_fraction_of_nonzeros,
+             "bwd_grad_feature_wise_dropped_fraction": grads.stats_grad.dropped_fraction_of_nonzeros,
+             "plan_sparse_features": cache.plan.n_sparse, "plan_dense_features": cache.plan.n_dense}
+
+    ms_step = t_recipe / args.steps
+    value = world * n * args.steps / (t_recipe / 1e3)
+    flops_useful = 12.0 * n * d * h
+    result = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "tokens_per_gpu": n, "global_tokens": n * world, "d": d,
+                   "h": h, "activation_sparsity": SPARSITY, "recipe": "sparse24 fwd + split_masked bwd (ratio 0.95) "
+                   "+ mask_grad_with_fwd + permute_tokens", "parallelism": f"dp{world} (token shards, NCCL "
+                   "all-reduce of dW1/dW2)" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) between timed steps, outside the step events"},
+    }
+    if t_dense is not None:
+        result["dense_twin"] = {"value": world * n * args.steps / (t_dense / 1e3), "unit": "tokens/s",
+                                "ms_per_step": t_dense / args.steps}
+        result["speedup_vs_dense"] = t_dense / t_recipe
+    result["sparse_tflops"] = flops_useful / (ms_step / 1e3) / 1e12
+    result["drops"] = drops
+
+    # per-kernel breakdown and roofline of the dominant kernel (timed region)
+    agg = tracer.summary()
+    kernels = []
+    for label, a in sorted(agg.items(), key=lambda kv: -kv[1]["ms"]):
+        avg = a["ms"] / a["launches"]
+        per_launch = a["work"] / a["launches"]
+        if a["kind"] == "hbm":
+            ach, peak, unit = per_launch / (avg / 1e3) / 1e9, pk["hbm_gbs"], "GB/s"
+        elif a["kind"] == "tensor_sparse":
+            ach, peak, unit = per_launch / (avg / 1e3) / 1e12, 2 * pk["bf16_tflops"], "TFLOP/s"
+        elif a["kind"] == "tensor":
+            ach, peak, unit = per_launch / (avg / 1e3) / 1e12, pk["bf16_tflops"], "TFLOP/s"
+        else:
+            ach, peak, unit = 0.0, 1.0, "-"
+        kernels.append({"kernel": label, "launches_per_step": a["launches"] / args.steps,
+                        "ms_per_step": a["ms"] / args.steps, "share": a["ms"] / max(t_recipe, 1e-9),
+                        "achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak if peak else None})
+    dom = kernels[0]
+    result["roofline"] = {"kernel": dom["kernel"], "bound": "hbm" if dom["unit"] == "GB/s" else "tensor",
+                          "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
+                          "frac": dom["frac"], "traffic": None,
+                          "peak_source": f"{pk['source']} (MEASURED_PEAKS.json bf16 burst / hbm copy"
+                                         f"{'; 2:4 sparse peak = 2x dense, derived' if 'sparse' in dom['kernel'] or 'spmm' in dom['kernel'] else ''})"}
+    result["kernels"] = kernels
+    result["gpu_launches"] = tracer.launches
+    result["clocks"] = clk
+
+    # end-to-end through the public API with host buffers
+    if not args.no_e2e:
+        pin = dict(pin_memory=True)
+        xh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+        gh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+        xh.copy_(x)
+        gh.copy_(dy)
+        oh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+        dxh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+        dw1h = torch.empty(d, h, dtype=torch.float32, **pin)
+        dw2h = torch.empty(h, d, dtype=torch.float32, **pin)
+
+        def e2e_step():
+            xd = xh.to(dev, non_blocking=True)
+            gd = gh.to(dev, non_blocking=True)
+            out, cache, grads = step(recipe, xd, gd)
+            oh.copy_(out, non_blocking=True)
+            dxh.copy_(grads.d_x, non_blocking=True)
+            dw1h.copy_(grads.d_w1, non_blocking=True)
+            dw2h.copy_(grads.d_w2, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        evs = []
+        for _ in range(args.steps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            e2e_step()
+            e.record()
+            evs.append((s, e))
+        barrier()
+        t_e2e = max_over_ranks(sum(s.elapsed_time(e) for s, e in evs))
+        result["e2e"] = {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s",
+                         "h2d_bytes_per_step": 2 * n * d * 2,
+                         "d2h_bytes_per_step": 2 * n * d * 2 + 2 * d * h * 4,
+                         "ms_per_step": t_e2e / args.steps,
+                         "path": "ffn_forward/ffn_backward (public API) with pinned host x, dY in and out, dX, "
+                                 "dW1, dW2 out"}
+
+    # CPU baseline: the oracle port on this host, rank 0, N=1 only
+    if rank == 0 and world == 1 and not args.no_cpu:
+        t = _cpu_sample(11, CPU_SAMPLE_TOKENS, d, h)
+        result["cpu_baseline"] = {
+            "value": CPU_SAMPLE_TOKENS / t, "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"{CPU_SAMPLE_TOKENS} tokens of the {WORKLOAD[args.config]} workload through "
+                      f"oracle/srelu24_np.py (recipe fwd+bwd, ordered fp32 GEMMs), one process, {t:.1f} s"}
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -81,9 +81,25 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
+_tracer = None
+
+
+def set_tracer(tracer) -> None:
+    """Install (or clear with None) an object with before(name, args) / after(name)
+    hooks around every entry-point call; bench.py uses it to bracket each
+    kernel with CUDA events on the launching stream and to count launches."""
+    global _tracer
+    _tracer = tracer
+
+
 def call(name: str, *args) -> None:
     """Invoke an s24_* entry point and map a non-zero status to the exception."""
+    tr = _tracer
+    if tr is not None:
+        tr.before(name, args)
     rc = getattr(load(), name)(*args)
+    if tr is not None:
+        tr.after(name)
     if rc != 0:
         msg = load().s24_last_error().decode(errors="replace")
         raise _CODE_TO_EXC.get(rc, errors.BackendError)(msg)
