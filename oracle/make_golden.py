@@ -1,0 +1,155 @@
+"""TEST INFRASTRUCTURE ONLY -- regenerate tests/golden/*.npz from the reference.
+
+Imports the reference implementation itself (pure Python/numpy, read-only at
+/root/reference/pkg/src) and records its outputs on seeded inputs: the known
+answer cases of the reference's own tests plus random cases for every
+hot-path function (sparsifiers, mask compression, split plan, permutation,
+split GEMM, full FFN forward/backward under several configs). The fixtures
+are committed; /root/reference is not needed at test time.
+
+usage: python oracle/make_golden.py [--ref /root/reference/pkg/src]
+"""
+
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+
+
+def rng(seed):
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def bern(r, rows, cols, p):
+    return ((r.random((rows, cols)) < p) * r.standard_normal((rows, cols))).astype(np.float32)
+
+
+def stats_arr(st):
+    return np.array([st.total_entries, st.nonzeros_before, st.nonzeros_after, st.dropped], dtype=np.int64)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default="/root/reference/pkg/src")
+    args = ap.parse_args()
+    sys.path.insert(0, args.ref)
+    import srelu24 as R  # the reference package
+
+    OUT.mkdir(parents=True, exist_ok=True)
+
+    # ---------------------------------------------------------------- sparsifiers
+    cases = {}
+    kats = [np.array([[1, -2, 0, 0.5]], np.float32), np.array([[0, 0, 5, 0]], np.float32),
+            np.array([[1, -1, 2, 0]], np.float32), np.zeros((2, 8), np.float32)]
+    for i, a in enumerate(kats):
+        s, m, st = R.sparsify_token_wise(a)
+        cases[f"kat{i}_a"] = a
+        cases[f"kat{i}_values"] = s.values
+        cases[f"kat{i}_meta"] = s.meta
+        cases[f"kat{i}_mask"] = m
+        cases[f"kat{i}_stats"] = stats_arr(st)
+    for i, (rows, cols, p, seed) in enumerate([(64, 128, 0.3, 1), (32, 256, 0.1, 2), (16, 64, 0.9, 3)]):
+        a = bern(rng(seed), rows, cols, p)
+        a[0, :4] = [2.0, -2.0, 2.0, 0.0]  # three-way magnitude tie
+        s, m, st = R.sparsify_token_wise(a)
+        cases[f"tok{i}_a"] = a
+        cases[f"tok{i}_values"] = s.values
+        cases[f"tok{i}_meta"] = s.meta
+        cases[f"tok{i}_mask"] = m
+        cases[f"tok{i}_stats"] = stats_arr(st)
+        f, fm, fst = R.sparsify_feature_wise(a)
+        cases[f"feat{i}_values"] = f.values
+        cases[f"feat{i}_meta"] = f.meta
+        cases[f"feat{i}_mask"] = fm
+        cases[f"feat{i}_stats"] = stats_arr(fst)
+        kept = R.decompress(s)
+        c = R.compress_token_wise_with_mask(kept, m)
+        cases[f"cmp{i}_values"] = c.values
+        cases[f"cmp{i}_meta"] = c.meta
+        b = rng(seed + 50).standard_normal((cols, 8)).astype(np.float32)
+        cases[f"spg{i}_b"] = b
+        cases[f"spg{i}_out"] = R.sp_gemm(s, b)
+        bt = rng(seed + 60).standard_normal((rows, 8)).astype(np.float32)
+        cases[f"spgt{i}_b"] = bt
+        cases[f"spgt{i}_out"] = R.sp_gemm_t(f, bt)
+    np.savez_compressed(OUT / "sparse24.npz", **cases)
+
+    # ---------------------------------------------------------------- plan / permutation / split GEMM
+    cases = {}
+    plan_cases = [(np.array([0, 5, 1, 9]), 0.5), (np.array([3, 3, 3, 3]), 0.5), (np.zeros(4096, np.int64), 0.95),
+                  (np.arange(8), 1.0), (np.arange(8), 0.0), (np.array([5, 1, 5, 1, 0, 7, 7, 2, 2, 2]), 0.29)]
+    r = rng(2)
+    for _ in range(6):
+        h = int(r.integers(1, 300))
+        plan_cases.append((r.integers(0, 17, h), float(r.random())))
+    for i, (counts, ratio) in enumerate(plan_cases):
+        plan = R.partition_features(counts, ratio)
+        cases[f"plan{i}_counts"] = np.asarray(counts, np.int64)
+        cases[f"plan{i}_ratio"] = np.array([ratio])
+        cases[f"plan{i}_sparse"] = plan.sparse_features
+        cases[f"plan{i}_dense"] = plan.dense_features
+    for i, (seed, n) in enumerate([(0, 16), (3, 100), (0, 4096), (7, 1), (11, 37)]):
+        cases[f"perm{i}_seed"] = np.array([seed])
+        cases[f"perm{i}_p"] = R.make_permutation(seed, n)
+    for i, seed in enumerate(range(5, 9)):
+        rr = rng(seed)
+        a = bern(rr, 16, 12, 0.3)
+        _, mask, _ = R.sparsify_token_wise(a)
+        b = rr.standard_normal((16, 6)).astype(np.float32)
+        plan = R.partition_features(R.column_nonzero_counts(a), 0.75)
+        cases[f"split{i}_a"] = a
+        cases[f"split{i}_mask"] = mask
+        cases[f"split{i}_b"] = b
+        cases[f"split{i}_out"] = R.split_gemm_t(a, mask, b, plan)
+        cases[f"split{i}_sparse"] = plan.sparse_features
+        cases[f"split{i}_dense"] = plan.dense_features
+    np.savez_compressed(OUT / "splitgemm.npz", **cases)
+
+    # ---------------------------------------------------------------- full FFN
+    cases = {}
+    configs = {
+        "recipe": R.FfnConfig(forward_mode="sparse24", backward_mode="split_masked", mask_grad_with_fwd=True,
+                              permute_tokens=True),
+        "dense": R.FfnConfig(),
+        "fwd_sparse": R.FfnConfig(forward_mode="sparse24"),
+        "naive_masked": R.FfnConfig(forward_mode="sparse24", backward_mode="naive_sparse", mask_grad_with_fwd=True),
+        "split_nomask": R.FfnConfig(forward_mode="sparse24", backward_mode="split_masked"),
+        "recipe_seed3_r05": R.FfnConfig(forward_mode="sparse24", backward_mode="split_masked",
+                                        mask_grad_with_fwd=True, permute_tokens=True, permute_seed=3,
+                                        split_ratio=0.5),
+    }
+    for shape_i, (n, d, h) in enumerate([(32, 8, 16), (128, 32, 64)]):
+        rr = rng(100 + shape_i)
+        x = rr.standard_normal((n, d)).astype(np.float32)
+        w1 = (rr.standard_normal((d, h)) / np.sqrt(d)).astype(np.float32)
+        w2 = (rr.standard_normal((h, d)) / np.sqrt(h)).astype(np.float32)
+        g = rr.standard_normal((n, d)).astype(np.float32)
+        p = R.FfnParams(w1=w1, w2=w2)
+        tag = f"s{shape_i}"
+        cases[f"{tag}_x"], cases[f"{tag}_w1"], cases[f"{tag}_w2"], cases[f"{tag}_g"] = x, w1, w2, g
+        for name, cfg in configs.items():
+            out, cache = R.ffn_forward(x, p, cfg)
+            grads = R.ffn_backward(g, cache, p, cfg)
+            k = f"{tag}_{name}"
+            cases[f"{k}_out"] = out
+            cases[f"{k}_d_w1"] = grads.d_w1
+            cases[f"{k}_d_w2"] = grads.d_w2
+            cases[f"{k}_d_x"] = grads.d_x
+            cases[f"{k}_census"] = np.array([int(e.sparse) for e in cache.census + grads.census])
+            if cache.fwd_mask is not None:
+                cases[f"{k}_mask"] = cache.fwd_mask
+                cases[f"{k}_stats"] = stats_arr(cache.stats)
+            if cache.plan is not None:
+                cases[f"{k}_plan_sparse"] = cache.plan.sparse_features
+    np.savez_compressed(OUT / "ffn.npz", **cases)
+    for f in sorted(OUT.glob("*.npz")):
+        print(f, f.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

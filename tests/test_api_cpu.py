@@ -1,0 +1,79 @@
+"""Host-side logic of the drop-in API that needs no GPU: config validation
+(ref tests/test_ffn.py:85-114), split-plan sizing, MAC accounting, token
+sharding, and the loud failure when no device is present."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2503_16672_b200 as s24
+from paper_2503_16672_b200.dp import shard_bounds
+from paper_2503_16672_b200.splitgemm import ceil_fraction
+
+
+def test_config_defaults_and_recipe():
+    c = s24.FfnConfig()
+    assert (c.forward_mode, c.backward_mode, c.split_ratio) == ("dense", "dense", 0.95)
+    r = s24.RECIPE
+    assert r.forward_mode == "sparse24" and r.backward_mode == "split_masked"
+    assert r.mask_grad_with_fwd and r.permute_tokens
+    d = r.densified()
+    assert d.forward_mode == "dense" and not d.permute_tokens and d.split_ratio == r.split_ratio
+
+
+@pytest.mark.parametrize("kw", [
+    dict(backward_mode="split_masked"),
+    dict(backward_mode="naive_sparse"),
+    dict(mask_grad_with_fwd=True),
+    dict(split_ratio=1.5),
+    dict(split_ratio=-0.1),
+    dict(fp8_backward=True),
+    dict(activation="gelu"),
+    dict(forward_mode="sparse"),
+    dict(backward_mode="weird"),
+    dict(activation="swiglu", forward_mode="sparse24"),
+])
+def test_config_validation(kw):
+    with pytest.raises(s24.ConfigError):
+        s24.FfnConfig(**kw)
+
+
+def test_ceil_fraction_matches_reference_cases():
+    # ref tests/test_splitgemm.py:57-59 and the float-noise guard (splitgemm.py:33-38)
+    assert ceil_fraction(0.95, 4096) == 3892
+    assert ceil_fraction(0.95, 16384) == 15565
+    assert ceil_fraction(0.95, 8192) == 7783
+    assert ceil_fraction(0.29, 100) == 29
+    assert ceil_fraction(0.5, 3) == 2
+
+
+def test_mac_accounting():
+    assert s24.gemm_macs(2, 3, 4) == 24
+    assert s24.sp_gemm_macs(4, 8, 2) == 32
+
+
+def test_token_shards_cover_and_align():
+    for n, g in [(16384, 8), (32768, 3), (4096, 1), (100, 7)]:
+        bounds = [shard_bounds(n, g, r) for r in range(g)]
+        assert bounds[0][0] == 0 and bounds[-1][1] == n
+        for (a0, a1), (b0, b1) in zip(bounds, bounds[1:]):
+            assert a1 == b0
+        assert all((b - a) % 4 == 0 for a, b in bounds)
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 0)
+
+
+def test_permutation_is_the_reference_stream():
+    # PCG64 Fisher-Yates from the top: same as ref matcore.py:269-280
+    p = s24.make_permutation(0, 16)
+    assert sorted(p.tolist()) == list(range(16))
+    assert np.array_equal(p, s24.make_permutation(0, 16))
+    assert not np.array_equal(p, s24.make_permutation(1, 16))
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device failure mode")
+def test_no_cpu_fallback():
+    with pytest.raises(s24.BackendError):
+        s24.sparsify_token_wise(np.zeros((4, 8), np.float32))
+    with pytest.raises(s24.BackendError):
+        s24.FfnParams(w1=np.zeros((8, 16), np.float32), w2=np.zeros((16, 8), np.float32))
