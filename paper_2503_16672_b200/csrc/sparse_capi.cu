@@ -383,12 +383,43 @@ __global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts, i
 
 // ---------------------------------------------------------------------------
 // K4: feature-wise transposed split of a token-wise compressed [n, h] matrix.
-// CTA tile: 128 tokens x 128 features. Phase 1 decompresses the tile into
-// smem (row pitch 272 B, conflict-free 16 B stores); phase 2 walks each
-// feature column in token groups of 4 and emits either the feature-wise 2:4
-// form (sparse features, K-major along tokens + hw metadata) or the dense
-// column (dense features), both transposed so the dW GEMMs read K-major A.
-constexpr int K4_PITCH = 136;  // bf16 elements per smem row (128 + 8 pad)
+// CTA tile: 128 tokens x 128 features, 8 warps; warp w owns 16 features (one
+// 16-column metadata halfword per token), lane l owns the token group
+// 4l..4l+3. Everything stays in registers:
+//   1. each lane loads its 4 tokens' compressed 16-feature slices (16 B each)
+//      and metadata halfwords, and expands them with byte permutes into packed
+//      bf16 pairs X[token][feature pair];
+//   2. the feature-wise top-2 over the 4 tokens runs two features at a time in
+//      the 16-bit halves of 32-bit registers, on integer keys (|x| order of
+//      bf16 == unsigned order of its low 15 bits; NaN ranked last);
+//   3. sparse features emit (v0, v1) packed + a nibble (coalesced 128 B per
+//      warp per feature, halfwords assembled with 2 shuffles); dense features
+//      emit their 4 token values (coalesced 256 B per warp per feature).
+__constant__ unsigned long long kKeepToNibble = 0x000E0DC009804000ull;  // keep bits -> i0 | i1 << 2
+
+// bf16x2 magnitude keys, NaN mapped below zero (-1.0); ordered with native
+// bf16 compares (HSET2), which keeps the selection at one instruction per pair
+__device__ __forceinline__ uint32_t k4_key2(uint32_t x) {
+  const uint32_t mag = x & 0x7FFF7FFFu;
+  const __nv_bfloat162 m = *reinterpret_cast<const __nv_bfloat162*>(&mag);
+  const uint32_t nan = __hne2_mask(m, m);
+  return (mag & ~nan) | (0xBF80BF80u & nan);
+}
+
+__device__ __forceinline__ uint32_t k4_ge(uint32_t a, uint32_t b) {
+  return __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&a), *reinterpret_cast<const __nv_bfloat162*>(&b));
+}
+
+__device__ __forceinline__ uint32_t k4_nz(uint32_t x) {  // 1 per nonzero half, packed
+  const uint32_t mag = x & 0x7FFF7FFFu;
+  const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
+  return __hne2_mask(*reinterpret_cast<const __nv_bfloat162*>(&mag), z) & 0x00010001u;
+}
+
+__device__ __forceinline__ uint32_t k4_sel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
+
+// majority of three bitwise masks
+__device__ __forceinline__ uint32_t k4_maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 
 __global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __restrict__ vals,
                                                        const uint8_t* __restrict__ meta_hw, int n, int h,
@@ -396,92 +427,84 @@ __global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __re
                                                        __nv_bfloat16* __restrict__ vs, uint8_t* __restrict__ es,
                                                        __nv_bfloat16* __restrict__ vd,
                                                        unsigned long long* stats) {
-  __shared__ __align__(16) __nv_bfloat16 tile[128 * K4_PITCH];
-  const int f0 = blockIdx.x * 128, t0 = blockIdx.y * 128;
-  const int tid = threadIdx.x;
-  {
-    // phase 1: 2 threads per token row, 64 features (4 halfwords) each
-    const int tr = tid >> 1, half = tid & 1;
-    const int t = t0 + tr;
-    const __nv_bfloat16* src = vals + static_cast<long long>(t) * (h / 2) + f0 / 2 + half * 32;
-    uint32_t w[16];
+  // nibble -> PRMT selectors expanding (lo, hi) of a kept pair into 4 halfwords
+  __shared__ uint2 sel_lut[16];
+  if (threadIdx.x < 16) {
+    const uint32_t nib = threadIdx.x, i0 = nib & 3u, i1 = nib >> 2;
+    uint32_t sel[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 v = reinterpret_cast<const uint4*>(src)[i];
-      w[4 * i] = v.x;
-      w[4 * i + 1] = v.y;
-      w[4 * i + 2] = v.z;
-      w[4 * i + 3] = v.w;
-    }
-    __nv_bfloat16* dst = tile + tr * K4_PITCH + half * 64;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t m16 = *reinterpret_cast<const uint16_t*>(
-          meta_hw + meta_hw_halfword_offset(t, (f0 + half * 64) / 16 + q, h));
-      uint32_t outw[8];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const uint32_t nib = (m16 >> (4 * g)) & 0xFu;
-        const uint32_t pair = w[q * 4 + g];
-        const uint32_t lo = pair & 0xFFFFu, hi = pair >> 16;
-        uint32_t e[4] = {0u, 0u, 0u, 0u};
-        e[nib & 3u] = lo;
-        e[nib >> 2] = hi;
-        outw[2 * g] = e[0] | (e[1] << 16);
-        outw[2 * g + 1] = e[2] | (e[3] << 16);
-      }
-      uint4* d4 = reinterpret_cast<uint4*>(dst + q * 16);
-      d4[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-      d4[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
-    }
+    for (uint32_t q = 0; q < 4; ++q) sel[q] = (q == i0) ? 0x10u : (q == i1) ? 0x32u : 0x44u;
+    sel_lut[threadIdx.x] = make_uint2(sel[0] | (sel[1] << 8), sel[2] | (sel[3] << 8));
   }
   __syncthreads();
-  // phase 2: thread = (feature j, token half); 16 groups of 4 tokens
-  const int j = tid & 127, th = tid >> 7;
-  const int pos = feat_pos[f0 + j];
-  unsigned long long nb = 0, na = 0;
-  if (pos >= 0) {
-    uint32_t packed[16];
-    uint32_t m16[4] = {0u, 0u, 0u, 0u};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fbase = blockIdx.x * 128 + warp * 16;
+  const int t0 = blockIdx.y * 128;
+  const int t = t0 + 4 * lane;
+
+  // 1. load + expand: X[r][k] = bf16 pair of features (2k, 2k+1) for token t+r
+  uint32_t X[4][8];
 #pragma unroll
-    for (int g = 0; g < 16; ++g) {
-      const int tr = th * 64 + 4 * g;
-      const float x0 = __bfloat162float(tile[tr * K4_PITCH + j]);
-      const float x1 = __bfloat162float(tile[(tr + 1) * K4_PITCH + j]);
-      const float x2 = __bfloat162float(tile[(tr + 2) * K4_PITCH + j]);
-      const float x3 = __bfloat162float(tile[(tr + 3) * K4_PITCH + j]);
-      nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
-      const uint32_t keep = top2_keep_mask(x0, x1, x2, x3);
-      const uint32_t nib = keep_to_nibble(keep);
-      const float v0 = sel4(x0, x1, x2, x3, nib & 3u), v1 = sel4(x0, x1, x2, x3, nib >> 2);
-      na += (v0 != 0.f) + (v1 != 0.f);
-      packed[g] = pack_bf16x2(v0, v1);
-      m16[g >> 2] |= nib << (4 * (g & 3));
+  for (int r = 0; r < 4; ++r) {
+    const uint4 v = *reinterpret_cast<const uint4*>(vals + static_cast<long long>(t + r) * (h / 2) + fbase / 2);
+    const uint32_t m16 = *reinterpret_cast<const uint16_t*>(meta_hw + meta_hw_halfword_offset(t + r, fbase / 16, h));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint2 sl = sel_lut[(m16 >> (4 * g)) & 0xFu];
+      X[r][2 * g] = __byte_perm(w[g], 0u, sl.x);
+      X[r][2 * g + 1] = __byte_perm(w[g], 0u, sl.y);
     }
-    uint4* dst = reinterpret_cast<uint4*>(vs + static_cast<long long>(pos) * (n / 2) + t0 / 2 + th * 32);
+  }
+// feature positions (warp-uniform per feature)
+  const int my_pos = lane < 16 ? feat_pos[fbase + lane] : 0;
+  const unsigned long long lut = kKeepToNibble;
+
+  uint32_t cnt_b = 0, cnt_a = 0;  // packed per-half nonzero counters (sparse features only)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x0 = X[0][k], x1 = X[1][k], x2 = X[2][k], x3 = X[3][k];
+    const uint32_t k0 = k4_key2(x0), k1 = k4_key2(x1), k2 = k4_key2(x2), k3 = k4_key2(x3);
+    // i beats j (i < j) iff key_i >= key_j: ties go to the lower index
+    const uint32_t b01 = k4_ge(k0, k1), b02 = k4_ge(k0, k2), b03 = k4_ge(k0, k3);
+    const uint32_t b12 = k4_ge(k1, k2), b13 = k4_ge(k1, k3), b23 = k4_ge(k2, k3);
+    // kept <=> beats at least two of the other three
+    const uint32_t K0 = k4_maj(b01, b02, b03), K1 = k4_maj(~b01, b12, b13);
+    const uint32_t K2 = k4_maj(~b02, ~b12, b23), K3 = k4_maj(~b03, ~b13, ~b23);
+    const uint32_t v0 = k4_sel(K0, x0, k4_sel(K1, x1, x2));  // first kept token
+    const uint32_t v1 = k4_sel(K3, x3, k4_sel(K2, x2, x1));  // second kept token
+    const uint32_t kb = (K0 & 0x00010001u) | (K1 & 0x00020002u) | (K2 & 0x00040004u) | (K3 & 0x00080008u);
+    const uint32_t nib_lo = static_cast<uint32_t>(lut >> (4 * (kb & 0xFu))) & 0xFu;
+    const uint32_t nib_hi = static_cast<uint32_t>(lut >> (4 * ((kb >> 16) & 0xFu))) & 0xFu;
+    const uint32_t nzb = k4_nz(x0) + k4_nz(x1) + k4_nz(x2) + k4_nz(x3);
+    const uint32_t nza = k4_nz(v0) + k4_nz(v1);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      *reinterpret_cast<uint16_t*>(es + meta_hw_halfword_offset(pos, (t0 + th * 64) / 16 + q, n)) =
-          static_cast<uint16_t>(m16[q]);
-  } else {
-    const int dpos = -pos - 1;
-    uint32_t wds[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int tr = th * 64 + 2 * i;
-      const uint32_t lo = *reinterpret_cast<const uint16_t*>(&tile[tr * K4_PITCH + j]);
-      const uint32_t hi = *reinterpret_cast<const uint16_t*>(&tile[(tr + 1) * K4_PITCH + j]);
-      wds[i] = lo | (hi << 16);
+    for (int half = 0; half < 2; ++half) {
+      const int f = 2 * k + half;
+      const int pos = __shfl_sync(0xffffffffu, my_pos, f);
+      const uint32_t sh = 16u * half;
+      if (pos >= 0) {
+        cnt_b += (nzb >> sh) & 0xFFFFu;
+        cnt_a += (nza >> sh) & 0xFFFFu;
+        const uint32_t p0 = (v0 >> sh) & 0xFFFFu, p1 = (v1 >> sh) & 0xFFFFu;
+        reinterpret_cast<uint32_t*>(vs + static_cast<long long>(pos) * (n / 2) + t0 / 2)[lane] = p0 | (p1 << 16);
+        uint32_t hw = (half ? nib_hi : nib_lo) << (4 * (lane & 3));
+        hw |= __shfl_xor_sync(0xffffffffu, hw, 1);
+        hw |= __shfl_xor_sync(0xffffffffu, hw, 2);
+        if ((lane & 3) == 0)
+          *reinterpret_cast<uint16_t*>(es + meta_hw_halfword_offset(pos, t0 / 16 + (lane >> 2), n)) =
+              static_cast<uint16_t>(hw);
+      } else {
+        const int dpos = -pos - 1;
+        const uint32_t lo = half ? __byte_perm(x0, x1, 0x7632) : __byte_perm(x0, x1, 0x5410);
+        const uint32_t hi = half ? __byte_perm(x2, x3, 0x7632) : __byte_perm(x2, x3, 0x5410);
+        reinterpret_cast<uint2*>(vd + static_cast<long long>(dpos) * n + t0)[lane] = make_uint2(lo, hi);
+      }
     }
-    uint4* dst = reinterpret_cast<uint4*>(vd + static_cast<long long>(dpos) * n + t0 + th * 64);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) dst[i] = make_uint4(wds[4 * i], wds[4 * i + 1], wds[4 * i + 2], wds[4 * i + 3]);
   }
   if (stats) {
-    block_sum_u64_to(nb, stats);
-    block_sum_u64_to(na, stats + 1);
+    block_sum_u64_to(cnt_b, stats);
+    block_sum_u64_to(cnt_a, stats + 1);
   }
 }
 

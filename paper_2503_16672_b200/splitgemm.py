@@ -129,14 +129,32 @@ def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int
     transposed=True writes out as [d, h] (dW1 layout)."""
     d = b.shape[1]
     ld = out.shape[1]
-    if plan.n_sparse:
-        _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), plan.n_sparse, d, n, ptr(out),
-                  _lib.F32 if out.dtype == F32 else _lib.BF16, ld, ptr(plan.sparse_features), int(transposed),
-                  plan.n_sparse, stream())
+    code = _lib.F32 if out.dtype == F32 else _lib.BF16
+    main = torch.cuda.current_stream()
+    side = _side_stream(out.device) if plan.n_sparse and plan.n_dense else main
     if plan.n_dense:
-        _lib.call("s24_gemm", ptr(fs.vd), 0, n, ptr(b), 1, b.stride(0), plan.n_dense, d, n, ptr(out),
-                  _lib.F32 if out.dtype == F32 else _lib.BF16, ld, ptr(plan.dense_features), int(transposed),
-                  plan.n_dense, stream())
+        # the thin dense remainder (~5% of the rows) runs on a side stream so its
+        # CTAs fill the SMs the sparse GEMM's last wave leaves idle
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            _lib.call("s24_gemm", ptr(fs.vd), 0, n, ptr(b), 1, b.stride(0), plan.n_dense, d, n, ptr(out), code, ld,
+                      ptr(plan.dense_features), int(transposed), plan.n_dense, side.cuda_stream)
+    if plan.n_sparse:
+        _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), plan.n_sparse, d, n, ptr(out), code,
+                  ld, ptr(plan.sparse_features), int(transposed), plan.n_sparse, main.cuda_stream)
+    if side is not main:
+        main.wait_stream(side)
+
+
+_side_streams: dict[int, torch.cuda.Stream] = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    st = _side_streams.get(idx)
+    if st is None:
+        st = _side_streams[idx] = torch.cuda.Stream(device=device)
+    return st
 
 
 def split_gemm_t(a, fwd_mask, b, plan: SplitPlan, out_dtype: torch.dtype = F32) -> torch.Tensor:
