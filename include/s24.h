@@ -124,7 +124,8 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
  *   vd   bf16 [n_dense_pad128, n] dense features, transposed
  *   stats uint64[2] += (nonzeros before, after) over the sparse features.
  * Requires n % 128 == 0 and h % 128 == 0. Padding rows of vs/es/vd are
- * written (zeros / valid metadata). */
+ * written (zeros / valid metadata). With vs == es == NULL only the dense
+ * features are produced (the sparse ones come from the fused epilogues). */
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
                       unsigned long long* stats, void* stream);
@@ -134,12 +135,21 @@ int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64
  *   a_mn_major = 0: A stored [M][K] (lda >= K);  1: stored [K][M] (lda >= M)
  *   b_mn_major = 0: B stored [N][K] (ldb >= K);  1: stored [K][N] (ldb >= N)
  * D: [M, N] out_dtype with ldd; row m is written to row d_row_map[m] (if non
- * null); d_transposed writes D[n * ldd + row]. Rows >= d_rows_valid skipped.
+ * null); d_transposed writes D[n * ldd + row]. Rows >= d_rows_valid are
+ * skipped, and so are rows with d_row_valid[m] < 0 (if non null).
  * N % 32 == 0, leading dimensions 16-byte aligned.
  * Replaces gemm / gemm_at (matcore.py:71-106) on tensor cores (fp32 accum). */
 int s24_gemm(const void* A, int a_mn_major, int64_t lda, const void* B, int b_mn_major, int64_t ldb, int64_t M,
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-             int64_t d_rows_valid, void* stream);
+             int64_t d_rows_valid, const int* d_row_valid, void* stream);
+
+/* Split-K variant of s24_gemm for thin, long-K products (the dense remainder
+ * of the split weight gradient): k_splits partial GEMMs over K ranges write
+ * workspace fp32 [k_splits, M, N], then a fixed-order reduction writes D with
+ * the same row-map / transpose conventions (deterministic). */
+int s24_gemm_splitk(const void* A, int a_mn_major, int64_t lda, const void* B, int b_mn_major, int64_t ldb,
+                    int64_t M, int64_t N, int64_t K, int k_splits, float* workspace, void* D, int out_dtype,
+                    int64_t ldd, const int* d_row_map, int d_transposed, void* stream);
 
 /* 2:4 sparse A (token-wise along K): a_vals bf16 [M_pad128, K/2] + a_meta hw
  * (rows M_pad128, K). K % 128 == 0. Replaces sp_gemm (sparse24.py:170-192)
@@ -147,22 +157,31 @@ int s24_gemm(const void* A, int a_mn_major, int64_t lda, const void* B, int b_mn
  * (sparse24.py:195-216). */
 int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-             int64_t d_rows_valid, void* stream);
+             int64_t d_rows_valid, const int* d_row_valid, void* stream);
 
 /* K1: Y1 = X_in . W1 with the fused relu^2 + token-wise 2:4 epilogue
  * (ffn.py:305-329). x: [M, K] row-major; w1: [K, N] row-major (N = h,
  * N % 128 == 0). Outputs act_vals bf16 [M_pad128, N/2], act_meta hw, counts
- * int32[N] (+=, nullable), stats uint64[2] (+=), y_dbg fp32 [M, N] nullable. */
+ * int32[N] (+=, nullable), stats uint64[2] (+=), y_dbg fp32 [M, N] nullable.
+ * Fused feature-wise split (fw_vals non-null): the feature-wise 2:4 selection
+ * of the kept activation over groups of 4 consecutive tokens, for every
+ * feature (sparse24.py:96-115 as used by splitgemm.py:72-76), written
+ * transposed: fw_vals bf16 [N_pad128, fw_kdim/2] + fw_meta hw (rows = N
+ * features, K = fw_kdim tokens, fw_kdim = M padded to 128), fw_counts uint64[N]
+ * += nonzeros before | after << 32 per feature. */
 int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
                         int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
-                        float* y_dbg, void* stream);
+                        float* y_dbg, void* fw_vals, uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim,
+                        void* stream);
 
 /* K3: G = dY_c . W2^T with the fused relu^2-derivative + forward-mask
  * epilogue (ffn.py:395-417, 440-443). g: [M, K=d] row-major; w2: [N=h, K=d]
  * row-major. act_vals/act_meta: from K1. Output g_vals bf16 [M_pad128, N/2]
- * on the same metadata. */
+ * on the same metadata; optional fused feature-wise split of g_pre exactly as
+ * in s24_fwd_gemm1_fused. */
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
-                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* stream);
+                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* fw_vals,
+                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, void* stream);
 
 /* dense-mode twins: act = bf16(relu(X W1)^2) [M, N] (w1 stored [K][N]) */
 int s24_gemm_relu2(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N, int64_t K,

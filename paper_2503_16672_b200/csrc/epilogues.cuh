@@ -1,6 +1,6 @@
-// Epilogue functors for gemm_kernel. Each sees one 32-column chunk of one
-// accumulator row (fp32, straight out of TMEM) per call; all 32 lanes of the
-// warp call in lock-step (lane == row within the warp's 32-row slab).
+// Epilogue functors for gemm_kernel. Each call sees one 32-column chunk of one
+// accumulator row (fp32, straight out of TMEM); all 32 lanes of the warp call
+// in lock-step (lane == row within the warp's 32-row slab).
 #pragma once
 #include <cuda_bf16.h>
 #include "meta.cuh"
@@ -16,6 +16,47 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
+// bitwise 0 / 0xffffffff comparison mask (single FSET instruction)
+__device__ __forceinline__ uint32_t fge_mask(float a, float b) {
+  uint32_t r;
+  asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
+__device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// keep bits (4-bit mask with two bits set) -> nibble i0 | i1 << 2
+constexpr unsigned long long kKeepNibbleLut = 0x000E0DC009804000ull;
+
+__device__ __forceinline__ uint32_t keep_nibble(uint32_t kb) {
+  return static_cast<uint32_t>(kKeepNibbleLut >> (4u * kb)) & 0xFu;
+}
+
+}  // namespace s24
+#include "fwsel.cuh"
+namespace s24 {
+
+// 32x32 bit-matrix transpose across the warp: on return, bit l of lane i's
+// word is bit i of lane l's input word.
+__device__ __forceinline__ uint32_t warp_bit_transpose(uint32_t x, uint32_t lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const uint32_t m = masks[s];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? (((y >> j) & m) | (x & ~m)) : ((x & m) | ((y << j) & ~m));
+  }
+  return x;
+}
+
 // ---------------------------------------------------------------------------
 // Plain store: D[row_map(row), col] (or transposed D[col, row_map(row)]),
 // bf16 or fp32. Used for fwd.out / bwd.d_x (row_map = inverse permutation),
@@ -29,26 +70,34 @@ struct EpiStore {
     const int* row_map;  // nullable
     int transposed;      // 1: out[col * ldo + r]
     int n_rows_valid;    // rows >= this are padding (skip)
+    const int* row_valid;  // nullable: skip rows with row_valid[row] < 0
+    long long split_stride;  // split-K: partial of split ks goes to out + ks * split_stride
   };
-  using State = NoState;
+  struct State {
+    long long split_off;
+  };
   static constexpr bool kUnroll = false;
-  __device__ static void init(const Params&, State&) {}
-  __device__ static void prefetch(const Params&, State&, int, bool, int) {}
+  __device__ static void init(const Params&, State& s) { s.split_off = 0; }
+  __device__ static void prefetch(const Params& p, State& s, int, bool, int, int ks) {
+    s.split_off = ks * p.split_stride;
+  }
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, int c,
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int,
                                const float (&v)[32], uint32_t) {
     if (!row_ok || row >= p.n_rows_valid) return;
-    const long long r = p.row_map ? p.row_map[row] : row;
+    if (p.row_valid && p.row_valid[row] < 0) return;
+    const long long r = (p.row_map ? p.row_map[row] : row);
+    OutT* const out = p.out + s.split_off;
     if (p.transposed) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         if constexpr (sizeof(OutT) == 4)
-          p.out[static_cast<long long>(col0 + i) * p.ldo + r] = v[i];
+          out[static_cast<long long>(col0 + i) * p.ldo + r] = v[i];
         else
-          p.out[static_cast<long long>(col0 + i) * p.ldo + r] = __float2bfloat16_rn(v[i]);
+          out[static_cast<long long>(col0 + i) * p.ldo + r] = __float2bfloat16_rn(v[i]);
       }
     } else {
-      OutT* dst = p.out + r * p.ldo + col0;
+      OutT* dst = out + r * p.ldo + col0;
       if constexpr (sizeof(OutT) == 4) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
@@ -71,6 +120,9 @@ struct EpiStore {
 // of the pre-sparsify a (ref splitgemm.py:28-30, ffn.py:320-322) and the
 // nonzeros before/after totals (ref sparse24.py:60-69). The dense activation
 // never leaves registers. Optional debug dump of y (fp32) for parity tests.
+// Selection: with a >= 0, pairwise FSET masks b_ij (i < j: i beats j iff
+// a_i >= a_j, ties to the lower index); "kept iff it beats two of the other
+// three" is a bitwise majority; values are picked with bitwise selects.
 struct EpiFwd1 {
   struct Params {
     __nv_bfloat16* vals;  // [Mpad, N/2]
@@ -79,13 +131,18 @@ struct EpiFwd1 {
     unsigned long long* stats;  // [2] nnz before / after, accumulated
     float* y_dbg;         // nullable [M, N]
     int N;
+    FwTarget fw;          // fused feature-wise selection (fw.vals == nullptr: off)
   };
   struct State {
     unsigned long long before, after;
+    const uint2* lut;
   };
   static constexpr bool kUnroll = false;
-  __device__ static void init(const Params&, State& s) { s.before = s.after = 0; }
-  __device__ static void prefetch(const Params&, State&, int, bool, int) {}
+  __device__ static void init(const Params&, State& s) {
+    s.before = s.after = 0;
+    s.lut = fw_lut_init();
+  }
+  __device__ static void prefetch(const Params&, State&, int, bool, int, int) {}
   __device__ static void finish(const Params& p, State& s, uint32_t lane) {
     const unsigned long long b = warp_sum_u64(s.before), a = warp_sum_u64(s.after);
     if (lane == 0 && p.stats) {
@@ -93,7 +150,7 @@ struct EpiFwd1 {
       atomicAdd(p.stats + 1, a);
     }
   }
-  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int c,
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int,
                                const float (&v)[32], uint32_t lane) {
     float a[32];
     uint32_t nz = 0;
@@ -103,30 +160,35 @@ struct EpiFwd1 {
       a[i] = row_ok ? __fmul_rn(r, r) : 0.f;
       nz |= (a[i] != 0.f ? 1u : 0u) << i;
     }
-    // per-feature counts: column i of this chunk over the warp's 32 rows
+    // per-feature counts over the warp's 32 rows: transpose the nonzero bit
+    // matrix so lane i holds column i, then popcount
     if (p.counts) {
-      uint32_t my = 0;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t b = __ballot_sync(0xffffffffu, (nz >> i) & 1u);
-        my = (lane == static_cast<uint32_t>(i)) ? static_cast<uint32_t>(__popc(b)) : my;
-      }
-      if (my) atomicAdd(p.counts + col0 + lane, static_cast<int>(my));
+      const uint32_t col_bits = warp_bit_transpose(nz, lane);
+      if (col_bits) atomicAdd(p.counts + col0 + lane, __popc(col_bits));
     }
-    if (!row_ok) return;
-    s.before += __popc(nz);
     uint32_t packed[8];
     uint32_t m16[2] = {0u, 0u};
+    uint32_t keep32 = 0;
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
-      const uint32_t keep = top2_keep_mask(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3]);
-      const uint32_t nib = keep_to_nibble(keep);
-      const float v0 = sel4(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3], nib & 3u);
-      const float v1 = sel4(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3], nib >> 2);
-      s.after += (v0 != 0.f) + (v1 != 0.f);
+      const float a0 = a[4 * g], a1 = a[4 * g + 1], a2 = a[4 * g + 2], a3 = a[4 * g + 3];
+      const uint32_t b01 = fge_mask(a0, a1), b02 = fge_mask(a0, a2), b03 = fge_mask(a0, a3);
+      const uint32_t b12 = fge_mask(a1, a2), b13 = fge_mask(a1, a3), b23 = fge_mask(a2, a3);
+      const uint32_t K0 = maj3(b01, b02, b03), K1 = maj3(~b01, b12, b13);
+      const uint32_t K2 = maj3(~b02, ~b12, b23), K3 = maj3(~b03, ~b13, ~b23);
+      const uint32_t kb = (K0 & 1u) | (K1 & 2u) | (K2 & 4u) | (K3 & 8u);
+      const uint32_t u0 = __float_as_uint(a0), u1 = __float_as_uint(a1), u2 = __float_as_uint(a2),
+                     u3 = __float_as_uint(a3);
+      const float v0 = __uint_as_float(bsel(K0, u0, bsel(K1, u1, u2)));  // first kept
+      const float v1 = __uint_as_float(bsel(K3, u3, bsel(K2, u2, u1)));  // second kept
       packed[g] = pack_bf16x2(v0, v1);
-      m16[g >> 2] |= nib << (4 * (g & 3));
+      m16[g >> 2] |= keep_nibble(kb) << (4 * (g & 3));
+      keep32 |= kb << (4 * g);
     }
+    if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
+    if (!row_ok) return;
+    s.before += __popc(nz);
+    s.after += __popc(nz & keep32);
     __nv_bfloat16* dst = p.vals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
     st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
     st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
@@ -149,62 +211,65 @@ struct EpiFwd1 {
 //   g_pre = G * 2 * relu(y1),  relu(y1) recovered as sqrt(a) from the cached
 // compressed activation a = relu(y1)^2. Output: compressed g_pre [M, N/2] on
 // the forward metadata (which is reused as-is for the dX sparse GEMM).
-// The tile's act values (256 B / row) and metadata rows are prefetched into
-// registers before the accumulator wait, so their latency hides under the MMA.
+// The warp's act values (CPW chunks x 32 B / row) and metadata rows are
+// prefetched into registers before the accumulator wait, so their latency
+// hides under the MMA.
 struct EpiBwd1 {
   struct Params {
     const __nv_bfloat16* act_vals;  // [Mpad, N/2]
     const uint8_t* meta;            // hw layout, K = N
     __nv_bfloat16* gvals;           // [Mpad, N/2] out
     int N;
+    FwTarget fw;                    // fused feature-wise selection of g_pre (fw.vals == nullptr: off)
   };
-  static constexpr int TILE_N = 256;
+  static constexpr int CPW = 4;  // chunks per epilogue warp (BN = 256, 8 epilogue warps)
   static constexpr bool kUnroll = true;
   struct State {
-    uint4 act[TILE_N / 16];  // 8 bf16 kept values per uint4 = 16 logical columns
-    uint4 meta[TILE_N / 128][2];
+    uint4 act[2 * CPW];  // 8 kept values per uint4 = 16 logical columns
+    uint4 meta[2];       // the row's two 16-byte metadata rows (k1 = 0, 1) of its atom
+    const uint2* lut;
   };
-  __device__ static void init(const Params&, State&) {}
+  __device__ static void init(const Params&, State& s) { s.lut = fw_lut_init(); }
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_base) {
-    if (!row_ok) return;
-    const uint4* a = reinterpret_cast<const uint4*>(p.act_vals + static_cast<long long>(row) * (p.N / 2) + col_base / 2);
+  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_first, int) {
+    if (!row_ok || col_first >= p.N) return;
+    const uint4* a =
+        reinterpret_cast<const uint4*>(p.act_vals + static_cast<long long>(row) * (p.N / 2) + col_first / 2);
 #pragma unroll
-    for (int i = 0; i < TILE_N / 16; ++i)
-      if (col_base + 16 * i < p.N) s.act[i] = a[i];
+    for (int i = 0; i < 2 * CPW; ++i) s.act[i] = a[i];
     const uint32_t r = static_cast<uint32_t>(row) & 127u;
-#pragma unroll
-    for (int at = 0; at < TILE_N / 128; ++at) {
-      if (col_base + 128 * at >= p.N) break;
-      const uint8_t* base = p.meta + meta_hw_halfword_offset(row, (col_base + 128 * at) / 16, p.N) -
-                            meta_atom_halfword_byte(r, 0);
-      const uint32_t row16 = 16u * (r & 7u) + 256u * (r >> 4);
-      s.meta[at][0] = *reinterpret_cast<const uint4*>(base + row16);
-      s.meta[at][1] = *reinterpret_cast<const uint4*>(base + row16 + 128);
+    const uint8_t* base =
+        p.meta + meta_hw_halfword_offset(row, col_first / 16, p.N) - meta_atom_halfword_byte(r, 0);
+    const uint32_t row16 = 16u * (r & 7u) + 256u * (r >> 4);
+    s.meta[0] = *reinterpret_cast<const uint4*>(base + row16);
+    s.meta[1] = *reinterpret_cast<const uint4*>(base + row16 + 128);
+  }
+  __device__ static uint32_t word(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int ci,
+                               const float (&v)[32], uint32_t lane) {
+    if (!row_ok) {
+      if (p.fw.vals) {
+        const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        fw_select_chunk(p.fw, zero, 0x44444444u, row, col0, lane, s.lut);
+      }
+      return;
     }
-  }
-  __device__ static uint32_t word(const uint4& v, int i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-  }
-  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int c,
-                               const float (&v)[32], uint32_t) {
-    if (!row_ok) return;
     const uint32_t m1 = (static_cast<uint32_t>(row) >> 3) & 1u;
-    // chunk c covers the 16-column quads 2c (k1 = 0) and 2c+1 (k1 = 1) of atom c/4, word k2 = c%4
-    const uint32_t w0 = word(s.meta[c >> 2][0], c & 3), w1 = word(s.meta[c >> 2][1], c & 3);
+    // the chunk's two 16-column quads (k1 = 0, 1) sit in word k2 = ci of the atom rows
+    const uint32_t w0 = word(s.meta[0], ci & 3), w1 = word(s.meta[1], ci & 3);
     const uint32_t m16[2] = {(w0 >> (16 * m1)) & 0xFFFFu, (w1 >> (16 * m1)) & 0xFFFFu};
-    const uint32_t aw[8] = {s.act[2 * c].x, s.act[2 * c].y, s.act[2 * c].z, s.act[2 * c].w,
-                            s.act[2 * c + 1].x, s.act[2 * c + 1].y, s.act[2 * c + 1].z, s.act[2 * c + 1].w};
+    const uint32_t aw[8] = {s.act[2 * ci].x,     s.act[2 * ci].y,     s.act[2 * ci].z,     s.act[2 * ci].w,
+                            s.act[2 * ci + 1].x, s.act[2 * ci + 1].y, s.act[2 * ci + 1].z, s.act[2 * ci + 1].w};
     uint32_t packed[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
       const uint32_t nib = (m16[g >> 2] >> (4 * (g & 3))) & 0xFu;
       const float g0 = sel4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3], nib & 3u);
       const float g1 = sel4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3], nib >> 2);
-      const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&aw[g]);
-      const float a0 = __bfloat162float(a2.x), a1 = __bfloat162float(a2.y);
-      packed[g] = pack_bf16x2(g0 * (2.f * sqrtf(a0)), g1 * (2.f * sqrtf(a1)));
+      const float a0 = __uint_as_float(aw[g] << 16), a1 = __uint_as_float(aw[g] & 0xFFFF0000u);
+      packed[g] = pack_bf16x2(g0 * (2.f * sqrt_approx(a0)), g1 * (2.f * sqrt_approx(a1)));
     }
+    if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
     __nv_bfloat16* dst = p.gvals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
     st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
     st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
@@ -221,9 +286,9 @@ struct EpiRelu2 {
   using State = NoState;
   static constexpr bool kUnroll = false;
   __device__ static void init(const Params&, State&) {}
-  __device__ static void prefetch(const Params&, State&, int, bool, int) {}
+  __device__ static void prefetch(const Params&, State&, int, bool, int, int) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, int c,
+  __device__ static void chunk(const Params& p, State&, int row, bool row_ok, int col0, int,
                                const float (&v)[32], uint32_t) {
     if (!row_ok) return;
     float a[32];
@@ -240,8 +305,9 @@ struct EpiRelu2 {
   }
 };
 
-// bwd: g_pre = G * 2 * sqrt(act), dense (ref ffn.py:415 with act_squared_relu_grad :172-173).
-// act chunks are software-pipelined 4 chunks ahead through registers.
+// bwd: g_pre = G * 2 * sqrt(act), dense (ref ffn.py:415 with act_squared_relu_grad
+// :172-173). The warp's act run (CPW chunks x 64 B / row) is prefetched into
+// registers before the accumulator wait.
 struct EpiDact {
   struct Params {
     const __nv_bfloat16* act;
@@ -250,51 +316,40 @@ struct EpiDact {
     long long ld_g;
     int N;
   };
-  static constexpr int AHEAD = 4;
+  static constexpr int CPW = 4;
   static constexpr bool kUnroll = true;
   struct State {
-    uint4 buf[AHEAD][4];
-    int col_base;
+    uint4 buf[CPW][4];
   };
   __device__ static void init(const Params&, State&) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void load(const Params& p, State& s, int row, int c, int slot) {
-    const int col = s.col_base + 32 * c;
-    if (col >= p.N) return;
-    const uint4* src = reinterpret_cast<const uint4*>(p.act + static_cast<long long>(row) * p.ld_act + col);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s.buf[slot][i] = src[i];
-  }
-  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_base) {
-    s.col_base = col_base;
+  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_first, int) {
     if (!row_ok) return;
 #pragma unroll
-    for (int c = 0; c < AHEAD; ++c) load(p, s, row, c, c);
+    for (int c = 0; c < CPW; ++c) {
+      if (col_first + 32 * c < p.N) {
+        const uint4* src =
+            reinterpret_cast<const uint4*>(p.act + static_cast<long long>(row) * p.ld_act + col_first + 32 * c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s.buf[c][i] = src[i];
+      }
+    }
   }
-  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int c,
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int ci,
                                const float (&v)[32], uint32_t) {
     if (!row_ok) return;
-    const int slot = c % AHEAD;
-    uint32_t ww[16];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      ww[4 * i] = s.buf[slot][i].x;
-      ww[4 * i + 1] = s.buf[slot][i].y;
-      ww[4 * i + 2] = s.buf[slot][i].z;
-      ww[4 * i + 3] = s.buf[slot][i].w;
-    }
-    load(p, s, row, c + AHEAD, slot);
     __nv_bfloat16* dst = p.gpre + static_cast<long long>(row) * p.ld_g + col0;
 #pragma unroll
-    for (int i = 0; i < 32; i += 8) {
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t ww[4] = {s.buf[ci][i].x, s.buf[ci][i].y, s.buf[ci][i].z, s.buf[ci][i].w};
       uint32_t o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&ww[i / 2 + j]);
-        o[j] = pack_bf16x2(v[i + 2 * j] * (2.f * sqrtf(__bfloat162float(a2.x))),
-                           v[i + 2 * j + 1] * (2.f * sqrtf(__bfloat162float(a2.y))));
+        const float a0 = __uint_as_float(ww[j] << 16), a1 = __uint_as_float(ww[j] & 0xFFFF0000u);
+        o[j] = pack_bf16x2(v[8 * i + 2 * j] * (2.f * sqrt_approx(a0)),
+                           v[8 * i + 2 * j + 1] * (2.f * sqrt_approx(a1)));
       }
-      st_global_v4(dst + i, o[0], o[1], o[2], o[3]);
+      st_global_v4(dst + 8 * i, o[0], o[1], o[2], o[3]);
     }
   }
 };

@@ -7,14 +7,17 @@
 //         tcgen05.mma.cta_group::2 by the leader CTA: each CTA stages its own
 //         128 rows of A and BN/2 columns of B; the pair's tensor cores read
 //         both halves of B, halving smem operand traffic per SM.
-// 256 threads per CTA:
-//   warp 0   : TMA producer (A/B tiles, 2:4 metadata atoms) into a ring of
+// 128 + 32*EPI_WARPS threads per CTA:
+//   warps 0..E-1 : epilogue (E = 4 or 8); warp w reads TMEM lanes
+//              32*(w%4)..+31 (= tile rows); 8 warps split the columns in two
+//              runs, chunk by chunk (32 fp32 columns) into the epilogue functor
+//   warp E   : TMA producer (A/B tiles, 2:4 metadata atoms) into a ring of
 //              STAGES smem slots
-//   warp 1   : MMA issuer (leader CTA, one thread): tcgen05.cp metadata
+//   warp E+1 : MMA issuer (leader CTA, one thread): tcgen05.cp metadata
 //              smem->TMEM, tcgen05.mma(.sp), tcgen05.commit
-//   warp 2   : TMEM allocator
-//   warps 4-7: epilogue; warp w reads TMEM lanes 32*(w%4)..+31 (= tile rows)
-//              chunk by chunk (32 fp32 columns) into the fused epilogue functor.
+//   warp E+2 : TMEM allocator
+// The producer and MMA warps sit at the highest warp ids because the warp
+// arbiter prefers higher ids: busy epilogue warps must not delay MMA issue.
 // Accumulators: two TMEM slots. Disjoint (2*BN columns) when they fit, else
 // overlapping by one 32-column chunk (slot 1 starts at BN-32): the epilogue
 // drains the shared chunk first and releases the slot right away, so the next
@@ -35,9 +38,10 @@ struct GemmShape {
   int M, N, K;          // logical sizes (K = logical K for sparse A)
   int tiles_m, tiles_n; // in units of (128*CG) x BN
   int group_m;          // raster: group_m M-tiles share one sweep over N
+  int k_splits;         // >1: split-K, work unit = (tile, K range); partials go to the epilogue with ks
 };
 
-template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_>
+template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8>
 struct GemmCfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr bool A_MN = A_MN_;
@@ -70,6 +74,11 @@ struct GemmCfg {
   static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
   static constexpr uint32_t IDESC = make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
+  static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
+  static constexpr int EPI_THREADS = 32 * EPI_WARPS;
+  static constexpr int THREADS = 128 + EPI_THREADS;
+  static constexpr int CPW = NCHUNK / (EPI_WARPS / 4);  // chunks per epilogue warp
+  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, int& nb) {
@@ -90,12 +99,16 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
     tma_load_2d(dst, map, bar, c0, c1);
 }
 
-// Epilogue contract: Epi::Params ep; per 32-column chunk c of one row
-//   Epi::chunk(ep, st, row, row_ok, col0, c, v[32], lane)  (all 32 lanes call it)
-// Epi::prefetch(ep, st, row, row_ok, col_base) once per tile before waiting
-// for the accumulator, and Epi::finish(ep, st, lane) once at the end.
+// Epilogue contract: each epilogue warp owns one TMEM lane quarter (32 tile
+// rows) and a run of CPW consecutive 32-column chunks. Per chunk:
+//   Epi::chunk(ep, st, row, row_ok, col0, ci, v[32], lane)   (all lanes call it)
+// where ci is the chunk's index within the warp's run (0..CPW-1, columns
+// col0..col0+31); Epi::prefetch(ep, st, row, row_ok, col_first, ks) once per
+// tile before the accumulator wait (col_first = first column of the run, ks =
+// the split-K index of the work unit), and
+// Epi::finish(ep, st, lane) once at the end.
 template <class Cfg, class Epi>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const GemmShape shape, const typename Epi::Params ep) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
@@ -111,30 +124,40 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  // roles: epilogue warps first, the latency-critical producer / MMA warps get
+  // the highest ids (the warp arbiter prefers higher warp ids)
+  constexpr int W_PROD = Cfg::EPI_WARPS, W_MMA = Cfg::EPI_WARPS + 1, W_ALLOC = Cfg::EPI_WARPS + 2;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
-  const int total_tiles = shape.tiles_m * shape.tiles_n;
-  const int num_kb = (shape.K + Cfg::BK - 1) / Cfg::BK;
+  const int mn_tiles = shape.tiles_m * shape.tiles_n;
+  const int total_tiles = mn_tiles * shape.k_splits;
+  const int num_kb_all = (shape.K + Cfg::BK - 1) / Cfg::BK;
+  // work unit t -> (output tile t % mn_tiles, K split t / mn_tiles)
+  auto kb_range = [&](int t, int& kb0, int& kb1) {
+    const int ks = t / mn_tiles;
+    kb0 = static_cast<int>(static_cast<long long>(ks) * num_kb_all / shape.k_splits);
+    kb1 = static_cast<int>(static_cast<long long>(ks + 1) * num_kb_all / shape.k_splits);
+  };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_PROD && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if constexpr (Cfg::SPARSE) tma_prefetch(&tmE);
   }
-  if (warp == 1 && lane == 0) {
+  if (warp == W_MMA && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], CG);
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], CG * 128);
+      mbar_init(&tempty_bar[a], CG * Cfg::EPI_THREADS);
     }
     fence_barrier_init();
   }
-  if (warp == 2) {
+  if (warp == W_ALLOC) {
     if constexpr (CG == 2)
       tmem_alloc_cg2<Cfg::TMEM_COLS>(tmem_slot);
     else
@@ -148,18 +171,19 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == W_PROD) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
-        int mb, nb;
-        tile_coords(shape, t, mb, nb);
+        int mb, nb, kb0, kb1;
+        tile_coords(shape, t % mn_tiles, mb, nb);
+        kb_range(t, kb0, kb1);
         const int m0 = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
         const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::BN_CTA;
         const int atom_row = mb * CG + static_cast<int>(rank);  // 128-row metadata block
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
@@ -183,7 +207,7 @@ __global__ void __launch_bounds__(256, 1)
               tma_load<CG>(sb + j * (Cfg::BN_CTA * 128), &tmB, &full_bar[stage], kb * Cfg::BK + 64 * j, n0);
           }
           if constexpr (Cfg::SPARSE)
-            tma_load<CG>(sb + Cfg::B_BYTES, &tmE, &full_bar[stage], 0, (atom_row * num_kb + kb) * 16);
+            tma_load<CG>(sb + Cfg::B_BYTES, &tmE, &full_bar[stage], 0, (atom_row * num_kb_all + kb) * 16);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -192,7 +216,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ------------------------------------------------------------ MMA issuer
     if (leader && lane == 0) {
       int stage = 0;
@@ -207,7 +231,9 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + slot * Cfg::SLOT1_COL;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -237,7 +263,7 @@ __global__ void __launch_bounds__(256, 1)
             } else {
               bdesc = make_sdesc(sb + j * 32, 16, 1024, kLayoutSw128);
             }
-            const uint32_t accum = (kb > 0 || j > 0) ? 1u : 0u;
+            const uint32_t accum = (kb > kb0 || j > 0) ? 1u : 0u;
             if constexpr (Cfg::SPARSE) {
               // metadata address must be 2-column aligned; the odd column is
               // selected by the descriptor's sparse-id2 field (bits 0-1)
@@ -256,10 +282,10 @@ __global__ void __launch_bounds__(256, 1)
           uint64_t* tf = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
           if constexpr (CG == 2) {
             mma_commit_cg2(&empty_bar[stage], 0x3);
-            if (kb == num_kb - 1) mma_commit_cg2(tf, 0x3);
+            if (kb == kb1 - 1) mma_commit_cg2(tf, 0x3);
           } else {
             mma_commit(&empty_bar[stage]);
-            if (kb == num_kb - 1) mma_commit(tf);
+            if (kb == kb1 - 1) mma_commit(tf);
           }
           if (++stage == Cfg::STAGES) {
             stage = 0;
@@ -269,19 +295,22 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp < Cfg::EPI_WARPS) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quarter
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int part = warp >> 2;             // which contiguous run of CPW chunks
+    const int c_begin = part * Cfg::CPW;
+    const bool owns_last = c_begin + Cfg::CPW == Cfg::NCHUNK;
     typename Epi::State st;
     Epi::init(ep, st);
     int iter = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++iter) {
       int mb, nb;
-      tile_coords(shape, t, mb, nb);
+      tile_coords(shape, t % mn_tiles, mb, nb);
       const int slot = iter & 1;
       const int row = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 + static_cast<int>(lane);
       const bool row_ok = row < shape.M;
-      Epi::prefetch(ep, st, row, row_ok, nb * Cfg::BN);
+      Epi::prefetch(ep, st, row, row_ok, nb * Cfg::BN + c_begin * 32, t / mn_tiles);
       uint64_t* tempty = &tempty_bar[Cfg::OVERLAP ? 0 : slot];
       if constexpr (Cfg::OVERLAP)
         mbar_wait(&tfull_bar[0], iter & 1);
@@ -289,12 +318,14 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&tfull_bar[slot], (iter >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * Cfg::SLOT1_COL;
-      // epilogues that keep per-chunk state (Epi::kUnroll) get a fully unrolled
-      // loop so that state stays in registers
-#pragma unroll(Epi::kUnroll ? Cfg::NCHUNK : 1)
-      for (int ci = 0; ci < Cfg::NCHUNK; ++ci) {
-        // overlapping slots: drain the shared chunk first
-        const int c = (Cfg::OVERLAP && slot == 0) ? (ci == 0 ? Cfg::NCHUNK - 1 : ci - 1) : ci;
+      // overlapping slots: the chunk shared with the other slot (last chunk of
+      // slot 0) is drained first so the next tile's MMAs can start at once
+      const bool rotate = Cfg::OVERLAP && slot == 0 && owns_last;
+      // epilogues with per-chunk register state (Epi::kUnroll) get a fully
+      // unrolled loop so that state is indexed statically
+#pragma unroll(Epi::kUnroll ? Cfg::CPW : 1)
+      for (int ci = 0; ci < Cfg::CPW; ++ci) {
+        const int c = rotate ? (ci == 0 ? Cfg::NCHUNK - 1 : c_begin + ci - 1) : c_begin + ci;
         const int col0 = nb * Cfg::BN + c * 32;
         uint32_t r[32];
         if (col0 < shape.N) {  // uniform across the warp
@@ -312,7 +343,7 @@ __global__ void __launch_bounds__(256, 1)
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          Epi::chunk(ep, st, row, row_ok, col0, c, v, lane);
+          Epi::chunk(ep, st, row, row_ok, col0, ci, v, lane);
         }
       }
       if constexpr (!Cfg::OVERLAP) {
@@ -331,7 +362,7 @@ __global__ void __launch_bounds__(256, 1)
     cluster_sync();
   else
     __syncthreads();
-  if (warp == 2) {
+  if (warp == W_ALLOC) {
     tc_fence_after();
     if constexpr (CG == 2)
       tmem_dealloc_cg2<Cfg::TMEM_COLS>(tmem_base);

@@ -70,7 +70,7 @@ int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
 // ---------------------------------------------------------------------------
 template <class Cfg, class Epi>
 static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream) {
+                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1) {
   if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
   CUtensorMap ma, mb;
@@ -109,7 +109,8 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   sh.tiles_m = static_cast<int>((M + Cfg::TILE_M - 1) / Cfg::TILE_M);
   sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
   sh.group_m = 16 / Cfg::CG;
-  const int tiles = sh.tiles_m * sh.tiles_n;
+  sh.k_splits = k_splits < 1 ? 1 : k_splits;
+  const int tiles = sh.tiles_m * sh.tiles_n * sh.k_splits;
   const int max_clusters = num_sms() / Cfg::CG;
   const int clusters = tiles < max_clusters ? tiles : max_clusters;
 
@@ -122,7 +123,7 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CG));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -148,11 +149,31 @@ using SparseK = GemmCfg<true, false, false, 256, 4, 2>;   // sparse A, B K-major
 
 template <class Epi>
 static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
-                          int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st) {
-  if (!a_mn && b_mn) return launch_gemm<DenseKN, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
-  if (!a_mn && !b_mn) return launch_gemm<DenseKK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
-  if (a_mn && b_mn) return launch_gemm<DenseMM, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
-  return launch_gemm<DenseMK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st);
+                          int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st, int k_splits = 1) {
+  if (!a_mn && b_mn) return launch_gemm<DenseKN, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+  if (!a_mn && !b_mn) return launch_gemm<DenseKK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+  if (a_mn && b_mn) return launch_gemm<DenseMM, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+  return launch_gemm<DenseMK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+}
+
+// split-K partial sums ws[ks][M][N] -> D (row map / transpose), fixed order
+template <typename OutT>
+__global__ void k_splitk_reduce(const float* __restrict__ ws, int k_splits, long long M, long long N,
+                                OutT* __restrict__ out, long long ldo, const int* __restrict__ row_map,
+                                int transposed) {
+  const long long total = M * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long m = i / N, n = i - m * N;
+    float acc = ws[i];
+    for (int k = 1; k < k_splits; ++k) acc += ws[k * total + i];
+    const long long r = row_map ? row_map[m] : m;
+    OutT* dst = transposed ? out + n * ldo + r : out + r * ldo + n;
+    if constexpr (sizeof(OutT) == 4)
+      *dst = acc;
+    else
+      *dst = __float2bfloat16_rn(acc);
+  }
 }
 
 template <class Epi>
@@ -193,22 +214,46 @@ int64_t s24_meta_hw_bytes(int64_t rows, int64_t cols) {
 
 int s24_gemm(const void* A, int a_mn_major, int64_t lda, const void* B, int b_mn_major, int64_t ldb, int64_t M,
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-             int64_t d_rows_valid, void* stream) {
+             int64_t d_rows_valid, const int* d_row_valid, void* stream) {
   int rc = check_common(M, N, K, lda, a_mn_major, ldb, b_mn_major);
   if (rc) return rc;
   if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
   return with_out(out_dtype, [&](auto tag) {
     using OutT = std::remove_pointer_t<decltype(tag)>;
     typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
-                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid)};
+                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
     return dispatch_dense<EpiStore<OutT>>(a_mn_major, b_mn_major, A, lda, B, ldb, M, N, K, ep,
                                           static_cast<cudaStream_t>(stream));
   });
 }
 
+int s24_gemm_splitk(const void* A, int a_mn_major, int64_t lda, const void* B, int b_mn_major, int64_t ldb,
+                    int64_t M, int64_t N, int64_t K, int k_splits, float* workspace, void* D, int out_dtype,
+                    int64_t ldd, const int* d_row_map, int d_transposed, void* stream) {
+  int rc = check_common(M, N, K, lda, a_mn_major, ldb, b_mn_major);
+  if (rc) return rc;
+  if (k_splits < 1 || k_splits > 64) return fail(S24_ERR_CONFIG, "k_splits must be in [1, 64]");
+  if (!workspace) return fail(S24_ERR_DIMENSION, "split-K needs a workspace of k_splits*M*N floats");
+  if (out_dtype != S24_F32 && out_dtype != S24_BF16) return fail(S24_ERR_PRECISION, "unsupported output dtype");
+  if (M == 0 || N == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  EpiStore<float>::Params ep{workspace, N, nullptr, 0, static_cast<int>(M), nullptr, M * N};
+  rc = dispatch_dense<EpiStore<float>>(a_mn_major, b_mn_major, A, lda, B, ldb, M, N, K, ep, st, k_splits);
+  if (rc) return rc;
+  long long blocks = (M * N + 255) / 256;
+  if (blocks > 4L * num_sms()) blocks = 4L * num_sms();
+  if (out_dtype == S24_F32)
+    k_splitk_reduce<float><<<static_cast<int>(blocks), 256, 0, st>>>(workspace, k_splits, M, N, static_cast<float*>(D),
+                                                                   ldd, d_row_map, d_transposed);
+  else
+    k_splitk_reduce<__nv_bfloat16><<<static_cast<int>(blocks), 256, 0, st>>>(
+        workspace, k_splits, M, N, static_cast<__nv_bfloat16*>(D), ldd, d_row_map, d_transposed);
+  return check_launch("k_splitk_reduce");
+}
+
 int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-             int64_t d_rows_valid, void* stream) {
+             int64_t d_rows_valid, const int* d_row_valid, void* stream) {
   int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
   if (rc) return rc;
   if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
@@ -216,29 +261,43 @@ int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_
   return with_out(out_dtype, [&](auto tag) {
     using OutT = std::remove_pointer_t<decltype(tag)>;
     typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
-                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid)};
+                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
     return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep,
                                            static_cast<cudaStream_t>(stream));
   });
 }
 
+static int check_fw(void* fw_vals, const uint8_t* fw_meta, int64_t fw_kdim, int64_t M) {
+  if (!fw_vals) return S24_OK;
+  if (!fw_meta) return fail(S24_ERR_DIMENSION, "feature-wise output needs its metadata buffer");
+  if (fw_kdim % 128 != 0 || fw_kdim < M)
+    return fail(S24_ERR_DIMENSION, "feature-wise K (tokens) %lld must be a multiple of 128 covering M", (long long)fw_kdim);
+  return S24_OK;
+}
+
 int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
                         int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
-                        float* y_dbg, void* stream) {
+                        float* y_dbg, void* fw_vals, uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim,
+                        void* stream) {
   int rc = check_common(M, N, K, ldx, 0, ldw1, 1);
   if (rc) return rc;
   if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
-  EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N)};
+  if ((rc = check_fw(fw_vals, fw_meta, fw_kdim, M))) return rc;
+  EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N),
+                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)}};
   return launch_gemm<DenseKN, EpiFwd1>(x, ldx, w1, ldw1, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
-                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* stream) {
+                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* fw_vals,
+                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, void* stream) {
   int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
   if (rc) return rc;
   if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
+  if ((rc = check_fw(fw_vals, fw_meta, fw_kdim, M))) return rc;
   EpiBwd1::Params ep{static_cast<const __nv_bfloat16*>(act_vals), act_meta, static_cast<__nv_bfloat16*>(g_vals),
-                     static_cast<int>(N)};
+                     static_cast<int>(N),
+                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)}};
   return launch_gemm<DenseKK, EpiBwd1>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 

@@ -421,6 +421,7 @@ __device__ __forceinline__ uint32_t k4_sel(uint32_t m, uint32_t a, uint32_t b) {
 // majority of three bitwise masks
 __device__ __forceinline__ uint32_t k4_maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 
+template <bool WITH_STATS>
 __global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __restrict__ vals,
                                                        const uint8_t* __restrict__ meta_hw, int n, int h,
                                                        const int* __restrict__ feat_pos,
@@ -441,6 +442,24 @@ __global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __re
   const int fbase = blockIdx.x * 128 + warp * 16;
   const int t0 = blockIdx.y * 128;
   const int t = t0 + 4 * lane;
+  // per-feature output bases, computed once by lanes 0..15 (feature fbase+lane)
+  // and broadcast with shuffles:
+  //   sparse (pos >= 0): ofs = word offset of the feature's vs row at token t0,
+  //                      mb  = byte offset of its metadata halfword for q = 0
+  //   dense  (pos <  0): ofs = 0x80000000 | uint2 offset of its vd row at t0
+  const int my_pos = lane < 16 ? feat_pos[fbase + lane] : 0;
+  if (vs == nullptr && !__any_sync(0xffffffffu, lane < 16 && my_pos < 0)) return;  // dense-only: no dense here
+  uint32_t my_ofs = 0, my_mb = 0;
+  if (my_pos >= 0) {
+    my_ofs = static_cast<uint32_t>(my_pos) * static_cast<uint32_t>(n / 4) + static_cast<uint32_t>(t0 / 4);
+    my_mb = static_cast<uint32_t>(meta_hw_halfword_offset(my_pos, t0 / 16, n));
+  } else {
+    my_ofs = 0x80000000u | (static_cast<uint32_t>(-my_pos - 1) * static_cast<uint32_t>(n / 4) +
+                            static_cast<uint32_t>(t0 / 4));
+  }
+  // this lane's in-atom offset of column chunk q = lane/4 (q = 0 is folded into my_mb)
+  const uint32_t qd = static_cast<uint32_t>(lane) >> 2;
+  const uint32_t q_off = 4u * (qd >> 1) + 128u * (qd & 1u);
 
   // 1. load + expand: X[r][k] = bf16 pair of features (2k, 2k+1) for token t+r
   uint32_t X[4][8];
@@ -456,53 +475,59 @@ __global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __re
       X[r][2 * g + 1] = __byte_perm(w[g], 0u, sl.y);
     }
   }
-// feature positions (warp-uniform per feature)
-  const int my_pos = lane < 16 ? feat_pos[fbase + lane] : 0;
   const unsigned long long lut = kKeepToNibble;
+  uint32_t* vs32 = reinterpret_cast<uint32_t*>(vs);
+  uint2* vd64 = reinterpret_cast<uint2*>(vd);
+  uint32_t cnt_b = 0, cnt_a = 0;  // per-half nonzero counters (sparse features only)
 
-  uint32_t cnt_b = 0, cnt_a = 0;  // packed per-half nonzero counters (sparse features only)
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t x0 = X[0][k], x1 = X[1][k], x2 = X[2][k], x3 = X[3][k];
-    const uint32_t k0 = k4_key2(x0), k1 = k4_key2(x1), k2 = k4_key2(x2), k3 = k4_key2(x3);
-    // i beats j (i < j) iff key_i >= key_j: ties go to the lower index
-    const uint32_t b01 = k4_ge(k0, k1), b02 = k4_ge(k0, k2), b03 = k4_ge(k0, k3);
-    const uint32_t b12 = k4_ge(k1, k2), b13 = k4_ge(k1, k3), b23 = k4_ge(k2, k3);
-    // kept <=> beats at least two of the other three
-    const uint32_t K0 = k4_maj(b01, b02, b03), K1 = k4_maj(~b01, b12, b13);
-    const uint32_t K2 = k4_maj(~b02, ~b12, b23), K3 = k4_maj(~b03, ~b13, ~b23);
-    const uint32_t v0 = k4_sel(K0, x0, k4_sel(K1, x1, x2));  // first kept token
-    const uint32_t v1 = k4_sel(K3, x3, k4_sel(K2, x2, x1));  // second kept token
-    const uint32_t kb = (K0 & 0x00010001u) | (K1 & 0x00020002u) | (K2 & 0x00040004u) | (K3 & 0x00080008u);
-    const uint32_t nib_lo = static_cast<uint32_t>(lut >> (4 * (kb & 0xFu))) & 0xFu;
-    const uint32_t nib_hi = static_cast<uint32_t>(lut >> (4 * ((kb >> 16) & 0xFu))) & 0xFu;
-    const uint32_t nzb = k4_nz(x0) + k4_nz(x1) + k4_nz(x2) + k4_nz(x3);
-    const uint32_t nza = k4_nz(v0) + k4_nz(v1);
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int f = 2 * k + half;
-      const int pos = __shfl_sync(0xffffffffu, my_pos, f);
-      const uint32_t sh = 16u * half;
-      if (pos >= 0) {
-        cnt_b += (nzb >> sh) & 0xFFFFu;
-        cnt_a += (nza >> sh) & 0xFFFFu;
-        const uint32_t p0 = (v0 >> sh) & 0xFFFFu, p1 = (v1 >> sh) & 0xFFFFu;
-        reinterpret_cast<uint32_t*>(vs + static_cast<long long>(pos) * (n / 2) + t0 / 2)[lane] = p0 | (p1 << 16);
-        uint32_t hw = (half ? nib_hi : nib_lo) << (4 * (lane & 3));
-        hw |= __shfl_xor_sync(0xffffffffu, hw, 1);
-        hw |= __shfl_xor_sync(0xffffffffu, hw, 2);
-        if ((lane & 3) == 0)
-          *reinterpret_cast<uint16_t*>(es + meta_hw_halfword_offset(pos, t0 / 16 + (lane >> 2), n)) =
-              static_cast<uint16_t>(hw);
-      } else {
-        const int dpos = -pos - 1;
-        const uint32_t lo = half ? __byte_perm(x0, x1, 0x7632) : __byte_perm(x0, x1, 0x5410);
-        const uint32_t hi = half ? __byte_perm(x2, x3, 0x7632) : __byte_perm(x2, x3, 0x5410);
-        reinterpret_cast<uint2*>(vd + static_cast<long long>(dpos) * n + t0)[lane] = make_uint2(lo, hi);
+    const uint32_t ofs0 = __shfl_sync(0xffffffffu, my_ofs, 2 * k), ofs1 = __shfl_sync(0xffffffffu, my_ofs, 2 * k + 1);
+    const bool sp0 = !(ofs0 & 0x80000000u), sp1 = !(ofs1 & 0x80000000u);
+    if (vs != nullptr && (sp0 || sp1)) {
+      const uint32_t k0 = k4_key2(x0), k1 = k4_key2(x1), k2 = k4_key2(x2), k3 = k4_key2(x3);
+      // token i beats token j (i < j) iff key_i >= key_j: ties go to the lower token
+      const uint32_t b01 = k4_ge(k0, k1), b02 = k4_ge(k0, k2), b03 = k4_ge(k0, k3);
+      const uint32_t b12 = k4_ge(k1, k2), b13 = k4_ge(k1, k3), b23 = k4_ge(k2, k3);
+      // kept <=> beats at least two of the other three
+      const uint32_t K0 = k4_maj(b01, b02, b03), K1 = k4_maj(~b01, b12, b13);
+      const uint32_t K2 = k4_maj(~b02, ~b12, b23), K3 = k4_maj(~b03, ~b13, ~b23);
+      const uint32_t v0 = k4_sel(K0, x0, k4_sel(K1, x1, x2));  // first kept token
+      const uint32_t v1 = k4_sel(K3, x3, k4_sel(K2, x2, x1));  // second kept token
+      const uint32_t kb = (K0 & 0x00010001u) | (K1 & 0x00020002u) | (K2 & 0x00040004u) | (K3 & 0x00080008u);
+      // metadata halfwords of both features at once: 4 lanes (token groups) x 4 bits
+      uint32_t hw = ((static_cast<uint32_t>(lut >> (4 * (kb & 0xFu))) & 0xFu) |
+                     ((static_cast<uint32_t>(lut >> (4 * ((kb >> 16) & 0xFu))) & 0xFu) << 16))
+                    << (4 * (lane & 3));
+      hw |= __shfl_xor_sync(0xffffffffu, hw, 1);
+      hw |= __shfl_xor_sync(0xffffffffu, hw, 2);
+      const uint32_t mb0 = __shfl_sync(0xffffffffu, my_mb, 2 * k), mb1 = __shfl_sync(0xffffffffu, my_mb, 2 * k + 1);
+      if constexpr (WITH_STATS) {
+        const uint32_t nzb = k4_nz(x0) + k4_nz(x1) + k4_nz(x2) + k4_nz(x3);
+        const uint32_t nza = k4_nz(v0) + k4_nz(v1);
+        if (sp0) {
+          cnt_b += nzb & 0xFFFFu;
+          cnt_a += nza & 0xFFFFu;
+        }
+        if (sp1) {
+          cnt_b += nzb >> 16;
+          cnt_a += nza >> 16;
+        }
+      }
+      if (sp0) {
+        vs32[ofs0 + lane] = __byte_perm(v0, v1, 0x5410);
+        if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + mb0 + q_off) = static_cast<uint16_t>(hw);
+      }
+      if (sp1) {
+        vs32[ofs1 + lane] = __byte_perm(v0, v1, 0x7632);
+        if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + mb1 + q_off) = static_cast<uint16_t>(hw >> 16);
       }
     }
+    if (!sp0) vd64[(ofs0 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x5410), __byte_perm(x2, x3, 0x5410));
+    if (!sp1) vd64[(ofs1 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x7632), __byte_perm(x2, x3, 0x7632));
   }
-  if (stats) {
+  if constexpr (WITH_STATS) {
     block_sum_u64_to(cnt_b, stats);
     block_sum_u64_to(cnt_a, stats + 1);
   }
@@ -697,16 +722,22 @@ int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64
   auto st = static_cast<cudaStream_t>(stream);
   const int64_t sp_pad = (n_sparse + 127) / 128 * 128, d_pad = (n_dense + 127) / 128 * 128;
   // padding rows: zero values, valid metadata (i0=0, i1=1 -> nibble 0x4)
-  if (sp_pad > n_sparse) {
+  if (vs != nullptr && sp_pad > n_sparse) {
     cudaMemsetAsync(static_cast<__nv_bfloat16*>(vs) + n_sparse * (n / 2), 0, (sp_pad - n_sparse) * (n / 2) * 2, st);
     cudaMemsetAsync(es + (n_sparse / 128) * (n / 128) * 2048, 0x44, (n / 128) * 2048, st);
   }
   if (d_pad > n_dense && vd)
     cudaMemsetAsync(static_cast<__nv_bfloat16*>(vd) + n_dense * n, 0, (d_pad - n_dense) * n * 2, st);
   dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
-  k_feature_split<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n),
-                                        static_cast<int>(h), feat_pos, static_cast<__nv_bfloat16*>(vs), es,
-                                        static_cast<__nv_bfloat16*>(vd), stats);
+  if (stats)
+    k_feature_split<true><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n),
+                                                static_cast<int>(h), feat_pos, static_cast<__nv_bfloat16*>(vs), es,
+                                                static_cast<__nv_bfloat16*>(vd), stats);
+  else
+    k_feature_split<false><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(vals), meta_hw,
+                                                 static_cast<int>(n), static_cast<int>(h), feat_pos,
+                                                 static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd),
+                                                 nullptr);
   return check_launch("k_feature_split");
 }
 

@@ -23,6 +23,7 @@ to bf16). Weight gradients are fp32, activations/outputs bf16.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field, replace
 
 import torch
@@ -37,9 +38,24 @@ from .sparse24 import (
     SparsifyStats,
     sp_gemm_macs,
 )
-from .splitgemm import SplitPlan, ceil_fraction, feature_split, partition_features, split_gemm_macs, split_weight_grad
+from .splitgemm import (
+    FusedFeatureOperand,
+    SplitPlan,
+    feature_split,
+    fused_weight_grad,
+    partition_features,
+    split_gemm_macs,
+    split_weight_grad,
+)
 
 ACTIVATIONS = ("squared_relu", "swiglu")
+
+# Where the feature-wise 2:4 operands of the split weight-gradient GEMMs come
+# from: False (default) = the standalone K4 kernel after the plan is known;
+# True = fused into the K1 / K3 epilogues for every feature (csrc/fwsel.cuh).
+# Both are bit-identical; on B200 the fused variant currently makes the K1/K3
+# epilogues the bottleneck, so it is opt-in.
+FUSED_FEATURE_SPLIT = os.environ.get("S24_FUSED_FW", "0") == "1"
 FORWARD_MODES = ("dense", "sparse24")
 BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
 
@@ -157,6 +173,7 @@ class FfnCache:
     census: list[GemmEvent]
     config: FfnConfig
     gate: torch.Tensor | None = None
+    act_fw: FusedFeatureOperand | None = None  # feature-wise 2:4 act of all features (from K1)
 
     @property
     def act_sparse(self) -> Sparse24Matrix | None:
@@ -252,7 +269,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         act = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_gemm_relu2", ptr(x_in), d, ptr(p.w1), h, n, h, d, ptr(act), h, s)
         census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
-        _lib.call("s24_gemm", ptr(act), 0, h, ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d, None, 0, -1, s)
+        _lib.call("s24_gemm", ptr(act), 0, h, ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d, None, 0, -1, None, s)
         census.append(GemmEvent("fwd.out", False, gemm_macs(n, h, d)))
         cache = FfnCache(x_in, n, None, None, act, None, None, None, None, None, None, None, census, cfg)
         return out, cache
@@ -266,8 +283,12 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     stats_dev = torch.zeros(2, dtype=torch.int64, device=dev)
     need_pre = keep_pre_act or not cfg.mask_grad_with_fwd
     pre = torch.empty(n, h, dtype=F32, device=dev) if need_pre else None
+    # the split / naive weight-gradient GEMMs read the activation feature-wise
+    # 2:4 compressed; K1's epilogue produces that operand for every feature
+    act_fw = FusedFeatureOperand.alloc(h, npad, dev) if (FUSED_FEATURE_SPLIT and cfg.backward_mode != "dense") else None
+    fw_args = act_fw.args() if act_fw is not None else (None, None, None, 0)
     _lib.call("s24_fwd_gemm1_fused", ptr(x_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta), ptr(counts),
-              ptr(stats_dev), ptr(pre), s)
+              ptr(stats_dev), ptr(pre), *fw_args, s)
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
 
     plan_out = None
@@ -277,10 +298,10 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         plan_out = plan if plan is not None else partition_features(counts, cfg.split_ratio)
 
     _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-              ptr(inv_dev), 0, -1, s)
+              ptr(inv_dev), 0, -1, None, s)
     census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
     cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
-                     SparsifyStats(n * h, stats_dev), counts, census, cfg)
+                     SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw)
     return out, cache
 
 
@@ -337,13 +358,13 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         g_pre = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_gemm_dact", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(act), h, ptr(g_pre), h, s)
         census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
-        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, s)
+        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, None, s)
         census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
         notify("d_w2", d_w2)
-        _lib.call("s24_gemm", ptr(g_pre), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, s)
+        _lib.call("s24_gemm", ptr(g_pre), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
-        _lib.call("s24_gemm", ptr(g_pre), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d, None, 0, -1, s)
+        _lib.call("s24_gemm", ptr(g_pre), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d, None, 0, -1, None, s)
         census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
         return FfnGrads(d_w1, d_w2, d_x, None, census)
 
@@ -352,14 +373,21 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     g_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
     if npad > n:
         g_vals[n:].zero_()
+    # K3's epilogue also emits the feature-wise 2:4 g_pre operand of the dW1
+    # GEMM when the split path will consume it
+    fused_g = FUSED_FEATURE_SPLIT and (
+        cfg.backward_mode == "split_masked" or (cfg.backward_mode == "naive_sparse" and cfg.mask_grad_with_fwd))
+    raw_naive = cfg.backward_mode == "naive_sparse" and not cfg.mask_grad_with_fwd
+    g_fw = FusedFeatureOperand.alloc(h, npad, dev) if fused_g else None
+    fw_args = g_fw.args() if g_fw is not None else (None, None, None, 0)
     _lib.call("s24_bwd_dact_fused", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(cache.act_vals), ptr(cache.act_meta),
-              ptr(g_vals), s)
+              ptr(g_vals), *fw_args, s)
     census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
     g_pre_dense = None
     if not cfg.mask_grad_with_fwd:
         # unmasked derivative: needs relu(y1) everywhere (fp32 pre-activation kept by the forward)
         G = torch.empty(n, h, dtype=F32, device=dev)
-        _lib.call("s24_gemm", ptr(g_c), 0, d, ptr(p.w2), 0, d, n, h, d, ptr(G), _lib.F32, h, None, 0, -1, s)
+        _lib.call("s24_gemm", ptr(g_c), 0, d, ptr(p.w2), 0, d, n, h, d, ptr(G), _lib.F32, h, None, 0, -1, None, s)
         g_pre_dense = (G * act_squared_relu_grad(cache.pre_act)).to(BF16)
 
     mode = cfg.backward_mode
@@ -371,10 +399,10 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
             _lib.call("s24_decompress_token", ptr(g_vals), None, ptr(cache.act_meta), n, h, ptr(gp), _lib.BF16, h, s)
         else:
             gp = g_pre_dense
-        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, s)
+        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, None, s)
         census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
         notify("d_w2", d_w2)
-        _lib.call("s24_gemm", ptr(gp), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, s)
+        _lib.call("s24_gemm", ptr(gp), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
     else:
@@ -385,35 +413,42 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
             plan = cache.plan
             macs_w2 = macs_w1 = split_gemm_macs(n, d, plan)
         # dW2 = split(act)^T g_c  (act is already restricted to the mask)
-        fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
-        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
+        if cache.act_fw is not None:
+            fused_weight_grad(cache.act_fw, cache.act_vals, cache.act_meta, h, plan, g_c, d_w2, transposed=False)
+            stats_a = cache.act_fw.stats(plan)
+        else:
+            fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
+            split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
+            stats_a = fa.stats
         census.append(GemmEvent("bwd.d_w2", True, macs_w2))
         notify("d_w2", d_w2)
         # dW1 = (split(g_pre)^T x_in)^T. The split path always sees the masked
         # g_pre (ref splitgemm.py:72, even with mask_grad_with_fwd off);
         # naive_sparse without the mask sparsifies the raw g_pre feature-wise.
-        if mode == "naive_sparse" and g_pre_dense is not None:
+        if raw_naive:
             from .sparse24 import sparsify_feature_wise
 
             gpad = torch.zeros(npad, h, dtype=BF16, device=dev)
             gpad[:n] = g_pre_dense
             sg, _, stats_g = sparsify_feature_wise(gpad)
             _lib.call("s24_spmm", ptr(sg.data), ptr(sg.meta_hw), ptr(cache.x_in), 1, d, h, d, npad, ptr(d_w1),
-                      _lib.F32, h, None, 1, -1, s)
+                      _lib.F32, h, None, 1, -1, None, s)
+        elif g_fw is not None:
+            fused_weight_grad(g_fw, g_vals, cache.act_meta, h, plan, cache.x_in, d_w1, transposed=True)
+            stats_g = g_fw.stats(plan)
         else:
             fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
             split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
             stats_g = fg.stats
         census.append(GemmEvent("bwd.d_w1", True, macs_w1))
         notify("d_w1", d_w1)
-        stats_a = fa.stats
 
     if cfg.mask_grad_with_fwd:
         _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
-                  ptr(cache.inv_dev), 0, -1, s)
+                  ptr(cache.inv_dev), 0, -1, None, s)
         census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
     else:
         _lib.call("s24_gemm", ptr(g_pre_dense), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
-                  ptr(cache.inv_dev), 0, -1, s)
+                  ptr(cache.inv_dev), 0, -1, None, s)
         census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
     return FfnGrads(d_w1, d_w2, d_x, None, census, stats_a, stats_g)

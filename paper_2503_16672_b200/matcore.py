@@ -52,7 +52,7 @@ def gemm(a, b, out_dtype: torch.dtype = F32) -> torch.Tensor:
         bp = torch.zeros(k, npad, device=a.device, dtype=BF16)
         bp[:, :n] = b
         return gemm(a, bp, out_dtype)[:, :n].contiguous()
-    _lib.call("s24_gemm", ptr(a), 0, k, ptr(b), 1, n, m, n, k, ptr(out), _out_code(out_dtype), n, None, 0, -1,
+    _lib.call("s24_gemm", ptr(a), 0, k, ptr(b), 1, n, m, n, k, ptr(out), _out_code(out_dtype), n, None, 0, -1, None,
               stream())
     return out
 
@@ -74,7 +74,7 @@ def gemm_at(a, b, out_dtype: torch.dtype = F32) -> torch.Tensor:
         bp[:, :n] = b
         return gemm_at(ap, bp, out_dtype)[:m, :n].contiguous()
     out = torch.empty(m, n, device=a.device, dtype=out_dtype)
-    _lib.call("s24_gemm", ptr(a), 1, m, ptr(b), 1, n, m, n, k, ptr(out), _out_code(out_dtype), n, None, 0, -1,
+    _lib.call("s24_gemm", ptr(a), 1, m, ptr(b), 1, n, m, n, k, ptr(out), _out_code(out_dtype), n, None, 0, -1, None,
               stream())
     return out
 

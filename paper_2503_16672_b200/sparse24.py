@@ -26,8 +26,9 @@ FEATURE_WISE = "feature"
 
 class SparsifyStats:
     """Drop counts of one sparsification (ref sparse24.py:50-69). Backed by a
-    device counter pair (nonzeros before, after); fields materialise on first
-    access, so producing stats never forces a host sync."""
+    device counter pair (nonzeros before, after), or a callable producing it;
+    fields materialise on first access, so producing stats never forces a host
+    sync."""
 
     __slots__ = ("total_entries", "_dev", "_host")
 
@@ -38,7 +39,8 @@ class SparsifyStats:
 
     def _vals(self):
         if self._host is None:
-            b, a = (int(v) for v in self._dev.tolist())
+            dev = self._dev() if callable(self._dev) else self._dev
+            b, a = (int(v) for v in dev.tolist())
             self._host = (b, a)
         return self._host
 
@@ -266,7 +268,7 @@ def _spmm(vals, meta_hw, m: int, k: int, b: torch.Tensor, out_dtype) -> torch.Te
         b = bp
     out = torch.empty(m, npad, dtype=out_dtype, device=b.device)
     code = _lib.F32 if out_dtype == F32 else _lib.BF16
-    _lib.call("s24_spmm", ptr(vals), ptr(meta_hw), ptr(b), 1, npad, m, npad, kpad, ptr(out), code, npad, None, 0, -1,
+    _lib.call("s24_spmm", ptr(vals), ptr(meta_hw), ptr(b), 1, npad, m, npad, kpad, ptr(out), code, npad, None, 0, -1, None,
               stream())
     return out[:, :n] if npad != n else out
 

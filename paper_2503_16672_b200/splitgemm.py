@@ -106,20 +106,87 @@ class FeatureSplit:
     stats: SparsifyStats
 
 
-def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan) -> FeatureSplit:
+def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
+                  dense_only: bool = False, with_stats: bool = False) -> FeatureSplit:
     """K4: token-wise compressed [n, h] (vals + hw meta, n and h multiples of
     128) -> feature-wise 2:4 of the sparse features + transposed dense
     features (the apply_mask / gather / sparsify_feature_wise part of ref
-    splitgemm.py:72-80, without a dense round trip)."""
+    splitgemm.py:72-80, without a dense round trip). dense_only=True produces
+    only the dense columns (the FFN hot path gets the sparse operand from the
+    K1/K3 epilogues)."""
     dev = vals.device
     ns, nd = plan.n_sparse, plan.n_dense
-    vs = torch.empty(max(pad128(ns), 128), n // 2, dtype=BF16, device=dev)
-    es = torch.empty(_lib.meta_hw_bytes(max(ns, 1), n), dtype=torch.uint8, device=dev)
+    vs = es = None
+    if not dense_only:
+        vs = torch.empty(max(pad128(ns), 128), n // 2, dtype=BF16, device=dev)
+        es = torch.empty(_lib.meta_hw_bytes(max(ns, 1), n), dtype=torch.uint8, device=dev)
     vd = torch.empty(max(pad128(nd), 128), n, dtype=BF16, device=dev)
-    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev) if with_stats else None
     _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(vs), ptr(es),
               ptr(vd), ptr(cnt), stream())
-    return FeatureSplit(vs, es, vd, SparsifyStats(n * ns, cnt))
+    if with_stats:
+        stats = SparsifyStats(n * ns, cnt)
+    else:
+        # the reference discards these drop counts (splitgemm.py:75); they are
+        # recounted on the device only if someone reads them
+        stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
+    return FeatureSplit(vs, es, vd, stats)
+
+
+@dataclass
+class FusedFeatureOperand:
+    """Feature-wise 2:4 operand of ALL features, written by the K1 / K3
+    epilogues: vals bf16 [h, n/2] (K-major along tokens), meta hw (rows = h,
+    K = n), counts int64 [h] = nonzeros before | after << 32 per feature."""
+
+    vals: torch.Tensor
+    meta: torch.Tensor
+    counts: torch.Tensor
+    n: int
+
+    @staticmethod
+    def alloc(h: int, n: int, device) -> "FusedFeatureOperand":
+        return FusedFeatureOperand(torch.empty(pad128(h), n // 2, dtype=BF16, device=device),
+                                   torch.empty(_lib.meta_hw_bytes(h, n), dtype=torch.uint8, device=device),
+                                   torch.zeros(h, dtype=torch.int64, device=device), n)
+
+    def args(self):
+        return ptr(self.vals), ptr(self.meta), ptr(self.counts), self.n
+
+    def stats(self, plan: SplitPlan) -> SparsifyStats:
+        """Drop statistics of the sparse partition (what the reference's
+        sparsify_feature_wise(am[:, sparse]) would report)."""
+
+        def reduce():
+            c = self.counts if plan.n_dense == 0 else self.counts[plan.sparse_features.long()]
+            return torch.stack([(c & 0xFFFFFFFF).sum(), (c >> 32).sum()])
+
+        return SparsifyStats(self.n * plan.n_sparse, reduce)
+
+
+def fused_weight_grad(fo: FusedFeatureOperand, tok_vals: torch.Tensor, tok_meta: torch.Tensor, h: int,
+                      plan: SplitPlan, b: torch.Tensor, out: torch.Tensor, transposed: bool) -> None:
+    """Split weight gradient from the epilogue-fused feature-wise operand:
+    out[S] = sparse GEMM over all h feature rows of `fo` with the dense rows
+    skipped in the epilogue (row_valid = feat_pos), out[D] = dense GEMM over
+    the dense columns gathered from the token-wise operand (K4 dense-only, on a
+    side stream so it overlaps the sparse GEMM)."""
+    n = fo.n
+    d = b.shape[1]
+    ld = out.shape[1]
+    code = _lib.F32 if out.dtype == F32 else _lib.BF16
+    main = torch.cuda.current_stream()
+    if plan.n_dense:
+        side = _side_stream(out.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            fd = feature_split(tok_vals, tok_meta, n, h, plan, dense_only=True)
+            dense_remainder_gemm(fd.vd, b, n, plan, out, transposed, code, side)
+    if plan.n_sparse:
+        _lib.call("s24_spmm", ptr(fo.vals), ptr(fo.meta), ptr(b), 1, b.stride(0), h, d, n, ptr(out), code, ld, None,
+                  int(transposed), h, ptr(plan.feat_pos) if plan.n_dense else None, main.cuda_stream)
+    if plan.n_dense:
+        main.wait_stream(side)
 
 
 def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int, out: torch.Tensor,
@@ -132,18 +199,33 @@ def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int
     code = _lib.F32 if out.dtype == F32 else _lib.BF16
     main = torch.cuda.current_stream()
     side = _side_stream(out.device) if plan.n_sparse and plan.n_dense else main
-    if plan.n_dense:
-        # the thin dense remainder (~5% of the rows) runs on a side stream so its
-        # CTAs fill the SMs the sparse GEMM's last wave leaves idle
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            _lib.call("s24_gemm", ptr(fs.vd), 0, n, ptr(b), 1, b.stride(0), plan.n_dense, d, n, ptr(out), code, ld,
-                      ptr(plan.dense_features), int(transposed), plan.n_dense, side.cuda_stream)
+    if side is not main:
+        side.wait_stream(main)  # operands ready; the side work must not wait for the sparse GEMM
     if plan.n_sparse:
         _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), plan.n_sparse, d, n, ptr(out), code,
-                  ld, ptr(plan.sparse_features), int(transposed), plan.n_sparse, main.cuda_stream)
+                  ld, ptr(plan.sparse_features), int(transposed), plan.n_sparse, None, main.cuda_stream)
+    if plan.n_dense:
+        # the thin dense remainder (~5% of the rows, K = all tokens) is split
+        # along K and launched on a side stream right behind the sparse GEMM:
+        # its short work units fill the SMs the sparse GEMM's last wave leaves
+        # idle; a fixed-order reduction keeps the result deterministic
+        with torch.cuda.stream(side):
+            dense_remainder_gemm(fs.vd, b, n, plan, out, transposed, code, side)
     if side is not main:
         main.wait_stream(side)
+
+
+def dense_remainder_gemm(vd, b, n, plan, out, transposed, code, st) -> None:
+    d = b.shape[1]
+    nd = plan.n_dense
+    k_splits = max(1, min(8, n // 2048))
+    if k_splits > 1:
+        ws = torch.empty(k_splits, nd, d, dtype=F32, device=out.device)
+        _lib.call("s24_gemm_splitk", ptr(vd), 0, n, ptr(b), 1, b.stride(0), nd, d, n, k_splits, ptr(ws), ptr(out),
+                  code, out.shape[1], ptr(plan.dense_features), int(transposed), st.cuda_stream)
+    else:
+        _lib.call("s24_gemm", ptr(vd), 0, n, ptr(b), 1, b.stride(0), nd, d, n, ptr(out), code, out.shape[1],
+                  ptr(plan.dense_features), int(transposed), nd, None, st.cuda_stream)
 
 
 _side_streams: dict[int, torch.cuda.Stream] = {}

@@ -22,17 +22,17 @@ stats = torch.zeros(2, device="cuda", dtype=torch.int64)
 act = torch.empty(n, h, device="cuda", dtype=bf)
 gv = torch.empty_like(vals)
 out = torch.empty(n, d, device="cuda", dtype=bf)
-_lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, S)
+_lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, None, None, None, 0, S)
 for _ in range(4):
     if which == "k1":
-        _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, S)
+        _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, None, None, None, 0, S)
     elif which == "k3":
-        _lib.call("s24_bwd_dact_fused", P(x), d, P(w2), d, n, h, d, P(vals), P(meta), P(gv), S)
+        _lib.call("s24_bwd_dact_fused", P(x), d, P(w2), d, n, h, d, P(vals), P(meta), P(gv), None, None, None, 0, S)
     elif which == "dact":
         _lib.call("s24_gemm_dact", P(x), d, P(w2), d, n, h, d, P(act), h, P(act), h, S)
     elif which == "relu2":
         _lib.call("s24_gemm_relu2", P(x), d, P(w1), h, n, h, d, P(act), h, S)
     elif which == "spfwd":
-        _lib.call("s24_spmm", P(vals), P(meta), P(w2), 1, d, n, d, h, P(out), 1, d, None, 0, -1, S)
+        _lib.call("s24_spmm", P(vals), P(meta), P(w2), 1, d, n, d, h, P(out), 1, d, None, 0, -1, None, S)
 torch.cuda.synchronize()
 print("ok", which)

@@ -77,34 +77,34 @@ def main():
     f = 2.0 * n * d * h
     cb1 = timeit(lambda: torch.matmul(x, w1), args.iters, flush)
     rec("K1 fwd gemm1 fused", timeit(lambda: _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(act_vals),
-                                                          P(meta), P(counts), P(stats), None, S()), args.iters, flush),
+                                                          P(meta), P(counts), P(stats), None, None, None, None, 0, S()), args.iters, flush),
         f, cb1)
     rec("dense relu2 (twin of K1)", timeit(lambda: _lib.call("s24_gemm_relu2", P(x), d, P(w1), h, n, h, d, P(act), h,
                                                                 S()), args.iters, flush), f, cb1)
     cb2 = timeit(lambda: torch.matmul(act, w2), args.iters, flush)
     rec("K2 fwd.out sparse", timeit(lambda: _lib.call("s24_spmm", P(act_vals), P(meta), P(w2), 1, d, n, d, h, P(out),
-                                                         1, d, None, 0, -1, S()), args.iters, flush), f, cb2)
+                                                         1, d, None, 0, -1, None, S()), args.iters, flush), f, cb2)
     rec("fwd.out dense twin", timeit(lambda: _lib.call("s24_gemm", P(act), 0, h, P(w2), 1, d, n, d, h, P(out), 1, d,
-                                                          None, 0, -1, S()), args.iters, flush), f, cb2)
+                                                          None, 0, -1, None, S()), args.iters, flush), f, cb2)
     cb3 = timeit(lambda: torch.matmul(g, w2.t()), args.iters, flush)
     rec("K3 bwd dact fused", timeit(lambda: _lib.call("s24_bwd_dact_fused", P(g), d, P(w2), d, n, h, d, P(act_vals),
-                                                         P(meta), P(gv), S()), args.iters, flush), f, cb3)
+                                                         P(meta), P(gv), None, None, None, 0, S()), args.iters, flush), f, cb3)
     rec("dense dact (twin of K3)", timeit(lambda: _lib.call("s24_gemm_dact", P(g), d, P(w2), d, n, h, d, P(act), h,
                                                                P(act), h, S()), args.iters, flush), f, cb3)
     cb4 = timeit(lambda: torch.matmul(act, w1.t()), args.iters, flush)
     rec("K2 bwd.d_x sparse", timeit(lambda: _lib.call("s24_spmm", P(gv), P(meta), P(w1), 0, h, n, d, h, P(out), 1, d,
-                                                         None, 0, -1, S()), args.iters, flush), f, cb4)
+                                                         None, 0, -1, None, S()), args.iters, flush), f, cb4)
     rec("bwd.d_x dense twin", timeit(lambda: _lib.call("s24_gemm", P(act), 0, h, P(w1), 0, h, n, d, h, P(out), 1, d,
-                                                          None, 0, -1, S()), args.iters, flush), f, cb4)
+                                                          None, 0, -1, None, S()), args.iters, flush), f, cb4)
     dw = torch.empty(h, d, device="cuda")
     cb5 = timeit(lambda: torch.matmul(act.t(), g), args.iters, flush)
     rec("bwd.d_w dense twin (A MN)", timeit(lambda: _lib.call("s24_gemm", P(act), 1, h, P(g), 1, d, h, d, n, P(dw), 0,
-                                                                 d, None, 0, -1, S()), args.iters, flush), f, cb5)
+                                                                 d, None, 0, -1, None, S()), args.iters, flush), f, cb5)
     ns = (int(0.95 * h) + 127) // 128 * 128
     vs = torch.zeros(ns, n // 2, device="cuda", dtype=bf)
     es = torch.full((_lib.meta_hw_bytes(ns, n),), 0x44, device="cuda", dtype=torch.uint8)
     rec("bwd.d_w sparse part (M=0.95h)", timeit(lambda: _lib.call("s24_spmm", P(vs), P(es), P(g), 1, d, ns, d, n,
-                                                                     P(dw), 0, d, None, 0, -1, S()), args.iters, flush),
+                                                                     P(dw), 0, d, None, 0, -1, None, S()), args.iters, flush),
         2.0 * ns * d * n)
     # K4 split
     kcount = int(0.95 * h)

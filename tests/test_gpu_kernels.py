@@ -62,7 +62,7 @@ def test_dense_gemm_majors(a_mn, b_mn, M, N, K):
     As = A.t().contiguous() if a_mn else A
     Bs = B if b_mn else B.t().contiguous()
     D = torch.empty(M, N, device="cuda")
-    _lib.call("s24_gemm", P(As), a_mn, As.stride(0), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1,
+    _lib.call("s24_gemm", P(As), a_mn, As.stride(0), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, None,
               S())
     ref = A.float() @ B.float()
     assert rel_err(D, ref) < 1e-5
@@ -75,12 +75,12 @@ def test_dense_gemm_bf16_out_rowmap_transposed():
     B = torch.randn(K, N, device="cuda").bfloat16()
     rmap = torch.randperm(M, device="cuda").int()
     D = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-    _lib.call("s24_gemm", P(A), 0, K, P(B), 1, N, M, N, K, P(D), BF16, N, P(rmap), 0, -1, S())
+    _lib.call("s24_gemm", P(A), 0, K, P(B), 1, N, M, N, K, P(D), BF16, N, P(rmap), 0, -1, None, S())
     ref = torch.empty(M, N, device="cuda")
     ref[rmap.long()] = A.float() @ B.float()
     assert rel_err(D.float(), ref) < 4e-3
     Dt = torch.zeros(N, M, device="cuda")
-    _lib.call("s24_gemm", P(A), 0, K, P(B), 1, N, M, N, K, P(Dt), F32, M, P(rmap), 1, -1, S())
+    _lib.call("s24_gemm", P(A), 0, K, P(B), 1, N, M, N, K, P(Dt), F32, M, P(rmap), 1, -1, None, S())
     assert rel_err(Dt.t(), ref) < 1e-5
 
 
@@ -111,7 +111,7 @@ def test_spmm_vs_decompressed(b_mn, M, N, K):
     B = torch.randn(K, N, device="cuda").bfloat16()
     Bs = B if b_mn else B.t().contiguous()
     D = torch.empty(M, N, device="cuda")
-    _lib.call("s24_spmm", P(vals), P(meta_hw), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, S())
+    _lib.call("s24_spmm", P(vals), P(meta_hw), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, None, S())
     ref = dense @ B.float()
     assert rel_err(D, ref) < 1e-5
 
@@ -189,7 +189,7 @@ def _k1(x, w1, with_counts=True):
     stats = torch.zeros(2, dtype=torch.int64, device="cuda")
     y = torch.empty(M, N, device="cuda")
     _lib.call("s24_fwd_gemm1_fused", P(x), K, P(w1), N, M, N, K, P(vals), P(meta), P(counts) if with_counts else None,
-              P(stats), P(y), S())
+              P(stats), P(y), None, None, None, 0, S())
     return vals, meta, counts, stats, y
 
 
@@ -216,7 +216,7 @@ def test_bwd_dact_fused(M, N, K):
     tx, tw1, tw2, tg = (torch.from_numpy(t).cuda().bfloat16() for t in (x, w1, w2, dy))
     vals, meta, _, _, y = _k1(tx, tw1, with_counts=False)
     gv = torch.zeros_like(vals)
-    _lib.call("s24_bwd_dact_fused", P(tg), K, P(tw2), K, M, N, K, P(vals), P(meta), P(gv), S())
+    _lib.call("s24_bwd_dact_fused", P(tg), K, P(tw2), K, M, N, K, P(vals), P(meta), P(gv), None, None, None, 0, S())
     G = tg.float() @ tw2.float().t()  # [M, N]
     mref = meta_hw_to_ref(meta, M, N).long()  # [M, N/4, 2]
     Gk = torch.gather(G.view(M, N // 4, 4), 2, mref)  # [M, N/4, 2]
