@@ -151,6 +151,9 @@ class KernelTracer:
             return "tensor", 2.0 * a[6] * a[7] * a[8], f"gemm dense M={a[6]} N={a[7]} K={a[8]}"
         if name == "s24_spmm":
             return "tensor_sparse", 2.0 * a[5] * a[6] * a[7], f"spmm 2:4 M={a[5]} N={a[6]} K={a[7]}"
+        if name == "s24_spmm_bg":
+            return ("tensor_sparse", 2.0 * a[5] * a[6] * a[7],
+                    f"spmm 2:4 M={a[5]} N={a[6]} K={a[7]} + K4 split in background warps")
         if name in ("s24_fwd_gemm1_fused",):
             return "tensor", 2.0 * a[4] * a[5] * a[6], "K1 gemm+relu2+2:4 (fwd.pre_act)"
         if name in ("s24_bwd_dact_fused",):

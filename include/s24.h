@@ -159,6 +159,16 @@ int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
              int64_t d_rows_valid, const int* d_row_valid, void* stream);
 
+/* s24_spmm plus a feature-wise split (the K4 job of s24_feature_split with
+ * stats == NULL) run as background work by the GEMM's epilogue warps while
+ * they wait for accumulators: the tensor-bound sparse GEMM hides the
+ * ALU-bound split. k4_counter: one device int of workspace (reset here). */
+int s24_spmm_bg(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
+                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
+                int64_t d_rows_valid, const int* d_row_valid, const void* k4_vals, const uint8_t* k4_meta,
+                int64_t k4_n, int64_t k4_h, const int* k4_feat_pos, int64_t k4_n_sparse, int64_t k4_n_dense,
+                void* k4_vs, uint8_t* k4_es, void* k4_vd, int* k4_counter, void* stream);
+
 /* K1: Y1 = X_in . W1 with the fused relu^2 + token-wise 2:4 epilogue
  * (ffn.py:305-329). x: [M, K] row-major; w1: [K, N] row-major (N = h,
  * N % 128 == 0). Outputs act_vals bf16 [M_pad128, N/2], act_meta hw, counts

@@ -38,6 +38,8 @@ SIGNATURES: dict[str, list] = {
     "s24_gemm": [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],
     "s24_gemm_splitk": [P, INT, I64, P, INT, I64, I64, I64, I64, INT, P, P, INT, I64, P, INT, P],
     "s24_spmm": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],
+    "s24_spmm_bg": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P, P, I64, I64, P, I64, I64, P, P, P,
+                    P, P],
     "s24_fwd_gemm1_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, P, P, I64, P],
     "s24_bwd_dact_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, I64, P],
     "s24_gemm_relu2": [P, I64, P, I64, I64, I64, I64, P, I64, P],

@@ -29,6 +29,7 @@
 //   MN-major : boxes of 64 (M or N) elements x BK rows of K, box stride BK*128 B
 // Descriptors: K-major SBO = 1024; MN-major LBO = box stride, SBO = 1024.
 #pragma once
+#include "k4.cuh"
 #include "meta.cuh"
 #include "ptx.cuh"
 
@@ -39,6 +40,8 @@ struct GemmShape {
   int tiles_m, tiles_n; // in units of (128*CG) x BN
   int group_m;          // raster: group_m M-tiles share one sweep over N
   int k_splits;         // >1: split-K, work unit = (tile, K range); partials go to the epilogue with ks
+  int has_bg;           // 1: epilogue warps run K4 units (bg) while waiting for accumulators
+  K4Job bg;
 };
 
 template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8>
@@ -79,6 +82,9 @@ struct GemmCfg {
   static constexpr int THREADS = 128 + EPI_THREADS;
   static constexpr int CPW = NCHUNK / (EPI_WARPS / 4);  // chunks per epilogue warp
   static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
+  // 4-epilogue-warp configs cap registers at 128/thread so that an
+  // independent kernel (e.g. K4 on a side stream) can co-reside on the SM
+  static constexpr int MIN_BLOCKS = EPI_WARPS == 4 ? 2 : 1;
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, int& nb) {
@@ -108,7 +114,7 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 // the split-K index of the work unit), and
 // Epi::finish(ep, st, lane) once at the end.
 template <class Cfg, class Epi>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const GemmShape shape, const typename Epi::Params ep) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], CG * Cfg::EPI_THREADS);
+      mbar_init(&tempty_bar[a], CG * (Cfg::OVERLAP ? 128 : Cfg::EPI_THREADS));
     }
     fence_barrier_init();
   }
@@ -303,6 +309,20 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     const bool owns_last = c_begin + Cfg::CPW == Cfg::NCHUNK;
     typename Epi::State st;
     Epi::init(ep, st);
+    // optional background job: K4 warp units taken from a global queue while
+    // this warp would otherwise sit waiting for an accumulator
+    bool bg_more = shape.has_bg != 0;
+    const uint2* bg_lut = bg_more ? k4_lut_init() : nullptr;
+    auto bg_unit = [&]() -> bool {
+      int u = 0;
+      if (lane == 0) u = atomicAdd(shape.bg.counter, 1);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= shape.bg.units) return false;
+      int t0, fb;
+      k4_unit_coords(shape.bg.a, u, t0, fb);
+      k4_warp_unit<false>(shape.bg.a, t0, fb, static_cast<int>(lane), bg_lut);
+      return true;
+    };
     int iter = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++iter) {
       int mb, nb;
@@ -312,14 +332,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const bool row_ok = row < shape.M;
       Epi::prefetch(ep, st, row, row_ok, nb * Cfg::BN + c_begin * 32, t / mn_tiles);
       uint64_t* tempty = &tempty_bar[Cfg::OVERLAP ? 0 : slot];
-      if constexpr (Cfg::OVERLAP)
-        mbar_wait(&tfull_bar[0], iter & 1);
-      else
-        mbar_wait(&tfull_bar[slot], (iter >> 1) & 1);
+      // overlapping slots: the chunk shared with the other slot (last chunk of
+      // slot 0, first of slot 1) gates the next tile's MMAs. Only the part that
+      // owns it releases the accumulator (right after draining it). Ownership
+      // alternates with the slot, so the owner of tile t+1 is the other part of
+      // tile t: its release of t+1 also certifies it finished reading tile t,
+      // whose slot the MMAs of tile t+2 overwrite.
+      const bool owner = Cfg::OVERLAP && (slot == 0 ? owns_last : c_begin == 0);
+      uint64_t* tfull = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
+      const uint32_t tparity = Cfg::OVERLAP ? (iter & 1) : ((iter >> 1) & 1);
+      if (bg_more && !owner) {
+        while (!mbar_test(tfull, tparity)) {
+          if (!bg_unit()) {
+            bg_more = false;
+            break;
+          }
+        }
+      }
+      mbar_wait(tfull, tparity);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * Cfg::SLOT1_COL;
-      // overlapping slots: the chunk shared with the other slot (last chunk of
-      // slot 0) is drained first so the next tile's MMAs can start at once
       const bool rotate = Cfg::OVERLAP && slot == 0 && owns_last;
       // epilogues with per-chunk register state (Epi::kUnroll) get a fully
       // unrolled loop so that state is indexed statically
@@ -332,7 +364,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           tmem_ld32(t_row + c * 32, r);
           tmem_ld_wait();
         }
-        if (Cfg::OVERLAP && ci == 0) {
+        if (owner && ci == 0) {
           tc_fence_before();
           if (leader)
             mbar_arrive(tempty);
@@ -353,6 +385,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         else
           mbar_arrive_remote(tempty, 0);
       }
+    }
+    // drain what is left of the background queue
+    while (bg_more && bg_unit()) {
     }
     Epi::finish(ep, st, lane);
   }

@@ -70,7 +70,8 @@ int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
 // ---------------------------------------------------------------------------
 template <class Cfg, class Epi>
 static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1) {
+                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1,
+                       const K4Job* bg = nullptr) {
   if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
   CUtensorMap ma, mb;
@@ -110,6 +111,11 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
   sh.group_m = 16 / Cfg::CG;
   sh.k_splits = k_splits < 1 ? 1 : k_splits;
+  sh.has_bg = bg != nullptr;
+  if (bg)
+    sh.bg = *bg;
+  else
+    std::memset(&sh.bg, 0, sizeof(sh.bg));
   const int tiles = sh.tiles_m * sh.tiles_n * sh.k_splits;
   const int max_clusters = num_sms() / Cfg::CG;
   const int clusters = tiles < max_clusters ? tiles : max_clusters;
@@ -144,8 +150,10 @@ using DenseKN = GemmCfg<false, false, true, 256, 6, 2>;   // A K-major, B MN-maj
 using DenseKK = GemmCfg<false, false, false, 256, 6, 2>;  // A K-major, B K-major
 using DenseMM = GemmCfg<false, true, true, 256, 6, 2>;    // A MN-major, B MN-major
 using DenseMK = GemmCfg<false, true, false, 256, 6, 2>;   // A MN-major, B K-major
-using SparseN = GemmCfg<true, false, true, 256, 4, 2>;    // sparse A, B MN-major
-using SparseK = GemmCfg<true, false, false, 256, 4, 2>;   // sparse A, B K-major
+// sparse: light epilogue, 4 epilogue warps and <= 128 registers/thread, leaving
+// room for a co-resident side-stream kernel (the feature-wise split K4)
+using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4>;  // sparse A, B MN-major
+using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4>; // sparse A, B K-major
 
 template <class Epi>
 static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
@@ -178,9 +186,10 @@ __global__ void k_splitk_reduce(const float* __restrict__ ws, int k_splits, long
 
 template <class Epi>
 static int dispatch_sparse(int b_mn, const void* A, const uint8_t* meta, const void* B, int64_t ldb, int64_t M,
-                           int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st) {
-  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st);
-  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st);
+                           int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st,
+                           const K4Job* bg = nullptr) {
+  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg);
+  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg);
 }
 
 static int check_common(int64_t M, int64_t N, int64_t K, int64_t lda, int a_mn, int64_t ldb, int b_mn) {
@@ -264,6 +273,31 @@ int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_
                                        static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
     return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep,
                                            static_cast<cudaStream_t>(stream));
+  });
+}
+
+int s24_spmm_bg(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
+                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
+                int64_t d_rows_valid, const int* d_row_valid, const void* k4_vals, const uint8_t* k4_meta,
+                int64_t k4_n, int64_t k4_h, const int* k4_feat_pos, int64_t k4_n_sparse, int64_t k4_n_dense,
+                void* k4_vs, uint8_t* k4_es, void* k4_vd, int* k4_counter, void* stream) {
+  int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
+  if (rc) return rc;
+  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
+  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  auto st = static_cast<cudaStream_t>(stream);
+  K4Job job;
+  rc = k4_prepare(k4_vals, k4_meta, k4_n, k4_h, k4_feat_pos, k4_n_sparse, k4_n_dense, k4_vs, k4_es, k4_vd, st, &job.a);
+  if (rc) return rc;
+  if (!k4_counter) return fail(S24_ERR_DIMENSION, "background split needs a counter");
+  cudaMemsetAsync(k4_counter, 0, sizeof(int), st);
+  job.counter = k4_counter;
+  job.units = static_cast<int>((k4_n / 128) * (k4_h / 16));
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
+                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
+    return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep, st, &job);
   });
 }
 

@@ -9,6 +9,7 @@
 #include "host_util.h"
 #include "meta.cuh"
 #include "ptx.cuh"
+#include "k4.cuh"
 
 namespace s24 {
 
@@ -382,155 +383,12 @@ __global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts, i
 }
 
 // ---------------------------------------------------------------------------
-// K4: feature-wise transposed split of a token-wise compressed [n, h] matrix.
-// CTA tile: 128 tokens x 128 features, 8 warps; warp w owns 16 features (one
-// 16-column metadata halfword per token), lane l owns the token group
-// 4l..4l+3. Everything stays in registers:
-//   1. each lane loads its 4 tokens' compressed 16-feature slices (16 B each)
-//      and metadata halfwords, and expands them with byte permutes into packed
-//      bf16 pairs X[token][feature pair];
-//   2. the feature-wise top-2 over the 4 tokens runs two features at a time in
-//      the 16-bit halves of 32-bit registers, on integer keys (|x| order of
-//      bf16 == unsigned order of its low 15 bits; NaN ranked last);
-//   3. sparse features emit (v0, v1) packed + a nibble (coalesced 128 B per
-//      warp per feature, halfwords assembled with 2 shuffles); dense features
-//      emit their 4 token values (coalesced 256 B per warp per feature).
-__constant__ unsigned long long kKeepToNibble = 0x000E0DC009804000ull;  // keep bits -> i0 | i1 << 2
-
-// bf16x2 magnitude keys, NaN mapped below zero (-1.0); ordered with native
-// bf16 compares (HSET2), which keeps the selection at one instruction per pair
-__device__ __forceinline__ uint32_t k4_key2(uint32_t x) {
-  const uint32_t mag = x & 0x7FFF7FFFu;
-  const __nv_bfloat162 m = *reinterpret_cast<const __nv_bfloat162*>(&mag);
-  const uint32_t nan = __hne2_mask(m, m);
-  return (mag & ~nan) | (0xBF80BF80u & nan);
-}
-
-__device__ __forceinline__ uint32_t k4_ge(uint32_t a, uint32_t b) {
-  return __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&a), *reinterpret_cast<const __nv_bfloat162*>(&b));
-}
-
-__device__ __forceinline__ uint32_t k4_nz(uint32_t x) {  // 1 per nonzero half, packed
-  const uint32_t mag = x & 0x7FFF7FFFu;
-  const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
-  return __hne2_mask(*reinterpret_cast<const __nv_bfloat162*>(&mag), z) & 0x00010001u;
-}
-
-__device__ __forceinline__ uint32_t k4_sel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
-
-// majority of three bitwise masks
-__device__ __forceinline__ uint32_t k4_maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
-
+// K4 standalone grid: CTA = 128 tokens x 128 features = 8 warp units.
 template <bool WITH_STATS>
-__global__ void __launch_bounds__(256) k_feature_split(const __nv_bfloat16* __restrict__ vals,
-                                                       const uint8_t* __restrict__ meta_hw, int n, int h,
-                                                       const int* __restrict__ feat_pos,
-                                                       __nv_bfloat16* __restrict__ vs, uint8_t* __restrict__ es,
-                                                       __nv_bfloat16* __restrict__ vd,
-                                                       unsigned long long* stats) {
-  // nibble -> PRMT selectors expanding (lo, hi) of a kept pair into 4 halfwords
-  __shared__ uint2 sel_lut[16];
-  if (threadIdx.x < 16) {
-    const uint32_t nib = threadIdx.x, i0 = nib & 3u, i1 = nib >> 2;
-    uint32_t sel[4];
-#pragma unroll
-    for (uint32_t q = 0; q < 4; ++q) sel[q] = (q == i0) ? 0x10u : (q == i1) ? 0x32u : 0x44u;
-    sel_lut[threadIdx.x] = make_uint2(sel[0] | (sel[1] << 8), sel[2] | (sel[3] << 8));
-  }
-  __syncthreads();
+__global__ void __launch_bounds__(256) k_feature_split(K4Args a) {
+  const uint2* lut = k4_lut_init();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int fbase = blockIdx.x * 128 + warp * 16;
-  const int t0 = blockIdx.y * 128;
-  const int t = t0 + 4 * lane;
-  // per-feature output bases, computed once by lanes 0..15 (feature fbase+lane)
-  // and broadcast with shuffles:
-  //   sparse (pos >= 0): ofs = word offset of the feature's vs row at token t0,
-  //                      mb  = byte offset of its metadata halfword for q = 0
-  //   dense  (pos <  0): ofs = 0x80000000 | uint2 offset of its vd row at t0
-  const int my_pos = lane < 16 ? feat_pos[fbase + lane] : 0;
-  if (vs == nullptr && !__any_sync(0xffffffffu, lane < 16 && my_pos < 0)) return;  // dense-only: no dense here
-  uint32_t my_ofs = 0, my_mb = 0;
-  if (my_pos >= 0) {
-    my_ofs = static_cast<uint32_t>(my_pos) * static_cast<uint32_t>(n / 4) + static_cast<uint32_t>(t0 / 4);
-    my_mb = static_cast<uint32_t>(meta_hw_halfword_offset(my_pos, t0 / 16, n));
-  } else {
-    my_ofs = 0x80000000u | (static_cast<uint32_t>(-my_pos - 1) * static_cast<uint32_t>(n / 4) +
-                            static_cast<uint32_t>(t0 / 4));
-  }
-  // this lane's in-atom offset of column chunk q = lane/4 (q = 0 is folded into my_mb)
-  const uint32_t qd = static_cast<uint32_t>(lane) >> 2;
-  const uint32_t q_off = 4u * (qd >> 1) + 128u * (qd & 1u);
-
-  // 1. load + expand: X[r][k] = bf16 pair of features (2k, 2k+1) for token t+r
-  uint32_t X[4][8];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const uint4 v = *reinterpret_cast<const uint4*>(vals + static_cast<long long>(t + r) * (h / 2) + fbase / 2);
-    const uint32_t m16 = *reinterpret_cast<const uint16_t*>(meta_hw + meta_hw_halfword_offset(t + r, fbase / 16, h));
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const uint2 sl = sel_lut[(m16 >> (4 * g)) & 0xFu];
-      X[r][2 * g] = __byte_perm(w[g], 0u, sl.x);
-      X[r][2 * g + 1] = __byte_perm(w[g], 0u, sl.y);
-    }
-  }
-  const unsigned long long lut = kKeepToNibble;
-  uint32_t* vs32 = reinterpret_cast<uint32_t*>(vs);
-  uint2* vd64 = reinterpret_cast<uint2*>(vd);
-  uint32_t cnt_b = 0, cnt_a = 0;  // per-half nonzero counters (sparse features only)
-
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t x0 = X[0][k], x1 = X[1][k], x2 = X[2][k], x3 = X[3][k];
-    const uint32_t ofs0 = __shfl_sync(0xffffffffu, my_ofs, 2 * k), ofs1 = __shfl_sync(0xffffffffu, my_ofs, 2 * k + 1);
-    const bool sp0 = !(ofs0 & 0x80000000u), sp1 = !(ofs1 & 0x80000000u);
-    if (vs != nullptr && (sp0 || sp1)) {
-      const uint32_t k0 = k4_key2(x0), k1 = k4_key2(x1), k2 = k4_key2(x2), k3 = k4_key2(x3);
-      // token i beats token j (i < j) iff key_i >= key_j: ties go to the lower token
-      const uint32_t b01 = k4_ge(k0, k1), b02 = k4_ge(k0, k2), b03 = k4_ge(k0, k3);
-      const uint32_t b12 = k4_ge(k1, k2), b13 = k4_ge(k1, k3), b23 = k4_ge(k2, k3);
-      // kept <=> beats at least two of the other three
-      const uint32_t K0 = k4_maj(b01, b02, b03), K1 = k4_maj(~b01, b12, b13);
-      const uint32_t K2 = k4_maj(~b02, ~b12, b23), K3 = k4_maj(~b03, ~b13, ~b23);
-      const uint32_t v0 = k4_sel(K0, x0, k4_sel(K1, x1, x2));  // first kept token
-      const uint32_t v1 = k4_sel(K3, x3, k4_sel(K2, x2, x1));  // second kept token
-      const uint32_t kb = (K0 & 0x00010001u) | (K1 & 0x00020002u) | (K2 & 0x00040004u) | (K3 & 0x00080008u);
-      // metadata halfwords of both features at once: 4 lanes (token groups) x 4 bits
-      uint32_t hw = ((static_cast<uint32_t>(lut >> (4 * (kb & 0xFu))) & 0xFu) |
-                     ((static_cast<uint32_t>(lut >> (4 * ((kb >> 16) & 0xFu))) & 0xFu) << 16))
-                    << (4 * (lane & 3));
-      hw |= __shfl_xor_sync(0xffffffffu, hw, 1);
-      hw |= __shfl_xor_sync(0xffffffffu, hw, 2);
-      const uint32_t mb0 = __shfl_sync(0xffffffffu, my_mb, 2 * k), mb1 = __shfl_sync(0xffffffffu, my_mb, 2 * k + 1);
-      if constexpr (WITH_STATS) {
-        const uint32_t nzb = k4_nz(x0) + k4_nz(x1) + k4_nz(x2) + k4_nz(x3);
-        const uint32_t nza = k4_nz(v0) + k4_nz(v1);
-        if (sp0) {
-          cnt_b += nzb & 0xFFFFu;
-          cnt_a += nza & 0xFFFFu;
-        }
-        if (sp1) {
-          cnt_b += nzb >> 16;
-          cnt_a += nza >> 16;
-        }
-      }
-      if (sp0) {
-        vs32[ofs0 + lane] = __byte_perm(v0, v1, 0x5410);
-        if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + mb0 + q_off) = static_cast<uint16_t>(hw);
-      }
-      if (sp1) {
-        vs32[ofs1 + lane] = __byte_perm(v0, v1, 0x7632);
-        if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + mb1 + q_off) = static_cast<uint16_t>(hw >> 16);
-      }
-    }
-    if (!sp0) vd64[(ofs0 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x5410), __byte_perm(x2, x3, 0x5410));
-    if (!sp1) vd64[(ofs1 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x7632), __byte_perm(x2, x3, 0x7632));
-  }
-  if constexpr (WITH_STATS) {
-    block_sum_u64_to(cnt_b, stats);
-    block_sum_u64_to(cnt_a, stats + 1);
-  }
+  k4_warp_unit<WITH_STATS>(a, blockIdx.y * 128, blockIdx.x * 128 + warp * 16, lane, lut);
 }
 
 static int grid_for(long long work, int block) {
@@ -539,6 +397,26 @@ static int grid_for(long long work, int block) {
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return static_cast<int>(g);
+}
+
+// validates a K4 job and writes the padding rows of its outputs (zero values,
+// valid (0,1) selectors); shared by the standalone grid and the GEMM
+// background mode
+int k4_prepare(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
+               int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd, cudaStream_t st, K4Args* out) {
+  if (n % 128 != 0 || h % 128 != 0) return fail(S24_ERR_DIMENSION, "feature split needs n, h multiples of 128");
+  if (n_sparse + n_dense != h) return fail(S24_ERR_STATE, "plan sizes do not add up to h");
+  if ((vs == nullptr) != (es == nullptr)) return fail(S24_ERR_DIMENSION, "vs and es go together");
+  const int64_t sp_pad = (n_sparse + 127) / 128 * 128, d_pad = (n_dense + 127) / 128 * 128;
+  if (vs != nullptr && sp_pad > n_sparse) {
+    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vs) + n_sparse * (n / 2), 0, (sp_pad - n_sparse) * (n / 2) * 2, st);
+    cudaMemsetAsync(es + (n_sparse / 128) * (n / 128) * 2048, 0x44, (n / 128) * 2048, st);
+  }
+  if (d_pad > n_dense && vd)
+    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vd) + n_dense * n, 0, (d_pad - n_dense) * n * 2, st);
+  *out = K4Args{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
+                static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd), nullptr};
+  return S24_OK;
 }
 
 }  // namespace s24
@@ -716,28 +594,17 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
                       unsigned long long* stats, void* stream) {
-  if (n % 128 != 0 || h % 128 != 0) return fail(S24_ERR_DIMENSION, "feature split needs n, h multiples of 128");
-  if (n_sparse + n_dense != h) return fail(S24_ERR_STATE, "plan sizes do not add up to h");
-  if (n == 0 || h == 0) return S24_OK;
   auto st = static_cast<cudaStream_t>(stream);
-  const int64_t sp_pad = (n_sparse + 127) / 128 * 128, d_pad = (n_dense + 127) / 128 * 128;
-  // padding rows: zero values, valid metadata (i0=0, i1=1 -> nibble 0x4)
-  if (vs != nullptr && sp_pad > n_sparse) {
-    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vs) + n_sparse * (n / 2), 0, (sp_pad - n_sparse) * (n / 2) * 2, st);
-    cudaMemsetAsync(es + (n_sparse / 128) * (n / 128) * 2048, 0x44, (n / 128) * 2048, st);
-  }
-  if (d_pad > n_dense && vd)
-    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vd) + n_dense * n, 0, (d_pad - n_dense) * n * 2, st);
+  K4Args a;
+  int rc = k4_prepare(vals, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs, es, vd, st, &a);
+  if (rc) return rc;
+  if (n == 0 || h == 0) return S24_OK;
+  a.stats = stats;
   dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
   if (stats)
-    k_feature_split<true><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n),
-                                                static_cast<int>(h), feat_pos, static_cast<__nv_bfloat16*>(vs), es,
-                                                static_cast<__nv_bfloat16*>(vd), stats);
+    k_feature_split<true><<<grid, 256, 0, st>>>(a);
   else
-    k_feature_split<false><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(vals), meta_hw,
-                                                 static_cast<int>(n), static_cast<int>(h), feat_pos,
-                                                 static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd),
-                                                 nullptr);
+    k_feature_split<false><<<grid, 256, 0, st>>>(a);
   return check_launch("k_feature_split");
 }
 

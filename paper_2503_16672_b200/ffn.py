@@ -39,7 +39,12 @@ from .sparse24 import (
     sp_gemm_macs,
 )
 from .splitgemm import (
+    FeatureSplit,
     FusedFeatureOperand,
+    alloc_feature_split,
+    k4_job_args,
+    run_feature_split,
+    side_stream,
     SplitPlan,
     feature_split,
     fused_weight_grad,
@@ -56,6 +61,14 @@ ACTIVATIONS = ("squared_relu", "swiglu")
 # Both are bit-identical; on B200 the fused variant currently makes the K1/K3
 # epilogues the bottleneck, so it is opt-in.
 FUSED_FEATURE_SPLIT = os.environ.get("S24_FUSED_FW", "0") == "1"
+
+# How the standalone K4 runs next to the sparse GEMM that precedes its use
+# (fwd.out for the activation split, bwd.d_x for the g_pre split):
+#   "side"       -- on a side stream, co-resident with the GEMM (the sparse
+#                   GEMMs cap their registers to leave room for it)  [default]
+#   "background" -- inside the GEMM, in its idle epilogue warps (s24_spmm_bg)
+#   "inline"     -- serialized on the main stream
+K4_MODE = os.environ.get("S24_K4_MODE", "side")
 FORWARD_MODES = ("dense", "sparse24")
 BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
 
@@ -174,6 +187,8 @@ class FfnCache:
     config: FfnConfig
     gate: torch.Tensor | None = None
     act_fw: FusedFeatureOperand | None = None  # feature-wise 2:4 act of all features (from K1)
+    act_split: FeatureSplit | None = None  # feature-wise split of act (K4, run during fwd.out)
+    act_split_ready: object = None  # CUDA event after which act_split is complete (side-stream K4)
 
     @property
     def act_sparse(self) -> Sparse24Matrix | None:
@@ -229,10 +244,12 @@ def _check_dims(n: int, d: int, h: int) -> None:
         raise DimensionError(f"hidden width {h} must be a multiple of 128 on the device path")
 
 
-def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, keep_pre_act: bool = False):
+def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, keep_pre_act: bool = False,
+                for_backward: bool = True):
     """Run the forward pass; returns (out [n, d] bf16, FfnCache) (ref ffn.py:276-363).
     keep_pre_act=True also stores the fp32 pre-activation in the cache (parity
-    tests use it to replay the selection on identical inputs)."""
+    tests use it to replay the selection on identical inputs). for_backward=False
+    (inference prefill) skips the feature-wise split the backward would need."""
     require_cuda()
     _unsupported(cfg)
     x = as_matrix(x, "x", BF16)
@@ -297,12 +314,52 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
         plan_out = plan if plan is not None else partition_features(counts, cfg.split_ratio)
 
-    _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-              ptr(inv_dev), 0, -1, None, s)
+    # fwd.out on tensor cores; when the backward will need the feature-wise
+    # split of act (and the plan is known), K4 runs as background work in the
+    # GEMM's idle epilogue warps
+    act_split = None
+    bg_plan = plan_out if cfg.backward_mode == "split_masked" else (
+        _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else None)
+    split_ready = None
+    if for_backward and bg_plan is not None and act_fw is None:
+        act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan)
+        if K4_MODE == "background":
+            counter = torch.empty(1, dtype=torch.int32, device=dev)
+            _lib.call("s24_spmm_bg", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16,
+                      d, ptr(inv_dev), 0, -1, None,
+                      *k4_job_args(act_vals, act_meta, npad, h, bg_plan, act_split, counter), s)
+        else:
+            split_ready = _spmm_with_split(
+                lambda st: _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out),
+                                     _lib.BF16, d, ptr(inv_dev), 0, -1, None, st),
+                act_split, act_vals, act_meta, npad, h, bg_plan)
+    else:
+        _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
+                  ptr(inv_dev), 0, -1, None, s)
     census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
     cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
-                     SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw)
+                     SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw, act_split=act_split,
+                     act_split_ready=split_ready)
     return out, cache
+
+
+def _spmm_with_split(launch_gemm, fs, vals, meta, n, h, plan):
+    """Launch a sparse GEMM on the current stream and the K4 job filling `fs`
+    next to it (K4_MODE "side": side stream, co-resident; "inline": after it).
+    Returns the CUDA event after which `fs` is complete (None if inline)."""
+    main = torch.cuda.current_stream()
+    if K4_MODE != "side":
+        launch_gemm(main.cuda_stream)
+        run_feature_split(fs, vals, meta, n, h, plan)
+        return None
+    side = side_stream(vals.device)
+    side.wait_stream(main)  # K4's inputs are ready; it must not wait for the GEMM
+    launch_gemm(main.cuda_stream)
+    with torch.cuda.stream(side):
+        run_feature_split(fs, vals, meta, n, h, plan)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    return ev
 
 
 def _all_sparse_plan(h: int, dev) -> SplitPlan:
@@ -391,6 +448,28 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         g_pre_dense = (G * act_squared_relu_grad(cache.pre_act)).to(BF16)
 
     mode = cfg.backward_mode
+    ev_dx = None
+    if mode != "dense":
+        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache.plan
+        macs_w = sp_gemm_macs(n, h, d) if mode == "naive_sparse" else split_gemm_macs(n, d, plan)
+    fg = None
+    fg_ready = None
+    if cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None and not raw_naive:
+        # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
+        # as background work in its idle epilogue warps
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan)
+        if K4_MODE == "background":
+            counter = torch.empty(1, dtype=torch.int32, device=dev)
+            _lib.call("s24_spmm_bg", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x),
+                      _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None,
+                      *k4_job_args(g_vals, cache.act_meta, npad, h, plan, fg, counter), s)
+        else:
+            fg_ready = _spmm_with_split(
+                lambda st: _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h,
+                                     ptr(d_x), _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None, st),
+                fg, g_vals, cache.act_meta, npad, h, plan)
+        ev_dx = GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d))
+
     if mode == "dense":
         act = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_decompress_token", ptr(cache.act_vals), None, ptr(cache.act_meta), n, h, ptr(act), _lib.BF16, h, s)
@@ -406,21 +485,20 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
     else:
-        if mode == "naive_sparse":
-            plan = _all_sparse_plan(h, dev)
-            macs_w2 = macs_w1 = sp_gemm_macs(n, h, d)
-        else:
-            plan = cache.plan
-            macs_w2 = macs_w1 = split_gemm_macs(n, d, plan)
         # dW2 = split(act)^T g_c  (act is already restricted to the mask)
         if cache.act_fw is not None:
             fused_weight_grad(cache.act_fw, cache.act_vals, cache.act_meta, h, plan, g_c, d_w2, transposed=False)
             stats_a = cache.act_fw.stats(plan)
         else:
-            fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
+            if cache.act_split is not None:
+                fa = cache.act_split
+                if cache.act_split_ready is not None:
+                    torch.cuda.current_stream().wait_event(cache.act_split_ready)
+            else:
+                fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
             split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
             stats_a = fa.stats
-        census.append(GemmEvent("bwd.d_w2", True, macs_w2))
+        census.append(GemmEvent("bwd.d_w2", True, macs_w))
         notify("d_w2", d_w2)
         # dW1 = (split(g_pre)^T x_in)^T. The split path always sees the masked
         # g_pre (ref splitgemm.py:72, even with mask_grad_with_fwd off);
@@ -437,13 +515,18 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
             fused_weight_grad(g_fw, g_vals, cache.act_meta, h, plan, cache.x_in, d_w1, transposed=True)
             stats_g = g_fw.stats(plan)
         else:
-            fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+            if fg is None:
+                fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+            elif fg_ready is not None:
+                torch.cuda.current_stream().wait_event(fg_ready)
             split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
             stats_g = fg.stats
-        census.append(GemmEvent("bwd.d_w1", True, macs_w1))
+        census.append(GemmEvent("bwd.d_w1", True, macs_w))
         notify("d_w1", d_w1)
 
-    if cfg.mask_grad_with_fwd:
+    if ev_dx is not None:
+        census.append(ev_dx)
+    elif cfg.mask_grad_with_fwd:
         _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
                   ptr(cache.inv_dev), 0, -1, None, s)
         census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))

@@ -114,6 +114,22 @@ def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, pla
     splitgemm.py:72-80, without a dense round trip). dense_only=True produces
     only the dense columns (the FFN hot path gets the sparse operand from the
     K1/K3 epilogues)."""
+    fs = alloc_feature_split(vals, meta_hw, n, h, plan, dense_only)
+    ns, nd = plan.n_sparse, plan.n_dense
+    cnt = torch.zeros(2, dtype=torch.int64, device=vals.device) if with_stats else None
+    _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(fs.vs),
+              ptr(fs.es), ptr(fs.vd), ptr(cnt), stream())
+    if with_stats:
+        fs.stats = SparsifyStats(n * ns, cnt)
+    return fs
+
+
+def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
+                        dense_only: bool = False) -> FeatureSplit:
+    """Output buffers of one K4 job (filled by s24_feature_split or by a GEMM's
+    background warps via s24_spmm_bg). Its drop statistics are not counted on
+    the hot path -- the reference discards them (splitgemm.py:75) -- and are
+    recounted on the device only if someone reads them."""
     dev = vals.device
     ns, nd = plan.n_sparse, plan.n_dense
     vs = es = None
@@ -121,16 +137,27 @@ def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, pla
         vs = torch.empty(max(pad128(ns), 128), n // 2, dtype=BF16, device=dev)
         es = torch.empty(_lib.meta_hw_bytes(max(ns, 1), n), dtype=torch.uint8, device=dev)
     vd = torch.empty(max(pad128(nd), 128), n, dtype=BF16, device=dev)
-    cnt = torch.zeros(2, dtype=torch.int64, device=dev) if with_stats else None
-    _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(vs), ptr(es),
-              ptr(vd), ptr(cnt), stream())
-    if with_stats:
-        stats = SparsifyStats(n * ns, cnt)
-    else:
-        # the reference discards these drop counts (splitgemm.py:75); they are
-        # recounted on the device only if someone reads them
-        stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
+    stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
     return FeatureSplit(vs, es, vd, stats)
+
+
+def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int,
+                      plan: SplitPlan) -> None:
+    """Fill preallocated K4 outputs on the current stream (no drop counting)."""
+    _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense,
+              ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, stream())
+
+
+def side_stream(device) -> torch.cuda.Stream:
+    return _side_stream(device)
+
+
+def k4_job_args(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan, fs: FeatureSplit,
+                counter: torch.Tensor) -> tuple:
+    """The K4 argument tail of s24_spmm_bg (feature split run as background work
+    of a sparse GEMM)."""
+    return (ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense, ptr(fs.vs), ptr(fs.es),
+            ptr(fs.vd), ptr(counter))
 
 
 @dataclass
