@@ -125,10 +125,13 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
  *   stats uint64[2] += (nonzeros before, after) over the sparse features.
  * Requires n % 128 == 0 and h % 128 == 0. Padding rows of vs/es/vd are
  * written (zeros / valid metadata). With vs == es == NULL only the dense
- * features are produced (the sparse ones come from the fused epilogues). */
+ * features are produced (the sparse ones come from the fused epilogues).
+ * operand_nonneg = 1 declares the values >= 0 and NaN-free (the relu^2
+ * activation): the feature-wise top-2 then ranks raw values (same result,
+ * fewer instructions); 0 ranks magnitudes with NaN last (any operand). */
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
-                      unsigned long long* stats, void* stream);
+                      unsigned long long* stats, int operand_nonneg, void* stream);
 
 /* ---------------------------------------------------------------- GEMMs
  * Operand conventions: A is logically [M, K], B is logically [K, N].
@@ -159,6 +162,17 @@ int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
              int64_t d_rows_valid, const int* d_row_valid, void* stream);
 
+/* Two s24_spmm problems of identical (M, N, K) and output dtype in ONE
+ * persistent launch (group-major work units): the two split weight gradients
+ * (dW2 and dW1^T, ffn.py:430-450 via splitgemm.py:55-81) share one tile
+ * schedule, so the second fills the first one's partial last wave. Rows are
+ * valid up to M; d_row_valid* as in s24_gemm. */
+int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype, const void* a_vals0,
+                  const uint8_t* a_meta0, const void* B0, int64_t ldb0, void* D0, int64_t ldd0, const int* d_row_map0,
+                  int d_transposed0, const int* d_row_valid0, const void* a_vals1, const uint8_t* a_meta1,
+                  const void* B1, int64_t ldb1, void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1,
+                  const int* d_row_valid1, void* stream);
+
 /* s24_spmm plus a feature-wise split (the K4 job of s24_feature_split with
  * stats == NULL) run as background work by the GEMM's epilogue warps while
  * they wait for accumulators: the tensor-bound sparse GEMM hides the
@@ -178,20 +192,25 @@ int s24_spmm_bg(const void* a_vals, const uint8_t* a_meta, const void* B, int b_
  * feature (sparse24.py:96-115 as used by splitgemm.py:72-76), written
  * transposed: fw_vals bf16 [N_pad128, fw_kdim/2] + fw_meta hw (rows = N
  * features, K = fw_kdim tokens, fw_kdim = M padded to 128), fw_counts uint64[N]
- * += nonzeros before | after << 32 per feature. */
+ * += nonzeros before | after << 32 per feature. row_map (nullable, not with
+ * the fused feature-wise output): input row r is written as act row
+ * row_map[r] (and y_dbg row row_map[r]) -- the token permutation applied in
+ * the epilogue, so X is read unpermuted. */
 int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
                         int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
                         float* y_dbg, void* fw_vals, uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim,
-                        void* stream);
+                        const int* row_map, void* stream);
 
 /* K3: G = dY_c . W2^T with the fused relu^2-derivative + forward-mask
  * epilogue (ffn.py:395-417, 440-443). g: [M, K=d] row-major; w2: [N=h, K=d]
  * row-major. act_vals/act_meta: from K1. Output g_vals bf16 [M_pad128, N/2]
  * on the same metadata; optional fused feature-wise split of g_pre exactly as
- * in s24_fwd_gemm1_fused. */
+ * in s24_fwd_gemm1_fused. row_map (nullable): input row r pairs with act /
+ * g_vals row row_map[r] (unpermuted dY against the permuted activation). */
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
                        int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* fw_vals,
-                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, void* stream);
+                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, const int* row_map,
+                       void* stream);
 
 /* dense-mode twins: act = bf16(relu(X W1)^2) [M, N] (w1 stored [K][N]) */
 int s24_gemm_relu2(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N, int64_t K,

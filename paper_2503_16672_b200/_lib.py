@@ -8,13 +8,15 @@ raise BackendError loudly.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from . import errors
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libs24.so"
+# S24_LIB: alternative build of the same library (A/B experiments, scripts/)
+LIB_PATH = Path(os.environ.get("S24_LIB") or (_PKG / "libs24.so"))
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None
@@ -34,14 +36,15 @@ SIGNATURES: dict[str, list] = {
     "s24_meta_ref_to_hw": [P, I64, I64, P, P],
     "s24_gather_rows": [P, I64, I64, I64, P, P, I64, P],
     "s24_plan": [P, I64, I64, P, P, P, P],
-    "s24_feature_split": [P, P, I64, I64, P, I64, I64, P, P, P, P, P],
+    "s24_feature_split": [P, P, I64, I64, P, I64, I64, P, P, P, P, INT, P],
     "s24_gemm": [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],
     "s24_gemm_splitk": [P, INT, I64, P, INT, I64, I64, I64, I64, INT, P, P, INT, I64, P, INT, P],
     "s24_spmm": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],
+    "s24_spmm_pair": [INT, I64, I64, I64, INT, P, P, P, I64, P, I64, P, INT, P, P, P, P, I64, P, I64, P, INT, P, P],
     "s24_spmm_bg": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P, P, I64, I64, P, I64, I64, P, P, P,
                     P, P],
-    "s24_fwd_gemm1_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, P, P, I64, P],
-    "s24_bwd_dact_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, I64, P],
+    "s24_fwd_gemm1_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, P, P, I64, P, P],
+    "s24_bwd_dact_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, I64, P, P],
     "s24_gemm_relu2": [P, I64, P, I64, I64, I64, I64, P, I64, P],
     "s24_gemm_dact": [P, I64, P, I64, I64, I64, I64, P, I64, P, I64, P],
     "s24_last_error": [],

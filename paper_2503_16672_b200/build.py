@@ -36,14 +36,19 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.is_file())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Compile libs24.so. `defines`/`out` build an experimental variant
+    (e.g. a different tile configuration) next to the product library."""
+    lib = Path(out) if out else LIB
+    if not force and not defines and lib == LIB and not _stale():
         return LIB
     nvcc = _nvcc()
     objs = []
-    tmp = PKG_DIR / "_build"
-    tmp.mkdir(exist_ok=True)
+    tmp = PKG_DIR / "_build" / (lib.stem if lib != LIB else "")
+    tmp.mkdir(parents=True, exist_ok=True)
     flags = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", *ARCH, "-I", str(REPO / "include")]
+    flags += [f"-D{d}" for d in (defines or [])]
     procs = []
     for src in SOURCES:
         obj = tmp / (Path(src).stem + ".o")
@@ -56,13 +61,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         out, _ = p.communicate()
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{out}")
-    link = [nvcc, "-shared", *ARCH, "-o", str(LIB) + ".tmp", *map(str, objs), "-lcudart_static"]
+    link = [nvcc, "-shared", *ARCH, "-o", str(lib) + ".tmp", *map(str, objs), "-lcudart_static"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}{r.stderr}")
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    argv = sys.argv[1:]
+    defs = [argv[i + 1] for i, a in enumerate(argv) if a == "-D"]
+    out = next((argv[i + 1] for i, a in enumerate(argv) if a == "--out"), None)
+    print(build(force="--force" in argv, verbose=True, defines=defs, out=out))

@@ -132,17 +132,22 @@ struct EpiFwd1 {
     float* y_dbg;         // nullable [M, N]
     int N;
     FwTarget fw;          // fused feature-wise selection (fw.vals == nullptr: off)
+    const int* row_map;   // nullable: input row r is written as output row row_map[r]
+                          // (the token permutation applied on the way out)
   };
   struct State {
     unsigned long long before, after;
     const uint2* lut;
+    int drow;             // destination row of this lane's row in the current tile
   };
   static constexpr bool kUnroll = false;
   __device__ static void init(const Params&, State& s) {
     s.before = s.after = 0;
     s.lut = fw_lut_init();
   }
-  __device__ static void prefetch(const Params&, State&, int, bool, int, int) {}
+  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int, int) {
+    s.drow = (p.row_map && row_ok) ? __ldg(p.row_map + row) : row;
+  }
   __device__ static void finish(const Params& p, State& s, uint32_t lane) {
     const unsigned long long b = warp_sum_u64(s.before), a = warp_sum_u64(s.after);
     if (lane == 0 && p.stats) {
@@ -162,7 +167,10 @@ struct EpiFwd1 {
     }
     // per-feature counts over the warp's 32 rows: transpose the nonzero bit
     // matrix so lane i holds column i, then popcount
-    if (p.counts) {
+#ifndef S24_K1_PROBE
+#define S24_K1_PROBE 0  // experiment builds only: 1 = no counts, 2 = no stores
+#endif
+    if (S24_K1_PROBE != 1 && p.counts) {
       const uint32_t col_bits = warp_bit_transpose(nz, lane);
       if (col_bits) atomicAdd(p.counts + col0 + lane, __popc(col_bits));
     }
@@ -189,14 +197,19 @@ struct EpiFwd1 {
     if (!row_ok) return;
     s.before += __popc(nz);
     s.after += __popc(nz & keep32);
-    __nv_bfloat16* dst = p.vals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
+    if (S24_K1_PROBE == 2) {
+      if (packed[0] == 0x12345678u && m16[0] == 77u) p.vals[0] = __float2bfloat16(1.f);  // keep the work alive
+      return;
+    }
+    const int drow = s.drow;
+    __nv_bfloat16* dst = p.vals + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
     st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
     st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
     uint16_t* mh = reinterpret_cast<uint16_t*>(p.meta);
-    mh[meta_hw_halfword_offset(row, col0 / 16, p.N) / 2] = static_cast<uint16_t>(m16[0]);
-    mh[meta_hw_halfword_offset(row, col0 / 16 + 1, p.N) / 2] = static_cast<uint16_t>(m16[1]);
+    st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16, p.N) / 2, static_cast<uint16_t>(m16[0]));
+    st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16 + 1, p.N) / 2, static_cast<uint16_t>(m16[1]));
     if (p.y_dbg) {
-      float* y = p.y_dbg + static_cast<long long>(row) * p.N + col0;
+      float* y = p.y_dbg + static_cast<long long>(drow) * p.N + col0;
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
         st_global_v4(y + i, __float_as_uint(v[i]), __float_as_uint(v[i + 1]), __float_as_uint(v[i + 2]),
@@ -221,6 +234,7 @@ struct EpiBwd1 {
     __nv_bfloat16* gvals;           // [Mpad, N/2] out
     int N;
     FwTarget fw;                    // fused feature-wise selection of g_pre (fw.vals == nullptr: off)
+    const int* row_map;             // nullable: input row r <-> act / g_pre row row_map[r]
   };
   static constexpr int CPW = 4;  // chunks per epilogue warp (BN = 256, 8 epilogue warps)
   static constexpr bool kUnroll = true;
@@ -228,10 +242,13 @@ struct EpiBwd1 {
     uint4 act[2 * CPW];  // 8 kept values per uint4 = 16 logical columns
     uint4 meta[2];       // the row's two 16-byte metadata rows (k1 = 0, 1) of its atom
     const uint2* lut;
+    int drow;            // act / g_pre row of this lane's input row
   };
   __device__ static void init(const Params&, State& s) { s.lut = fw_lut_init(); }
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_first, int) {
+  __device__ static void prefetch(const Params& p, State& s, int row_in, bool row_ok, int col_first, int) {
+    const int row = (p.row_map && row_ok) ? __ldg(p.row_map + row_in) : row_in;
+    s.drow = row;
     if (!row_ok || col_first >= p.N) return;
     const uint4* a =
         reinterpret_cast<const uint4*>(p.act_vals + static_cast<long long>(row) * (p.N / 2) + col_first / 2);
@@ -254,7 +271,7 @@ struct EpiBwd1 {
       }
       return;
     }
-    const uint32_t m1 = (static_cast<uint32_t>(row) >> 3) & 1u;
+    const uint32_t m1 = (static_cast<uint32_t>(s.drow) >> 3) & 1u;
     // the chunk's two 16-column quads (k1 = 0, 1) sit in word k2 = ci of the atom rows
     const uint32_t w0 = word(s.meta[0], ci & 3), w1 = word(s.meta[1], ci & 3);
     const uint32_t m16[2] = {(w0 >> (16 * m1)) & 0xFFFFu, (w1 >> (16 * m1)) & 0xFFFFu};
@@ -270,7 +287,7 @@ struct EpiBwd1 {
       packed[g] = pack_bf16x2(g0 * (2.f * sqrt_approx(a0)), g1 * (2.f * sqrt_approx(a1)));
     }
     if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
-    __nv_bfloat16* dst = p.gvals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
+    __nv_bfloat16* dst = p.gvals + static_cast<long long>(s.drow) * (p.N / 2) + col0 / 2;
     st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
     st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
   }

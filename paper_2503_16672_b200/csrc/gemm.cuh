@@ -16,6 +16,11 @@
 //   warp E+1 : MMA issuer (leader CTA, one thread): tcgen05.cp metadata
 //              smem->TMEM, tcgen05.mma(.sp), tcgen05.commit
 //   warp E+2 : TMEM allocator
+// MC = 2: clusters of two CTA pairs on vertically adjacent tiles (same N
+// columns). B is the operand both pairs read, so each CTA fetches half of its
+// B slice and TMA-multicasts it to its counterpart in the other pair: L2->SM
+// traffic per MAC drops by a third for 2:4 A (where B dominates the stage),
+// and stage slots are recycled only when both pairs' MMAs have released them.
 // The producer and MMA warps sit at the highest warp ids because the warp
 // arbiter prefers higher ids: busy epilogue warps must not delay MMA issue.
 // Accumulators: two TMEM slots. Disjoint (2*BN columns) when they fit, else
@@ -33,6 +38,13 @@
 #include "meta.cuh"
 #include "ptx.cuh"
 
+// experiment-only pipeline probes (never set in the product build):
+//   S24_PIPE_PROBE=1 : no TMA (stages are released empty) -> MMA-issue bound
+//   S24_PIPE_PROBE=2 : no MMA (stages are consumed unread) -> operand-feed bound
+#ifndef S24_PIPE_PROBE
+#define S24_PIPE_PROBE 0
+#endif
+
 namespace s24 {
 
 struct GemmShape {
@@ -40,11 +52,14 @@ struct GemmShape {
   int tiles_m, tiles_n; // in units of (128*CG) x BN
   int group_m;          // raster: group_m M-tiles share one sweep over N
   int k_splits;         // >1: split-K, work unit = (tile, K range); partials go to the epilogue with ks
+  int groups;           // 1 or 2 problems of this shape (second: tmA2/tmB2/tmE2, ep2), group-major units
   int has_bg;           // 1: epilogue warps run K4 units (bg) while waiting for accumulators
+  int* sched;           // dynamic tile scheduler {next, done} (zero at launch, reset by the
+                        // last cluster), or nullptr: static round-robin units
   K4Job bg;
 };
 
-template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8>
+template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8, int MC_ = 1>
 struct GemmCfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr bool A_MN = A_MN_;
@@ -74,7 +89,8 @@ struct GemmCfg {
   static_assert(BN_CTA % 64 == 0 && BN <= 256, "BN");
   static_assert(CG == 1 || CG == 2, "CG");
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int SCHED_SLOTS = 4;  // work-unit broadcast ring (dynamic scheduler)
+  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20 + 1024;
   static constexpr uint32_t IDESC = make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
@@ -85,6 +101,14 @@ struct GemmCfg {
   // 4-epilogue-warp configs cap registers at 128/thread so that an
   // independent kernel (e.g. K4 on a side stream) can co-reside on the SM
   static constexpr int MIN_BLOCKS = EPI_WARPS == 4 ? 2 : 1;
+  // B multicast across MC CTA pairs (see header)
+  static constexpr int MC = MC_;
+  static constexpr int CLUSTER = CG * MC;
+  static constexpr int B_KBOX = BK / 64;  // K-major B: 64-wide K boxes per stage
+  // K-major B with fewer K boxes than pairs is split by rows instead
+  static constexpr int B_ROW_SPLIT = (!B_MN && B_KBOX % MC != 0) ? MC : 1;
+  static constexpr int B_BOX_ROWS = BN_CTA / B_ROW_SPLIT;
+  static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast needs CTA pairs");
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, int& nb) {
@@ -116,7 +140,9 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 template <class Cfg, class Epi>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmE, const GemmShape shape, const typename Epi::Params ep) {
+                const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmA2,
+                const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmE2,
+                const GemmShape shape, const typename Epi::Params ep, const typename Epi::Params ep2) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   constexpr int CG = Cfg::CG;
   extern __shared__ uint8_t smem_raw[];
@@ -127,22 +153,37 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  // dynamic scheduling: the leader CTA's producer takes work units from a
+  // global counter and broadcasts them through this ring to its own MMA and
+  // epilogue warps (sched_full, local arrive) and to the peer CTA (st.async
+  // completing 4 tx bytes on the peer's sched_full); every consumer of both
+  // CTAs releases a slot on the leader's sched_empty
+  constexpr int NS = Cfg::SCHED_SLOTS;
+  uint64_t* sched_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);
+  uint64_t* sched_empty = sched_full + NS;
+  uint32_t* sched_tile = reinterpret_cast<uint32_t*>(sched_empty + NS);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   // roles: epilogue warps first, the latency-critical producer / MMA warps get
   // the highest ids (the warp arbiter prefers higher warp ids)
   constexpr int W_PROD = Cfg::EPI_WARPS, W_MMA = Cfg::EPI_WARPS + 1, W_ALLOC = Cfg::EPI_WARPS + 2;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  constexpr int MC = Cfg::MC;
+  const uint32_t crank = Cfg::CLUSTER > 1 ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank % CG;      // rank within the CTA pair
+  const uint32_t pair = crank / CG;      // which pair of the cluster (MC > 1)
+  const uint32_t leader_rank = pair * CG;
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x / CG;
-  const int num_clusters = gridDim.x / CG;
+  const int cluster_id = blockIdx.x / Cfg::CLUSTER;
+  const int num_clusters = gridDim.x / Cfg::CLUSTER;
   const int mn_tiles = shape.tiles_m * shape.tiles_n;
-  const int total_tiles = mn_tiles * shape.k_splits;
+  const int group_units = mn_tiles * shape.k_splits;
+  const int total_tiles = group_units * shape.groups;
   const int num_kb_all = (shape.K + Cfg::BK - 1) / Cfg::BK;
-  // work unit t -> (output tile t % mn_tiles, K split t / mn_tiles)
+  // work unit t -> (problem t / group_units; within it: output tile
+  // t % mn_tiles, K split t / mn_tiles)
   auto kb_range = [&](int t, int& kb0, int& kb1) {
-    const int ks = t / mn_tiles;
+    const int ks = (t % group_units) / mn_tiles;
     kb0 = static_cast<int>(static_cast<long long>(ks) * num_kb_all / shape.k_splits);
     kb1 = static_cast<int>(static_cast<long long>(ks + 1) * num_kb_all / shape.k_splits);
   };
@@ -151,15 +192,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if constexpr (Cfg::SPARSE) tma_prefetch(&tmE);
+    if (shape.groups > 1) {
+      tma_prefetch(&tmA2);
+      tma_prefetch(&tmB2);
+      if constexpr (Cfg::SPARSE) tma_prefetch(&tmE2);
+    }
   }
   if (warp == W_MMA && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], CG);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], MC);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], CG * (Cfg::OVERLAP ? 128 : Cfg::EPI_THREADS));
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&sched_full[i], 1);
+      // leader MMA + leader epilogue warps (+ peer producer + peer epilogue warps)
+      mbar_init(&sched_empty[i], 1 + Cfg::EPI_WARPS + (CG - 1) * (1 + Cfg::EPI_WARPS));
     }
     fence_barrier_init();
   }
@@ -170,50 +221,126 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   }
   tc_fence_before();
-  if constexpr (CG == 2)
+  if constexpr (Cfg::CLUSTER > 1)
     cluster_sync();
   else
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  const bool dyn = shape.sched != nullptr;
+  // consumer side of the work-unit ring (all lanes of the calling warp, or a
+  // single thread with one_thread): wait, read, release
+  auto sched_take = [&](int iter, bool one_thread) -> int {
+    const int slot = iter % NS;
+    mbar_wait(&sched_full[slot], static_cast<uint32_t>(iter / NS) & 1u);
+    const int t = static_cast<int>(*reinterpret_cast<volatile uint32_t*>(&sched_tile[slot]));
+    if (!one_thread) __syncwarp();
+    if (one_thread || lane == 0) {
+      if (leader)
+        mbar_arrive(&sched_empty[slot]);
+      else
+        mbar_arrive_remote_release(&sched_empty[slot], leader_rank);
+    }
+    return t;
+  };
+
   if (warp == W_PROD) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      uint16_t mc_mask = 0;  // this CTA and its counterparts in the other pairs
+#pragma unroll
+      for (int p = 0; p < MC; ++p) mc_mask |= static_cast<uint16_t>(1u << (p * CG + rank));
+      for (int iter = 0;; ++iter) {
+        int t;
+        if (!dyn) {
+          t = cluster_id + iter * num_clusters;
+        } else if (leader) {
+          const int slot = iter % NS;
+          mbar_wait(&sched_empty[slot], (static_cast<uint32_t>(iter / NS) & 1u) ^ 1u);
+          t = atomicAdd(shape.sched, 1);
+          sched_tile[slot] = static_cast<uint32_t>(t);
+          mbar_arrive(&sched_full[slot]);
+          if constexpr (CG == 2) st_async_remote_u32(&sched_tile[slot], static_cast<uint32_t>(t), &sched_full[slot],
+                                                     leader_rank + 1);
+          if (t >= total_tiles) {
+            // last cluster out resets the counters for the next launch
+            __threadfence();
+            if (atomicAdd(shape.sched + 1, 1) == num_clusters - 1) {
+              atomicExch(shape.sched, 0);
+              atomicExch(shape.sched + 1, 0);
+            }
+          }
+        } else {
+          const int slot = iter % NS;
+          mbar_arrive_expect_tx(&sched_full[slot], 4);
+          t = sched_take(iter, true);
+        }
+        if (t >= total_tiles) break;
         int mb, nb, kb0, kb1;
         tile_coords(shape, t % mn_tiles, mb, nb);
         kb_range(t, kb0, kb1);
-        const int m0 = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
+        const bool g2 = t >= group_units;
+        const CUtensorMap* mapA = g2 ? &tmA2 : &tmA;
+        const CUtensorMap* mapB = g2 ? &tmB2 : &tmB;
+        const CUtensorMap* mapE = g2 ? &tmE2 : &tmE;
+        const int mt = mb * MC + static_cast<int>(pair);  // this pair's M tile
+        const int m0 = mt * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
         const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::BN_CTA;
-        const int atom_row = mb * CG + static_cast<int>(rank);  // 128-row metadata block
+        const int atom_row = mt * CG + static_cast<int>(rank);  // 128-row metadata block
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
+          if constexpr (S24_PIPE_PROBE == 1) {
+            if (leader)
+              mbar_arrive(&full_bar[stage]);
+            else
+              mbar_arrive_remote(&full_bar[stage], leader_rank);
+            if (++stage == Cfg::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (leader)
             mbar_arrive_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
           else
-            mbar_arrive_remote(&full_bar[stage], 0);
+            mbar_arrive_remote(&full_bar[stage], leader_rank);
+          auto load_b = [&](void* dst, int c0, int c1) {
+            if constexpr (MC == 1)
+              tma_load<CG>(dst, mapB, &full_bar[stage], c0, c1);
+            else
+              tma_load_2d_cg2_mc(dst, mapB, &full_bar[stage], c0, c1, mc_mask);
+          };
           if constexpr (Cfg::A_MN) {
-            tma_load<CG>(sa, &tmA, &full_bar[stage], m0, kb * Cfg::BK);
-            tma_load<CG>(sa + Cfg::A_BYTES / 2, &tmA, &full_bar[stage], m0 + 64, kb * Cfg::BK);
+            tma_load<CG>(sa, mapA, &full_bar[stage], m0, kb * Cfg::BK);
+            tma_load<CG>(sa + Cfg::A_BYTES / 2, mapA, &full_bar[stage], m0 + 64, kb * Cfg::BK);
           } else {
-            tma_load<CG>(sa, &tmA, &full_bar[stage], kb * Cfg::A_COLS, m0);
+            tma_load<CG>(sa, mapA, &full_bar[stage], kb * Cfg::A_COLS, m0);
           }
+          // B boxes: with MC pairs, pair p fetches every MC-th box (or row
+          // slice) and multicasts it to the same slot of all pairs
           if constexpr (Cfg::B_MN) {
 #pragma unroll
             for (int j = 0; j < Cfg::BN_CTA / 64; ++j)
-              tma_load<CG>(sb + j * (Cfg::BK * 128), &tmB, &full_bar[stage], n0 + 64 * j, kb * Cfg::BK);
-          } else {
+              if (MC == 1 || j % MC == static_cast<int>(pair))
+                load_b(sb + j * (Cfg::BK * 128), n0 + 64 * j, kb * Cfg::BK);
+          } else if constexpr (Cfg::B_ROW_SPLIT == 1) {
 #pragma unroll
-            for (int j = 0; j < Cfg::BK / 64; ++j)
-              tma_load<CG>(sb + j * (Cfg::BN_CTA * 128), &tmB, &full_bar[stage], kb * Cfg::BK + 64 * j, n0);
+            for (int j = 0; j < Cfg::B_KBOX; ++j)
+              if (MC == 1 || j % MC == static_cast<int>(pair))
+                load_b(sb + j * (Cfg::BN_CTA * 128), kb * Cfg::BK + 64 * j, n0);
+          } else {
+            const int r0 = static_cast<int>(pair) * Cfg::B_BOX_ROWS;
+#pragma unroll
+            for (int j = 0; j < Cfg::B_KBOX; ++j)
+              load_b(sb + j * (Cfg::BN_CTA * 128) + r0 * 128, kb * Cfg::BK + 64 * j, n0 + r0);
           }
           if constexpr (Cfg::SPARSE)
-            tma_load<CG>(sb + Cfg::B_BYTES, &tmE, &full_bar[stage], 0, (atom_row * num_kb_all + kb) * 16);
+            tma_load<CG>(sb + Cfg::B_BYTES, mapE, &full_bar[stage], 0, (atom_row * num_kb_all + kb) * 16);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -227,8 +354,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if (leader && lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int iter = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++iter) {
+      for (int iter = 0;; ++iter) {
+        const int t = dyn ? sched_take(iter, true) : cluster_id + iter * num_clusters;
+        if (t >= total_tiles) break;
         const int slot = iter & 1;
         if constexpr (Cfg::OVERLAP) {
           if (iter > 0) mbar_wait(&tempty_bar[0], (iter - 1) & 1);
@@ -254,7 +382,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
               tmem_cp_128x128b(e_tmem, edesc);
           }
 #pragma unroll
-          for (int j = 0; j < Cfg::KSTEPS; ++j) {
+          for (int j = 0; j < (S24_PIPE_PROBE == 2 ? 0 : Cfg::KSTEPS); ++j) {
             uint64_t adesc, bdesc;
             if constexpr (Cfg::A_MN) {
               adesc = make_sdesc(sa + j * 2048, Cfg::A_BYTES / 2, 1024, kLayoutSw128);
@@ -287,8 +415,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           }
           uint64_t* tf = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
           if constexpr (CG == 2) {
-            mma_commit_cg2(&empty_bar[stage], 0x3);
-            if (kb == kb1 - 1) mma_commit_cg2(tf, 0x3);
+            // the slot may be refilled (by every pair's multicast) once all
+            // pairs released it; the accumulator belongs to this pair only
+            mma_commit_cg2(&empty_bar[stage], static_cast<uint16_t>((1u << Cfg::CLUSTER) - 1));
+            if (kb == kb1 - 1) mma_commit_cg2(tf, static_cast<uint16_t>(0x3u << leader_rank));
           } else {
             mma_commit(&empty_bar[stage]);
             if (kb == kb1 - 1) mma_commit(tf);
@@ -323,14 +453,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       k4_warp_unit<false>(shape.bg.a, t0, fb, static_cast<int>(lane), bg_lut);
       return true;
     };
-    int iter = 0;
-    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++iter) {
+    for (int iter = 0;; ++iter) {
+      const int t = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
+      if (t >= total_tiles) break;
       int mb, nb;
       tile_coords(shape, t % mn_tiles, mb, nb);
       const int slot = iter & 1;
-      const int row = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 + static_cast<int>(lane);
+      const int row = (mb * MC + static_cast<int>(pair)) * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 +
+                      static_cast<int>(lane);
       const bool row_ok = row < shape.M;
-      Epi::prefetch(ep, st, row, row_ok, nb * Cfg::BN + c_begin * 32, t / mn_tiles);
+      const typename Epi::Params& epg = t >= group_units ? ep2 : ep;
+      Epi::prefetch(epg, st, row, row_ok, nb * Cfg::BN + c_begin * 32, (t % group_units) / mn_tiles);
       uint64_t* tempty = &tempty_bar[Cfg::OVERLAP ? 0 : slot];
       // overlapping slots: the chunk shared with the other slot (last chunk of
       // slot 0, first of slot 1) gates the next tile's MMAs. Only the part that
@@ -369,13 +502,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           if (leader)
             mbar_arrive(tempty);
           else
-            mbar_arrive_remote(tempty, 0);
+            mbar_arrive_remote(tempty, leader_rank);
         }
         if (col0 < shape.N) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          Epi::chunk(ep, st, row, row_ok, col0, ci, v, lane);
+          Epi::chunk(epg, st, row, row_ok, col0, ci, v, lane);
         }
       }
       if constexpr (!Cfg::OVERLAP) {
@@ -383,7 +516,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         if (leader)
           mbar_arrive(tempty);
         else
-          mbar_arrive_remote(tempty, 0);
+          mbar_arrive_remote(tempty, leader_rank);
       }
     }
     // drain what is left of the background queue
@@ -393,7 +526,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   }
 
   tc_fence_before();
-  if constexpr (CG == 2)
+  if constexpr (Cfg::CLUSTER > 1)
     cluster_sync();
   else
     __syncthreads();

@@ -68,92 +68,168 @@ int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
 }
 
 // ---------------------------------------------------------------------------
-template <class Cfg, class Epi>
-static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1,
-                       const K4Job* bg = nullptr) {
-  if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
-  if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
-  CUtensorMap ma, mb;
+// Dynamic tile scheduler counters: {next, done} int pairs in device memory,
+// zeroed once and reset by each launch's last cluster. Launches take pairs
+// round-robin, so concurrent launches on different streams never share one.
+static constexpr int kSchedSlots = 4096;
+
+static int* sched_counter() {
+  static std::mutex mu;
+  static int* pool[64] = {nullptr};
+  static unsigned next[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    int* p = nullptr;
+    if (cudaMalloc(&p, sizeof(int) * 2 * kSchedSlots) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, sizeof(int) * 2 * kSchedSlots) != cudaSuccess) return nullptr;
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    pool[dev] = p;
+  }
+  return pool[dev] + 2 * (next[dev]++ % kSchedSlots);
+}
+
+// operands of one GEMM problem (the grouped launch takes two of equal shape)
+template <class Epi>
+struct GemmOperands {
+  const void* A;
+  int64_t lda;
+  const void* B;
+  int64_t ldb;
+  const uint8_t* meta;
+  typename Epi::Params ep;
+};
+
+template <class Cfg>
+static int make_operand_maps(const void* A, int64_t lda, const void* B, int64_t ldb, const uint8_t* meta, int64_t M,
+                             int64_t N, int64_t K, CUtensorMap* ma, CUtensorMap* mb, CUtensorMap* me) {
   int rc;
   // A
   if constexpr (Cfg::A_MN) {
-    rc = make_map_bf16(&ma, A, M, K, lda, 64, Cfg::BK);
+    rc = make_map_bf16(ma, A, M, K, lda, 64, Cfg::BK);
   } else if constexpr (Cfg::SPARSE) {
     const int64_t mpad = (M + 127) / 128 * 128;
-    rc = make_map_bf16(&ma, A, K / 2, mpad, K / 2, 64, Cfg::BM);
+    rc = make_map_bf16(ma, A, K / 2, mpad, K / 2, 64, Cfg::BM);
   } else {
-    rc = make_map_bf16(&ma, A, K, M, lda, 64, Cfg::BM);
+    rc = make_map_bf16(ma, A, K, M, lda, 64, Cfg::BM);
   }
   if (rc) return rc;
   // B
   if constexpr (Cfg::B_MN) {
-    rc = make_map_bf16(&mb, B, N, K, ldb, 64, Cfg::BK);
+    rc = make_map_bf16(mb, B, N, K, ldb, 64, Cfg::BK);
   } else {
-    rc = make_map_bf16(&mb, B, K, N, ldb, 64, Cfg::BN_CTA);
+    rc = make_map_bf16(mb, B, K, N, ldb, 64, Cfg::B_BOX_ROWS);
   }
   if (rc) return rc;
-
-  CUtensorMap me;
-  std::memset(&me, 0, sizeof(me));
+  std::memset(me, 0, sizeof(*me));
   if constexpr (Cfg::SPARSE) {
     // metadata atoms viewed as [atoms * 16 rows, 128 bytes]; one box = one atom
     const int64_t atoms = (M + 127) / 128 * (K / 128);
-    rc = make_map_2d(&me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16, false);
+    rc = make_map_2d(me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16, false);
     if (rc) return rc;
+  }
+  return S24_OK;
+}
+
+template <class Cfg, class Epi>
+static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                       const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1,
+                       const K4Job* bg = nullptr, const GemmOperands<Epi>* second = nullptr) {
+  if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
+  if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
+  CUtensorMap ma, mb, me, ma2, mb2, me2;
+  int rc = make_operand_maps<Cfg>(A, lda, B, ldb, meta, M, N, K, &ma, &mb, &me);
+  if (rc) return rc;
+  if (second) {
+    rc = make_operand_maps<Cfg>(second->A, second->lda, second->B, second->ldb, second->meta, M, N, K, &ma2, &mb2,
+                                &me2);
+    if (rc) return rc;
+  } else {
+    ma2 = ma;
+    mb2 = mb;
+    me2 = me;
   }
 
   GemmShape sh;
   sh.M = static_cast<int>(M);
   sh.N = static_cast<int>(N);
   sh.K = static_cast<int>(K);
-  sh.tiles_m = static_cast<int>((M + Cfg::TILE_M - 1) / Cfg::TILE_M);
+  // work units cover MC vertically adjacent tiles (one per CTA pair)
+  sh.tiles_m = static_cast<int>((M + Cfg::TILE_M * Cfg::MC - 1) / (Cfg::TILE_M * Cfg::MC));
   sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
-  sh.group_m = 16 / Cfg::CG;
+  sh.group_m = 16 / Cfg::CLUSTER;
   sh.k_splits = k_splits < 1 ? 1 : k_splits;
+  sh.groups = second ? 2 : 1;
+  sh.sched = nullptr;
+#ifndef S24_STATIC_SCHED
+  if constexpr (Cfg::MC == 1) {
+    // dynamic work units: clusters that start late (SMs still busy with a
+    // co-running kernel) or run slow simply take fewer units
+    sh.sched = sched_counter();
+    if (!sh.sched) return fail(S24_ERR_CUDA, "scheduler counters unavailable");
+  }
+#endif
   sh.has_bg = bg != nullptr;
   if (bg)
     sh.bg = *bg;
   else
     std::memset(&sh.bg, 0, sizeof(sh.bg));
-  const int tiles = sh.tiles_m * sh.tiles_n * sh.k_splits;
-  const int max_clusters = num_sms() / Cfg::CG;
-  const int clusters = tiles < max_clusters ? tiles : max_clusters;
+  const int tiles = sh.tiles_m * sh.tiles_n * sh.k_splits * sh.groups;
 
   auto kern = gemm_kernel<Cfg, Epi>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CG));
   cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = Cfg::CG;
+  attr[0].val.clusterDim.x = Cfg::CLUSTER;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, sh, ep);
+  // persistent grid: as many clusters as fit at once (clusters of 4 may not
+  // tile every GPC exactly, so ask the occupancy calculator)
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int max_clusters = 0;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    max_clusters = num_sms() / Cfg::CLUSTER;
+    if (attr_err == cudaSuccess && Cfg::CLUSTER > 2) {
+      cfg.gridDim = dim3(static_cast<unsigned>(max_clusters * Cfg::CLUSTER));
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0 && n < max_clusters)
+        max_clusters = n;
+      cudaGetLastError();
+    }
+  });
+  if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  const int clusters = tiles < max_clusters ? tiles : max_clusters;
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CLUSTER));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, ma2, mb2, me2, sh, ep, second ? second->ep : ep);
   if (e != cudaSuccess) return fail(S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return check_launch("gemm_kernel");
 }
 
 // tile configurations
 // <sparse, A MN-major, B MN-major, BN, stages, CTA-group>
-using DenseKN = GemmCfg<false, false, true, 256, 6, 2>;   // A K-major, B MN-major
-using DenseKK = GemmCfg<false, false, false, 256, 6, 2>;  // A K-major, B K-major
-using DenseMM = GemmCfg<false, true, true, 256, 6, 2>;    // A MN-major, B MN-major
-using DenseMK = GemmCfg<false, true, false, 256, 6, 2>;   // A MN-major, B K-major
+#ifndef S24_DENSE_MC
+#define S24_DENSE_MC 1
+#endif
+using DenseKN = GemmCfg<false, false, true, 256, 6, 2, 8, S24_DENSE_MC>;   // A K-major, B MN-major
+using DenseKK = GemmCfg<false, false, false, 256, 6, 2, 8, S24_DENSE_MC>;  // A K-major, B K-major
+using DenseMM = GemmCfg<false, true, true, 256, 6, 2, 8, S24_DENSE_MC>;    // A MN-major, B MN-major
+using DenseMK = GemmCfg<false, true, false, 256, 6, 2, 8, S24_DENSE_MC>;   // A MN-major, B K-major
 // sparse: light epilogue, 4 epilogue warps and <= 128 registers/thread, leaving
 // room for a co-resident side-stream kernel (the feature-wise split K4)
-using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4>;  // sparse A, B MN-major
-using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4>; // sparse A, B K-major
+// (S24_SPARSE_MC = CTA pairs per cluster sharing B by TMA multicast)
+#ifndef S24_SPARSE_MC
+#define S24_SPARSE_MC 1
+#endif
+using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4, S24_SPARSE_MC>;   // sparse A, B MN-major
+using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, S24_SPARSE_MC>;  // sparse A, B K-major
 
 template <class Epi>
 static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
@@ -164,32 +240,51 @@ static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const 
   return launch_gemm<DenseMK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
 }
 
-// split-K partial sums ws[ks][M][N] -> D (row map / transpose), fixed order
+// split-K partial sums ws[ks][M][N] -> D (row map / transpose), fixed order.
+// One thread per 4 consecutive columns (float4 partial reads; N % 32 == 0).
 template <typename OutT>
-__global__ void k_splitk_reduce(const float* __restrict__ ws, int k_splits, long long M, long long N,
-                                OutT* __restrict__ out, long long ldo, const int* __restrict__ row_map,
-                                int transposed) {
-  const long long total = M * N;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ ws, int k_splits, long long M,
+                                                       long long N, OutT* __restrict__ out, long long ldo,
+                                                       const int* __restrict__ row_map, int transposed) {
+  const long long total = M * N, quads = total / 4;
+  for (long long qi = blockIdx.x * (long long)blockDim.x + threadIdx.x; qi < quads;
+       qi += (long long)gridDim.x * blockDim.x) {
+    const long long i = qi * 4;
+    float4 acc = *reinterpret_cast<const float4*>(ws + i);
+    for (int k = 1; k < k_splits; ++k) {
+      const float4 p = *reinterpret_cast<const float4*>(ws + k * total + i);
+      acc.x += p.x;
+      acc.y += p.y;
+      acc.z += p.z;
+      acc.w += p.w;
+    }
     const long long m = i / N, n = i - m * N;
-    float acc = ws[i];
-    for (int k = 1; k < k_splits; ++k) acc += ws[k * total + i];
     const long long r = row_map ? row_map[m] : m;
-    OutT* dst = transposed ? out + n * ldo + r : out + r * ldo + n;
-    if constexpr (sizeof(OutT) == 4)
-      *dst = acc;
-    else
-      *dst = __float2bfloat16_rn(acc);
+    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+    if (transposed) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (sizeof(OutT) == 4)
+          out[(n + j) * ldo + r] = v[j];
+        else
+          out[(n + j) * ldo + r] = __float2bfloat16_rn(v[j]);
+      }
+    } else if constexpr (sizeof(OutT) == 4) {
+      *reinterpret_cast<float4*>(out + r * ldo + n) = acc;
+    } else {
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + r * ldo + n);
+      o[0] = __floats2bfloat162_rn(v[0], v[1]);
+      o[1] = __floats2bfloat162_rn(v[2], v[3]);
+    }
   }
 }
 
 template <class Epi>
 static int dispatch_sparse(int b_mn, const void* A, const uint8_t* meta, const void* B, int64_t ldb, int64_t M,
                            int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st,
-                           const K4Job* bg = nullptr) {
-  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg);
-  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg);
+                           const K4Job* bg = nullptr, const GemmOperands<Epi>* second = nullptr) {
+  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg, second);
+  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg, second);
 }
 
 static int check_common(int64_t M, int64_t N, int64_t K, int64_t lda, int a_mn, int64_t ldb, int b_mn) {
@@ -243,14 +338,15 @@ int s24_gemm_splitk(const void* A, int a_mn_major, int64_t lda, const void* B, i
   if (rc) return rc;
   if (k_splits < 1 || k_splits > 64) return fail(S24_ERR_CONFIG, "k_splits must be in [1, 64]");
   if (!workspace) return fail(S24_ERR_DIMENSION, "split-K needs a workspace of k_splits*M*N floats");
+  if (ldd % 4 != 0 && !d_transposed) return fail(S24_ERR_DIMENSION, "split-K output needs ldd %% 4 == 0");
   if (out_dtype != S24_F32 && out_dtype != S24_BF16) return fail(S24_ERR_PRECISION, "unsupported output dtype");
   if (M == 0 || N == 0) return S24_OK;
   auto st = static_cast<cudaStream_t>(stream);
   EpiStore<float>::Params ep{workspace, N, nullptr, 0, static_cast<int>(M), nullptr, M * N};
   rc = dispatch_dense<EpiStore<float>>(a_mn_major, b_mn_major, A, lda, B, ldb, M, N, K, ep, st, k_splits);
   if (rc) return rc;
-  long long blocks = (M * N + 255) / 256;
-  if (blocks > 4L * num_sms()) blocks = 4L * num_sms();
+  long long blocks = (M * N / 4 + 255) / 256;
+  if (blocks > 8L * num_sms()) blocks = 8L * num_sms();
   if (out_dtype == S24_F32)
     k_splitk_reduce<float><<<static_cast<int>(blocks), 256, 0, st>>>(workspace, k_splits, M, N, static_cast<float*>(D),
                                                                    ldd, d_row_map, d_transposed);
@@ -301,6 +397,29 @@ int s24_spmm_bg(const void* a_vals, const uint8_t* a_meta, const void* B, int b_
   });
 }
 
+int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype, const void* a_vals0,
+                  const uint8_t* a_meta0, const void* B0, int64_t ldb0, void* D0, int64_t ldd0, const int* d_row_map0,
+                  int d_transposed0, const int* d_row_valid0, const void* a_vals1, const uint8_t* a_meta1,
+                  const void* B1, int64_t ldb1, void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1,
+                  const int* d_row_valid1, void* stream) {
+  int rc = check_common(M, N, K, K, 0, ldb0, b_mn_major);
+  if (rc) return rc;
+  if ((rc = check_common(M, N, K, K, 0, ldb1, b_mn_major))) return rc;
+  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
+  if ((!d_transposed0 && ldd0 < N) || (!d_transposed1 && ldd1 < N)) return fail(S24_ERR_DIMENSION, "ldd too small");
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    using Epi = EpiStore<OutT>;
+    typename Epi::Params ep0{static_cast<OutT*>(D0), ldd0, d_row_map0, d_transposed0, static_cast<int>(M),
+                             d_row_valid0, 0};
+    GemmOperands<Epi> second{a_vals1, K / 2, B1, ldb1, a_meta1,
+                             typename Epi::Params{static_cast<OutT*>(D1), ldd1, d_row_map1, d_transposed1,
+                                                  static_cast<int>(M), d_row_valid1, 0}};
+    return dispatch_sparse<Epi>(b_mn_major, a_vals0, a_meta0, B0, ldb0, M, N, K, ep0,
+                                static_cast<cudaStream_t>(stream), nullptr, &second);
+  });
+}
+
 static int check_fw(void* fw_vals, const uint8_t* fw_meta, int64_t fw_kdim, int64_t M) {
   if (!fw_vals) return S24_OK;
   if (!fw_meta) return fail(S24_ERR_DIMENSION, "feature-wise output needs its metadata buffer");
@@ -312,26 +431,31 @@ static int check_fw(void* fw_vals, const uint8_t* fw_meta, int64_t fw_kdim, int6
 int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
                         int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
                         float* y_dbg, void* fw_vals, uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim,
-                        void* stream) {
+                        const int* row_map, void* stream) {
   int rc = check_common(M, N, K, ldx, 0, ldw1, 1);
   if (rc) return rc;
   if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
   if ((rc = check_fw(fw_vals, fw_meta, fw_kdim, M))) return rc;
+  if (row_map && fw_vals) return fail(S24_ERR_CONFIG, "the fused feature-wise output needs unmapped rows");
   EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N),
-                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)}};
+                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)},
+                     row_map};
   return launch_gemm<DenseKN, EpiFwd1>(x, ldx, w1, ldw1, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
                        int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* fw_vals,
-                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, void* stream) {
+                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, const int* row_map,
+                       void* stream) {
   int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
   if (rc) return rc;
   if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
   if ((rc = check_fw(fw_vals, fw_meta, fw_kdim, M))) return rc;
   EpiBwd1::Params ep{static_cast<const __nv_bfloat16*>(act_vals), act_meta, static_cast<__nv_bfloat16*>(g_vals),
                      static_cast<int>(N),
-                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)}};
+                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)},
+                     row_map};
+  if (row_map && fw_vals) return fail(S24_ERR_CONFIG, "the fused feature-wise output needs unmapped rows");
   return launch_gemm<DenseKK, EpiBwd1>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 

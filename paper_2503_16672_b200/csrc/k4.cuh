@@ -31,6 +31,7 @@ struct K4Args {
   uint8_t* es;                // hw metadata of vs (rows = sparse rank, K = n)
   __nv_bfloat16* vd;          // [pad128(n_dense), n]
   unsigned long long* stats;  // += nonzeros before/after over sparse features (WITH_STATS)
+  int nonneg;                 // 1: values are >= 0 and NaN-free (relu^2): rank raw values
 };
 
 // background-job descriptor for the GEMM epilogue warps
@@ -67,8 +68,6 @@ __device__ __forceinline__ const uint2* k4_lut_init() {
   return lut[warp];
 }
 
-constexpr unsigned long long kK4KeepToNibble = 0x000E0DC009804000ull;  // keep bits -> i0 | i1 << 2
-
 // bf16x2 magnitude keys, NaN mapped below zero (-1.0); ordered with native
 // bf16 compares (HSET2), which keeps the selection at one instruction per pair
 __device__ __forceinline__ uint32_t k4_key2(uint32_t x) {
@@ -93,7 +92,9 @@ __device__ __forceinline__ uint32_t k4_sel(uint32_t m, uint32_t a, uint32_t b) {
 // majority of three bitwise masks
 __device__ __forceinline__ uint32_t k4_maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 
-template <bool WITH_STATS>
+// NONNEG: the operand is relu^2 (>= 0, never NaN), so the raw bf16 values
+// order correctly under HSET2 and the magnitude/NaN keys are skipped
+template <bool WITH_STATS, bool NONNEG = false>
 __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase, int lane, const uint2* sel_lut) {
   const __nv_bfloat16* __restrict__ vals = a.vals;
   const uint8_t* __restrict__ meta_hw = a.meta;
@@ -137,7 +138,6 @@ __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase,
       X[r][2 * g + 1] = __byte_perm(w[g], 0u, sl.y);
     }
   }
-  const unsigned long long lut = kK4KeepToNibble;
   uint32_t* vs32 = reinterpret_cast<uint32_t*>(vs);
   uint2* vd64 = reinterpret_cast<uint2*>(vd);
   uint32_t cnt_b = 0, cnt_a = 0;  // per-half nonzero counters (sparse features only)
@@ -148,7 +148,13 @@ __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase,
     const uint32_t ofs0 = __shfl_sync(0xffffffffu, my_ofs, 2 * k), ofs1 = __shfl_sync(0xffffffffu, my_ofs, 2 * k + 1);
     const bool sp0 = !(ofs0 & 0x80000000u), sp1 = !(ofs1 & 0x80000000u);
     if (vs != nullptr && (sp0 || sp1)) {
-      const uint32_t k0 = k4_key2(x0), k1 = k4_key2(x1), k2 = k4_key2(x2), k3 = k4_key2(x3);
+      uint32_t k0 = x0, k1 = x1, k2 = x2, k3 = x3;
+      if constexpr (!NONNEG) {
+        k0 = k4_key2(x0);
+        k1 = k4_key2(x1);
+        k2 = k4_key2(x2);
+        k3 = k4_key2(x3);
+      }
       // token i beats token j (i < j) iff key_i >= key_j: ties go to the lower token
       const uint32_t b01 = k4_ge(k0, k1), b02 = k4_ge(k0, k2), b03 = k4_ge(k0, k3);
       const uint32_t b12 = k4_ge(k1, k2), b13 = k4_ge(k1, k3), b23 = k4_ge(k2, k3);
@@ -157,11 +163,12 @@ __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase,
       const uint32_t K2 = k4_maj(~b02, ~b12, b23), K3 = k4_maj(~b03, ~b13, ~b23);
       const uint32_t v0 = k4_sel(K0, x0, k4_sel(K1, x1, x2));  // first kept token
       const uint32_t v1 = k4_sel(K3, x3, k4_sel(K2, x2, x1));  // second kept token
-      const uint32_t kb = (K0 & 0x00010001u) | (K1 & 0x00020002u) | (K2 & 0x00040004u) | (K3 & 0x00080008u);
+      // selector nibble i0 | i1 << 2 of both features (16-bit halves) straight
+      // from the keep masks: i0 = first kept (0, 1 or 2), i1 = last kept (1, 2 or 3)
+      const uint32_t nib = ((~K0 & K1) & 0x00010001u) | ((~K0 & ~K1) & 0x00020002u) | ((K3 | ~K2) & 0x00040004u) |
+                           ((K3 | K2) & 0x00080008u);
       // metadata halfwords of both features at once: 4 lanes (token groups) x 4 bits
-      uint32_t hw = ((static_cast<uint32_t>(lut >> (4 * (kb & 0xFu))) & 0xFu) |
-                     ((static_cast<uint32_t>(lut >> (4 * ((kb >> 16) & 0xFu))) & 0xFu) << 16))
-                    << (4 * (lane & 3));
+      uint32_t hw = nib << (4 * (lane & 3));
       hw |= __shfl_xor_sync(0xffffffffu, hw, 1);
       hw |= __shfl_xor_sync(0xffffffffu, hw, 2);
       const uint32_t mb0 = __shfl_sync(0xffffffffu, my_mb, 2 * k), mb1 = __shfl_sync(0xffffffffu, my_mb, 2 * k + 1);

@@ -384,11 +384,11 @@ __global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts, i
 
 // ---------------------------------------------------------------------------
 // K4 standalone grid: CTA = 128 tokens x 128 features = 8 warp units.
-template <bool WITH_STATS>
+template <bool WITH_STATS, bool NONNEG>
 __global__ void __launch_bounds__(256) k_feature_split(K4Args a) {
   const uint2* lut = k4_lut_init();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  k4_warp_unit<WITH_STATS>(a, blockIdx.y * 128, blockIdx.x * 128 + warp * 16, lane, lut);
+  k4_warp_unit<WITH_STATS, NONNEG>(a, blockIdx.y * 128, blockIdx.x * 128 + warp * 16, lane, lut);
 }
 
 static int grid_for(long long work, int block) {
@@ -415,7 +415,7 @@ int k4_prepare(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, c
   if (d_pad > n_dense && vd)
     cudaMemsetAsync(static_cast<__nv_bfloat16*>(vd) + n_dense * n, 0, (d_pad - n_dense) * n * 2, st);
   *out = K4Args{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
-                static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd), nullptr};
+                static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd), nullptr, 0};
   return S24_OK;
 }
 
@@ -593,18 +593,19 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
 
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
-                      unsigned long long* stats, void* stream) {
+                      unsigned long long* stats, int operand_nonneg, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   K4Args a;
   int rc = k4_prepare(vals, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs, es, vd, st, &a);
   if (rc) return rc;
   if (n == 0 || h == 0) return S24_OK;
   a.stats = stats;
+  a.nonneg = operand_nonneg ? 1 : 0;
   dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
   if (stats)
-    k_feature_split<true><<<grid, 256, 0, st>>>(a);
+    (a.nonneg ? k_feature_split<true, true> : k_feature_split<true, false>)<<<grid, 256, 0, st>>>(a);
   else
-    k_feature_split<false><<<grid, 256, 0, st>>>(a);
+    (a.nonneg ? k_feature_split<false, true> : k_feature_split<false, false>)<<<grid, 256, 0, st>>>(a);
   return check_launch("k_feature_split");
 }
 

@@ -3,18 +3,21 @@ for the reference's pkg/src/srelu24/ffn.py (ffn_forward / ffn_backward and
 their dataclasses; activation = squared_relu).
 
 Recipe forward (ref ffn.py:276-363), one device pass each:
-  K6  x_in = permute_rows(x, perm)                    (row gather)
-  K1  Y1 = x_in . W1 -> relu^2 -> token-wise 2:4       (tcgen05 GEMM, fused epilogue:
-      compressed act + hw metadata + per-feature counts + drop stats)
-  K7  plan = partition_features(counts, ratio)        (device radix select)
+  K1  Y1 = x . W1 -> relu^2 -> token-wise 2:4          (tcgen05 GEMM, fused epilogue:
+      compressed act + hw metadata + per-feature counts + drop stats; input row
+      r is written as act row perm[r], i.e. permute_rows folded into the store)
   K2  out = inverse_permute_rows(act_sp . W2)          (tcgen05.mma.sp, row map epilogue)
+  side stream, next to K2:
+  K7  plan = partition_features(counts, ratio)         (device radix select)
+  K6  x_in = permute_rows(x, perm)                     (row gather, dW1 operand)
+  K4  feature-wise 2:4 split of act (sparse features) + dense columns
 Recipe backward (ref ffn.py:366-451):
-  K6  g_c = permute_rows(g_out, perm)
-  K3  g_pre = (g_c . W2^T) * 2 relu(y1) on the forward keep pattern (fused, compressed)
-  K4  feature-wise 2:4 split of act and of g_pre (sparse features) + dense columns
-  K5  dW2 = split(act)^T g_c ; dW1 = (split(g_pre)^T x_in)^T  (sparse + dense GEMMs,
-      feature-index scatter / transpose in the epilogue)
+  K3  g_pre = (dY . W2^T) * 2 relu(y1) on the forward keep pattern (fused,
+      compressed, rows paired with act row perm[r])
   K2  dX = inverse_permute_rows(g_pre_sp . W1^T)       (exact: forward metadata)
+  side stream: K6 g_c = permute_rows(dY, perm); K4 split of g_pre (next to dX)
+  K5  dW2 = split(act)^T g_c ; dW1 = (split(g_pre)^T x_in)^T  (one grouped sparse
+      launch + dense remainders, feature-index scatter / transpose in the epilogue)
 Dense mode runs the same GEMM kernels with dense operands (the "dense twin").
 
 Tensors are bf16 on the device (numpy float32 inputs are uploaded and rounded
@@ -51,6 +54,7 @@ from .splitgemm import (
     partition_features,
     split_gemm_macs,
     split_weight_grad,
+    split_weight_grad_pair,
 )
 
 ACTIVATIONS = ("squared_relu", "swiglu")
@@ -69,6 +73,16 @@ FUSED_FEATURE_SPLIT = os.environ.get("S24_FUSED_FW", "0") == "1"
 #   "background" -- inside the GEMM, in its idle epilogue warps (s24_spmm_bg)
 #   "inline"     -- serialized on the main stream
 K4_MODE = os.environ.get("S24_K4_MODE", "side")
+# Both split weight gradients in one grouped sparse launch (s24_spmm_pair)
+# when no per-gradient hook needs dW2 early. S24_PAIRED_WGRAD=0 disables.
+PAIRED_WEIGHT_GRADS = os.environ.get("S24_PAIRED_WGRAD", "1") == "1"
+# Gather the permuted copies x_in / g_c (weight-gradient operands only) on the
+# side stream next to the GEMMs ("1") or on the main stream right before
+# their first use ("0").
+SIDE_GATHERS = os.environ.get("S24_SIDE_GATHERS", "1") == "1"
+# K1 / K3 read x / dY unpermuted and apply the permutation as an epilogue row
+# map ("1"), or read the gathered copies x_in / g_c ("0").
+ROWMAP_GEMMS = os.environ.get("S24_ROWMAP", "0") == "1"
 FORWARD_MODES = ("dense", "sparse24")
 BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
 
@@ -189,6 +203,7 @@ class FfnCache:
     act_fw: FusedFeatureOperand | None = None  # feature-wise 2:4 act of all features (from K1)
     act_split: FeatureSplit | None = None  # feature-wise split of act (K4, run during fwd.out)
     act_split_ready: object = None  # CUDA event after which act_split is complete (side-stream K4)
+    x_in_ready: object = None  # CUDA event after which x_in is complete (gathered on the side stream)
 
     @property
     def act_sparse(self) -> Sparse24Matrix | None:
@@ -268,27 +283,20 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     npad = pad128(n)
     census: list[GemmEvent] = []
 
-    # compute-frame input, padded to a multiple of 128 rows (zero rows are
-    # transparent to every stage: they produce zero activations and gradients)
-    x_in = torch.empty(npad, d, dtype=BF16, device=dev)
-    if npad > n:
-        x_in[n:].zero_()
     perm = perm_dev = inv_dev = None
-    if cfg.permute_tokens and sparse_fwd:
+    permute = cfg.permute_tokens and sparse_fwd
+    if permute:
         perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
         perm = perm_dev
-        gather_rows(x, inv_dev, x_in)  # x_in[p[i]] = x[i]
-    else:
-        x_in[:n].copy_(x)
 
     out = torch.empty(n, d, dtype=BF16, device=dev)
     if not sparse_fwd:
         act = torch.empty(n, h, dtype=BF16, device=dev)
-        _lib.call("s24_gemm_relu2", ptr(x_in), d, ptr(p.w1), h, n, h, d, ptr(act), h, s)
+        _lib.call("s24_gemm_relu2", ptr(x), d, ptr(p.w1), h, n, h, d, ptr(act), h, s)
         census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
         _lib.call("s24_gemm", ptr(act), 0, h, ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d, None, 0, -1, None, s)
         census.append(GemmEvent("fwd.out", False, gemm_macs(n, h, d)))
-        cache = FfnCache(x_in, n, None, None, act, None, None, None, None, None, None, None, census, cfg)
+        cache = FfnCache(x, n, None, None, act, None, None, None, None, None, None, None, census, cfg)
         return out, cache
 
     act_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
@@ -304,62 +312,147 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     # 2:4 compressed; K1's epilogue produces that operand for every feature
     act_fw = FusedFeatureOperand.alloc(h, npad, dev) if (FUSED_FEATURE_SPLIT and cfg.backward_mode != "dense") else None
     fw_args = act_fw.args() if act_fw is not None else (None, None, None, 0)
-    _lib.call("s24_fwd_gemm1_fused", ptr(x_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta), ptr(counts),
-              ptr(stats_dev), ptr(pre), *fw_args, s)
+
+    # The compute frame is the token-permuted order (ref ffn.py:297-303). K1
+    # reads x as is and writes input row r as activation row perm[r] (row map
+    # in its epilogue); the permuted copy x_in (zero rows up to a multiple of
+    # 128) is only the B operand of the dW1 GEMM, so it is gathered off the
+    # critical path. The fused feature-wise epilogue needs permuted input rows.
+    side = side_stream(dev) if (for_backward and K4_MODE == "side") else None
+    # (inference prefill, for_backward=False, needs no x_in at all)
+    x_in = _frame_rows(x, npad, inv_dev if permute else None, defer=True) if for_backward else None
+    k1_in, k1_map = x, (perm_dev if permute else None)
+    if (act_fw is not None or not ROWMAP_GEMMS) and permute:
+        if x_in is None:
+            x_in = _frame_rows(x, npad, inv_dev, defer=True)
+        _fill_frame_rows(x_in, x, inv_dev)
+        k1_in, k1_map = x_in, None
+    _lib.call("s24_fwd_gemm1_fused", ptr(k1_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta),
+              ptr(counts), ptr(stats_dev), ptr(pre), *fw_args, ptr(k1_map), s)
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
+    if plan is not None and plan.hidden_dim != h:
+        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+    need_plan = cfg.backward_mode == "split_masked"
 
-    plan_out = None
-    if cfg.backward_mode == "split_masked":
-        if plan is not None and plan.hidden_dim != h:
-            raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
-        plan_out = plan if plan is not None else partition_features(counts, cfg.split_ratio)
-
-    # fwd.out on tensor cores; when the backward will need the feature-wise
-    # split of act (and the plan is known), K4 runs as background work in the
-    # GEMM's idle epilogue warps
+    # fwd.out on tensor cores (inverse permutation as its epilogue row map).
+    # Next to it, on a side stream: the split plan (K7), x_in, and -- when the
+    # backward will need it -- K4, the feature-wise split of act.
     act_split = None
-    bg_plan = plan_out if cfg.backward_mode == "split_masked" else (
-        _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else None)
-    split_ready = None
-    if for_backward and bg_plan is not None and act_fw is None:
-        act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan)
-        if K4_MODE == "background":
+    split_ready = x_in_ready = None
+    plan_out = plan
+    want_split = for_backward and cfg.backward_mode != "dense" and act_fw is None
+
+    def fwd_out(st):
+        _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
+                  ptr(inv_dev), 0, -1, None, st)
+
+    if side is not None:
+        main = torch.cuda.current_stream()
+        side.wait_stream(main)  # K1's outputs are ready; the side work must not wait for fwd.out
+        fwd_out(s)
+        if need_plan and plan_out is None:
+            plan_out = partition_features(counts, cfg.split_ratio, launch_stream=side)
+        bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
+        if want_split:
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan)
+        with torch.cuda.stream(side):
+            if SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
+                _fill_frame_rows(x_in, x, inv_dev)
+            if want_split:
+                run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True)  # relu^2: >= 0
+            ev = torch.cuda.Event()
+            ev.record(side)
+        split_ready = x_in_ready = ev
+        if not SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
+            _fill_frame_rows(x_in, x, inv_dev)
+        _used_on(side, x, x_in, act_vals, act_meta, counts, inv_dev)
+        if need_plan and plan is None:
+            _used_on(side, plan_out.sparse_features, plan_out.dense_features, plan_out.feat_pos)
+        if act_split is not None:
+            _used_on(side, act_split.vs, act_split.es, act_split.vd)
+    else:
+        if need_plan and plan_out is None:
+            plan_out = partition_features(counts, cfg.split_ratio)
+        if x_in is not None and x_in is not x and k1_in is not x_in:
+            _fill_frame_rows(x_in, x, inv_dev)
+        bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
+        if want_split:
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan)
+        if want_split and K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16,
                       d, ptr(inv_dev), 0, -1, None,
                       *k4_job_args(act_vals, act_meta, npad, h, bg_plan, act_split, counter), s)
         else:
-            split_ready = _spmm_with_split(
-                lambda st: _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out),
-                                     _lib.BF16, d, ptr(inv_dev), 0, -1, None, st),
-                act_split, act_vals, act_meta, npad, h, bg_plan)
-    else:
-        _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-                  ptr(inv_dev), 0, -1, None, s)
+            fwd_out(s)
+            if want_split:
+                run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True)
     census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
     cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
                      SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw, act_split=act_split,
-                     act_split_ready=split_ready)
+                     act_split_ready=split_ready, x_in_ready=x_in_ready)
     return out, cache
 
 
-def _spmm_with_split(launch_gemm, fs, vals, meta, n, h, plan):
+def _frame_rows(a: torch.Tensor, npad: int, src_rows, defer: bool = False) -> torch.Tensor:
+    """The compute-frame copy of a [n, d] input: rows permuted (out[i] =
+    a[src_rows[i]]) and zero-padded to npad rows. Returns `a` itself when
+    neither applies. defer=True only allocates (fill with _fill_frame_rows)."""
+    n = a.shape[0]
+    if src_rows is None and npad == n:
+        return a
+    out = torch.empty(npad, a.shape[1], dtype=a.dtype, device=a.device)
+    if not defer:
+        _fill_frame_rows(out, a, src_rows)
+    return out
+
+
+def _fill_frame_rows(out: torch.Tensor, a: torch.Tensor, src_rows) -> None:
+    """Fill a _frame_rows buffer on the current stream."""
+    n = a.shape[0]
+    if out.shape[0] > n:
+        out[n:].zero_()
+    if src_rows is not None:
+        gather_rows(a, src_rows, out)
+    else:
+        out[:n].copy_(a)
+
+
+def _used_on(st: torch.cuda.Stream, *tensors) -> None:
+    """Tensors allocated on the current stream but read/written by work queued
+    on `st`: keep the allocator from reusing them before that work is done."""
+    for t in tensors:
+        if isinstance(t, torch.Tensor):
+            t.record_stream(st)
+
+
+def _spmm_with_split(launch_gemm, fs, vals, meta, n, h, plan, nonneg=False):
     """Launch a sparse GEMM on the current stream and the K4 job filling `fs`
     next to it (K4_MODE "side": side stream, co-resident; "inline": after it).
     Returns the CUDA event after which `fs` is complete (None if inline)."""
     main = torch.cuda.current_stream()
     if K4_MODE != "side":
         launch_gemm(main.cuda_stream)
-        run_feature_split(fs, vals, meta, n, h, plan)
+        run_feature_split(fs, vals, meta, n, h, plan, nonneg)
         return None
     side = side_stream(vals.device)
     side.wait_stream(main)  # K4's inputs are ready; it must not wait for the GEMM
     launch_gemm(main.cuda_stream)
     with torch.cuda.stream(side):
-        run_feature_split(fs, vals, meta, n, h, plan)
+        run_feature_split(fs, vals, meta, n, h, plan, nonneg)
         ev = torch.cuda.Event()
         ev.record(side)
     return ev
+
+
+def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
+    """The feature-wise split of the cached activation (made by the forward
+    next to fwd.out when K4 runs on the side stream, else here)."""
+    if cache.act_split is None:
+        return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True)
+    if cache.act_split_ready is not None:
+        torch.cuda.current_stream().wait_event(cache.act_split_ready)
+    return cache.act_split
 
 
 def _all_sparse_plan(h: int, dev) -> SplitPlan:
@@ -378,6 +471,8 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         raise StateError("cache was produced under a different configuration")
     _unsupported(cfg)
     n = cache.n
+    if cache.x_in is None:
+        raise StateError("cache comes from an inference forward (for_backward=False)")
     d = cache.x_in.shape[1]
     g_out = as_matrix(g_out, "g_out", BF16)
     if tuple(g_out.shape) != (n, d):
@@ -396,14 +491,6 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     census: list[GemmEvent] = []
     notify = grad_ready or (lambda name, t: None)
 
-    g_c = torch.empty(npad, d, dtype=BF16, device=dev)
-    if npad > n:
-        g_c[n:].zero_()
-    if cache.inv_dev is not None:
-        gather_rows(g_out, cache.inv_dev, g_c)
-    else:
-        g_c[:n].copy_(g_out)
-
     d_w1 = torch.empty(d, h, dtype=F32, device=dev)
     d_w2 = torch.empty(h, d, dtype=F32, device=dev)
     d_x = torch.empty(n, d, dtype=BF16, device=dev)
@@ -413,9 +500,9 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         # ---------------------------------------------------------- dense twin
         act = cache.act_dense
         g_pre = torch.empty(n, h, dtype=BF16, device=dev)
-        _lib.call("s24_gemm_dact", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(act), h, ptr(g_pre), h, s)
+        _lib.call("s24_gemm_dact", ptr(g_out), d, ptr(p.w2), d, n, h, d, ptr(act), h, ptr(g_pre), h, s)
         census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
-        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, None, s)
+        _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_out), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, None, s)
         census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
         notify("d_w2", d_w2)
         _lib.call("s24_gemm", ptr(g_pre), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
@@ -437,12 +524,53 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     raw_naive = cfg.backward_mode == "naive_sparse" and not cfg.mask_grad_with_fwd
     g_fw = FusedFeatureOperand.alloc(h, npad, dev) if fused_g else None
     fw_args = g_fw.args() if g_fw is not None else (None, None, None, 0)
-    _lib.call("s24_bwd_dact_fused", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(cache.act_vals), ptr(cache.act_meta),
-              ptr(g_vals), *fw_args, s)
+    # The permuted, padded copy g_c of dY is only an operand of the weight
+    # gradients (B of dW2) and of the unmasked-derivative path, so it is
+    # gathered on the side stream while K3 reads dY as is (row map).
+    main = torch.cuda.current_stream()
+    side = side_stream(dev) if K4_MODE == "side" else None
+    g_c = _frame_rows(g_out, npad, cache.inv_dev, defer=True)
+    g_ready = None
+    rowmap = ROWMAP_GEMMS and g_fw is None
+    if g_c is not g_out:
+        if not rowmap and cache.perm_dev is not None:
+            _fill_frame_rows(g_c, g_out, cache.inv_dev)  # K3 reads g_c
+        elif side is not None and SIDE_GATHERS:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                _fill_frame_rows(g_c, g_out, cache.inv_dev)
+                g_ready = torch.cuda.Event()
+                g_ready.record(side)
+            _used_on(side, g_out, g_c)
+        elif side is None:
+            _fill_frame_rows(g_c, g_out, cache.inv_dev)
+    late_g_c = g_c is not g_out and side is not None and not SIDE_GATHERS and rowmap
+
+    def need_frame_inputs():
+        """Main-stream consumers of g_c / x_in wait for their side-stream gathers."""
+        nonlocal g_ready, late_g_c
+        if late_g_c:
+            _fill_frame_rows(g_c, g_out, cache.inv_dev)
+            late_g_c = False
+        if g_ready is not None:
+            main.wait_event(g_ready)
+            g_ready = None
+        if cache.x_in_ready is not None:
+            main.wait_event(cache.x_in_ready)
+
+    # K3 reads dY unpermuted and pairs input row r with act / g_pre row
+    # perm[r]; the fused feature-wise epilogue needs the permuted rows
+    k3_in, k3_map = g_out, cache.perm_dev
+    if not rowmap and cache.perm_dev is not None:
+        need_frame_inputs()
+        k3_in, k3_map = g_c, None
+    _lib.call("s24_bwd_dact_fused", ptr(k3_in), d, ptr(p.w2), d, n, h, d, ptr(cache.act_vals), ptr(cache.act_meta),
+              ptr(g_vals), *fw_args, ptr(k3_map), s)
     census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
     g_pre_dense = None
     if not cfg.mask_grad_with_fwd:
         # unmasked derivative: needs relu(y1) everywhere (fp32 pre-activation kept by the forward)
+        need_frame_inputs()
         G = torch.empty(n, h, dtype=F32, device=dev)
         _lib.call("s24_gemm", ptr(g_c), 0, d, ptr(p.w2), 0, d, n, h, d, ptr(G), _lib.F32, h, None, 0, -1, None, s)
         g_pre_dense = (G * act_squared_relu_grad(cache.pre_act)).to(BF16)
@@ -470,6 +598,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
                 fg, g_vals, cache.act_meta, npad, h, plan)
         ev_dx = GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d))
 
+    need_frame_inputs()
     if mode == "dense":
         act = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_decompress_token", ptr(cache.act_vals), None, ptr(cache.act_meta), n, h, ptr(act), _lib.BF16, h, s)
@@ -484,18 +613,28 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         _lib.call("s24_gemm", ptr(gp), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
+    elif (grad_ready is None and cache.act_fw is None and g_fw is None and not raw_naive
+          and PAIRED_WEIGHT_GRADS):
+        # both split weight gradients in one grouped launch: dW2 = split(act)^T g_c
+        # and dW1^T = split(g_pre)^T x_in share (M, N, K) = (|S|, d, n), so the
+        # second fills the first one's partial last wave (no per-gradient hook
+        # to serve, hence only without grad_ready)
+        fa = _act_split(cache, npad, h, plan)
+        if fg is None:
+            fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+        elif fg_ready is not None:
+            torch.cuda.current_stream().wait_event(fg_ready)
+        split_weight_grad_pair(fa, fg, plan, g_c, cache.x_in, npad, d_w2, d_w1)
+        stats_a, stats_g = fa.stats, fg.stats
+        census.append(GemmEvent("bwd.d_w2", True, macs_w))
+        census.append(GemmEvent("bwd.d_w1", True, macs_w))
     else:
         # dW2 = split(act)^T g_c  (act is already restricted to the mask)
         if cache.act_fw is not None:
             fused_weight_grad(cache.act_fw, cache.act_vals, cache.act_meta, h, plan, g_c, d_w2, transposed=False)
             stats_a = cache.act_fw.stats(plan)
         else:
-            if cache.act_split is not None:
-                fa = cache.act_split
-                if cache.act_split_ready is not None:
-                    torch.cuda.current_stream().wait_event(cache.act_split_ready)
-            else:
-                fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
+            fa = _act_split(cache, npad, h, plan)
             split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
             stats_a = fa.stats
         census.append(GemmEvent("bwd.d_w2", True, macs_w))

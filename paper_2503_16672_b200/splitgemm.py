@@ -67,10 +67,12 @@ def ceil_fraction(ratio: float, h: int) -> int:
     return math.ceil(x)
 
 
-def partition_features(counts, ratio: float) -> SplitPlan:
+def partition_features(counts, ratio: float, launch_stream=None) -> SplitPlan:
     """Stable ascending (count, index) order; the first ceil(ratio*h) features
     are sparse, both lists ascending (ref splitgemm.py:41-52). Runs on the
-    device (radix select + block scan, csrc/sparse_capi.cu k_plan)."""
+    device (radix select + block scan, csrc/sparse_capi.cu k_plan).
+    launch_stream: run the kernel there (outputs are still allocated on the
+    current stream, which must wait for launch_stream before reading them)."""
     if not 0.0 <= ratio <= 1.0:
         raise ConfigError(f"split ratio must be in [0, 1], got {ratio}")
     if isinstance(counts, np.ndarray) or not isinstance(counts, torch.Tensor):
@@ -87,7 +89,8 @@ def partition_features(counts, ratio: float) -> SplitPlan:
     if h:
         sp_buf = sp if k else torch.empty(1, dtype=torch.int32, device=dev)
         de_buf = de if h - k else torch.empty(1, dtype=torch.int32, device=dev)
-        _lib.call("s24_plan", ptr(c32), h, k, ptr(sp_buf), ptr(de_buf), ptr(pos), stream())
+        st = launch_stream.cuda_stream if launch_stream is not None else stream()
+        _lib.call("s24_plan", ptr(c32), h, k, ptr(sp_buf), ptr(de_buf), ptr(pos), st)
     return SplitPlan(h, ratio, counts, sp, de, pos)
 
 
@@ -107,18 +110,19 @@ class FeatureSplit:
 
 
 def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
-                  dense_only: bool = False, with_stats: bool = False) -> FeatureSplit:
+                  dense_only: bool = False, with_stats: bool = False, nonneg: bool = False) -> FeatureSplit:
     """K4: token-wise compressed [n, h] (vals + hw meta, n and h multiples of
     128) -> feature-wise 2:4 of the sparse features + transposed dense
     features (the apply_mask / gather / sparsify_feature_wise part of ref
     splitgemm.py:72-80, without a dense round trip). dense_only=True produces
     only the dense columns (the FFN hot path gets the sparse operand from the
-    K1/K3 epilogues)."""
+    K1/K3 epilogues). nonneg=True declares the values >= 0 and NaN-free (the
+    relu^2 activation), letting K4 rank raw values."""
     fs = alloc_feature_split(vals, meta_hw, n, h, plan, dense_only)
     ns, nd = plan.n_sparse, plan.n_dense
     cnt = torch.zeros(2, dtype=torch.int64, device=vals.device) if with_stats else None
     _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(fs.vs),
-              ptr(fs.es), ptr(fs.vd), ptr(cnt), stream())
+              ptr(fs.es), ptr(fs.vd), ptr(cnt), int(nonneg), stream())
     if with_stats:
         fs.stats = SparsifyStats(n * ns, cnt)
     return fs
@@ -142,10 +146,10 @@ def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: in
 
 
 def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int,
-                      plan: SplitPlan) -> None:
+                      plan: SplitPlan, nonneg: bool = False) -> None:
     """Fill preallocated K4 outputs on the current stream (no drop counting)."""
     _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense,
-              ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, stream())
+              ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, int(nonneg), stream())
 
 
 def side_stream(device) -> torch.cuda.Stream:
@@ -238,6 +242,34 @@ def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int
         # idle; a fixed-order reduction keeps the result deterministic
         with torch.cuda.stream(side):
             dense_remainder_gemm(fs.vd, b, n, plan, out, transposed, code, side)
+    if side is not main:
+        main.wait_stream(side)
+
+
+def split_weight_grad_pair(fa: FeatureSplit, fb: FeatureSplit, plan: SplitPlan, b_a: torch.Tensor,
+                           b_b: torch.Tensor, n: int, out_a: torch.Tensor, out_b: torch.Tensor) -> None:
+    """split_weight_grad for two operands sharing one plan and one (|S|, d, n)
+    shape: out_a[S] = sparse(fa)^T b_a (row-major [h, d]) and out_b = (sparse(fb)^T b_b)^T
+    (transposed [d, h]) in ONE grouped sparse launch, the two dense
+    remainders on the side stream next to it."""
+    d = b_a.shape[1]
+    if b_b.shape[1] != d or out_a.dtype != out_b.dtype:
+        raise DimensionError("paired weight gradients need equal widths and output dtypes")
+    code = _lib.F32 if out_a.dtype == F32 else _lib.BF16
+    main = torch.cuda.current_stream()
+    side = _side_stream(out_a.device) if plan.n_sparse and plan.n_dense else main
+    if side is not main:
+        side.wait_stream(main)
+    if plan.n_sparse:
+        sf = ptr(plan.sparse_features)
+        _lib.call("s24_spmm_pair", 1, plan.n_sparse, d, n, code,
+                  ptr(fa.vs), ptr(fa.es), ptr(b_a), b_a.stride(0), ptr(out_a), out_a.shape[1], sf, 0, None,
+                  ptr(fb.vs), ptr(fb.es), ptr(b_b), b_b.stride(0), ptr(out_b), out_b.shape[1], sf, 1, None,
+                  main.cuda_stream)
+    if plan.n_dense:
+        with torch.cuda.stream(side):
+            dense_remainder_gemm(fa.vd, b_a, n, plan, out_a, False, code, side)
+            dense_remainder_gemm(fb.vd, b_b, n, plan, out_b, True, code, side)
     if side is not main:
         main.wait_stream(side)
 

@@ -22,12 +22,12 @@ stats = torch.zeros(2, device="cuda", dtype=torch.int64)
 act = torch.empty(n, h, device="cuda", dtype=bf)
 gv = torch.empty_like(vals)
 out = torch.empty(n, d, device="cuda", dtype=bf)
-_lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, None, None, None, 0, S)
+_lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, None, None, None, 0, None, S)
 for _ in range(4):
     if which == "k1":
-        _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, None, None, None, 0, S)
+        _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(vals), P(meta), P(counts), P(stats), None, None, None, None, 0, None, S)
     elif which == "k3":
-        _lib.call("s24_bwd_dact_fused", P(x), d, P(w2), d, n, h, d, P(vals), P(meta), P(gv), None, None, None, 0, S)
+        _lib.call("s24_bwd_dact_fused", P(x), d, P(w2), d, n, h, d, P(vals), P(meta), P(gv), None, None, None, 0, None, S)
     elif which == "dact":
         _lib.call("s24_gemm_dact", P(x), d, P(w2), d, n, h, d, P(act), h, P(act), h, S)
     elif which == "relu2":

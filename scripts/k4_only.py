@@ -10,7 +10,7 @@ from paper_2503_16672_b200 import _lib  # noqa: E402
 P = lambda t: t.data_ptr()  # noqa: E731
 n, h = (int(v) for v in sys.argv[1:3]) if len(sys.argv) > 2 else (16384, 8192)
 S = torch.cuda.current_stream().cuda_stream
-a = torch.randn(n, h, device="cuda").bfloat16()
+a = torch.relu(torch.randn(n, h, device="cuda")).square().bfloat16()  # relu^2-like operand
 vals = torch.zeros(n, h // 2, device="cuda", dtype=torch.bfloat16)
 meta = torch.zeros(_lib.meta_hw_bytes(n, h), device="cuda", dtype=torch.uint8)
 _lib.call("s24_sparsify_token", P(a), 1, n, h, h, P(vals), None, P(meta), None, None, S)
@@ -25,6 +25,6 @@ es = torch.zeros(_lib.meta_hw_bytes(ks, n), device="cuda", dtype=torch.uint8)
 vd = torch.zeros((h - ks + 127) // 128 * 128, n, device="cuda", dtype=torch.bfloat16)
 st = torch.zeros(2, dtype=torch.int64, device="cuda")
 for _ in range(5):
-    _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, h - ks, P(vs), P(es), P(vd), P(st), S)
+    _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, h - ks, P(vs), P(es), P(vd), None, 1, S)  # hot-path variant: no stats
 torch.cuda.synchronize()
 print("ok")

@@ -77,10 +77,13 @@ def main():
     f = 2.0 * n * d * h
     cb1 = timeit(lambda: torch.matmul(x, w1), args.iters, flush)
     rec("K1 fwd gemm1 fused", timeit(lambda: _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(act_vals),
-                                                          P(meta), P(counts), P(stats), None, None, None, None, 0, S()), args.iters, flush),
+                                                          P(meta), P(counts), P(stats), None, None, None, None, 0, None, S()), args.iters, flush),
         f, cb1)
     rec("dense relu2 (twin of K1)", timeit(lambda: _lib.call("s24_gemm_relu2", P(x), d, P(w1), h, n, h, d, P(act), h,
                                                                 S()), args.iters, flush), f, cb1)
+    rec("dense plain store (K1 shape)", timeit(lambda: _lib.call("s24_gemm", P(x), 0, d, P(w1), 1, h, n, h, d, P(act),
+                                                                    1, h, None, 0, -1, None, S()), args.iters, flush),
+        f, cb1)
     cb2 = timeit(lambda: torch.matmul(act, w2), args.iters, flush)
     rec("K2 fwd.out sparse", timeit(lambda: _lib.call("s24_spmm", P(act_vals), P(meta), P(w2), 1, d, n, d, h, P(out),
                                                          1, d, None, 0, -1, None, S()), args.iters, flush), f, cb2)
@@ -88,7 +91,7 @@ def main():
                                                           None, 0, -1, None, S()), args.iters, flush), f, cb2)
     cb3 = timeit(lambda: torch.matmul(g, w2.t()), args.iters, flush)
     rec("K3 bwd dact fused", timeit(lambda: _lib.call("s24_bwd_dact_fused", P(g), d, P(w2), d, n, h, d, P(act_vals),
-                                                         P(meta), P(gv), None, None, None, 0, S()), args.iters, flush), f, cb3)
+                                                         P(meta), P(gv), None, None, None, 0, None, S()), args.iters, flush), f, cb3)
     rec("dense dact (twin of K3)", timeit(lambda: _lib.call("s24_gemm_dact", P(g), d, P(w2), d, n, h, d, P(act), h,
                                                                P(act), h, S()), args.iters, flush), f, cb3)
     cb4 = timeit(lambda: torch.matmul(act, w1.t()), args.iters, flush)
@@ -117,7 +120,7 @@ def main():
     vd = torch.zeros((h - kcount + 127) // 128 * 128, n, device="cuda", dtype=bf)
     k4_bytes = n * h * 1.125 + kcount * n * 1.125 + (h - kcount) * n * 2
     rec("K4 feature split", timeit(lambda: _lib.call("s24_feature_split", P(act_vals), P(meta), n, h, P(pos), kcount,
-                                                        h - kcount, P(vs), P(es), P(vd), P(stats), S()), args.iters,
+                                                        h - kcount, P(vs), P(es), P(vd), P(stats), 1, S()), args.iters,
                                     flush), 1e-9, bytes_=k4_bytes)
     src = torch.randperm(n, device="cuda").int()
     rec("K6 gather rows", timeit(lambda: _lib.call("s24_gather_rows", P(x), n, 2 * d, 2 * d, P(src), P(out), 2 * d,

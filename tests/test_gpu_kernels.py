@@ -84,6 +84,28 @@ def test_dense_gemm_bf16_out_rowmap_transposed():
     assert rel_err(Dt.t(), ref) < 1e-5
 
 
+@pytest.mark.parametrize("transposed", [0, 1])
+@pytest.mark.parametrize("out_dt", [F32, BF16])
+def test_gemm_splitk_rowmap(transposed, out_dt):
+    """Split-K (fixed-order reduction, row map, optional transposed write) vs
+    the fp32 product; the dense-remainder path of the split weight gradient."""
+    torch.manual_seed(11)
+    M, N, K, ks = 300, 256, 4096, 8
+    A = torch.randn(M, K, device="cuda").bfloat16()   # stored MN-major, like vd
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    rows = M + 60
+    rmap = torch.randperm(rows, device="cuda")[:M].int()
+    ref = torch.zeros(rows, N, device="cuda")
+    ref[rmap.long()] = A.float() @ B.float()
+    dt = torch.float32 if out_dt == F32 else torch.bfloat16
+    D = torch.zeros((N, rows) if transposed else (rows, N), device="cuda", dtype=dt)
+    ws = torch.empty(ks, M, N, device="cuda")
+    _lib.call("s24_gemm_splitk", P(A), 0, K, P(B), 1, N, M, N, K, ks, P(ws), P(D), out_dt, D.shape[1], P(rmap),
+              transposed, S())
+    got = D.float().t() if transposed else D.float()
+    assert rel_err(got, ref) < (1e-5 if out_dt == F32 else 4e-3)
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_sparsify_token_matches_oracle(dtype):
     rng = np.random.Generator(np.random.PCG64(3))
@@ -114,6 +136,29 @@ def test_spmm_vs_decompressed(b_mn, M, N, K):
     _lib.call("s24_spmm", P(vals), P(meta_hw), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, None, S())
     ref = dense @ B.float()
     assert rel_err(D, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 512), (600, 384, 1024)])
+def test_spmm_pair_matches_two_launches(M, N, K):
+    """The grouped launch (two problems, one tile schedule) is bit-identical to
+    two s24_spmm calls, including row maps and the transposed write."""
+    torch.manual_seed(7)
+    ops = []
+    for _ in range(2):
+        a = torch.randn(M, K, device="cuda").bfloat16()
+        vals, _, meta_hw, _, _ = gpu_sparsify_token(a)
+        ops.append((vals, meta_hw, torch.randn(K, N, device="cuda").bfloat16()))
+    rmap = torch.randperm(M + 40, device="cuda")[:M].int()
+    ref0 = torch.zeros(M + 40, N, device="cuda")
+    ref1 = torch.zeros(N, M + 40, device="cuda")
+    (v0, e0, b0), (v1, e1, b1) = ops
+    _lib.call("s24_spmm", P(v0), P(e0), P(b0), 1, N, M, N, K, P(ref0), F32, N, P(rmap), 0, -1, None, S())
+    _lib.call("s24_spmm", P(v1), P(e1), P(b1), 1, N, M, N, K, P(ref1), F32, M + 40, P(rmap), 1, -1, None, S())
+    out0, out1 = torch.zeros_like(ref0), torch.zeros_like(ref1)
+    _lib.call("s24_spmm_pair", 1, M, N, K, F32, P(v0), P(e0), P(b0), N, P(out0), N, P(rmap), 0, None,
+              P(v1), P(e1), P(b1), N, P(out1), M + 40, P(rmap), 1, None, S())
+    assert torch.equal(out0, ref0) and torch.equal(out1, ref1)
+    assert out0.abs().sum() > 0 and out1.abs().sum() > 0
 
 
 def test_decompress_roundtrip():
@@ -179,7 +224,7 @@ def test_plan_matches_oracle(h, ratio, hi):
     assert np.array_equal(-p[ode] - 1, np.arange(h - k))
 
 
-def _k1(x, w1, with_counts=True):
+def _k1(x, w1, with_counts=True, row_map=None):
     M, K = x.shape
     N = w1.shape[1]
     mp = (M + 127) // 128 * 128
@@ -189,8 +234,30 @@ def _k1(x, w1, with_counts=True):
     stats = torch.zeros(2, dtype=torch.int64, device="cuda")
     y = torch.empty(M, N, device="cuda")
     _lib.call("s24_fwd_gemm1_fused", P(x), K, P(w1), N, M, N, K, P(vals), P(meta), P(counts) if with_counts else None,
-              P(stats), P(y), None, None, None, 0, S())
+              P(stats), P(y), None, None, None, 0, P(row_map), S())
     return vals, meta, counts, stats, y
+
+
+@pytest.mark.parametrize("M", [512, 300])
+def test_k1_k3_row_map_equals_gathered_input(M):
+    """The token permutation applied in the K1 / K3 epilogues (row map) is
+    bit-identical to gathering the rows first (ref matcore.py:291-296)."""
+    N, K = 512, 256
+    x, w1, w2, dy = O.synthetic_ffn_inputs(M, K, N, sparsity=0.85, seed=3)
+    tx, tw1, tw2, tg = (torch.from_numpy(t).cuda().bfloat16() for t in (x, w1, w2, dy))
+    perm = torch.from_numpy(O.make_permutation(5, M).astype(np.int32)).cuda()
+    inv = torch.empty_like(perm)
+    inv[perm.long()] = torch.arange(M, dtype=torch.int32, device="cuda")
+    xg, gg = tx[inv.long()], tg[inv.long()]  # x_in[perm[r]] = x[r]
+    v0, m0, c0, s0, y0 = _k1(xg, tw1)
+    v1, m1, c1, s1, y1 = _k1(tx, tw1, row_map=perm)
+    assert torch.equal(v0, v1) and torch.equal(m0, m1) and torch.equal(c0, c1) and torch.equal(s0, s1)
+    assert torch.equal(y0, y1)
+    g0, g1 = torch.zeros_like(v0), torch.zeros_like(v0)
+    _lib.call("s24_bwd_dact_fused", P(gg), K, P(tw2), K, M, N, K, P(v0), P(m0), P(g0), None, None, None, 0, None, S())
+    _lib.call("s24_bwd_dact_fused", P(tg), K, P(tw2), K, M, N, K, P(v0), P(m0), P(g1), None, None, None, 0, P(perm),
+              S())
+    assert torch.equal(g0, g1) and g0.abs().sum() > 0
 
 
 @pytest.mark.parametrize("M,N,K", [(256, 512, 128), (4096, 2048, 512), (200, 256, 64)])
@@ -216,7 +283,7 @@ def test_bwd_dact_fused(M, N, K):
     tx, tw1, tw2, tg = (torch.from_numpy(t).cuda().bfloat16() for t in (x, w1, w2, dy))
     vals, meta, _, _, y = _k1(tx, tw1, with_counts=False)
     gv = torch.zeros_like(vals)
-    _lib.call("s24_bwd_dact_fused", P(tg), K, P(tw2), K, M, N, K, P(vals), P(meta), P(gv), None, None, None, 0, S())
+    _lib.call("s24_bwd_dact_fused", P(tg), K, P(tw2), K, M, N, K, P(vals), P(meta), P(gv), None, None, None, 0, None, S())
     G = tg.float() @ tw2.float().t()  # [M, N]
     mref = meta_hw_to_ref(meta, M, N).long()  # [M, N/4, 2]
     Gk = torch.gather(G.view(M, N // 4, 4), 2, mref)  # [M, N/4, 2]
@@ -225,10 +292,15 @@ def test_bwd_dact_fused(M, N, K):
     assert rel_err(gv[:M].float().view(M, N // 4, 2), expect) < 5e-3
 
 
-def test_feature_split_matches_oracle():
+@pytest.mark.parametrize("nonneg", [0, 1])
+def test_feature_split_matches_oracle(nonneg):
+    """K4 against the oracle; nonneg=1 (raw-value ranking for relu^2 operands)
+    on a non-negative operand with many ties must give the identical split."""
     n, h = 512, 384
     rng = np.random.Generator(np.random.PCG64(9))
     a = O.bf16_round(((rng.random((n, h)) < 0.25) * rng.standard_normal((n, h))).astype(np.float32))
+    if nonneg:
+        a = O.bf16_round(np.round(a * a * 4) / 4)  # >= 0, coarse values -> frequent ties
     ta = torch.from_numpy(a).cuda().bfloat16()
     vals, meta_ref, meta_hw, mask, _ = gpu_sparsify_token(ta)
     am = a * mask.cpu().numpy().astype(np.float32)
@@ -245,7 +317,8 @@ def test_feature_split_matches_oracle():
     es = torch.zeros(_lib.meta_hw_bytes(sp_pad, n), dtype=torch.uint8, device="cuda")
     vd = torch.full((d_pad, n), 7.0, dtype=torch.bfloat16, device="cuda")
     stats = torch.zeros(2, dtype=torch.int64, device="cuda")
-    _lib.call("s24_feature_split", P(vals), P(meta_hw), n, h, P(tpos), ks, h - ks, P(vs), P(es), P(vd), P(stats), S())
+    _lib.call("s24_feature_split", P(vals), P(meta_hw), n, h, P(tpos), ks, h - ks, P(vs), P(es), P(vd), P(stats), nonneg,
+              S())
     ov, om, _, ost = O.sparsify_feature(np.ascontiguousarray(am[:, osp]))
     got_meta = meta_hw_to_ref(es, sp_pad, n).cpu().numpy()  # [sp_pad, n/4, 2]
     assert np.array_equal(got_meta[:ks].transpose(1, 0, 2), om)
