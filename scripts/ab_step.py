@@ -24,6 +24,7 @@ VARIANTS = {
     "k4_inline": {"K4_MODE": "inline"},
     "main_gathers": {"SIDE_GATHERS": False},
     "rowmap": {"ROWMAP_GEMMS": True},
+    "graph": {"_graph": True},
 }
 
 
@@ -44,22 +45,34 @@ def main():
     cfgs = [(nm, s24.RECIPE) for nm in names]
     if args.dense:
         cfgs.append(("dense_twin", s24.FfnConfig()))
-    base = {k: getattr(F, k) for v in VARIANTS.values() for k in v}
+        cfgs.append(("dense_graph", s24.FfnConfig()))
+        VARIANTS["dense_graph"] = {"_graph": True}
+    base = {k: getattr(F, k) for v in VARIANTS.values() for k in v if not k.startswith("_")}
 
     def apply(nm):
         for k, v in base.items():
             setattr(F, k, v)
         for k, v in VARIANTS.get(nm, {}).items():
-            setattr(F, k, v)
+            if not k.startswith("_"):
+                setattr(F, k, v)
 
-    def step(cfg):
+    graphs = {}
+
+    def step(cfg, nm=None):
+        if VARIANTS.get(nm, {}).get("_graph"):
+            if nm not in graphs:
+                graphs[nm] = s24.FfnStepGraph(p, cfg, n)
+                graphs[nm].x.copy_(x)
+                graphs[nm].dy.copy_(dy)
+            graphs[nm].replay()
+            return
         out, cache = s24.ffn_forward(x, p, cfg)
         s24.ffn_backward(dy, cache, p, cfg)
 
     for nm, cfg in cfgs:
         apply(nm)
         for _ in range(3):
-            step(cfg)
+            step(cfg, nm)
     torch.cuda.synchronize()
     res = {nm: [] for nm, _ in cfgs}
     clk = {nm: [] for nm, _ in cfgs}
@@ -74,7 +87,7 @@ def main():
                 flush.zero_()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
-                step(cfg)
+                step(cfg, nm)
                 e.record()
                 evs.append((s, e))
             torch.cuda.synchronize()

@@ -209,3 +209,26 @@ def test_sparse_api_functions_match_oracle():
     out = s24.split_gemm_t(a, mask, bt, plan)
     ref, _ = O.split_gemm_t(a, omask, bt, osp, ode, ordered=False)
     assert rel(out.cpu(), ref) < 1e-5
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_graph_replay_equals_eager(dense):
+    """FfnStepGraph (the whole fwd+bwd captured as one CUDA graph, side-stream
+    fork/join included) reproduces the eager step bit for bit, and picks up
+    new inputs written into its static buffers."""
+    n, d, h = 512, 256, 512
+    cfg = s24.FfnConfig() if dense else s24.RECIPE
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.9, seed=21)
+    x2, _, _, dy2 = O.synthetic_ffn_inputs(n, d, h, sparsity=0.9, seed=22)
+    p = s24.FfnParams(w1=w1, w2=w2)
+    g = s24.FfnStepGraph(p, cfg, n)
+    for xx, gg in ((x, dy), (x2, dy2)):
+        tx, tg = torch.from_numpy(xx).cuda().bfloat16(), torch.from_numpy(gg).cuda().bfloat16()
+        out, cache = s24.ffn_forward(tx, p, cfg)
+        gr = s24.ffn_backward(tg, cache, p, cfg)
+        g.x.copy_(tx)
+        g.dy.copy_(tg)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(g.out, out)
+        assert torch.equal(g.d_x, gr.d_x) and torch.equal(g.d_w1, gr.d_w1) and torch.equal(g.d_w2, gr.d_w2)
