@@ -54,6 +54,7 @@ struct GemmShape {
   int k_splits;         // >1: split-K, work unit = (tile, K range); partials go to the epilogue with ks
   int groups;           // 1 or 2 problems of this shape (second: tmA2/tmB2/tmE2, ep2), group-major units
   int has_bg;           // 1: epilogue warps run K4 units (bg) while waiting for accumulators
+  int a_stream;         // 1: A panels are not re-read after their raster group (L2 evict-first)
   int* sched;           // dynamic tile scheduler {next, done} (zero at launch, reset by the
                         // last cluster), or nullptr: static round-robin units
   K4Job bg;
@@ -122,12 +123,23 @@ __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, 
 }
 
 template <int CG>
-__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                         uint64_t pol) {
   if constexpr (CG == 2)
-    tma_load_2d_cg2(dst, map, bar, c0, c1);
+    tma_load_2d_cg2_hint(dst, map, bar, c0, c1, pol);
   else
-    tma_load_2d(dst, map, bar, c0, c1);
+    tma_load_2d_hint(dst, map, bar, c0, c1, pol);
 }
+
+// L2 policy of the operand loads. B (the weights / the other activation) is
+// re-read by every tile row: evict-last. When one wave of clusters covers a
+// whole raster group (shape.a_stream), the A panel of a tile row is consumed
+// by the clusters sweeping that row's N tiles at about the same time and then
+// never again: evict-first, so streaming A does not push B out of L2.
+// S24_L2_POLICY=0 disables both (experiments).
+#ifndef S24_L2_POLICY
+#define S24_L2_POLICY 1
+#endif
 
 // Epilogue contract: each epilogue warp owns one TMEM lane quarter (32 tile
 // rows) and a run of CPW consecutive 32-column chunks. Per chunk:
@@ -250,6 +262,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pol_a =
+          (S24_L2_POLICY == 1 && shape.a_stream) ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t pol_b = S24_L2_POLICY == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
       uint16_t mc_mask = 0;  // this CTA and its counterparts in the other pairs
 #pragma unroll
       for (int p = 0; p < MC; ++p) mc_mask |= static_cast<uint16_t>(1u << (p * CG + rank));
@@ -311,15 +326,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             mbar_arrive_remote(&full_bar[stage], leader_rank);
           auto load_b = [&](void* dst, int c0, int c1) {
             if constexpr (MC == 1)
-              tma_load<CG>(dst, mapB, &full_bar[stage], c0, c1);
+              tma_load<CG>(dst, mapB, &full_bar[stage], c0, c1, pol_b);
             else
-              tma_load_2d_cg2_mc(dst, mapB, &full_bar[stage], c0, c1, mc_mask);
+              tma_load_2d_cg2_mc_hint(dst, mapB, &full_bar[stage], c0, c1, mc_mask, pol_b);
           };
           if constexpr (Cfg::A_MN) {
-            tma_load<CG>(sa, mapA, &full_bar[stage], m0, kb * Cfg::BK);
-            tma_load<CG>(sa + Cfg::A_BYTES / 2, mapA, &full_bar[stage], m0 + 64, kb * Cfg::BK);
+            tma_load<CG>(sa, mapA, &full_bar[stage], m0, kb * Cfg::BK, pol_a);
+            tma_load<CG>(sa + Cfg::A_BYTES / 2, mapA, &full_bar[stage], m0 + 64, kb * Cfg::BK, pol_a);
           } else {
-            tma_load<CG>(sa, mapA, &full_bar[stage], kb * Cfg::A_COLS, m0);
+            tma_load<CG>(sa, mapA, &full_bar[stage], kb * Cfg::A_COLS, m0, pol_a);
           }
           // B boxes: with MC pairs, pair p fetches every MC-th box (or row
           // slice) and multicasts it to the same slot of all pairs
@@ -340,7 +355,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
               load_b(sb + j * (Cfg::BN_CTA * 128) + r0 * 128, kb * Cfg::BK + 64 * j, n0 + r0);
           }
           if constexpr (Cfg::SPARSE)
-            tma_load<CG>(sb + Cfg::B_BYTES, mapE, &full_bar[stage], 0, (atom_row * num_kb_all + kb) * 16);
+            tma_load<CG>(sb + Cfg::B_BYTES, mapE, &full_bar[stage], 0, (atom_row * num_kb_all + kb) * 16, pol_a);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;

@@ -205,6 +205,19 @@ class FfnCache:
     act_split_ready: object = None  # CUDA event after which act_split is complete (side-stream K4)
     x_in_ready: object = None  # CUDA event after which x_in is complete (gathered on the side stream)
 
+    # Side-stream work of the forward reads and writes tensors allocated on
+    # the main stream (no record_stream: its deferred frees stall the caching
+    # allocator). The backward joins that work before its first use; a cache
+    # dropped without a backward joins it here, so the memory is never handed
+    # to new main-stream work while the side stream still uses it.
+    def __del__(self):
+        try:
+            ev = self.act_split_ready or self.x_in_ready
+            if ev is not None and torch.cuda.is_initialized():
+                torch.cuda.current_stream(self.act_vals.device if self.act_vals is not None else None).wait_event(ev)
+        except Exception:  # interpreter shutdown
+            pass
+
     @property
     def act_sparse(self) -> Sparse24Matrix | None:
         if self.act_vals is None:
@@ -365,11 +378,6 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         split_ready = x_in_ready = ev
         if not SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
             _fill_frame_rows(x_in, x, inv_dev)
-        _used_on(side, x, x_in, act_vals, act_meta, counts, inv_dev)
-        if need_plan and plan is None:
-            _used_on(side, plan_out.sparse_features, plan_out.dense_features, plan_out.feat_pos)
-        if act_split is not None:
-            _used_on(side, act_split.vs, act_split.es, act_split.vd)
     else:
         if need_plan and plan_out is None:
             plan_out = partition_features(counts, cfg.split_ratio)
@@ -418,12 +426,7 @@ def _fill_frame_rows(out: torch.Tensor, a: torch.Tensor, src_rows) -> None:
         out[:n].copy_(a)
 
 
-def _used_on(st: torch.cuda.Stream, *tensors) -> None:
-    """Tensors allocated on the current stream but read/written by work queued
-    on `st`: keep the allocator from reusing them before that work is done."""
-    for t in tensors:
-        if isinstance(t, torch.Tensor):
-            t.record_stream(st)
+
 
 
 def _spmm_with_split(launch_gemm, fs, vals, meta, n, h, plan, nonneg=False):
@@ -541,7 +544,6 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
                 _fill_frame_rows(g_c, g_out, cache.inv_dev)
                 g_ready = torch.cuda.Event()
                 g_ready.record(side)
-            _used_on(side, g_out, g_c)
         elif side is None:
             _fill_frame_rows(g_c, g_out, cache.inv_dev)
     late_g_c = g_c is not g_out and side is not None and not SIDE_GATHERS and rowmap
