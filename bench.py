@@ -69,6 +69,19 @@ def peaks():
 # --------------------------------------------------------------------------- CPU reference (oracle port)
 
 
+def measured_traffic(label: str):
+    """DRAM bytes (read + write) per launch of a kernel, from the newest
+    committed ncu --set full capture (profiles/rNN/traffic.json), or None."""
+    for f in sorted(Path(__file__).resolve().parent.glob("profiles/r*/traffic.json"), reverse=True):
+        try:
+            t = json.loads(f.read_text()).get(label)
+        except (OSError, ValueError):
+            continue
+        if t:
+            return t["traffic_bytes"], f"{t['profile']} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
+    return None, None
+
+
 def _cpu_sample(seed: int, n: int, d: int, h: int) -> float:
     """One bounded sample of the workload on the CPU oracle (ordered-accumulation
     GEMMs, the reference's own arithmetic): returns wall seconds."""
@@ -433,9 +446,10 @@ def run_ours(args):
                         "ms_per_step": a["ms"] / args.steps, "share": a["ms"] / max(t_eager, 1e-9),
                         "achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak if peak else None})
     dom = next(k for k in kernels if "overlapped" not in k["kernel"])
+    traffic, traffic_src = measured_traffic(dom["kernel"])
     result["roofline"] = {"kernel": dom["kernel"], "bound": "hbm" if dom["unit"] == "GB/s" else "tensor",
                           "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-                          "frac": dom["frac"], "traffic": None,
+                          "frac": dom["frac"], "traffic": traffic, "traffic_source": traffic_src,
                           "peak_source": f"{pk['source']} (MEASURED_PEAKS.json bf16 burst / hbm copy"
                                          f"{'; 2:4 sparse peak = 2x dense, derived' if 'sparse' in dom['kernel'] or 'spmm' in dom['kernel'] else ''})"}
     result["kernels"] = kernels

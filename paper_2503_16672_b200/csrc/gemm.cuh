@@ -55,6 +55,7 @@ struct GemmShape {
   int groups;           // 1 or 2 problems of this shape (second: tmA2/tmB2/tmE2, ep2), group-major units
   int has_bg;           // 1: epilogue warps run K4 units (bg) while waiting for accumulators
   int a_stream;         // 1: A panels are not re-read after their raster group (L2 evict-first)
+  int b_keep;           // 1: B is small enough to pin in L2 (evict-last)
   int* sched;           // dynamic tile scheduler {next, done} (zero at launch, reset by the
                         // last cluster), or nullptr: static round-robin units
   K4Job bg;
@@ -132,7 +133,8 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 }
 
 // L2 policy of the operand loads. B (the weights / the other activation) is
-// re-read by every tile row: evict-last. When one wave of clusters covers a
+// re-read by every tile row: evict-last when it fits comfortably in L2
+// (shape.b_keep; a 64 MiB activation B thrashes instead). When one wave of clusters covers a
 // whole raster group (shape.a_stream), the A panel of a tile row is consumed
 // by the clusters sweeping that row's N tiles at about the same time and then
 // never again: evict-first, so streaming A does not push B out of L2.
@@ -264,7 +266,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       uint32_t phase = 0;
       const uint64_t pol_a =
           (S24_L2_POLICY == 1 && shape.a_stream) ? l2_policy_evict_first() : l2_policy_evict_normal();
-      const uint64_t pol_b = S24_L2_POLICY == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+      const uint64_t pol_b =
+          (S24_L2_POLICY == 1 && shape.b_keep) ? l2_policy_evict_last() : l2_policy_evict_normal();
       uint16_t mc_mask = 0;  // this CTA and its counterparts in the other pairs
 #pragma unroll
       for (int p = 0; p < MC; ++p) mc_mask |= static_cast<uint16_t>(1u << (p * CG + rank));

@@ -207,7 +207,11 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   });
   if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   const int clusters = tiles < max_clusters ? tiles : max_clusters;
-  sh.a_stream = sh.group_m * sh.tiles_n <= clusters;
+  // L2 policies (see gemm.cuh): pin B when it fits, and only then let the
+  // A panels stream through (measured: with a 64 MiB B, evict-first A panels
+  // are lost before all N tiles of their row have read them)
+  sh.b_keep = static_cast<long long>(K) * N * 2 * sh.groups <= (40ll << 20);
+  sh.a_stream = sh.b_keep && sh.group_m * sh.tiles_n <= clusters;
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CLUSTER));
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, ma2, mb2, me2, sh, ep, second ? second->ep : ep);
   if (e != cudaSuccess) return fail(S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
