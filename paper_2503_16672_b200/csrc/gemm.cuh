@@ -41,6 +41,7 @@
 // experiment-only pipeline probes (never set in the product build):
 //   S24_PIPE_PROBE=1 : no TMA (stages are released empty) -> MMA-issue bound
 //   S24_PIPE_PROBE=2 : no MMA (stages are consumed unread) -> operand-feed bound
+//   S24_PIPE_PROBE=3 : no TMEM reads in the epilogue (accumulator drain cost)
 #ifndef S24_PIPE_PROBE
 #define S24_PIPE_PROBE 0
 #endif
@@ -92,7 +93,9 @@ struct GemmCfg {
   static_assert(CG == 1 || CG == 2, "CG");
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int SCHED_SLOTS = 4;  // work-unit broadcast ring (dynamic scheduler)
-  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20 + 1024;
+  // the dynamic smem base is declared 1024-aligned (SWIZZLE_128B atoms), so no
+  // alignment slack is reserved: 7 dense stages fit next to a 2 KB static LUT
+  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20;
   static constexpr uint32_t IDESC = make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
@@ -159,9 +162,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 const GemmShape shape, const typename Epi::Params ep, const typename Epi::Params ep2) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   constexpr int CG = Cfg::CG;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw_u32 = smem_u32(smem_raw);
-  uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();  // the layout below relies on it
+  uint8_t* smem = smem_raw;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
@@ -459,17 +462,24 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     Epi::init(ep, st);
     // optional background job: K4 warp units taken from a global queue while
     // this warp would otherwise sit waiting for an accumulator
-    bool bg_more = shape.has_bg != 0;
-    const uint2* bg_lut = bg_more ? k4_lut_init() : nullptr;
+    // (sparse configurations only: the job's LUT costs dense kernels 2 KB of
+    // static shared memory, i.e. a pipeline stage)
+    bool bg_more = Cfg::SPARSE && shape.has_bg != 0;
+    const uint2* bg_lut = nullptr;
+    if constexpr (Cfg::SPARSE) bg_lut = bg_more ? k4_lut_init() : nullptr;
     auto bg_unit = [&]() -> bool {
-      int u = 0;
-      if (lane == 0) u = atomicAdd(shape.bg.counter, 1);
-      u = __shfl_sync(0xffffffffu, u, 0);
-      if (u >= shape.bg.units) return false;
-      int t0, fb;
-      k4_unit_coords(shape.bg.a, u, t0, fb);
-      k4_warp_unit<false>(shape.bg.a, t0, fb, static_cast<int>(lane), bg_lut);
-      return true;
+      if constexpr (Cfg::SPARSE) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(shape.bg.counter, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= shape.bg.units) return false;
+        int t0, fb;
+        k4_unit_coords(shape.bg.a, u, t0, fb);
+        k4_warp_unit<false>(shape.bg.a, t0, fb, static_cast<int>(lane), bg_lut);
+        return true;
+      } else {
+        return false;
+      }
     };
     for (int iter = 0;; ++iter) {
       const int t = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
@@ -512,8 +522,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const int col0 = nb * Cfg::BN + c * 32;
         uint32_t r[32];
         if (col0 < shape.N) {  // uniform across the warp
-          tmem_ld32(t_row + c * 32, r);
-          tmem_ld_wait();
+          if constexpr (S24_PIPE_PROBE == 3) {  // experiment: no accumulator reads
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = static_cast<uint32_t>(i + c) * 0x3F800000u;
+          } else {
+            tmem_ld32(t_row + c * 32, r);
+            tmem_ld_wait();
+          }
         }
         if (owner && ci == 0) {
           tc_fence_before();

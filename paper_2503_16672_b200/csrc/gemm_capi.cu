@@ -158,7 +158,13 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   // work units cover MC vertically adjacent tiles (one per CTA pair)
   sh.tiles_m = static_cast<int>((M + Cfg::TILE_M * Cfg::MC - 1) / (Cfg::TILE_M * Cfg::MC));
   sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
-  sh.group_m = 16 / Cfg::CLUSTER;
+  // raster: groups of 512 rows sweep N (measured best for the 2:4 GEMMs,
+  // neutral for the dense ones; 2048-row groups cost up to 10%)
+  sh.group_m = Cfg::CLUSTER >= 4 ? 1 : 4 / Cfg::CLUSTER;
+  if (const char* g = std::getenv("S24_GROUP_M")) {  // experiments: raster group height in tiles
+    const int v = std::atoi(g);
+    if (v > 0) sh.group_m = v;
+  }
   sh.k_splits = k_splits < 1 ? 1 : k_splits;
   sh.groups = second ? 2 : 1;
   sh.sched = nullptr;
@@ -223,10 +229,13 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
 #ifndef S24_DENSE_MC
 #define S24_DENSE_MC 1
 #endif
-using DenseKN = GemmCfg<false, false, true, 256, 6, 2, 8, S24_DENSE_MC>;   // A K-major, B MN-major
-using DenseKK = GemmCfg<false, false, false, 256, 6, 2, 8, S24_DENSE_MC>;  // A K-major, B K-major
-using DenseMM = GemmCfg<false, true, true, 256, 6, 2, 8, S24_DENSE_MC>;    // A MN-major, B MN-major
-using DenseMK = GemmCfg<false, true, false, 256, 6, 2, 8, S24_DENSE_MC>;   // A MN-major, B K-major
+#ifndef S24_DENSE_STAGES
+#define S24_DENSE_STAGES 6
+#endif
+using DenseKN = GemmCfg<false, false, true, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;   // A K-major, B MN-major
+using DenseKK = GemmCfg<false, false, false, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;  // A K-major, B K-major
+using DenseMM = GemmCfg<false, true, true, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;    // A MN-major, B MN-major
+using DenseMK = GemmCfg<false, true, false, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;   // A MN-major, B K-major
 // sparse: light epilogue, 4 epilogue warps and <= 128 registers/thread, leaving
 // room for a co-resident side-stream kernel (the feature-wise split K4)
 // (S24_SPARSE_MC = CTA pairs per cluster sharing B by TMA multicast)
