@@ -128,10 +128,16 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
  * features are produced (the sparse ones come from the fused epilogues).
  * operand_nonneg = 1 declares the values >= 0 and NaN-free (the relu^2
  * activation): the feature-wise top-2 then ranks raw values (same result,
- * fewer instructions); 0 ranks magnitudes with NaN last (any operand). */
+ * fewer instructions); 0 ranks magnitudes with NaN last (any operand).
+ * pair_rows = 2 * n_dense selects the paired layout: no vd; vs rows
+ * [0, pair_rows) hold dense feature r as the two fixed-selector 2:4 rows
+ * 2r (tokens 4j, 4j+1) and 2r+1 (tokens 4j+2, 4j+3), and the sparse feature
+ * of rank s is row pair_rows + s (vs holds pad128(pair_rows + n_sparse) rows).
+ * A 2:4 GEMM with the same pair_rows then yields the whole split product.
+ * pair_rows = -1: dense features go to vd. */
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
-                      unsigned long long* stats, int operand_nonneg, void* stream);
+                      unsigned long long* stats, int operand_nonneg, int64_t pair_rows, void* stream);
 
 /* ---------------------------------------------------------------- GEMMs
  * Operand conventions: A is logically [M, K], B is logically [K, N].
@@ -157,10 +163,12 @@ int s24_gemm_splitk(const void* A, int a_mn_major, int64_t lda, const void* B, i
 /* 2:4 sparse A (token-wise along K): a_vals bf16 [M_pad128, K/2] + a_meta hw
  * (rows M_pad128, K). K % 128 == 0. Replaces sp_gemm (sparse24.py:170-192)
  * and, with the feature-wise operand from s24_feature_split, sp_gemm_t
- * (sparse24.py:195-216). */
+ * (sparse24.py:195-216). pair_rows (even, usually 0): rows below it come in
+ * (even, odd) pairs whose sum is written as the even row (row map of the
+ * even row) -- the paired dense features of s24_feature_split. */
 int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-             int64_t d_rows_valid, const int* d_row_valid, void* stream);
+             int64_t d_rows_valid, const int* d_row_valid, int64_t pair_rows, void* stream);
 
 /* Two s24_spmm problems of identical (M, N, K) and output dtype in ONE
  * persistent launch (group-major work units): the two split weight gradients
@@ -171,7 +179,7 @@ int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype
                   const uint8_t* a_meta0, const void* B0, int64_t ldb0, void* D0, int64_t ldd0, const int* d_row_map0,
                   int d_transposed0, const int* d_row_valid0, const void* a_vals1, const uint8_t* a_meta1,
                   const void* B1, int64_t ldb1, void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1,
-                  const int* d_row_valid1, void* stream);
+                  const int* d_row_valid1, int64_t pair_rows, void* stream);
 
 /* s24_spmm plus a feature-wise split (the K4 job of s24_feature_split with
  * stats == NULL) run as background work by the GEMM's epilogue warps while

@@ -72,6 +72,8 @@ struct EpiStore {
     int n_rows_valid;    // rows >= this are padding (skip)
     const int* row_valid;  // nullable: skip rows with row_valid[row] < 0
     long long split_stride;  // split-K: partial of split ks goes to out + ks * split_stride
+    int pair_rows;           // rows < pair_rows come in (even, odd) pairs: their sum is the even row's
+                             // output (a dense feature stored as two 2:4 rows, see k4.cuh)
   };
   struct State {
     long long split_off;
@@ -83,7 +85,20 @@ struct EpiStore {
   }
   __device__ static void finish(const Params&, State&, uint32_t) {}
   __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int,
-                               const float (&v)[32], uint32_t) {
+                               const float (&v_in)[32], uint32_t lane) {
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = v_in[i];
+    // (warp-uniform test: every lane of the warp calls chunk)
+    if (__any_sync(0xffffffffu, row < p.pair_rows)) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float o = __shfl_down_sync(0xffffffffu, v[i], 1);
+        if (row < p.pair_rows) v[i] += o;
+      }
+      if (row < p.pair_rows && (row & 1)) return;  // added into the even row
+    }
+    (void)lane;
     if (!row_ok || row >= p.n_rows_valid) return;
     if (p.row_valid && p.row_valid[row] < 0) return;
     const long long r = (p.row_map ? p.row_map[row] : row);

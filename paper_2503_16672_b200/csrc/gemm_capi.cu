@@ -372,15 +372,17 @@ int s24_gemm_splitk(const void* A, int a_mn_major, int64_t lda, const void* B, i
 
 int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
              int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-             int64_t d_rows_valid, const int* d_row_valid, void* stream) {
+             int64_t d_rows_valid, const int* d_row_valid, int64_t pair_rows, void* stream) {
   int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
   if (rc) return rc;
   if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
   if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  if (pair_rows < 0 || pair_rows % 2 || pair_rows > M) return fail(S24_ERR_DIMENSION, "pair_rows must be even, <= M");
   return with_out(out_dtype, [&](auto tag) {
     using OutT = std::remove_pointer_t<decltype(tag)>;
     typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
-                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
+                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0,
+                                       static_cast<int>(pair_rows)};
     return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep,
                                            static_cast<cudaStream_t>(stream));
   });
@@ -415,20 +417,22 @@ int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype
                   const uint8_t* a_meta0, const void* B0, int64_t ldb0, void* D0, int64_t ldd0, const int* d_row_map0,
                   int d_transposed0, const int* d_row_valid0, const void* a_vals1, const uint8_t* a_meta1,
                   const void* B1, int64_t ldb1, void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1,
-                  const int* d_row_valid1, void* stream) {
+                  const int* d_row_valid1, int64_t pair_rows, void* stream) {
   int rc = check_common(M, N, K, K, 0, ldb0, b_mn_major);
   if (rc) return rc;
   if ((rc = check_common(M, N, K, K, 0, ldb1, b_mn_major))) return rc;
   if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
   if ((!d_transposed0 && ldd0 < N) || (!d_transposed1 && ldd1 < N)) return fail(S24_ERR_DIMENSION, "ldd too small");
+  if (pair_rows < 0 || pair_rows % 2 || pair_rows > M) return fail(S24_ERR_DIMENSION, "pair_rows must be even, <= M");
   return with_out(out_dtype, [&](auto tag) {
     using OutT = std::remove_pointer_t<decltype(tag)>;
     using Epi = EpiStore<OutT>;
+    const int pr = static_cast<int>(pair_rows);
     typename Epi::Params ep0{static_cast<OutT*>(D0), ldd0, d_row_map0, d_transposed0, static_cast<int>(M),
-                             d_row_valid0, 0};
+                             d_row_valid0, 0, pr};
     GemmOperands<Epi> second{a_vals1, K / 2, B1, ldb1, a_meta1,
                              typename Epi::Params{static_cast<OutT*>(D1), ldd1, d_row_map1, d_transposed1,
-                                                  static_cast<int>(M), d_row_valid1, 0}};
+                                                  static_cast<int>(M), d_row_valid1, 0, pr}};
     return dispatch_sparse<Epi>(b_mn_major, a_vals0, a_meta0, B0, ldb0, M, N, K, ep0,
                                 static_cast<cudaStream_t>(stream), nullptr, &second);
   });

@@ -45,6 +45,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 struct K4Args;
 int k4_prepare(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
-               int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd, cudaStream_t st, K4Args* out);
+               int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd, cudaStream_t st, K4Args* out,
+               int64_t pair_rows = -1);
 
 }  // namespace s24

@@ -32,7 +32,14 @@ struct K4Args {
   __nv_bfloat16* vd;          // [pad128(n_dense), n]
   unsigned long long* stats;  // += nonzeros before/after over sparse features (WITH_STATS)
   int nonneg;                 // 1: values are >= 0 and NaN-free (relu^2): rank raw values
+  int pair_rows;              // >= 0: "paired" layout (below); -1: dense features go to vd
 };
+// Paired layout (pair_rows = 2 * n_dense): vs rows [0, pair_rows) hold each
+// dense feature r as two 2:4 rows 2r, 2r+1 -- tokens 4j, 4j+1 (selector
+// nibble 0x4) and 4j+2, 4j+3 (0xE) of every group -- and the sparse feature
+// of rank s sits at row pair_rows + s. One 2:4 GEMM over all rows then
+// computes both parts; its epilogue adds each pair (exact dense dot product,
+// summed in two halves), so the split weight gradient needs no dense GEMM.
 
 // background-job descriptor for the GEMM epilogue warps
 struct K4Job {
@@ -109,13 +116,22 @@ __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase,
   // and broadcast with shuffles:
   //   sparse (pos >= 0): ofs = word offset of the feature's vs row at token t0,
   //                      mb  = byte offset of its metadata halfword for q = 0
-  //   dense  (pos <  0): ofs = 0x80000000 | uint2 offset of its vd row at t0
-  const int my_pos = lane < 16 ? feat_pos[fbase + lane] : 0;
+  //   dense  (pos <  0): ofs = 0x80000000 | uint2 offset of its vd row at t0,
+  //                      or (paired) 0x40000000 | word offset of its first vs
+  //                      row, mb as for sparse; lanes 16..31 hold the second
+  //                      row's mb of feature fbase + lane - 16
+  const int paired = a.pair_rows;
+  const int my_pos = feat_pos[fbase + (lane & 15)];
   if (vs == nullptr && !__any_sync(0xffffffffu, lane < 16 && my_pos < 0)) return;  // dense-only: no dense here
   uint32_t my_ofs = 0, my_mb = 0;
   if (my_pos >= 0) {
-    my_ofs = static_cast<uint32_t>(my_pos) * static_cast<uint32_t>(n / 4) + static_cast<uint32_t>(t0 / 4);
-    my_mb = static_cast<uint32_t>(meta_hw_halfword_offset(my_pos, t0 / 16, n));
+    const uint32_t row = static_cast<uint32_t>(my_pos + (paired > 0 ? paired : 0));
+    my_ofs = row * static_cast<uint32_t>(n / 4) + static_cast<uint32_t>(t0 / 4);
+    my_mb = static_cast<uint32_t>(meta_hw_halfword_offset(row, t0 / 16, n));
+  } else if (paired >= 0) {
+    const uint32_t row = 2u * static_cast<uint32_t>(-my_pos - 1) + (lane >= 16 ? 1u : 0u);
+    my_ofs = 0x40000000u | ((row & ~1u) * static_cast<uint32_t>(n / 4) + static_cast<uint32_t>(t0 / 4));
+    my_mb = static_cast<uint32_t>(meta_hw_halfword_offset(row, t0 / 16, n));
   } else {
     my_ofs = 0x80000000u | (static_cast<uint32_t>(-my_pos - 1) * static_cast<uint32_t>(n / 4) +
                             static_cast<uint32_t>(t0 / 4));
@@ -146,7 +162,36 @@ __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase,
   for (int k = 0; k < 8; ++k) {
     const uint32_t x0 = X[0][k], x1 = X[1][k], x2 = X[2][k], x3 = X[3][k];
     const uint32_t ofs0 = __shfl_sync(0xffffffffu, my_ofs, 2 * k), ofs1 = __shfl_sync(0xffffffffu, my_ofs, 2 * k + 1);
-    const bool sp0 = !(ofs0 & 0x80000000u), sp1 = !(ofs1 & 0x80000000u);
+    const bool sp0 = !(ofs0 & 0xC0000000u), sp1 = !(ofs1 & 0xC0000000u);
+    if (paired >= 0) {
+      // dense features as two fixed-selector 2:4 rows: (x0, x1) | 0x4, (x2, x3) | 0xE
+      const uint32_t nw = static_cast<uint32_t>(n / 4);
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const uint32_t ofs = f ? ofs1 : ofs0;
+        if (ofs & 0x40000000u) {
+          const uint32_t o = ofs & 0x3FFFFFFFu;
+          const uint32_t sel_a = f ? 0x7632u : 0x5410u;
+          vs32[o + lane] = __byte_perm(x0, x1, sel_a);
+          vs32[o + nw + lane] = __byte_perm(x2, x3, sel_a);
+        }
+      }
+      // selector halfwords: every lane takes part in the shuffles, then lanes
+      // with lane % 4 == 0 store one halfword per row and token quad
+      const uint32_t mba0 = __shfl_sync(0xffffffffu, my_mb, 2 * k), mbb0 = __shfl_sync(0xffffffffu, my_mb, 16 + 2 * k);
+      const uint32_t mba1 = __shfl_sync(0xffffffffu, my_mb, 2 * k + 1),
+                     mbb1 = __shfl_sync(0xffffffffu, my_mb, 17 + 2 * k);
+      if ((lane & 3) == 0) {
+        if (ofs0 & 0x40000000u) {
+          *reinterpret_cast<uint16_t*>(es + mba0 + q_off) = 0x4444;
+          *reinterpret_cast<uint16_t*>(es + mbb0 + q_off) = 0xEEEE;
+        }
+        if (ofs1 & 0x40000000u) {
+          *reinterpret_cast<uint16_t*>(es + mba1 + q_off) = 0x4444;
+          *reinterpret_cast<uint16_t*>(es + mbb1 + q_off) = 0xEEEE;
+        }
+      }
+    }
     if (vs != nullptr && (sp0 || sp1)) {
       uint32_t k0 = x0, k1 = x1, k2 = x2, k3 = x3;
       if constexpr (!NONNEG) {
@@ -193,8 +238,10 @@ __device__ __forceinline__ void k4_warp_unit(const K4Args& a, int t0, int fbase,
         if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + mb1 + q_off) = static_cast<uint16_t>(hw >> 16);
       }
     }
-    if (!sp0) vd64[(ofs0 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x5410), __byte_perm(x2, x3, 0x5410));
-    if (!sp1) vd64[(ofs1 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x7632), __byte_perm(x2, x3, 0x7632));
+    if (ofs0 & 0x80000000u)
+      vd64[(ofs0 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x5410), __byte_perm(x2, x3, 0x5410));
+    if (ofs1 & 0x80000000u)
+      vd64[(ofs1 & 0x7FFFFFFFu) + lane] = make_uint2(__byte_perm(x0, x1, 0x7632), __byte_perm(x2, x3, 0x7632));
   }
   if constexpr (WITH_STATS) {
     k4_warp_add(cnt_b, stats);

@@ -403,19 +403,25 @@ static int grid_for(long long work, int block) {
 // valid (0,1) selectors); shared by the standalone grid and the GEMM
 // background mode
 int k4_prepare(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
-               int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd, cudaStream_t st, K4Args* out) {
+               int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd, cudaStream_t st, K4Args* out,
+               int64_t pair_rows) {
   if (n % 128 != 0 || h % 128 != 0) return fail(S24_ERR_DIMENSION, "feature split needs n, h multiples of 128");
   if (n_sparse + n_dense != h) return fail(S24_ERR_STATE, "plan sizes do not add up to h");
   if ((vs == nullptr) != (es == nullptr)) return fail(S24_ERR_DIMENSION, "vs and es go together");
-  const int64_t sp_pad = (n_sparse + 127) / 128 * 128, d_pad = (n_dense + 127) / 128 * 128;
-  if (vs != nullptr && sp_pad > n_sparse) {
-    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vs) + n_sparse * (n / 2), 0, (sp_pad - n_sparse) * (n / 2) * 2, st);
-    cudaMemsetAsync(es + (n_sparse / 128) * (n / 128) * 2048, 0x44, (n / 128) * 2048, st);
+  const bool paired = pair_rows >= 0;
+  if (paired && (pair_rows != 2 * n_dense || vs == nullptr))
+    return fail(S24_ERR_DIMENSION, "paired layout needs pair_rows == 2 * n_dense and the sparse operand");
+  const int64_t vs_rows = (paired ? pair_rows : 0) + n_sparse;  // rows of the 2:4 operand
+  const int64_t sp_pad = (vs_rows + 127) / 128 * 128, d_pad = (n_dense + 127) / 128 * 128;
+  if (vs != nullptr && sp_pad > vs_rows) {
+    cudaMemsetAsync(static_cast<__nv_bfloat16*>(vs) + vs_rows * (n / 2), 0, (sp_pad - vs_rows) * (n / 2) * 2, st);
+    cudaMemsetAsync(es + (vs_rows / 128) * (n / 128) * 2048, 0x44, (n / 128) * 2048, st);
   }
-  if (d_pad > n_dense && vd)
+  if (!paired && d_pad > n_dense && vd)
     cudaMemsetAsync(static_cast<__nv_bfloat16*>(vd) + n_dense * n, 0, (d_pad - n_dense) * n * 2, st);
   *out = K4Args{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
-                static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd), nullptr, 0};
+                static_cast<__nv_bfloat16*>(vs), es, static_cast<__nv_bfloat16*>(vd), nullptr, 0,
+                static_cast<int>(paired ? pair_rows : -1)};
   return S24_OK;
 }
 
@@ -593,10 +599,10 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
 
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
-                      unsigned long long* stats, int operand_nonneg, void* stream) {
+                      unsigned long long* stats, int operand_nonneg, int64_t pair_rows, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   K4Args a;
-  int rc = k4_prepare(vals, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs, es, vd, st, &a);
+  int rc = k4_prepare(vals, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs, es, vd, st, &a, pair_rows);
   if (rc) return rc;
   if (n == 0 || h == 0) return S24_OK;
   a.stats = stats;

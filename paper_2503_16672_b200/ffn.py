@@ -83,6 +83,14 @@ SIDE_GATHERS = os.environ.get("S24_SIDE_GATHERS", "1") == "1"
 # K1 / K3 read x / dY unpermuted and apply the permutation as an epilogue row
 # map ("1"), or read the gathered copies x_in / g_c ("0").
 ROWMAP_GEMMS = os.environ.get("S24_ROWMAP", "0") == "1"
+# Feature-wise split in the paired layout: the dense features travel inside
+# the 2:4 weight-gradient operand as fixed-selector row pairs, so no dense
+# remainder GEMM / split-K reduction runs ("1"); "0": separate dense operand.
+PAIRED_DENSE = os.environ.get("S24_PAIRED_DENSE", "1") == "1"
+
+
+def _paired_layout() -> bool:
+    return PAIRED_DENSE and K4_MODE != "background"  # the in-GEMM K4 job writes the separate layout
 FORWARD_MODES = ("dense", "sparse24")
 BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
 
@@ -357,7 +365,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
 
     def fwd_out(st):
         _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-                  ptr(inv_dev), 0, -1, None, st)
+                  ptr(inv_dev), 0, -1, None, 0, st)
 
     if side is not None:
         main = torch.cuda.current_stream()
@@ -367,7 +375,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             plan_out = partition_features(counts, cfg.split_ratio, launch_stream=side)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan)
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, paired=_paired_layout())
         with torch.cuda.stream(side):
             if SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
                 _fill_frame_rows(x_in, x, inv_dev)
@@ -385,7 +393,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             _fill_frame_rows(x_in, x, inv_dev)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan)
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, paired=_paired_layout())
         if want_split and K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16,
@@ -452,7 +460,7 @@ def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
     """The feature-wise split of the cached activation (made by the forward
     next to fwd.out when K4 runs on the side stream, else here)."""
     if cache.act_split is None:
-        return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True)
+        return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, paired=_paired_layout())
     if cache.act_split_ready is not None:
         torch.cuda.current_stream().wait_event(cache.act_split_ready)
     return cache.act_split
@@ -587,7 +595,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     if cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None and not raw_naive:
         # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
         # as background work in its idle epilogue warps
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan)
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, paired=_paired_layout())
         if K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x),
@@ -596,7 +604,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         else:
             fg_ready = _spmm_with_split(
                 lambda st: _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h,
-                                     ptr(d_x), _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None, st),
+                                     ptr(d_x), _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None, 0, st),
                 fg, g_vals, cache.act_meta, npad, h, plan)
         ev_dx = GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d))
 
@@ -623,7 +631,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         # to serve, hence only without grad_ready)
         fa = _act_split(cache, npad, h, plan)
         if fg is None:
-            fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+            fg = feature_split(g_vals, cache.act_meta, npad, h, plan, paired=_paired_layout())
         elif fg_ready is not None:
             torch.cuda.current_stream().wait_event(fg_ready)
         split_weight_grad_pair(fa, fg, plan, g_c, cache.x_in, npad, d_w2, d_w1)
@@ -651,13 +659,13 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
             gpad[:n] = g_pre_dense
             sg, _, stats_g = sparsify_feature_wise(gpad)
             _lib.call("s24_spmm", ptr(sg.data), ptr(sg.meta_hw), ptr(cache.x_in), 1, d, h, d, npad, ptr(d_w1),
-                      _lib.F32, h, None, 1, -1, None, s)
+                      _lib.F32, h, None, 1, -1, None, 0, s)
         elif g_fw is not None:
             fused_weight_grad(g_fw, g_vals, cache.act_meta, h, plan, cache.x_in, d_w1, transposed=True)
             stats_g = g_fw.stats(plan)
         else:
             if fg is None:
-                fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+                fg = feature_split(g_vals, cache.act_meta, npad, h, plan, paired=_paired_layout())
             elif fg_ready is not None:
                 torch.cuda.current_stream().wait_event(fg_ready)
             split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
@@ -669,7 +677,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         census.append(ev_dx)
     elif cfg.mask_grad_with_fwd:
         _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
-                  ptr(cache.inv_dev), 0, -1, None, s)
+                  ptr(cache.inv_dev), 0, -1, None, 0, s)
         census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
     else:
         _lib.call("s24_gemm", ptr(g_pre_dense), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,

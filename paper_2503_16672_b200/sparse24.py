@@ -268,7 +268,7 @@ def _spmm(vals, meta_hw, m: int, k: int, b: torch.Tensor, out_dtype) -> torch.Te
         b = bp
     out = torch.empty(m, npad, dtype=out_dtype, device=b.device)
     code = _lib.F32 if out_dtype == F32 else _lib.BF16
-    _lib.call("s24_spmm", ptr(vals), ptr(meta_hw), ptr(b), 1, npad, m, npad, kpad, ptr(out), code, npad, None, 0, -1, None,
+    _lib.call("s24_spmm", ptr(vals), ptr(meta_hw), ptr(b), 1, npad, m, npad, kpad, ptr(out), code, npad, None, 0, -1, None, 0,
               stream())
     return out[:, :n] if npad != n else out
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass
+from functools import cached_property
 
 import numpy as np
 import torch
@@ -50,6 +51,12 @@ class SplitPlan:
     @property
     def n_dense(self) -> int:
         return int(self.dense_features.shape[0])
+
+    @cached_property
+    def paired_row_map(self) -> torch.Tensor:
+        """Output row of each row of a paired-layout operand: dense feature r
+        twice (rows 2r, 2r+1), then the sparse features."""
+        return torch.cat([self.dense_features.repeat_interleave(2), self.sparse_features]).to(torch.int32)
 
 
 def column_nonzero_counts(a) -> torch.Tensor:
@@ -105,51 +112,64 @@ class FeatureSplit:
 
     vs: torch.Tensor  # bf16 [pad128(n_sparse), n/2] feature-wise 2:4 values, K-major along tokens
     es: torch.Tensor  # hw metadata, rows = sparse rank, K = tokens
-    vd: torch.Tensor  # bf16 [pad128(n_dense), n] dense features, transposed
+    vd: torch.Tensor | None  # bf16 [pad128(n_dense), n] dense features, transposed (None when paired)
     stats: SparsifyStats
+    # >= 0: paired layout (csrc/k4.cuh): vs rows [0, pair_rows) are the dense
+    # features as fixed-selector 2:4 row pairs, sparse rank s is row pair_rows + s
+    pair_rows: int = -1
+
+    def rows(self, plan: "SplitPlan") -> int:
+        """Rows of the 2:4 operand vs that carry features."""
+        return max(self.pair_rows, 0) + plan.n_sparse
 
 
 def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
-                  dense_only: bool = False, with_stats: bool = False, nonneg: bool = False) -> FeatureSplit:
+                  dense_only: bool = False, with_stats: bool = False, nonneg: bool = False,
+                  paired: bool = False) -> FeatureSplit:
     """K4: token-wise compressed [n, h] (vals + hw meta, n and h multiples of
     128) -> feature-wise 2:4 of the sparse features + transposed dense
     features (the apply_mask / gather / sparsify_feature_wise part of ref
     splitgemm.py:72-80, without a dense round trip). dense_only=True produces
     only the dense columns (the FFN hot path gets the sparse operand from the
     K1/K3 epilogues). nonneg=True declares the values >= 0 and NaN-free (the
-    relu^2 activation), letting K4 rank raw values."""
-    fs = alloc_feature_split(vals, meta_hw, n, h, plan, dense_only)
+    relu^2 activation), letting K4 rank raw values. paired=True writes the
+    dense features into vs as fixed-selector 2:4 row pairs (one sparse GEMM
+    then covers the whole split product, see split_weight_grad)."""
+    fs = alloc_feature_split(vals, meta_hw, n, h, plan, dense_only, paired)
     ns, nd = plan.n_sparse, plan.n_dense
     cnt = torch.zeros(2, dtype=torch.int64, device=vals.device) if with_stats else None
     _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(fs.vs),
-              ptr(fs.es), ptr(fs.vd), ptr(cnt), int(nonneg), stream())
+              ptr(fs.es), ptr(fs.vd), ptr(cnt), int(nonneg), fs.pair_rows, stream())
     if with_stats:
         fs.stats = SparsifyStats(n * ns, cnt)
     return fs
 
 
 def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
-                        dense_only: bool = False) -> FeatureSplit:
+                        dense_only: bool = False, paired: bool = False) -> FeatureSplit:
     """Output buffers of one K4 job (filled by s24_feature_split or by a GEMM's
     background warps via s24_spmm_bg). Its drop statistics are not counted on
     the hot path -- the reference discards them (splitgemm.py:75) -- and are
     recounted on the device only if someone reads them."""
     dev = vals.device
     ns, nd = plan.n_sparse, plan.n_dense
-    vs = es = None
+    paired = paired and not dense_only
+    rows = ns + (2 * nd if paired else 0)
+    vs = es = vd = None
     if not dense_only:
-        vs = torch.empty(max(pad128(ns), 128), n // 2, dtype=BF16, device=dev)
-        es = torch.empty(_lib.meta_hw_bytes(max(ns, 1), n), dtype=torch.uint8, device=dev)
-    vd = torch.empty(max(pad128(nd), 128), n, dtype=BF16, device=dev)
+        vs = torch.empty(max(pad128(rows), 128), n // 2, dtype=BF16, device=dev)
+        es = torch.empty(_lib.meta_hw_bytes(max(rows, 1), n), dtype=torch.uint8, device=dev)
+    if not paired:
+        vd = torch.empty(max(pad128(nd), 128), n, dtype=BF16, device=dev)
     stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
-    return FeatureSplit(vs, es, vd, stats)
+    return FeatureSplit(vs, es, vd, stats, 2 * nd if paired else -1)
 
 
 def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int,
                       plan: SplitPlan, nonneg: bool = False) -> None:
     """Fill preallocated K4 outputs on the current stream (no drop counting)."""
     _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense,
-              ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, int(nonneg), stream())
+              ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, int(nonneg), fs.pair_rows, stream())
 
 
 def side_stream(device) -> torch.cuda.Stream:
@@ -215,7 +235,7 @@ def fused_weight_grad(fo: FusedFeatureOperand, tok_vals: torch.Tensor, tok_meta:
             dense_remainder_gemm(fd.vd, b, n, plan, out, transposed, code, side)
     if plan.n_sparse:
         _lib.call("s24_spmm", ptr(fo.vals), ptr(fo.meta), ptr(b), 1, b.stride(0), h, d, n, ptr(out), code, ld, None,
-                  int(transposed), h, ptr(plan.feat_pos) if plan.n_dense else None, main.cuda_stream)
+                  int(transposed), h, ptr(plan.feat_pos) if plan.n_dense else None, 0, main.cuda_stream)
     if plan.n_dense:
         main.wait_stream(side)
 
@@ -224,17 +244,24 @@ def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int
                       transposed: bool) -> None:
     """out[S] = sparse(fs)^T b, out[D] = dense(fs)^T b on tensor cores, scattered
     by feature index in the epilogue. b: bf16 [n, d] (K = tokens, MN-major).
-    transposed=True writes out as [d, h] (dW1 layout)."""
+    transposed=True writes out as [d, h] (dW1 layout). A paired-layout fs
+    (dense features as 2:4 row pairs) needs a single sparse GEMM."""
     d = b.shape[1]
     ld = out.shape[1]
     code = _lib.F32 if out.dtype == F32 else _lib.BF16
+    if fs.pair_rows >= 0:
+        rows = fs.rows(plan)
+        if rows:
+            _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), rows, d, n, ptr(out), code, ld,
+                      ptr(plan.paired_row_map), int(transposed), rows, None, fs.pair_rows, stream())
+        return
     main = torch.cuda.current_stream()
     side = _side_stream(out.device) if plan.n_sparse and plan.n_dense else main
     if side is not main:
         side.wait_stream(main)  # operands ready; the side work must not wait for the sparse GEMM
     if plan.n_sparse:
         _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), plan.n_sparse, d, n, ptr(out), code,
-                  ld, ptr(plan.sparse_features), int(transposed), plan.n_sparse, None, main.cuda_stream)
+                  ld, ptr(plan.sparse_features), int(transposed), plan.n_sparse, None, 0, main.cuda_stream)
     if plan.n_dense:
         # the thin dense remainder (~5% of the rows, K = all tokens) is split
         # along K and launched on a side stream right behind the sparse GEMM:
@@ -251,11 +278,22 @@ def split_weight_grad_pair(fa: FeatureSplit, fb: FeatureSplit, plan: SplitPlan, 
     """split_weight_grad for two operands sharing one plan and one (|S|, d, n)
     shape: out_a[S] = sparse(fa)^T b_a (row-major [h, d]) and out_b = (sparse(fb)^T b_b)^T
     (transposed [d, h]) in ONE grouped sparse launch, the two dense
-    remainders on the side stream next to it."""
+    remainders on the side stream next to it -- or, for paired-layout
+    operands, inside the same launch as 2:4 row pairs."""
     d = b_a.shape[1]
     if b_b.shape[1] != d or out_a.dtype != out_b.dtype:
         raise DimensionError("paired weight gradients need equal widths and output dtypes")
+    if fa.pair_rows != fb.pair_rows:
+        raise DimensionError("both operands must use the same (paired or separate-dense) layout")
     code = _lib.F32 if out_a.dtype == F32 else _lib.BF16
+    if fa.pair_rows >= 0:
+        rows, rm = fa.rows(plan), ptr(plan.paired_row_map)
+        if rows:
+            _lib.call("s24_spmm_pair", 1, rows, d, n, code,
+                      ptr(fa.vs), ptr(fa.es), ptr(b_a), b_a.stride(0), ptr(out_a), out_a.shape[1], rm, 0, None,
+                      ptr(fb.vs), ptr(fb.es), ptr(b_b), b_b.stride(0), ptr(out_b), out_b.shape[1], rm, 1, None,
+                      fa.pair_rows, stream())
+        return
     main = torch.cuda.current_stream()
     side = _side_stream(out_a.device) if plan.n_sparse and plan.n_dense else main
     if side is not main:
@@ -264,7 +302,7 @@ def split_weight_grad_pair(fa: FeatureSplit, fb: FeatureSplit, plan: SplitPlan, 
         sf = ptr(plan.sparse_features)
         _lib.call("s24_spmm_pair", 1, plan.n_sparse, d, n, code,
                   ptr(fa.vs), ptr(fa.es), ptr(b_a), b_a.stride(0), ptr(out_a), out_a.shape[1], sf, 0, None,
-                  ptr(fb.vs), ptr(fb.es), ptr(b_b), b_b.stride(0), ptr(out_b), out_b.shape[1], sf, 1, None,
+                  ptr(fb.vs), ptr(fb.es), ptr(b_b), b_b.stride(0), ptr(out_b), out_b.shape[1], sf, 1, None, 0,
                   main.cuda_stream)
     if plan.n_dense:
         with torch.cuda.stream(side):

@@ -33,6 +33,6 @@ for _ in range(4):
     elif which == "relu2":
         _lib.call("s24_gemm_relu2", P(x), d, P(w1), h, n, h, d, P(act), h, S)
     elif which == "spfwd":
-        _lib.call("s24_spmm", P(vals), P(meta), P(w2), 1, d, n, d, h, P(out), 1, d, None, 0, -1, None, S)
+        _lib.call("s24_spmm", P(vals), P(meta), P(w2), 1, d, n, d, h, P(out), 1, d, None, 0, -1, None, 0, S)
 torch.cuda.synchronize()
 print("ok", which)

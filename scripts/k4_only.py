@@ -25,6 +25,6 @@ es = torch.zeros(_lib.meta_hw_bytes(ks, n), device="cuda", dtype=torch.uint8)
 vd = torch.zeros((h - ks + 127) // 128 * 128, n, device="cuda", dtype=torch.bfloat16)
 st = torch.zeros(2, dtype=torch.int64, device="cuda")
 for _ in range(5):
-    _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, h - ks, P(vs), P(es), P(vd), None, 1, S)  # hot-path variant: no stats
+    _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, h - ks, P(vs), P(es), P(vd), None, 1, -1, S)  # hot-path variant: no stats
 torch.cuda.synchronize()
 print("ok")

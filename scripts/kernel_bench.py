@@ -86,7 +86,7 @@ def main():
         f, cb1)
     cb2 = timeit(lambda: torch.matmul(act, w2), args.iters, flush)
     rec("K2 fwd.out sparse", timeit(lambda: _lib.call("s24_spmm", P(act_vals), P(meta), P(w2), 1, d, n, d, h, P(out),
-                                                         1, d, None, 0, -1, None, S()), args.iters, flush), f, cb2)
+                                                         1, d, None, 0, -1, None, 0, S()), args.iters, flush), f, cb2)
     rec("fwd.out dense twin", timeit(lambda: _lib.call("s24_gemm", P(act), 0, h, P(w2), 1, d, n, d, h, P(out), 1, d,
                                                           None, 0, -1, None, S()), args.iters, flush), f, cb2)
     cb3 = timeit(lambda: torch.matmul(g, w2.t()), args.iters, flush)
@@ -96,7 +96,7 @@ def main():
                                                                P(act), h, S()), args.iters, flush), f, cb3)
     cb4 = timeit(lambda: torch.matmul(act, w1.t()), args.iters, flush)
     rec("K2 bwd.d_x sparse", timeit(lambda: _lib.call("s24_spmm", P(gv), P(meta), P(w1), 0, h, n, d, h, P(out), 1, d,
-                                                         None, 0, -1, None, S()), args.iters, flush), f, cb4)
+                                                         None, 0, -1, None, 0, S()), args.iters, flush), f, cb4)
     rec("bwd.d_x dense twin", timeit(lambda: _lib.call("s24_gemm", P(act), 0, h, P(w1), 0, h, n, d, h, P(out), 1, d,
                                                           None, 0, -1, None, S()), args.iters, flush), f, cb4)
     dw = torch.empty(h, d, device="cuda")
@@ -107,7 +107,7 @@ def main():
     vs = torch.zeros(ns, n // 2, device="cuda", dtype=bf)
     es = torch.full((_lib.meta_hw_bytes(ns, n),), 0x44, device="cuda", dtype=torch.uint8)
     rec("bwd.d_w sparse part (M=0.95h)", timeit(lambda: _lib.call("s24_spmm", P(vs), P(es), P(g), 1, d, ns, d, n,
-                                                                     P(dw), 0, d, None, 0, -1, None, S()), args.iters, flush),
+                                                                     P(dw), 0, d, None, 0, -1, None, 0, S()), args.iters, flush),
         2.0 * ns * d * n)
     # K4 split
     kcount = int(0.95 * h)
@@ -120,7 +120,7 @@ def main():
     vd = torch.zeros((h - kcount + 127) // 128 * 128, n, device="cuda", dtype=bf)
     k4_bytes = n * h * 1.125 + kcount * n * 1.125 + (h - kcount) * n * 2
     rec("K4 feature split", timeit(lambda: _lib.call("s24_feature_split", P(act_vals), P(meta), n, h, P(pos), kcount,
-                                                        h - kcount, P(vs), P(es), P(vd), P(stats), 1, S()), args.iters,
+                                                        h - kcount, P(vs), P(es), P(vd), P(stats), 1, -1, S()), args.iters,
                                     flush), 1e-9, bytes_=k4_bytes)
     src = torch.randperm(n, device="cuda").int()
     rec("K6 gather rows", timeit(lambda: _lib.call("s24_gather_rows", P(x), n, 2 * d, 2 * d, P(src), P(out), 2 * d,

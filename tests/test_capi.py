@@ -59,5 +59,5 @@ def test_argument_validation_needs_no_device(lib):
         _lib.call("s24_plan", None, 10, 11, None, None, None, None)
     assert type(e.value).__name__ == "ConfigError"
     with pytest.raises(Exception) as e:
-        _lib.call("s24_spmm", None, None, None, 1, 64, 128, 64, 100, None, 0, 64, None, 0, -1, None, None)
+        _lib.call("s24_spmm", None, None, None, 1, 64, 128, 64, 100, None, 0, 64, None, 0, -1, None, 0, None)
     assert type(e.value).__name__ == "DimensionError"

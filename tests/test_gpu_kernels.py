@@ -133,7 +133,7 @@ def test_spmm_vs_decompressed(b_mn, M, N, K):
     B = torch.randn(K, N, device="cuda").bfloat16()
     Bs = B if b_mn else B.t().contiguous()
     D = torch.empty(M, N, device="cuda")
-    _lib.call("s24_spmm", P(vals), P(meta_hw), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, None, S())
+    _lib.call("s24_spmm", P(vals), P(meta_hw), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1, None, 0, S())
     ref = dense @ B.float()
     assert rel_err(D, ref) < 1e-5
 
@@ -152,11 +152,11 @@ def test_spmm_pair_matches_two_launches(M, N, K):
     ref0 = torch.zeros(M + 40, N, device="cuda")
     ref1 = torch.zeros(N, M + 40, device="cuda")
     (v0, e0, b0), (v1, e1, b1) = ops
-    _lib.call("s24_spmm", P(v0), P(e0), P(b0), 1, N, M, N, K, P(ref0), F32, N, P(rmap), 0, -1, None, S())
-    _lib.call("s24_spmm", P(v1), P(e1), P(b1), 1, N, M, N, K, P(ref1), F32, M + 40, P(rmap), 1, -1, None, S())
+    _lib.call("s24_spmm", P(v0), P(e0), P(b0), 1, N, M, N, K, P(ref0), F32, N, P(rmap), 0, -1, None, 0, S())
+    _lib.call("s24_spmm", P(v1), P(e1), P(b1), 1, N, M, N, K, P(ref1), F32, M + 40, P(rmap), 1, -1, None, 0, S())
     out0, out1 = torch.zeros_like(ref0), torch.zeros_like(ref1)
     _lib.call("s24_spmm_pair", 1, M, N, K, F32, P(v0), P(e0), P(b0), N, P(out0), N, P(rmap), 0, None,
-              P(v1), P(e1), P(b1), N, P(out1), M + 40, P(rmap), 1, None, S())
+              P(v1), P(e1), P(b1), N, P(out1), M + 40, P(rmap), 1, None, 0, S())
     assert torch.equal(out0, ref0) and torch.equal(out1, ref1)
     assert out0.abs().sum() > 0 and out1.abs().sum() > 0
 
@@ -317,7 +317,7 @@ def test_feature_split_matches_oracle(nonneg):
     es = torch.zeros(_lib.meta_hw_bytes(sp_pad, n), dtype=torch.uint8, device="cuda")
     vd = torch.full((d_pad, n), 7.0, dtype=torch.bfloat16, device="cuda")
     stats = torch.zeros(2, dtype=torch.int64, device="cuda")
-    _lib.call("s24_feature_split", P(vals), P(meta_hw), n, h, P(tpos), ks, h - ks, P(vs), P(es), P(vd), P(stats), nonneg,
+    _lib.call("s24_feature_split", P(vals), P(meta_hw), n, h, P(tpos), ks, h - ks, P(vs), P(es), P(vd), P(stats), nonneg, -1,
               S())
     ov, om, _, ost = O.sparsify_feature(np.ascontiguousarray(am[:, osp]))
     got_meta = meta_hw_to_ref(es, sp_pad, n).cpu().numpy()  # [sp_pad, n/4, 2]
@@ -328,3 +328,67 @@ def test_feature_split_matches_oracle(nonneg):
     assert np.array_equal(vd[: h - ks].float().cpu().numpy(), am[:, ode].T)
     assert not vd[h - ks:].float().any()
     assert stats.cpu().tolist() == [ost["nonzeros_before"], ost["nonzeros_after"]]
+
+
+def test_feature_split_paired_layout():
+    """Paired layout: dense feature r -> 2:4 rows 2r (tokens 4j, 4j+1; selector
+    (0,1)) and 2r+1 (tokens 4j+2, 4j+3; selector (2,3)); sparse rank s -> row
+    2*n_dense + s, identical to the separate layout's sparse rows."""
+    n, h = 512, 384
+    rng = np.random.Generator(np.random.PCG64(19))
+    a = O.bf16_round(((rng.random((n, h)) < 0.3) * rng.standard_normal((n, h))).astype(np.float32))
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    vals, _, meta_hw, mask, _ = gpu_sparsify_token(ta)
+    am = a * mask.cpu().numpy().astype(np.float32)
+    osp, ode = O.partition(O.column_counts(am), 0.9)
+    ks, nd = len(osp), len(ode)
+    pos = np.empty(h, np.int32)
+    pos[osp] = np.arange(ks)
+    pos[ode] = -np.arange(nd) - 1
+    tpos = torch.from_numpy(pos).cuda()
+    rows = 2 * nd + ks
+    rp = (rows + 127) // 128 * 128
+    vs = torch.full((rp, n // 2), 7.0, dtype=torch.bfloat16, device="cuda")
+    es = torch.zeros(_lib.meta_hw_bytes(rp, n), dtype=torch.uint8, device="cuda")
+    _lib.call("s24_feature_split", P(vals), P(meta_hw), n, h, P(tpos), ks, nd, P(vs), P(es), None, None, 0, 2 * nd,
+              S())
+    ov, om, _, _ = O.sparsify_feature(np.ascontiguousarray(am[:, osp]))
+    got_meta = meta_hw_to_ref(es, rp, n).cpu().numpy()  # [rp, n/4, 2]
+    got_v = vs.float().cpu().numpy().reshape(rp, n // 4, 2)
+    assert np.array_equal(got_meta[2 * nd:rows].transpose(1, 0, 2), om)
+    assert np.array_equal(got_v[2 * nd:rows].transpose(1, 0, 2), ov)
+    dense = am[:, ode].T.reshape(nd, n // 4, 4)  # [nd, groups, 4 tokens]
+    assert np.array_equal(got_v[0:2 * nd:2], dense[:, :, 0:2])
+    assert np.array_equal(got_v[1:2 * nd:2], dense[:, :, 2:4])
+    assert (got_meta[0:2 * nd:2] == np.array([0, 1])).all() and (got_meta[1:2 * nd:2] == np.array([2, 3])).all()
+    assert not got_v[rows:].any()
+
+
+@pytest.mark.parametrize("transposed", [0, 1])
+def test_split_weight_grad_paired_equals_separate(transposed):
+    """The split weight gradient from the paired layout (one 2:4 GEMM, row
+    pairs summed in the epilogue) matches the separate sparse + dense GEMMs
+    and the fp32 product of the masked operand."""
+    import paper_2503_16672_b200 as s24
+    from paper_2503_16672_b200.splitgemm import feature_split, split_weight_grad
+    n, h, d = 1024, 512, 256
+    rng = np.random.Generator(np.random.PCG64(23))
+    a = O.bf16_round(((rng.random((n, h)) < 0.2) * rng.standard_normal((n, h))).astype(np.float32))
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    vals, _, meta_hw, mask, _ = gpu_sparsify_token(ta)
+    am = a * mask.cpu().numpy().astype(np.float32)
+    plan = s24.partition_features(torch.from_numpy(O.column_counts(am).astype(np.int32)).cuda(), 0.9)
+    b = torch.randn(n, d, device="cuda").bfloat16()
+    outs = []
+    for paired in (False, True):
+        fs = feature_split(vals, meta_hw, n, h, plan, paired=paired)
+        out = torch.zeros((d, h) if transposed else (h, d), device="cuda")
+        split_weight_grad(fs, plan, b, n, out, transposed=bool(transposed))
+        outs.append(out.t() if transposed else out)
+    torch.cuda.synchronize()
+    # reference: feature-wise 2:4 of the sparse features, dense features exact
+    osp, ode = O.partition(O.column_counts(am), 0.9)
+    ref, _ = O.split_gemm_t(am, mask.cpu().numpy().astype(bool), b.float().cpu().numpy(), osp, ode, ordered=False)
+    for o in outs:
+        assert rel_err(o.cpu(), torch.from_numpy(ref)) < 1e-5
+    assert rel_err(outs[1], outs[0]) < 1e-6
