@@ -135,6 +135,29 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
  * of rank s is row pair_rows + s (vs holds pad128(pair_rows + n_sparse) rows).
  * A 2:4 GEMM with the same pair_rows then yields the whole split product.
  * pair_rows = -1: dense features go to vd. */
+/* K4 for the hot path: the paired layout of s24_feature_split (pair_rows =
+ * 2 * n_dense) for one or two token-wise operands sharing meta_hw (the
+ * activation and g_pre of one FFN step; vals_b/vs_b/es_b NULL for one).
+ * Metadata, selectors and output offsets are computed once for both.
+ * a_nonneg = 1: operand a is relu^2 (>= 0, NaN-free); operand b is ranked by
+ * magnitude with NaN last. No drop statistics. */
+int s24_feature_split_x(const void* vals_a, const void* vals_b, const uint8_t* meta_hw, int64_t n, int64_t h,
+                        const int* feat_pos, int64_t n_sparse, int64_t n_dense, void* vs_a, uint8_t* es_a, void* vs_b,
+                        uint8_t* es_b, int a_nonneg, void* stream);
+
+/* K4 in the identity layout (coalesced in and out; the hot-path variant):
+ * vs bf16 [pair_pad + h, n/2] + es hw metadata (rows pair_pad + h, K = n),
+ * pair_pad = pad128(2 * n_dense). Rows [0, 2*n_dense): dense feature of rank
+ * r as two fixed-selector 2:4 rows (2r: tokens 4j, 4j+1; 2r+1: 4j+2, 4j+3);
+ * rows up to pair_pad: zero; row pair_pad + f: the feature-wise 2:4 of
+ * feature f (every feature, in index order). One s24_spmm(_pair) with
+ * pair_rows = 2*n_dense, a row map (dense rank / feature index) and
+ * row_valid (skip the padding and the dense features' identity rows) then
+ * yields the whole split product (splitgemm.py:55-81). stats as above. */
+int s24_feature_split_id(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
+                         int64_t n_dense, void* vs, uint8_t* es, unsigned long long* stats, int operand_nonneg,
+                         void* stream);
+
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
                       unsigned long long* stats, int operand_nonneg, int64_t pair_rows, void* stream);

@@ -55,6 +55,7 @@ from .splitgemm import (
     split_gemm_macs,
     split_weight_grad,
     split_weight_grad_pair,
+    run_feature_split_dual,
 )
 
 ACTIVATIONS = ("squared_relu", "swiglu")
@@ -87,10 +88,28 @@ ROWMAP_GEMMS = os.environ.get("S24_ROWMAP", "0") == "1"
 # the 2:4 weight-gradient operand as fixed-selector row pairs, so no dense
 # remainder GEMM / split-K reduction runs ("1"); "0": separate dense operand.
 PAIRED_DENSE = os.environ.get("S24_PAIRED_DENSE", "1") == "1"
+# ... and in the identity layout (coalesced K4, csrc/k4id.cuh): rows in
+# feature order after the dense pairs ("1"), or rank order ("0").
+IDENTITY_LAYOUT = os.environ.get("S24_IDENTITY_LAYOUT", "0") == "1"
+# Where the feature-wise split of act (K4) runs on the side stream: next to
+# fwd.out in the forward ("0"), or next to K3 at the start of the backward
+# ("1": K3 is tensor/epilogue-bound and leaves room for it, fwd.out is
+# operand-feed-bound).
+ACT_SPLIT_IN_BWD = os.environ.get("S24_ACT_SPLIT_IN_BWD", "0") == "1"
+# One K4 pass for the activation and g_pre together (shared metadata work),
+# next to the dX GEMM in the backward ("1"), instead of two passes.
+DUAL_K4 = os.environ.get("S24_DUAL_K4", "0") == "1"
 
 
-def _paired_layout() -> bool:
-    return PAIRED_DENSE and K4_MODE != "background"  # the in-GEMM K4 job writes the separate layout
+def _dual_k4() -> bool:
+    lay = _layout()
+    return DUAL_K4 and K4_MODE == "side" and lay["paired"] and not lay["identity"]
+
+
+def _layout() -> dict:
+    """Layout of the feature-wise split operands (see splitgemm.FeatureSplit)."""
+    paired = PAIRED_DENSE and K4_MODE != "background"  # the in-GEMM K4 job writes the separate layout
+    return {"paired": paired, "identity": paired and IDENTITY_LAYOUT}
 FORWARD_MODES = ("dense", "sparse24")
 BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
 
@@ -362,6 +381,8 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     split_ready = x_in_ready = None
     plan_out = plan
     want_split = for_backward and cfg.backward_mode != "dense" and act_fw is None
+    defer_split = want_split and side is not None and (ACT_SPLIT_IN_BWD or _dual_k4())
+    want_split = want_split and not defer_split
 
     def fwd_out(st):
         _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
@@ -375,7 +396,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             plan_out = partition_features(counts, cfg.split_ratio, launch_stream=side)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, paired=_paired_layout())
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, **_layout())
         with torch.cuda.stream(side):
             if SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
                 _fill_frame_rows(x_in, x, inv_dev)
@@ -393,7 +414,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             _fill_frame_rows(x_in, x, inv_dev)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, paired=_paired_layout())
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, **_layout())
         if want_split and K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16,
@@ -437,20 +458,21 @@ def _fill_frame_rows(out: torch.Tensor, a: torch.Tensor, src_rows) -> None:
 
 
 
-def _spmm_with_split(launch_gemm, fs, vals, meta, n, h, plan, nonneg=False):
-    """Launch a sparse GEMM on the current stream and the K4 job filling `fs`
+def _spmm_with_split(launch_gemm, k4_work):
+    """Launch a sparse GEMM on the current stream and the K4 job `k4_work()`
     next to it (K4_MODE "side": side stream, co-resident; "inline": after it).
-    Returns the CUDA event after which `fs` is complete (None if inline)."""
+    Returns the CUDA event after which the K4 outputs are complete (None if
+    inline)."""
     main = torch.cuda.current_stream()
     if K4_MODE != "side":
         launch_gemm(main.cuda_stream)
-        run_feature_split(fs, vals, meta, n, h, plan, nonneg)
+        k4_work()
         return None
-    side = side_stream(vals.device)
+    side = side_stream(main.device)
     side.wait_stream(main)  # K4's inputs are ready; it must not wait for the GEMM
     launch_gemm(main.cuda_stream)
     with torch.cuda.stream(side):
-        run_feature_split(fs, vals, meta, n, h, plan, nonneg)
+        k4_work()
         ev = torch.cuda.Event()
         ev.record(side)
     return ev
@@ -460,7 +482,7 @@ def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
     """The feature-wise split of the cached activation (made by the forward
     next to fwd.out when K4 runs on the side stream, else here)."""
     if cache.act_split is None:
-        return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, paired=_paired_layout())
+        return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, **_layout())
     if cache.act_split_ready is not None:
         torch.cuda.current_stream().wait_event(cache.act_split_ready)
     return cache.act_split
@@ -568,6 +590,19 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         if cache.x_in_ready is not None:
             main.wait_event(cache.x_in_ready)
 
+    # the feature-wise split of act, when the forward left it for here: on the
+    # side stream next to K3
+    if cache.act_split is None and cache.act_fw is None and side is not None and \
+            cfg.backward_mode != "dense" and ACT_SPLIT_IN_BWD and not _dual_k4():
+        plan_a = _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else cache.plan
+        fa_b = alloc_feature_split(cache.act_vals, cache.act_meta, npad, h, plan_a, **_layout())
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            run_feature_split(fa_b, cache.act_vals, cache.act_meta, npad, h, plan_a, nonneg=True)
+            ev_a = torch.cuda.Event()
+            ev_a.record(side)
+        cache.act_split, cache.act_split_ready = fa_b, ev_a
+
     # K3 reads dY unpermuted and pairs input row r with act / g_pre row
     # perm[r]; the fused feature-wise epilogue needs the permuted rows
     k3_in, k3_map = g_out, cache.perm_dev
@@ -595,17 +630,28 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     if cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None and not raw_naive:
         # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
         # as background work in its idle epilogue warps
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, paired=_paired_layout())
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
         if K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x),
                       _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None,
                       *k4_job_args(g_vals, cache.act_meta, npad, h, plan, fg, counter), s)
         else:
+            dual = cache.act_split is None and cache.act_fw is None and _dual_k4()
+            fa = alloc_feature_split(cache.act_vals, cache.act_meta, npad, h, plan, **_layout()) if dual else None
+
+            def k4_side():
+                if dual:  # act (>= 0) and g_pre share the keep pattern: one pass for both
+                    run_feature_split_dual(fa, fg, cache.act_vals, g_vals, cache.act_meta, npad, h, plan)
+                else:
+                    run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
+
             fg_ready = _spmm_with_split(
                 lambda st: _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h,
                                      ptr(d_x), _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None, 0, st),
-                fg, g_vals, cache.act_meta, npad, h, plan)
+                k4_side)
+            if dual:
+                cache.act_split, cache.act_split_ready = fa, fg_ready
         ev_dx = GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d))
 
     need_frame_inputs()
@@ -631,7 +677,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         # to serve, hence only without grad_ready)
         fa = _act_split(cache, npad, h, plan)
         if fg is None:
-            fg = feature_split(g_vals, cache.act_meta, npad, h, plan, paired=_paired_layout())
+            fg = feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
         elif fg_ready is not None:
             torch.cuda.current_stream().wait_event(fg_ready)
         split_weight_grad_pair(fa, fg, plan, g_c, cache.x_in, npad, d_w2, d_w1)
@@ -665,7 +711,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
             stats_g = g_fw.stats(plan)
         else:
             if fg is None:
-                fg = feature_split(g_vals, cache.act_meta, npad, h, plan, paired=_paired_layout())
+                fg = feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
             elif fg_ready is not None:
                 torch.cuda.current_stream().wait_event(fg_ready)
             split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)

@@ -53,6 +53,20 @@ class SplitPlan:
         return int(self.dense_features.shape[0])
 
     @cached_property
+    def identity_rows(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(row map, row_valid) of an identity-layout operand (csrc/k4id.cuh):
+        dense pairs, zero padding to 128 rows, then every feature in index
+        order; the dense features' and padding rows are skipped."""
+        nd, h = self.n_dense, self.hidden_dim
+        pad = pad128(2 * nd) - 2 * nd
+        dev = self.feat_pos.device
+        rmap = torch.cat([self.dense_features.repeat_interleave(2), torch.zeros(pad, dtype=torch.int32, device=dev),
+                          torch.arange(h, dtype=torch.int32, device=dev)]).to(torch.int32)
+        valid = torch.cat([torch.zeros(2 * nd, dtype=torch.int32, device=dev),
+                           torch.full((pad,), -1, dtype=torch.int32, device=dev), self.feat_pos]).to(torch.int32)
+        return rmap, valid
+
+    @cached_property
     def paired_row_map(self) -> torch.Tensor:
         """Output row of each row of a paired-layout operand: dense feature r
         twice (rows 2r, 2r+1), then the sparse features."""
@@ -117,15 +131,27 @@ class FeatureSplit:
     # >= 0: paired layout (csrc/k4.cuh): vs rows [0, pair_rows) are the dense
     # features as fixed-selector 2:4 row pairs, sparse rank s is row pair_rows + s
     pair_rows: int = -1
+    # identity layout (csrc/k4id.cuh): the dense pairs padded to 128 rows,
+    # then every feature f at row pair_pad + f
+    identity: bool = False
 
     def rows(self, plan: "SplitPlan") -> int:
         """Rows of the 2:4 operand vs that carry features."""
+        if self.identity:
+            return pad128(self.pair_rows) + plan.hidden_dim
         return max(self.pair_rows, 0) + plan.n_sparse
+
+    def gemm_rows(self, plan: "SplitPlan"):
+        """(M, row map, row_valid) of the split weight-gradient GEMM over vs."""
+        if self.identity:
+            rmap, valid = plan.identity_rows
+            return self.rows(plan), rmap, valid
+        return self.rows(plan), plan.paired_row_map, None
 
 
 def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
                   dense_only: bool = False, with_stats: bool = False, nonneg: bool = False,
-                  paired: bool = False) -> FeatureSplit:
+                  paired: bool = False, identity: bool = False) -> FeatureSplit:
     """K4: token-wise compressed [n, h] (vals + hw meta, n and h multiples of
     128) -> feature-wise 2:4 of the sparse features + transposed dense
     features (the apply_mask / gather / sparsify_feature_wise part of ref
@@ -134,25 +160,36 @@ def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, pla
     K1/K3 epilogues). nonneg=True declares the values >= 0 and NaN-free (the
     relu^2 activation), letting K4 rank raw values. paired=True writes the
     dense features into vs as fixed-selector 2:4 row pairs (one sparse GEMM
-    then covers the whole split product, see split_weight_grad)."""
-    fs = alloc_feature_split(vals, meta_hw, n, h, plan, dense_only, paired)
+    then covers the whole split product, see split_weight_grad); identity=True
+    the coalesced identity-order variant of that (csrc/k4id.cuh)."""
+    fs = alloc_feature_split(vals, meta_hw, n, h, plan, dense_only, paired, identity)
     ns, nd = plan.n_sparse, plan.n_dense
     cnt = torch.zeros(2, dtype=torch.int64, device=vals.device) if with_stats else None
-    _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(fs.vs),
-              ptr(fs.es), ptr(fs.vd), ptr(cnt), int(nonneg), fs.pair_rows, stream())
+    if fs.identity:
+        _lib.call("s24_feature_split_id", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), nd, ptr(fs.vs),
+                  ptr(fs.es), ptr(cnt), int(nonneg), stream())
+    else:
+        _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), ns, nd, ptr(fs.vs),
+                  ptr(fs.es), ptr(fs.vd), ptr(cnt), int(nonneg), fs.pair_rows, stream())
     if with_stats:
         fs.stats = SparsifyStats(n * ns, cnt)
     return fs
 
 
 def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
-                        dense_only: bool = False, paired: bool = False) -> FeatureSplit:
+                        dense_only: bool = False, paired: bool = False, identity: bool = False) -> FeatureSplit:
     """Output buffers of one K4 job (filled by s24_feature_split or by a GEMM's
     background warps via s24_spmm_bg). Its drop statistics are not counted on
     the hot path -- the reference discards them (splitgemm.py:75) -- and are
     recounted on the device only if someone reads them."""
     dev = vals.device
     ns, nd = plan.n_sparse, plan.n_dense
+    stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
+    if identity and not dense_only:
+        rows = pad128(2 * nd) + h
+        vs = torch.empty(rows, n // 2, dtype=BF16, device=dev)
+        es = torch.empty(_lib.meta_hw_bytes(rows, n), dtype=torch.uint8, device=dev)
+        return FeatureSplit(vs, es, None, stats, 2 * nd, identity=True)
     paired = paired and not dense_only
     rows = ns + (2 * nd if paired else 0)
     vs = es = vd = None
@@ -161,15 +198,36 @@ def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: in
         es = torch.empty(_lib.meta_hw_bytes(max(rows, 1), n), dtype=torch.uint8, device=dev)
     if not paired:
         vd = torch.empty(max(pad128(nd), 128), n, dtype=BF16, device=dev)
-    stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
     return FeatureSplit(vs, es, vd, stats, 2 * nd if paired else -1)
 
 
 def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int,
                       plan: SplitPlan, nonneg: bool = False) -> None:
     """Fill preallocated K4 outputs on the current stream (no drop counting)."""
-    _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense,
-              ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, int(nonneg), fs.pair_rows, stream())
+    for _ in range(K4_REPEAT):
+        if fs.identity:
+            _lib.call("s24_feature_split_id", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_dense,
+                      ptr(fs.vs), ptr(fs.es), None, int(nonneg), stream())
+        elif fs.pair_rows >= 0:
+            _lib.call("s24_feature_split_x", ptr(vals), None, ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse,
+                      plan.n_dense, ptr(fs.vs), ptr(fs.es), None, None, int(nonneg), stream())
+        else:
+            _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse,
+                      plan.n_dense, ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, int(nonneg), fs.pair_rows, stream())
+
+
+K4_REPEAT = 1  # experiments only (scripts/ab_step.py): marginal cost of K4 in the step
+
+
+def run_feature_split_dual(fa: FeatureSplit, fb: FeatureSplit, vals_a: torch.Tensor, vals_b: torch.Tensor,
+                           meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan) -> None:
+    """K4 for two operands on one keep pattern (the activation, >= 0, and
+    g_pre) in one pass: paired rank layout for both."""
+    if not (fa.pair_rows >= 0 and fb.pair_rows >= 0 and not fa.identity and not fb.identity):
+        raise DimensionError("the dual feature split writes the paired rank layout")
+    for _ in range(K4_REPEAT):
+        _lib.call("s24_feature_split_x", ptr(vals_a), ptr(vals_b), ptr(meta_hw), n, h, ptr(plan.feat_pos),
+                  plan.n_sparse, plan.n_dense, ptr(fa.vs), ptr(fa.es), ptr(fb.vs), ptr(fb.es), 1, stream())
 
 
 def side_stream(device) -> torch.cuda.Stream:
@@ -250,10 +308,10 @@ def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int
     ld = out.shape[1]
     code = _lib.F32 if out.dtype == F32 else _lib.BF16
     if fs.pair_rows >= 0:
-        rows = fs.rows(plan)
+        rows, rmap, valid = fs.gemm_rows(plan)
         if rows:
             _lib.call("s24_spmm", ptr(fs.vs), ptr(fs.es), ptr(b), 1, b.stride(0), rows, d, n, ptr(out), code, ld,
-                      ptr(plan.paired_row_map), int(transposed), rows, None, fs.pair_rows, stream())
+                      ptr(rmap), int(transposed), rows, ptr(valid), fs.pair_rows, stream())
         return
     main = torch.cuda.current_stream()
     side = _side_stream(out.device) if plan.n_sparse and plan.n_dense else main
@@ -283,15 +341,16 @@ def split_weight_grad_pair(fa: FeatureSplit, fb: FeatureSplit, plan: SplitPlan, 
     d = b_a.shape[1]
     if b_b.shape[1] != d or out_a.dtype != out_b.dtype:
         raise DimensionError("paired weight gradients need equal widths and output dtypes")
-    if fa.pair_rows != fb.pair_rows:
-        raise DimensionError("both operands must use the same (paired or separate-dense) layout")
+    if fa.pair_rows != fb.pair_rows or fa.identity != fb.identity:
+        raise DimensionError("both operands must use the same layout")
     code = _lib.F32 if out_a.dtype == F32 else _lib.BF16
     if fa.pair_rows >= 0:
-        rows, rm = fa.rows(plan), ptr(plan.paired_row_map)
+        rows, rmap, valid = fa.gemm_rows(plan)
+        rm, rv = ptr(rmap), ptr(valid)
         if rows:
             _lib.call("s24_spmm_pair", 1, rows, d, n, code,
-                      ptr(fa.vs), ptr(fa.es), ptr(b_a), b_a.stride(0), ptr(out_a), out_a.shape[1], rm, 0, None,
-                      ptr(fb.vs), ptr(fb.es), ptr(b_b), b_b.stride(0), ptr(out_b), out_b.shape[1], rm, 1, None,
+                      ptr(fa.vs), ptr(fa.es), ptr(b_a), b_a.stride(0), ptr(out_a), out_a.shape[1], rm, 0, rv,
+                      ptr(fb.vs), ptr(fb.es), ptr(b_b), b_b.stride(0), ptr(out_b), out_b.shape[1], rm, 1, rv,
                       fa.pair_rows, stream())
         return
     main = torch.cuda.current_stream()

@@ -17,6 +17,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2503_16672_b200 as s24  # noqa: E402
 from paper_2503_16672_b200 import ffn as F  # noqa: E402
+from paper_2503_16672_b200 import splitgemm as SG  # noqa: E402
 
 VARIANTS = {
     "default": {},
@@ -25,6 +26,13 @@ VARIANTS = {
     "main_gathers": {"SIDE_GATHERS": False},
     "rowmap": {"ROWMAP_GEMMS": True},
     "graph": {"_graph": True},
+    "act_split_bwd": {"ACT_SPLIT_IN_BWD": True},
+    "k4_twice_graph": {"_k4_repeat": 2, "_graph": True},
+    "fused_fw_graph": {"FUSED_FEATURE_SPLIT": True, "_graph": True},
+    "nodual_graph": {"DUAL_K4": False, "_graph": True},
+    "identity_graph": {"IDENTITY_LAYOUT": True, "_graph": True},
+    "k4_none_graph": {"_k4_repeat": 0, "_graph": True},
+    "act_split_bwd_graph": {"ACT_SPLIT_IN_BWD": True, "_graph": True},
 }
 
 
@@ -50,6 +58,7 @@ def main():
     base = {k: getattr(F, k) for v in VARIANTS.values() for k in v if not k.startswith("_")}
 
     def apply(nm):
+        SG.K4_REPEAT = VARIANTS.get(nm, {}).get("_k4_repeat", 1)
         for k, v in base.items():
             setattr(F, k, v)
         for k, v in VARIANTS.get(nm, {}).items():

@@ -1,0 +1,3 @@
+J='import json,sys; d=json.loads(sys.stdin.read()); print({k:(v["median_ms"],v["min_ms"]) for k,v in d.items()})'
+timeout 600 python scripts/ab_step.py --blocks 5 --variants graph,k4_none_graph,k4_twice_graph 2>&1 | tail -1 | python -c "$J"
+timeout 600 python scripts/ab_step.py --blocks 5 --variants k4_twice_graph,k4_none_graph,graph 2>&1 | tail -1 | python -c "$J"

@@ -122,6 +122,20 @@ def main():
     rec("K4 feature split", timeit(lambda: _lib.call("s24_feature_split", P(act_vals), P(meta), n, h, P(pos), kcount,
                                                         h - kcount, P(vs), P(es), P(vd), P(stats), 1, -1, S()), args.iters,
                                     flush), 1e-9, bytes_=k4_bytes)
+    nd = h - kcount
+    vsx = torch.empty((2 * nd + kcount + 127) // 128 * 128, n // 2, device="cuda", dtype=bf)
+    esx = torch.empty(_lib.meta_hw_bytes(2 * nd + kcount, n), device="cuda", dtype=torch.uint8)
+    k4x_bytes = n * h * 1.125 + (2 * nd + kcount) * n * 0.5625
+    rec("K4x paired (hot path)", timeit(lambda: _lib.call("s24_feature_split_x", P(act_vals), None, P(meta), n, h,
+                                                             P(pos), kcount, nd, P(vsx), P(esx), None, None, 1, S()),
+                                         args.iters, flush), 1e-9, bytes_=k4x_bytes)
+    pad = (2 * nd + 127) // 128 * 128
+    vsi = torch.empty(pad + h, n // 2, device="cuda", dtype=bf)
+    esi = torch.empty(_lib.meta_hw_bytes(pad + h, n), device="cuda", dtype=torch.uint8)
+    k4i_bytes = n * h * 1.125 + (pad + h) * n * 0.5625 + 0.0
+    rec("K4 identity layout", timeit(lambda: _lib.call("s24_feature_split_id", P(act_vals), P(meta), n, h, P(pos), nd,
+                                                          P(vsi), P(esi), None, 1, S()), args.iters, flush),
+        1e-9, bytes_=k4i_bytes)
     src = torch.randperm(n, device="cuda").int()
     rec("K6 gather rows", timeit(lambda: _lib.call("s24_gather_rows", P(x), n, 2 * d, 2 * d, P(src), P(out), 2 * d,
                                                       S()), args.iters, flush), 1e-9, bytes_=2 * n * d * 2)

@@ -364,8 +364,9 @@ def test_feature_split_paired_layout():
     assert not got_v[rows:].any()
 
 
+@pytest.mark.parametrize("layout", ["paired", "identity"])
 @pytest.mark.parametrize("transposed", [0, 1])
-def test_split_weight_grad_paired_equals_separate(transposed):
+def test_split_weight_grad_paired_equals_separate(transposed, layout):
     """The split weight gradient from the paired layout (one 2:4 GEMM, row
     pairs summed in the epilogue) matches the separate sparse + dense GEMMs
     and the fp32 product of the masked operand."""
@@ -381,7 +382,7 @@ def test_split_weight_grad_paired_equals_separate(transposed):
     b = torch.randn(n, d, device="cuda").bfloat16()
     outs = []
     for paired in (False, True):
-        fs = feature_split(vals, meta_hw, n, h, plan, paired=paired)
+        fs = feature_split(vals, meta_hw, n, h, plan, paired=paired, identity=paired and layout == "identity")
         out = torch.zeros((d, h) if transposed else (h, d), device="cuda")
         split_weight_grad(fs, plan, b, n, out, transposed=bool(transposed))
         outs.append(out.t() if transposed else out)
@@ -392,3 +393,90 @@ def test_split_weight_grad_paired_equals_separate(transposed):
     for o in outs:
         assert rel_err(o.cpu(), torch.from_numpy(ref)) < 1e-5
     assert rel_err(outs[1], outs[0]) < 1e-6
+
+
+@pytest.mark.parametrize("nonneg", [0, 1])
+def test_feature_split_identity_layout(nonneg):
+    """Identity layout (coalesced K4): dense pairs, zero padding to 128 rows,
+    then feature f at row pad + f with the oracle's feature-wise 2:4."""
+    n, h = 512, 384
+    rng = np.random.Generator(np.random.PCG64(29))
+    a = O.bf16_round(((rng.random((n, h)) < 0.3) * rng.standard_normal((n, h))).astype(np.float32))
+    if nonneg:
+        a = O.bf16_round(np.round(a * a * 4) / 4)
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    vals, _, meta_hw, mask, _ = gpu_sparsify_token(ta)
+    am = a * mask.cpu().numpy().astype(np.float32)
+    osp, ode = O.partition(O.column_counts(am), 0.9)
+    ks, nd = len(osp), len(ode)
+    pos = np.empty(h, np.int32)
+    pos[osp] = np.arange(ks)
+    pos[ode] = -np.arange(nd) - 1
+    pad = (2 * nd + 127) // 128 * 128
+    rows = pad + h
+    vs = torch.full((rows, n // 2), 7.0, dtype=torch.bfloat16, device="cuda")
+    es = torch.zeros(_lib.meta_hw_bytes(rows, n), dtype=torch.uint8, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.call("s24_feature_split_id", P(vals), P(meta_hw), n, h, P(torch.from_numpy(pos).cuda()), nd, P(vs), P(es),
+              P(stats), nonneg, S())
+    ov, om, _, ost = O.sparsify_feature(am)  # every feature
+    got_meta = meta_hw_to_ref(es, rows, n).cpu().numpy()
+    got_v = vs.float().cpu().numpy().reshape(rows, n // 4, 2)
+    assert np.array_equal(got_meta[pad:].transpose(1, 0, 2), om)
+    assert np.array_equal(got_v[pad:].transpose(1, 0, 2), ov)
+    dense = am[:, ode].T.reshape(nd, n // 4, 4)
+    assert np.array_equal(got_v[0:2 * nd:2], dense[:, :, 0:2])
+    assert np.array_equal(got_v[1:2 * nd:2], dense[:, :, 2:4])
+    assert (got_meta[0:2 * nd:2] == np.array([0, 1])).all() and (got_meta[1:2 * nd:2] == np.array([2, 3])).all()
+    assert not got_v[2 * nd:pad].any()
+    _, _, _, ost_s = O.sparsify_feature(np.ascontiguousarray(am[:, osp]))
+    assert stats.cpu().tolist() == [ost_s["nonzeros_before"], ost_s["nonzeros_after"]]
+
+
+@pytest.mark.parametrize("dual", [False, True])
+def test_feature_split_x_matches_reference_kernel(dual):
+    """The hot-path K4x (one or two operands sharing the keep pattern) writes
+    exactly what the reference-layout K4 writes in the paired layout."""
+    n, h = 512, 512
+    rng = np.random.Generator(np.random.PCG64(31))
+    y = O.bf16_round(rng.standard_normal((n, h)).astype(np.float32))
+    act = O.bf16_round(np.maximum(y, 0) ** 2)
+    ta = torch.from_numpy(act).cuda().bfloat16()
+    vals, _, meta_hw, mask, _ = gpu_sparsify_token(ta)
+    g = torch.randn(n, h, device="cuda").bfloat16() * mask.bfloat16()
+    gvals = torch.zeros_like(vals)
+    # g on the forward keep pattern, compressed with the same metadata
+    _lib.call("s24_compress_token_with_mask", P(g), BF16, n, h, h, P(mask), P(gvals), None, None, None, S())
+    am = act * mask.cpu().numpy().astype(np.float32)
+    osp, ode = O.partition(O.column_counts(am), 0.9)
+    ks, nd = len(osp), len(ode)
+    pos = np.empty(h, np.int32)
+    pos[osp] = np.arange(ks)
+    pos[ode] = -np.arange(nd) - 1
+    tpos = torch.from_numpy(pos).cuda()
+    rows = 2 * nd + ks
+    rp = (rows + 127) // 128 * 128
+
+    def bufs():
+        return (torch.full((rp, n // 2), 7.0, dtype=torch.bfloat16, device="cuda"),
+                torch.zeros(_lib.meta_hw_bytes(rp, n), dtype=torch.uint8, device="cuda"))
+    ref = []
+    for v, nn in ((vals, 1), (gvals, 0)):
+        vs, es = bufs()
+        _lib.call("s24_feature_split", P(v), P(meta_hw), n, h, P(tpos), ks, nd, P(vs), P(es), None, None, nn,
+                  2 * nd, S())
+        ref.append((vs, es))
+    va, ea = bufs()
+    vb, eb = bufs()
+    if dual:
+        _lib.call("s24_feature_split_x", P(vals), P(gvals), P(meta_hw), n, h, P(tpos), ks, nd, P(va), P(ea), P(vb),
+                  P(eb), 1, S())
+        got = [(va, ea), (vb, eb)]
+    else:
+        _lib.call("s24_feature_split_x", P(vals), None, P(meta_hw), n, h, P(tpos), ks, nd, P(va), P(ea), None, None,
+                  1, S())
+        _lib.call("s24_feature_split_x", P(gvals), None, P(meta_hw), n, h, P(tpos), ks, nd, P(vb), P(eb), None, None,
+                  0, S())
+        got = [(va, ea), (vb, eb)]
+    for (rv, re_), (gv_, ge) in zip(ref, got):
+        assert torch.equal(rv, gv_) and torch.equal(re_, ge)
