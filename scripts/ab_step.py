@@ -33,6 +33,7 @@ VARIANTS = {
     "identity_graph": {"IDENTITY_LAYOUT": True, "_graph": True},
     "k4_none_graph": {"_k4_repeat": 0, "_graph": True},
     "act_split_bwd_graph": {"ACT_SPLIT_IN_BWD": True, "_graph": True},
+    "act_split_bwd_k4none_graph": {"ACT_SPLIT_IN_BWD": True, "_graph": True, "_k4_repeat": 0},
 }
 
 

@@ -8,7 +8,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2503_16672_b200 import _lib  # noqa: E402
 
 P = lambda t: t.data_ptr()  # noqa: E731
-n, h = (int(v) for v in sys.argv[1:3]) if len(sys.argv) > 2 else (16384, 8192)
+n, h = (int(v) for v in sys.argv[1:3]) if len(sys.argv) > 2 and sys.argv[1].isdigit() else (16384, 8192)
 S = torch.cuda.current_stream().cuda_stream
 a = torch.relu(torch.randn(n, h, device="cuda")).square().bfloat16()  # relu^2-like operand
 vals = torch.zeros(n, h // 2, device="cuda", dtype=torch.bfloat16)
@@ -24,7 +24,13 @@ vs = torch.zeros((ks + 127) // 128 * 128, n // 2, device="cuda", dtype=torch.bfl
 es = torch.zeros(_lib.meta_hw_bytes(ks, n), device="cuda", dtype=torch.uint8)
 vd = torch.zeros((h - ks + 127) // 128 * 128, n, device="cuda", dtype=torch.bfloat16)
 st = torch.zeros(2, dtype=torch.int64, device="cuda")
+nd = h - ks
+vsx = torch.zeros((2 * nd + ks + 127) // 128 * 128 + 1, n // 2, device="cuda", dtype=torch.bfloat16)
+esx = torch.zeros(_lib.meta_hw_bytes((2 * nd + ks + 127) // 128 * 128 + 128, n), device="cuda", dtype=torch.uint8)
 for _ in range(5):
-    _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, h - ks, P(vs), P(es), P(vd), None, 1, -1, S)  # hot-path variant: no stats
+    if "x" in sys.argv[3:]:  # the hot-path K4x (paired rank layout)
+        _lib.call("s24_feature_split_x", P(vals), None, P(meta), n, h, P(pos), ks, nd, P(vsx), P(esx), None, None, 1, S)
+    else:
+        _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, nd, P(vs), P(es), P(vd), None, 1, -1, S)
 torch.cuda.synchronize()
 print("ok")

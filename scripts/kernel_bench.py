@@ -123,8 +123,9 @@ def main():
                                                         h - kcount, P(vs), P(es), P(vd), P(stats), 1, -1, S()), args.iters,
                                     flush), 1e-9, bytes_=k4_bytes)
     nd = h - kcount
-    vsx = torch.empty((2 * nd + kcount + 127) // 128 * 128, n // 2, device="cuda", dtype=bf)
-    esx = torch.empty(_lib.meta_hw_bytes(2 * nd + kcount, n), device="cuda", dtype=torch.uint8)
+    vsx = torch.empty((2 * nd + kcount + 127) // 128 * 128 + 1, n // 2, device="cuda", dtype=bf)
+    esx = torch.empty(_lib.meta_hw_bytes((2 * nd + kcount + 127) // 128 * 128 + 128, n), device="cuda",
+                      dtype=torch.uint8)
     k4x_bytes = n * h * 1.125 + (2 * nd + kcount) * n * 0.5625
     rec("K4x paired (hot path)", timeit(lambda: _lib.call("s24_feature_split_x", P(act_vals), None, P(meta), n, h,
                                                              P(pos), kcount, nd, P(vsx), P(esx), None, None, 1, S()),
