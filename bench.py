@@ -74,9 +74,11 @@ def measured_traffic(label: str):
     committed ncu --set full capture (profiles/rNN/traffic.json), or None."""
     for f in sorted(Path(__file__).resolve().parent.glob("profiles/r*/traffic.json"), reverse=True):
         try:
-            t = json.loads(f.read_text()).get(label)
+            table = json.loads(f.read_text())
         except (OSError, ValueError):
             continue
+        # keys are label prefixes (shapes may follow in the live label)
+        t = next((v for k, v in table.items() if label.startswith(k)), None)
         if t:
             return t["traffic_bytes"], f"{t['profile']} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
     return None, None

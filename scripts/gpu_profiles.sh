@@ -10,4 +10,4 @@ cap spmm_fwdout 'GemmCfgILb1ELb0ELb1E.*EpiStoreI13__nv_bfloat16'
 cap spmm_pair 'GemmCfgILb1ELb0ELb1E.*EpiStoreIfE'
 cap k1 'EpiFwd1'
 cap k3 'EpiBwd1'
-cap k4 'k_feature_split'
+cap k4 'k_feature_split_x'
