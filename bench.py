@@ -35,10 +35,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "Squared-ReLU FFN fwd+bwd tokens/sec & speedup vs dense bf16; sparse TFLOPS"
-CONFIGS = {"c1": (4096, 512, 2048), "c2": (16384, 2048, 8192), "c3": (32768, 4096, 16384)}
+CONFIGS = {"c1": (4096, 512, 2048), "c2": (16384, 2048, 8192), "c3": (32768, 4096, 16384),
+           "c4": (32768, 4096, 16384)}
 WORKLOAD = {"c1": "c1: FFN d=512 h=2048, 4096 tokens/GPU, fwd+bwd",
             "c2": "c2: FFN d=2048 h=8192 (1.5B-class), 16384 tokens/GPU, fwd+bwd",
-            "c3": "c4: FFN d=4096 h=16384 (7B-class), 32768 tokens/GPU, fwd+bwd"}
+            "c3": "c3: FFN d=4096 h=16384 (7B-class), 32768 tokens/GPU, inference prefill (forward only)",
+            "c4": "c4: FFN d=4096 h=16384 (7B-class), 32768 tokens/GPU, fwd+bwd + dW all-reduce"}
+PREFILL = {"c3"}  # forward-only configurations (BASELINE configs[2])
 SPARSITY = 0.9
 CPU_SAMPLE_TOKENS = 192
 REF_SAMPLE_TOKENS = 32
@@ -54,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--sparsity", type=float, default=SPARSITY,
+                    help="target activation sparsity of the synthetic inputs (c5 sweep)")
     return ap.parse_args()
 
 
@@ -84,7 +89,7 @@ def measured_traffic(label: str):
     return None, None
 
 
-def _cpu_sample(seed: int, n: int, d: int, h: int) -> float:
+def _cpu_sample(seed: int, n: int, d: int, h: int, forward_only: bool = False) -> float:
     """One bounded sample of the workload on the CPU oracle (ordered-accumulation
     GEMMs, the reference's own arithmetic): returns wall seconds."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -93,23 +98,29 @@ def _cpu_sample(seed: int, n: int, d: int, h: int) -> float:
     x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=SPARSITY, seed=seed)
     t0 = time.perf_counter()
     out, cache = O.ffn_forward(x, w1, w2, O.RECIPE, ordered=True)
-    O.ffn_backward(dy, cache, w1, w2, O.RECIPE, ordered=True)
+    if not forward_only:
+        O.ffn_backward(dy, cache, w1, w2, O.RECIPE, ordered=True)
     return time.perf_counter() - t0
 
 
+def cpu_sample_tokens(d: int, h: int) -> int:
+    """CPU sample size: ~15 s of oracle work whatever the model width."""
+    return max(16, int(CPU_SAMPLE_TOKENS * (2048 * 8192) / (d * h)) // 4 * 4)
+
+
 def _cpu_worker(args):
-    seed, n, d, h = args
-    return _cpu_sample(seed, n, d, h)
+    seed, n, d, h, fwd_only = args
+    return _cpu_sample(seed, n, d, h, fwd_only)
 
 
-def cpu_parallel_step(procs: int, n: int, d: int, h: int, seed0: int = 0) -> float:
+def cpu_parallel_step(procs: int, n: int, d: int, h: int, seed0: int = 0, forward_only: bool = False) -> float:
     """procs independent samples in parallel processes; returns wall seconds."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(procs) as pool:
-        pool.map(_cpu_worker, [(seed0 + i, n, d, h) for i in range(procs)])
+        pool.map(_cpu_worker, [(seed0 + i, n, d, h, forward_only) for i in range(procs)])
     return time.perf_counter() - t0
 
 
@@ -126,15 +137,17 @@ def run_reference(args):
         return
     n_total, d, h = CONFIGS[args.config]
     procs = max(1, min(host_cores(), 32))
-    tok = REF_SAMPLE_TOKENS
+    fwd_only = args.config in PREFILL
+    tok = max(8, int(REF_SAMPLE_TOKENS * (2048 * 8192) / (d * h)) // 4 * 4)
     # the pool start-up is part of every step; warm-up steps absorb import costs
     for i in range(args.warmup):
-        cpu_parallel_step(procs, tok, d, h, seed0=1000 * (i + 1))
-    times = [cpu_parallel_step(procs, tok, d, h, seed0=7 + 100 * i) for i in range(args.steps)]
+        cpu_parallel_step(procs, tok, d, h, seed0=1000 * (i + 1), forward_only=fwd_only)
+    times = [cpu_parallel_step(procs, tok, d, h, seed0=7 + 100 * i, forward_only=fwd_only) for i in range(args.steps)]
     total = sum(times)
     value = procs * tok * len(times) / total
     sample = (f"{procs} processes x {tok} tokens each per step of the {WORKLOAD[args.config]} workload "
-              f"(oracle/srelu24_np.py recipe fwd+bwd, ordered fp32 GEMMs = the reference's arithmetic)")
+              f"(oracle/srelu24_np.py recipe {'forward' if fwd_only else 'fwd+bwd'}, ordered fp32 GEMMs = the "
+              f"reference's arithmetic)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
@@ -274,7 +287,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": "NVML, 2 ms polling during the timed steps"}
 
 
-def synthetic_device_inputs(torch, n, d, h, seed, device):
+def synthetic_device_inputs(torch, n, d, h, seed, device, sparsity=SPARSITY):
     """SURVEY 8d generator on the device (bf16): x ~ N(0,1) with a bias-carrier
     last column; W1 ~ N(0, 1/(d-1)) with last row = Phi^-1(1 - s_j)."""
     g = torch.Generator(device=device)
@@ -283,7 +296,7 @@ def synthetic_device_inputs(torch, n, d, h, seed, device):
     x = torch.randn(n, d, generator=g, device=device)
     x[:, -1] = 1.0
     w1 = torch.randn(d, h, generator=g, device=device) / math.sqrt(d - 1)
-    s = torch.full((h,), SPARSITY, device=device)
+    s = torch.full((h,), sparsity, device=device)
     dense_idx = torch.randperm(h, generator=g, device=device)[: int(round(0.05 * h))]
     s[dense_idx] = 0.5
     w1[-1] = torch.special.ndtri(1.0 - s)
@@ -309,8 +322,9 @@ def run_ours(args):
     from paper_2503_16672_b200.dp import GradAllReducer
 
     n, d, h = CONFIGS[args.config]
+    prefill = args.config in PREFILL
     pk = peaks()
-    x, w1, w2, dy = synthetic_device_inputs(torch, n, d, h, seed=1234 + rank, device=dev)
+    x, w1, w2, dy = synthetic_device_inputs(torch, n, d, h, seed=1234 + rank, device=dev, sparsity=args.sparsity)
     params = s24.FfnParams(w1=w1, w2=w2)
     recipe = s24.RECIPE
     dense = s24.FfnConfig()
@@ -318,7 +332,9 @@ def run_ours(args):
 
     def step(cfg, xx, gg):
         """Eager step through the public API (per-kernel breakdown pass)."""
-        out, cache = s24.ffn_forward(xx, params, cfg)
+        out, cache = s24.ffn_forward(xx, params, cfg, for_backward=not prefill)
+        if prefill:
+            return out, cache, None
         if world > 1:
             red = GradAllReducer()
             grads = s24.ffn_backward(gg, cache, params, cfg, grad_ready=red)
@@ -336,14 +352,14 @@ def run_ours(args):
         key = "recipe" if cfg is recipe else "dense"
         g = graphs.get(key)
         if g is None:
-            g = graphs[key] = s24.FfnStepGraph(params, cfg, n)
+            g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill)
             g.x.copy_(x)
             g.dy.copy_(dy)
         if xx is not None:
             g.x.copy_(xx, non_blocking=True)
             g.dy.copy_(gg, non_blocking=True)
         g.replay()
-        if world > 1:
+        if world > 1 and not prefill:
             dist.all_reduce(g.d_w1)
             dist.all_reduce(g.d_w2)
         return g
@@ -391,7 +407,12 @@ def run_ours(args):
     clocks.start()
     t_recipe = timed(recipe, args.steps)
     clk = clocks.stop()
-    t_dense = timed(dense, args.steps) if not args.no_dense else None
+    t_dense = None
+    if not args.no_dense:
+        clocks_d = ClockSampler(local)
+        clocks_d.start()
+        t_dense = timed(dense, args.steps)
+        clk_dense = clocks_d.stop()
     for _ in range(2):  # re-warm the eager allocator pools after the graph phase
         step(recipe, x, dy)
     t_eager = timed(recipe, args.steps, eager=True)
@@ -404,20 +425,21 @@ def run_ours(args):
     out, cache, grads = step(recipe, x, dy)
     torch.cuda.synchronize()
     drops = {"fwd_token_wise_dropped_fraction": cache.stats.dropped_fraction_of_nonzeros,
-             "fwd_activation_sparsity": cache.stats.sparsity_before,
-             "bwd_act_feature_wise_dropped_fraction": grads.stats_act.dropped_fraction_of_nonzeros,
-             "bwd_grad_feature_wise_dropped_fraction": grads.stats_grad.dropped_fraction_of_nonzeros,
-             "plan_sparse_features": cache.plan.n_sparse, "plan_dense_features": cache.plan.n_dense}
+             "fwd_activation_sparsity": cache.stats.sparsity_before}
+    if not prefill:
+        drops.update({"bwd_act_feature_wise_dropped_fraction": grads.stats_act.dropped_fraction_of_nonzeros,
+                      "bwd_grad_feature_wise_dropped_fraction": grads.stats_grad.dropped_fraction_of_nonzeros,
+                      "plan_sparse_features": cache.plan.n_sparse, "plan_dense_features": cache.plan.n_dense})
 
     ms_step = t_recipe / args.steps
     value = world * n * args.steps / (t_recipe / 1e3)
-    flops_useful = 12.0 * n * d * h
+    flops_useful = (4.0 if prefill else 12.0) * n * d * h
     result = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "tokens_per_gpu": n, "global_tokens": n * world, "d": d,
-                   "h": h, "activation_sparsity": SPARSITY, "recipe": "sparse24 fwd + split_masked bwd (ratio 0.95) "
+                   "h": h, "activation_sparsity": args.sparsity, "recipe": "sparse24 fwd + split_masked bwd (ratio 0.95) "
                    "+ mask_grad_with_fwd + permute_tokens", "parallelism": f"dp{world} (token shards, NCCL "
                    "all-reduce of dW1/dW2)" if world > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps, outside the step events",
@@ -429,6 +451,7 @@ def run_ours(args):
         result["dense_twin"] = {"value": world * n * args.steps / (t_dense / 1e3), "unit": "tokens/s",
                                 "ms_per_step": t_dense / args.steps}
         result["speedup_vs_dense"] = t_dense / t_recipe
+        result["dense_twin"]["clocks"] = {k: clk_dense.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")}
     result["sparse_tflops"] = flops_useful / (ms_step / 1e3) / 1e12
     result["drops"] = drops
 
@@ -475,6 +498,8 @@ def run_ours(args):
         def e2e_step():
             g = graph_step(recipe, xh, gh)  # pinned host -> the graph's input buffers, replay
             oh.copy_(g.out, non_blocking=True)
+            if prefill:
+                return
             dxh.copy_(g.d_x, non_blocking=True)
             dw1h.copy_(g.d_w1, non_blocking=True)
             dw2h.copy_(g.d_w2, non_blocking=True)
@@ -493,19 +518,22 @@ def run_ours(args):
         barrier()
         t_e2e = max_over_ranks(sum(s.elapsed_time(e) for s, e in evs))
         result["e2e"] = {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s",
-                         "h2d_bytes_per_step": 2 * n * d * 2,
-                         "d2h_bytes_per_step": 2 * n * d * 2 + 2 * d * h * 4,
+                         "h2d_bytes_per_step": (1 if prefill else 2) * n * d * 2,
+                         "d2h_bytes_per_step": n * d * 2 if prefill else 2 * n * d * 2 + 2 * d * h * 4,
                          "ms_per_step": t_e2e / args.steps,
-                         "path": "s24.FfnStepGraph (public API: ffn_forward + ffn_backward captured) with pinned "
-                                 "host x, dY copied in and out, dX, dW1, dW2 copied out every step"}
+                         "path": ("s24.FfnStepGraph(backward=False) (public API: ffn_forward captured) with pinned "
+                                  "host x copied in and out copied out every step" if prefill else
+                                  "s24.FfnStepGraph (public API: ffn_forward + ffn_backward captured) with pinned "
+                                  "host x, dY copied in and out, dX, dW1, dW2 copied out every step")}
 
     # CPU baseline: the oracle port on this host, rank 0, N=1 only
     if rank == 0 and world == 1 and not args.no_cpu:
-        t = _cpu_sample(11, CPU_SAMPLE_TOKENS, d, h)
+        tok = cpu_sample_tokens(d, h)
+        t = _cpu_sample(11, tok, d, h, forward_only=prefill)
         result["cpu_baseline"] = {
-            "value": CPU_SAMPLE_TOKENS / t, "unit": "tokens/s", "cores": 1, "kind": "port",
-            "sample": f"{CPU_SAMPLE_TOKENS} tokens of the {WORKLOAD[args.config]} workload through "
-                      f"oracle/srelu24_np.py (recipe fwd+bwd, ordered fp32 GEMMs), one process, {t:.1f} s"}
+            "value": tok / t, "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"{tok} tokens of the {WORKLOAD[args.config]} workload through oracle/srelu24_np.py "
+                      f"(recipe {'forward' if prefill else 'fwd+bwd'}, ordered fp32 GEMMs), one process, {t:.1f} s"}
 
     if rank == 0:
         print(json.dumps(result), flush=True)

@@ -31,13 +31,32 @@ struct K4xSlot {
   uint32_t dense;  // 1: paired dense feature
 };
 
+#ifndef S24_K4X_SWIZZLE
+#define S24_K4X_SWIZZLE 1
+#endif
 template <int NOPS, bool NONNEG0>
 __global__ void __launch_bounds__(256) k_feature_split_x(K4xArgs a) {
   __shared__ K4xSlot slots[8][16];
   const uint2* lut = k4_lut_init();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = a.n, h = a.h;
-  const int t0 = blockIdx.y * 128, fbase = blockIdx.x * 128 + warp * 16;
+  // CTA order: square super-tiles of SW x SW blocks (feature-block fastest
+  // inside), so that consecutive CTAs read adjacent 128-byte pieces of the
+  // same token rows AND write adjacent pieces of the same feature rows
+  int fb = blockIdx.x, tb = blockIdx.y;
+  if constexpr (S24_K4X_SWIZZLE > 1) {
+    constexpr int SW = S24_K4X_SWIZZLE;
+    const int nfb = gridDim.x, ntb = gridDim.y;
+    const int id = blockIdx.y * nfb + blockIdx.x;
+    const int per_row = SW * nfb;  // CTAs per super-row (SW token blocks x all feature blocks)
+    const int sr = id / per_row, rem = id - sr * per_row;
+    const int rows_here = min(SW, ntb - sr * SW);
+    const int sc = rem / (SW * rows_here), in = rem - sc * SW * rows_here;
+    const int cols_here = min(SW, nfb - sc * SW);
+    fb = sc * SW + in % cols_here;
+    tb = sr * SW + in / cols_here;
+  }
+  const int t0 = tb * 128, fbase = fb * 128 + warp * 16;
   const uint32_t nw = static_cast<uint32_t>(n / 4);
   if (lane < 16) {
     const int pos = __ldg(a.feat_pos + fbase + lane);

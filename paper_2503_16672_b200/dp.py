@@ -79,5 +79,5 @@ def prefill(x_shard, params, cfg):
     """Inference prefill on this rank's tokens: no communication."""
     from .ffn import ffn_forward
 
-    out, _ = ffn_forward(x_shard, params, cfg)
+    out, _ = ffn_forward(x_shard, params, cfg, for_backward=False)
     return out

@@ -232,3 +232,27 @@ def test_graph_replay_equals_eager(dense):
         torch.cuda.synchronize()
         assert torch.equal(g.out, out)
         assert torch.equal(g.d_x, gr.d_x) and torch.equal(g.d_w1, gr.d_w1) and torch.equal(g.d_w2, gr.d_w2)
+
+
+def test_nn_module_autograd_matches_api():
+    """SquaredReluFFN24 (autograd.Function over ffn_forward/ffn_backward) gives
+    the drop-in API's outputs and gradients; odd token counts are padded."""
+    from paper_2503_16672_b200.nn import SquaredReluFFN24
+
+    torch.manual_seed(5)
+    d, h = 256, 512
+    m = SquaredReluFFN24(d, h)
+    x = torch.randn(3, 341, d, device="cuda").bfloat16().requires_grad_(True)  # 1023 tokens
+    y = m(x)
+    g = torch.randn_like(y)
+    (y.float() * g.float()).sum().backward()
+    # the same through the API on the padded batch
+    xf = torch.cat([x.detach().reshape(-1, d), x.new_zeros(1, d)])
+    gf = torch.cat([g.reshape(-1, d), g.new_zeros(1, d)])
+    p = s24.FfnParams(w1=m.w1.detach(), w2=m.w2.detach())
+    out, cache = s24.ffn_forward(xf, p, s24.RECIPE)
+    gr = s24.ffn_backward(gf, cache, p, s24.RECIPE)
+    assert torch.equal(y.reshape(-1, d), out[:1023])
+    assert torch.equal(x.grad.reshape(-1, d), gr.d_x[:1023])
+    assert torch.equal(m.w1.grad, gr.d_w1) and torch.equal(m.w2.grad, gr.d_w2)
+    assert m.w1.grad.dtype == torch.float32
