@@ -147,6 +147,48 @@ def main():
             if cache.plan is not None:
                 cases[f"{k}_plan_sparse"] = cache.plan.sparse_features
     np.savez_compressed(OUT / "ffn.npz", **cases)
+
+    # ---------------------------------------------------------------- file formats (S24C / S24M)
+    import tempfile
+
+    cases = {}
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        fmt_cases = [("tok", "token", 8, 16, 0.4, 51), ("feat", "feature", 16, 12, 0.4, 52),
+                     ("odd", "token", 3, 4, 0.6, 53)]  # 3 groups: padded last metadata byte
+        for tag, orient, rows, cols, p, seed in fmt_cases:
+            a = bern(rng(seed), rows, cols, p)
+            s, _, _ = (R.sparsify_token_wise(a) if orient == "token" else R.sparsify_feature_wise(a))
+            R.write_sparse(td / f"{tag}.s24c", s)
+            blob = (td / f"{tag}.s24c").read_bytes()
+            back = R.read_sparse(td / f"{tag}.s24c")
+            assert np.array_equal(back.values, s.values) and np.array_equal(back.meta, s.meta)
+            cases[f"{tag}_a"] = a
+            cases[f"{tag}_values"] = s.values
+            cases[f"{tag}_meta"] = s.meta
+            cases[f"{tag}_bytes"] = np.frombuffer(blob, dtype=np.uint8)
+        m = rng(54).standard_normal((5, 7)).astype(np.float32)
+        R.write_matrix(td / "m.s24m", m)
+        cases["mat_a"] = m
+        cases["mat_bytes"] = np.frombuffer((td / "m.s24m").read_bytes(), dtype=np.uint8)
+        # malformed files and the reference's error (message with byte offset)
+        good = (td / "tok.s24c").read_bytes()
+        bad = {"magic": b"XXXX" + good[4:], "short": good[:10], "trunc": good[:-1],
+               "version": good[:4] + (2).to_bytes(4, "little") + good[8:],
+               "orient": good[:8] + bytes([7]) + good[9:]}
+        mgood = (td / "m.s24m").read_bytes()
+        bad.update({"m_magic": b"ABCD" + mgood[4:], "m_trunc": mgood[:-3], "m_trail": mgood + b"\0\0\0\0",
+                    "m_nan": mgood[:16] + np.float32(np.nan).tobytes() + mgood[20:]})
+        for k, blob in bad.items():
+            (td / "bad").write_bytes(blob)
+            try:
+                (R.read_matrix if k.startswith("m_") else R.read_sparse)(td / "bad")
+                err = ""
+            except R.FormatError as e:
+                err = str(e)
+            cases[f"bad_{k}_bytes"] = np.frombuffer(blob, dtype=np.uint8)
+            cases[f"bad_{k}_error"] = np.array(err)
+    np.savez_compressed(OUT / "formats.npz", **cases)
     for f in sorted(OUT.glob("*.npz")):
         print(f, f.stat().st_size)
 
