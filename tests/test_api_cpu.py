@@ -77,3 +77,22 @@ def test_no_cpu_fallback():
         s24.sparsify_token_wise(np.zeros((4, 8), np.float32))
     with pytest.raises(s24.BackendError):
         s24.FfnParams(w1=np.zeros((8, 16), np.float32), w2=np.zeros((16, 8), np.float32))
+
+
+def test_toy_schedule_and_config_validation():
+    import math as _m
+
+    from paper_2503_16672_b200 import toy
+    from paper_2503_16672_b200.errors import ConfigError
+    tc = toy.TrainConfig(steps=100, lr=1.0, lr_warmup_steps=10, warmup_dense_steps=5)
+    assert toy.lr_at(tc, 5) == 0.5 and toy.lr_at(tc, 10) == 1.0
+    assert toy.lr_at(tc, 11) == 1.0 and abs(toy.lr_at(tc, 100)) < 1e-12
+    assert abs(toy.lr_at(tc, 55) - 0.5 * (1 + _m.cos(_m.pi * 44 / 89))) < 1e-12
+    for bad in (dict(batch_tokens=6), dict(steps=10, warmup_dense_steps=11), dict(plan_refresh_every=0)):
+        with pytest.raises(ConfigError):
+            toy.TrainConfig(**bad)
+    with pytest.raises(ConfigError):
+        toy.ToyModelConfig(hidden=100)
+    (tr, ev) = toy.byte_windows(bytes(range(20)), 4, 0.5, "cpu")
+    assert tr[0].shape == (8, 4) and ev[0].shape == (8, 4)
+    assert tr[0][3].tolist() == [3, 4, 5, 6] and int(tr[1][3]) == 7
