@@ -250,6 +250,54 @@ int s24_gemm_relu2(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int
 int s24_gemm_dact(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N, int64_t K,
                   const void* act, int64_t ld_act, void* gpre, int64_t ld_g, void* stream);
 
+/* ---------------------------------------------------------------- e4m3 (fp8) path
+ * FfnConfig.fp8_emulation / fp8_backward (ref pkg/src/srelu24/ffn.py:206-268,
+ * :305, :330-341, :395-447) on the kind::f8f6f4 tensor cores. Quantization
+ * follows ref matcore.py:113-261: scale = amax/448 per row or column (1 when
+ * amax == 0), codes = e4m3(x / scale), round-to-nearest-even, saturating.
+ * "f8 metadata": the e4m3 2:4 operand-E layout, 2048-byte atoms of 128 rows x
+ * 128 logical columns with row r's 16 bytes at 16*r (same size as hw). */
+
+/* per-row (rows < pair_rows: per (even, odd) row pair) e4m3 codes + scales of
+ * an fp32/bf16 [rows, cols] matrix; amax_in (nullable, float bits) supplies
+ * precomputed row maxima; deq_bf16 / raw_bf16 (nullable) receive the bf16
+ * dequantized (code * scale) / unquantized images. ref matcore.py:203-225,
+ * ffn.py:221-237. */
+int s24_fp8_quant_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ld_in,
+                       const unsigned* amax_in, int64_t pair_rows, uint8_t* codes, int64_t ld_codes, float* scales,
+                       void* deq_bf16, int64_t ld_deq, void* raw_bf16, int64_t ld_raw, void* stream);
+/* per-column codes of a bf16 [rows, cols] matrix, written transposed
+ * codes_t[cols, rows] (the K-major operand), scales[cols]; amax_ws: cols
+ * uint32 of workspace. ref matcore.py:203-225 with axis="cols". */
+int s24_fp8_quant_cols_t(const void* in_bf16, int64_t rows, int64_t cols, int64_t ld_in, uint8_t* codes_t,
+                         int64_t ld_out, float* scales, unsigned* amax_ws, void* stream);
+/* hw metadata -> f8 metadata (same logical content) */
+int s24_meta_hw_to_f8(const uint8_t* meta_hw, int64_t rows, int64_t kdim, uint8_t* meta_f8, void* stream);
+/* elementwise e4m3 encode of fp32 values (ref matcore.py:155-197) */
+int s24_e4m3_encode(const float* x, int64_t n, uint8_t* codes, void* stream);
+/* D = (row_scale[i] * col_scale[j]) * sum_k A[i,k] B[j,k] over e4m3 codes
+ * (A [M,K], B [N,K], both K-major): ref matcore.py:238-258 */
+int s24_gemm_f8(const uint8_t* A, int64_t lda, const uint8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                const float* row_scale, const float* col_scale, void* D, int out_dtype, int64_t ldd,
+                const int* d_row_map, int d_transposed, int64_t d_rows_valid, void* stream);
+/* the same with a 2:4 A: codes [Mpad, K/2] + f8 metadata; K % 128 == 0.
+ * ref ffn.py:240-255 (_sp_mm / _sp_mm_t) and the split weight gradient. */
+int s24_spmm_f8(const uint8_t* a_codes, const uint8_t* a_meta_f8, const uint8_t* B, int64_t ldb, int64_t M,
+                int64_t N, int64_t K, const float* row_scale, const float* col_scale, void* D, int out_dtype,
+                int64_t ldd, const int* d_row_map, int d_transposed, int64_t d_rows_valid, const int* d_row_valid,
+                int64_t pair_rows, void* stream);
+/* K1 on e4m3 operands (W1 codes as [N, K]): y = (sx * s1) * acc, then as
+ * s24_fwd_gemm1_fused but the kept values go out fp32 [Mpad, N/2] with the
+ * per-row max kept value in row_amax (float bits, zeroed by the caller) */
+int s24_fwd_gemm1_f8(const uint8_t* xq, int64_t ldx, const uint8_t* w1q, int64_t ldw1, int64_t M, int64_t N,
+                     int64_t K, const float* x_scale, const float* w1_scale, float* act_vals32, unsigned* row_amax,
+                     uint8_t* act_meta, int* counts, unsigned long long* stats, float* y_dbg, void* stream);
+/* K3 on e4m3 operands (W2 codes as [N=h, K=d]): G = (sg * s2) * acc, then as
+ * s24_bwd_dact_fused without the fused feature-wise output */
+int s24_bwd_dact_f8(const uint8_t* gq, int64_t ldg, const uint8_t* w2q, int64_t ldw2, int64_t M, int64_t N,
+                    int64_t K, const float* g_scale, const float* w2_scale, const void* act_vals,
+                    const uint8_t* act_meta, void* g_vals, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,11 +36,15 @@ def stats_arr(st):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
+    ap.add_argument("--only", default="", help="regenerate one fixture set (e.g. fp8)")
     args = ap.parse_args()
     sys.path.insert(0, args.ref)
     import srelu24 as R  # the reference package
 
     OUT.mkdir(parents=True, exist_ok=True)
+    if args.only == "fp8":
+        make_fp8(R)
+        return
 
     # ---------------------------------------------------------------- sparsifiers
     cases = {}
@@ -191,6 +195,78 @@ def main():
     np.savez_compressed(OUT / "formats.npz", **cases)
     for f in sorted(OUT.glob("*.npz")):
         print(f, f.stat().st_size)
+
+
+def make_fp8(R):
+    """e4m3 encode / quantize / GEMM known answers and the fp8 FFN configs
+    (ref matcore.py:113-261, ffn.py:206-268)."""
+    from srelu24 import matcore as RM
+
+    cases = {}
+    dec = RM._E4M3_DECODE
+    finite = dec[~np.isnan(dec)]
+    pos = np.unique(np.abs(finite))
+    mids = (pos[1:] + pos[:-1]) / 2
+    r = rng(300)
+    xs = np.concatenate([finite, mids, -mids, pos * 1.0001, pos * 0.9999, [1e9, -1e9, 449.0, 464.0, 480.0, 2.0**-10,
+                         -2.0**-10, 2.0**-11, 3 * 2.0**-11, -0.0, 0.0]],
+                        ).astype(np.float64)
+    xs = np.concatenate([xs, r.standard_normal(4096) * 10.0 ** r.uniform(-4, 3, 4096)])
+    cases["enc_x"] = xs
+    cases["enc_codes"] = RM.e4m3_encode(xs)
+    cases["dec_table"] = dec
+    for i, (rows, cols, seed, zero_row) in enumerate([(16, 32, 301, True), (8, 64, 302, False), (33, 40, 303, True)]):
+        a = rng(seed).standard_normal((rows, cols)).astype(np.float32) * np.float32(10.0 ** (i - 1))
+        if zero_row:
+            a[1] = 0.0
+            a[:, 2] = 0.0
+        for axis in ("rows", "cols"):
+            q = R.fp8_quantize_rowwise(a, axis)
+            cases[f"q{i}_{axis}_codes"] = q.codes
+            cases[f"q{i}_{axis}_scales"] = q.scales
+        cases[f"q{i}_a"] = a
+    a = rng(109).uniform(-1, 1, (32, 48)).astype(np.float32)
+    b = rng(110).uniform(-1, 1, (48, 24)).astype(np.float32)
+    cases["gemm_a"], cases["gemm_b"] = a, b
+    cases["gemm_out"] = R.fp8_gemm_rowwise(R.fp8_quantize_rowwise(a, "rows"), R.fp8_quantize_rowwise(b, "cols"))
+    recipe = dict(forward_mode="sparse24", backward_mode="split_masked", mask_grad_with_fwd=True, permute_tokens=True)
+    configs = {
+        "recipe_f8fwd": R.FfnConfig(**recipe, fp8_emulation=True),
+        "recipe_f8all": R.FfnConfig(**recipe, fp8_emulation=True, fp8_backward=True),
+        "dense_f8all": R.FfnConfig(fp8_emulation=True, fp8_backward=True),
+        "naive_f8all": R.FfnConfig(forward_mode="sparse24", backward_mode="naive_sparse", mask_grad_with_fwd=True,
+                                   fp8_emulation=True, fp8_backward=True),
+        "split_nomask_f8all": R.FfnConfig(forward_mode="sparse24", backward_mode="split_masked", fp8_emulation=True,
+                                          fp8_backward=True),
+    }
+    for shape_i, (n, d, h) in enumerate([(32, 8, 16), (64, 32, 64)]):
+        rr = rng(400 + shape_i)
+        x = rr.standard_normal((n, d)).astype(np.float32)
+        w1 = (rr.standard_normal((d, h)) / np.sqrt(d)).astype(np.float32)
+        w2 = (rr.standard_normal((h, d)) / np.sqrt(h)).astype(np.float32)
+        g = rr.standard_normal((n, d)).astype(np.float32)
+        p = R.FfnParams(w1=w1, w2=w2)
+        tag = f"s{shape_i}"
+        cases[f"{tag}_x"], cases[f"{tag}_w1"], cases[f"{tag}_w2"], cases[f"{tag}_g"] = x, w1, w2, g
+        for name, cfg in configs.items():
+            out, cache = R.ffn_forward(x, p, cfg)
+            grads = R.ffn_backward(g, cache, p, cfg)
+            k = f"{tag}_{name}"
+            cases[f"{k}_out"] = out
+            cases[f"{k}_d_w1"] = grads.d_w1
+            cases[f"{k}_d_w2"] = grads.d_w2
+            cases[f"{k}_d_x"] = grads.d_x
+            if cache.act_sparse is not None:
+                cases[f"{k}_act_values"] = cache.act_sparse.values
+    # the reference's known answer: selection sees the unquantized values
+    # (ref tests/test_ffn.py:360-367)
+    p = R.FfnParams(w1=np.eye(4, dtype=np.float32), w2=np.eye(4, dtype=np.float32))
+    x = np.array([[3.01, 3.0, 2.99, -1.0]] * 4, np.float32)
+    _, cache = R.ffn_forward(x, p, R.FfnConfig(forward_mode="sparse24", fp8_emulation=True))
+    cases["kat_sel_x"] = x
+    cases["kat_sel_meta"] = cache.act_sparse.meta
+    np.savez_compressed(OUT / "fp8.npz", **cases)
+    print(OUT / "fp8.npz", (OUT / "fp8.npz").stat().st_size)
 
 
 if __name__ == "__main__":

@@ -137,6 +137,120 @@ def decompress_feature(vals: np.ndarray, meta: np.ndarray, rows: int, cols: int)
     return np.ascontiguousarray(out.transpose(0, 2, 1)).reshape(rows, cols)
 
 
+# ---------------------------------------------------------------- e4m3 (fp8)
+
+E4M3_MAX = 448.0
+
+
+def e4m3_values() -> np.ndarray:
+    """float64 value of every code (ref matcore.py:113-145): sign | 4-bit
+    exponent (bias 7) | 3-bit mantissa, subnormals at exponent 0, NaN only at
+    S.1111.111, no infinities; 0x80 is -0."""
+    c = np.arange(256)
+    e, m = (c >> 3) & 0xF, c & 7
+    mag = np.where(e == 0, m * 2.0**-9, np.ldexp(1.0 + m / 8.0, e - 7))
+    v = np.where(c & 0x80, -mag, mag)
+    v[(e == 15) & (m == 7)] = np.nan
+    return v
+
+
+_E4M3 = e4m3_values()
+_E4M3_F32 = _E4M3.astype(np.float32)
+_E4M3_GRID = _E4M3[:127]  # codes 0x00..0x7E: the non-negative finite values, increasing
+
+
+def e4m3_encode(x) -> np.ndarray:
+    """Nearest code, ties to the even code (= even mantissa), magnitudes above
+    448 saturate to 0x7E, sign from the sign bit (ref matcore.py:155-197). A
+    nearest-neighbour search on the value grid rather than the reference's
+    frexp arithmetic; pinned against it in tests/golden/fp8.npz."""
+    xf = np.asarray(x, dtype=np.float64)
+    if not np.all(np.isfinite(xf)):
+        raise ValueError("e4m3_encode requires finite input")
+    ax = np.minimum(np.abs(xf), E4M3_MAX)
+    hi = np.clip(np.searchsorted(_E4M3_GRID, ax, side="left"), 1, 126)
+    lo = hi - 1
+    dlo, dhi = ax - _E4M3_GRID[lo], _E4M3_GRID[hi] - ax
+    code = np.where(dlo < dhi, lo, np.where(dhi < dlo, hi, np.where(lo % 2 == 0, lo, hi)))
+    code = np.where(ax == 0, 0, code)
+    return (code | np.where(np.signbit(xf), 0x80, 0)).astype(np.uint8)
+
+
+def e4m3_scales(amax: np.ndarray) -> np.ndarray:
+    """amax / 448 in float32, 1 for zero or underflowing slices (ref
+    matcore.py:214-220)."""
+    amax = np.asarray(amax, dtype=np.float32)
+    s = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
+    return np.where(s > 0, s, np.float32(1.0)).astype(np.float32)
+
+
+def quantize(a: np.ndarray, axis: str):
+    """Per-row ("rows") or per-column ("cols") e4m3 codes and float32 scales of
+    a float32 matrix (ref matcore.py:203-225)."""
+    red = 1 if axis == "rows" else 0
+    amax = np.max(np.abs(a), axis=red) if a.shape[red] else np.zeros(a.shape[1 - red], np.float32)
+    sc = e4m3_scales(amax)
+    den = sc[:, None] if axis == "rows" else sc[None, :]
+    return e4m3_encode(a / den).reshape(a.shape), sc
+
+
+def quantize_groups(vals: np.ndarray, axes) -> tuple:
+    """Scales over the kept values of a compressed matrix (token-wise: axes
+    (1, 2) per row; feature-wise: (0, 2) per column) and the values snapped to
+    the e4m3 grid, unscaled (ref ffn.py:221-237)."""
+    if vals.size == 0:
+        return vals, np.ones(vals.shape[0] if axes == (1, 2) else vals.shape[1], np.float32)
+    amax = np.max(np.abs(vals), axis=axes)
+    sc = e4m3_scales(amax)
+    den = sc[:, None, None] if axes == (1, 2) else sc[None, :, None]
+    return _E4M3_F32[e4m3_encode(vals / den)], sc
+
+
+def mm_f8(a, b, ordered=True):
+    """(sa x sb) * (decode(qa) @ decode(qb)), a per row, b per column
+    (ref ffn.py:206-209, matcore.py:238-258)."""
+    qa, sa = quantize(a, "rows")
+    qb, sb = quantize(b, "cols")
+    return (sa[:, None] * sb[None, :]) * gemm(_E4M3_F32[qa], _E4M3_F32[qb], ordered)
+
+
+def mm_at_f8(a, b, ordered=True):
+    """a^T b with both operands per column (ref ffn.py:212-218)."""
+    qa, sa = quantize(a, "cols")
+    qb, sb = quantize(b, "cols")
+    return (sa[:, None] * sb[None, :]) * gemm_at(_E4M3_F32[qa], _E4M3_F32[qb], ordered)
+
+
+def sp_mm_f8(vals, meta, rows, cols, b, ordered=True):
+    """token-wise 2:4 (per-row scales) times b (per-column), ref ffn.py:240-246"""
+    grid, sr = quantize_groups(vals, (1, 2))
+    qb, sb = quantize(b, "cols")
+    acc = gemm(decompress_token(grid, meta, rows, cols), _E4M3_F32[qb], ordered)
+    return (sr[:, None] * sb[None, :]) * acc
+
+
+def sp_mm_t_f8(vals, meta, rows, cols, b, ordered=True):
+    """feature-wise 2:4 transposed (per-feature scales) times b, ref ffn.py:249-255"""
+    grid, sc = quantize_groups(vals, (0, 2))
+    qb, sb = quantize(b, "cols")
+    acc = gemm_at(decompress_feature(grid, meta, rows, cols), _E4M3_F32[qb], ordered)
+    return (sc[:, None] * sb[None, :]) * acc
+
+
+def split_mm_t_f8(a, mask, b, sparse, dense, ordered=True):
+    """ref ffn.py:258-270: masked a; sparse features through sp_mm_t_f8, dense
+    features through mm_at_f8 (each quantized on its own slice)."""
+    am = np.where(mask, a, a.dtype.type(0))
+    out = np.zeros((a.shape[1], b.shape[1]), dtype=a.dtype)
+    if len(sparse):
+        sub = np.ascontiguousarray(am[:, sparse])
+        v, m, _, _ = sparsify_feature(sub)
+        out[sparse] = sp_mm_t_f8(v, m, *sub.shape, b, ordered)
+    if len(dense):
+        out[dense] = mm_at_f8(np.ascontiguousarray(am[:, dense]), b, ordered)
+    return out
+
+
 # ---------------------------------------------------------------- split plan
 
 
@@ -213,16 +327,17 @@ DENSE = dict(forward_mode="dense", backward_mode="dense", mask_grad_with_fwd=Fal
 
 
 def ffn_forward(x, w1, w2, cfg, plan=None, ordered=True):
-    """Squared-ReLU FFN forward (ref ffn.py:276-363, squared_relu, no fp8).
-    Returns (out, cache dict)."""
+    """Squared-ReLU FFN forward (ref ffn.py:276-363, squared_relu), with the
+    e4m3 emulation when cfg["fp8_emulation"]. Returns (out, cache dict)."""
     n = x.shape[0]
+    fp8 = cfg.get("fp8_emulation", False)
     sparse_fwd = cfg["forward_mode"] == "sparse24"
     perm = None
     x_in = x
     if cfg["permute_tokens"] and sparse_fwd:
         perm = make_permutation(cfg["permute_seed"], n)
         x_in = permute_rows(x, perm)
-    pre = gemm(x_in, w1, ordered)
+    pre = mm_f8(x_in, w1, ordered) if fp8 else gemm(x_in, w1, ordered)
     r = np.maximum(pre, pre.dtype.type(0))
     act = r * r
     counts = column_counts(act)
@@ -232,19 +347,31 @@ def ffn_forward(x, w1, w2, cfg, plan=None, ordered=True):
                  act=None, stats=None)
     if sparse_fwd:
         vals, meta, mask, st = sparsify_token(act)
-        kept = decompress_token(vals, meta, *act.shape)
-        out_c = gemm(kept, w2, ordered)
+        if fp8:
+            # quantize after selection (ref ffn.py:330-341): the backward sees
+            # the dequantized values
+            grid, sr = quantize_groups(vals, (1, 2))
+            qw2, s2 = quantize(w2, "cols")
+            out_c = (sr[:, None] * s2[None, :]) * gemm(decompress_token(grid, meta, *act.shape), _E4M3_F32[qw2],
+                                                       ordered)
+            vals = grid * sr[:, None, None]
+            kept = decompress_token(vals, meta, *act.shape)
+        else:
+            kept = decompress_token(vals, meta, *act.shape)
+            out_c = gemm(kept, w2, ordered)
         cache.update(mask=mask, vals=vals, meta=meta, act=kept, stats=st)
     else:
-        out_c = gemm(act, w2, ordered)
+        out_c = mm_f8(act, w2, ordered) if fp8 else gemm(act, w2, ordered)
         cache.update(act=act)
     out = inverse_permute_rows(out_c, perm) if perm is not None else out_c
     return out, cache
 
 
 def ffn_backward(g_out, cache, w1, w2, cfg, ordered=True):
-    """Six-GEMM backward (ref ffn.py:366-451, squared_relu, no fp8).
-    Returns dict(d_w1, d_w2, d_x, fstats_act, fstats_g)."""
+    """Six-GEMM backward (ref ffn.py:366-451, squared_relu), e4m3 GEMMs when
+    cfg["fp8_backward"]. Returns dict(d_w1, d_w2, d_x, fstats_act, fstats_g)."""
+    if cfg.get("fp8_backward", False):
+        return _ffn_backward_f8(g_out, cache, w1, w2, cfg, ordered)
     perm = cache["perm"]
     g_c = permute_rows(g_out, perm) if perm is not None else g_out
     g_act = gemm(g_c, np.ascontiguousarray(w2.T), ordered)
@@ -271,6 +398,37 @@ def ffn_backward(g_out, cache, w1, w2, cfg, ordered=True):
     d_x = inverse_permute_rows(d_x_c, perm) if perm is not None else d_x_c
     return dict(d_w1=np.ascontiguousarray(d_w1), d_w2=d_w2, d_x=d_x, g_pre=g_pre, fstats_act=fst_a,
                 fstats_g=fst_g)
+
+
+def _ffn_backward_f8(g_out, cache, w1, w2, cfg, ordered=True):
+    """ref ffn.py:389-447 with fp8b: every GEMM through the e4m3 emulation."""
+    perm = cache["perm"]
+    g_c = permute_rows(g_out, perm) if perm is not None else g_out
+    g_act = mm_f8(g_c, np.ascontiguousarray(w2.T), ordered)
+    g_pre = g_act * (2 * np.maximum(cache["pre"], cache["pre"].dtype.type(0)))
+    if cfg["mask_grad_with_fwd"]:
+        g_pre = np.where(cache["mask"], g_pre, g_pre.dtype.type(0))
+    act = cache["act"]
+    mode = cfg["backward_mode"]
+    if mode == "dense":
+        d_w2 = mm_at_f8(act, g_c, ordered)
+        d_w1 = mm_at_f8(cache["x_in"], g_pre, ordered)
+    elif mode == "naive_sparse":
+        v, m, _, _ = sparsify_feature(act)
+        d_w2 = sp_mm_t_f8(v, m, *act.shape, g_c, ordered)
+        v, m, _, _ = sparsify_feature(g_pre)
+        d_w1 = sp_mm_t_f8(v, m, *g_pre.shape, cache["x_in"], ordered).T
+    else:
+        sp, de = cache["plan"]
+        d_w2 = split_mm_t_f8(act, cache["mask"], g_c, sp, de, ordered)
+        d_w1 = split_mm_t_f8(g_pre, cache["mask"], cache["x_in"], sp, de, ordered).T
+    if cfg["mask_grad_with_fwd"]:
+        v, m = compress_with_mask(g_pre, cache["mask"])
+        d_x_c = sp_mm_f8(v, m, *g_pre.shape, np.ascontiguousarray(w1.T), ordered)
+    else:
+        d_x_c = mm_f8(g_pre, np.ascontiguousarray(w1.T), ordered)
+    d_x = inverse_permute_rows(d_x_c, perm) if perm is not None else d_x_c
+    return dict(d_w1=np.ascontiguousarray(d_w1), d_w2=d_w2, d_x=d_x, g_pre=g_pre, fstats_act=None, fstats_g=None)
 
 
 # ---------------------------------------------------------------- synthetic inputs (SURVEY §8d)

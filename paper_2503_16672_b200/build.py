@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB = PKG_DIR / "libs24.so"
-SOURCES = ["gemm_capi.cu", "sparse_capi.cu"]
+SOURCES = ["gemm_capi.cu", "sparse_capi.cu", "fp8.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

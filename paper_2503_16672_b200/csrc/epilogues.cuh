@@ -62,7 +62,9 @@ __device__ __forceinline__ uint32_t warp_bit_transpose(uint32_t x, uint32_t lane
 // bf16 or fp32. Used for fwd.out / bwd.d_x (row_map = inverse permutation),
 // the dense twins, and the split weight-gradient GEMMs (row_map = feature
 // index list of the partition, transposed for dW1).
-template <typename OutT>
+// SCALED: e4m3 GEMMs, D = (row_scale[row] * col_scale[col]) * acc (the
+// reference's order, ref matcore.py:257-258), applied before any pair sum.
+template <typename OutT, bool SCALED = false>
 struct EpiStore {
   struct Params {
     OutT* out;
@@ -74,6 +76,8 @@ struct EpiStore {
     long long split_stride;  // split-K: partial of split ks goes to out + ks * split_stride
     int pair_rows;           // rows < pair_rows come in (even, odd) pairs: their sum is the even row's
                              // output (a dense feature stored as two 2:4 rows, see k4.cuh)
+    const float* row_scale;  // SCALED only: [M] per GEMM row
+    const float* col_scale;  // SCALED only: [N]
   };
   struct State {
     long long split_off;
@@ -87,8 +91,14 @@ struct EpiStore {
   __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int,
                                const float (&v_in)[32], uint32_t lane) {
     float v[32];
+    if constexpr (SCALED) {
+      const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = v_in[i];
+      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(sr, __ldg(p.col_scale + col0 + i)), v_in[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = v_in[i];
+    }
     // (warp-uniform test: every lane of the warp calls chunk)
     if (__any_sync(0xffffffffu, row < p.pair_rows)) {
 #pragma unroll
@@ -138,7 +148,12 @@ struct EpiStore {
 // Selection: with a >= 0, pairwise FSET masks b_ij (i < j: i beats j iff
 // a_i >= a_j, ties to the lower index); "kept iff it beats two of the other
 // three" is a bitwise majority; values are picked with bitwise selects.
-struct EpiFwd1 {
+// F8 (e4m3 K1, ref ffn.py:305 + :330-341): y = (row_scale[r] * col_scale[c]) * acc;
+// the kept values go out as fp32 (vals32) with a per-row running max of the
+// kept |a| (row_amax, float bits, atomicMax) for the per-token quantization
+// that follows (fp8.cu); the bf16 vals are not written.
+template <bool F8>
+struct EpiFwd1T {
   struct Params {
     __nv_bfloat16* vals;  // [Mpad, N/2]
     uint8_t* meta;        // hw layout, K = N
@@ -149,6 +164,10 @@ struct EpiFwd1 {
     FwTarget fw;          // fused feature-wise selection (fw.vals == nullptr: off)
     const int* row_map;   // nullable: input row r is written as output row row_map[r]
                           // (the token permutation applied on the way out)
+    const float* row_scale;  // F8 only
+    const float* col_scale;
+    float* vals32;           // F8 only: [Mpad, N/2]
+    unsigned* row_amax;      // F8 only: [Mpad], zeroed before the launch
   };
   struct State {
     unsigned long long before, after;
@@ -171,7 +190,16 @@ struct EpiFwd1 {
     }
   }
   __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int,
-                               const float (&v)[32], uint32_t lane) {
+                               const float (&v_in)[32], uint32_t lane) {
+    float v[32];
+    if constexpr (F8) {
+      const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(sr, __ldg(p.col_scale + col0 + i)), v_in[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = v_in[i];
+    }
     float a[32];
     uint32_t nz = 0;
 #pragma unroll
@@ -190,6 +218,7 @@ struct EpiFwd1 {
       if (col_bits) atomicAdd(p.counts + col0 + lane, __popc(col_bits));
     }
     uint32_t packed[8];
+    float kept[16];
     uint32_t m16[2] = {0u, 0u};
     uint32_t keep32 = 0;
 #pragma unroll
@@ -204,11 +233,18 @@ struct EpiFwd1 {
                      u3 = __float_as_uint(a3);
       const float v0 = __uint_as_float(bsel(K0, u0, bsel(K1, u1, u2)));  // first kept
       const float v1 = __uint_as_float(bsel(K3, u3, bsel(K2, u2, u1)));  // second kept
-      packed[g] = pack_bf16x2(v0, v1);
+      if constexpr (F8) {
+        kept[2 * g] = v0;
+        kept[2 * g + 1] = v1;
+      } else {
+        packed[g] = pack_bf16x2(v0, v1);
+      }
       m16[g >> 2] |= keep_nibble(kb) << (4 * (g & 3));
       keep32 |= kb << (4 * g);
     }
-    if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
+    if constexpr (!F8) {
+      if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
+    }
     if (!row_ok) return;
     s.before += __popc(nz);
     s.after += __popc(nz & keep32);
@@ -217,9 +253,21 @@ struct EpiFwd1 {
       return;
     }
     const int drow = s.drow;
-    __nv_bfloat16* dst = p.vals + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
-    st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
-    st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
+    if constexpr (F8) {
+      float* dst = p.vals32 + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
+      float mx = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) {
+        st_global_v4(dst + i, __float_as_uint(kept[i]), __float_as_uint(kept[i + 1]), __float_as_uint(kept[i + 2]),
+                     __float_as_uint(kept[i + 3]));
+        mx = fmaxf(mx, fmaxf(fmaxf(kept[i], kept[i + 1]), fmaxf(kept[i + 2], kept[i + 3])));
+      }
+      if (mx > 0.f) atomicMax(p.row_amax + drow, __float_as_uint(mx));  // a >= 0: uint order = float order
+    } else {
+      __nv_bfloat16* dst = p.vals + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
+      st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
+      st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
+    }
     uint16_t* mh = reinterpret_cast<uint16_t*>(p.meta);
     st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16, p.N) / 2, static_cast<uint16_t>(m16[0]));
     st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16 + 1, p.N) / 2, static_cast<uint16_t>(m16[1]));
@@ -233,6 +281,8 @@ struct EpiFwd1 {
   }
 };
 
+using EpiFwd1 = EpiFwd1T<false>;
+
 // ---------------------------------------------------------------------------
 // K3: bwd.d_act epilogue. G = acc (= dY_c . W2^T). On the forward keep pattern
 // only (ref ffn.py:415-417 + sparse24.py:138-154, exact by construction):
@@ -242,7 +292,9 @@ struct EpiFwd1 {
 // The warp's act values (CPW chunks x 32 B / row) and metadata rows are
 // prefetched into registers before the accumulator wait, so their latency
 // hides under the MMA.
-struct EpiBwd1 {
+// F8 (fp8_backward, ref ffn.py:395): G = (row_scale[r] * col_scale[c]) * acc.
+template <bool F8>
+struct EpiBwd1T {
   struct Params {
     const __nv_bfloat16* act_vals;  // [Mpad, N/2]
     const uint8_t* meta;            // hw layout, K = N
@@ -250,6 +302,8 @@ struct EpiBwd1 {
     int N;
     FwTarget fw;                    // fused feature-wise selection of g_pre (fw.vals == nullptr: off)
     const int* row_map;             // nullable: input row r <-> act / g_pre row row_map[r]
+    const float* row_scale;         // F8 only
+    const float* col_scale;
   };
   static constexpr int CPW = 4;  // chunks per epilogue warp (BN = 256, 8 epilogue warps)
   static constexpr bool kUnroll = true;
@@ -278,7 +332,16 @@ struct EpiBwd1 {
   }
   __device__ static uint32_t word(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
   __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int ci,
-                               const float (&v)[32], uint32_t lane) {
+                               const float (&v_in)[32], uint32_t lane) {
+    float v[32];
+    if constexpr (F8) {
+      const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(sr, __ldg(p.col_scale + col0 + i)), v_in[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = v_in[i];
+    }
     if (!row_ok) {
       if (p.fw.vals) {
         const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -307,6 +370,8 @@ struct EpiBwd1 {
     st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
   }
 };
+
+using EpiBwd1 = EpiBwd1T<false>;
 
 // ---------------------------------------------------------------------------
 // Dense-mode twins. fwd: act = relu(y)^2 stored dense bf16 (ref ffn.py:314).

@@ -1,0 +1,326 @@
+// e4m3 quantization for the fp8 FFN path (FfnConfig.fp8_emulation /
+// fp8_backward) and the metadata layout the e4m3 2:4 MMA reads.
+//
+// Reference semantics (ref pkg/src/srelu24/matcore.py:113-261, ffn.py:206-268):
+//   scale = amax / 448 per row (or column), 1 where amax == 0 or the division
+//   underflows; code = e4m3(x / scale) rounded to nearest, ties to even
+//   mantissa, saturating at +-448 (no infinities), -0 -> 0x80.
+// cvt.rn.satfinite.e4m3x2.f32 is exactly that rounding of the fp32 quotient,
+// and the quotient is the IEEE fp32 division the reference performs, so codes
+// and scales are bit-identical to the reference on identical fp32 inputs.
+//
+// Kernels (all HBM-bound, one pass over the operand plus its output):
+//   k_quant_rows    per-row (or per row pair) scales, codes in place of the
+//                   row; optional bf16 dequantized image (what an 8-bit store
+//                   reproduces, ref ffn.py:335-340) and bf16 raw image
+//   k_col_amax +    per-column scales with the codes written TRANSPOSED
+//   k_quant_cols_t  ([C, R]: the K-major operand layout the e4m3 MMA needs)
+//   k_meta_to_f8    2:4 metadata atoms, kind::f16 layout -> kind::f8f6f4 layout
+//   k_e4m3_encode   elementwise encode (parity tests of the conversion)
+#include <cuda_bf16.h>
+
+#include <type_traits>
+
+#include "host_util.h"
+#include "meta.cuh"
+
+namespace s24 {
+
+constexpr float kE4m3Max = 448.f;
+
+__device__ __forceinline__ float e4m3_scale(float amax) {
+  float s = amax > 0.f ? __fdiv_rn(amax, kE4m3Max) : 1.f;
+  return s > 0.f ? s : 1.f;
+}
+
+// two fp32 -> two e4m3 codes (lo in the low byte)
+__device__ __forceinline__ uint32_t e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ float e4m3_decode(uint32_t code) {
+  // exact: e4m3 -> f16x2 (hardware) -> f32
+  uint32_t h2;
+  const uint16_t c = static_cast<uint16_t>(code & 0xFFu);
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(c));
+  float f;
+  asm("{ .reg .f16 lo, hi; mov.b32 {lo, hi}, %1; cvt.f32.f16 %0, lo; }" : "=f"(f) : "r"(h2));
+  return f;
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&v)[8]) {
+  if constexpr (std::is_same_v<T, float>) {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// One warp per unit: a single row, or (rows < pair_rows) an (even, odd) row
+// pair sharing one scale (a dense feature stored as two 2:4 rows, k4.cuh).
+// cols % 8 == 0; every row pointer 16-byte aligned.
+template <typename InT>
+__global__ void __launch_bounds__(256) k_quant_rows(const InT* __restrict__ in, long long ld_in, int rows, int cols,
+                                                    const unsigned* __restrict__ amax_in, int pair_rows,
+                                                    uint8_t* __restrict__ codes, long long ld_codes,
+                                                    float* __restrict__ scales, __nv_bfloat16* __restrict__ deq,
+                                                    long long ld_deq, __nv_bfloat16* __restrict__ raw,
+                                                    long long ld_raw) {
+  const int lane = threadIdx.x & 31;
+  const int units = pair_rows / 2 + (rows - pair_rows);
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < units; u += (gridDim.x * blockDim.x) >> 5) {
+    const int r0 = u < pair_rows / 2 ? 2 * u : u + pair_rows / 2;
+    const int nr = u < pair_rows / 2 ? 2 : 1;
+    float amax = 0.f;
+    if (amax_in) {
+      for (int k = 0; k < nr; ++k) amax = fmaxf(amax, __uint_as_float(amax_in[r0 + k]));
+    } else {
+      for (int k = 0; k < nr; ++k) {
+        const InT* src = in + static_cast<long long>(r0 + k) * ld_in;
+        for (int c = 8 * lane; c < cols; c += 256) {
+          float v[8];
+          load8(src + c, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    const float s = e4m3_scale(amax);
+    if (lane == 0)
+      for (int k = 0; k < nr; ++k) scales[r0 + k] = s;
+    for (int k = 0; k < nr; ++k) {
+      const long long r = r0 + k;
+      const InT* src = in + r * ld_in;
+      for (int c = 8 * lane; c < cols; c += 256) {
+        float v[8];
+        load8(src + c, v);
+        uint32_t q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = e4m3x2(__fdiv_rn(v[2 * i], s), __fdiv_rn(v[2 * i + 1], s));
+        *reinterpret_cast<uint2*>(codes + r * ld_codes + c) = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
+        if (deq) {
+          uint32_t o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            o[i] = bf16x2_bits(__fmul_rn(e4m3_decode(q[i]), s), __fmul_rn(e4m3_decode(q[i] >> 8), s));
+          *reinterpret_cast<uint4*>(deq + r * ld_deq + c) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        if (raw) {
+          *reinterpret_cast<uint4*>(raw + r * ld_raw + c) =
+              make_uint4(bf16x2_bits(v[0], v[1]), bf16x2_bits(v[2], v[3]), bf16x2_bits(v[4], v[5]),
+                         bf16x2_bits(v[6], v[7]));
+        }
+      }
+    }
+  }
+}
+
+// column |max| of a bf16 [R, C] matrix into amax[C] (float bits, atomicMax;
+// zeroed by the caller). Block: 32 x 8 threads, 256 columns x rows_per_block.
+__global__ void __launch_bounds__(256) k_col_amax(const __nv_bfloat16* __restrict__ in, long long ld, int R, int C,
+                                                  int rows_per_block, unsigned* __restrict__ amax) {
+  __shared__ float red[8][256 + 8];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * 256 + 8 * tx;
+  const int rb = blockIdx.y * rows_per_block;
+  const int re = min(R, rb + rows_per_block);
+  float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 + 8 <= C) {
+    for (int r = rb + ty; r < re; r += 8) {
+      float v[8];
+      load8(in + static_cast<long long>(r) * ld + c0, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], fabsf(v[i]));
+    }
+  } else {
+    for (int r = rb + ty; r < re; r += 8)
+      for (int i = 0; i < 8 && c0 + i < C; ++i)
+        m[i] = fmaxf(m[i], fabsf(__bfloat162float(in[static_cast<long long>(r) * ld + c0 + i])));
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[ty][8 * tx + i] = m[i];
+  __syncthreads();
+  const int c = threadIdx.x;  // 0..255
+  float x = red[0][c];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) x = fmaxf(x, red[k][c]);
+  if (blockIdx.x * 256 + c < C && x > 0.f) atomicMax(amax + blockIdx.x * 256 + c, __float_as_uint(x));
+}
+
+// codes_t[c, r] = e4m3(in[r, c] / scale[c]); 64 x 64 tiles through shared
+// memory so both the bf16 reads and the code writes are row-contiguous.
+__global__ void __launch_bounds__(256) k_quant_cols_t(const __nv_bfloat16* __restrict__ in, long long ld, int R,
+                                                      int C, const unsigned* __restrict__ amax,
+                                                      uint8_t* __restrict__ out, long long ld_out,
+                                                      float* __restrict__ scales) {
+  __shared__ uint8_t tile[64][64 + 16];
+  __shared__ float sc[64];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const int t = threadIdx.x;
+  if (t < 64) {
+    const float s = (c0 + t < C) ? e4m3_scale(__uint_as_float(amax[c0 + t])) : 1.f;
+    sc[t] = s;
+    if (blockIdx.y == 0 && c0 + t < C) scales[c0 + t] = s;
+  }
+  __syncthreads();
+  {
+    const int rr = t >> 2, cc = (t & 3) * 16;  // one row, 16 columns
+    const int r = r0 + rr;
+    float v[16];
+    if (r < R && c0 + cc + 16 <= C) {
+      float a[8], b[8];
+      load8(in + static_cast<long long>(r) * ld + c0 + cc, a);
+      load8(in + static_cast<long long>(r) * ld + c0 + cc + 8, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = a[i];
+        v[8 + i] = b[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        v[i] = (r < R && c0 + cc + i < C) ? __bfloat162float(in[static_cast<long long>(r) * ld + c0 + cc + i]) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      const uint32_t q = e4m3x2(__fdiv_rn(v[i], sc[cc + i]), __fdiv_rn(v[i + 1], sc[cc + i + 1]));
+      tile[cc + i][rr] = static_cast<uint8_t>(q & 0xFFu);
+      tile[cc + i + 1][rr] = static_cast<uint8_t>(q >> 8);
+    }
+  }
+  __syncthreads();
+  {
+    const int cc = t >> 2, rr = (t & 3) * 16;  // one output row (column c), 16 codes
+    const int c = c0 + cc, r = r0 + rr;
+    if (c < C) {
+      uint8_t* dst = out + static_cast<long long>(c) * ld_out + r;
+      if (r + 16 <= R) {
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(&tile[cc][rr]);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(s32[0], s32[1], s32[2], s32[3]);
+      } else {
+        for (int i = 0; i < 16 && r + i < R; ++i) dst[i] = tile[cc][rr + i];
+      }
+    }
+  }
+}
+
+// kind::f16 metadata atom (meta.cuh) -> kind::f8f6f4 atom: the same 2048
+// bytes per 128 rows x 128 logical K, row r's 8 halfwords contiguous at 16 r.
+__global__ void __launch_bounds__(256) k_meta_to_f8(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                                    long long halfwords) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < halfwords;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long atom = i >> 10;
+    const uint32_t w = static_cast<uint32_t>(i & 1023);
+    dst[i] = src[atom * 1024 + meta_atom_halfword_byte(w >> 3, w & 7u) / 2];
+  }
+}
+
+__global__ void k_e4m3_encode(const float* __restrict__ x, long long n, uint8_t* __restrict__ codes) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    codes[i] = static_cast<uint8_t>(e4m3x2(x[i], 0.f) & 0xFFu);
+}
+
+static int grid_for(long long work, int per_block) {
+  long long b = (work + per_block - 1) / per_block;
+  const long long cap = 16ll * num_sms();
+  if (b > cap) b = cap;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+}  // namespace s24
+
+using namespace s24;
+
+extern "C" {
+
+int s24_fp8_quant_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ld_in,
+                       const unsigned* amax_in, int64_t pair_rows, uint8_t* codes, int64_t ld_codes, float* scales,
+                       void* deq_bf16, int64_t ld_deq, void* raw_bf16, int64_t ld_raw, void* stream) {
+  if (rows < 0 || cols < 0) return fail(S24_ERR_DIMENSION, "negative dimension");
+  if (cols % 8 != 0) return fail(S24_ERR_DIMENSION, "quantized row length %lld must be a multiple of 8", (long long)cols);
+  if (pair_rows < 0 || pair_rows % 2 || pair_rows > rows) return fail(S24_ERR_DIMENSION, "pair_rows must be even, <= rows");
+  if (!codes || !scales) return fail(S24_ERR_DIMENSION, "codes and scales are required");
+  if (in_dtype != S24_F32 && in_dtype != S24_BF16) return fail(S24_ERR_PRECISION, "input must be fp32 or bf16");
+  if (ld_in < cols || ld_codes < cols || (deq_bf16 && ld_deq < cols) || (raw_bf16 && ld_raw < cols))
+    return fail(S24_ERR_DIMENSION, "leading dimension too small");
+  if (ld_codes % 8 || (deq_bf16 && ld_deq % 8) || (raw_bf16 && ld_raw % 8) || ld_in % (in_dtype == S24_F32 ? 4 : 8))
+    return fail(S24_ERR_DIMENSION, "leading dimensions must keep rows 16-byte aligned");
+  if (rows == 0 || cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  const long long units = pair_rows / 2 + (rows - pair_rows);
+  const int grid = grid_for(units * 32, 256);
+  if (in_dtype == S24_F32)
+    k_quant_rows<float><<<grid, 256, 0, st>>>(static_cast<const float*>(in), ld_in, static_cast<int>(rows),
+                                              static_cast<int>(cols), amax_in, static_cast<int>(pair_rows), codes,
+                                              ld_codes, scales, static_cast<__nv_bfloat16*>(deq_bf16), ld_deq,
+                                              static_cast<__nv_bfloat16*>(raw_bf16), ld_raw);
+  else
+    k_quant_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), ld_in, static_cast<int>(rows), static_cast<int>(cols), amax_in,
+        static_cast<int>(pair_rows), codes, ld_codes, scales, static_cast<__nv_bfloat16*>(deq_bf16), ld_deq,
+        static_cast<__nv_bfloat16*>(raw_bf16), ld_raw);
+  return check_launch("k_quant_rows");
+}
+
+int s24_fp8_quant_cols_t(const void* in_bf16, int64_t rows, int64_t cols, int64_t ld_in, uint8_t* codes_t,
+                         int64_t ld_out, float* scales, unsigned* amax_ws, void* stream) {
+  if (rows < 0 || cols < 0) return fail(S24_ERR_DIMENSION, "negative dimension");
+  if (!codes_t || !scales || !amax_ws) return fail(S24_ERR_DIMENSION, "codes, scales and the workspace are required");
+  if (ld_in < cols || ld_in % 8) return fail(S24_ERR_DIMENSION, "ld_in must be >= cols and a multiple of 8");
+  if (ld_out < rows || ld_out % 16) return fail(S24_ERR_DIMENSION, "ld_out must be >= rows and a multiple of 16");
+  if (rows > (1ll << 31) - 64 || cols > (1ll << 31) - 256) return fail(S24_ERR_DIMENSION, "matrix too large");
+  if (cols == 0) return S24_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(amax_ws, 0, sizeof(unsigned) * cols, st);
+  if (rows > 0) {
+    const int cb = static_cast<int>((cols + 255) / 256);
+    int rpb = 256;
+    while (static_cast<long long>(cb) * ((rows + rpb - 1) / rpb) > 8ll * num_sms() && rpb < (1 << 20)) rpb *= 2;
+    dim3 g1(cb, static_cast<unsigned>((rows + rpb - 1) / rpb));
+    k_col_amax<<<g1, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in_bf16), ld_in, static_cast<int>(rows),
+                                   static_cast<int>(cols), rpb, amax_ws);
+    int rc = check_launch("k_col_amax");
+    if (rc) return rc;
+  }
+  dim3 g2(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(rows > 0 ? (rows + 63) / 64 : 1));
+  k_quant_cols_t<<<g2, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in_bf16), ld_in, static_cast<int>(rows),
+                                     static_cast<int>(cols), amax_ws, codes_t, ld_out, scales);
+  return check_launch("k_quant_cols_t");
+}
+
+int s24_meta_hw_to_f8(const uint8_t* meta_hw, int64_t rows, int64_t kdim, uint8_t* meta_f8, void* stream) {
+  if (rows < 0 || kdim < 0 || kdim % 128) return fail(S24_ERR_DIMENSION, "metadata K must be a multiple of 128");
+  const long long bytes = (rows + 127) / 128 * 128 * kdim / 8;
+  if (bytes == 0) return S24_OK;
+  k_meta_to_f8<<<grid_for(bytes / 2, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint16_t*>(meta_hw), reinterpret_cast<uint16_t*>(meta_f8), bytes / 2);
+  return check_launch("k_meta_to_f8");
+}
+
+int s24_e4m3_encode(const float* x, int64_t n, uint8_t* codes, void* stream) {
+  if (n < 0) return fail(S24_ERR_DIMENSION, "negative length");
+  if (n == 0) return S24_OK;
+  k_e4m3_encode<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, n, codes);
+  return check_launch("k_e4m3_encode");
+}
+
+}  // extern "C"

@@ -1,6 +1,6 @@
 // Persistent, warp-specialised tcgen05 GEMM for sm_100a, dense or 2:4-sparse A.
 //
-//   D[M,N] = A[M,K] * B[K,N]      (bf16 operands, fp32 accumulation in TMEM)
+//   D[M,N] = A[M,K] * B[K,N]      (bf16 or e4m3 operands, fp32 accumulation in TMEM)
 //
 // CG = 1: one CTA per tile of 128 x BN.
 // CG = 2: a CTA pair (cluster of 2 on one TPC) per tile of 256 x BN, issued as
@@ -62,9 +62,16 @@ struct GemmShape {
   K4Job bg;
 };
 
-template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8, int MC_ = 1>
+template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8, int MC_ = 1,
+          bool F8_ = false>
 struct GemmCfg {
   static constexpr bool SPARSE = SPARSE_;
+  // F8: e4m3 operands (tcgen05 kind::f8f6f4). Every stage and MMA step moves
+  // the same BYTES as the bf16 configuration (twice the K elements), so the
+  // smem layouts and descriptor strides below are shared; the 2:4 metadata
+  // doubles per stage (two atoms, see meta.cuh).
+  static constexpr bool F8 = F8_;
+  static constexpr int EB = F8 ? 1 : 2;          // bytes per operand element
   static constexpr bool A_MN = A_MN_;
   static constexpr bool B_MN = B_MN_;
   static constexpr int CG = CG_;
@@ -73,14 +80,16 @@ struct GemmCfg {
   static constexpr int BN = BN_;                 // columns per tile (MMA N)
   static constexpr int BN_CTA = BN / CG;         // B columns staged per CTA
   static constexpr int STAGES = STAGES_;
-  static constexpr int BK = SPARSE ? 128 : 64;   // logical K per stage
-  static constexpr int A_COLS = 64;              // stored A elements per row per stage
-  static constexpr int KSTEPS = 4;               // MMAs per stage (K16 dense / K32 sparse)
-  static constexpr uint32_t A_BYTES = BM * A_COLS * 2;
-  static constexpr uint32_t B_BYTES = BN_CTA * BK * 2;
-  static constexpr uint32_t E_BYTES = SPARSE ? 2048 : 0;
+  static constexpr int BK = (SPARSE ? 128 : 64) * (2 / EB);  // logical K per stage
+  static constexpr int A_COLS = 128 / EB;        // stored A elements per row per stage (128 bytes)
+  static constexpr int BOX_K = 128 / EB;         // K elements per 128-byte swizzle row
+  static constexpr int KSTEPS = 4;               // MMAs per stage (bf16: K16 dense / K32 sparse; e4m3: K32 / K64)
+  static constexpr uint32_t A_BYTES = BM * 128;
+  static constexpr uint32_t B_BYTES = BN_CTA * BK * EB;
+  static constexpr int E_ATOMS = SPARSE ? (F8 ? 2 : 1) : 0;  // 2 KB metadata atoms per stage
+  static constexpr uint32_t E_BYTES = 2048 * E_ATOMS;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
-  static constexpr uint32_t E_COLS = SPARSE ? STAGES * 4 : 0;
+  static constexpr uint32_t E_COLS = STAGES * 4 * E_ATOMS;
   static constexpr bool OVERLAP = 2 * BN + E_COLS > 512;
   static constexpr uint32_t SLOT1_COL = OVERLAP ? BN - 32 : BN;
   static constexpr uint32_t E_COL = SLOT1_COL + BN;
@@ -89,6 +98,7 @@ struct GemmCfg {
                                        : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static_assert(!(SPARSE && A_MN), "sparse A must be K-major");
+  static_assert(!(F8 && (A_MN || B_MN)), "e4m3 operands are K-major");
   static_assert(BN_CTA % 64 == 0 && BN <= 256, "BN");
   static_assert(CG == 1 || CG == 2, "CG");
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
@@ -96,7 +106,8 @@ struct GemmCfg {
   // the dynamic smem base is declared 1024-aligned (SWIZZLE_128B atoms), so no
   // alignment slack is reserved: 7 dense stages fit next to a 2 KB static LUT
   static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20;
-  static constexpr uint32_t IDESC = make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
+  static constexpr uint32_t IDESC =
+      F8 ? make_idesc_e4m3(TILE_M, BN, SPARSE) : make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
   static constexpr int EPI_THREADS = 32 * EPI_WARPS;
@@ -109,7 +120,7 @@ struct GemmCfg {
   // B multicast across MC CTA pairs (see header)
   static constexpr int MC = MC_;
   static constexpr int CLUSTER = CG * MC;
-  static constexpr int B_KBOX = BK / 64;  // K-major B: 64-wide K boxes per stage
+  static constexpr int B_KBOX = BK / BOX_K;  // K-major B: 128-byte K boxes per stage
   // K-major B with fewer K boxes than pairs is split by rows instead
   static constexpr int B_ROW_SPLIT = (!B_MN && B_KBOX % MC != 0) ? MC : 1;
   static constexpr int B_BOX_ROWS = BN_CTA / B_ROW_SPLIT;
@@ -353,15 +364,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 #pragma unroll
             for (int j = 0; j < Cfg::B_KBOX; ++j)
               if (MC == 1 || j % MC == static_cast<int>(pair))
-                load_b(sb + j * (Cfg::BN_CTA * 128), kb * Cfg::BK + 64 * j, n0);
+                load_b(sb + j * (Cfg::BN_CTA * 128), kb * Cfg::BK + Cfg::BOX_K * j, n0);
           } else {
             const int r0 = static_cast<int>(pair) * Cfg::B_BOX_ROWS;
 #pragma unroll
             for (int j = 0; j < Cfg::B_KBOX; ++j)
-              load_b(sb + j * (Cfg::BN_CTA * 128) + r0 * 128, kb * Cfg::BK + 64 * j, n0 + r0);
+              load_b(sb + j * (Cfg::BN_CTA * 128) + r0 * 128, kb * Cfg::BK + Cfg::BOX_K * j, n0 + r0);
           }
           if constexpr (Cfg::SPARSE)
-            tma_load<CG>(sb + Cfg::B_BYTES, mapE, &full_bar[stage], 0, (atom_row * num_kb_all + kb) * 16, pol_a);
+            tma_load<CG>(sb + Cfg::B_BYTES, mapE, &full_bar[stage], 0,
+                         (atom_row * ((shape.K + 127) / 128) + kb * Cfg::E_ATOMS) * 16, pol_a);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -395,12 +407,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           const uint32_t sb = sa + Cfg::A_BYTES;
           uint32_t e_tmem = 0;
           if constexpr (Cfg::SPARSE) {
-            e_tmem = tmem_base + Cfg::E_COL + stage * 4;
-            const uint64_t edesc = make_sdesc(sb + Cfg::B_BYTES, 0, 128, kLayoutNone);
-            if constexpr (CG == 2)
-              tmem_cp_128x128b_cg2(e_tmem, edesc);
-            else
-              tmem_cp_128x128b(e_tmem, edesc);
+            e_tmem = tmem_base + Cfg::E_COL + stage * (4 * Cfg::E_ATOMS);
+#pragma unroll
+            for (int a = 0; a < Cfg::E_ATOMS; ++a) {
+              const uint64_t edesc = make_sdesc(sb + Cfg::B_BYTES + 2048 * a, 0, 128, kLayoutNone);
+              if constexpr (CG == 2)
+                tmem_cp_128x128b_cg2(e_tmem + 4 * a, edesc);
+              else
+                tmem_cp_128x128b(e_tmem + 4 * a, edesc);
+            }
           }
 #pragma unroll
           for (int j = 0; j < (S24_PIPE_PROBE == 2 ? 0 : Cfg::KSTEPS); ++j) {
@@ -419,7 +434,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
               bdesc = make_sdesc(sb + j * 32, 16, 1024, kLayoutSw128);
             }
             const uint32_t accum = (kb > kb0 || j > 0) ? 1u : 0u;
-            if constexpr (Cfg::SPARSE) {
+            if constexpr (Cfg::SPARSE && Cfg::F8) {
+              // e4m3: one K=64 step reads 64 metadata bits per row = TMEM
+              // columns 2j, 2j+1 of the stage
+              if constexpr (CG == 2)
+                mma_sp_e4m3_cg2(d_tmem, adesc, bdesc, e_tmem + 2 * j, Cfg::IDESC, accum);
+              else
+                mma_sp_e4m3(d_tmem, adesc, bdesc, e_tmem + 2 * j, Cfg::IDESC, accum);
+            } else if constexpr (Cfg::SPARSE) {
               // metadata address must be 2-column aligned; the odd column is
               // selected by the descriptor's sparse-id2 field (bits 0-1)
               const uint32_t id = Cfg::IDESC | static_cast<uint32_t>(j & 1);
@@ -427,6 +449,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 mma_sp_bf16_cg2(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
               else
                 mma_sp_bf16(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
+            } else if constexpr (Cfg::F8) {
+              if constexpr (CG == 2)
+                mma_e4m3_cg2(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+              else
+                mma_e4m3(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
             } else {
               if constexpr (CG == 2)
                 mma_bf16_cg2(d_tmem, adesc, bdesc, Cfg::IDESC, accum);

@@ -105,6 +105,24 @@ template <class Cfg>
 static int make_operand_maps(const void* A, int64_t lda, const void* B, int64_t ldb, const uint8_t* meta, int64_t M,
                              int64_t N, int64_t K, CUtensorMap* ma, CUtensorMap* mb, CUtensorMap* me) {
   int rc;
+  if constexpr (Cfg::F8) {
+    // e4m3 codes, both operands K-major (uint8 maps, 128-element boxes)
+    if constexpr (Cfg::SPARSE) {
+      const int64_t mpad = (M + 127) / 128 * 128;
+      rc = make_map_2d(ma, A, false, K / 2, mpad, K / 2, 128, Cfg::BM, true);
+    } else {
+      rc = make_map_2d(ma, A, false, K, M, lda, 128, Cfg::BM, true);
+    }
+    if (rc) return rc;
+    rc = make_map_2d(mb, B, false, K, N, ldb, 128, Cfg::B_BOX_ROWS, true);
+    if (rc) return rc;
+    std::memset(me, 0, sizeof(*me));
+    if constexpr (Cfg::SPARSE) {
+      const int64_t atoms = (M + 127) / 128 * (K / 128);
+      rc = make_map_2d(me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16 * Cfg::E_ATOMS, false);
+    }
+    return rc;
+  }
   // A
   if constexpr (Cfg::A_MN) {
     rc = make_map_bf16(ma, A, M, K, lda, 64, Cfg::BK);
@@ -216,7 +234,7 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   // L2 policies (see gemm.cuh): pin B when it fits, and only then let the
   // A panels stream through (measured: with a 64 MiB B, evict-first A panels
   // are lost before all N tiles of their row have read them)
-  sh.b_keep = static_cast<long long>(K) * N * 2 * sh.groups <= (40ll << 20);
+  sh.b_keep = static_cast<long long>(K) * N * Cfg::EB * sh.groups <= (40ll << 20);
   sh.a_stream = sh.b_keep && sh.group_m * sh.tiles_n <= clusters;
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CLUSTER));
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, ma2, mb2, me2, sh, ep, second ? second->ep : ep);
@@ -244,6 +262,10 @@ using DenseMK = GemmCfg<false, true, false, 256, S24_DENSE_STAGES, 2, 8, S24_DEN
 #endif
 using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4, S24_SPARSE_MC>;   // sparse A, B MN-major
 using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, S24_SPARSE_MC>;  // sparse A, B K-major
+
+// e4m3 (kind::f8f6f4): same byte geometry per stage as the bf16 configs
+using F8DenseKK = GemmCfg<false, false, false, 256, S24_DENSE_STAGES, 2, 8, 1, true>;
+using F8SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, 1, true>;
 
 template <class Epi>
 static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
@@ -493,6 +515,82 @@ int s24_gemm_dact(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int6
   EpiDact::Params ep{static_cast<const __nv_bfloat16*>(act), ld_act, static_cast<__nv_bfloat16*>(gpre), ld_g,
                      static_cast<int>(N)};
   return launch_gemm<DenseKK, EpiDact>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+}
+
+
+// ---------------------------------------------------------------------------
+// e4m3 GEMMs (FfnConfig.fp8_emulation / fp8_backward on the tensor cores).
+// Operands are e4m3 codes, K-major (A [M, K] or the 2:4 compressed [M, K/2]
+// with e4m3-layout metadata, B as [N, K]); D = (row_scale x col_scale) * acc.
+
+int s24_gemm_f8(const uint8_t* A, int64_t lda, const uint8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                const float* row_scale, const float* col_scale, void* D, int out_dtype, int64_t ldd,
+                const int* d_row_map, int d_transposed, int64_t d_rows_valid, void* stream) {
+  int rc = check_common(M, N, K, lda, 0, ldb, 0);
+  if (rc) return rc;
+  if (!row_scale || !col_scale) return fail(S24_ERR_DIMENSION, "e4m3 GEMM needs row and column scales");
+  if (K % 16 != 0) return fail(S24_ERR_DIMENSION, "e4m3 K = %lld must be a multiple of 16", (long long)K);
+  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    using Epi = EpiStore<OutT, true>;
+    typename Epi::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
+                            static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), nullptr, 0, 0, row_scale,
+                            col_scale};
+    return launch_gemm<F8DenseKK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int s24_spmm_f8(const uint8_t* a_codes, const uint8_t* a_meta_f8, const uint8_t* B, int64_t ldb, int64_t M,
+                int64_t N, int64_t K, const float* row_scale, const float* col_scale, void* D, int out_dtype,
+                int64_t ldd, const int* d_row_map, int d_transposed, int64_t d_rows_valid, const int* d_row_valid,
+                int64_t pair_rows, void* stream) {
+  int rc = check_common(M, N, K, K, 0, ldb, 0);
+  if (rc) return rc;
+  if (!row_scale || !col_scale) return fail(S24_ERR_DIMENSION, "e4m3 GEMM needs row and column scales");
+  // (a stage spans 256 logical K; with K % 256 == 128 the last stage's second
+  // half reads zero-filled A and B, whatever metadata sits next to it)
+  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
+  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  if (pair_rows < 0 || pair_rows % 2 || pair_rows > M) return fail(S24_ERR_DIMENSION, "pair_rows must be even, <= M");
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    using Epi = EpiStore<OutT, true>;
+    typename Epi::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
+                            static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0,
+                            static_cast<int>(pair_rows), row_scale, col_scale};
+    return launch_gemm<F8SparseK, Epi>(a_codes, K / 2, B, ldb, M, N, K, a_meta_f8, ep,
+                                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int s24_fwd_gemm1_f8(const uint8_t* xq, int64_t ldx, const uint8_t* w1q, int64_t ldw1, int64_t M, int64_t N,
+                     int64_t K, const float* x_scale, const float* w1_scale, float* act_vals32, unsigned* row_amax,
+                     uint8_t* act_meta, int* counts, unsigned long long* stats, float* y_dbg, void* stream) {
+  int rc = check_common(M, N, K, ldx, 0, ldw1, 0);
+  if (rc) return rc;
+  if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
+  if (K % 16 != 0) return fail(S24_ERR_DIMENSION, "e4m3 K = %lld must be a multiple of 16", (long long)K);
+  if (!x_scale || !w1_scale || !act_vals32 || !row_amax)
+    return fail(S24_ERR_DIMENSION, "e4m3 K1 needs scales, the fp32 value buffer and the row maxima");
+  using Epi = EpiFwd1T<true>;
+  Epi::Params ep{nullptr, act_meta, counts, stats, y_dbg, static_cast<int>(N), FwTarget{nullptr, nullptr, nullptr, 0},
+                 nullptr, x_scale, w1_scale, act_vals32, row_amax};
+  return launch_gemm<F8DenseKK, Epi>(xq, ldx, w1q, ldw1, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+}
+
+int s24_bwd_dact_f8(const uint8_t* gq, int64_t ldg, const uint8_t* w2q, int64_t ldw2, int64_t M, int64_t N,
+                    int64_t K, const float* g_scale, const float* w2_scale, const void* act_vals,
+                    const uint8_t* act_meta, void* g_vals, void* stream) {
+  int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
+  if (rc) return rc;
+  if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
+  if (K % 16 != 0) return fail(S24_ERR_DIMENSION, "e4m3 K = %lld must be a multiple of 16", (long long)K);
+  if (!g_scale || !w2_scale) return fail(S24_ERR_DIMENSION, "e4m3 K3 needs row and column scales");
+  using Epi = EpiBwd1T<true>;
+  Epi::Params ep{static_cast<const __nv_bfloat16*>(act_vals), act_meta, static_cast<__nv_bfloat16*>(g_vals),
+                 static_cast<int>(N), FwTarget{nullptr, nullptr, nullptr, 0}, nullptr, g_scale, w2_scale};
+  return launch_gemm<F8DenseKK, Epi>(gq, ldg, w2q, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

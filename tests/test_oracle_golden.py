@@ -119,3 +119,72 @@ def test_analytic_drop_fraction():
     a = ((np.random.default_rng(42).random((512, 2048)) < p) * 1.0).astype(np.float32)
     _, _, _, st = O.sparsify_token(a)
     assert abs(st["dropped_fraction_of_nonzeros"] - analytic) < 0.0015
+
+
+# ---------------------------------------------------------------- e4m3 (fp8)
+
+
+@pytest.fixture(scope="module")
+def f8():
+    return np.load(GOLD / "fp8.npz")
+
+
+def test_e4m3_decode_and_encode_bitwise(f8):
+    dec = f8["dec_table"]
+    assert np.array_equal(np.isnan(dec), np.isnan(O._E4M3))
+    ok = ~np.isnan(dec)
+    assert np.array_equal(dec[ok], O._E4M3[ok]) and np.array_equal(np.signbit(dec[ok]), np.signbit(O._E4M3[ok]))
+    assert np.array_equal(O.e4m3_encode(f8["enc_x"]), f8["enc_codes"])
+    # all 254 non-NaN codes round-trip (ref tests/test_acceptance.py:272-280)
+    codes = np.arange(256)[ok]
+    assert np.array_equal(O.e4m3_encode(O._E4M3[codes]), codes.astype(np.uint8))
+
+
+@pytest.mark.parametrize("i", range(3))
+@pytest.mark.parametrize("axis", ["rows", "cols"])
+def test_quantize_bitwise(f8, i, axis):
+    codes, scales = O.quantize(f8[f"q{i}_a"], axis)
+    assert np.array_equal(codes, f8[f"q{i}_{axis}_codes"])
+    assert np.array_equal(scales, f8[f"q{i}_{axis}_scales"])
+
+
+def test_fp8_gemm_bitwise_and_error_bound(f8):
+    a, b = f8["gemm_a"], f8["gemm_b"]
+    out = O.mm_f8(a, b)
+    assert np.array_equal(out, f8["gemm_out"])
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) <= 0.06  # ref tests/test_acceptance.py:283-291
+
+
+F8_CONFIGS = {
+    "recipe_f8fwd": dict(O.RECIPE, fp8_emulation=True),
+    "recipe_f8all": dict(O.RECIPE, fp8_emulation=True, fp8_backward=True),
+    "dense_f8all": dict(O.DENSE, fp8_emulation=True, fp8_backward=True),
+    "naive_f8all": dict(O.DENSE, forward_mode="sparse24", backward_mode="naive_sparse", mask_grad_with_fwd=True,
+                        fp8_emulation=True, fp8_backward=True),
+    "split_nomask_f8all": dict(O.DENSE, forward_mode="sparse24", backward_mode="split_masked", fp8_emulation=True,
+                               fp8_backward=True),
+}
+
+
+@pytest.mark.parametrize("shape", ["s0", "s1"])
+@pytest.mark.parametrize("name", sorted(F8_CONFIGS))
+def test_fp8_ffn_bitwise(f8, shape, name):
+    x, w1, w2, g = (f8[f"{shape}_{k}"] for k in ("x", "w1", "w2", "g"))
+    cfg = F8_CONFIGS[name]
+    out, cache = O.ffn_forward(x, w1, w2, cfg)
+    grads = O.ffn_backward(g, cache, w1, w2, cfg)
+    k = f"{shape}_{name}"
+    assert np.array_equal(out, f8[f"{k}_out"])
+    for t in ("d_w1", "d_w2", "d_x"):
+        assert np.array_equal(grads[t], f8[f"{k}_{t}"]), t
+    if f"{k}_act_values" in f8:
+        assert np.array_equal(cache["vals"], f8[f"{k}_act_values"])
+
+
+def test_fp8_selects_before_quantizing(f8):
+    # ref tests/test_ffn.py:360-367: 3.01, 3.0, 2.99 share one code, the
+    # selection still keeps the two largest unquantized values
+    eye = np.eye(4, dtype=np.float32)
+    _, cache = O.ffn_forward(f8["kat_sel_x"], eye, eye, dict(O.DENSE, forward_mode="sparse24", fp8_emulation=True))
+    assert np.array_equal(cache["meta"], f8["kat_sel_meta"])
