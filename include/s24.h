@@ -266,10 +266,10 @@ int s24_gemm_dact(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int6
 int s24_fp8_quant_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ld_in,
                        const unsigned* amax_in, int64_t pair_rows, uint8_t* codes, int64_t ld_codes, float* scales,
                        void* deq_bf16, int64_t ld_deq, void* raw_bf16, int64_t ld_raw, void* stream);
-/* per-column codes of a bf16 [rows, cols] matrix, written transposed
+/* per-column codes of an fp32/bf16 [rows, cols] matrix, written transposed
  * codes_t[cols, rows] (the K-major operand), scales[cols]; amax_ws: cols
  * uint32 of workspace. ref matcore.py:203-225 with axis="cols". */
-int s24_fp8_quant_cols_t(const void* in_bf16, int64_t rows, int64_t cols, int64_t ld_in, uint8_t* codes_t,
+int s24_fp8_quant_cols_t(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ld_in, uint8_t* codes_t,
                          int64_t ld_out, float* scales, unsigned* amax_ws, void* stream);
 /* hw metadata -> f8 metadata (same logical content) */
 int s24_meta_hw_to_f8(const uint8_t* meta_hw, int64_t rows, int64_t kdim, uint8_t* meta_f8, void* stream);

@@ -50,7 +50,7 @@ SIGNATURES: dict[str, list] = {
     "s24_gemm_relu2": [P, I64, P, I64, I64, I64, I64, P, I64, P],
     "s24_gemm_dact": [P, I64, P, I64, I64, I64, I64, P, I64, P, I64, P],
     "s24_fp8_quant_rows": [P, INT, I64, I64, I64, P, I64, P, I64, P, P, I64, P, I64, P],
-    "s24_fp8_quant_cols_t": [P, I64, I64, I64, P, I64, P, P, P],
+    "s24_fp8_quant_cols_t": [P, INT, I64, I64, I64, P, I64, P, P, P],
     "s24_meta_hw_to_f8": [P, I64, I64, P, P],
     "s24_e4m3_encode": [P, I64, P, P],
     "s24_gemm_f8": [P, I64, P, I64, I64, I64, I64, P, P, P, INT, I64, P, INT, I64, P],

@@ -132,9 +132,19 @@ __global__ void __launch_bounds__(256) k_quant_rows(const InT* __restrict__ in, 
   }
 }
 
-// column |max| of a bf16 [R, C] matrix into amax[C] (float bits, atomicMax;
-// zeroed by the caller). Block: 32 x 8 threads, 256 columns x rows_per_block.
-__global__ void __launch_bounds__(256) k_col_amax(const __nv_bfloat16* __restrict__ in, long long ld, int R, int C,
+template <typename T>
+__device__ __forceinline__ float ld1(const T* p) {
+  if constexpr (std::is_same_v<T, float>)
+    return *p;
+  else
+    return __bfloat162float(*p);
+}
+
+// column |max| of a bf16 / fp32 [R, C] matrix into amax[C] (float bits,
+// atomicMax; zeroed by the caller). Block: 32 x 8 threads, 256 columns x
+// rows_per_block.
+template <typename InT>
+__global__ void __launch_bounds__(256) k_col_amax(const InT* __restrict__ in, long long ld, int R, int C,
                                                   int rows_per_block, unsigned* __restrict__ amax) {
   __shared__ float red[8][256 + 8];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -152,7 +162,7 @@ __global__ void __launch_bounds__(256) k_col_amax(const __nv_bfloat16* __restric
   } else {
     for (int r = rb + ty; r < re; r += 8)
       for (int i = 0; i < 8 && c0 + i < C; ++i)
-        m[i] = fmaxf(m[i], fabsf(__bfloat162float(in[static_cast<long long>(r) * ld + c0 + i])));
+        m[i] = fmaxf(m[i], fabsf(ld1(in + static_cast<long long>(r) * ld + c0 + i)));
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) red[ty][8 * tx + i] = m[i];
@@ -166,7 +176,8 @@ __global__ void __launch_bounds__(256) k_col_amax(const __nv_bfloat16* __restric
 
 // codes_t[c, r] = e4m3(in[r, c] / scale[c]); 64 x 64 tiles through shared
 // memory so both the bf16 reads and the code writes are row-contiguous.
-__global__ void __launch_bounds__(256) k_quant_cols_t(const __nv_bfloat16* __restrict__ in, long long ld, int R,
+template <typename InT>
+__global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in, long long ld, int R,
                                                       int C, const unsigned* __restrict__ amax,
                                                       uint8_t* __restrict__ out, long long ld_out,
                                                       float* __restrict__ scales) {
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(256) k_quant_cols_t(const __nv_bfloat16* __res
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        v[i] = (r < R && c0 + cc + i < C) ? __bfloat162float(in[static_cast<long long>(r) * ld + c0 + cc + i]) : 0.f;
+        v[i] = (r < R && c0 + cc + i < C) ? ld1(in + static_cast<long long>(r) * ld + c0 + cc + i) : 0.f;
     }
 #pragma unroll
     for (int i = 0; i < 16; i += 2) {
@@ -281,11 +292,13 @@ int s24_fp8_quant_rows(const void* in, int in_dtype, int64_t rows, int64_t cols,
   return check_launch("k_quant_rows");
 }
 
-int s24_fp8_quant_cols_t(const void* in_bf16, int64_t rows, int64_t cols, int64_t ld_in, uint8_t* codes_t,
+int s24_fp8_quant_cols_t(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t ld_in, uint8_t* codes_t,
                          int64_t ld_out, float* scales, unsigned* amax_ws, void* stream) {
   if (rows < 0 || cols < 0) return fail(S24_ERR_DIMENSION, "negative dimension");
+  if (in_dtype != S24_F32 && in_dtype != S24_BF16) return fail(S24_ERR_PRECISION, "input must be fp32 or bf16");
   if (!codes_t || !scales || !amax_ws) return fail(S24_ERR_DIMENSION, "codes, scales and the workspace are required");
-  if (ld_in < cols || ld_in % 8) return fail(S24_ERR_DIMENSION, "ld_in must be >= cols and a multiple of 8");
+  if (ld_in < cols || ld_in % (in_dtype == S24_F32 ? 4 : 8))
+    return fail(S24_ERR_DIMENSION, "ld_in must be >= cols and keep rows 16-byte aligned");
   if (ld_out < rows || ld_out % 16) return fail(S24_ERR_DIMENSION, "ld_out must be >= rows and a multiple of 16");
   if (rows > (1ll << 31) - 64 || cols > (1ll << 31) - 256) return fail(S24_ERR_DIMENSION, "matrix too large");
   if (cols == 0) return S24_OK;
@@ -296,14 +309,23 @@ int s24_fp8_quant_cols_t(const void* in_bf16, int64_t rows, int64_t cols, int64_
     int rpb = 256;
     while (static_cast<long long>(cb) * ((rows + rpb - 1) / rpb) > 8ll * num_sms() && rpb < (1 << 20)) rpb *= 2;
     dim3 g1(cb, static_cast<unsigned>((rows + rpb - 1) / rpb));
-    k_col_amax<<<g1, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in_bf16), ld_in, static_cast<int>(rows),
-                                   static_cast<int>(cols), rpb, amax_ws);
+    if (in_dtype == S24_F32)
+      k_col_amax<float><<<g1, 256, 0, st>>>(static_cast<const float*>(in), ld_in, static_cast<int>(rows),
+                                            static_cast<int>(cols), rpb, amax_ws);
+    else
+      k_col_amax<__nv_bfloat16><<<g1, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in), ld_in,
+                                                    static_cast<int>(rows), static_cast<int>(cols), rpb, amax_ws);
     int rc = check_launch("k_col_amax");
     if (rc) return rc;
   }
   dim3 g2(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(rows > 0 ? (rows + 63) / 64 : 1));
-  k_quant_cols_t<<<g2, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in_bf16), ld_in, static_cast<int>(rows),
-                                     static_cast<int>(cols), amax_ws, codes_t, ld_out, scales);
+  if (in_dtype == S24_F32)
+    k_quant_cols_t<float><<<g2, 256, 0, st>>>(static_cast<const float*>(in), ld_in, static_cast<int>(rows),
+                                              static_cast<int>(cols), amax_ws, codes_t, ld_out, scales);
+  else
+    k_quant_cols_t<__nv_bfloat16><<<g2, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in), ld_in,
+                                                      static_cast<int>(rows), static_cast<int>(cols), amax_ws,
+                                                      codes_t, ld_out, scales);
   return check_launch("k_quant_cols_t");
 }
 

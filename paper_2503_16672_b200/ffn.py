@@ -231,6 +231,11 @@ class FfnCache:
     act_split: FeatureSplit | None = None  # feature-wise split of act (K4, run during fwd.out)
     act_split_ready: object = None  # CUDA event after which act_split is complete (side-stream K4)
     x_in_ready: object = None  # CUDA event after which x_in is complete (gathered on the side stream)
+    # fp8_emulation (fp8.py): act_vals holds the dequantized activation (the
+    # reference's act_sparse); K3 recovers relu(y1) from the unquantized one
+    act_raw: torch.Tensor | None = None
+    act_meta8: torch.Tensor | None = None  # act metadata in the e4m3 operand-E layout
+    act_f32: torch.Tensor | None = None  # dense fp8 forward: the fp32 activation
 
     # Side-stream work of the forward reads and writes tensors allocated on
     # the main stream (no record_stream: its deferred frees stall the caching
@@ -288,8 +293,6 @@ def _unsupported(cfg: FfnConfig) -> None:
     if cfg.activation != "squared_relu":
         raise ConfigError("the B200 backend implements the squared_relu FFN only (SwiGLU is the "
                           "reference's dense Table-1 baseline, out of scope)")
-    if cfg.fp8_emulation:
-        raise ConfigError("the fp8 (e4m3) path is not part of this build")
 
 
 def _check_dims(n: int, d: int, h: int) -> None:
@@ -318,6 +321,13 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         raise DimensionError(f"sparse modes need token count % 4 == 0, got {n}")
     h = p.hidden_dim
     _check_dims(n, d, h)
+    if cfg.fp8_emulation:
+        # e4m3 operands on the kind::f8f6f4 tensor cores (fp8.py)
+        if d % 32:
+            raise DimensionError(f"the fp8 path needs model dim % 32 == 0, got {d}")
+        from .fp8 import ffn_forward_f8
+
+        return ffn_forward_f8(x, p, cfg, plan, keep_pre_act, for_backward)
     dev = x.device
     s = stream()
     npad = pad128(n)
@@ -518,6 +528,10 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     if cfg.backward_mode == "split_masked" and cache.plan is None:
         raise StateError("split backward needs the plan computed in forward")
     h = p.hidden_dim
+    if cfg.fp8_backward:
+        from .fp8 import ffn_backward_f8
+
+        return ffn_backward_f8(g_out, cache, p, cfg, grad_ready)
     dev = g_out.device
     s = stream()
     npad = pad128(n)
@@ -609,7 +623,9 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     if not rowmap and cache.perm_dev is not None:
         need_frame_inputs()
         k3_in, k3_map = g_c, None
-    _lib.call("s24_bwd_dact_fused", ptr(k3_in), d, ptr(p.w2), d, n, h, d, ptr(cache.act_vals), ptr(cache.act_meta),
+    # (fp8 forward: relu(y1) comes from the unquantized activation)
+    k3_act = cache.act_raw if cache.act_raw is not None else cache.act_vals
+    _lib.call("s24_bwd_dact_fused", ptr(k3_in), d, ptr(p.w2), d, n, h, d, ptr(k3_act), ptr(cache.act_meta),
               ptr(g_vals), *fw_args, ptr(k3_map), s)
     census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
     g_pre_dense = None

@@ -45,7 +45,8 @@ def quant_cols_t(a):
     codes_t = torch.zeros(cols, ld, dtype=torch.uint8, device="cuda")
     scales = torch.empty(cols, dtype=torch.float32, device="cuda")
     ws = torch.empty(cols, dtype=torch.int32, device="cuda")
-    _lib.call("s24_fp8_quant_cols_t", P(a), rows, cols, a.stride(0), P(codes_t), ld, P(scales), P(ws), S())
+    dt = F32 if a.dtype == torch.float32 else BF16
+    _lib.call("s24_fp8_quant_cols_t", P(a), dt, rows, cols, a.stride(0), P(codes_t), ld, P(scales), P(ws), S())
     return codes_t[:, :rows], scales
 
 
@@ -102,10 +103,11 @@ def test_quant_rows_pairs_share_scales():
     assert np.array_equal(codes[8:].cpu().numpy(), rc) and np.array_equal(scales[8:].cpu().numpy(), rs)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("rows,cols", [(256, 128), (100, 72), (64, 1000)])
-def test_quant_cols_transposed_bitwise(rows, cols):
+def test_quant_cols_transposed_bitwise(dtype, rows, cols):
     torch.manual_seed(rows * cols)
-    a = (torch.randn(rows, cols, device="cuda") * torch.logspace(-2, 3, cols, device="cuda")[None, :]).bfloat16()
+    a = (torch.randn(rows, cols, device="cuda") * torch.logspace(-2, 3, cols, device="cuda")[None, :]).to(dtype)
     a[:, 3] = 0
     codes_t, scales = quant_cols_t(a)
     rc, rs = O.quantize(a.float().cpu().numpy(), "cols")
