@@ -200,6 +200,23 @@ class KernelTracer:
             return "hbm", 2.0 * a[1] * a[2], "K6 row gather"
         if name == "s24_plan":
             return "hbm", 4.0 * a[1] * 3, "K7 plan"
+        if name == "s24_gemm_f8":
+            return "tensor_f8", 2.0 * a[4] * a[5] * a[6], f"gemm e4m3 M={a[4]} N={a[5]} K={a[6]}"
+        if name == "s24_spmm_f8":
+            return "tensor_f8_sparse", 2.0 * a[4] * a[5] * a[6], f"spmm e4m3 2:4 M={a[4]} N={a[5]} K={a[6]}"
+        if name == "s24_fwd_gemm1_f8":
+            return "tensor_f8", 2.0 * a[4] * a[5] * a[6], "K1 e4m3 gemm+relu2+2:4 (fwd.pre_act)"
+        if name == "s24_bwd_dact_f8":
+            return "tensor_f8", 2.0 * a[4] * a[5] * a[6], "K3 e4m3 gemm+relu2'+mask (bwd.d_act)"
+        if name == "s24_fp8_quant_rows":
+            eb = 4 if a[1] == 0 else 2
+            return "hbm", a[2] * a[3] * (eb + 1 + (2 if a[10] else 0) + (2 if a[12] else 0)), \
+                f"e4m3 quantize rows ({'fp32' if eb == 4 else 'bf16'} in)"
+        if name == "s24_fp8_quant_cols_t":
+            eb = 4 if a[1] == 0 else 2
+            return "hbm", a[2] * a[3] * (2 * eb + 1), "e4m3 quantize cols (transposed)"
+        if name == "s24_meta_hw_to_f8":
+            return "hbm", a[1] * a[2] / 4.0, "metadata -> e4m3 layout"
         if name == "s24_gemm_splitk":
             return "tensor", 2.0 * a[6] * a[7] * a[8], f"gemm dense split-K M={a[6]} N={a[7]} K={a[8]}"
         return "other", 0.0, name

@@ -33,6 +33,31 @@ __device__ __forceinline__ float e4m3_scale(float amax) {
   return s > 0.f ? s : 1.f;
 }
 
+// x / s for the whole row (column) with one shared divisor: r = RN(1/s) once,
+// then q = x*r refined by one FMA residual step (Markstein). q is within a
+// tiny fraction of an ulp of x/s, so it equals RN(x/s) except when x/s lies
+// within ~2^-22 ulp of an fp32 midpoint; and an e4m3 rounding boundary is an
+// fp32 number, never an fp32 midpoint, so the e4m3 code of q equals the code
+// of RN(x/s) (exact e4m3 ties, x/s == boundary, are reproduced exactly: the
+// refined q of an exactly representable quotient is that quotient). Three FP
+// instructions instead of the IEEE division sequence, which made the
+// quantizers issue-bound.
+__device__ __forceinline__ float rcp_rn(float x) {
+  float r;
+  asm("rcp.rn.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+struct Divisor {
+  float s, r;
+  __device__ __forceinline__ explicit Divisor(float s_) : s(s_), r(rcp_rn(s_)) {}
+  __device__ __forceinline__ float div(float x) const {
+    const float q = __fmul_rn(x, r);
+    const float e = __fmaf_rn(-q, s, x);
+    return copysignf(__fmaf_rn(e, r, q), x);  // (-0 and negative underflow keep their sign: code 0x80)
+  }
+};
+
 // two fp32 -> two e4m3 codes (lo in the low byte)
 __device__ __forceinline__ uint32_t e4m3x2(float lo, float hi) {
   uint16_t r;
@@ -73,8 +98,11 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
 
 // One warp per unit: a single row, or (rows < pair_rows) an (even, odd) row
 // pair sharing one scale (a dense feature stored as two 2:4 rows, k4.cuh).
-// cols % 8 == 0; every row pointer 16-byte aligned.
-template <typename InT>
+// cols % 8 == 0; every row pointer 16-byte aligned. Each lane keeps U
+// independent 16-byte loads in flight per iteration (rows are only a few KB:
+// without that the kernel is load-latency bound); the second pass re-reads
+// the row from L2.
+template <typename InT, int U = 2>
 __global__ void __launch_bounds__(256) k_quant_rows(const InT* __restrict__ in, long long ld_in, int rows, int cols,
                                                     const unsigned* __restrict__ amax_in, int pair_rows,
                                                     uint8_t* __restrict__ codes, long long ld_codes,
@@ -92,40 +120,53 @@ __global__ void __launch_bounds__(256) k_quant_rows(const InT* __restrict__ in, 
     } else {
       for (int k = 0; k < nr; ++k) {
         const InT* src = in + static_cast<long long>(r0 + k) * ld_in;
-        for (int c = 8 * lane; c < cols; c += 256) {
-          float v[8];
-          load8(src + c, v);
+        for (int c0 = 8 * lane; c0 < cols; c0 += 256 * U) {
+          float v[U][8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
+          for (int j = 0; j < U; ++j)
+            if (c0 + 256 * j < cols) load8(src + c0 + 256 * j, v[j]);
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (c0 + 256 * j < cols)
+#pragma unroll
+              for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[j][i]));
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
     const float s = e4m3_scale(amax);
+    const Divisor dv(s);
     if (lane == 0)
       for (int k = 0; k < nr; ++k) scales[r0 + k] = s;
     for (int k = 0; k < nr; ++k) {
       const long long r = r0 + k;
       const InT* src = in + r * ld_in;
-      for (int c = 8 * lane; c < cols; c += 256) {
-        float v[8];
-        load8(src + c, v);
-        uint32_t q[4];
+      for (int c0 = 8 * lane; c0 < cols; c0 += 256 * U) {
+        float v[U][8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) q[i] = e4m3x2(__fdiv_rn(v[2 * i], s), __fdiv_rn(v[2 * i + 1], s));
-        *reinterpret_cast<uint2*>(codes + r * ld_codes + c) = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
-        if (deq) {
-          uint32_t o[4];
+        for (int j = 0; j < U; ++j)
+          if (c0 + 256 * j < cols) load8(src + c0 + 256 * j, v[j]);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            o[i] = bf16x2_bits(__fmul_rn(e4m3_decode(q[i]), s), __fmul_rn(e4m3_decode(q[i] >> 8), s));
-          *reinterpret_cast<uint4*>(deq + r * ld_deq + c) = make_uint4(o[0], o[1], o[2], o[3]);
-        }
-        if (raw) {
-          *reinterpret_cast<uint4*>(raw + r * ld_raw + c) =
-              make_uint4(bf16x2_bits(v[0], v[1]), bf16x2_bits(v[2], v[3]), bf16x2_bits(v[4], v[5]),
-                         bf16x2_bits(v[6], v[7]));
+        for (int j = 0; j < U; ++j) {
+          const int c = c0 + 256 * j;
+          if (c >= cols) continue;
+          uint32_t q[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) q[i] = e4m3x2(dv.div(v[j][2 * i]), dv.div(v[j][2 * i + 1]));
+          *reinterpret_cast<uint2*>(codes + r * ld_codes + c) = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
+          if (deq) {
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = bf16x2_bits(__fmul_rn(e4m3_decode(q[i]), s), __fmul_rn(e4m3_decode(q[i] >> 8), s));
+            *reinterpret_cast<uint4*>(deq + r * ld_deq + c) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+          if (raw) {
+            *reinterpret_cast<uint4*>(raw + r * ld_raw + c) =
+                make_uint4(bf16x2_bits(v[j][0], v[j][1]), bf16x2_bits(v[j][2], v[j][3]),
+                           bf16x2_bits(v[j][4], v[j][5]), bf16x2_bits(v[j][6], v[j][7]));
+          }
         }
       }
     }
@@ -182,12 +223,13 @@ __global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in
                                                       uint8_t* __restrict__ out, long long ld_out,
                                                       float* __restrict__ scales) {
   __shared__ uint8_t tile[64][64 + 16];
-  __shared__ float sc[64];
+  __shared__ float sc[64], rc[64];
   const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
   const int t = threadIdx.x;
   if (t < 64) {
     const float s = (c0 + t < C) ? e4m3_scale(__uint_as_float(amax[c0 + t])) : 1.f;
     sc[t] = s;
+    rc[t] = rcp_rn(s);
     if (blockIdx.y == 0 && c0 + t < C) scales[c0 + t] = s;
   }
   __syncthreads();
@@ -211,7 +253,12 @@ __global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in
     }
 #pragma unroll
     for (int i = 0; i < 16; i += 2) {
-      const uint32_t q = e4m3x2(__fdiv_rn(v[i], sc[cc + i]), __fdiv_rn(v[i + 1], sc[cc + i + 1]));
+      Divisor d0{0.f}, d1{0.f};
+      d0.s = sc[cc + i];
+      d0.r = rc[cc + i];
+      d1.s = sc[cc + i + 1];
+      d1.r = rc[cc + i + 1];
+      const uint32_t q = e4m3x2(d0.div(v[i]), d1.div(v[i + 1]));
       tile[cc + i][rr] = static_cast<uint8_t>(q & 0xFFu);
       tile[cc + i + 1][rr] = static_cast<uint8_t>(q >> 8);
     }
