@@ -26,6 +26,19 @@ __device__ __forceinline__ uint32_t fge_mask(float a, float b) {
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 __device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
 
+// e4m3 GEMMs: v = (sr * col_scale[j]) * acc (the reference's order), the 32
+// column scales of the chunk read as 8 broadcast 16-byte loads
+__device__ __forceinline__ void scale_chunk(const float* cs, float sr, const float (&acc)[32], float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 c = __ldg(reinterpret_cast<const float4*>(cs + i));
+    v[i] = __fmul_rn(__fmul_rn(sr, c.x), acc[i]);
+    v[i + 1] = __fmul_rn(__fmul_rn(sr, c.y), acc[i + 1]);
+    v[i + 2] = __fmul_rn(__fmul_rn(sr, c.z), acc[i + 2]);
+    v[i + 3] = __fmul_rn(__fmul_rn(sr, c.w), acc[i + 3]);
+  }
+}
+
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -93,8 +106,7 @@ struct EpiStore {
     float v[32];
     if constexpr (SCALED) {
       const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(sr, __ldg(p.col_scale + col0 + i)), v_in[i]);
+      scale_chunk(p.col_scale + col0, sr, v_in, v);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = v_in[i];
@@ -194,8 +206,7 @@ struct EpiFwd1T {
     float v[32];
     if constexpr (F8) {
       const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(sr, __ldg(p.col_scale + col0 + i)), v_in[i]);
+      scale_chunk(p.col_scale + col0, sr, v_in, v);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = v_in[i];
@@ -336,8 +347,7 @@ struct EpiBwd1T {
     float v[32];
     if constexpr (F8) {
       const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(sr, __ldg(p.col_scale + col0 + i)), v_in[i]);
+      scale_chunk(p.col_scale + col0, sr, v_in, v);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = v_in[i];

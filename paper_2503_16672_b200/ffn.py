@@ -236,6 +236,7 @@ class FfnCache:
     act_raw: torch.Tensor | None = None
     act_meta8: torch.Tensor | None = None  # act metadata in the e4m3 operand-E layout
     act_f32: torch.Tensor | None = None  # dense fp8 forward: the fp32 activation
+    f8: dict | None = None  # e4m3 backward operands prepared next to the forward GEMMs (fp8.py)
 
     # Side-stream work of the forward reads and writes tensors allocated on
     # the main stream (no record_stream: its deferred frees stall the caching

@@ -56,40 +56,96 @@ def _decode_table(device) -> torch.Tensor:
 
 def quant_rows(a: torch.Tensor, rows: int | None = None, pair_rows: int = 0, amax: torch.Tensor | None = None,
                codes: torch.Tensor | None = None, deq: torch.Tensor | None = None,
-               raw: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-    """Per-row e4m3 codes [R, C] and scales [R] of the first `rows` rows of a
-    (bf16 or fp32). Rows past `rows` in a preallocated `codes` are left as they
-    are. deq / raw: optional bf16 outputs (dequantized / unquantized images)."""
+               raw: torch.Tensor | None = None, scales: torch.Tensor | None = None,
+               st=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-row e4m3 codes [R, C] and scales of the first `rows` rows of a
+    (bf16 or fp32). Rows past `rows` in a preallocated `codes` / `scales` are
+    left as they are. deq / raw: optional bf16 outputs (dequantized /
+    unquantized images). Outputs are allocated on the current stream; st
+    (a torch stream) launches the kernel elsewhere."""
     R = a.shape[0] if rows is None else rows
     C = a.shape[1]
     if codes is None:
         codes = torch.empty(a.shape[0], C, dtype=U8, device=a.device)
-    scales = torch.ones(codes.shape[0], dtype=F32, device=a.device)
+    if scales is None:
+        scales = torch.empty(codes.shape[0], dtype=F32, device=a.device)
     _lib.call("s24_fp8_quant_rows", ptr(a), _dtype_code(a), R, C, a.stride(0), ptr(amax), pair_rows, ptr(codes),
               codes.stride(0), ptr(scales), ptr(deq), deq.stride(0) if deq is not None else 0, ptr(raw),
-              raw.stride(0) if raw is not None else 0, stream())
+              raw.stride(0) if raw is not None else 0, st.cuda_stream if st is not None else stream())
     return codes, scales
 
 
-def quant_cols_t(a: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+def quant_cols_t(a: torch.Tensor, codes_t: torch.Tensor | None = None, scales: torch.Tensor | None = None,
+                 st=None, keep: list | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """Per-column codes of a [R, C] (bf16 or fp32), transposed: ([C, R16]
-    codes with R16 = R rounded up to 16, zero beyond R; scales [C])."""
+    codes with R16 = R rounded up to 16, zero beyond R; scales [C]). With st
+    (another stream) the workspace is appended to `keep`, to stay alive until
+    that stream's work has been joined."""
     R, C = a.shape
     ld = (R + 15) // 16 * 16
-    codes_t = torch.empty(C, ld, dtype=U8, device=a.device)
-    if ld > R:
-        codes_t[:, R:].zero_()
-    scales = torch.empty(C, dtype=F32, device=a.device)
+    if codes_t is None:
+        codes_t = torch.empty(C, ld, dtype=U8, device=a.device)
+        if ld > R:
+            codes_t[:, R:].zero_()
+    if scales is None:
+        scales = torch.empty(C, dtype=F32, device=a.device)
     ws = torch.empty(max(C, 1), dtype=torch.int32, device=a.device)
-    _lib.call("s24_fp8_quant_cols_t", ptr(a), _dtype_code(a), R, C, a.stride(0), ptr(codes_t), ld, ptr(scales),
-              ptr(ws), stream())
+    if keep is not None:
+        keep.append(ws)
+    _lib.call("s24_fp8_quant_cols_t", ptr(a), _dtype_code(a), R, C, a.stride(0), ptr(codes_t), codes_t.stride(0),
+              ptr(scales), ptr(ws), st.cuda_stream if st is not None else stream())
     return codes_t, scales
 
 
-def meta_to_f8(meta_hw: torch.Tensor, rows: int, kdim: int) -> torch.Tensor:
-    out = torch.empty_like(meta_hw)
-    _lib.call("s24_meta_hw_to_f8", ptr(meta_hw), rows, kdim, ptr(out), stream())
+def meta_to_f8(meta_hw: torch.Tensor, rows: int, kdim: int, out: torch.Tensor | None = None,
+               st=None) -> torch.Tensor:
+    out = torch.empty_like(meta_hw) if out is None else out
+    _lib.call("s24_meta_hw_to_f8", ptr(meta_hw), rows, kdim, ptr(out), st.cuda_stream if st is not None else stream())
     return out
+
+
+def _t_codes(R: int, C: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
+    """Output buffers of quant_cols_t for an [R, C] operand (padding zeroed)."""
+    ld = (R + 15) // 16 * 16
+    codes_t = torch.empty(C, ld, dtype=U8, device=dev)
+    if ld > R:
+        codes_t[:, R:].zero_()
+    return codes_t, torch.empty(C, dtype=F32, device=dev)
+
+
+class _Overlap:
+    """Side-stream work next to the main-stream GEMMs (the bf16 path's K4_MODE
+    "side" scheme): outputs are allocated on the main stream before the side
+    stream is forked, temporaries are kept alive in `keep` until the main
+    stream has joined the side stream's event."""
+
+    def __init__(self, dev, enabled: bool):
+        from .splitgemm import side_stream
+
+        self.main = torch.cuda.current_stream(dev)
+        self.side = side_stream(dev) if enabled else None
+        self.keep: list = []
+
+    @property
+    def st(self):
+        return self.side if self.side is not None else self.main
+
+    def fork(self, ev=None) -> None:
+        """The side stream waits for the main stream's work so far (or ev)."""
+        if self.side is not None:
+            if ev is not None:
+                self.side.wait_event(ev)
+            else:
+                self.side.wait_stream(self.main)
+
+    def record(self, stream=None):
+        ev = torch.cuda.Event()
+        ev.record(stream or self.st)
+        return ev
+
+    def join(self, ev) -> None:
+        if ev is not None and self.side is not None:
+            self.main.wait_event(ev)
 
 
 def gemm_f8(aq, sa, bq, sb, M, N, K, out, row_map=None, transposed=False, rows_valid=-1) -> torch.Tensor:
@@ -249,11 +305,11 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     perm_dev = inv_dev = None
     if cfg.permute_tokens and sparse_fwd:
         perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
-    x_in = _frame_rows(x, npad, inv_dev)
-    xq, sx = quant_rows(x_in)
-    w1q, s1 = quant_cols_t(p.w1)  # [h, d] (d % 32 == 0)
     out = torch.empty(n, d, dtype=BF16, device=dev)
     if not sparse_fwd:
+        x_in = _frame_rows(x, npad, None)
+        xq, sx = quant_rows(x_in)
+        w1q, s1 = quant_cols_t(p.w1)  # [h, d] (d % 32 == 0)
         pre = gemm_f8(xq, sx, w1q, s1, n, h, d, torch.empty(n, h, dtype=F32, device=dev), rows_valid=n)
         census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
         r = torch.clamp_min(pre, 0)
@@ -266,6 +322,29 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
                          act_f32=act)
         return out, cache
 
+    from .ffn import K4_MODE, _all_sparse_plan
+    from .splitgemm import alloc_feature_split, run_feature_split
+
+    ov = _Overlap(dev, K4_MODE == "side")
+    fp8b = cfg.fp8_backward and for_backward
+    split_bwd = for_backward and cfg.backward_mode != "dense"
+    # W2 codes for fwd.out -- and the backward's weight codes -- on the side
+    # stream while the main stream gathers / quantizes x and runs K1
+    w2q, s2 = _t_codes(h, d, dev)  # [d, h]
+    wb = None
+    if fp8b:
+        wb = {"w2r": torch.empty(h, d, dtype=U8, device=dev), "s2r": torch.empty(h, dtype=F32, device=dev),
+              "w1r": torch.empty(d, h, dtype=U8, device=dev), "s1r": torch.empty(d, dtype=F32, device=dev)}
+    ov.fork()
+    quant_cols_t(p.w2, w2q, s2, st=ov.st, keep=ov.keep)
+    if wb is not None:
+        quant_rows(p.w2, codes=wb["w2r"], scales=wb["s2r"], st=ov.st)  # w2t per column (K3 B)
+        quant_rows(p.w1, codes=wb["w1r"], scales=wb["s1r"], st=ov.st)  # w1t per column (dX B)
+    ev_w = ov.record()
+
+    x_in = _frame_rows(x, npad, inv_dev)
+    xq, sx = quant_rows(x_in)
+    w1q, s1 = quant_cols_t(p.w1)  # [h, d] (d % 32 == 0)
     vals32 = torch.empty(npad, h // 2, dtype=F32, device=dev)
     amax = torch.zeros(npad, dtype=torch.int32, device=dev)
     act_meta = torch.empty(_lib.meta_hw_bytes(n, h), dtype=U8, device=dev)
@@ -286,16 +365,57 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
     _, sa = quant_rows(vals32, rows=n, amax=amax, codes=aq, deq=act_vals, raw=act_raw)
     meta8 = meta_to_f8(act_meta, n, h)
-    w2q, s2 = quant_cols_t(p.w2)  # [d, h]
-    spmm_f8(aq, meta8, sa, w2q, s2, n, d, h, out, row_map=inv_dev, rows_valid=n)
-    census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
     if plan is not None and plan.hidden_dim != h:
         raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+
+    # backward operands that depend only on the forward, prepared on the side
+    # stream next to fwd.out: the plan, the feature-wise split of act (K4),
+    # and under fp8_backward its e4m3 codes plus the codes of x_in^T (dW1's B).
+    # Everything the side stream reads or writes is allocated (and, with
+    # kernels, initialised) on the main stream before the fork point ev_k1.
+    naive_plan = _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else None
+    ev_k1 = ov.record(ov.main)
+    ov.fork(ev_k1)
     plan_out = plan
     if cfg.backward_mode == "split_masked" and plan_out is None:
-        plan_out = partition_features(counts, cfg.split_ratio)
+        plan_out = partition_features(counts, cfg.split_ratio, launch_stream=ov.st)  # (allocations only here)
+    bplan = naive_plan if naive_plan is not None else plan_out
+    fa = f8 = None
+    if split_bwd:
+        fa = alloc_feature_split(act_vals, act_meta, npad, h, bplan, paired=True)
+    if split_bwd and fp8b:
+        xt = torch.empty(d, npad, dtype=U8, device=dev)  # npad % 128 == 0: no padding columns
+        f8 = dict(wb, vq_a=torch.empty(fa.vs.shape, dtype=U8, device=dev),
+                  sv_a=torch.empty(fa.vs.shape[0], dtype=F32, device=dev), e8_a=torch.empty_like(fa.es),
+                  rows_a=fa.rows(bplan), xt=xt, sxt=torch.empty(d, dtype=F32, device=dev), keep=ov.keep)
+    elif wb is not None:
+        f8 = dict(wb, keep=ov.keep)
+    ov.join(ev_w)
+    spmm_f8(aq, meta8, sa, w2q, s2, n, d, h, out, row_map=inv_dev, rows_valid=n)
+    census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
+    ev_side = None
+    if split_bwd:
+        with torch.cuda.stream(ov.st):
+            run_feature_split(fa, act_vals, act_meta, npad, h, bplan, nonneg=True)
+            if f8 is not None and "vq_a" in f8:
+                f8["vq_a"].zero_()  # (padding rows of the operand)
+        if f8 is not None and "vq_a" in f8:
+            quant_rows(fa.vs, rows=f8["rows_a"], pair_rows=fa.pair_rows, codes=f8["vq_a"], scales=f8["sv_a"],
+                       st=ov.st)
+            meta_to_f8(fa.es, f8["rows_a"], npad, out=f8["e8_a"], st=ov.st)
+            quant_cols_t(x_in, f8["xt"], f8["sxt"], st=ov.st, keep=ov.keep)
+        ev_side = ov.record()
+    elif ov.side is not None and plan_out is not None and plan is None:
+        ev_side = ov.record()
+    if ov.side is None:
+        ev_side = None
+    elif ev_side is None:
+        ev_side = ev_w
     cache = FfnCache(x_in if for_backward else None, n, act_vals, act_meta, None, pre, perm_dev, perm_dev, inv_dev,
-                     plan_out, SparsifyStats(n * h, stats_dev), counts, census, cfg, act_raw=act_raw, act_meta8=meta8)
+                     plan_out, SparsifyStats(n * h, stats_dev), counts, census, cfg, act_split=fa,
+                     act_split_ready=ev_side, act_raw=act_raw, act_meta8=meta8, f8=f8)
+    if ov.side is not None and not for_backward:
+        ov.join(ev_side)
     return out, cache
 
 
@@ -348,10 +468,32 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
         census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
         return FfnGrads(d_w1, d_w2, d_x, None, census)
 
+    # ---------------------------------------------------------- sparse forward
+    from .ffn import K4_MODE
+    from .splitgemm import alloc_feature_split, run_feature_split
+
+    f8 = cache.f8 or {}
+    ov = _Overlap(dev, K4_MODE == "side")
+    mode = cfg.backward_mode
+    raw_naive = mode == "naive_sparse" and not cfg.mask_grad_with_fwd
+    split = mode != "dense" and not raw_naive and cache.act_split is not None
+    # weight codes: prepared by the forward on its side stream (joined before
+    # fwd.out), else here
+    if "w2r" in f8:
+        w2q, s2, w1r, s1r = f8["w2r"], f8["s2r"], f8["w1r"], f8["s1r"]
+    else:
+        w2q, s2 = quant_rows(p.w2)  # w2t per column = w2 per row: [h, d]
+        w1r, s1r = quant_rows(p.w1)  # w1t per column = w1 per row: [d, h]
+    gt = sgt = None
+    if split:
+        # g_c^T codes (dW2's B operand) on the side stream, next to K3
+        gt = torch.empty(d, npad, dtype=U8, device=dev)
+        sgt = torch.empty(d, dtype=F32, device=dev)
+        ov.fork()
+        quant_cols_t(g_c, gt, sgt, st=ov.st, keep=ov.keep)
     # K3 on e4m3 codes: g_pre on the forward keep pattern (relu from the
     # unquantized activation), compressed
     gq, sg = quant_rows(g_c)
-    w2q, s2 = quant_rows(p.w2)  # w2t per column = w2 per row: [h, d]
     g_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
     if npad > n:
         g_vals[n:].zero_()
@@ -363,7 +505,36 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
         G = gemm_f8(gq, sg, w2q, s2, n, h, d, torch.empty(n, h, dtype=F32, device=dev), rows_valid=n)
         g_pre_dense = G * (2 * torch.clamp_min(cache.pre_act, 0))
 
-    mode = cfg.backward_mode
+    # K4 of g_pre and its codes on the side stream, next to the dX GEMM
+    ev_g = None
+    if split:
+        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache.plan
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, paired=True)
+        rows_g = fg.rows(plan)
+        vq_g = torch.empty(fg.vs.shape, dtype=U8, device=dev)
+        sv_g = torch.empty(fg.vs.shape[0], dtype=F32, device=dev)
+        e8_g = torch.empty_like(fg.es)
+        ov.fork()
+        with torch.cuda.stream(ov.st):
+            run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
+            vq_g.zero_()
+        quant_rows(fg.vs, rows=rows_g, pair_rows=fg.pair_rows, codes=vq_g, scales=sv_g, st=ov.st)
+        meta_to_f8(fg.es, rows_g, npad, out=e8_g, st=ov.st)
+        ev_g = ov.record()
+
+    # dX (main stream)
+    if cfg.mask_grad_with_fwd:
+        gsq = torch.empty(npad, h // 2, dtype=U8, device=dev)
+        if npad > n:
+            gsq[n:].zero_()
+        _, sgs = quant_rows(g_vals, rows=n, codes=gsq)
+        spmm_f8(gsq, cache.act_meta8, sgs, w1r, s1r, n, d, h, d_x, row_map=cache.inv_dev, rows_valid=n)
+        ev_dx = GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d))
+    else:
+        aq, sa = quant_rows(g_pre_dense)
+        gemm_f8(aq, sa, w1r, s1r, n, d, h, d_x, row_map=cache.inv_dev, rows_valid=n)
+        ev_dx = GemmEvent("bwd.d_x", False, gemm_macs(n, h, d))
+
     stats_a = stats_g = None
     if mode == "dense":
         act = torch.empty(n, h, dtype=BF16, device=dev)
@@ -383,12 +554,25 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
     else:
         plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache.plan
         macs_w = sp_gemm_macs(n, h, d) if mode == "naive_sparse" else split_gemm_macs(n, d, plan)
-        fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, paired=True)
-        _split_grad_f8(fa, plan, g_c, npad, d_w2, transposed=False)
+        # the forward's side work (act split, its codes, x_in^T codes) and ours
+        if cache.act_split_ready is not None:
+            torch.cuda.current_stream().wait_event(cache.act_split_ready)
+        ov.join(ev_g)
+        fa = cache.act_split
+        if fa is None:
+            fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, paired=True)
+        if "vq_a" in f8:
+            if gt is None:
+                gt, sgt = quant_cols_t(g_c)
+            rows_a, rmap, valid = fa.gemm_rows(plan)
+            spmm_f8(f8["vq_a"], f8["e8_a"], f8["sv_a"], gt, sgt, rows_a, d, npad, d_w2, row_map=rmap,
+                    rows_valid=rows_a, row_valid=valid, pair_rows=max(fa.pair_rows, 0))
+        else:
+            _split_grad_f8(fa, plan, g_c, npad, d_w2, transposed=False)
         stats_a = fa.stats
         census.append(GemmEvent("bwd.d_w2", True, macs_w))
         notify("d_w2", d_w2)
-        if mode == "naive_sparse" and not cfg.mask_grad_with_fwd:
+        if raw_naive:
             gpad = torch.zeros(npad, h, dtype=F32, device=dev)
             gpad[:n] = g_pre_dense
             sgw, _, stats_g = sparsify_feature_wise(gpad)
@@ -396,22 +580,17 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
             _, sv = quant_rows(sgw.data, rows=h, codes=vq)
             bq, sb = quant_cols_t(cache.x_in)
             spmm_f8(vq, meta_to_f8(sgw.meta_hw, h, npad), sv, bq, sb, h, d, npad, d_w1, transposed=True, rows_valid=h)
+        elif ev_g is not None:
+            _, rmap, valid = fg.gemm_rows(plan)
+            xt, sxt = (f8["xt"], f8["sxt"]) if "xt" in f8 else quant_cols_t(cache.x_in)
+            spmm_f8(vq_g, e8_g, sv_g, xt, sxt, rows_g, d, npad, d_w1, row_map=rmap, transposed=True,
+                    rows_valid=rows_g, row_valid=valid, pair_rows=max(fg.pair_rows, 0))
+            stats_g = fg.stats
         else:
             fg = feature_split(g_vals, cache.act_meta, npad, h, plan, paired=True)
             _split_grad_f8(fg, plan, cache.x_in, npad, d_w1, transposed=True)
             stats_g = fg.stats
         census.append(GemmEvent("bwd.d_w1", True, macs_w))
         notify("d_w1", d_w1)
-
-    if cfg.mask_grad_with_fwd:
-        gsq = torch.empty(npad, h // 2, dtype=U8, device=dev)
-        if npad > n:
-            gsq[n:].zero_()
-        _, sgs = quant_rows(g_vals, rows=n, codes=gsq)
-        w1q, s1 = quant_rows(p.w1)  # w1t per column = w1 per row: [d, h]
-        spmm_f8(gsq, cache.act_meta8, sgs, w1q, s1, n, d, h, d_x, row_map=cache.inv_dev, rows_valid=n)
-        census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
-    else:
-        mm_f8(g_pre_dense, p.w1, d_x, row_map=cache.inv_dev)
-        census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
+    census.append(ev_dx)
     return FfnGrads(d_w1, d_w2, d_x, None, census, stats_a, stats_g)
