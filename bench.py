@@ -29,6 +29,7 @@ import subprocess
 import sys
 import tempfile
 import time
+from dataclasses import replace
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -57,6 +58,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the e4m3 (fp8_emulation + fp8_backward) variant")
     ap.add_argument("--sparsity", type=float, default=SPARSITY,
                     help="target activation sparsity of the synthetic inputs (c5 sweep)")
     return ap.parse_args()
@@ -365,8 +367,10 @@ def run_ours(args):
     # weight gradients are then summed across ranks (NCCL all-reduce).
     graphs = {}
 
+    fp8 = replace(recipe, fp8_emulation=True, fp8_backward=not prefill)
+
     def graph_step(cfg, xx=None, gg=None):
-        key = "recipe" if cfg is recipe else "dense"
+        key = "recipe" if cfg is recipe else ("fp8" if cfg is fp8 else "dense")
         g = graphs.get(key)
         if g is None:
             g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill)
@@ -430,6 +434,13 @@ def run_ours(args):
         clocks_d.start()
         t_dense = timed(dense, args.steps)
         clk_dense = clocks_d.stop()
+    # the e4m3 variant of the recipe (the paper's precision): same timing method
+    t_fp8 = None
+    if not args.no_fp8:
+        for _ in range(3):
+            graph_step(fp8)
+        torch.cuda.synchronize()
+        t_fp8 = timed(fp8, args.steps)
     for _ in range(2):  # re-warm the eager allocator pools after the graph phase
         step(recipe, x, dy)
     t_eager = timed(recipe, args.steps, eager=True)
@@ -469,6 +480,13 @@ def run_ours(args):
                                 "ms_per_step": t_dense / args.steps}
         result["speedup_vs_dense"] = t_dense / t_recipe
         result["dense_twin"]["clocks"] = {k: clk_dense.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")}
+    if t_fp8 is not None:
+        result["fp8_variant"] = {
+            "config": "recipe + fp8_emulation" + ("" if prefill else " + fp8_backward"),
+            "dtype": "e4m3 operands (tcgen05 kind::f8f6f4, dense and 2:4), fp32 accumulate, bf16 activations",
+            "ms_per_step": t_fp8 / args.steps, "value": world * n * args.steps / (t_fp8 / 1e3), "unit": "tokens/s",
+            "speedup_vs_bf16_recipe": t_recipe / t_fp8,
+            "speedup_vs_dense_bf16": (t_dense / t_fp8) if t_dense is not None else None}
     result["sparse_tflops"] = flops_useful / (ms_step / 1e3) / 1e12
     result["drops"] = drops
 
