@@ -99,6 +99,11 @@ ACT_SPLIT_IN_BWD = os.environ.get("S24_ACT_SPLIT_IN_BWD", "0") == "1"
 # One K4 pass for the activation and g_pre together (shared metadata work),
 # next to the dX GEMM in the backward ("1"), instead of two passes.
 DUAL_K4 = os.environ.get("S24_DUAL_K4", "0") == "1"
+# Backward tail order: dW2 on the main stream next to K4(g_pre) on the side
+# stream, then dW1 (side, after K4) and dX (third stream, after K3), so each
+# persistent GEMM's last partial wave is filled by the next one's CTAs ("1");
+# or dX next to K4(g_pre), then both weight gradients in one grouped launch ("0").
+WGRAD_OVERLAP = os.environ.get("S24_WGRAD_OVERLAP", "0") == "1"
 
 
 def _dual_k4() -> bool:
@@ -499,6 +504,17 @@ def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
     return cache.act_split
 
 
+_third_streams: dict = {}
+
+
+def _third_stream(device) -> torch.cuda.Stream:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    st = _third_streams.get(idx)
+    if st is None:
+        st = _third_streams[idx] = torch.cuda.Stream(device=device)
+    return st
+
+
 def _all_sparse_plan(h: int, dev) -> SplitPlan:
     pos = torch.arange(h, dtype=torch.int32, device=dev)
     return SplitPlan(h, 1.0, torch.zeros(h, dtype=torch.int64, device=dev), pos,
@@ -644,6 +660,36 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         macs_w = sp_gemm_macs(n, h, d) if mode == "naive_sparse" else split_gemm_macs(n, d, plan)
     fg = None
     fg_ready = None
+    if (WGRAD_OVERLAP and side is not None and cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None
+            and not raw_naive and grad_ready is None and cache.act_fw is None and _layout()["paired"]
+            and not _dual_k4()):
+        # dW2 (main) || K4(g_pre) (side) ; then dW1 (side) || dX (third stream)
+        ev_k3 = torch.cuda.Event()
+        ev_k3.record(main)
+        fa = _act_split(cache, npad, h, plan)
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
+        need_frame_inputs()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
+        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
+        with torch.cuda.stream(side):
+            split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
+            ev_w1 = torch.cuda.Event()
+            ev_w1.record(side)
+        third = _third_stream(dev)
+        third.wait_event(ev_k3)
+        with torch.cuda.stream(third):
+            _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16,
+                      d, ptr(cache.inv_dev), 0, -1, None, 0, third.cuda_stream)
+            ev_x = torch.cuda.Event()
+            ev_x.record(third)
+        main.wait_event(ev_w1)
+        main.wait_event(ev_x)
+        census.append(GemmEvent("bwd.d_w2", True, macs_w))
+        census.append(GemmEvent("bwd.d_w1", True, macs_w))
+        census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
+        return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, fg.stats)
     if cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None and not raw_naive:
         # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
         # as background work in its idle epilogue warps

@@ -256,3 +256,26 @@ def test_nn_module_autograd_matches_api():
     assert torch.equal(x.grad.reshape(-1, d), gr.d_x[:1023])
     assert torch.equal(m.w1.grad, gr.d_w1) and torch.equal(m.w2.grad, gr.d_w2)
     assert m.w1.grad.dtype == torch.float32
+
+
+def test_wgrad_overlap_order_is_bitwise_identical(monkeypatch):
+    """S24_WGRAD_OVERLAP (dW2 || K4(g), then dW1 || dX on three streams) gives
+    the same bits as the default order (dX || K4(g), grouped dW launch)."""
+    from paper_2503_16672_b200 import ffn as F
+
+    n, d, h = 1024, 256, 1024
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=77)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
+    runs = []
+    for flag in (False, True):
+        monkeypatch.setattr(F, "WGRAD_OVERLAP", flag)
+        out, cache = s24.ffn_forward(tx, p, s24.RECIPE)
+        g = s24.ffn_backward(tg, cache, p, s24.RECIPE)
+        torch.cuda.synchronize()
+        runs.append((out, g))
+    (o0, g0), (o1, g1) = runs
+    assert torch.equal(o0, o1)
+    for t in ("d_w1", "d_w2", "d_x"):
+        assert torch.equal(getattr(g0, t), getattr(g1, t)), t
+    assert [e.name for e in g0.census] == [e.name for e in g1.census]
