@@ -286,6 +286,14 @@ int s24_spmm_f8(const uint8_t* a_codes, const uint8_t* a_meta_f8, const uint8_t*
                 int64_t N, int64_t K, const float* row_scale, const float* col_scale, void* D, int out_dtype,
                 int64_t ldd, const int* d_row_map, int d_transposed, int64_t d_rows_valid, const int* d_row_valid,
                 int64_t pair_rows, void* stream);
+/* two s24_spmm_f8 problems of one (M, N, K) in one grouped launch (dW2 and
+ * dW1^T of the fp8_backward split weight gradient) */
+int s24_spmm_pair_f8(int64_t M, int64_t N, int64_t K, int out_dtype, const uint8_t* a0, const uint8_t* meta0,
+                     const uint8_t* B0, int64_t ldb0, const float* rs0, const float* cs0, void* D0, int64_t ldd0,
+                     const int* d_row_map0, int d_transposed0, const int* d_row_valid0, const uint8_t* a1,
+                     const uint8_t* meta1, const uint8_t* B1, int64_t ldb1, const float* rs1, const float* cs1,
+                     void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1, const int* d_row_valid1,
+                     int64_t pair_rows, void* stream);
 /* K1 on e4m3 operands (W1 codes as [N, K]): y = (sx * s1) * acc, then as
  * s24_fwd_gemm1_fused but the kept values go out fp32 [Mpad, N/2] with the
  * per-row max kept value in row_amax (float bits, zeroed by the caller) */

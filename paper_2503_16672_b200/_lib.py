@@ -55,6 +55,8 @@ SIGNATURES: dict[str, list] = {
     "s24_e4m3_encode": [P, I64, P, P],
     "s24_gemm_f8": [P, I64, P, I64, I64, I64, I64, P, P, P, INT, I64, P, INT, I64, P],
     "s24_spmm_f8": [P, P, P, I64, I64, I64, I64, P, P, P, INT, I64, P, INT, I64, P, I64, P],
+    "s24_spmm_pair_f8": [I64, I64, I64, INT, P, P, P, I64, P, P, P, I64, P, INT, P, P, P, P, I64, P, P, P, I64, P, INT,
+                         P, I64, P],
     "s24_fwd_gemm1_f8": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, P, P, P],
     "s24_bwd_dact_f8": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P],
     "s24_last_error": [],

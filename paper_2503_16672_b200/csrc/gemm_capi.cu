@@ -564,6 +564,33 @@ int s24_spmm_f8(const uint8_t* a_codes, const uint8_t* a_meta_f8, const uint8_t*
   });
 }
 
+int s24_spmm_pair_f8(int64_t M, int64_t N, int64_t K, int out_dtype, const uint8_t* a0, const uint8_t* meta0,
+                     const uint8_t* B0, int64_t ldb0, const float* rs0, const float* cs0, void* D0, int64_t ldd0,
+                     const int* d_row_map0, int d_transposed0, const int* d_row_valid0, const uint8_t* a1,
+                     const uint8_t* meta1, const uint8_t* B1, int64_t ldb1, const float* rs1, const float* cs1,
+                     void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1, const int* d_row_valid1,
+                     int64_t pair_rows, void* stream) {
+  int rc = check_common(M, N, K, K, 0, ldb0, 0);
+  if (rc) return rc;
+  if ((rc = check_common(M, N, K, K, 0, ldb1, 0))) return rc;
+  if (!rs0 || !cs0 || !rs1 || !cs1) return fail(S24_ERR_DIMENSION, "e4m3 GEMM needs row and column scales");
+  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
+  if ((!d_transposed0 && ldd0 < N) || (!d_transposed1 && ldd1 < N)) return fail(S24_ERR_DIMENSION, "ldd too small");
+  if (pair_rows < 0 || pair_rows % 2 || pair_rows > M) return fail(S24_ERR_DIMENSION, "pair_rows must be even, <= M");
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    using Epi = EpiStore<OutT, true>;
+    const int pr = static_cast<int>(pair_rows);
+    typename Epi::Params ep0{static_cast<OutT*>(D0), ldd0, d_row_map0, d_transposed0, static_cast<int>(M),
+                             d_row_valid0, 0, pr, rs0, cs0};
+    GemmOperands<Epi> second{a1, K / 2, B1, ldb1, meta1,
+                             typename Epi::Params{static_cast<OutT*>(D1), ldd1, d_row_map1, d_transposed1,
+                                                  static_cast<int>(M), d_row_valid1, 0, pr, rs1, cs1}};
+    return launch_gemm<F8SparseK, Epi>(a0, K / 2, B0, ldb0, M, N, K, meta0, ep0, static_cast<cudaStream_t>(stream),
+                                       1, nullptr, &second);
+  });
+}
+
 int s24_fwd_gemm1_f8(const uint8_t* xq, int64_t ldx, const uint8_t* w1q, int64_t ldw1, int64_t M, int64_t N,
                      int64_t K, const float* x_scale, const float* w1_scale, float* act_vals32, unsigned* row_amax,
                      uint8_t* act_meta, int* counts, unsigned long long* stats, float* y_dbg, void* stream) {

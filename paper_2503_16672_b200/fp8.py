@@ -561,6 +561,19 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
         fa = cache.act_split
         if fa is None:
             fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, paired=True)
+        if "vq_a" in f8 and ev_g is not None and grad_ready is None and gt is not None and "xt" in f8:
+            # both split weight gradients in one grouped e4m3 launch (no
+            # per-gradient hook to serve): dW2 = split(act)^T g_c, dW1^T = split(g_pre)^T x_in
+            rows_a, rmap, valid = fa.gemm_rows(plan)
+            _lib.call("s24_spmm_pair_f8", rows_a, d, npad, _lib.F32,
+                      ptr(f8["vq_a"]), ptr(f8["e8_a"]), ptr(gt), gt.stride(0), ptr(f8["sv_a"]), ptr(sgt), ptr(d_w2),
+                      d_w2.stride(0), ptr(rmap), 0, ptr(valid),
+                      ptr(vq_g), ptr(e8_g), ptr(f8["xt"]), f8["xt"].stride(0), ptr(sv_g), ptr(f8["sxt"]), ptr(d_w1),
+                      d_w1.stride(0), ptr(rmap), 1, ptr(valid), max(fa.pair_rows, 0), s)
+            census.append(GemmEvent("bwd.d_w2", True, macs_w))
+            census.append(GemmEvent("bwd.d_w1", True, macs_w))
+            census.append(ev_dx)
+            return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, fg.stats)
         if "vq_a" in f8:
             if gt is None:
                 gt, sgt = quant_cols_t(g_c)

@@ -252,3 +252,27 @@ def test_quant_rows_boundary_stress():
     # (bf16-rounded copy for the column path, checked against its own oracle)
     rc2, rs2 = O.quantize(t.t().contiguous().bfloat16().float().cpu().numpy(), "cols")
     assert np.array_equal(cs.cpu().numpy(), rs2) and np.array_equal(ct.cpu().numpy(), rc2.T)
+
+
+def test_spmm_pair_f8_matches_two_launches():
+    torch.manual_seed(31)
+    M, N, K = 384, 256, 512
+    ops = []
+    for i in range(2):
+        a = torch.randn(M, K, device="cuda").bfloat16()
+        vals, _, meta_hw, _, _ = gpu_sparsify_token(a)
+        codes, scales, _, _ = quant_rows(vals[:M].contiguous(), pair_rows=64)
+        meta8 = torch.empty_like(meta_hw)
+        _lib.call("s24_meta_hw_to_f8", P(meta_hw), M, K, P(meta8), S())
+        ops.append((codes, meta8, scales, rand_codes(N, K, seed=40 + i), torch.rand(N, device="cuda") + 0.5))
+    rmap = torch.randperm(M + 16, device="cuda")[:M].int()
+    refs = [torch.zeros(M + 16, N, device="cuda"), torch.zeros(N, M + 16, device="cuda")]
+    for (c, e, sa, b, sb), ref, tr in zip(ops, refs, (0, 1)):
+        _lib.call("s24_spmm_f8", P(c), P(e), P(b), K, M, N, K, P(sa), P(sb), P(ref), F32, ref.shape[1], P(rmap), tr,
+                  -1, None, 64, S())
+    outs = [torch.zeros_like(refs[0]), torch.zeros_like(refs[1])]
+    (c0, e0, sa0, b0, sb0), (c1, e1, sa1, b1, sb1) = ops
+    _lib.call("s24_spmm_pair_f8", M, N, K, F32, P(c0), P(e0), P(b0), K, P(sa0), P(sb0), P(outs[0]), N, P(rmap), 0,
+              None, P(c1), P(e1), P(b1), K, P(sa1), P(sb1), P(outs[1]), M + 16, P(rmap), 1, None, 64, S())
+    assert torch.equal(outs[0], refs[0]) and torch.equal(outs[1], refs[1])
+    assert outs[0].abs().sum() > 0 and outs[1].abs().sum() > 0
