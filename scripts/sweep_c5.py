@@ -1,6 +1,7 @@
 """c5: activation-sparsity sweep at the 7B-class shape.
 
-For each target sparsity s: the recipe fwd+bwd step (graph) vs the dense twin,
+For each target sparsity s: the recipe fwd+bwd step (graph) vs the dense twin
+(timed in interleaved blocks by bench.py, so both see the same clocks),
 the drop fractions (token-wise forward, feature-wise backward for act and
 g_pre) and the sparse TFLOPS. One bench.py process per point (c4 shape,
 32768 tokens, d=4096, h=16384). Writes a JSON list and prints a table.
@@ -38,17 +39,21 @@ def main():
             continue
         row = {"sparsity": s, "ms_per_step": d["ms_per_step"], "dense_ms_per_step": d["dense_twin"]["ms_per_step"],
                "speedup_vs_dense": d["speedup_vs_dense"], "sparse_tflops": d["sparse_tflops"],
-               "iid_token_wise_drop": IID_DROP[s], **d["drops"], "clocks": d["clocks"]}
+               "iid_token_wise_drop": IID_DROP[s], **d["drops"], "clocks": d["clocks"],
+               "dense_clocks": d["dense_twin"].get("clocks"),
+               "fp8_ms_per_step": (d.get("fp8_variant") or {}).get("ms_per_step"),
+               "fp8_speedup_vs_dense_bf16": (d.get("fp8_variant") or {}).get("speedup_vs_dense_bf16")}
         rows.append(row)
         print(json.dumps(row), flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(rows, indent=1))
     print(f"\n{'s':>5} {'ms':>7} {'dense':>7} {'speedup':>8} {'TF/s':>7} {'fwd drop':>9} {'iid':>7} "
-          f"{'act fw':>7} {'g fw':>7}")
+          f"{'act fw':>7} {'g fw':>7} {'fp8 ms':>7} {'MHz':>6}")
     for r in rows:
         print(f"{r['sparsity']:5.2f} {r['ms_per_step']:7.3f} {r['dense_ms_per_step']:7.3f} {r['speedup_vs_dense']:8.3f} "
               f"{r['sparse_tflops']:7.0f} {r['fwd_token_wise_dropped_fraction']:9.4%} {r['iid_token_wise_drop']:7.3%} "
-              f"{r['bwd_act_feature_wise_dropped_fraction']:7.3%} {r['bwd_grad_feature_wise_dropped_fraction']:7.3%}")
+              f"{r['bwd_act_feature_wise_dropped_fraction']:7.3%} {r['bwd_grad_feature_wise_dropped_fraction']:7.3%} "
+              f"{r['fp8_ms_per_step'] or 0:7.3f} {r['clocks'].get('sm_mhz') or 0:6.0f}")
 
 
 if __name__ == "__main__":
