@@ -204,6 +204,17 @@ int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype
                   const void* B1, int64_t ldb1, void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1,
                   const int* d_row_valid1, int64_t pair_rows, void* stream);
 
+/* s24_spmm whose CTAs also compute the paired-layout feature-wise split
+ * (s24_feature_split_x) of the GEMM's own A operand -- the token-wise
+ * compressed [M, K/2] values + hw metadata -- from the pipeline stages the
+ * MMA consumes (no separate read of A). fs_n = pad128(M) tokens; outputs
+ * vs / es as s24_feature_split_x. The fwd.out / bwd.d_x GEMM of the recipe
+ * with the K4 of act / g_pre folded in. */
+int s24_spmm_fs(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
+                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
+                int64_t d_rows_valid, const int* d_row_valid, int64_t fs_n, const int* fs_feat_pos,
+                int64_t fs_n_sparse, int64_t fs_n_dense, void* fs_vs, uint8_t* fs_es, int fs_nonneg, void* stream);
+
 /* s24_spmm plus a feature-wise split (the K4 job of s24_feature_split with
  * stats == NULL) run as background work by the GEMM's epilogue warps while
  * they wait for accumulators: the tensor-bound sparse GEMM hides the

@@ -43,6 +43,7 @@ SIGNATURES: dict[str, list] = {
     "s24_gemm_splitk": [P, INT, I64, P, INT, I64, I64, I64, I64, INT, P, P, INT, I64, P, INT, P],
     "s24_spmm": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, I64, P],
     "s24_spmm_pair": [INT, I64, I64, I64, INT, P, P, P, I64, P, I64, P, INT, P, P, P, P, I64, P, I64, P, INT, P, I64, P],
+    "s24_spmm_fs": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, I64, P, I64, I64, P, P, INT, P],
     "s24_spmm_bg": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P, P, I64, I64, P, I64, I64, P, P, P,
                     P, P],
     "s24_fwd_gemm1_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, P, P, I64, P, P],

@@ -35,6 +35,7 @@
 // Descriptors: K-major SBO = 1024; MN-major LBO = box stride, SBO = 1024.
 #pragma once
 #include "k4.cuh"
+#include "k4s.cuh"
 #include "meta.cuh"
 #include "ptx.cuh"
 
@@ -60,10 +61,12 @@ struct GemmShape {
   int* sched;           // dynamic tile scheduler {next, done} (zero at launch, reset by the
                         // last cluster), or nullptr: static round-robin units
   K4Job bg;
+  int has_fs;           // 1: the K4 warps split this GEMM's own A stages (K4W > 0, k4s.cuh)
+  K4Args fs;            // their outputs (feat_pos, pair_rows, vs, es, n = padded tokens, h, nonneg)
 };
 
 template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8, int MC_ = 1,
-          bool F8_ = false>
+          bool F8_ = false, int K4W_ = 0>
 struct GemmCfg {
   static constexpr bool SPARSE = SPARSE_;
   // F8: e4m3 operands (tcgen05 kind::f8f6f4). Every stage and MMA step moves
@@ -105,18 +108,27 @@ struct GemmCfg {
   static constexpr int SCHED_SLOTS = 4;  // work-unit broadcast ring (dynamic scheduler)
   // the dynamic smem base is declared 1024-aligned (SWIZZLE_128B atoms), so no
   // alignment slack is reserved: 7 dense stages fit next to a 2 KB static LUT
-  static constexpr uint32_t SMEM_BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20;
+  // K4W > 0: warps that split the A stages feature-wise (k4s.cuh); each stage
+  // then also waits for their release, and the peer CTA learns that a stage
+  // landed through its own k4_ready barrier (the TMA completes on the leader's)
+  static constexpr int K4W = K4W_;
+  // (each stage index must always be served by the same K4 warp, or a warp's
+  // parity wait could match the previous phase of a stage another warp uses)
+  static_assert(K4W == 0 || (SPARSE && !F8 && K4W % 4 == 0 && MC_ == 1 && STAGES_ % K4W == 0),
+                "K4 warps: bf16 2:4 configs, STAGES a multiple of K4W");
+  static constexpr uint32_t SMEM_BYTES =
+      BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20 + (K4W > 0 ? 8 + STAGES * 8 : 0);
   static constexpr uint32_t IDESC =
       F8 ? make_idesc_e4m3(TILE_M, BN, SPARSE) : make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
   static constexpr int EPI_THREADS = 32 * EPI_WARPS;
-  static constexpr int THREADS = 128 + EPI_THREADS;
+  static constexpr int THREADS = 128 + EPI_THREADS + 32 * K4W;
   static constexpr int CPW = NCHUNK / (EPI_WARPS / 4);  // chunks per epilogue warp
   static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
   // 4-epilogue-warp configs cap registers at 128/thread so that an
   // independent kernel (e.g. K4 on a side stream) can co-reside on the SM
-  static constexpr int MIN_BLOCKS = EPI_WARPS == 4 ? 2 : 1;
+  static constexpr int MIN_BLOCKS = (EPI_WARPS == 4 && K4W == 0) ? 2 : 1;
   // B multicast across MC CTA pairs (see header)
   static constexpr int MC = MC_;
   static constexpr int CLUSTER = CG * MC;
@@ -190,12 +202,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   uint64_t* sched_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);
   uint64_t* sched_empty = sched_full + NS;
   uint32_t* sched_tile = reinterpret_cast<uint32_t*>(sched_empty + NS);
+  uint64_t* k4_ready = reinterpret_cast<uint64_t*>(sched_tile + NS + 2);  // (8-byte aligned)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   // roles: epilogue warps first, the latency-critical producer / MMA warps get
   // the highest ids (the warp arbiter prefers higher warp ids)
-  constexpr int W_PROD = Cfg::EPI_WARPS, W_MMA = Cfg::EPI_WARPS + 1, W_ALLOC = Cfg::EPI_WARPS + 2;
+  // (K4 warps, when present, take the lowest ids: 0 .. K4W-1)
+  constexpr int K4W = Cfg::K4W;
+  constexpr int W_PROD = K4W + Cfg::EPI_WARPS, W_MMA = W_PROD + 1, W_ALLOC = W_PROD + 2;
   constexpr int MC = Cfg::MC;
   const uint32_t crank = Cfg::CLUSTER > 1 ? cluster_ctarank() : 0u;
   const uint32_t rank = crank % CG;      // rank within the CTA pair
@@ -229,7 +244,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   if (warp == W_MMA && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], CG);
-      mbar_init(&empty_bar[s], MC);
+      mbar_init(&empty_bar[s], MC + (K4W > 0 ? 1 : 0));
+      if constexpr (K4W > 0) mbar_init(&k4_ready[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     for (int i = 0; i < NS; ++i) {
       mbar_init(&sched_full[i], 1);
       // leader MMA + leader epilogue warps (+ peer producer + peer epilogue warps)
-      mbar_init(&sched_empty[i], 1 + Cfg::EPI_WARPS + (CG - 1) * (1 + Cfg::EPI_WARPS));
+      mbar_init(&sched_empty[i], 1 + Cfg::EPI_WARPS + (CG - 1) * (1 + Cfg::EPI_WARPS) + K4W * CG);
     }
     fence_barrier_init();
   }
@@ -479,10 +495,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       }
     }
     __syncwarp();
-  } else if (warp < Cfg::EPI_WARPS) {
+  } else if (warp >= K4W && warp < K4W + Cfg::EPI_WARPS) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;                 // TMEM lane quarter
-    const int part = warp >> 2;             // which contiguous run of CPW chunks
+    const int ew = warp - K4W;              // (K4W % 4 == 0: warp % 4 is still the TMEM lane quarter)
+    const int q = ew & 3;                   // TMEM lane quarter
+    const int part = ew >> 2;               // which contiguous run of CPW chunks
     const int c_begin = part * Cfg::CPW;
     const bool owns_last = c_begin + Cfg::CPW == Cfg::NCHUNK;
     typename Epi::State st;
@@ -583,6 +600,65 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     while (bg_more && bg_unit()) {
     }
     Epi::finish(ep, st, lane);
+  } else if (K4W > 0 && warp < K4W) {
+    // ------------------------------------------------------------ K4 warps (k4s.cuh)
+    // Walk the same stage sequence as the MMA; warp w serves the stage uses
+    // it with it % K4W == w: wait until the stage landed, copy this tile's
+    // units to registers, release the stage, split them.
+    if constexpr (K4W > 0) {
+      __shared__ K4sSlot k4s_slots[K4W][16];
+      const uint2* lut = k4_lut_init();
+      const int tn = shape.tiles_n < 8 ? shape.tiles_n : 8;
+      int stage = 0;
+      uint32_t phase = 0;
+      long long it = 0;
+      for (int iter = 0;; ++iter) {
+        const int t = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
+        if (t >= total_tiles) break;
+        int mb, nb, kb0, kb1;
+        tile_coords(shape, t % mn_tiles, mb, nb);
+        kb_range(t, kb0, kb1);
+        const int m0 = (mb * MC + static_cast<int>(pair)) * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
+        const bool work = shape.has_fs && nb < tn && m0 < shape.fs.n;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (static_cast<int>(it % K4W) == warp) {
+            if (leader) {
+              mbar_wait(&full_bar[stage], phase);
+              if constexpr (CG == 2)
+                if (lane == 0) mbar_arrive_remote_release(&k4_ready[stage], leader_rank + 1);
+            } else {
+              mbar_wait_cluster(&k4_ready[stage], phase);
+            }
+            const uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+            const uint8_t* se = sa + Cfg::A_BYTES + Cfg::B_BYTES;
+            K4sRegs u;
+            int j = nb;
+            if (work) k4s_load(sa, se, j, static_cast<int>(lane), u);
+            if (work && j + tn < 8) {
+              // small N (fewer than 8 N tiles): this tile owns several units;
+              // all but the last are split while the stage is still held
+              for (; j + tn < 8; j += tn) {
+                k4s_compute(shape.fs, u, kb * 128 + j * 16, m0, static_cast<int>(lane), lut, k4s_slots[warp]);
+                k4s_load(sa, se, j + tn, static_cast<int>(lane), u);
+              }
+            }
+            // release the stage only once this warp's copies have landed in
+            // registers (the arrive depends on the loaded words) and are
+            // ordered before the TMA refill (generic -> async proxy)
+            uint32_t dep = 1u;
+            if (work) dep |= k4s_fold(u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            dep = __reduce_or_sync(0xffffffffu, dep);
+            if (lane == 0 && dep != 0u) mbar_arrive(&empty_bar[stage]);
+            if (work) k4s_compute(shape.fs, u, kb * 128 + j * 16, m0, static_cast<int>(lane), lut, k4s_slots[warp]);
+          }
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
   }
 
   tc_fence_before();

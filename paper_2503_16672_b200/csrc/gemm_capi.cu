@@ -153,7 +153,8 @@ static int make_operand_maps(const void* A, int64_t lda, const void* B, int64_t 
 template <class Cfg, class Epi>
 static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                        const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1,
-                       const K4Job* bg = nullptr, const GemmOperands<Epi>* second = nullptr) {
+                       const K4Job* bg = nullptr, const GemmOperands<Epi>* second = nullptr,
+                       const K4Args* fs = nullptr) {
   if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
   CUtensorMap ma, mb, me, ma2, mb2, me2;
@@ -199,6 +200,12 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
     sh.bg = *bg;
   else
     std::memset(&sh.bg, 0, sizeof(sh.bg));
+  sh.has_fs = fs != nullptr;
+  if (fs)
+    sh.fs = *fs;
+  else
+    std::memset(&sh.fs, 0, sizeof(sh.fs));
+  if (fs && (k_splits > 1 || second)) return fail(S24_ERR_CONFIG, "the in-GEMM feature split needs one problem, no split-K");
   const int tiles = sh.tiles_m * sh.tiles_n * sh.k_splits * sh.groups;
 
   auto kern = gemm_kernel<Cfg, Epi>;
@@ -262,6 +269,12 @@ using DenseMK = GemmCfg<false, true, false, 256, S24_DENSE_STAGES, 2, 8, S24_DEN
 #endif
 using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4, S24_SPARSE_MC>;   // sparse A, B MN-major
 using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, S24_SPARSE_MC>;  // sparse A, B K-major
+// ... plus warps that split the A stages feature-wise (k4s.cuh)
+#ifndef S24_FS_WARPS
+#define S24_FS_WARPS 4
+#endif
+using SparseN_FS = GemmCfg<true, false, true, 256, 4, 2, 4, 1, false, S24_FS_WARPS>;
+using SparseK_FS = GemmCfg<true, false, false, 256, 4, 2, 4, 1, false, S24_FS_WARPS>;
 
 // e4m3 (kind::f8f6f4): same byte geometry per stage as the bf16 configs
 using F8DenseKK = GemmCfg<false, false, false, 256, S24_DENSE_STAGES, 2, 8, 1, true>;
@@ -407,6 +420,35 @@ int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_
                                        static_cast<int>(pair_rows)};
     return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep,
                                            static_cast<cudaStream_t>(stream));
+  });
+}
+
+int s24_spmm_fs(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
+                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
+                int64_t d_rows_valid, const int* d_row_valid, int64_t fs_n, const int* fs_feat_pos,
+                int64_t fs_n_sparse, int64_t fs_n_dense, void* fs_vs, uint8_t* fs_es, int fs_nonneg, void* stream) {
+  int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
+  if (rc) return rc;
+  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
+  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
+  if (fs_n % 128 != 0 || fs_n < M || fs_n > (M + 255) / 256 * 256)
+    return fail(S24_ERR_DIMENSION, "feature split tokens %lld must be pad128(M) for M = %lld", (long long)fs_n,
+                (long long)M);
+  if (!fs_vs || !fs_es || !fs_feat_pos) return fail(S24_ERR_DIMENSION, "feature split outputs required");
+  auto st = static_cast<cudaStream_t>(stream);
+  K4Args fs;
+  rc = k4_prepare(a_vals, a_meta, fs_n, K, fs_feat_pos, fs_n_sparse, fs_n_dense, fs_vs, fs_es, nullptr, st, &fs,
+                  2 * fs_n_dense);
+  if (rc) return rc;
+  fs.nonneg = fs_nonneg;
+  return with_out(out_dtype, [&](auto tag) {
+    using OutT = std::remove_pointer_t<decltype(tag)>;
+    using Epi = EpiStore<OutT>;
+    typename Epi::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
+                            static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
+    if (b_mn_major)
+      return launch_gemm<SparseN_FS, Epi>(a_vals, K / 2, B, ldb, M, N, K, a_meta, ep, st, 1, nullptr, nullptr, &fs);
+    return launch_gemm<SparseK_FS, Epi>(a_vals, K / 2, B, ldb, M, N, K, a_meta, ep, st, 1, nullptr, nullptr, &fs);
   });
 }
 

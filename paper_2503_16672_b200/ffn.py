@@ -73,6 +73,8 @@ FUSED_FEATURE_SPLIT = os.environ.get("S24_FUSED_FW", "0") == "1"
 #                   GEMMs cap their registers to leave room for it)  [default]
 #   "background" -- inside the GEMM, in its idle epilogue warps (s24_spmm_bg)
 #   "inline"     -- serialized on the main stream
+#   "gemm"       -- inside the GEMM, by extra warps that split its own A
+#                   pipeline stages (s24_spmm_fs, csrc/k4s.cuh)
 K4_MODE = os.environ.get("S24_K4_MODE", "side")
 # Both split weight gradients in one grouped sparse launch (s24_spmm_pair)
 # when no per-gradient hook needs dW2 early. S24_PAIRED_WGRAD=0 disables.
@@ -431,7 +433,12 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
             act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, **_layout())
-        if want_split and K4_MODE == "background":
+        if want_split and K4_MODE == "gemm" and _layout()["paired"] and not _layout()["identity"]:
+            # fwd.out whose CTAs also split their act stages feature-wise
+            _lib.call("s24_spmm_fs", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
+                      ptr(inv_dev), 0, -1, None, npad, ptr(bg_plan.feat_pos), bg_plan.n_sparse, bg_plan.n_dense,
+                      ptr(act_split.vs), ptr(act_split.es), 1, s)
+        elif want_split and K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16,
                       d, ptr(inv_dev), 0, -1, None,
@@ -694,7 +701,12 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
         # as background work in its idle epilogue warps
         fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
-        if K4_MODE == "background":
+        if K4_MODE == "gemm" and fg.pair_rows >= 0 and not fg.identity:
+            # dX whose CTAs also split their g_pre stages feature-wise
+            _lib.call("s24_spmm_fs", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16,
+                      d, ptr(cache.inv_dev), 0, -1, None, npad, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense,
+                      ptr(fg.vs), ptr(fg.es), 0, s)
+        elif K4_MODE == "background":
             counter = torch.empty(1, dtype=torch.int32, device=dev)
             _lib.call("s24_spmm_bg", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x),
                       _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None,

@@ -279,3 +279,26 @@ def test_wgrad_overlap_order_is_bitwise_identical(monkeypatch):
     for t in ("d_w1", "d_w2", "d_x"):
         assert torch.equal(getattr(g0, t), getattr(g1, t)), t
     assert [e.name for e in g0.census] == [e.name for e in g1.census]
+
+
+@pytest.mark.parametrize("n,d,h", [(1024, 256, 1024), (640, 512, 512)])
+def test_k4_in_gemm_is_bitwise_identical(monkeypatch, n, d, h):
+    """S24_K4_MODE=gemm (the act / g_pre feature splits computed by extra
+    warps of fwd.out / dX from their own A stages, s24_spmm_fs) gives the same
+    bits as the side-stream K4 kernels."""
+    from paper_2503_16672_b200 import ffn as F
+
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=78)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
+    runs = []
+    for mode in ("side", "gemm"):
+        monkeypatch.setattr(F, "K4_MODE", mode)
+        out, cache = s24.ffn_forward(tx, p, s24.RECIPE)
+        g = s24.ffn_backward(tg, cache, p, s24.RECIPE)
+        torch.cuda.synchronize()
+        runs.append((out, g))
+    (o0, g0), (o1, g1) = runs
+    assert torch.equal(o0, o1)
+    for t in ("d_w1", "d_w2", "d_x"):
+        assert torch.equal(getattr(g0, t), getattr(g1, t)), t
