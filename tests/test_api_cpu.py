@@ -88,11 +88,18 @@ def test_toy_schedule_and_config_validation():
     assert toy.lr_at(tc, 5) == 0.5 and toy.lr_at(tc, 10) == 1.0
     assert toy.lr_at(tc, 11) == 1.0 and abs(toy.lr_at(tc, 100)) < 1e-12
     assert abs(toy.lr_at(tc, 55) - 0.5 * (1 + _m.cos(_m.pi * 44 / 89))) < 1e-12
-    for bad in (dict(batch_tokens=6), dict(steps=10, warmup_dense_steps=11), dict(plan_refresh_every=0)):
+    for bad in (dict(batch_tokens=0), dict(steps=10, warmup_dense_steps=11), dict(plan_refresh_every=0),
+                dict(eval_every=0), dict(lr_schedule="step"), dict(split_fraction=0.0)):
         with pytest.raises(ConfigError):
             toy.TrainConfig(**bad)
     with pytest.raises(ConfigError):
         toy.ToyModelConfig(hidden=100)
-    (tr, ev) = toy.byte_windows(bytes(range(20)), 4, 0.5, "cpu")
-    assert tr[0].shape == (8, 4) and ev[0].shape == (8, 4)
-    assert tr[0][3].tolist() == [3, 4, 5, 6] and int(tr[1][3]) == 7
+    tr, ev = toy.build_dataset(bytes(range(20)), 4, 0.5, "cpu")
+    assert tr.contexts.shape == (8, 4) and ev.contexts.shape == (8, 4) and len(tr) == 8
+    assert tr.contexts[3].tolist() == [3, 4, 5, 6] and int(tr.targets[3]) == 7
+    from paper_2503_16672_b200.errors import DataError
+    with pytest.raises(DataError):
+        toy.build_dataset(b"abc", 4, 0.9, "cpu")
+    assert [k for k, _ in toy.ABLATION_ROWS][:3] == ["dense-swiglu", "dense-relu2", "recipe"]
+    mc, tcr = toy.ablation_configs(toy.ToyModelConfig(), toy.TrainConfig(), "no-permute")
+    assert tcr.ffn.forward_mode == "sparse24" and not tcr.ffn.permute_tokens

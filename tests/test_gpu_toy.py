@@ -1,13 +1,19 @@
 """Toy-scale recipe parity (ref tests/test_acceptance.py:294-318, SURVEY 8f
 row 1): a byte-level LM whose FFN blocks run on the B200 kernels trains to
 the same eval loss with the full recipe (dense warmup, sparse24 forward,
-split backward) as with the dense FFN, within the reference's 5% gap."""
+split backward, plans reused for 2 steps) as with the dense FFN, within the
+reference's 5% gap; plus the harness API (metrics, ablation rows, divergence,
+checkpoints)."""
 
+import json
 import math
 from pathlib import Path
 
+import numpy as np
 import pytest
+import torch
 
+import paper_2503_16672_b200 as s24
 from paper_2503_16672_b200 import toy
 
 pytestmark = pytest.mark.gpu
@@ -20,19 +26,49 @@ def corpus() -> bytes:
     return b"\n".join((ROOT / f).read_bytes() for f in files)
 
 
-def test_recipe_trains_like_dense():
+def test_recipe_trains_like_dense(tmp_path):
+    path = tmp_path / "corpus.txt"
+    path.write_bytes(corpus())
     mc = toy.ToyModelConfig(embed_dim=64, hidden=256, num_blocks=2, context=8)
     tc = toy.TrainConfig(steps=400, warmup_dense_steps=40, batch_tokens=256, lr=3e-3, lr_warmup_steps=40,
                          eval_every=200, eval_tokens=4096, plan_refresh_every=2)
-    rows = {r.label: r for r in toy.ablate(corpus(), mc, tc, rows=("dense-relu2", "recipe"))}
+    rows = {r.key: r for r in toy.ablate(path, mc, tc, rows=("dense-relu2", "recipe"))}
     dense, recipe = rows["dense-relu2"], rows["recipe"]
     assert not dense.diverged and not recipe.diverged
     assert math.isfinite(recipe.final_eval_loss) and recipe.final_eval_loss < 3.5  # learned (ln 256 = 5.5)
     gap = abs(recipe.final_eval_loss - dense.final_eval_loss) / dense.final_eval_loss
     assert gap <= 0.05, (recipe.final_eval_loss, dense.final_eval_loss)
-    # token-wise drop fractions of the forward (reported; at toy scale the
-    # activation is dense, so they are high -- the reference does not assert them)
-    drops = [f for row in recipe.dropped_fraction for f in row]
-    assert drops and all(0.0 <= f < 1.0 for f in drops)
-    print(f"[reported] eval dense {dense.final_eval_loss:.4f} recipe {recipe.final_eval_loss:.4f} gap {gap:.2%}; "
-          f"forward drop first {drops[0]:.3f} last {drops[-1]:.3f}")
+    assert recipe.gemms_sparse_last_step > 0 and dense.gemms_sparse_last_step == 0
+    print(f"[reported] eval dense {dense.final_eval_loss:.4f} recipe {recipe.final_eval_loss:.4f} gap {gap:.2%}")
+
+
+def test_harness_metrics_checkpoint_and_divergence(tmp_path):
+    mc = toy.ToyModelConfig(embed_dim=64, hidden=128, num_blocks=2, context=8)
+    tc = toy.TrainConfig(steps=20, warmup_dense_steps=5, batch_tokens=128, lr_warmup_steps=5, eval_every=10,
+                         eval_tokens=512, ffn=s24.RECIPE)
+    metrics, model = toy.train(mc, tc, corpus())
+    assert [m.step for m in metrics] == [10, 20]
+    last = metrics[-1]
+    assert len(last.per_layer_sparsity) == 2 and all(0.0 <= s <= 1.0 for s in last.per_layer_sparsity)
+    assert all(0.0 <= f < 1.0 for f in last.per_layer_dropped_fraction)
+    # recipe census per block: fwd.pre_act (dense), fwd.out (2:4), bwd.d_act (dense), dW2, dW1, dX (2:4)
+    assert last.gemms_dense == 2 * 2 and last.gemms_sparse == 2 * 4 and last.macs_this_step > 0
+    csv = toy.metrics_to_csv(metrics).splitlines()
+    assert csv[0] == toy.METRICS_HEADER and len(csv) == 1 + 2 * 2
+    toy.save_checkpoint(tmp_path / "ckpt", model, mc, tc, 20, corpus="corpus.txt")
+    man = json.loads((tmp_path / "ckpt" / "manifest.json").read_text())
+    assert man["step"] == 20 and set(man["params"]) == set(model.param_dict())
+    w = s24.read_matrix(tmp_path / "ckpt" / man["params"]["block0.w1"]["file"])
+    assert np.array_equal(w, model.w1[0].detach().cpu().numpy())
+
+    def blow_up(step, grads):  # a NaN gradient at step 3 is reported with its step
+        if step == 3:
+            grads = dict(grads)
+            grads["head"] = torch.full_like(grads["head"], float("nan"))
+        return grads
+
+    with pytest.raises(s24.DivergenceError) as ei:
+        toy.train(mc, tc, corpus(), grad_transform=blow_up)
+    assert ei.value.step == 3
+    with pytest.raises(s24.ConfigError):
+        toy.ablate(corpus(), mc, tc, rows=["dense-swiglu"])
