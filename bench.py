@@ -381,7 +381,7 @@ def run_ours(args):
         key = "recipe" if cfg is recipe else ("fp8" if cfg is fp8 else "dense")
         g = graphs.get(key)
         if g is None:
-            g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill)
+            g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill, grad_bucket=world > 1)
             g.x.copy_(x)
             g.dy.copy_(dy)
         if xx is not None:
@@ -389,8 +389,7 @@ def run_ours(args):
             g.dy.copy_(gg, non_blocking=True)
         g.replay()
         if world > 1 and not prefill:
-            dist.all_reduce(g.d_w1)
-            dist.all_reduce(g.d_w2)
+            dist.all_reduce(g.bucket)  # one NCCL all-reduce of [dW1 | dW2]
         return g
 
     def barrier():
@@ -485,10 +484,10 @@ def run_ours(args):
         "config": {"workload": WORKLOAD[args.config], "tokens_per_gpu": n, "global_tokens": n * world, "d": d,
                    "h": h, "activation_sparsity": args.sparsity, "recipe": "sparse24 fwd + split_masked bwd (ratio 0.95) "
                    "+ mask_grad_with_fwd + permute_tokens", "parallelism": f"dp{world} (token shards, NCCL "
-                   "all-reduce of dW1/dW2)" if world > 1 else "single GPU",
+                   "all-reduce of the [dW1 | dW2] bucket)" if world > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps, outside the step events",
                    "step": "s24.FfnStepGraph replay (whole fwd+bwd as one CUDA graph)"
-                           + (" + NCCL all-reduce of dW1, dW2" if world > 1 else "")},
+                           + (" + one NCCL all-reduce of the [dW1 | dW2] bucket" if world > 1 else "")},
         "eager_ms_per_step": t_eager / args.steps,
     }
     if t_dense is not None:

@@ -511,6 +511,15 @@ def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
     return cache.act_split
 
 
+def weight_grad_buffers(d: int, h: int, dev, bucket: torch.Tensor | None = None):
+    """(d_w1 [d, h], d_w2 [h, d]) fp32: fresh tensors, or views into bucket."""
+    if bucket is None:
+        return torch.empty(d, h, dtype=F32, device=dev), torch.empty(h, d, dtype=F32, device=dev)
+    if bucket.dtype != F32 or bucket.numel() != 2 * d * h or not bucket.is_contiguous():
+        raise DimensionError(f"grad_bucket must be a contiguous fp32 buffer of {2 * d * h} elements")
+    return bucket[: d * h].view(d, h), bucket[d * h:].view(h, d)
+
+
 _third_streams: dict = {}
 
 
@@ -528,12 +537,15 @@ def _all_sparse_plan(h: int, dev) -> SplitPlan:
                      torch.empty(0, dtype=torch.int32, device=dev), pos)
 
 
-def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_ready=None) -> FfnGrads:
+def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_ready=None,
+                 grad_bucket: torch.Tensor | None = None) -> FfnGrads:
     """Backward matching the cached forward (ref ffn.py:366-451).
 
     grad_ready(name, tensor), if given, is called as soon as d_w2 and then
     d_w1 are final on the current stream (used by the data-parallel step to
-    launch their all-reduce while the rest of the backward runs)."""
+    launch their all-reduce while the rest of the backward runs).
+    grad_bucket: optional fp32 buffer of 2*d*h elements; d_w1 and d_w2 are then
+    written as views into it ([d_w1 | d_w2]), so one collective covers both."""
     if cache.config != cfg:
         raise StateError("cache was produced under a different configuration")
     _unsupported(cfg)
@@ -555,15 +567,14 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     if cfg.fp8_backward:
         from .fp8 import ffn_backward_f8
 
-        return ffn_backward_f8(g_out, cache, p, cfg, grad_ready)
+        return ffn_backward_f8(g_out, cache, p, cfg, grad_ready, grad_bucket)
     dev = g_out.device
     s = stream()
     npad = pad128(n)
     census: list[GemmEvent] = []
     notify = grad_ready or (lambda name, t: None)
 
-    d_w1 = torch.empty(d, h, dtype=F32, device=dev)
-    d_w2 = torch.empty(h, d, dtype=F32, device=dev)
+    d_w1, d_w2 = weight_grad_buffers(d, h, dev, grad_bucket)
     d_x = torch.empty(n, d, dtype=BF16, device=dev)
     stats_a = stats_g = None
 

@@ -433,10 +433,10 @@ def _split_grad_f8(fs, plan, b: torch.Tensor, npad: int, out: torch.Tensor, tran
             row_valid=valid, pair_rows=max(fs.pair_rows, 0))
 
 
-def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
+def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bucket=None):
     """ffn_backward under fp8_backward (ref ffn.py:366-451 with fp8b=True):
     every backward GEMM on e4m3 operands."""
-    from .ffn import FfnGrads, GemmEvent, _all_sparse_plan, _frame_rows
+    from .ffn import FfnGrads, GemmEvent, _all_sparse_plan, _frame_rows, weight_grad_buffers
     from .matcore import gemm_macs
     from .sparse24 import sp_gemm_macs, sparsify_feature_wise
     from .splitgemm import feature_split, split_gemm_macs
@@ -449,8 +449,7 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None):
     s = stream()
     census = []
     notify = grad_ready or (lambda name, t: None)
-    d_w1 = torch.empty(d, h, dtype=F32, device=dev)
-    d_w2 = torch.empty(h, d, dtype=F32, device=dev)
+    d_w1, d_w2 = weight_grad_buffers(d, h, dev, grad_bucket)
     d_x = torch.empty(n, d, dtype=BF16, device=dev)
     g_c = _frame_rows(g_out, npad, cache.inv_dev)
 

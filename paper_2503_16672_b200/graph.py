@@ -29,11 +29,16 @@ class FfnStepGraph:
     tensors every replay). backward=False captures the forward only (prefill).
     """
 
-    def __init__(self, params: FfnParams, cfg: FfnConfig, n: int, backward: bool = True, warmup: int = 2):
+    def __init__(self, params: FfnParams, cfg: FfnConfig, n: int, backward: bool = True, warmup: int = 2,
+                 grad_bucket: bool = False):
         require_cuda()
         d = params.model_dim
         dev = params.w1.device
         self.params, self.cfg, self.backward = params, cfg, backward
+        # grad_bucket=True: d_w1 and d_w2 live in one flat fp32 buffer
+        # (self.bucket), so the data-parallel step all-reduces them in one call
+        self.bucket = (torch.empty(2 * d * params.hidden_dim, dtype=torch.float32, device=dev)
+                       if grad_bucket and backward else None)
         self.x = torch.zeros(n, d, dtype=BF16, device=dev)
         self.dy = torch.zeros(n, d, dtype=BF16, device=dev)
         self.pool = torch.cuda.graph_pool_handle()
@@ -54,7 +59,7 @@ class FfnStepGraph:
 
     def _step(self):
         out, cache = ffn_forward(self.x, self.params, self.cfg, for_backward=self.backward)
-        grads = ffn_backward(self.dy, cache, self.params, self.cfg) if self.backward else None
+        grads = ffn_backward(self.dy, cache, self.params, self.cfg, grad_bucket=self.bucket) if self.backward else None
         return out, cache, grads
 
     @property

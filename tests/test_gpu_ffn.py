@@ -302,3 +302,34 @@ def test_k4_in_gemm_is_bitwise_identical(monkeypatch, n, d, h):
     assert torch.equal(o0, o1)
     for t in ("d_w1", "d_w2", "d_x"):
         assert torch.equal(getattr(g0, t), getattr(g1, t)), t
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_grad_bucket_views_are_bitwise_identical(fp8):
+    """ffn_backward(grad_bucket=...) writes dW1 / dW2 as views of one flat
+    buffer (one all-reduce for both in the data-parallel step), same bits;
+    FfnStepGraph(grad_bucket=True) exposes it as .bucket."""
+    from dataclasses import replace
+
+    n, d, h = 512, 256, 512
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=79)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    cfg = replace(s24.RECIPE, fp8_emulation=fp8, fp8_backward=fp8)
+    tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
+    out, cache = s24.ffn_forward(tx, p, cfg)
+    g0 = s24.ffn_backward(tg, cache, p, cfg)
+    bucket = torch.empty(2 * d * h, device="cuda")
+    out, cache = s24.ffn_forward(tx, p, cfg)
+    g1 = s24.ffn_backward(tg, cache, p, cfg, grad_bucket=bucket)
+    torch.cuda.synchronize()
+    assert torch.equal(g0.d_w1, g1.d_w1) and torch.equal(g0.d_w2, g1.d_w2)
+    assert g1.d_w1.data_ptr() == bucket.data_ptr() and torch.equal(bucket[d * h:].view(h, d), g1.d_w2)
+    step = s24.FfnStepGraph(p, cfg, n, grad_bucket=True)
+    step.x.copy_(tx.bfloat16())
+    step.dy.copy_(tg.bfloat16())
+    step.replay()
+    torch.cuda.synchronize()
+    assert step.d_w1.data_ptr() == step.bucket.data_ptr()
+    assert torch.equal(step.d_w1, g0.d_w1) and torch.equal(step.d_w2, g0.d_w2)
+    with pytest.raises(s24.DimensionError):
+        s24.ffn_backward(tg, s24.ffn_forward(tx, p, cfg)[1], p, cfg, grad_bucket=torch.empty(7, device="cuda"))
