@@ -132,3 +132,31 @@ def test_fp8_api_matches_reference():
         s24.e4m3_encode([1.0, float("nan")])
     with pytest.raises(s24.OrientationError):
         s24.fp8_gemm_rowwise(qb, qa)
+
+
+def test_fp8_shape_errors_and_module():
+    """fp8 needs model dim % 32 (e4m3 operand rows of 16 bytes, N tiles); the
+    nn.Module and the graph capture run the e4m3 configs like the bf16 ones."""
+    from dataclasses import replace
+
+    cfg = replace(s24.RECIPE, fp8_emulation=True, fp8_backward=True)
+    x = torch.randn(64, 40, device="cuda")
+    p = s24.FfnParams(w1=torch.randn(40, 128, device="cuda"), w2=torch.randn(128, 40, device="cuda"))
+    with pytest.raises(s24.DimensionError):
+        s24.ffn_forward(x, p, cfg)
+    torch.manual_seed(0)
+    layer = s24.SquaredReluFFN24(64, 256, cfg=cfg)
+    xin = torch.randn(2, 50, 64, device="cuda", requires_grad=True)  # 100 tokens: padded to a multiple of 4
+    y = layer(xin)
+    y.float().pow(2).mean().backward()
+    assert y.shape == xin.shape and xin.grad is not None and layer.w1.grad is not None
+    assert bool(torch.isfinite(layer.w1.grad).all()) and bool(torch.isfinite(xin.grad).all())
+    step = s24.FfnStepGraph(s24.FfnParams(w1=layer.w1.detach(), w2=layer.w2.detach()), cfg, 128)
+    xs = torch.randn(128, 64, device="cuda").bfloat16()
+    step.x.copy_(xs)
+    step.dy.copy_(xs)
+    step.replay()
+    out_e, cache = s24.ffn_forward(xs, s24.FfnParams(w1=layer.w1.detach(), w2=layer.w2.detach()), cfg)
+    g_e = s24.ffn_backward(xs, cache, s24.FfnParams(w1=layer.w1.detach(), w2=layer.w2.detach()), cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(step.out, out_e) and torch.equal(step.d_w1, g_e.d_w1) and torch.equal(step.d_x, g_e.d_x)
