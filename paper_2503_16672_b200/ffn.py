@@ -342,7 +342,10 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     census: list[GemmEvent] = []
 
     perm = perm_dev = inv_dev = None
-    permute = cfg.permute_tokens and sparse_fwd
+    # The token permutation only shapes the feature-wise groups of the
+    # backward; every forward stage maps one token row to one output row, so an
+    # inference forward (for_backward=False) skips it: same bits, no gathers.
+    permute = cfg.permute_tokens and sparse_fwd and for_backward
     if permute:
         perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
         perm = perm_dev

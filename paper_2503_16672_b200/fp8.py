@@ -303,7 +303,7 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     census = []
     sparse_fwd = cfg.forward_mode == "sparse24"
     perm_dev = inv_dev = None
-    if cfg.permute_tokens and sparse_fwd:
+    if cfg.permute_tokens and sparse_fwd and for_backward:  # (inference: see ffn.ffn_forward)
         perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
     out = torch.empty(n, d, dtype=BF16, device=dev)
     if not sparse_fwd:

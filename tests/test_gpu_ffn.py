@@ -333,3 +333,25 @@ def test_grad_bucket_views_are_bitwise_identical(fp8):
     assert torch.equal(step.d_w1, g0.d_w1) and torch.equal(step.d_w2, g0.d_w2)
     with pytest.raises(s24.DimensionError):
         s24.ffn_backward(tg, s24.ffn_forward(tx, p, cfg)[1], p, cfg, grad_bucket=torch.empty(7, device="cuda"))
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_inference_forward_skips_permutation_same_bits(fp8):
+    """for_backward=False runs the forward without the token permutation
+    (no gathers, no row map): the output is bit-identical to the training
+    forward's, and so are the counts, plan and drop statistics."""
+    from dataclasses import replace
+
+    n, d, h = 640, 256, 512
+    x, w1, w2, _ = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=80)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    cfg = replace(s24.RECIPE, fp8_emulation=fp8)
+    tx = torch.from_numpy(x).cuda()
+    o_train, c_train = s24.ffn_forward(tx, p, cfg)
+    o_inf, c_inf = s24.ffn_forward(tx, p, cfg, for_backward=False)
+    torch.cuda.synchronize()
+    assert torch.equal(o_train, o_inf)
+    assert torch.equal(c_train.counts, c_inf.counts)
+    assert c_train.stats.dropped == c_inf.stats.dropped
+    assert torch.equal(c_train.plan.sparse_features, c_inf.plan.sparse_features)
+    assert c_inf.perm is None and c_train.perm is not None
