@@ -143,7 +143,9 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
  * magnitude with NaN last. No drop statistics. */
 int s24_feature_split_x(const void* vals_a, const void* vals_b, const uint8_t* meta_hw, int64_t n, int64_t h,
                         const int* feat_pos, int64_t n_sparse, int64_t n_dense, void* vs_a, uint8_t* es_a, void* vs_b,
-                        uint8_t* es_b, int a_nonneg, void* stream);
+                        uint8_t* es_b, int a_nonneg, const int* row_map, void* stream);
+/* (row_map, nullable int32 [n]: token j of the split reads row row_map[j] of
+ * vals / meta_hw -- the split of a permuted token order without gathering) */
 
 /* K4 in the identity layout (coalesced in and out; the hot-path variant):
  * vs bf16 [pair_pad + h, n/2] + es hw metadata (rows pair_pad + h, K = n),

@@ -21,6 +21,7 @@ struct K4xArgs {
   int pair_rows;                 // 2 * n_dense: rows of the dense pairs in front
   __nv_bfloat16* vs[2];          // [pad128(pair_rows + n_sparse), n/2]
   uint8_t* es[2];                // hw metadata of vs
+  const int* row_map;            // nullable [n]: token j of the split is row row_map[j] of vals / meta
 };
 
 // per-feature output slot of one warp unit
@@ -77,11 +78,13 @@ __global__ void __launch_bounds__(256) k_feature_split_x(K4xArgs a) {
   uint32_t X[NOPS][4][8];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const uint32_t m16 = __ldg(reinterpret_cast<const uint16_t*>(a.meta + meta_hw_halfword_offset(t + r, fbase / 16, h)));
+    // (row_map: the split's token order is a permutation of the rows of vals)
+    const int src = a.row_map ? __ldg(a.row_map + t + r) : t + r;
+    const uint32_t m16 = __ldg(reinterpret_cast<const uint16_t*>(a.meta + meta_hw_halfword_offset(src, fbase / 16, h)));
     uint4 v[NOPS];
 #pragma unroll
     for (int o = 0; o < NOPS; ++o)
-      v[o] = __ldg(reinterpret_cast<const uint4*>(a.vals[o] + static_cast<long long>(t + r) * (h / 2) + fbase / 2));
+      v[o] = __ldg(reinterpret_cast<const uint4*>(a.vals[o] + static_cast<long long>(src) * (h / 2) + fbase / 2));
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const uint2 sl = lut[(m16 >> (4 * g)) & 0xFu];

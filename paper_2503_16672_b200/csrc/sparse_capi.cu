@@ -607,7 +607,7 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
 
 int s24_feature_split_x(const void* vals_a, const void* vals_b, const uint8_t* meta_hw, int64_t n, int64_t h,
                         const int* feat_pos, int64_t n_sparse, int64_t n_dense, void* vs_a, uint8_t* es_a, void* vs_b,
-                        uint8_t* es_b, int a_nonneg, void* stream) {
+                        uint8_t* es_b, int a_nonneg, const int* row_map, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   K4Args pa, pb;
   int rc = k4_prepare(vals_a, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs_a, es_a, nullptr, st, &pa, 2 * n_dense);
@@ -624,7 +624,8 @@ int s24_feature_split_x(const void* vals_a, const void* vals_b, const uint8_t* m
             feat_pos,
             static_cast<int>(2 * n_dense),
             {static_cast<__nv_bfloat16*>(vs_a), static_cast<__nv_bfloat16*>(vs_b)},
-            {es_a, es_b}};
+            {es_a, es_b},
+            row_map};
   dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
   if (two)
     (a_nonneg ? k_feature_split_x<2, true> : k_feature_split_x<2, false>)<<<grid, 256, 0, st>>>(a);

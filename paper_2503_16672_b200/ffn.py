@@ -106,6 +106,16 @@ DUAL_K4 = os.environ.get("S24_DUAL_K4", "0") == "1"
 # persistent GEMM's last partial wave is filled by the next one's CTAs ("1");
 # or dX next to K4(g_pre), then both weight gradients in one grouped launch ("0").
 WGRAD_OVERLAP = os.environ.get("S24_WGRAD_OVERLAP", "0") == "1"
+# Token-order storage ("1"): the recipe's activations stay in the caller's
+# token order -- K1 reads x and fwd.out writes out without row maps, K3 reads
+# dY and dX is written without one -- and the compute frame's permutation is
+# applied only where the backward needs it: inside K4 (row-mapped reads) and
+# in the permuted copies x_in / g_c that feed the weight-gradient GEMMs, both
+# on the side stream. "0": gather x / dY into the permuted frame before K1 / K3.
+# Measured slower on B200 (2.06 vs 1.99 ms at c2: row-mapped K4 reads scatter
+# over the whole activation, and the overlapped gathers slow K1 / K3 more than
+# the serialized ones cost), so opt-in.
+TOKEN_ORDER_STORAGE = os.environ.get("S24_TOKEN_ORDER", "0") == "1"
 
 
 def _dual_k4() -> bool:
@@ -244,6 +254,9 @@ class FfnCache:
     act_meta8: torch.Tensor | None = None  # act metadata in the e4m3 operand-E layout
     act_f32: torch.Tensor | None = None  # dense fp8 forward: the fp32 activation
     f8: dict | None = None  # e4m3 backward operands prepared next to the forward GEMMs (fp8.py)
+    # token-order storage (TOKEN_ORDER_STORAGE): act_vals / act_meta rows are in
+    # the caller's token order; compute-frame token j is storage row row_frame[j]
+    row_frame: torch.Tensor | None = None
 
     # Side-stream work of the forward reads and writes tensors allocated on
     # the main stream (no record_stream: its deferred frees stall the caching
@@ -260,10 +273,18 @@ class FfnCache:
 
     @property
     def act_sparse(self) -> Sparse24Matrix | None:
+        """The compressed activation in the compute frame (ref FfnCache.act_sparse)."""
         if self.act_vals is None:
             return None
         h = self.act_vals.shape[1] * 2
-        return Sparse24Matrix(self.n, h, TOKEN_WISE, self.act_vals, self.act_meta)
+        stored = Sparse24Matrix(self.n, h, TOKEN_WISE, self.act_vals, self.act_meta)
+        if self.row_frame is None:
+            return stored
+        # token-order storage: gather the rows into the compute frame (API view only)
+        from .splitgemm import frame_rows_compressed
+
+        data, hw = frame_rows_compressed(self.act_vals, self.act_meta, self.row_frame, self.n, h)
+        return Sparse24Matrix(self.n, h, TOKEN_WISE, data, hw)
 
     @property
     def fwd_mask(self) -> torch.Tensor | None:
@@ -383,7 +404,16 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     # (inference prefill, for_backward=False, needs no x_in at all)
     x_in = _frame_rows(x, npad, inv_dev if permute else None, defer=True) if for_backward else None
     k1_in, k1_map = x, (perm_dev if permute else None)
-    if (act_fw is not None or not ROWMAP_GEMMS) and permute:
+    row_frame = None
+    if (TOKEN_ORDER_STORAGE and permute and side is not None and cfg.mask_grad_with_fwd and act_fw is None
+            and cfg.backward_mode in ("split_masked", "naive_sparse") and _layout()["paired"]
+            and not _layout()["identity"] and not _dual_k4() and not ACT_SPLIT_IN_BWD):
+        # token-order storage: K1 on x as is; the permutation is applied by K4
+        # and by the side-stream gathers (see TOKEN_ORDER_STORAGE)
+        row_frame = inv_dev if npad == n else torch.cat(
+            [inv_dev, torch.arange(n, npad, dtype=inv_dev.dtype, device=dev)])
+        k1_map = None
+    elif (act_fw is not None or not ROWMAP_GEMMS) and permute:
         if x_in is None:
             x_in = _frame_rows(x, npad, inv_dev, defer=True)
         _fill_frame_rows(x_in, x, inv_dev)
@@ -407,7 +437,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
 
     def fwd_out(st):
         _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-                  ptr(inv_dev), 0, -1, None, 0, st)
+                  ptr(inv_dev if row_frame is None else None), 0, -1, None, 0, st)
 
     if side is not None:
         main = torch.cuda.current_stream()
@@ -417,12 +447,12 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             plan_out = partition_features(counts, cfg.split_ratio, launch_stream=side)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, **_layout())
+            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, row_map=row_frame, **_layout())
         with torch.cuda.stream(side):
             if SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
                 _fill_frame_rows(x_in, x, inv_dev)
-            if want_split:
-                run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True)  # relu^2: >= 0
+            if want_split:  # (relu^2: >= 0)
+                run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True, row_map=row_frame)
             ev = torch.cuda.Event()
             ev.record(side)
         split_ready = x_in_ready = ev
@@ -451,9 +481,11 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
             if want_split:
                 run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True)
     census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
+    if row_frame is not None and pre is not None:
+        pre = pre[row_frame[:n].long()]  # (debug / parity view: the compute frame)
     cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
                      SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw, act_split=act_split,
-                     act_split_ready=split_ready, x_in_ready=x_in_ready)
+                     act_split_ready=split_ready, x_in_ready=x_in_ready, row_frame=row_frame)
     return out, cache
 
 
@@ -508,6 +540,11 @@ def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
     """The feature-wise split of the cached activation (made by the forward
     next to fwd.out when K4 runs on the side stream, else here)."""
     if cache.act_split is None:
+        if cache.row_frame is not None:
+            fs = alloc_feature_split(cache.act_vals, cache.act_meta, npad, h, plan, paired=True,
+                                     row_map=cache.row_frame)
+            run_feature_split(fs, cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, row_map=cache.row_frame)
+            return fs
         return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, **_layout())
     if cache.act_split_ready is not None:
         torch.cuda.current_stream().wait_event(cache.act_split_ready)
@@ -617,8 +654,11 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     g_c = _frame_rows(g_out, npad, cache.inv_dev, defer=True)
     g_ready = None
     rowmap = ROWMAP_GEMMS and g_fw is None
+    stored = cache.row_frame is not None  # token-order storage: K3 / dX need no frame rows
+    if stored and (side is None or g_fw is not None or not cfg.mask_grad_with_fwd):
+        raise StateError("token-order storage needs the side-stream backward with mask_grad_with_fwd")
     if g_c is not g_out:
-        if not rowmap and cache.perm_dev is not None:
+        if not rowmap and cache.perm_dev is not None and not stored:
             _fill_frame_rows(g_c, g_out, cache.inv_dev)  # K3 reads g_c
         elif side is not None and SIDE_GATHERS:
             side.wait_stream(main)
@@ -658,7 +698,9 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     # K3 reads dY unpermuted and pairs input row r with act / g_pre row
     # perm[r]; the fused feature-wise epilogue needs the permuted rows
     k3_in, k3_map = g_out, cache.perm_dev
-    if not rowmap and cache.perm_dev is not None:
+    if stored:
+        k3_in, k3_map = g_out, None  # dY rows pair with the stored act rows as they are
+    elif not rowmap and cache.perm_dev is not None:
         need_frame_inputs()
         k3_in, k3_map = g_c, None
     # (fp8 forward: relu(y1) comes from the unquantized activation)
@@ -688,11 +730,11 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         ev_k3 = torch.cuda.Event()
         ev_k3.record(main)
         fa = _act_split(cache, npad, h, plan)
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame, **_layout())
         need_frame_inputs()
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
+            run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame)
         split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
         with torch.cuda.stream(side):
             split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
@@ -702,7 +744,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
         third.wait_event(ev_k3)
         with torch.cuda.stream(third):
             _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16,
-                      d, ptr(cache.inv_dev), 0, -1, None, 0, third.cuda_stream)
+                      d, ptr(None if stored else cache.inv_dev), 0, -1, None, 0, third.cuda_stream)
             ev_x = torch.cuda.Event()
             ev_x.record(third)
         main.wait_event(ev_w1)
@@ -714,7 +756,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     if cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None and not raw_naive:
         # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
         # as background work in its idle epilogue warps
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame, **_layout())
         if K4_MODE == "gemm" and fg.pair_rows >= 0 and not fg.identity:
             # dX whose CTAs also split their g_pre stages feature-wise
             _lib.call("s24_spmm_fs", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16,
@@ -733,11 +775,12 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
                 if dual:  # act (>= 0) and g_pre share the keep pattern: one pass for both
                     run_feature_split_dual(fa, fg, cache.act_vals, g_vals, cache.act_meta, npad, h, plan)
                 else:
-                    run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
+                    run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame)
 
             fg_ready = _spmm_with_split(
                 lambda st: _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h,
-                                     ptr(d_x), _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None, 0, st),
+                                     ptr(d_x), _lib.BF16, d, ptr(None if stored else cache.inv_dev), 0, -1, None,
+                                     0, st),
                 k4_side)
             if dual:
                 cache.act_split, cache.act_split_ready = fa, fg_ready

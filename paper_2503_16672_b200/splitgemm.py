@@ -176,15 +176,35 @@ def feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, pla
     return fs
 
 
+def frame_rows_compressed(vals: torch.Tensor, meta_hw: torch.Tensor, row_map: torch.Tensor, n: int, h: int):
+    """Token-wise compressed [n, h] (vals + hw metadata) with its rows
+    gathered: row j of the result is row row_map[j] (for statistics and API
+    views of token-order storage; not on the hot path)."""
+    from .sparse24 import TOKEN_WISE, Sparse24Matrix
+
+    rows = row_map[:n].long()
+    ref = Sparse24Matrix(n, h, TOKEN_WISE, vals, meta_hw).meta[rows].contiguous()
+    v = torch.zeros_like(vals)
+    v[:n] = vals[rows]
+    hw = torch.full_like(meta_hw, 0x44)
+    _lib.call("s24_meta_ref_to_hw", ptr(ref), n, h, ptr(hw), stream())
+    return v, hw
+
+
 def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
-                        dense_only: bool = False, paired: bool = False, identity: bool = False) -> FeatureSplit:
+                        dense_only: bool = False, paired: bool = False, identity: bool = False,
+                        row_map: torch.Tensor | None = None) -> FeatureSplit:
     """Output buffers of one K4 job (filled by s24_feature_split or by a GEMM's
     background warps via s24_spmm_bg). Its drop statistics are not counted on
     the hot path -- the reference discards them (splitgemm.py:75) -- and are
     recounted on the device only if someone reads them."""
     dev = vals.device
     ns, nd = plan.n_sparse, plan.n_dense
-    stats = SparsifyStats(n * ns, lambda: feature_split(vals, meta_hw, n, h, plan, with_stats=True).stats._dev)
+    def recount():
+        v, m = (vals, meta_hw) if row_map is None else frame_rows_compressed(vals, meta_hw, row_map, n, h)
+        return feature_split(v, m, n, h, plan, with_stats=True).stats._dev
+
+    stats = SparsifyStats(n * ns, recount)
     if identity and not dense_only:
         rows = pad128(2 * nd) + h
         vs = torch.empty(rows, n // 2, dtype=BF16, device=dev)
@@ -202,15 +222,19 @@ def alloc_feature_split(vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: in
 
 
 def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tensor, n: int, h: int,
-                      plan: SplitPlan, nonneg: bool = False) -> None:
-    """Fill preallocated K4 outputs on the current stream (no drop counting)."""
+                      plan: SplitPlan, nonneg: bool = False, row_map: torch.Tensor | None = None) -> None:
+    """Fill preallocated K4 outputs on the current stream (no drop counting).
+    row_map (paired layout only): token j of the split is row row_map[j] of
+    vals / meta_hw (the compute frame's permutation, applied while reading)."""
+    if row_map is not None and (fs.identity or fs.pair_rows < 0):
+        raise DimensionError("a row-mapped feature split needs the paired rank layout")
     for _ in range(K4_REPEAT):
         if fs.identity:
             _lib.call("s24_feature_split_id", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_dense,
                       ptr(fs.vs), ptr(fs.es), None, int(nonneg), stream())
         elif fs.pair_rows >= 0:
             _lib.call("s24_feature_split_x", ptr(vals), None, ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse,
-                      plan.n_dense, ptr(fs.vs), ptr(fs.es), None, None, int(nonneg), stream())
+                      plan.n_dense, ptr(fs.vs), ptr(fs.es), None, None, int(nonneg), ptr(row_map), stream())
         else:
             _lib.call("s24_feature_split", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse,
                       plan.n_dense, ptr(fs.vs), ptr(fs.es), ptr(fs.vd), None, int(nonneg), fs.pair_rows, stream())
@@ -220,14 +244,15 @@ K4_REPEAT = 1  # experiments only (scripts/ab_step.py): marginal cost of K4 in t
 
 
 def run_feature_split_dual(fa: FeatureSplit, fb: FeatureSplit, vals_a: torch.Tensor, vals_b: torch.Tensor,
-                           meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan) -> None:
+                           meta_hw: torch.Tensor, n: int, h: int, plan: SplitPlan,
+                           row_map: torch.Tensor | None = None) -> None:
     """K4 for two operands on one keep pattern (the activation, >= 0, and
     g_pre) in one pass: paired rank layout for both."""
     if not (fa.pair_rows >= 0 and fb.pair_rows >= 0 and not fa.identity and not fb.identity):
         raise DimensionError("the dual feature split writes the paired rank layout")
     for _ in range(K4_REPEAT):
         _lib.call("s24_feature_split_x", ptr(vals_a), ptr(vals_b), ptr(meta_hw), n, h, ptr(plan.feat_pos),
-                  plan.n_sparse, plan.n_dense, ptr(fa.vs), ptr(fa.es), ptr(fb.vs), ptr(fb.es), 1, stream())
+                  plan.n_sparse, plan.n_dense, ptr(fa.vs), ptr(fa.es), ptr(fb.vs), ptr(fb.es), 1, ptr(row_map), stream())
 
 
 def side_stream(device) -> torch.cuda.Stream:

@@ -36,6 +36,7 @@ VARIANTS = {
     "act_split_bwd_k4none_graph": {"ACT_SPLIT_IN_BWD": True, "_graph": True, "_k4_repeat": 0},
     "wgrad_overlap_graph": {"WGRAD_OVERLAP": True, "_graph": True},
     "k4_gemm_graph": {"K4_MODE": "gemm", "_graph": True},
+    "frame_gather_graph": {"TOKEN_ORDER_STORAGE": False, "_graph": True},
 }
 
 

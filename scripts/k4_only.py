@@ -29,7 +29,7 @@ vsx = torch.zeros((2 * nd + ks + 127) // 128 * 128 + 1, n // 2, device="cuda", d
 esx = torch.zeros(_lib.meta_hw_bytes((2 * nd + ks + 127) // 128 * 128 + 128, n), device="cuda", dtype=torch.uint8)
 for _ in range(5):
     if "x" in sys.argv[3:]:  # the hot-path K4x (paired rank layout)
-        _lib.call("s24_feature_split_x", P(vals), None, P(meta), n, h, P(pos), ks, nd, P(vsx), P(esx), None, None, 1, S)
+        _lib.call("s24_feature_split_x", P(vals), None, P(meta), n, h, P(pos), ks, nd, P(vsx), P(esx), None, None, 1, None, S)
     else:
         _lib.call("s24_feature_split", P(vals), P(meta), n, h, P(pos), ks, nd, P(vs), P(es), P(vd), None, 1, -1, S)
 torch.cuda.synchronize()

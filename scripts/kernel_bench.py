@@ -128,7 +128,7 @@ def main():
                       dtype=torch.uint8)
     k4x_bytes = n * h * 1.125 + (2 * nd + kcount) * n * 0.5625
     rec("K4x paired (hot path)", timeit(lambda: _lib.call("s24_feature_split_x", P(act_vals), None, P(meta), n, h,
-                                                             P(pos), kcount, nd, P(vsx), P(esx), None, None, 1, S()),
+                                                             P(pos), kcount, nd, P(vsx), P(esx), None, None, 1, None, S()),
                                          args.iters, flush), 1e-9, bytes_=k4x_bytes)
     pad = (2 * nd + 127) // 128 * 128
     vsi = torch.empty(pad + h, n // 2, device="cuda", dtype=bf)

@@ -355,3 +355,36 @@ def test_inference_forward_skips_permutation_same_bits(fp8):
     assert c_train.stats.dropped == c_inf.stats.dropped
     assert torch.equal(c_train.plan.sparse_features, c_inf.plan.sparse_features)
     assert c_inf.perm is None and c_train.perm is not None
+
+
+@pytest.mark.parametrize("n,d,h,mode", [(1024, 256, 1024, "split_masked"), (600, 512, 512, "split_masked"),
+                                         (512, 256, 512, "naive_sparse")])
+def test_token_order_storage_is_bitwise_identical(monkeypatch, n, d, h, mode):
+    """TOKEN_ORDER_STORAGE (activations kept in the caller's token order, the
+    permutation applied inside K4 and by the side-stream gathers) gives the
+    same bits as gathering into the permuted frame first, and the cache's
+    compute-frame views (act_sparse, fwd_mask, pre_act) are unchanged."""
+    from dataclasses import replace
+
+    from paper_2503_16672_b200 import ffn as F
+
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=81)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    cfg = replace(s24.RECIPE, backward_mode=mode)
+    tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
+    runs = []
+    for flag in (False, True):
+        monkeypatch.setattr(F, "TOKEN_ORDER_STORAGE", flag)
+        out, cache = s24.ffn_forward(tx, p, cfg, keep_pre_act=True)
+        views = (cache.act_sparse.values.clone(), cache.act_sparse.meta.clone(), cache.fwd_mask.clone(),
+                 cache.pre_act.clone())
+        g = s24.ffn_backward(tg, cache, p, cfg)
+        torch.cuda.synchronize()
+        assert (cache.row_frame is not None) == flag
+        runs.append((out, g, views))
+    (o0, g0, v0), (o1, g1, v1) = runs
+    assert torch.equal(o0, o1)
+    for t in ("d_w1", "d_w2", "d_x"):
+        assert torch.equal(getattr(g0, t), getattr(g1, t)), t
+    for a, b in zip(v0, v1):
+        assert torch.equal(a, b)

@@ -470,13 +470,13 @@ def test_feature_split_x_matches_reference_kernel(dual):
     vb, eb = bufs()
     if dual:
         _lib.call("s24_feature_split_x", P(vals), P(gvals), P(meta_hw), n, h, P(tpos), ks, nd, P(va), P(ea), P(vb),
-                  P(eb), 1, S())
+                  P(eb), 1, None, S())
         got = [(va, ea), (vb, eb)]
     else:
         _lib.call("s24_feature_split_x", P(vals), None, P(meta_hw), n, h, P(tpos), ks, nd, P(va), P(ea), None, None,
-                  1, S())
+                  1, None, S())
         _lib.call("s24_feature_split_x", P(gvals), None, P(meta_hw), n, h, P(tpos), ks, nd, P(vb), P(eb), None, None,
-                  0, S())
+                  0, None, S())
         got = [(va, ea), (vb, eb)]
     for (rv, re_), (gv_, ge) in zip(ref, got):
         assert torch.equal(rv, gv_) and torch.equal(re_, ge)
@@ -521,7 +521,7 @@ def test_spmm_fs_equals_spmm_plus_feature_split(M, N, K, b_mn):
                 _lib.call("s24_spmm", P(vp), P(mp), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0, -1,
                           None, 0, S())
                 _lib.call("s24_feature_split_x", P(vp), None, P(mp), npad, K, P(tpos), ks, nd, P(vs), P(es), None,
-                          None, nonneg, S())
+                          None, nonneg, None, S())
             torch.cuda.synchronize()
             outs.append((D, vs, es))
         (d0, v0, e0), (d1, v1, e1) = outs
