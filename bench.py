@@ -25,9 +25,7 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 from dataclasses import replace
 from pathlib import Path

@@ -1,7 +1,6 @@
 """The C-ABI library loads without a GPU and exports every entry point that
 include/s24.h declares (no compute calls here)."""
 
-import ctypes
 import re
 from pathlib import Path
 

@@ -5,7 +5,6 @@ gloo, plus prefill's no-communication sharding contract."""
 import os
 import socket
 
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
