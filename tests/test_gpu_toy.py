@@ -72,3 +72,13 @@ def test_harness_metrics_checkpoint_and_divergence(tmp_path):
     assert ei.value.step == 3
     with pytest.raises(s24.ConfigError):
         toy.ablate(corpus(), mc, tc, rows=["dense-swiglu"])
+
+
+def test_init_activation_sparsity_is_about_half():
+    """ref tests/test_acceptance.py:107-122 (c03): at initialisation about half
+    of the squared-ReLU activations are zero, per layer."""
+    mc = toy.ToyModelConfig(embed_dim=64, hidden=256, num_blocks=2, context=8)
+    train_split, _ = toy.build_dataset(corpus(), mc.context, 0.9)
+    model = toy.ToyModel(mc)
+    sp = toy.measure_activation_sparsity(model, train_split.contexts[:2048])
+    assert len(sp) == 2 and all(abs(s - 0.5) <= 0.05 for s in sp), sp
