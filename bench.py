@@ -544,28 +544,65 @@ def run_ours(args):
         dw1h = torch.empty(d, h, dtype=torch.float32, **pin)
         dw2h = torch.empty(h, d, dtype=torch.float32, **pin)
 
-        def e2e_step():
-            g = graph_step(recipe, xh, gh)  # pinned host -> the graph's input buffers, replay
-            oh.copy_(g.out, non_blocking=True)
-            if prefill:
-                return
-            dxh.copy_(g.d_x, non_blocking=True)
-            dw1h.copy_(g.d_w1, non_blocking=True)
-            dw2h.copy_(g.d_w2, non_blocking=True)
+        # Two captured instances of the step alternate (double buffering), so
+        # the H2D of step i+1 (copy stream) and the D2H of step i (a second
+        # copy stream) run while step i computes: a standard input / output
+        # pipeline. Every step's own copies are inside the timed region.
+        g_a = graph_step(recipe)
+        g_b = s24.FfnStepGraph(params, recipe, n, backward=not prefill, grad_bucket=world > 1)
+        gs = (g_a, g_b)
+        comp = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        outs_of = (lambda g: (g.out,)) if prefill else (lambda g: (g.out, g.d_x, g.d_w1, g.d_w2))
+        hosts = (oh,) if prefill else (oh, dxh, dw1h, dw2h)
 
-        for _ in range(2):
-            e2e_step()
+        def e2e_run(k: int):
+            """k pipelined steps; returns (start, end) events on the compute stream."""
+            ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+            ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
+            ev_out = [torch.cuda.Event(), torch.cuda.Event()]
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st.record(comp)
+            s_in.wait_event(st)
+            with torch.cuda.stream(s_in):
+                g_a.x.copy_(xh, non_blocking=True)
+                if not prefill:
+                    g_a.dy.copy_(gh, non_blocking=True)
+                ev_in[0].record(s_in)
+            for i in range(k):
+                j = i % 2
+                g = gs[j]
+                comp.wait_event(ev_in[j])
+                if i >= 2:
+                    comp.wait_event(ev_out[j])  # step i-2's outputs of this instance were read
+                flush.zero_()
+                g.replay()
+                if world > 1 and not prefill:
+                    dist.all_reduce(g.bucket)
+                ev_comp[j].record(comp)
+                if i + 1 < k:
+                    nxt = gs[1 - j]
+                    if i >= 1:
+                        s_in.wait_event(ev_comp[1 - j])  # step i-1 finished reading its inputs
+                    with torch.cuda.stream(s_in):
+                        nxt.x.copy_(xh, non_blocking=True)
+                        if not prefill:
+                            nxt.dy.copy_(gh, non_blocking=True)
+                        ev_in[1 - j].record(s_in)
+                s_out.wait_event(ev_comp[j])
+                with torch.cuda.stream(s_out):
+                    for hb, dv in zip(hosts, outs_of(g)):
+                        hb.copy_(dv, non_blocking=True)
+                    ev_out[j].record(s_out)
+            comp.wait_stream(s_out)
+            en.record(comp)
+            return st, en
+
+        e2e_run(3)
         barrier()
-        evs = []
-        for _ in range(args.steps):
-            flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            e2e_step()
-            e.record()
-            evs.append((s, e))
+        st, en = e2e_run(args.steps)
         barrier()
-        t_e2e = max_over_ranks(sum(s.elapsed_time(e) for s, e in evs))
+        t_e2e = max_over_ranks(st.elapsed_time(en))
         result["e2e"] = {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s",
                          "h2d_bytes_per_step": (1 if prefill else 2) * n * d * 2,
                          "d2h_bytes_per_step": n * d * 2 if prefill else 2 * n * d * 2 + 2 * d * h * 4,
@@ -573,7 +610,9 @@ def run_ours(args):
                          "path": ("s24.FfnStepGraph(backward=False) (public API: ffn_forward captured) with pinned "
                                   "host x copied in and out copied out every step" if prefill else
                                   "s24.FfnStepGraph (public API: ffn_forward + ffn_backward captured) with pinned "
-                                  "host x, dY copied in and out, dX, dW1, dW2 copied out every step")}
+                                  "host x, dY copied in and out, dX, dW1, dW2 copied out every step")
+                                 + "; two graph instances alternate so the H2D of step i+1 and the D2H of step i "
+                                   "overlap step i's compute (copy streams); L2 flushed before every step"}
 
     # CPU baseline: the oracle port on this host, rank 0, N=1 only
     if rank == 0 and world == 1 and not args.no_cpu:
