@@ -453,6 +453,8 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
                 _fill_frame_rows(x_in, x, inv_dev)
             if want_split:  # (relu^2: >= 0)
                 run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True, row_map=row_frame)
+                if act_split.pair_rows >= 0 and not act_split.identity:
+                    bg_plan.paired_row_map  # (the weight-gradient row map, built here off the main stream)
             ev = torch.cuda.Event()
             ev.record(side)
         split_ready = x_in_ready = ev
