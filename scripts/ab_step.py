@@ -23,6 +23,7 @@ VARIANTS = {
     "default": {},
     "unpaired": {"PAIRED_WEIGHT_GRADS": False},
     "k4_inline": {"K4_MODE": "inline"},
+    "k4_inline_graph": {"K4_MODE": "inline", "_graph": True},
     "main_gathers": {"SIDE_GATHERS": False},
     "rowmap": {"ROWMAP_GEMMS": True},
     "graph": {"_graph": True},
