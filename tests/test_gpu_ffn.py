@@ -388,3 +388,37 @@ def test_token_order_storage_is_bitwise_identical(monkeypatch, n, d, h, mode):
         assert torch.equal(getattr(g0, t), getattr(g1, t)), t
     for a, b in zip(v0, v1):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_minimum_and_degenerate_shapes(fp8):
+    """n = 4 tokens (one 2:4 group per feature column), h = 128 and d = 32,
+    the smallest dims the path takes, and an all-zero input (every group padded with
+    zeros, all counts 0, the plan is the first ceil(0.95 h) features by
+    index), against the oracle."""
+    from dataclasses import replace
+
+    d = 32
+    cfg = replace(s24.RECIPE, fp8_emulation=fp8, fp8_backward=fp8)
+    ocfg = dict(O.RECIPE, fp8_emulation=fp8, fp8_backward=fp8)
+    for n, zero in ((4, False), (8, True)):
+        x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, 128, sparsity=0.6, seed=n)
+        if zero:
+            x = np.zeros_like(x)
+        p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+        out, cache = s24.ffn_forward(torch.from_numpy(x).cuda(), p, cfg)
+        g = s24.ffn_backward(torch.from_numpy(dy).cuda(), cache, p, cfg)
+        torch.cuda.synchronize()
+        o_out, o_cache = O.ffn_forward(x, w1, w2, ocfg, ordered=False)
+        o_g = O.ffn_backward(dy, o_cache, w1, w2, ocfg, ordered=False)
+        assert np.array_equal(cache.fwd_mask.cpu().numpy(), o_cache["mask"])
+        assert np.array_equal(cache.plan.sparse_features.cpu().numpy(), o_cache["plan"][0])
+        if zero:
+            assert not out.float().any() and not g.d_w1.any() and not g.d_w2.any()
+            assert cache.stats.nonzeros_before == 0 and cache.stats.dropped == 0
+            continue
+        tol = 3e-2 if fp8 else 1e-2
+        for got, want in ((out.float(), o_out), (g.d_x.float(), o_g["d_x"]), (g.d_w1, o_g["d_w1"]),
+                          (g.d_w2, o_g["d_w2"])):
+            got = got.cpu().numpy().astype(np.float64)
+            assert np.linalg.norm(got - want) <= tol * max(np.linalg.norm(want), 1e-30)
