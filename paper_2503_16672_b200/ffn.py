@@ -51,7 +51,9 @@ from .splitgemm import (
     SplitPlan,
     feature_split,
     fused_weight_grad,
+    pad_plan,
     partition_features,
+    partition_features_padded,
     split_gemm_macs,
     split_weight_grad,
     split_weight_grad_pair,
@@ -257,6 +259,14 @@ class FfnCache:
     # token-order storage (TOKEN_ORDER_STORAGE): act_vals / act_meta rows are in
     # the caller's token order; compute-frame token j is storage row row_frame[j]
     row_frame: torch.Tensor | None = None
+    # padded FFN (model dim % 32 or hidden width % 128 != 0, see ffn_forward):
+    # this cache is the caller's view of d_valid x h_valid features; `core` is
+    # the device cache of the zero-padded FFN the backward runs on. On a core
+    # cache, plan_valid is the plan of the real features (plan: the padded one).
+    core: "FfnCache | None" = None
+    d_valid: int | None = None
+    h_valid: int | None = None
+    plan_valid: SplitPlan | None = None
 
     # Side-stream work of the forward reads and writes tensors allocated on
     # the main stream (no record_stream: its deferred frees stall the caching
@@ -277,6 +287,12 @@ class FfnCache:
         if self.act_vals is None:
             return None
         h = self.act_vals.shape[1] * 2
+        if self.core is not None and self.h_valid != h:
+            # padded hidden width: the first h_valid features (whole groups of 4)
+            full = self.core.act_sparse
+            hv = self.h_valid
+            return Sparse24Matrix(self.n, hv, TOKEN_WISE, full.data[:, : hv // 2].contiguous(), None,
+                                  meta_ref_cache=full.meta[:, : hv // 4].contiguous())
         stored = Sparse24Matrix(self.n, h, TOKEN_WISE, self.act_vals, self.act_meta)
         if self.row_frame is None:
             return stored
@@ -331,12 +347,95 @@ def _check_dims(n: int, d: int, h: int) -> None:
         raise DimensionError(f"hidden width {h} must be a multiple of 128 on the device path")
 
 
+def _pad_to(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+def _pad_cols(a: torch.Tensor, cols: int) -> torch.Tensor:
+    if a.shape[1] == cols:
+        return a
+    out = torch.zeros(a.shape[0], cols, dtype=a.dtype, device=a.device)
+    out[:, : a.shape[1]] = a
+    return out
+
+
+def _pad_params(p: FfnParams, dp: int, hp: int) -> FfnParams:
+    d, h = p.model_dim, p.hidden_dim
+    w1 = torch.zeros(dp, hp, dtype=BF16, device=p.w1.device)
+    w1[:d, :h] = p.w1
+    w2 = torch.zeros(hp, dp, dtype=BF16, device=p.w2.device)
+    w2[:h, :d] = p.w2
+    w3 = None
+    if p.w3 is not None:
+        w3 = torch.zeros(dp, hp, dtype=BF16, device=p.w3.device)
+        w3[:d, :h] = p.w3
+    return FfnParams(w1, w2, w3, p.beta)
+
+
+def _plan_split(counts, ratio: float, plan: SplitPlan | None, h: int, h_valid: int | None, launch_stream=None):
+    """(plan of the real features, device plan of all h features): computed
+    from K1's counts (plan None) or the caller's plan, padded when h_valid < h."""
+    if plan is None:
+        if h_valid is None:
+            pl = partition_features(counts, ratio, launch_stream=launch_stream)
+            return pl, pl
+        return partition_features_padded(counts, ratio, h_valid, launch_stream)
+    return plan, pad_plan(plan, h, launch_stream)
+
+
 def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, keep_pre_act: bool = False,
                 for_backward: bool = True):
     """Run the forward pass; returns (out [n, d] bf16, FfnCache) (ref ffn.py:276-363).
     keep_pre_act=True also stores the fp32 pre-activation in the cache (parity
     tests use it to replay the selection on identical inputs). for_backward=False
-    (inference prefill) skips the feature-wise split the backward would need."""
+    (inference prefill) skips the feature-wise split the backward would need.
+
+    Any d and h % 4 == 0 (the reference's shapes): the device GEMMs tile the
+    model dim by 32 and the hidden width by 128, so other sizes run on the FFN
+    zero-padded to those multiples. Padding features have zero pre-activation
+    (no kept values, count 0) and are appended to the plan's sparse list after
+    the real ones, so the real features' selection, plan, statistics, outputs
+    and gradients are those of the unpadded FFN."""
+    require_cuda()
+    _unsupported(cfg)
+    x = as_matrix(x, "x", BF16)
+    d, h = p.model_dim, p.hidden_dim
+    dp, hp = _pad_to(d, 32), _pad_to(h, 128)
+    if (dp, hp) == (d, h):
+        return _ffn_forward(x, p, cfg, plan, keep_pre_act, for_backward)
+    if x.shape[1] != d:
+        raise DimensionError(f"input width {x.shape[1]} does not match w1 {tuple(p.w1.shape)}")
+    if plan is not None and plan.hidden_dim != h:
+        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+    out, core = _ffn_forward(_pad_cols(x, dp), _pad_params(p, dp, hp), cfg, plan, keep_pre_act, for_backward,
+                             h_valid=h)
+    n = core.n
+    view = replace(core, pre_act=core.pre_act[:, :h] if core.pre_act is not None else None,
+                   counts=core.counts[:h] if core.counts is not None else None,
+                   plan=core.plan_valid if core.plan_valid is not None else core.plan,
+                   stats=SparsifyStats(n * h, core.stats._dev) if core.stats is not None else None,
+                   census=_census_real(core.census, n, d, h, core.plan_valid, cfg),
+                   act_split_ready=None, x_in_ready=None, core=core, d_valid=d, h_valid=h, plan_valid=None)
+    return (out[:, :d].contiguous() if dp != d else out), view
+
+
+def _census_real(events, n: int, d: int, h: int, plan: SplitPlan | None, cfg: FfnConfig) -> list:
+    """The GEMM census of a padded run restated at the real (n, d, h)."""
+    out = []
+    for ev in events:
+        if ev.name in ("bwd.d_w2", "bwd.d_w1") and ev.sparse:
+            m = split_gemm_macs(n, d, plan) if (cfg.backward_mode == "split_masked" and plan is not None) \
+                else sp_gemm_macs(n, h, d)
+        else:
+            m = sp_gemm_macs(n, h, d) if ev.sparse else gemm_macs(n, d, h)
+        out.append(GemmEvent(ev.name, ev.sparse, m))
+    return out
+
+
+def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_pre_act: bool, for_backward: bool,
+                 h_valid: int | None = None):
+    """ffn_forward on device-tileable sizes (d % 32 == 0, h % 128 == 0).
+    h_valid: the FFN is zero-padded beyond its first h_valid features."""
     require_cuda()
     _unsupported(cfg)
     x = as_matrix(x, "x", BF16)
@@ -354,7 +453,7 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         # e4m3 operands on the kind::f8f6f4 tensor cores (fp8.py)
         from .fp8 import ffn_forward_f8
 
-        return ffn_forward_f8(x, p, cfg, plan, keep_pre_act, for_backward)
+        return ffn_forward_f8(x, p, cfg, plan, keep_pre_act, for_backward, h_valid=h_valid)
     dev = x.device
     s = stream()
     npad = pad128(n)
@@ -419,9 +518,10 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     _lib.call("s24_fwd_gemm1_fused", ptr(k1_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta),
               ptr(counts), ptr(stats_dev), ptr(pre), *fw_args, ptr(k1_map), s)
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
-    if plan is not None and plan.hidden_dim != h:
-        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+    if plan is not None and plan.hidden_dim != (h_valid or h):
+        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h_valid or h}")
     need_plan = cfg.backward_mode == "split_masked"
+    plan_api = plan
 
     # fwd.out on tensor cores (inverse permutation as its epilogue row map).
     # Next to it, on a side stream: the split plan (K7), x_in, and -- when the
@@ -441,8 +541,8 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         main = torch.cuda.current_stream()
         side.wait_stream(main)  # K1's outputs are ready; the side work must not wait for fwd.out
         fwd_out(s)
-        if need_plan and plan_out is None:
-            plan_out = partition_features(counts, cfg.split_ratio, launch_stream=side)
+        if need_plan or plan is not None:
+            plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid, side)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
         if want_split:
             act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, row_map=row_frame, **_layout())
@@ -459,8 +559,8 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         if not SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
             _fill_frame_rows(x_in, x, inv_dev)
     else:
-        if need_plan and plan_out is None:
-            plan_out = partition_features(counts, cfg.split_ratio)
+        if need_plan or plan is not None:
+            plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid)
         if x_in is not None and x_in is not x and k1_in is not x_in:
             _fill_frame_rows(x_in, x, inv_dev)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
@@ -485,7 +585,8 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
         pre = pre[row_frame[:n].long()]  # (debug / parity view: the compute frame)
     cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
                      SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw, act_split=act_split,
-                     act_split_ready=split_ready, x_in_ready=x_in_ready, row_frame=row_frame)
+                     act_split_ready=split_ready, x_in_ready=x_in_ready, row_frame=row_frame,
+                     plan_valid=plan_api if h_valid is not None else None)
     return out, cache
 
 
@@ -585,7 +686,47 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     d_w1 are final on the current stream (used by the data-parallel step to
     launch their all-reduce while the rest of the backward runs).
     grad_bucket: optional fp32 buffer of 2*d*h elements; d_w1 and d_w2 are then
-    written as views into it ([d_w1 | d_w2]), so one collective covers both."""
+    written as views into it ([d_w1 | d_w2]), so one collective covers both.
+    A padded forward (see ffn_forward) runs the padded backward and returns
+    the gradients of the real d x h parameters."""
+    if cache.core is None:
+        gr = _ffn_backward(g_out, cache, p, cfg, grad_ready, grad_bucket)
+        gr.stats_act, gr.stats_grad = (_token_total(st, cache.n, 0) for st in (gr.stats_act, gr.stats_grad))
+        return gr
+    if cache.config != cfg:
+        raise StateError("cache was produced under a different configuration")
+    d, h, n = cache.d_valid, cache.h_valid, cache.n
+    if (p.model_dim, p.hidden_dim) != (d, h):
+        raise DimensionError(f"parameters {tuple(p.w1.shape)} do not match the cached FFN {(d, h)}")
+    g_out = as_matrix(g_out, "g_out", BF16)
+    if tuple(g_out.shape) != (n, d):
+        raise StateError(f"gradient shape {tuple(g_out.shape)} does not match cached input {(n, d)}")
+    dp, hp = _pad_to(d, 32), _pad_to(h, 128)
+    gr = _ffn_backward(_pad_cols(g_out, dp), cache.core, _pad_params(p, dp, hp), cfg)
+    d_w1, d_w2 = weight_grad_buffers(d, h, g_out.device, grad_bucket)
+    notify = grad_ready or (lambda name, t: None)
+    d_w2.copy_(gr.d_w2[:h, :d])
+    notify("d_w2", d_w2)
+    d_w1.copy_(gr.d_w1[:d, :h])
+    notify("d_w1", d_w1)
+    d_x = gr.d_x[:, :d].contiguous() if dp != d else gr.d_x
+    return FfnGrads(d_w1, d_w2, d_x, None, _census_real(gr.census, n, d, h, cache.plan, cfg),
+                    _token_total(gr.stats_act, n, hp - h), _token_total(gr.stats_grad, n, hp - h))
+
+
+def _token_total(st: SparsifyStats | None, n: int, pad_features: int) -> SparsifyStats | None:
+    """Feature-wise split statistics over the caller's n tokens and real
+    features: the device splits count pad128(n) token rows (zero padding rows)
+    and, in a padded FFN, pad_features all-zero features; the reference's
+    total is n x (sparse features) (ref splitgemm.py:75, sparse24.py:50-69)."""
+    if st is None:
+        return None
+    return SparsifyStats(st.total_entries // pad128(n) * n - n * pad_features, st._dev)
+
+
+def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_ready=None,
+                  grad_bucket: torch.Tensor | None = None) -> FfnGrads:
+    """ffn_backward on a device-tileable cache (see _ffn_forward)."""
     if cache.config != cfg:
         raise StateError("cache was produced under a different configuration")
     _unsupported(cfg)

@@ -285,14 +285,14 @@ def fp8_gemm_rowwise(a: Fp8Rowwise, b: Fp8Rowwise) -> torch.Tensor:
 # ---------------------------------------------------------------- FFN
 
 
-def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backward: bool):
+def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backward: bool, h_valid=None):
     """ffn_forward under fp8_emulation (ref ffn.py:276-363 with fp8=True): the
     two forward GEMMs on e4m3 operands. Sparse forward: K1 on e4m3 codes
     selects on the fp32 scaled pre-activation (selection before quantization,
     ref tests/test_ffn.py:360-367), the kept values are quantized per token,
     fwd.out is the e4m3 2:4 MMA. The cache holds the dequantized activation
     (what the backward of the reference sees) and, for K3, the unquantized one."""
-    from .ffn import FfnCache, GemmEvent, _frame_rows, partition_features
+    from .ffn import FfnCache, GemmEvent, _frame_rows, _plan_split
     from .matcore import device_permutation, gemm_macs
     from .sparse24 import SparsifyStats, sp_gemm_macs
 
@@ -365,8 +365,8 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
     _, sa = quant_rows(vals32, rows=n, amax=amax, codes=aq, deq=act_vals, raw=act_raw)
     meta8 = meta_to_f8(act_meta, n, h)
-    if plan is not None and plan.hidden_dim != h:
-        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+    if plan is not None and plan.hidden_dim != (h_valid or h):
+        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h_valid or h}")
 
     # backward operands that depend only on the forward, prepared on the side
     # stream next to fwd.out: the plan, the feature-wise split of act (K4),
@@ -376,9 +376,9 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     naive_plan = _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else None
     ev_k1 = ov.record(ov.main)
     ov.fork(ev_k1)
-    plan_out = plan
-    if cfg.backward_mode == "split_masked" and plan_out is None:
-        plan_out = partition_features(counts, cfg.split_ratio, launch_stream=ov.st)  # (allocations only here)
+    plan_api = plan_out = plan
+    if cfg.backward_mode == "split_masked" or plan is not None:  # (allocations only here)
+        plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid, ov.st)
     bplan = naive_plan if naive_plan is not None else plan_out
     fa = f8 = None
     if split_bwd:
@@ -405,7 +405,7 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
             meta_to_f8(fa.es, f8["rows_a"], npad, out=f8["e8_a"], st=ov.st)
             quant_cols_t(x_in, f8["xt"], f8["sxt"], st=ov.st, keep=ov.keep)
         ev_side = ov.record()
-    elif ov.side is not None and plan_out is not None and plan is None:
+    elif ov.side is not None and plan_out is not None and plan_out is not plan:
         ev_side = ov.record()
     if ov.side is None:
         ev_side = None
@@ -413,7 +413,8 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
         ev_side = ev_w
     cache = FfnCache(x_in if for_backward else None, n, act_vals, act_meta, None, pre, perm_dev, perm_dev, inv_dev,
                      plan_out, SparsifyStats(n * h, stats_dev), counts, census, cfg, act_split=fa,
-                     act_split_ready=ev_side, act_raw=act_raw, act_meta8=meta8, f8=f8)
+                     act_split_ready=ev_side, act_raw=act_raw, act_meta8=meta8, f8=f8,
+                     plan_valid=plan_api if h_valid is not None else None)
     if ov.side is not None and not for_backward:
         ov.join(ev_side)
     return out, cache

@@ -115,6 +115,38 @@ def partition_features(counts, ratio: float, launch_stream=None) -> SplitPlan:
     return SplitPlan(h, ratio, counts, sp, de, pos)
 
 
+def pad_plan(plan: SplitPlan, h_pad: int, launch_stream=None) -> SplitPlan:
+    """The plan of h features extended to h_pad >= h features: the padding
+    features [h, h_pad) (all-zero columns of a padded FFN) become extra sparse
+    ranks after the real ones; dense features are unchanged."""
+    h = plan.hidden_dim
+    if h_pad == h:
+        return plan
+    dev, ns, extra = plan.feat_pos.device, plan.n_sparse, h_pad - h
+    # outputs allocated on the current stream (the consumer's), filled on launch_stream
+    sp = torch.empty(ns + extra, dtype=torch.int32, device=dev)
+    pos = torch.empty(h_pad, dtype=torch.int32, device=dev)
+    counts = torch.empty(h_pad, dtype=plan.counts.dtype, device=dev)
+    with torch.cuda.stream(launch_stream or torch.cuda.current_stream(dev)):
+        sp[:ns].copy_(plan.sparse_features)
+        sp[ns:].copy_(torch.arange(h, h_pad, dtype=torch.int32, device=dev))
+        pos[:h].copy_(plan.feat_pos)
+        pos[h:].copy_(torch.arange(ns, ns + extra, dtype=torch.int32, device=dev))
+        counts[:h].copy_(plan.counts)
+        counts[h:].zero_()
+    return SplitPlan(h_pad, plan.ratio, counts, sp, plan.dense_features, pos)
+
+
+def partition_features_padded(counts, ratio: float, h_valid: int, launch_stream=None):
+    """partition_features over the first h_valid features of a padded FFN
+    (the reference's plan, returned first) and its padded device form."""
+    if h_valid == counts.shape[0]:
+        plan = partition_features(counts, ratio, launch_stream)
+        return plan, plan
+    plan = partition_features(counts[:h_valid], ratio, launch_stream)
+    return plan, pad_plan(plan, counts.shape[0], launch_stream)
+
+
 def split_gemm_macs(n: int, d: int, plan: SplitPlan) -> int:
     """Exact MAC count n*d*(|sparse|/2 + |dense|) (ref splitgemm.py:84-88)."""
     return sp_gemm_macs(n, plan.n_sparse, d) + gemm_macs(plan.n_dense, n, d)

@@ -93,7 +93,10 @@ def test_toy_schedule_and_config_validation():
         with pytest.raises(ConfigError):
             toy.TrainConfig(**bad)
     with pytest.raises(ConfigError):
-        toy.ToyModelConfig(hidden=100)
+        toy.ToyModelConfig(hidden=102)
+    with pytest.raises(ConfigError):
+        toy.ToyModelConfig(embed_dim=60, context=8)
+    toy.ToyModelConfig(hidden=100, embed_dim=24)  # (run zero-padded on the device)
     tr, ev = toy.build_dataset(bytes(range(20)), 4, 0.5, "cpu")
     assert tr.contexts.shape == (8, 4) and ev.contexts.shape == (8, 4) and len(tr) == 8
     assert tr.contexts[3].tolist() == [3, 4, 5, 6] and int(tr.targets[3]) == 7

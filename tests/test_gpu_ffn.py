@@ -74,6 +74,7 @@ def test_recipe_selection_exact_and_outputs_within_tolerance(n, d, h):
     # GPU's stored (bf16) act and g_pre values
     act_kept = s24.decompress(cache.act_sparse).cpu().numpy()
     _, _, _, fst = O.sparsify_feature(np.ascontiguousarray(act_kept[:, osp]))
+    assert grads.stats_act.total_entries == fst["total_entries"]
     assert grads.stats_act.nonzeros_before == fst["nonzeros_before"]
     assert grads.stats_act.dropped == fst["dropped"]
 

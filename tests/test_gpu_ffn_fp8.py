@@ -135,15 +135,18 @@ def test_fp8_api_matches_reference():
 
 
 def test_fp8_shape_errors_and_module():
-    """fp8 needs model dim % 32 (e4m3 operand rows of 16 bytes, N tiles); the
+    """A model dim the e4m3 GEMMs do not tile (40) runs zero-padded; the
     nn.Module and the graph capture run the e4m3 configs like the bf16 ones."""
     from dataclasses import replace
 
     cfg = replace(s24.RECIPE, fp8_emulation=True, fp8_backward=True)
     x = torch.randn(64, 40, device="cuda")
     p = s24.FfnParams(w1=torch.randn(40, 128, device="cuda"), w2=torch.randn(128, 40, device="cuda"))
+    out40, c40 = s24.ffn_forward(x, p, cfg)
+    g40 = s24.ffn_backward(x, c40, p, cfg)
+    assert out40.shape == (64, 40) and g40.d_w1.shape == (40, 128) and g40.d_x.shape == (64, 40)
     with pytest.raises(s24.DimensionError):
-        s24.ffn_forward(x, p, cfg)
+        s24.ffn_forward(torch.randn(64, 48, device="cuda"), p, cfg)
     torch.manual_seed(0)
     layer = s24.SquaredReluFFN24(64, 256, cfg=cfg)
     xin = torch.randn(2, 50, 64, device="cuda", requires_grad=True)  # 100 tokens: padded to a multiple of 4

@@ -82,3 +82,15 @@ def test_init_activation_sparsity_is_about_half():
     model = toy.ToyModel(mc)
     sp = toy.measure_activation_sparsity(model, train_split.contexts[:2048])
     assert len(sp) == 2 and all(abs(s - 0.5) <= 0.05 for s in sp), sp
+
+
+def test_untileable_dims_train():
+    """embed_dim 24, hidden 100: the FFN blocks run zero-padded (ffn.ffn_forward)."""
+    mc = toy.ToyModelConfig(embed_dim=24, hidden=100, num_blocks=2, context=8)
+    tc = toy.TrainConfig(steps=12, warmup_dense_steps=4, batch_tokens=64, lr_warmup_steps=4, eval_every=6,
+                         eval_tokens=256, ffn=s24.RECIPE)
+    metrics, model = toy.train(mc, tc, corpus())
+    assert [m.step for m in metrics] == [6, 12]
+    assert all(np.isfinite(m.eval_loss) for m in metrics)
+    assert model.w1[0].shape == (24, 100)
+    assert metrics[-1].gemms_sparse == 2 * 4
