@@ -135,16 +135,24 @@ struct EpiStore {
       }
     } else {
       OutT* dst = out + r * p.ldo + col0;
+      // whole 32-byte sectors per store (st_global_32b)
       if constexpr (sizeof(OutT) == 4) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          st_global_v4(dst + i, __float_as_uint(v[i]), __float_as_uint(v[i + 1]), __float_as_uint(v[i + 2]),
-                       __float_as_uint(v[i + 3]));
+        for (int i = 0; i < 32; i += 8) {
+          const uint32_t w[8] = {__float_as_uint(v[i]),     __float_as_uint(v[i + 1]), __float_as_uint(v[i + 2]),
+                                 __float_as_uint(v[i + 3]), __float_as_uint(v[i + 4]), __float_as_uint(v[i + 5]),
+                                 __float_as_uint(v[i + 6]), __float_as_uint(v[i + 7])};
+          st_global_32b(dst + i, w);
+        }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          st_global_v4(dst + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
-                       pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
+        for (int i = 0; i < 32; i += 16) {
+          const uint32_t w[8] = {pack_bf16x2(v[i], v[i + 1]),         pack_bf16x2(v[i + 2], v[i + 3]),
+                                 pack_bf16x2(v[i + 4], v[i + 5]),     pack_bf16x2(v[i + 6], v[i + 7]),
+                                 pack_bf16x2(v[i + 8], v[i + 9]),     pack_bf16x2(v[i + 10], v[i + 11]),
+                                 pack_bf16x2(v[i + 12], v[i + 13]), pack_bf16x2(v[i + 14], v[i + 15])};
+          st_global_32b(dst + i, w);
+        }
       }
     }
   }
@@ -268,16 +276,18 @@ struct EpiFwd1T {
       float* dst = p.vals32 + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
       float mx = 0.f;
 #pragma unroll
-      for (int i = 0; i < 16; i += 4) {
-        st_global_v4(dst + i, __float_as_uint(kept[i]), __float_as_uint(kept[i + 1]), __float_as_uint(kept[i + 2]),
-                     __float_as_uint(kept[i + 3]));
-        mx = fmaxf(mx, fmaxf(fmaxf(kept[i], kept[i + 1]), fmaxf(kept[i + 2], kept[i + 3])));
+      for (int i = 0; i < 16; i += 8) {
+        const uint32_t w[8] = {__float_as_uint(kept[i]),     __float_as_uint(kept[i + 1]), __float_as_uint(kept[i + 2]),
+                               __float_as_uint(kept[i + 3]), __float_as_uint(kept[i + 4]), __float_as_uint(kept[i + 5]),
+                               __float_as_uint(kept[i + 6]), __float_as_uint(kept[i + 7])};
+        st_global_32b(dst + i, w);
       }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) mx = fmaxf(mx, kept[i]);
       if (mx > 0.f) atomicMax(p.row_amax + drow, __float_as_uint(mx));  // a >= 0: uint order = float order
     } else {
       __nv_bfloat16* dst = p.vals + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
-      st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
-      st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
+      st_global_32b(dst, packed);
     }
     uint16_t* mh = reinterpret_cast<uint16_t*>(p.meta);
     st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16, p.N) / 2, static_cast<uint16_t>(m16[0]));
@@ -376,8 +386,7 @@ struct EpiBwd1T {
     }
     if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
     __nv_bfloat16* dst = p.gvals + static_cast<long long>(s.drow) * (p.N / 2) + col0 / 2;
-    st_global_v4(dst, packed[0], packed[1], packed[2], packed[3]);
-    st_global_v4(dst + 8, packed[4], packed[5], packed[6], packed[7]);
+    st_global_32b(dst, packed);
   }
 };
 
@@ -406,9 +415,13 @@ struct EpiRelu2 {
     }
     __nv_bfloat16* dst = p.act + static_cast<long long>(row) * p.ld + col0;
 #pragma unroll
-    for (int i = 0; i < 32; i += 8)
-      st_global_v4(dst + i, pack_bf16x2(a[i], a[i + 1]), pack_bf16x2(a[i + 2], a[i + 3]),
-                   pack_bf16x2(a[i + 4], a[i + 5]), pack_bf16x2(a[i + 6], a[i + 7]));
+    for (int i = 0; i < 32; i += 16) {
+      const uint32_t w[8] = {pack_bf16x2(a[i], a[i + 1]),         pack_bf16x2(a[i + 2], a[i + 3]),
+                             pack_bf16x2(a[i + 4], a[i + 5]),     pack_bf16x2(a[i + 6], a[i + 7]),
+                             pack_bf16x2(a[i + 8], a[i + 9]),     pack_bf16x2(a[i + 10], a[i + 11]),
+                             pack_bf16x2(a[i + 12], a[i + 13]), pack_bf16x2(a[i + 14], a[i + 15])};
+      st_global_32b(dst + i, w);
+    }
   }
 };
 
@@ -446,17 +459,22 @@ struct EpiDact {
                                const float (&v)[32], uint32_t) {
     if (!row_ok) return;
     __nv_bfloat16* dst = p.gpre + static_cast<long long>(row) * p.ld_g + col0;
+    uint32_t o[16];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t ww[4] = {s.buf[ci][i].x, s.buf[ci][i].y, s.buf[ci][i].z, s.buf[ci][i].w};
-      uint32_t o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float a0 = __uint_as_float(ww[j] << 16), a1 = __uint_as_float(ww[j] & 0xFFFF0000u);
-        o[j] = pack_bf16x2(v[8 * i + 2 * j] * (2.f * sqrt_approx(a0)),
-                           v[8 * i + 2 * j + 1] * (2.f * sqrt_approx(a1)));
+        o[4 * i + j] = pack_bf16x2(v[8 * i + 2 * j] * (2.f * sqrt_approx(a0)),
+                                   v[8 * i + 2 * j + 1] * (2.f * sqrt_approx(a1)));
       }
-      st_global_v4(dst + 8 * i, o[0], o[1], o[2], o[3]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t w[8] = {o[8 * h], o[8 * h + 1], o[8 * h + 2], o[8 * h + 3],
+                             o[8 * h + 4], o[8 * h + 5], o[8 * h + 6], o[8 * h + 7]};
+      st_global_32b(dst + 16 * h, w);
     }
   }
 };

@@ -23,6 +23,13 @@
 // and stage slots are recycled only when both pairs' MMAs have released them.
 // The producer and MMA warps sit at the highest warp ids because the warp
 // arbiter prefers higher ids: busy epilogue warps must not delay MMA issue.
+// BN = 512 (dense, CTA pairs): each k-step issues two N = 256 MMAs (sub-tiles
+//   s = 0, 1: CTA r stages B columns 256s + 128r .. +127 of the tile) into one
+//   512-column accumulator. Per CTA a stage moves 16 KB of A and 32 KB of B
+//   per 128 x 512 x 64 MACs, a quarter fewer bytes per MAC than BN = 256,
+//   for the L2->SM operand feed that bounds these GEMMs. The accumulator is
+//   single-buffered: the next tile's MMAs wait for the drain, while the
+//   producer keeps filling stages.
 // Accumulators: two TMEM slots. Disjoint (2*BN columns) when they fit, else
 // overlapping by one 32-column chunk (slot 1 starts at BN-32): the epilogue
 // drains the shared chunk first and releases the slot right away, so the next
@@ -82,6 +89,10 @@ struct GemmCfg {
   static constexpr int TILE_M = BM * CG;         // rows per tile
   static constexpr int BN = BN_;                 // columns per tile (MMA N)
   static constexpr int BN_CTA = BN / CG;         // B columns staged per CTA
+  static constexpr int NSUB = BN > 256 ? BN / 256 : 1;  // MMAs per k-step (N = 256 each)
+  static constexpr int MMA_N = BN / NSUB;
+  static constexpr int SUB_CTA = BN_CTA / NSUB;  // B columns per CTA per sub-tile
+  static constexpr int NSLOT = NSUB > 1 ? 1 : 2; // accumulator slots
   static constexpr int STAGES = STAGES_;
   static constexpr int BK = (SPARSE ? 128 : 64) * (2 / EB);  // logical K per stage
   static constexpr int A_COLS = 128 / EB;        // stored A elements per row per stage (128 bytes)
@@ -93,16 +104,16 @@ struct GemmCfg {
   static constexpr uint32_t E_BYTES = 2048 * E_ATOMS;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES + E_BYTES;
   static constexpr uint32_t E_COLS = STAGES * 4 * E_ATOMS;
-  static constexpr bool OVERLAP = 2 * BN + E_COLS > 512;
+  static constexpr bool OVERLAP = NSLOT == 2 && 2 * BN + E_COLS > 512;
   static constexpr uint32_t SLOT1_COL = OVERLAP ? BN - 32 : BN;
-  static constexpr uint32_t E_COL = SLOT1_COL + BN;
+  static constexpr uint32_t E_COL = NSLOT == 1 ? BN : SLOT1_COL + BN;
   static constexpr uint32_t TMEM_NEED = E_COL + E_COLS;
   static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128
                                        : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static_assert(!(SPARSE && A_MN), "sparse A must be K-major");
   static_assert(!(F8 && (A_MN || B_MN)), "e4m3 operands are K-major");
-  static_assert(BN_CTA % 64 == 0 && BN <= 256, "BN");
+  static_assert(BN_CTA % 64 == 0 && (BN <= 256 || (BN == 512 && !SPARSE && CG == 2 && MC_ == 1)), "BN");
   static_assert(CG == 1 || CG == 2, "CG");
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int SCHED_SLOTS = 4;  // work-unit broadcast ring (dynamic scheduler)
@@ -119,7 +130,7 @@ struct GemmCfg {
   static constexpr uint32_t SMEM_BYTES =
       BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20 + (K4W > 0 ? 8 + STAGES * 8 : 0);
   static constexpr uint32_t IDESC =
-      F8 ? make_idesc_e4m3(TILE_M, BN, SPARSE) : make_idesc_bf16(TILE_M, BN, A_MN, B_MN, SPARSE);
+      F8 ? make_idesc_e4m3(TILE_M, MMA_N, SPARSE) : make_idesc_bf16(TILE_M, MMA_N, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
   static constexpr int EPI_THREADS = 32 * EPI_WARPS;
@@ -135,7 +146,7 @@ struct GemmCfg {
   static constexpr int B_KBOX = BK / BOX_K;  // K-major B: 128-byte K boxes per stage
   // K-major B with fewer K boxes than pairs is split by rows instead
   static constexpr int B_ROW_SPLIT = (!B_MN && B_KBOX % MC != 0) ? MC : 1;
-  static constexpr int B_BOX_ROWS = BN_CTA / B_ROW_SPLIT;
+  static constexpr int B_BOX_ROWS = SUB_CTA / B_ROW_SPLIT;
   static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast needs CTA pairs");
 };
 
@@ -336,7 +347,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const CUtensorMap* mapE = g2 ? &tmE2 : &tmE;
         const int mt = mb * MC + static_cast<int>(pair);  // this pair's M tile
         const int m0 = mt * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
-        const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::BN_CTA;
+        // sub-tile s of this CTA: B columns n0 + s * MMA_N .. + SUB_CTA - 1
+        const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::SUB_CTA;
         const int atom_row = mt * CG + static_cast<int>(rank);  // 128-row metadata block
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -375,12 +387,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 #pragma unroll
             for (int j = 0; j < Cfg::BN_CTA / 64; ++j)
               if (MC == 1 || j % MC == static_cast<int>(pair))
-                load_b(sb + j * (Cfg::BK * 128), n0 + 64 * j, kb * Cfg::BK);
+                load_b(sb + j * (Cfg::BK * 128),
+                       n0 + (j / (Cfg::SUB_CTA / 64)) * Cfg::MMA_N + 64 * (j % (Cfg::SUB_CTA / 64)), kb * Cfg::BK);
           } else if constexpr (Cfg::B_ROW_SPLIT == 1) {
 #pragma unroll
             for (int j = 0; j < Cfg::B_KBOX; ++j)
               if (MC == 1 || j % MC == static_cast<int>(pair))
-                load_b(sb + j * (Cfg::BN_CTA * 128), kb * Cfg::BK + Cfg::BOX_K * j, n0);
+#pragma unroll
+                for (int sub = 0; sub < Cfg::NSUB; ++sub)
+                  load_b(sb + j * (Cfg::BN_CTA * 128) + sub * (Cfg::SUB_CTA * 128), kb * Cfg::BK + Cfg::BOX_K * j,
+                         n0 + sub * Cfg::MMA_N);
           } else {
             const int r0 = static_cast<int>(pair) * Cfg::B_BOX_ROWS;
 #pragma unroll
@@ -406,11 +422,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       for (int iter = 0;; ++iter) {
         const int t = dyn ? sched_take(iter, true) : cluster_id + iter * num_clusters;
         if (t >= total_tiles) break;
-        const int slot = iter & 1;
+        const int slot = iter % Cfg::NSLOT;
         if constexpr (Cfg::OVERLAP) {
           if (iter > 0) mbar_wait(&tempty_bar[0], (iter - 1) & 1);
         } else {
-          mbar_wait(&tempty_bar[slot], ((iter >> 1) & 1) ^ 1);
+          mbar_wait(&tempty_bar[slot], ((iter / Cfg::NSLOT) & 1) ^ 1);
         }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + slot * Cfg::SLOT1_COL;
@@ -434,7 +450,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
           }
 #pragma unroll
-          for (int j = 0; j < (S24_PIPE_PROBE == 2 ? 0 : Cfg::KSTEPS); ++j) {
+          for (int j = 0; j < (S24_PIPE_PROBE == 2 ? 0 : Cfg::KSTEPS); ++j)
+#pragma unroll
+          for (int sub = 0; sub < Cfg::NSUB; ++sub) {
+            // (NSUB > 1: dense only; sub-tile sub's B boxes and accumulator columns)
+            const uint32_t sbs = sb + sub * (Cfg::B_MN ? (Cfg::SUB_CTA / 64) * (Cfg::BK * 128) : Cfg::SUB_CTA * 128);
+            const uint32_t d_sub = d_tmem + static_cast<uint32_t>(sub * Cfg::MMA_N);
             uint64_t adesc, bdesc;
             if constexpr (Cfg::A_MN) {
               adesc = make_sdesc(sa + j * 2048, Cfg::A_BYTES / 2, 1024, kLayoutSw128);
@@ -443,11 +464,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
             if constexpr (Cfg::B_MN) {
               // dense: 16 K rows per step; sparse: 32 K rows per step
-              bdesc = make_sdesc(sb + j * (Cfg::SPARSE ? 4096 : 2048), Cfg::BK * 128, 1024, kLayoutSw128);
+              bdesc = make_sdesc(sbs + j * (Cfg::SPARSE ? 4096 : 2048), Cfg::BK * 128, 1024, kLayoutSw128);
             } else if constexpr (Cfg::SPARSE) {
               bdesc = make_sdesc(sb + (j >> 1) * (Cfg::BN_CTA * 128) + (j & 1) * 64, 16, 1024, kLayoutSw128);
             } else {
-              bdesc = make_sdesc(sb + j * 32, 16, 1024, kLayoutSw128);
+              bdesc = make_sdesc(sbs + j * 32, 16, 1024, kLayoutSw128);
             }
             const uint32_t accum = (kb > kb0 || j > 0) ? 1u : 0u;
             if constexpr (Cfg::SPARSE && Cfg::F8) {
@@ -467,14 +488,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
                 mma_sp_bf16(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
             } else if constexpr (Cfg::F8) {
               if constexpr (CG == 2)
-                mma_e4m3_cg2(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+                mma_e4m3_cg2(d_sub, adesc, bdesc, Cfg::IDESC, accum);
               else
-                mma_e4m3(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+                mma_e4m3(d_sub, adesc, bdesc, Cfg::IDESC, accum);
             } else {
               if constexpr (CG == 2)
-                mma_bf16_cg2(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+                mma_bf16_cg2(d_sub, adesc, bdesc, Cfg::IDESC, accum);
               else
-                mma_bf16(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+                mma_bf16(d_sub, adesc, bdesc, Cfg::IDESC, accum);
             }
           }
           uint64_t* tf = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
@@ -530,7 +551,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       if (t >= total_tiles) break;
       int mb, nb;
       tile_coords(shape, t % mn_tiles, mb, nb);
-      const int slot = iter & 1;
+      const int slot = iter % Cfg::NSLOT;
       const int row = (mb * MC + static_cast<int>(pair)) * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 +
                       static_cast<int>(lane);
       const bool row_ok = row < shape.M;
@@ -545,7 +566,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       // whose slot the MMAs of tile t+2 overwrite.
       const bool owner = Cfg::OVERLAP && (slot == 0 ? owns_last : c_begin == 0);
       uint64_t* tfull = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
-      const uint32_t tparity = Cfg::OVERLAP ? (iter & 1) : ((iter >> 1) & 1);
+      const uint32_t tparity = Cfg::OVERLAP ? (iter & 1) : ((iter / Cfg::NSLOT) & 1);
       if (bg_more && !owner) {
         while (!mbar_test(tfull, tparity)) {
           if (!bg_unit()) {
@@ -574,7 +595,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             tmem_ld_wait();
           }
         }
-        if (owner && ci == 0) {
+        // release the accumulator as soon as this warp's last load landed
+        // (overlapping slots: the shared chunk's owner, after its first load)
+        if (Cfg::OVERLAP ? (owner && ci == 0) : ci == Cfg::CPW - 1) {
           tc_fence_before();
           if (leader)
             mbar_arrive(tempty);
@@ -587,13 +610,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           Epi::chunk(epg, st, row, row_ok, col0, ci, v, lane);
         }
-      }
-      if constexpr (!Cfg::OVERLAP) {
-        tc_fence_before();
-        if (leader)
-          mbar_arrive(tempty);
-        else
-          mbar_arrive_remote(tempty, leader_rank);
       }
     }
     // drain what is left of the background queue

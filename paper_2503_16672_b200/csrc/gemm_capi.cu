@@ -280,13 +280,41 @@ using SparseK_FS = GemmCfg<true, false, false, 256, 4, 2, 4, 1, false, S24_FS_WA
 using F8DenseKK = GemmCfg<false, false, false, 256, S24_DENSE_STAGES, 2, 8, 1, true>;
 using F8SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, 1, true>;
 
+// wide dense tiles: 256 x 512 per CTA pair, one 512-column accumulator (see
+// gemm.cuh). A quarter fewer operand bytes per MAC than 256 x 256, but the
+// accumulator drain is exposed. Measured at c2 (scripts/gpu_wide.sh): the
+// MN-major-A weight-gradient GEMMs (K = tokens = 16384) gain 6-9%; the
+// K-major-A GEMMs lose 1-6% (K1 0.400 -> 0.423 ms: its heavier epilogue is
+// what gets exposed). Default: wide for MN-major A only.
+#ifndef S24_DENSE_WIDE_STAGES
+#define S24_DENSE_WIDE_STAGES 4
+#endif
+using DenseKN_W = GemmCfg<false, false, true, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
+using DenseKK_W = GemmCfg<false, false, false, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
+using DenseMM_W = GemmCfg<false, true, true, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
+using DenseMK_W = GemmCfg<false, true, false, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
+using F8DenseKK_W = GemmCfg<false, false, false, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1, true>;
+
+// S24_DENSE_BN=512 / 256 forces every dense GEMM wide / narrow (experiments)
+static bool dense_wide(bool a_mn) {
+  const char* e = std::getenv("S24_DENSE_BN");
+  return e ? std::atoi(e) == 512 : a_mn;
+}
+
+template <class Narrow, class Wide, class Epi>
+static int launch_dense(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                        const typename Epi::Params& ep, cudaStream_t st, int k_splits = 1) {
+  if (dense_wide(Narrow::A_MN)) return launch_gemm<Wide, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+  return launch_gemm<Narrow, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+}
+
 template <class Epi>
 static int dispatch_dense(int a_mn, int b_mn, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
                           int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st, int k_splits = 1) {
-  if (!a_mn && b_mn) return launch_gemm<DenseKN, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
-  if (!a_mn && !b_mn) return launch_gemm<DenseKK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
-  if (a_mn && b_mn) return launch_gemm<DenseMM, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
-  return launch_gemm<DenseMK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, st, k_splits);
+  if (!a_mn && b_mn) return launch_dense<DenseKN, DenseKN_W, Epi>(A, lda, B, ldb, M, N, K, ep, st, k_splits);
+  if (!a_mn && !b_mn) return launch_dense<DenseKK, DenseKK_W, Epi>(A, lda, B, ldb, M, N, K, ep, st, k_splits);
+  if (a_mn && b_mn) return launch_dense<DenseMM, DenseMM_W, Epi>(A, lda, B, ldb, M, N, K, ep, st, k_splits);
+  return launch_dense<DenseMK, DenseMK_W, Epi>(A, lda, B, ldb, M, N, K, ep, st, k_splits);
 }
 
 // split-K partial sums ws[ks][M][N] -> D (row map / transpose), fixed order.
@@ -522,7 +550,7 @@ int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1
   EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N),
                      FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)},
                      row_map};
-  return launch_gemm<DenseKN, EpiFwd1>(x, ldx, w1, ldw1, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+  return launch_dense<DenseKN, DenseKN_W, EpiFwd1>(x, ldx, w1, ldw1, M, N, K, ep, static_cast<cudaStream_t>(stream));
 }
 
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
@@ -546,8 +574,7 @@ int s24_gemm_relu2(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int
   int rc = check_common(M, N, K, ldx, 0, ldw1, 1);
   if (rc) return rc;
   EpiRelu2::Params ep{static_cast<__nv_bfloat16*>(act), ld_act};
-  return launch_gemm<DenseKN, EpiRelu2>(x, ldx, w1, ldw1, M, N, K, nullptr, ep,
-                                        static_cast<cudaStream_t>(stream));
+  return launch_dense<DenseKN, DenseKN_W, EpiRelu2>(x, ldx, w1, ldw1, M, N, K, ep, static_cast<cudaStream_t>(stream));
 }
 
 int s24_gemm_dact(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N, int64_t K,
@@ -579,7 +606,7 @@ int s24_gemm_f8(const uint8_t* A, int64_t lda, const uint8_t* B, int64_t ldb, in
     typename Epi::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
                             static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), nullptr, 0, 0, row_scale,
                             col_scale};
-    return launch_gemm<F8DenseKK, Epi>(A, lda, B, ldb, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+    return launch_dense<F8DenseKK, F8DenseKK_W, Epi>(A, lda, B, ldb, M, N, K, ep, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -645,7 +672,7 @@ int s24_fwd_gemm1_f8(const uint8_t* xq, int64_t ldx, const uint8_t* w1q, int64_t
   using Epi = EpiFwd1T<true>;
   Epi::Params ep{nullptr, act_meta, counts, stats, y_dbg, static_cast<int>(N), FwTarget{nullptr, nullptr, nullptr, 0},
                  nullptr, x_scale, w1_scale, act_vals32, row_amax};
-  return launch_gemm<F8DenseKK, Epi>(xq, ldx, w1q, ldw1, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
+  return launch_dense<F8DenseKK, F8DenseKK_W, Epi>(xq, ldx, w1q, ldw1, M, N, K, ep, static_cast<cudaStream_t>(stream));
 }
 
 int s24_bwd_dact_f8(const uint8_t* gq, int64_t ldg, const uint8_t* w2q, int64_t ldw2, int64_t M, int64_t N,

@@ -244,6 +244,25 @@ __device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, ui
     asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// 32 bytes from one lane (256-bit STG, sm_100): a whole L2 sector per request,
+// where two 16-byte stores to the same sector cost two write requests.
+// p must be 32-byte aligned.
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+
+// 32 bytes at p: one 256-bit store when p is 32-byte aligned, else two 16-byte ones
+__device__ __forceinline__ void st_global_32b(void* p, const uint32_t (&w)[8]) {
+  if ((reinterpret_cast<uintptr_t>(p) & 31u) == 0u) {
+    st_global_v8(p, w);
+  } else {
+    st_global_v4(p, w[0], w[1], w[2], w[3]);
+    st_global_v4(static_cast<uint8_t*>(p) + 16, w[4], w[5], w[6], w[7]);
+  }
+}
+
 __device__ __forceinline__ void st_global_u16(uint16_t* p, uint16_t v) {
   if constexpr (S24_ST_CS)
     __stcs(reinterpret_cast<unsigned short*>(p), v);
