@@ -193,8 +193,28 @@ struct EpiFwd1T {
     unsigned long long before, after;
     const uint2* lut;
     int drow;             // destination row of this lane's row in the current tile
+    uint32_t mq[4];       // metadata halfwords (k1 = 0 | k1 = 1 << 16) of the atom's chunks k2 = 0..3
   };
-  static constexpr bool kUnroll = false;
+  static constexpr bool kUnroll = true;  // (mq is indexed by the chunk)
+  // Without a row map the warp's run of chunks covers whole 128-column
+  // metadata atoms (a multiple of 4 chunks starting at a multiple of 4): the
+  // 8 halfwords a row has in an atom are gathered across lane pairs (rows r,
+  // r ^ 8 interleave per 4-byte word) and written as one 16-byte store per
+  // lane, whole sectors, instead of two 2-byte stores per chunk.
+  __device__ static void meta_flush(const Params& p, const State& s, int row, bool any_ok, int col0, uint32_t lane) {
+    const bool hi = (lane & 8u) != 0u;  // m1 = 1: this lane writes the k1 = 1 half of the pair
+    uint32_t w[4];
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const uint32_t lo16 = s.mq[k2] & 0xFFFFu, hi16 = s.mq[k2] >> 16;
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, hi ? lo16 : hi16, 8);
+      w[k2] = hi ? (recv | (hi16 << 16)) : (lo16 | (recv << 16));
+    }
+    if (!any_ok) return;  // (warp-uniform) every row of the warp is padding beyond the buffer's rows
+    const uint64_t off = meta_hw_halfword_offset(static_cast<uint64_t>(row) & ~8ull,
+                                                 static_cast<uint64_t>(col0 / 16) + (hi ? 1u : 0u), p.N);
+    st_global_v4(p.meta + off, w[0], w[1], w[2], w[3]);
+  }
   __device__ static void init(const Params&, State& s) {
     s.before = s.after = 0;
     s.lut = fw_lut_init();
@@ -209,7 +229,7 @@ struct EpiFwd1T {
       atomicAdd(p.stats + 1, a);
     }
   }
-  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int,
+  __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int ci,
                                const float (&v_in)[32], uint32_t lane) {
     float v[32];
     if constexpr (F8) {
@@ -264,6 +284,13 @@ struct EpiFwd1T {
     if constexpr (!F8) {
       if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
     }
+    const bool combine = p.row_map == nullptr;  // (warp-uniform)
+    if (combine) {
+      // padding rows inside the buffer (row >= M) get the (0, 1) selectors of
+      // an all-zero group, 0x4444: the value the host pre-fills them with
+      s.mq[ci & 3] = m16[0] | (m16[1] << 16);
+      if ((ci & 3) == 3) meta_flush(p, s, row, __any_sync(0xffffffffu, row_ok), col0 - 96, lane);
+    }
     if (!row_ok) return;
     s.before += __popc(nz);
     s.after += __popc(nz & keep32);
@@ -289,9 +316,11 @@ struct EpiFwd1T {
       __nv_bfloat16* dst = p.vals + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
       st_global_32b(dst, packed);
     }
-    uint16_t* mh = reinterpret_cast<uint16_t*>(p.meta);
-    st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16, p.N) / 2, static_cast<uint16_t>(m16[0]));
-    st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16 + 1, p.N) / 2, static_cast<uint16_t>(m16[1]));
+    if (!combine) {
+      uint16_t* mh = reinterpret_cast<uint16_t*>(p.meta);
+      st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16, p.N) / 2, static_cast<uint16_t>(m16[0]));
+      st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16 + 1, p.N) / 2, static_cast<uint16_t>(m16[1]));
+    }
     if (p.y_dbg) {
       float* y = p.y_dbg + static_cast<long long>(drow) * p.N + col0;
 #pragma unroll
