@@ -68,6 +68,41 @@ def test_dense_gemm_majors(a_mn, b_mn, M, N, K):
     assert rel_err(D, ref) < 1e-5
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 256), (320, 800, 448), (128, 288, 64)])
+def test_wide_dense_tiles_bitwise_equal_narrow(monkeypatch, a_mn, b_mn, M, N, K):
+    """256x512 tiles (two N=256 MMAs per k-step, one 512-column accumulator)
+    vs 256x256: same per-element K order, so the results are bit-identical;
+    also K1's fused epilogue (metadata gathered per atom) under both."""
+    torch.manual_seed(3)
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(K, N, device="cuda").bfloat16()
+    As = A.t().contiguous() if a_mn else A
+    Bs = B if b_mn else B.t().contiguous()
+    outs = []
+    for bn in ("256", "512"):
+        monkeypatch.setenv("S24_DENSE_BN", bn)
+        D = torch.full((M, N), float("nan"), device="cuda")
+        _lib.call("s24_gemm", P(As), a_mn, As.stride(0), P(Bs), b_mn, Bs.stride(0), M, N, K, P(D), F32, N, None, 0,
+                  -1, None, S())
+        outs.append(D)
+    assert torch.equal(outs[0], outs[1])
+    assert rel_err(outs[1], A.float() @ B.float()) < 1e-5
+    if not a_mn and b_mn and N % 128 == 0:
+        res = []
+        for bn in ("256", "512"):
+            monkeypatch.setenv("S24_DENSE_BN", bn)
+            vals = torch.zeros((M + 127) // 128 * 128, N // 2, device="cuda", dtype=torch.bfloat16)
+            meta = torch.full((_lib.meta_hw_bytes(M, N),), 0x44, device="cuda", dtype=torch.uint8)
+            counts = torch.zeros(N, device="cuda", dtype=torch.int32)
+            stats = torch.zeros(2, device="cuda", dtype=torch.int64)
+            _lib.call("s24_fwd_gemm1_fused", P(A), K, P(B), N, M, N, K, P(vals), P(meta), P(counts), P(stats), None,
+                      None, None, None, 0, None, S())
+            res.append((vals, meta, counts, stats))
+        for x, y in zip(*res):
+            assert torch.equal(x, y)
+
+
 def test_dense_gemm_bf16_out_rowmap_transposed():
     torch.manual_seed(1)
     M, N, K = 200, 256, 192
