@@ -68,6 +68,9 @@ struct GemmShape {
   int* sched;           // dynamic tile scheduler {next, done} (zero at launch, reset by the
                         // last cluster), or nullptr: static round-robin units
   K4Job bg;
+  int tail_split;       // the last tail_split tiles (in unit order) run as two N-halves each
+                        // (MN-major B only): a partial last wave of full tiles becomes a
+                        // half-length one (see unit_tile)
   int has_fs;           // 1: the K4 warps split this GEMM's own A stages (K4W > 0, k4s.cuh)
   K4Args fs;            // their outputs (feat_pos, pair_rows, vs, es, n = padded tokens, h, nonneg)
 };
@@ -131,6 +134,10 @@ struct GemmCfg {
       BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20 + (K4W > 0 ? 8 + STAGES * 8 : 0);
   static constexpr uint32_t IDESC =
       F8 ? make_idesc_e4m3(TILE_M, MMA_N, SPARSE) : make_idesc_bf16(TILE_M, MMA_N, A_MN, B_MN, SPARSE);
+  // half-width units (GemmShape::tail_split): N = BN / 2
+  static constexpr bool HALF_OK = B_MN && NSUB == 1 && BN_CTA % 128 == 0;
+  static constexpr uint32_t IDESC_HALF =
+      F8 ? make_idesc_e4m3(TILE_M, BN / 2, SPARSE) : make_idesc_bf16(TILE_M, BN / 2, A_MN, B_MN, SPARSE);
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
   static constexpr int EPI_THREADS = 32 * EPI_WARPS;
@@ -233,6 +240,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   const int mn_tiles = shape.tiles_m * shape.tiles_n;
   const int group_units = mn_tiles * shape.k_splits;
   const int total_tiles = group_units * shape.groups;
+  const int tail_split = Cfg::HALF_OK ? shape.tail_split : 0;
+  const int total_units = total_tiles + tail_split;
+  // scheduler unit u -> tile unit t (and which N-half, or -1 for the whole tile)
+  auto unit_tile = [&](int u, int& half) -> int {
+    const int full = total_tiles - tail_split;
+    if (u < full) {
+      half = -1;
+      return u;
+    }
+    half = (u - full) & 1;
+    return full + ((u - full) >> 1);
+  };
   const int num_kb_all = (shape.K + Cfg::BK - 1) / Cfg::BK;
   // work unit t -> (problem t / group_units; within it: output tile
   // t % mn_tiles, K split t / mn_tiles)
@@ -324,7 +343,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           mbar_arrive(&sched_full[slot]);
           if constexpr (CG == 2) st_async_remote_u32(&sched_tile[slot], static_cast<uint32_t>(t), &sched_full[slot],
                                                      leader_rank + 1);
-          if (t >= total_tiles) {
+          if (t >= total_units) {
             // last cluster out resets the counters for the next launch
             __threadfence();
             if (atomicAdd(shape.sched + 1, 1) == num_clusters - 1) {
@@ -337,7 +356,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           mbar_arrive_expect_tx(&sched_full[slot], 4);
           t = sched_take(iter, true);
         }
-        if (t >= total_tiles) break;
+        if (t >= total_units) break;
+        int half;
+        t = unit_tile(t, half);
         int mb, nb, kb0, kb1;
         tile_coords(shape, t % mn_tiles, mb, nb);
         kb_range(t, kb0, kb1);
@@ -349,6 +370,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const int m0 = mt * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
         // sub-tile s of this CTA: B columns n0 + s * MMA_N .. + SUB_CTA - 1
         const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::SUB_CTA;
+        // half unit: this CTA's B_CTA/2 columns of the half (box 0 .. BN_CTA/128 - 1)
+        const int n0h = nb * Cfg::BN + half * (Cfg::BN / 2) + static_cast<int>(rank) * (Cfg::BN_CTA / 2);
+        const uint32_t stage_tx = half < 0 ? Cfg::STAGE_BYTES : Cfg::STAGE_BYTES - Cfg::B_BYTES / 2;
         const int atom_row = mt * CG + static_cast<int>(rank);  // 128-row metadata block
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -366,7 +390,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             continue;
           }
           if (leader)
-            mbar_arrive_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full_bar[stage], CG * stage_tx);
           else
             mbar_arrive_remote(&full_bar[stage], leader_rank);
           auto load_b = [&](void* dst, int c0, int c1) {
@@ -386,7 +410,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           if constexpr (Cfg::B_MN) {
 #pragma unroll
             for (int j = 0; j < Cfg::BN_CTA / 64; ++j)
-              if (MC == 1 || j % MC == static_cast<int>(pair))
+              if (half >= 0) {
+                if (j < Cfg::BN_CTA / 128) load_b(sb + j * (Cfg::BK * 128), n0h + 64 * j, kb * Cfg::BK);
+              } else if (MC == 1 || j % MC == static_cast<int>(pair))
                 load_b(sb + j * (Cfg::BK * 128),
                        n0 + (j / (Cfg::SUB_CTA / 64)) * Cfg::MMA_N + 64 * (j % (Cfg::SUB_CTA / 64)), kb * Cfg::BK);
           } else if constexpr (Cfg::B_ROW_SPLIT == 1) {
@@ -420,8 +446,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       int stage = 0;
       uint32_t phase = 0;
       for (int iter = 0;; ++iter) {
-        const int t = dyn ? sched_take(iter, true) : cluster_id + iter * num_clusters;
-        if (t >= total_tiles) break;
+        const int u = dyn ? sched_take(iter, true) : cluster_id + iter * num_clusters;
+        if (u >= total_units) break;
+        int half;
+        const int t = unit_tile(u, half);
+        const uint32_t idesc = half < 0 ? Cfg::IDESC : Cfg::IDESC_HALF;
         const int slot = iter % Cfg::NSLOT;
         if constexpr (Cfg::OVERLAP) {
           if (iter > 0) mbar_wait(&tempty_bar[0], (iter - 1) & 1);
@@ -475,27 +504,27 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
               // e4m3: one K=64 step reads 64 metadata bits per row = TMEM
               // columns 2j, 2j+1 of the stage
               if constexpr (CG == 2)
-                mma_sp_e4m3_cg2(d_tmem, adesc, bdesc, e_tmem + 2 * j, Cfg::IDESC, accum);
+                mma_sp_e4m3_cg2(d_tmem, adesc, bdesc, e_tmem + 2 * j, idesc, accum);
               else
-                mma_sp_e4m3(d_tmem, adesc, bdesc, e_tmem + 2 * j, Cfg::IDESC, accum);
+                mma_sp_e4m3(d_tmem, adesc, bdesc, e_tmem + 2 * j, idesc, accum);
             } else if constexpr (Cfg::SPARSE) {
               // metadata address must be 2-column aligned; the odd column is
               // selected by the descriptor's sparse-id2 field (bits 0-1)
-              const uint32_t id = Cfg::IDESC | static_cast<uint32_t>(j & 1);
+              const uint32_t id = idesc | static_cast<uint32_t>(j & 1);
               if constexpr (CG == 2)
                 mma_sp_bf16_cg2(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
               else
                 mma_sp_bf16(d_tmem, adesc, bdesc, e_tmem + (j & ~1), id, accum);
             } else if constexpr (Cfg::F8) {
               if constexpr (CG == 2)
-                mma_e4m3_cg2(d_sub, adesc, bdesc, Cfg::IDESC, accum);
+                mma_e4m3_cg2(d_sub, adesc, bdesc, idesc, accum);
               else
-                mma_e4m3(d_sub, adesc, bdesc, Cfg::IDESC, accum);
+                mma_e4m3(d_sub, adesc, bdesc, idesc, accum);
             } else {
               if constexpr (CG == 2)
-                mma_bf16_cg2(d_sub, adesc, bdesc, Cfg::IDESC, accum);
+                mma_bf16_cg2(d_sub, adesc, bdesc, idesc, accum);
               else
-                mma_bf16(d_sub, adesc, bdesc, Cfg::IDESC, accum);
+                mma_bf16(d_sub, adesc, bdesc, idesc, accum);
             }
           }
           uint64_t* tf = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
@@ -547,16 +576,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       }
     };
     for (int iter = 0;; ++iter) {
-      const int t = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
-      if (t >= total_tiles) break;
+      const int u = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
+      if (u >= total_units) break;
+      int half;
+      const int t = unit_tile(u, half);
       int mb, nb;
       tile_coords(shape, t % mn_tiles, mb, nb);
+      // a half unit holds N = BN / 2 columns, starting at BN / 2 * half
+      const int col_base = nb * Cfg::BN + (half > 0 ? Cfg::BN / 2 : 0);
+      const int nck = half < 0 ? Cfg::NCHUNK : Cfg::NCHUNK / 2;
       const int slot = iter % Cfg::NSLOT;
       const int row = (mb * MC + static_cast<int>(pair)) * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 +
                       static_cast<int>(lane);
       const bool row_ok = row < shape.M;
       const typename Epi::Params& epg = t >= group_units ? ep2 : ep;
-      Epi::prefetch(epg, st, row, row_ok, nb * Cfg::BN + c_begin * 32, (t % group_units) / mn_tiles);
+      Epi::prefetch(epg, st, row, row_ok, col_base + c_begin * 32, (t % group_units) / mn_tiles);
       uint64_t* tempty = &tempty_bar[Cfg::OVERLAP ? 0 : slot];
       // overlapping slots: the chunk shared with the other slot (last chunk of
       // slot 0, first of slot 1) gates the next tile's MMAs. Only the part that
@@ -584,9 +618,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
 #pragma unroll(Epi::kUnroll ? Cfg::CPW : 1)
       for (int ci = 0; ci < Cfg::CPW; ++ci) {
         const int c = rotate ? (ci == 0 ? Cfg::NCHUNK - 1 : c_begin + ci - 1) : c_begin + ci;
-        const int col0 = nb * Cfg::BN + c * 32;
+        const int col0 = col_base + c * 32;
+        const bool cvalid = c < nck && col0 < shape.N;  // uniform across the warp
         uint32_t r[32];
-        if (col0 < shape.N) {  // uniform across the warp
+        if (cvalid) {
           if constexpr (S24_PIPE_PROBE == 3) {  // experiment: no accumulator reads
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] = static_cast<uint32_t>(i + c) * 0x3F800000u;
@@ -604,7 +639,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           else
             mbar_arrive_remote(tempty, leader_rank);
         }
-        if (col0 < shape.N) {
+        if (cvalid) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -629,8 +664,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       uint32_t phase = 0;
       long long it = 0;
       for (int iter = 0;; ++iter) {
-        const int t = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
-        if (t >= total_tiles) break;
+        const int u = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
+        if (u >= total_units) break;
+        int half;
+        const int t = unit_tile(u, half);
         int mb, nb, kb0, kb1;
         tile_coords(shape, t % mn_tiles, mb, nb);
         kb_range(t, kb0, kb1);

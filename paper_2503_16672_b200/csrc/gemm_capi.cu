@@ -243,6 +243,15 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   // are lost before all N tiles of their row have read them)
   sh.b_keep = static_cast<long long>(K) * N * Cfg::EB * sh.groups <= (40ll << 20);
   sh.a_stream = sh.b_keep && sh.group_m * sh.tiles_n <= clusters;
+  // a partial last wave of at most half the clusters: its tiles run as two
+  // N-halves each, so that wave takes half as long (dynamic scheduler only)
+  sh.tail_split = 0;
+  if constexpr (Cfg::HALF_OK) {
+    const int rem = tiles % clusters;
+    const char* e = std::getenv("S24_TAIL_SPLIT");
+    if (sh.sched && !fs && !bg && tiles > clusters && rem > 0 && 2 * rem <= clusters && !(e && e[0] == '0'))
+      sh.tail_split = rem;
+  }
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CLUSTER));
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, ma2, mb2, me2, sh, ep, second ? second->ep : ep);
   if (e != cudaSuccess) return fail(S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));

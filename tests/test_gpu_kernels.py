@@ -173,11 +173,16 @@ def test_spmm_vs_decompressed(b_mn, M, N, K):
     assert rel_err(D, ref) < 1e-5
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 256, 512), (600, 384, 1024)])
-def test_spmm_pair_matches_two_launches(M, N, K):
+@pytest.mark.parametrize("M,N,K", [(256, 256, 512), (600, 384, 1024), (2600, 2048, 256), (2600, 1920, 256)])
+@pytest.mark.parametrize("tail", ["1", "0"])
+def test_spmm_pair_matches_two_launches(monkeypatch, M, N, K, tail):
     """The grouped launch (two problems, one tile schedule) is bit-identical to
-    two s24_spmm calls, including row maps and the transposed write."""
+    two s24_spmm calls, including row maps and the transposed write. The
+    larger shapes leave a partial last wave of <= 74 / 2 tiles, which runs as
+    N-half units (GemmShape::tail_split) unless S24_TAIL_SPLIT=0; the
+    references always run without it."""
     torch.manual_seed(7)
+    monkeypatch.setenv("S24_TAIL_SPLIT", "0")
     ops = []
     for _ in range(2):
         a = torch.randn(M, K, device="cuda").bfloat16()
@@ -189,11 +194,21 @@ def test_spmm_pair_matches_two_launches(M, N, K):
     (v0, e0, b0), (v1, e1, b1) = ops
     _lib.call("s24_spmm", P(v0), P(e0), P(b0), 1, N, M, N, K, P(ref0), F32, N, P(rmap), 0, -1, None, 0, S())
     _lib.call("s24_spmm", P(v1), P(e1), P(b1), 1, N, M, N, K, P(ref1), F32, M + 40, P(rmap), 1, -1, None, 0, S())
+    torch.cuda.synchronize()
+    monkeypatch.setenv("S24_TAIL_SPLIT", tail)
     out0, out1 = torch.zeros_like(ref0), torch.zeros_like(ref1)
     _lib.call("s24_spmm_pair", 1, M, N, K, F32, P(v0), P(e0), P(b0), N, P(out0), N, P(rmap), 0, None,
               P(v1), P(e1), P(b1), N, P(out1), M + 40, P(rmap), 1, None, 0, S())
     assert torch.equal(out0, ref0) and torch.equal(out1, ref1)
     assert out0.abs().sum() > 0 and out1.abs().sum() > 0
+    # single launches with the tail split (bf16 out, no row map) vs without
+    outs = []
+    for tl in ("0", tail):
+        monkeypatch.setenv("S24_TAIL_SPLIT", tl)
+        o = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        _lib.call("s24_spmm", P(v0), P(e0), P(b0), 1, N, M, N, K, P(o), BF16, N, None, 0, -1, None, 0, S())
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
 
 
 def test_decompress_roundtrip():
