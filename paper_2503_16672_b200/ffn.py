@@ -118,6 +118,9 @@ WGRAD_OVERLAP = os.environ.get("S24_WGRAD_OVERLAP", "0") == "1"
 # over the whole activation, and the overlapped gathers slow K1 / K3 more than
 # the serialized ones cost), so opt-in.
 TOKEN_ORDER_STORAGE = os.environ.get("S24_TOKEN_ORDER", "0") == "1"
+# Side-stream start in the forward: right after K1 ("0": K4(act) co-runs with
+# fwd.out, a 2:4 GEMM) or after fwd.out ("1": K4(act) co-runs with K3, dense).
+K4_AFTER_FWD_OUT = os.environ.get("S24_K4_LATE", "0") == "1"
 
 
 def _dual_k4() -> bool:
@@ -539,8 +542,11 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
 
     if side is not None:
         main = torch.cuda.current_stream()
-        side.wait_stream(main)  # K1's outputs are ready; the side work must not wait for fwd.out
+        if not K4_AFTER_FWD_OUT:
+            side.wait_stream(main)  # K1's outputs are ready; the side work must not wait for fwd.out
         fwd_out(s)
+        if K4_AFTER_FWD_OUT:
+            side.wait_stream(main)
         if need_plan or plan is not None:
             plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid, side)
         bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)

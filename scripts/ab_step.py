@@ -38,6 +38,7 @@ VARIANTS = {
     "wgrad_overlap_graph": {"WGRAD_OVERLAP": True, "_graph": True},
     "k4_gemm_graph": {"K4_MODE": "gemm", "_graph": True},
     "frame_gather_graph": {"TOKEN_ORDER_STORAGE": False, "_graph": True},
+    "k4_late_graph": {"K4_AFTER_FWD_OUT": True, "_graph": True},
 }
 
 
