@@ -88,6 +88,10 @@ SIDE_GATHERS = os.environ.get("S24_SIDE_GATHERS", "1") == "1"
 # K1 / K3 read x / dY unpermuted and apply the permutation as an epilogue row
 # map ("1"), or read the gathered copies x_in / g_c ("0").
 ROWMAP_GEMMS = os.environ.get("S24_ROWMAP", "0") == "1"
+# K3 alone row-mapped (dY read as is; its epilogue reads / writes the act and
+# g_pre rows perm[r] with whole-sector stores): the g_c gather leaves the
+# critical path for the side stream (dW2's B operand only)
+ROWMAP_K3 = os.environ.get("S24_ROWMAP_K3", os.environ.get("S24_ROWMAP", "0")) == "1"
 # Feature-wise split in the paired layout: the dense features travel inside
 # the 2:4 weight-gradient operand as fixed-selector row pairs, so no dense
 # remainder GEMM / split-K reduction runs ("1"); "0": separate dense operand.
@@ -800,7 +804,7 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
     side = side_stream(dev) if K4_MODE == "side" else None
     g_c = _frame_rows(g_out, npad, cache.inv_dev, defer=True)
     g_ready = None
-    rowmap = ROWMAP_GEMMS and g_fw is None
+    rowmap = ROWMAP_K3 and g_fw is None
     stored = cache.row_frame is not None  # token-order storage: K3 / dX need no frame rows
     if stored and (side is None or g_fw is not None or not cfg.mask_grad_with_fwd):
         raise StateError("token-order storage needs the side-stream backward with mask_grad_with_fwd")

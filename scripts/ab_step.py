@@ -39,6 +39,8 @@ VARIANTS = {
     "k4_gemm_graph": {"K4_MODE": "gemm", "_graph": True},
     "frame_gather_graph": {"TOKEN_ORDER_STORAGE": False, "_graph": True},
     "k4_late_graph": {"K4_AFTER_FWD_OUT": True, "_graph": True},
+    "rowmap_k3_graph": {"ROWMAP_K3": True, "_graph": True},
+    "rowmap_graph": {"ROWMAP_GEMMS": True, "ROWMAP_K3": True, "_graph": True},
 }
 
 
