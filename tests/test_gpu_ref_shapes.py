@@ -287,3 +287,31 @@ def test_grad_bucket_and_hook_at_padded_shape():
     assert grads.d_w1.data_ptr() == bucket.data_ptr()
     assert torch.equal(grads.d_w1, ref.d_w1) and torch.equal(grads.d_w2, ref.d_w2)
     assert torch.equal(grads.d_x, ref.d_x)
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_graph_and_module_at_padded_shape(fp8):
+    """FfnStepGraph replay == eager, and the nn.Module runs, at d = 48, h = 200
+    (the padded path inside a captured step and under autograd)."""
+    from dataclasses import replace
+
+    n, d, h = 64, 48, 200
+    cfg = replace(s24.RECIPE, fp8_emulation=fp8, fp8_backward=fp8)
+    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.8, seed=31)
+    p = params(w1, w2)
+    g = s24.FfnStepGraph(p, cfg, n)
+    tx, tg = t(x).bfloat16(), t(dy).bfloat16()
+    out, cache = s24.ffn_forward(tx, p, cfg)
+    gr = s24.ffn_backward(tg, cache, p, cfg)
+    g.x.copy_(tx)
+    g.dy.copy_(tg)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(g.out, out)
+    assert torch.equal(g.d_x, gr.d_x) and torch.equal(g.d_w1, gr.d_w1) and torch.equal(g.d_w2, gr.d_w2)
+    layer = s24.SquaredReluFFN24(d, h, cfg=cfg)
+    xin = torch.randn(2, 30, d, device="cuda", requires_grad=True)
+    y = layer(xin)
+    y.float().pow(2).mean().backward()
+    assert y.shape == xin.shape and layer.w1.grad.shape == (d, h)
+    assert bool(torch.isfinite(layer.w1.grad).all()) and bool(torch.isfinite(xin.grad).all())
