@@ -242,9 +242,11 @@ struct EpiFwd1T {
     float a[32];
     uint32_t nz = 0;
 #pragma unroll
+    // (rows >= M: TMA zero-fills the A rows, so acc = 0 and a = 0 there; the
+    // F8 row scale is 0 for them as well)
     for (int i = 0; i < 32; ++i) {
       const float r = fmaxf(v[i], 0.f);
-      a[i] = row_ok ? __fmul_rn(r, r) : 0.f;
+      a[i] = __fmul_rn(r, r);
       nz |= (a[i] != 0.f ? 1u : 0u) << i;
     }
     // per-feature counts over the warp's 32 rows: transpose the nonzero bit
