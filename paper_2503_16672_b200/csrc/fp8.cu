@@ -215,66 +215,72 @@ __global__ void __launch_bounds__(256) k_col_amax(const InT* __restrict__ in, lo
   if (blockIdx.x * 256 + c < C && x > 0.f) atomicMax(amax + blockIdx.x * 256 + c, __float_as_uint(x));
 }
 
-// codes_t[c, r] = e4m3(in[r, c] / scale[c]); 64 x 64 tiles through shared
-// memory so both the bf16 reads and the code writes are row-contiguous.
+// codes_t[c, r] = e4m3(in[r, c] / scale[c]). A block transposes a 256-row x
+// 64-column tile through shared memory. Each thread quantizes two 4-row x
+// 8-column units (eight lanes read one row's 64 columns contiguously) and packs
+// each column's 4 row codes into one 32-bit word, so the transpose costs 8 word
+// stores per unit (2-way bank conflicts with the 65-word row pitch) instead of
+// 32 byte stores; the tile is then written out as 256-byte runs per output row
+// (16 lanes x 16 bytes). Every thread has all of its global loads in flight
+// before it converts (8 x 16 B for bf16).
 template <typename InT>
 __global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in, long long ld, int R,
                                                       int C, const unsigned* __restrict__ amax,
                                                       uint8_t* __restrict__ out, long long ld_out,
                                                       float* __restrict__ scales) {
-  __shared__ uint8_t tile[64][64 + 16];
-  __shared__ float sc[64], rc[64];
-  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  constexpr int kTR = 256, kTC = 64, kPitch = kTR / 4 + 1;  // tile rows, tile columns, words per tile row
+  __shared__ uint32_t tile[kTC * kPitch];
+  __shared__ float sc[kTC], rc[kTC];
+  const int r0 = blockIdx.y * kTR, c0 = blockIdx.x * kTC;
   const int t = threadIdx.x;
-  if (t < 64) {
+  if (t < kTC) {
     const float s = (c0 + t < C) ? e4m3_scale(__uint_as_float(amax[c0 + t])) : 1.f;
     sc[t] = s;
     rc[t] = rcp_rn(s);
     if (blockIdx.y == 0 && c0 + t < C) scales[c0 + t] = s;
   }
-  __syncthreads();
-  {
-    const int rr = t >> 2, cc = (t & 3) * 16;  // one row, 16 columns
-    const int r = r0 + rr;
-    float v[16];
-    if (r < R && c0 + cc + 16 <= C) {
-      float a[8], b[8];
-      load8(in + static_cast<long long>(r) * ld + c0 + cc, a);
-      load8(in + static_cast<long long>(r) * ld + c0 + cc + 8, b);
+  const int col8 = t & 7, row4 = t >> 3;  // unit: columns 8*col8.., rows 4*row4 (+128 for the second unit)
+  const int cb = c0 + 8 * col8;
+  float v[2][4][8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = a[i];
-        v[8 + i] = b[i];
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = r0 + 128 * u + 4 * row4 + k;
+      const InT* src = in + static_cast<long long>(r) * ld + cb;
+      if (r < R && cb + 8 <= C) {
+        load8(src, v[u][k]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[u][k][i] = (r < R && cb + i < C) ? ld1(src + i) : 0.f;
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        v[i] = (r < R && c0 + cc + i < C) ? ld1(in + static_cast<long long>(r) * ld + c0 + cc + i) : 0.f;
     }
+  __syncthreads();  // sc / rc
 #pragma unroll
-    for (int i = 0; i < 16; i += 2) {
-      Divisor d0{0.f}, d1{0.f};
-      d0.s = sc[cc + i];
-      d0.r = rc[cc + i];
-      d1.s = sc[cc + i + 1];
-      d1.r = rc[cc + i + 1];
-      const uint32_t q = e4m3x2(d0.div(v[i]), d1.div(v[i + 1]));
-      tile[cc + i][rr] = static_cast<uint8_t>(q & 0xFFu);
-      tile[cc + i + 1][rr] = static_cast<uint8_t>(q >> 8);
+  for (int i = 0; i < 8; ++i) {
+    Divisor dv{0.f};
+    dv.s = sc[8 * col8 + i];
+    dv.r = rc[8 * col8 + i];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t lo = e4m3x2(dv.div(v[u][0][i]), dv.div(v[u][1][i]));
+      const uint32_t hi = e4m3x2(dv.div(v[u][2][i]), dv.div(v[u][3][i]));
+      tile[(8 * col8 + i) * kPitch + 32 * u + row4] = lo | (hi << 16);
     }
   }
   __syncthreads();
-  {
-    const int cc = t >> 2, rr = (t & 3) * 16;  // one output row (column c), 16 codes
-    const int c = c0 + cc, r = r0 + rr;
-    if (c < C) {
-      uint8_t* dst = out + static_cast<long long>(c) * ld_out + r;
-      if (r + 16 <= R) {
-        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(&tile[cc][rr]);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(s32[0], s32[1], s32[2], s32[3]);
-      } else {
-        for (int i = 0; i < 16 && r + i < R; ++i) dst[i] = tile[cc][rr + i];
-      }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int q = t + 256 * m;
+    const int cc = q >> 4, w = (q & 15) * 4;  // output row c0 + cc, codes 4w .. 4w + 15
+    const int c = c0 + cc, r = r0 + 4 * w;
+    if (c >= C || r >= R) continue;
+    const uint32_t* s32 = tile + cc * kPitch + w;
+    uint8_t* dst = out + static_cast<long long>(c) * ld_out + r;
+    if (r + 16 <= R) {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(s32[0], s32[1], s32[2], s32[3]);
+    } else {
+      for (int i = 0; i < 16 && r + i < R; ++i) dst[i] = static_cast<uint8_t>(s32[i >> 2] >> (8 * (i & 3)));
     }
   }
 }
@@ -365,7 +371,7 @@ int s24_fp8_quant_cols_t(const void* in, int in_dtype, int64_t rows, int64_t col
     int rc = check_launch("k_col_amax");
     if (rc) return rc;
   }
-  dim3 g2(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(rows > 0 ? (rows + 63) / 64 : 1));
+  dim3 g2(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(rows > 0 ? (rows + 255) / 256 : 1));
   if (in_dtype == S24_F32)
     k_quant_cols_t<float><<<g2, 256, 0, st>>>(static_cast<const float*>(in), ld_in, static_cast<int>(rows),
                                               static_cast<int>(cols), amax_ws, codes_t, ld_out, scales);
