@@ -194,7 +194,17 @@ __global__ void __launch_bounds__(256) k_col_amax(const InT* __restrict__ in, lo
   const int re = min(R, rb + rows_per_block);
   float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 + 8 <= C) {
-    for (int r = rb + ty; r < re; r += 8) {
+    int r = rb + ty;
+    for (; r + 24 < re; r += 32) {  // four independent loads in flight
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load8(in + static_cast<long long>(r + 8 * u) * ld + c0, v[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], fabsf(v[u][i]));
+    }
+    for (; r < re; r += 8) {
       float v[8];
       load8(in + static_cast<long long>(r) * ld + c0, v);
 #pragma unroll
@@ -297,6 +307,27 @@ __global__ void __launch_bounds__(256) k_meta_to_f8(const uint16_t* __restrict__
   }
 }
 
+// The same conversion, 16-byte vectors. Rows r and r + 8 of an atom (m1 = 0/1)
+// read the same two 16-byte chunks of the source (byte 16 m0 + 256 m2, and
+// +128 for the odd halfwords q), so one thread loads both chunks and writes
+// both rows' 16 bytes: its halfword q of row m1 is chunk (q & 1)'s halfword
+// m1 + 2 (q >> 1). Needs 16-byte aligned buffers.
+__global__ void __launch_bounds__(256) k_meta_to_f8_v(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                      long long atoms) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < atoms * 64;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long atom = i >> 6;
+    const uint32_t j = static_cast<uint32_t>(i & 63), m0 = j & 7u, m2 = j >> 3;
+    const uint4* s = src + atom * 128 + m0 + 16 * m2;  // chunk A (16 B units); chunk B = A + 8
+    const uint4 a = s[0], b = s[8];
+    uint4* d = dst + atom * 128 + m0 + 16 * m2;  // row m0 + 16 m2 (m1 = 0); row + 8 at d + 8
+    d[0] = make_uint4(__byte_perm(a.x, b.x, 0x5410), __byte_perm(a.y, b.y, 0x5410), __byte_perm(a.z, b.z, 0x5410),
+                      __byte_perm(a.w, b.w, 0x5410));
+    d[8] = make_uint4(__byte_perm(a.x, b.x, 0x7632), __byte_perm(a.y, b.y, 0x7632), __byte_perm(a.z, b.z, 0x7632),
+                      __byte_perm(a.w, b.w, 0x7632));
+  }
+}
+
 __global__ void k_e4m3_encode(const float* __restrict__ x, long long n, uint8_t* __restrict__ codes) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -386,8 +417,12 @@ int s24_meta_hw_to_f8(const uint8_t* meta_hw, int64_t rows, int64_t kdim, uint8_
   if (rows < 0 || kdim < 0 || kdim % 128) return fail(S24_ERR_DIMENSION, "metadata K must be a multiple of 128");
   const long long bytes = (rows + 127) / 128 * 128 * kdim / 8;
   if (bytes == 0) return S24_OK;
-  k_meta_to_f8<<<grid_for(bytes / 2, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const uint16_t*>(meta_hw), reinterpret_cast<uint16_t*>(meta_f8), bytes / 2);
+  if ((reinterpret_cast<uintptr_t>(meta_hw) | reinterpret_cast<uintptr_t>(meta_f8)) % 16 == 0)
+    k_meta_to_f8_v<<<grid_for(bytes / 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const uint4*>(meta_hw), reinterpret_cast<uint4*>(meta_f8), bytes / 2048);
+  else
+    k_meta_to_f8<<<grid_for(bytes / 2, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const uint16_t*>(meta_hw), reinterpret_cast<uint16_t*>(meta_f8), bytes / 2);
   return check_launch("k_meta_to_f8");
 }
 

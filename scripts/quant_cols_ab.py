@@ -66,3 +66,28 @@ for R, C, dt in shapes[:3] + [(16384, 4096, torch.float32)]:
     med = [sorted(t)[len(t) // 2] for t in ts]
     gb = (R * C * a.element_size() * 2 + R * C) / 1e9  # amax pass + quant pass reads, code writes
     print(f"{R}x{C} {dt}: A {med[0]:.1f} us  B {med[1]:.1f} us  (B: {gb / med[1] * 1e6:.0f} GB/s over 2 reads + write)")
+
+# metadata layout conversion: bitwise and timed (c2 activation: 16384 x 8192)
+for lb in libs:
+    lb.s24_meta_hw_to_f8.restype = ctypes.c_int
+    lb.s24_meta_hw_to_f8.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+M, K = 16384, 8192
+src = torch.randint(0, 256, (M * K // 8,), dtype=torch.uint8, device=dev)
+outs = [torch.zeros_like(src) for _ in libs]
+for lb, o in zip(libs, outs):
+    assert lb.s24_meta_hw_to_f8(src.data_ptr(), M, K, o.data_ptr(), torch.cuda.current_stream().cuda_stream) == 0
+torch.cuda.synchronize()
+print("meta bitwise:", "ok" if torch.equal(outs[0], outs[1]) else "MISMATCH")
+ts = [[], []]
+for it in range(40):
+    k = it % 2
+    flush.zero_()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    libs[k].s24_meta_hw_to_f8(src.data_ptr(), M, K, outs[k].data_ptr(), torch.cuda.current_stream().cuda_stream)
+    e.record()
+    torch.cuda.synchronize()
+    if it >= 4:
+        ts[k].append(s.elapsed_time(e) * 1e3)
+med = [sorted(t)[len(t) // 2] for t in ts]
+print(f"meta {M}x{K}: A {med[0]:.1f} us  B {med[1]:.1f} us  (B: {2 * src.numel() / med[1] / 1e3:.0f} GB/s)")

@@ -276,3 +276,25 @@ def test_spmm_pair_f8_matches_two_launches():
               None, P(c1), P(e1), P(b1), K, P(sa1), P(sb1), P(outs[1]), M + 16, P(rmap), 1, None, 64, S())
     assert torch.equal(outs[0], refs[0]) and torch.equal(outs[1], refs[1])
     assert outs[0].abs().sum() > 0 and outs[1].abs().sum() > 0
+
+
+@pytest.mark.parametrize("M,K,offset", [(128, 128, 0), (300, 512, 0), (256, 256, 2)])
+def test_meta_to_f8_layout_bitwise(M, K, offset):
+    """s24_meta_hw_to_f8 against the atom map restated here: f8 halfword 8 r + q
+    of an atom = kind::f16 halfword at byte 2 m1 + 4 k2 + 16 m0 + 128 k1 + 256 m2
+    (r = m0 + 8 m1 + 16 m2, q = k1 + 2 k2). offset != 0 runs the unaligned
+    (halfword) kernel, offset 0 the 16-byte vector kernel."""
+    nb = _lib.meta_hw_bytes(M, K)
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    src_buf = torch.randint(0, 256, (nb + offset,), dtype=torch.uint8, device="cuda", generator=g)
+    dst_buf = torch.zeros(nb + offset, dtype=torch.uint8, device="cuda")
+    src, dst = src_buf[offset:], dst_buf[offset:]
+    _lib.call("s24_meta_hw_to_f8", P(src), M, K, P(dst), S())
+    torch.cuda.synchronize()
+    r = np.arange(128)[:, None]
+    q = np.arange(8)[None, :]
+    byte = 2 * ((r >> 3) & 1) + 4 * (q >> 1) + 16 * (r & 7) + 128 * (q & 1) + 256 * (r >> 4)
+    hw = src.cpu().numpy().view(np.uint16).reshape(-1, 1024)
+    want = hw[:, (byte // 2).reshape(-1)]
+    got = dst.cpu().numpy().view(np.uint16).reshape(-1, 1024)
+    assert np.array_equal(got, want)
