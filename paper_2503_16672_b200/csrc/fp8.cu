@@ -225,20 +225,21 @@ __global__ void __launch_bounds__(256) k_col_amax(const InT* __restrict__ in, lo
   if (blockIdx.x * 256 + c < C && x > 0.f) atomicMax(amax + blockIdx.x * 256 + c, __float_as_uint(x));
 }
 
-// codes_t[c, r] = e4m3(in[r, c] / scale[c]). A block transposes a 256-row x
-// 64-column tile through shared memory. Each thread quantizes two 4-row x
+// codes_t[c, r] = e4m3(in[r, c] / scale[c]). A block transposes a (128 U)-row
+// x 64-column tile through shared memory. Each thread quantizes U 4-row x
 // 8-column units (eight lanes read one row's 64 columns contiguously) and packs
 // each column's 4 row codes into one 32-bit word, so the transpose costs 8 word
-// stores per unit (2-way bank conflicts with the 65-word row pitch) instead of
-// 32 byte stores; the tile is then written out as 256-byte runs per output row
-// (16 lanes x 16 bytes). Every thread has all of its global loads in flight
-// before it converts (8 x 16 B for bf16).
-template <typename InT>
+// stores per unit (2-way bank conflicts with the odd row pitch) instead of 32
+// byte stores; the tile is then written out as (128 U)-byte runs per output row.
+// Every thread has all of its global loads in flight before it converts. U = 1
+// (48 registers, 5 CTAs/SM): 29.9 us for the c2 g_c operand vs 38.4 us at U = 2
+// (80 registers) and 43.7 us for the earlier 64 x 64 byte-transpose (ncu).
+template <typename InT, int U = 1>
 __global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in, long long ld, int R,
                                                       int C, const unsigned* __restrict__ amax,
                                                       uint8_t* __restrict__ out, long long ld_out,
                                                       float* __restrict__ scales) {
-  constexpr int kTR = 256, kTC = 64, kPitch = kTR / 4 + 1;  // tile rows, tile columns, words per tile row
+  constexpr int kTR = 128 * U, kTC = 64, kPitch = kTR / 4 + 1;  // tile rows, tile columns, words per tile row
   __shared__ uint32_t tile[kTC * kPitch];
   __shared__ float sc[kTC], rc[kTC];
   const int r0 = blockIdx.y * kTR, c0 = blockIdx.x * kTC;
@@ -251,9 +252,9 @@ __global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in
   }
   const int col8 = t & 7, row4 = t >> 3;  // unit: columns 8*col8.., rows 4*row4 (+128 for the second unit)
   const int cb = c0 + 8 * col8;
-  float v[2][4][8];
+  float v[U][4][8];
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < U; ++u)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int r = r0 + 128 * u + 4 * row4 + k;
@@ -272,17 +273,18 @@ __global__ void __launch_bounds__(256) k_quant_cols_t(const InT* __restrict__ in
     dv.s = sc[8 * col8 + i];
     dv.r = rc[8 * col8 + i];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t lo = e4m3x2(dv.div(v[u][0][i]), dv.div(v[u][1][i]));
       const uint32_t hi = e4m3x2(dv.div(v[u][2][i]), dv.div(v[u][3][i]));
       tile[(8 * col8 + i) * kPitch + 32 * u + row4] = lo | (hi << 16);
     }
   }
   __syncthreads();
+  constexpr int kChunks = kTR / 16;  // 16-code chunks per output row
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < 2 * U; ++m) {
     const int q = t + 256 * m;
-    const int cc = q >> 4, w = (q & 15) * 4;  // output row c0 + cc, codes 4w .. 4w + 15
+    const int cc = q / kChunks, w = (q % kChunks) * 4;  // output row c0 + cc, codes 4w .. 4w + 15
     const int c = c0 + cc, r = r0 + 4 * w;
     if (c >= C || r >= R) continue;
     const uint32_t* s32 = tile + cc * kPitch + w;
@@ -402,7 +404,7 @@ int s24_fp8_quant_cols_t(const void* in, int in_dtype, int64_t rows, int64_t col
     int rc = check_launch("k_col_amax");
     if (rc) return rc;
   }
-  dim3 g2(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(rows > 0 ? (rows + 255) / 256 : 1));
+  dim3 g2(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>(rows > 0 ? (rows + 127) / 128 : 1));
   if (in_dtype == S24_F32)
     k_quant_cols_t<float><<<g2, 256, 0, st>>>(static_cast<const float*>(in), ld_in, static_cast<int>(rows),
                                               static_cast<int>(cols), amax_ws, codes_t, ld_out, scales);
