@@ -260,7 +260,8 @@ __global__ void k_meta_ref_to_hw(const uint8_t* __restrict__ ref, long long rows
 }
 
 // ---------------------------------------------------------------------------
-// K6: row gather, one warp per row, 16-byte vectors
+// K6: row gather, one warp per row, 16-byte vectors (eight in flight per lane;
+// the source is streamed once, so its loads are evict-first)
 __global__ void k_gather_rows(const uint8_t* __restrict__ in, long long rows, long long row_bytes,
                               long long ld_in, const int* __restrict__ src, uint8_t* __restrict__ out,
                               long long ld_out) {
@@ -270,7 +271,15 @@ __global__ void k_gather_rows(const uint8_t* __restrict__ in, long long rows, lo
   for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
     const uint4* s = reinterpret_cast<const uint4*>(in + (long long)src[r] * ld_in);
     uint4* d = reinterpret_cast<uint4*>(out + r * ld_out);
-    for (long long v = lane; v < vecs; v += 32) d[v] = s[v];
+    long long v = lane;
+    for (; v + 32 * 7 < vecs; v += 256) {  // eight 16-byte loads in flight per lane, then the stores
+      uint4 t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] = __ldcs(s + v + 32 * j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[v + 32 * j] = t[j];
+    }
+    for (; v < vecs; v += 32) d[v] = s[v];
   }
 }
 
