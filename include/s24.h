@@ -11,8 +11,13 @@
  *
  * Conventions
  *  - Every pointer argument is a DEVICE pointer unless stated; the caller owns
- *    all memory (including outputs and workspace) and the library never frees
- *    caller memory or keeps device allocations between calls.
+ *    all memory (including outputs and workspace). The library never frees
+ *    caller memory and holds no device memory of its own: the GEMMs distribute
+ *    their tiles with Blackwell cluster launch control (the hardware cancels
+ *    not-yet-started clusters of the same launch and a running cluster takes
+ *    their tiles), so no scheduler counters live between or across calls and
+ *    any launch may run concurrently with any other, captured in a CUDA graph
+ *    or not.
  *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
  *    it. Shape/argument validation happens on the host before any launch.
  *  - Return value: 0 (S24_OK) or an s24_status code; s24_last_error() returns
@@ -27,8 +32,9 @@
  *    Size = s24_meta_hw_bytes(rows, cols).
  *  - "ref metadata": uint8 [rows, cols/4, 2] positions (i0, i1), i0 < i1, the
  *    reference's Sparse24Matrix.meta (pkg/src/srelu24/sparse24.py:30-47).
- *  - Thread safety: re-entrant; no global mutable state besides a
- *    mutex-guarded cache of kernel attributes.
+ *  - Thread safety: re-entrant. Host-side state is limited to read-only,
+ *    once-initialised caches (kernel attributes, the SM count, the driver's
+ *    tensor-map encoder entry point); there is no device-side state.
  */
 #ifndef S24_H_
 #define S24_H_
@@ -135,34 +141,19 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
  * of rank s is row pair_rows + s (vs holds pad128(pair_rows + n_sparse) rows).
  * A 2:4 GEMM with the same pair_rows then yields the whole split product.
  * pair_rows = -1: dense features go to vd. */
-/* K4 for the hot path: the paired layout of s24_feature_split (pair_rows =
- * 2 * n_dense) for one or two token-wise operands sharing meta_hw (the
- * activation and g_pre of one FFN step; vals_b/vs_b/es_b NULL for one).
- * Metadata, selectors and output offsets are computed once for both.
- * a_nonneg = 1: operand a is relu^2 (>= 0, NaN-free); operand b is ranked by
- * magnitude with NaN last. No drop statistics. */
-int s24_feature_split_x(const void* vals_a, const void* vals_b, const uint8_t* meta_hw, int64_t n, int64_t h,
-                        const int* feat_pos, int64_t n_sparse, int64_t n_dense, void* vs_a, uint8_t* es_a, void* vs_b,
-                        uint8_t* es_b, int a_nonneg, const int* row_map, void* stream);
-/* (row_map, nullable int32 [n]: token j of the split reads row row_map[j] of
- * vals / meta_hw -- the split of a permuted token order without gathering) */
-
-/* K4 in the identity layout (coalesced in and out; the hot-path variant):
- * vs bf16 [pair_pad + h, n/2] + es hw metadata (rows pair_pad + h, K = n),
- * pair_pad = pad128(2 * n_dense). Rows [0, 2*n_dense): dense feature of rank
- * r as two fixed-selector 2:4 rows (2r: tokens 4j, 4j+1; 2r+1: 4j+2, 4j+3);
- * rows up to pair_pad: zero; row pair_pad + f: the feature-wise 2:4 of
- * feature f (every feature, in index order). One s24_spmm(_pair) with
- * pair_rows = 2*n_dense, a row map (dense rank / feature index) and
- * row_valid (skip the padding and the dense features' identity rows) then
- * yields the whole split product (splitgemm.py:55-81). stats as above. */
-int s24_feature_split_id(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
-                         int64_t n_dense, void* vs, uint8_t* es, unsigned long long* stats, int operand_nonneg,
-                         void* stream);
-
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
                       int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, void* vd,
                       unsigned long long* stats, int operand_nonneg, int64_t pair_rows, void* stream);
+
+/* K4 on the hot path: s24_feature_split in the paired layout (pair_rows =
+ * 2 * n_dense), without drop statistics, one warp per 16 features x 128
+ * tokens with the per-feature output offsets tabled in shared memory.
+ * operand_nonneg = 1 (the relu^2 activation) ranks raw values unless
+ * *nan_flag (nullable; K1's stats[2]) is non-zero, in which case values are
+ * ranked by magnitude with NaN last, as with operand_nonneg = 0. */
+int s24_feature_split_x(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
+                        int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, int operand_nonneg,
+                        const unsigned long long* nan_flag, void* stream);
 
 /* ---------------------------------------------------------------- GEMMs
  * Operand conventions: A is logically [M, K], B is logically [K, N].
@@ -206,55 +197,27 @@ int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype
                   const void* B1, int64_t ldb1, void* D1, int64_t ldd1, const int* d_row_map1, int d_transposed1,
                   const int* d_row_valid1, int64_t pair_rows, void* stream);
 
-/* s24_spmm whose CTAs also compute the paired-layout feature-wise split
- * (s24_feature_split_x) of the GEMM's own A operand -- the token-wise
- * compressed [M, K/2] values + hw metadata -- from the pipeline stages the
- * MMA consumes (no separate read of A). fs_n = pad128(M) tokens; outputs
- * vs / es as s24_feature_split_x. The fwd.out / bwd.d_x GEMM of the recipe
- * with the K4 of act / g_pre folded in. */
-int s24_spmm_fs(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
-                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-                int64_t d_rows_valid, const int* d_row_valid, int64_t fs_n, const int* fs_feat_pos,
-                int64_t fs_n_sparse, int64_t fs_n_dense, void* fs_vs, uint8_t* fs_es, int fs_nonneg, void* stream);
-
-/* s24_spmm plus a feature-wise split (the K4 job of s24_feature_split with
- * stats == NULL) run as background work by the GEMM's epilogue warps while
- * they wait for accumulators: the tensor-bound sparse GEMM hides the
- * ALU-bound split. k4_counter: one device int of workspace (reset here). */
-int s24_spmm_bg(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
-                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-                int64_t d_rows_valid, const int* d_row_valid, const void* k4_vals, const uint8_t* k4_meta,
-                int64_t k4_n, int64_t k4_h, const int* k4_feat_pos, int64_t k4_n_sparse, int64_t k4_n_dense,
-                void* k4_vs, uint8_t* k4_es, void* k4_vd, int* k4_counter, void* stream);
-
 /* K1: Y1 = X_in . W1 with the fused relu^2 + token-wise 2:4 epilogue
  * (ffn.py:305-329). x: [M, K] row-major; w1: [K, N] row-major (N = h,
- * N % 128 == 0). Outputs act_vals bf16 [M_pad128, N/2], act_meta hw, counts
- * int32[N] (+=, nullable), stats uint64[2] (+=), y_dbg fp32 [M, N] nullable.
- * Fused feature-wise split (fw_vals non-null): the feature-wise 2:4 selection
- * of the kept activation over groups of 4 consecutive tokens, for every
- * feature (sparse24.py:96-115 as used by splitgemm.py:72-76), written
- * transposed: fw_vals bf16 [N_pad128, fw_kdim/2] + fw_meta hw (rows = N
- * features, K = fw_kdim tokens, fw_kdim = M padded to 128), fw_counts uint64[N]
- * += nonzeros before | after << 32 per feature. row_map (nullable, not with
- * the fused feature-wise output): input row r is written as act row
- * row_map[r] (and y_dbg row row_map[r]) -- the token permutation applied in
- * the epilogue, so X is read unpermuted. */
+ * N % 128 == 0). Outputs act_vals bf16 [M_pad128, N/2], act_meta hw (padding
+ * rows up to M_pad128 written as zero groups), counts int32[N] (+=,
+ * nullable), stats uint64[3]: [0] += nonzeros before, [1] += nonzeros after
+ * the token-wise selection, [2] |= 1 when a kept value is NaN (the caller
+ * zeroes it); y_dbg fp32 [M, N] nullable (the pre-activation, for parity
+ * checks). Non-finite values follow the reference's numpy semantics: relu
+ * keeps NaN (ffn.py:167-169), NaN counts as nonzero (splitgemm.py:28-30) and
+ * ranks below zero in the top-2 (sparse24.py:72-77). */
 int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
                         int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
-                        float* y_dbg, void* fw_vals, uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim,
-                        const int* row_map, void* stream);
+                        float* y_dbg, void* stream);
 
 /* K3: G = dY_c . W2^T with the fused relu^2-derivative + forward-mask
  * epilogue (ffn.py:395-417, 440-443). g: [M, K=d] row-major; w2: [N=h, K=d]
  * row-major. act_vals/act_meta: from K1. Output g_vals bf16 [M_pad128, N/2]
- * on the same metadata; optional fused feature-wise split of g_pre exactly as
- * in s24_fwd_gemm1_fused. row_map (nullable): input row r pairs with act /
- * g_vals row row_map[r] (unpermuted dY against the permuted activation). */
+ * on the same metadata (compress_token_wise_with_mask, exact by
+ * construction). */
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
-                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* fw_vals,
-                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, const int* row_map,
-                       void* stream);
+                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* stream);
 
 /* dense-mode twins: act = bf16(relu(X W1)^2) [M, N] (w1 stored [K][N]) */
 int s24_gemm_relu2(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N, int64_t K,
@@ -314,7 +277,7 @@ int s24_fwd_gemm1_f8(const uint8_t* xq, int64_t ldx, const uint8_t* w1q, int64_t
                      int64_t K, const float* x_scale, const float* w1_scale, float* act_vals32, unsigned* row_amax,
                      uint8_t* act_meta, int* counts, unsigned long long* stats, float* y_dbg, void* stream);
 /* K3 on e4m3 operands (W2 codes as [N=h, K=d]): G = (sg * s2) * acc, then as
- * s24_bwd_dact_fused without the fused feature-wise output */
+ * s24_bwd_dact_fused */
 int s24_bwd_dact_f8(const uint8_t* gq, int64_t ldg, const uint8_t* w2q, int64_t ldw2, int64_t M, int64_t N,
                     int64_t K, const float* g_scale, const float* w2_scale, const void* act_vals,
                     const uint8_t* act_meta, void* g_vals, void* stream);

@@ -36,18 +36,14 @@ SIGNATURES: dict[str, list] = {
     "s24_meta_ref_to_hw": [P, I64, I64, P, P],
     "s24_gather_rows": [P, I64, I64, I64, P, P, I64, P],
     "s24_plan": [P, I64, I64, P, P, P, P],
-    "s24_feature_split_x": [P, P, P, I64, I64, P, I64, I64, P, P, P, P, INT, P, P],
-    "s24_feature_split_id": [P, P, I64, I64, P, I64, P, P, P, INT, P],
+    "s24_feature_split_x": [P, P, I64, I64, P, I64, I64, P, P, INT, P, P],
     "s24_feature_split": [P, P, I64, I64, P, I64, I64, P, P, P, P, INT, I64, P],
     "s24_gemm": [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],
     "s24_gemm_splitk": [P, INT, I64, P, INT, I64, I64, I64, I64, INT, P, P, INT, I64, P, INT, P],
     "s24_spmm": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, I64, P],
     "s24_spmm_pair": [INT, I64, I64, I64, INT, P, P, P, I64, P, I64, P, INT, P, P, P, P, I64, P, I64, P, INT, P, I64, P],
-    "s24_spmm_fs": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, I64, P, I64, I64, P, P, INT, P],
-    "s24_spmm_bg": [P, P, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P, P, I64, I64, P, I64, I64, P, P, P,
-                    P, P],
-    "s24_fwd_gemm1_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, P, P, I64, P, P],
-    "s24_bwd_dact_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P, I64, P, P],
+    "s24_fwd_gemm1_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P, P, P],
+    "s24_bwd_dact_fused": [P, I64, P, I64, I64, I64, I64, P, P, P, P],
     "s24_gemm_relu2": [P, I64, P, I64, I64, I64, I64, P, I64, P],
     "s24_gemm_dact": [P, I64, P, I64, I64, I64, I64, P, I64, P, I64, P],
     "s24_fp8_quant_rows": [P, INT, I64, I64, I64, P, I64, P, I64, P, P, I64, P, I64, P],

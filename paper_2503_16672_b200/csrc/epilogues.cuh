@@ -52,9 +52,20 @@ __device__ __forceinline__ uint32_t keep_nibble(uint32_t kb) {
   return static_cast<uint32_t>(kKeepNibbleLut >> (4u * kb)) & 0xFu;
 }
 
-}  // namespace s24
-#include "fwsel.cuh"
-namespace s24 {
+// relu that keeps NaN (numpy's maximum(y, 0), ref ffn.py:167-169)
+__device__ __forceinline__ float relu_nan(float x) {
+  float r;
+  asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// any NaN among the 16 bf16 halves of 8 packed words (bf16 NaN: |bits| > 0x7F80)
+__device__ __forceinline__ bool any_nan_bf16x2(const uint32_t (&w)[8]) {
+  uint32_t t = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t |= (w[i] & 0x7FFF7FFFu) + 0x007F007Fu;
+  return (t & 0x80008000u) != 0u;
+}
 
 // 32x32 bit-matrix transpose across the warp: on return, bit l of lane i's
 // word is bit i of lane l's input word.
@@ -165,9 +176,14 @@ struct EpiStore {
 // of the pre-sparsify a (ref splitgemm.py:28-30, ffn.py:320-322) and the
 // nonzeros before/after totals (ref sparse24.py:60-69). The dense activation
 // never leaves registers. Optional debug dump of y (fp32) for parity tests.
-// Selection: with a >= 0, pairwise FSET masks b_ij (i < j: i beats j iff
-// a_i >= a_j, ties to the lower index); "kept iff it beats two of the other
-// three" is a bitwise majority; values are picked with bitwise selects.
+// Selection: pairwise FSET masks b_ij (i < j: i beats j iff k_i >= k_j, ties
+// to the lower index); "kept iff it beats two of the other three" is a
+// bitwise majority; values are picked with bitwise selects.
+// Non-finite values follow the reference's numpy semantics: relu keeps NaN
+// (np.maximum), NaN counts as a nonzero (np.count_nonzero) and ranks below
+// every number including zero (np.argsort puts NaN keys last): the selection
+// key is max(a, -1), which maps NaN to -1 and leaves a >= 0 unchanged. A kept
+// NaN raises stats[2] so that the feature-wise split ranks NaN-aware.
 // F8 (e4m3 K1, ref ffn.py:305 + :330-341): y = (row_scale[r] * col_scale[c]) * acc;
 // the kept values go out as fp32 (vals32) with a per-row running max of the
 // kept |a| (row_amax, float bits, atomicMax) for the per-token quantization
@@ -178,12 +194,9 @@ struct EpiFwd1T {
     __nv_bfloat16* vals;  // [Mpad, N/2]
     uint8_t* meta;        // hw layout, K = N
     int* counts;          // [N], accumulated (nullable)
-    unsigned long long* stats;  // [2] nnz before / after, accumulated
+    unsigned long long* stats;  // [3] nnz before / after, accumulated; [2] != 0: a kept value is NaN
     float* y_dbg;         // nullable [M, N]
     int N;
-    FwTarget fw;          // fused feature-wise selection (fw.vals == nullptr: off)
-    const int* row_map;   // nullable: input row r is written as output row row_map[r]
-                          // (the token permutation applied on the way out)
     const float* row_scale;  // F8 only
     const float* col_scale;
     float* vals32;           // F8 only: [Mpad, N/2]
@@ -191,16 +204,15 @@ struct EpiFwd1T {
   };
   struct State {
     unsigned long long before, after;
-    const uint2* lut;
-    int drow;             // destination row of this lane's row in the current tile
+    uint32_t nan_kept;
     uint32_t mq[4];       // metadata halfwords (k1 = 0 | k1 = 1 << 16) of the atom's chunks k2 = 0..3
   };
   static constexpr bool kUnroll = true;  // (mq is indexed by the chunk)
-  // Without a row map the warp's run of chunks covers whole 128-column
-  // metadata atoms (a multiple of 4 chunks starting at a multiple of 4): the
-  // 8 halfwords a row has in an atom are gathered across lane pairs (rows r,
-  // r ^ 8 interleave per 4-byte word) and written as one 16-byte store per
-  // lane, whole sectors, instead of two 2-byte stores per chunk.
+  // The warp's run of chunks covers whole 128-column metadata atoms (a
+  // multiple of 4 chunks starting at a multiple of 4): the 8 halfwords a row
+  // has in an atom are gathered across lane pairs (rows r, r ^ 8 interleave
+  // per 4-byte word) and written as one 16-byte store per lane, whole
+  // sectors, instead of two 2-byte stores per chunk.
   __device__ static void meta_flush(const Params& p, const State& s, int row, bool any_ok, int col0, uint32_t lane) {
     const bool hi = (lane & 8u) != 0u;  // m1 = 1: this lane writes the k1 = 1 half of the pair
     uint32_t w[4];
@@ -217,16 +229,16 @@ struct EpiFwd1T {
   }
   __device__ static void init(const Params&, State& s) {
     s.before = s.after = 0;
-    s.lut = fw_lut_init();
+    s.nan_kept = 0;
   }
-  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int, int) {
-    s.drow = (p.row_map && row_ok) ? __ldg(p.row_map + row) : row;
-  }
+  __device__ static void prefetch(const Params&, State&, int, bool, int, int) {}
   __device__ static void finish(const Params& p, State& s, uint32_t lane) {
     const unsigned long long b = warp_sum_u64(s.before), a = warp_sum_u64(s.after);
+    const bool nan_kept = __any_sync(0xffffffffu, s.nan_kept != 0u);
     if (lane == 0 && p.stats) {
       atomicAdd(p.stats, b);
       atomicAdd(p.stats + 1, a);
+      if (nan_kept) atomicOr(p.stats + 2, 1ull);
     }
   }
   __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int ci,
@@ -239,22 +251,20 @@ struct EpiFwd1T {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = v_in[i];
     }
-    float a[32];
+    float a[32], k[32];
     uint32_t nz = 0;
 #pragma unroll
     // (rows >= M: TMA zero-fills the A rows, so acc = 0 and a = 0 there; the
     // F8 row scale is 0 for them as well)
     for (int i = 0; i < 32; ++i) {
-      const float r = fmaxf(v[i], 0.f);
+      const float r = relu_nan(v[i]);
       a[i] = __fmul_rn(r, r);
+      k[i] = fmaxf(a[i], -1.f);
       nz |= (a[i] != 0.f ? 1u : 0u) << i;
     }
     // per-feature counts over the warp's 32 rows: transpose the nonzero bit
     // matrix so lane i holds column i, then popcount
-#ifndef S24_K1_PROBE
-#define S24_K1_PROBE 0  // experiment builds only: 1 = no counts, 2 = no stores
-#endif
-    if (S24_K1_PROBE != 1 && p.counts) {
+    if (p.counts) {
       const uint32_t col_bits = warp_bit_transpose(nz, lane);
       if (col_bits) atomicAdd(p.counts + col0 + lane, __popc(col_bits));
     }
@@ -264,14 +274,14 @@ struct EpiFwd1T {
     uint32_t keep32 = 0;
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
-      const float a0 = a[4 * g], a1 = a[4 * g + 1], a2 = a[4 * g + 2], a3 = a[4 * g + 3];
-      const uint32_t b01 = fge_mask(a0, a1), b02 = fge_mask(a0, a2), b03 = fge_mask(a0, a3);
-      const uint32_t b12 = fge_mask(a1, a2), b13 = fge_mask(a1, a3), b23 = fge_mask(a2, a3);
+      const float k0 = k[4 * g], k1 = k[4 * g + 1], k2 = k[4 * g + 2], k3 = k[4 * g + 3];
+      const uint32_t b01 = fge_mask(k0, k1), b02 = fge_mask(k0, k2), b03 = fge_mask(k0, k3);
+      const uint32_t b12 = fge_mask(k1, k2), b13 = fge_mask(k1, k3), b23 = fge_mask(k2, k3);
       const uint32_t K0 = maj3(b01, b02, b03), K1 = maj3(~b01, b12, b13);
       const uint32_t K2 = maj3(~b02, ~b12, b23), K3 = maj3(~b03, ~b13, ~b23);
       const uint32_t kb = (K0 & 1u) | (K1 & 2u) | (K2 & 4u) | (K3 & 8u);
-      const uint32_t u0 = __float_as_uint(a0), u1 = __float_as_uint(a1), u2 = __float_as_uint(a2),
-                     u3 = __float_as_uint(a3);
+      const uint32_t u0 = __float_as_uint(a[4 * g]), u1 = __float_as_uint(a[4 * g + 1]),
+                     u2 = __float_as_uint(a[4 * g + 2]), u3 = __float_as_uint(a[4 * g + 3]);
       const float v0 = __uint_as_float(bsel(K0, u0, bsel(K1, u1, u2)));  // first kept
       const float v1 = __uint_as_float(bsel(K3, u3, bsel(K2, u2, u1)));  // second kept
       if constexpr (F8) {
@@ -283,26 +293,15 @@ struct EpiFwd1T {
       m16[g >> 2] |= keep_nibble(kb) << (4 * (g & 3));
       keep32 |= kb << (4 * g);
     }
-    if constexpr (!F8) {
-      if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
-    }
-    const bool combine = p.row_map == nullptr;  // (warp-uniform)
-    if (combine) {
-      // padding rows inside the buffer (row >= M) get the (0, 1) selectors of
-      // an all-zero group, 0x4444: the value the host pre-fills them with
-      s.mq[ci & 3] = m16[0] | (m16[1] << 16);
-      if ((ci & 3) == 3) meta_flush(p, s, row, __any_sync(0xffffffffu, row_ok), col0 - 96, lane);
-    }
+    // padding rows inside the buffer (row >= M) get the (0, 1) selectors of
+    // an all-zero group, 0x4444: the value the host pre-fills them with
+    s.mq[ci & 3] = m16[0] | (m16[1] << 16);
+    if ((ci & 3) == 3) meta_flush(p, s, row, __any_sync(0xffffffffu, row_ok), col0 - 96, lane);
     if (!row_ok) return;
     s.before += __popc(nz);
     s.after += __popc(nz & keep32);
-    if (S24_K1_PROBE == 2) {
-      if (packed[0] == 0x12345678u && m16[0] == 77u) p.vals[0] = __float2bfloat16(1.f);  // keep the work alive
-      return;
-    }
-    const int drow = s.drow;
     if constexpr (F8) {
-      float* dst = p.vals32 + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
+      float* dst = p.vals32 + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
       float mx = 0.f;
 #pragma unroll
       for (int i = 0; i < 16; i += 8) {
@@ -313,18 +312,14 @@ struct EpiFwd1T {
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) mx = fmaxf(mx, kept[i]);
-      if (mx > 0.f) atomicMax(p.row_amax + drow, __float_as_uint(mx));  // a >= 0: uint order = float order
+      if (mx > 0.f) atomicMax(p.row_amax + row, __float_as_uint(mx));  // a >= 0: uint order = float order
     } else {
-      __nv_bfloat16* dst = p.vals + static_cast<long long>(drow) * (p.N / 2) + col0 / 2;
+      s.nan_kept |= any_nan_bf16x2(packed) ? 1u : 0u;
+      __nv_bfloat16* dst = p.vals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
       st_global_32b(dst, packed);
     }
-    if (!combine) {
-      uint16_t* mh = reinterpret_cast<uint16_t*>(p.meta);
-      st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16, p.N) / 2, static_cast<uint16_t>(m16[0]));
-      st_global_u16(mh + meta_hw_halfword_offset(drow, col0 / 16 + 1, p.N) / 2, static_cast<uint16_t>(m16[1]));
-    }
     if (p.y_dbg) {
-      float* y = p.y_dbg + static_cast<long long>(drow) * p.N + col0;
+      float* y = p.y_dbg + static_cast<long long>(row) * p.N + col0;
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
         st_global_v4(y + i, __float_as_uint(v[i]), __float_as_uint(v[i + 1]), __float_as_uint(v[i + 2]),
@@ -352,8 +347,6 @@ struct EpiBwd1T {
     const uint8_t* meta;            // hw layout, K = N
     __nv_bfloat16* gvals;           // [Mpad, N/2] out
     int N;
-    FwTarget fw;                    // fused feature-wise selection of g_pre (fw.vals == nullptr: off)
-    const int* row_map;             // nullable: input row r <-> act / g_pre row row_map[r]
     const float* row_scale;         // F8 only
     const float* col_scale;
   };
@@ -362,14 +355,10 @@ struct EpiBwd1T {
   struct State {
     uint4 act[2 * CPW];  // 8 kept values per uint4 = 16 logical columns
     uint4 meta[2];       // the row's two 16-byte metadata rows (k1 = 0, 1) of its atom
-    const uint2* lut;
-    int drow;            // act / g_pre row of this lane's input row
   };
-  __device__ static void init(const Params&, State& s) { s.lut = fw_lut_init(); }
+  __device__ static void init(const Params&, State&) {}
   __device__ static void finish(const Params&, State&, uint32_t) {}
-  __device__ static void prefetch(const Params& p, State& s, int row_in, bool row_ok, int col_first, int) {
-    const int row = (p.row_map && row_ok) ? __ldg(p.row_map + row_in) : row_in;
-    s.drow = row;
+  __device__ static void prefetch(const Params& p, State& s, int row, bool row_ok, int col_first, int) {
     if (!row_ok || col_first >= p.N) return;
     const uint4* a =
         reinterpret_cast<const uint4*>(p.act_vals + static_cast<long long>(row) * (p.N / 2) + col_first / 2);
@@ -384,23 +373,17 @@ struct EpiBwd1T {
   }
   __device__ static uint32_t word(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
   __device__ static void chunk(const Params& p, State& s, int row, bool row_ok, int col0, int ci,
-                               const float (&v_in)[32], uint32_t lane) {
+                               const float (&v_in)[32], uint32_t) {
+    if (!row_ok) return;
     float v[32];
     if constexpr (F8) {
-      const float sr = row_ok ? __ldg(p.row_scale + row) : 0.f;
+      const float sr = __ldg(p.row_scale + row);
       scale_chunk(p.col_scale + col0, sr, v_in, v);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = v_in[i];
     }
-    if (!row_ok) {
-      if (p.fw.vals) {
-        const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        fw_select_chunk(p.fw, zero, 0x44444444u, row, col0, lane, s.lut);
-      }
-      return;
-    }
-    const uint32_t m1 = (static_cast<uint32_t>(s.drow) >> 3) & 1u;
+    const uint32_t m1 = (static_cast<uint32_t>(row) >> 3) & 1u;
     // the chunk's two 16-column quads (k1 = 0, 1) sit in word k2 = ci of the atom rows
     const uint32_t w0 = word(s.meta[0], ci & 3), w1 = word(s.meta[1], ci & 3);
     const uint32_t m16[2] = {(w0 >> (16 * m1)) & 0xFFFFu, (w1 >> (16 * m1)) & 0xFFFFu};
@@ -415,8 +398,7 @@ struct EpiBwd1T {
       const float a0 = __uint_as_float(aw[g] << 16), a1 = __uint_as_float(aw[g] & 0xFFFF0000u);
       packed[g] = pack_bf16x2(g0 * (2.f * sqrt_approx(a0)), g1 * (2.f * sqrt_approx(a1)));
     }
-    if (p.fw.vals) fw_select_chunk(p.fw, packed, m16[0] | (m16[1] << 16), row, col0, lane, s.lut);
-    __nv_bfloat16* dst = p.gvals + static_cast<long long>(s.drow) * (p.N / 2) + col0 / 2;
+    __nv_bfloat16* dst = p.gvals + static_cast<long long>(row) * (p.N / 2) + col0 / 2;
     st_global_32b(dst, packed);
   }
 };
@@ -441,7 +423,7 @@ struct EpiRelu2 {
     float a[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const float r = fmaxf(v[i], 0.f);
+      const float r = relu_nan(v[i]);
       a[i] = __fmul_rn(r, r);
     }
     __nv_bfloat16* dst = p.act + static_cast<long long>(row) * p.ld + col0;

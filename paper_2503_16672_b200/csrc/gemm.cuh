@@ -16,11 +16,13 @@
 //   warp E+1 : MMA issuer (leader CTA, one thread): tcgen05.cp metadata
 //              smem->TMEM, tcgen05.mma(.sp), tcgen05.commit
 //   warp E+2 : TMEM allocator
-// MC = 2: clusters of two CTA pairs on vertically adjacent tiles (same N
-// columns). B is the operand both pairs read, so each CTA fetches half of its
-// B slice and TMA-multicasts it to its counterpart in the other pair: L2->SM
-// traffic per MAC drops by a third for 2:4 A (where B dominates the stage),
-// and stage slots are recycled only when both pairs' MMAs have released them.
+// Work distribution: the grid holds one cluster per work unit (tile, or
+// tile x K split, of one or two problems). Each cluster runs its own unit,
+// then keeps stealing units of clusters that have not started yet through
+// Blackwell's cluster launch control (clusterlaunchcontrol.try_cancel), so
+// the kernel behaves as a persistent one (one cluster per CTA pair of SMs,
+// units taken in launch order) with no device memory behind the scheduler:
+// launches are independent of each other, of streams and of graph replays.
 // The producer and MMA warps sit at the highest warp ids because the warp
 // arbiter prefers higher ids: busy epilogue warps must not delay MMA issue.
 // BN = 512 (dense, CTA pairs): each k-step issues two N = 256 MMAs (sub-tiles
@@ -41,17 +43,11 @@
 //   MN-major : boxes of 64 (M or N) elements x BK rows of K, box stride BK*128 B
 // Descriptors: K-major SBO = 1024; MN-major LBO = box stride, SBO = 1024.
 #pragma once
-#include "k4.cuh"
-#include "k4s.cuh"
 #include "meta.cuh"
 #include "ptx.cuh"
 
-// experiment-only pipeline probes (never set in the product build):
-//   S24_PIPE_PROBE=1 : no TMA (stages are released empty) -> MMA-issue bound
-//   S24_PIPE_PROBE=2 : no MMA (stages are consumed unread) -> operand-feed bound
-//   S24_PIPE_PROBE=3 : no TMEM reads in the epilogue (accumulator drain cost)
-#ifndef S24_PIPE_PROBE
-#define S24_PIPE_PROBE 0
+#ifndef S24_CLC_PREFETCH
+#define S24_CLC_PREFETCH 1
 #endif
 
 namespace s24 {
@@ -62,21 +58,14 @@ struct GemmShape {
   int group_m;          // raster: group_m M-tiles share one sweep over N
   int k_splits;         // >1: split-K, work unit = (tile, K range); partials go to the epilogue with ks
   int groups;           // 1 or 2 problems of this shape (second: tmA2/tmB2/tmE2, ep2), group-major units
-  int has_bg;           // 1: epilogue warps run K4 units (bg) while waiting for accumulators
   int a_stream;         // 1: A panels are not re-read after their raster group (L2 evict-first)
   int b_keep;           // 1: B is small enough to pin in L2 (evict-last)
-  int* sched;           // dynamic tile scheduler {next, done} (zero at launch, reset by the
-                        // last cluster), or nullptr: static round-robin units
-  K4Job bg;
   int tail_split;       // the last tail_split tiles (in unit order) run as two N-halves each
                         // (MN-major B only): a partial last wave of full tiles becomes a
                         // half-length one (see unit_tile)
-  int has_fs;           // 1: the K4 warps split this GEMM's own A stages (K4W > 0, k4s.cuh)
-  K4Args fs;            // their outputs (feat_pos, pair_rows, vs, es, n = padded tokens, h, nonneg)
 };
 
-template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8, int MC_ = 1,
-          bool F8_ = false, int K4W_ = 0>
+template <bool SPARSE_, bool A_MN_, bool B_MN_, int BN_, int STAGES_, int CG_, int EPI_WARPS_ = 8, bool F8_ = false>
 struct GemmCfg {
   static constexpr bool SPARSE = SPARSE_;
   // F8: e4m3 operands (tcgen05 kind::f8f6f4). Every stage and MMA step moves
@@ -116,22 +105,18 @@ struct GemmCfg {
   static_assert(TMEM_NEED <= 512, "TMEM budget");
   static_assert(!(SPARSE && A_MN), "sparse A must be K-major");
   static_assert(!(F8 && (A_MN || B_MN)), "e4m3 operands are K-major");
-  static_assert(BN_CTA % 64 == 0 && (BN <= 256 || (BN == 512 && !SPARSE && CG == 2 && MC_ == 1)), "BN");
+  static_assert(BN_CTA % 64 == 0 && (BN <= 256 || (BN == 512 && !SPARSE && CG == 2)), "BN");
   static_assert(CG == 1 || CG == 2, "CG");
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int SCHED_SLOTS = 4;  // work-unit broadcast ring (dynamic scheduler)
+  static constexpr int SCHED_SLOTS = 4;  // work-unit ring (cluster launch control responses)
+  // barriers: full/empty per stage, tfull/tempty per accumulator slot, the
+  // TMEM base word (+pad), sched_full/sched_empty per ring slot, then the
+  // 16-byte CLC responses (16-aligned: BAR_OFF is a multiple of 1024)
+  static constexpr uint32_t RESP_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 8 + 2 * SCHED_SLOTS * 8;
+  static constexpr uint32_t RESP_OFF16 = (RESP_OFF + 15) / 16 * 16;
   // the dynamic smem base is declared 1024-aligned (SWIZZLE_128B atoms), so no
-  // alignment slack is reserved: 7 dense stages fit next to a 2 KB static LUT
-  // K4W > 0: warps that split the A stages feature-wise (k4s.cuh); each stage
-  // then also waits for their release, and the peer CTA learns that a stage
-  // landed through its own k4_ready barrier (the TMA completes on the leader's)
-  static constexpr int K4W = K4W_;
-  // (each stage index must always be served by the same K4 warp, or a warp's
-  // parity wait could match the previous phase of a stage another warp uses)
-  static_assert(K4W == 0 || (SPARSE && !F8 && K4W % 4 == 0 && MC_ == 1 && STAGES_ % K4W == 0),
-                "K4 warps: bf16 2:4 configs, STAGES a multiple of K4W");
-  static constexpr uint32_t SMEM_BYTES =
-      BAR_OFF + (2 * STAGES + 4) * 8 + 16 + SCHED_SLOTS * 20 + (K4W > 0 ? 8 + STAGES * 8 : 0);
+  // alignment slack is reserved: 7 dense stages fit next to the static smem
+  static constexpr uint32_t SMEM_BYTES = RESP_OFF16 + 16 * SCHED_SLOTS;
   static constexpr uint32_t IDESC =
       F8 ? make_idesc_e4m3(TILE_M, MMA_N, SPARSE) : make_idesc_bf16(TILE_M, MMA_N, A_MN, B_MN, SPARSE);
   // half-width units (GemmShape::tail_split): N = BN / 2
@@ -141,20 +126,15 @@ struct GemmCfg {
   static constexpr int NCHUNK = BN / 32;
   static constexpr int EPI_WARPS = EPI_WARPS_;            // 4 or 8 (two warps per TMEM lane quarter)
   static constexpr int EPI_THREADS = 32 * EPI_WARPS;
-  static constexpr int THREADS = 128 + EPI_THREADS + 32 * K4W;
+  static constexpr int THREADS = 128 + EPI_THREADS;
   static constexpr int CPW = NCHUNK / (EPI_WARPS / 4);  // chunks per epilogue warp
   static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
   // 4-epilogue-warp configs cap registers at 128/thread so that an
-  // independent kernel (e.g. K4 on a side stream) can co-reside on the SM
-  static constexpr int MIN_BLOCKS = (EPI_WARPS == 4 && K4W == 0) ? 2 : 1;
-  // B multicast across MC CTA pairs (see header)
-  static constexpr int MC = MC_;
-  static constexpr int CLUSTER = CG * MC;
+  // independent kernel (K4 on the side stream) can co-reside on the SM
+  static constexpr int MIN_BLOCKS = EPI_WARPS == 4 ? 2 : 1;
+  static constexpr int CLUSTER = CG;
   static constexpr int B_KBOX = BK / BOX_K;  // K-major B: 128-byte K boxes per stage
-  // K-major B with fewer K boxes than pairs is split by rows instead
-  static constexpr int B_ROW_SPLIT = (!B_MN && B_KBOX % MC != 0) ? MC : 1;
-  static constexpr int B_BOX_ROWS = SUB_CTA / B_ROW_SPLIT;
-  static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast needs CTA pairs");
+  static constexpr int B_BOX_ROWS = SUB_CTA;
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& s, int t, int& mb, int& nb) {
@@ -182,10 +162,6 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 // whole raster group (shape.a_stream), the A panel of a tile row is consumed
 // by the clusters sweeping that row's N tiles at about the same time and then
 // never again: evict-first, so streaming A does not push B out of L2.
-// S24_L2_POLICY=0 disables both (experiments).
-#ifndef S24_L2_POLICY
-#define S24_L2_POLICY 1
-#endif
 
 // Epilogue contract: each epilogue warp owns one TMEM lane quarter (32 tile
 // rows) and a run of CPW consecutive 32-column chunks. Per chunk:
@@ -211,32 +187,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  // dynamic scheduling: the leader CTA's producer takes work units from a
-  // global counter and broadcasts them through this ring to its own MMA and
-  // epilogue warps (sched_full, local arrive) and to the peer CTA (st.async
-  // completing 4 tx bytes on the peer's sched_full); every consumer of both
-  // CTAs releases a slot on the leader's sched_empty
+  // work units after the first come from cluster launch control: the leader
+  // CTA's producer asks the hardware to cancel a not-yet-started cluster of
+  // this launch and takes over its unit. The 16-byte response lands in the
+  // same ring slot of both CTAs of the pair (multicast), completing 16 bytes
+  // on each CTA's sched_full; every consumer of both CTAs releases the slot on
+  // the leader's sched_empty before it is reused.
   constexpr int NS = Cfg::SCHED_SLOTS;
   uint64_t* sched_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);
   uint64_t* sched_empty = sched_full + NS;
-  uint32_t* sched_tile = reinterpret_cast<uint32_t*>(sched_empty + NS);
-  uint64_t* k4_ready = reinterpret_cast<uint64_t*>(sched_tile + NS + 2);  // (8-byte aligned)
+  uint8_t* sched_resp = smem + Cfg::RESP_OFF16;
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   // roles: epilogue warps first, the latency-critical producer / MMA warps get
-  // the highest ids (the warp arbiter prefers higher warp ids)
-  // (K4 warps, when present, take the lowest ids: 0 .. K4W-1)
-  constexpr int K4W = Cfg::K4W;
-  constexpr int W_PROD = K4W + Cfg::EPI_WARPS, W_MMA = W_PROD + 1, W_ALLOC = W_PROD + 2;
-  constexpr int MC = Cfg::MC;
-  const uint32_t crank = Cfg::CLUSTER > 1 ? cluster_ctarank() : 0u;
-  const uint32_t rank = crank % CG;      // rank within the CTA pair
-  const uint32_t pair = crank / CG;      // which pair of the cluster (MC > 1)
-  const uint32_t leader_rank = pair * CG;
+  // the highest ids (the warp arbiter prefers higher ids)
+  constexpr int W_PROD = Cfg::EPI_WARPS, W_MMA = W_PROD + 1, W_ALLOC = W_PROD + 2;
+  const uint32_t rank = CG > 1 ? cluster_ctarank() : 0u;  // rank within the CTA pair
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x / Cfg::CLUSTER;
-  const int num_clusters = gridDim.x / Cfg::CLUSTER;
+  const int first_unit = static_cast<int>(blockIdx.x) / Cfg::CLUSTER;
   const int mn_tiles = shape.tiles_m * shape.tiles_n;
   const int group_units = mn_tiles * shape.k_splits;
   const int total_tiles = group_units * shape.groups;
@@ -274,8 +243,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   if (warp == W_MMA && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], CG);
-      mbar_init(&empty_bar[s], MC + (K4W > 0 ? 1 : 0));
-      if constexpr (K4W > 0) mbar_init(&k4_ready[s], 1);
+      mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -284,7 +252,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     for (int i = 0; i < NS; ++i) {
       mbar_init(&sched_full[i], 1);
       // leader MMA + leader epilogue warps (+ peer producer + peer epilogue warps)
-      mbar_init(&sched_empty[i], 1 + Cfg::EPI_WARPS + (CG - 1) * (1 + Cfg::EPI_WARPS) + K4W * CG);
+      mbar_init(&sched_empty[i], 1 + Cfg::EPI_WARPS + (CG - 1) * (1 + Cfg::EPI_WARPS));
     }
     fence_barrier_init();
   }
@@ -302,19 +270,24 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const bool dyn = shape.sched != nullptr;
-  // consumer side of the work-unit ring (all lanes of the calling warp, or a
-  // single thread with one_thread): wait, read, release
+  // unit of iteration iter >= 1 from ring slot (iter - 1) % NS
+  auto resp_unit = [&](int slot) -> int {
+    const int x = clc_query(sched_resp + 16 * slot);
+    return x < 0 ? total_units : x / Cfg::CLUSTER;
+  };
+  // consumer side of the ring (all lanes of the calling warp, or a single
+  // thread with one_thread): wait, read, release
   auto sched_take = [&](int iter, bool one_thread) -> int {
-    const int slot = iter % NS;
-    mbar_wait(&sched_full[slot], static_cast<uint32_t>(iter / NS) & 1u);
-    const int t = static_cast<int>(*reinterpret_cast<volatile uint32_t*>(&sched_tile[slot]));
+    if (iter == 0) return first_unit;
+    const int slot = (iter - 1) % NS;
+    mbar_wait(&sched_full[slot], static_cast<uint32_t>((iter - 1) / NS) & 1u);
+    const int t = resp_unit(slot);
     if (!one_thread) __syncwarp();
     if (one_thread || lane == 0) {
       if (leader)
         mbar_arrive(&sched_empty[slot]);
       else
-        mbar_arrive_remote_release(&sched_empty[slot], leader_rank);
+        mbar_arrive_remote_release(&sched_empty[slot], 0);
     }
     return t;
   };
@@ -324,38 +297,37 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol_a =
-          (S24_L2_POLICY == 1 && shape.a_stream) ? l2_policy_evict_first() : l2_policy_evict_normal();
-      const uint64_t pol_b =
-          (S24_L2_POLICY == 1 && shape.b_keep) ? l2_policy_evict_last() : l2_policy_evict_normal();
-      uint16_t mc_mask = 0;  // this CTA and its counterparts in the other pairs
-#pragma unroll
-      for (int p = 0; p < MC; ++p) mc_mask |= static_cast<uint16_t>(1u << (p * CG + rank));
+      const uint64_t pol_a = shape.a_stream ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t pol_b = shape.b_keep ? l2_policy_evict_last() : l2_policy_evict_normal();
+      // the leader asks for unit iter + 1 as soon as unit iter is known to
+      // exist, so the response latency hides under this tile's loads
+      auto request = [&](int it) {
+        const int slot = (it - 1) % NS;
+        mbar_wait(&sched_empty[slot], (static_cast<uint32_t>((it - 1) / NS) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&sched_full[slot], 16);
+        if constexpr (CG == 2)
+          clc_try_cancel_all(sched_resp + 16 * slot, &sched_full[slot]);
+        else
+          clc_try_cancel(sched_resp + 16 * slot, &sched_full[slot]);
+      };
       for (int iter = 0;; ++iter) {
         int t;
-        if (!dyn) {
-          t = cluster_id + iter * num_clusters;
+        if (iter == 0) {
+          t = first_unit;
         } else if (leader) {
-          const int slot = iter % NS;
-          mbar_wait(&sched_empty[slot], (static_cast<uint32_t>(iter / NS) & 1u) ^ 1u);
-          t = atomicAdd(shape.sched, 1);
-          sched_tile[slot] = static_cast<uint32_t>(t);
-          mbar_arrive(&sched_full[slot]);
-          if constexpr (CG == 2) st_async_remote_u32(&sched_tile[slot], static_cast<uint32_t>(t), &sched_full[slot],
-                                                     leader_rank + 1);
-          if (t >= total_units) {
-            // last cluster out resets the counters for the next launch
-            __threadfence();
-            if (atomicAdd(shape.sched + 1, 1) == num_clusters - 1) {
-              atomicExch(shape.sched, 0);
-              atomicExch(shape.sched + 1, 0);
-            }
-          }
+#if S24_CLC_PREFETCH == 0
+          request(iter);
+#endif
+          const int slot = (iter - 1) % NS;
+          mbar_wait(&sched_full[slot], static_cast<uint32_t>((iter - 1) / NS) & 1u);
+          t = resp_unit(slot);  // (this thread reuses the slot only after NS more iterations)
         } else {
-          const int slot = iter % NS;
-          mbar_arrive_expect_tx(&sched_full[slot], 4);
+          mbar_arrive_expect_tx(&sched_full[(iter - 1) % NS], 16);
           t = sched_take(iter, true);
         }
+#if S24_CLC_PREFETCH
+        if (leader && t < total_units) request(iter + 1);
+#endif
         if (t >= total_units) break;
         int half;
         t = unit_tile(t, half);
@@ -366,68 +338,45 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const CUtensorMap* mapA = g2 ? &tmA2 : &tmA;
         const CUtensorMap* mapB = g2 ? &tmB2 : &tmB;
         const CUtensorMap* mapE = g2 ? &tmE2 : &tmE;
-        const int mt = mb * MC + static_cast<int>(pair);  // this pair's M tile
-        const int m0 = mt * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
+        const int m0 = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
         // sub-tile s of this CTA: B columns n0 + s * MMA_N .. + SUB_CTA - 1
         const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::SUB_CTA;
         // half unit: this CTA's B_CTA/2 columns of the half (box 0 .. BN_CTA/128 - 1)
         const int n0h = nb * Cfg::BN + half * (Cfg::BN / 2) + static_cast<int>(rank) * (Cfg::BN_CTA / 2);
         const uint32_t stage_tx = half < 0 ? Cfg::STAGE_BYTES : Cfg::STAGE_BYTES - Cfg::B_BYTES / 2;
-        const int atom_row = mt * CG + static_cast<int>(rank);  // 128-row metadata block
+        const int atom_row = mb * CG + static_cast<int>(rank);  // 128-row metadata block
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          if constexpr (S24_PIPE_PROBE == 1) {
-            if (leader)
-              mbar_arrive(&full_bar[stage]);
-            else
-              mbar_arrive_remote(&full_bar[stage], leader_rank);
-            if (++stage == Cfg::STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
-          }
           if (leader)
             mbar_arrive_expect_tx(&full_bar[stage], CG * stage_tx);
           else
-            mbar_arrive_remote(&full_bar[stage], leader_rank);
-          auto load_b = [&](void* dst, int c0, int c1) {
-            if constexpr (MC == 1)
-              tma_load<CG>(dst, mapB, &full_bar[stage], c0, c1, pol_b);
-            else
-              tma_load_2d_cg2_mc_hint(dst, mapB, &full_bar[stage], c0, c1, mc_mask, pol_b);
-          };
+            mbar_arrive_remote(&full_bar[stage], 0);
           if constexpr (Cfg::A_MN) {
             tma_load<CG>(sa, mapA, &full_bar[stage], m0, kb * Cfg::BK, pol_a);
             tma_load<CG>(sa + Cfg::A_BYTES / 2, mapA, &full_bar[stage], m0 + 64, kb * Cfg::BK, pol_a);
           } else {
             tma_load<CG>(sa, mapA, &full_bar[stage], kb * Cfg::A_COLS, m0, pol_a);
           }
-          // B boxes: with MC pairs, pair p fetches every MC-th box (or row
-          // slice) and multicasts it to the same slot of all pairs
           if constexpr (Cfg::B_MN) {
 #pragma unroll
             for (int j = 0; j < Cfg::BN_CTA / 64; ++j)
               if (half >= 0) {
-                if (j < Cfg::BN_CTA / 128) load_b(sb + j * (Cfg::BK * 128), n0h + 64 * j, kb * Cfg::BK);
-              } else if (MC == 1 || j % MC == static_cast<int>(pair))
-                load_b(sb + j * (Cfg::BK * 128),
-                       n0 + (j / (Cfg::SUB_CTA / 64)) * Cfg::MMA_N + 64 * (j % (Cfg::SUB_CTA / 64)), kb * Cfg::BK);
-          } else if constexpr (Cfg::B_ROW_SPLIT == 1) {
-#pragma unroll
-            for (int j = 0; j < Cfg::B_KBOX; ++j)
-              if (MC == 1 || j % MC == static_cast<int>(pair))
-#pragma unroll
-                for (int sub = 0; sub < Cfg::NSUB; ++sub)
-                  load_b(sb + j * (Cfg::BN_CTA * 128) + sub * (Cfg::SUB_CTA * 128), kb * Cfg::BK + Cfg::BOX_K * j,
-                         n0 + sub * Cfg::MMA_N);
+                if (j < Cfg::BN_CTA / 128)
+                  tma_load<CG>(sb + j * (Cfg::BK * 128), mapB, &full_bar[stage], n0h + 64 * j, kb * Cfg::BK, pol_b);
+              } else {
+                tma_load<CG>(sb + j * (Cfg::BK * 128), mapB, &full_bar[stage],
+                             n0 + (j / (Cfg::SUB_CTA / 64)) * Cfg::MMA_N + 64 * (j % (Cfg::SUB_CTA / 64)),
+                             kb * Cfg::BK, pol_b);
+              }
           } else {
-            const int r0 = static_cast<int>(pair) * Cfg::B_BOX_ROWS;
 #pragma unroll
             for (int j = 0; j < Cfg::B_KBOX; ++j)
-              load_b(sb + j * (Cfg::BN_CTA * 128) + r0 * 128, kb * Cfg::BK + Cfg::BOX_K * j, n0 + r0);
+#pragma unroll
+              for (int sub = 0; sub < Cfg::NSUB; ++sub)
+                tma_load<CG>(sb + j * (Cfg::BN_CTA * 128) + sub * (Cfg::SUB_CTA * 128), mapB, &full_bar[stage],
+                             kb * Cfg::BK + Cfg::BOX_K * j, n0 + sub * Cfg::MMA_N, pol_b);
           }
           if constexpr (Cfg::SPARSE)
             tma_load<CG>(sb + Cfg::B_BYTES, mapE, &full_bar[stage], 0,
@@ -446,7 +395,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       int stage = 0;
       uint32_t phase = 0;
       for (int iter = 0;; ++iter) {
-        const int u = dyn ? sched_take(iter, true) : cluster_id + iter * num_clusters;
+        const int u = sched_take(iter, true);
         if (u >= total_units) break;
         int half;
         const int t = unit_tile(u, half);
@@ -479,7 +428,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             }
           }
 #pragma unroll
-          for (int j = 0; j < (S24_PIPE_PROBE == 2 ? 0 : Cfg::KSTEPS); ++j)
+          for (int j = 0; j < Cfg::KSTEPS; ++j)
 #pragma unroll
           for (int sub = 0; sub < Cfg::NSUB; ++sub) {
             // (NSUB > 1: dense only; sub-tile sub's B boxes and accumulator columns)
@@ -529,10 +478,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           }
           uint64_t* tf = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
           if constexpr (CG == 2) {
-            // the slot may be refilled (by every pair's multicast) once all
-            // pairs released it; the accumulator belongs to this pair only
-            mma_commit_cg2(&empty_bar[stage], static_cast<uint16_t>((1u << Cfg::CLUSTER) - 1));
-            if (kb == kb1 - 1) mma_commit_cg2(tf, static_cast<uint16_t>(0x3u << leader_rank));
+            mma_commit_cg2(&empty_bar[stage], static_cast<uint16_t>(0x3u));
+            if (kb == kb1 - 1) mma_commit_cg2(tf, static_cast<uint16_t>(0x3u));
           } else {
             mma_commit(&empty_bar[stage]);
             if (kb == kb1 - 1) mma_commit(tf);
@@ -545,38 +492,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       }
     }
     __syncwarp();
-  } else if (warp >= K4W && warp < K4W + Cfg::EPI_WARPS) {
+  } else if (warp < Cfg::EPI_WARPS) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - K4W;              // (K4W % 4 == 0: warp % 4 is still the TMEM lane quarter)
-    const int q = ew & 3;                   // TMEM lane quarter
-    const int part = ew >> 2;               // which contiguous run of CPW chunks
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int part = warp >> 2;             // which contiguous run of CPW chunks
     const int c_begin = part * Cfg::CPW;
     const bool owns_last = c_begin + Cfg::CPW == Cfg::NCHUNK;
     typename Epi::State st;
     Epi::init(ep, st);
-    // optional background job: K4 warp units taken from a global queue while
-    // this warp would otherwise sit waiting for an accumulator
-    // (sparse configurations only: the job's LUT costs dense kernels 2 KB of
-    // static shared memory, i.e. a pipeline stage)
-    bool bg_more = Cfg::SPARSE && shape.has_bg != 0;
-    const uint2* bg_lut = nullptr;
-    if constexpr (Cfg::SPARSE) bg_lut = bg_more ? k4_lut_init() : nullptr;
-    auto bg_unit = [&]() -> bool {
-      if constexpr (Cfg::SPARSE) {
-        int u = 0;
-        if (lane == 0) u = atomicAdd(shape.bg.counter, 1);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= shape.bg.units) return false;
-        int t0, fb;
-        k4_unit_coords(shape.bg.a, u, t0, fb);
-        k4_warp_unit<false>(shape.bg.a, t0, fb, static_cast<int>(lane), bg_lut);
-        return true;
-      } else {
-        return false;
-      }
-    };
     for (int iter = 0;; ++iter) {
-      const int u = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
+      const int u = sched_take(iter, false);
       if (u >= total_units) break;
       int half;
       const int t = unit_tile(u, half);
@@ -586,8 +511,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       const int col_base = nb * Cfg::BN + (half > 0 ? Cfg::BN / 2 : 0);
       const int nck = half < 0 ? Cfg::NCHUNK : Cfg::NCHUNK / 2;
       const int slot = iter % Cfg::NSLOT;
-      const int row = (mb * MC + static_cast<int>(pair)) * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 +
-                      static_cast<int>(lane);
+      const int row = mb * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM + q * 32 + static_cast<int>(lane);
       const bool row_ok = row < shape.M;
       const typename Epi::Params& epg = t >= group_units ? ep2 : ep;
       Epi::prefetch(epg, st, row, row_ok, col_base + c_begin * 32, (t % group_units) / mn_tiles);
@@ -601,14 +525,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       const bool owner = Cfg::OVERLAP && (slot == 0 ? owns_last : c_begin == 0);
       uint64_t* tfull = &tfull_bar[Cfg::OVERLAP ? 0 : slot];
       const uint32_t tparity = Cfg::OVERLAP ? (iter & 1) : ((iter / Cfg::NSLOT) & 1);
-      if (bg_more && !owner) {
-        while (!mbar_test(tfull, tparity)) {
-          if (!bg_unit()) {
-            bg_more = false;
-            break;
-          }
-        }
-      }
       mbar_wait(tfull, tparity);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * Cfg::SLOT1_COL;
@@ -622,13 +538,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const bool cvalid = c < nck && col0 < shape.N;  // uniform across the warp
         uint32_t r[32];
         if (cvalid) {
-          if constexpr (S24_PIPE_PROBE == 3) {  // experiment: no accumulator reads
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = static_cast<uint32_t>(i + c) * 0x3F800000u;
-          } else {
-            tmem_ld32(t_row + c * 32, r);
-            tmem_ld_wait();
-          }
+          tmem_ld32(t_row + c * 32, r);
+          tmem_ld_wait();
         }
         // release the accumulator as soon as this warp's last load landed
         // (overlapping slots: the shared chunk's owner, after its first load)
@@ -637,7 +548,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           if (leader)
             mbar_arrive(tempty);
           else
-            mbar_arrive_remote(tempty, leader_rank);
+            mbar_arrive_remote(tempty, 0);
         }
         if (cvalid) {
           float v[32];
@@ -647,71 +558,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         }
       }
     }
-    // drain what is left of the background queue
-    while (bg_more && bg_unit()) {
-    }
     Epi::finish(ep, st, lane);
-  } else if (K4W > 0 && warp < K4W) {
-    // ------------------------------------------------------------ K4 warps (k4s.cuh)
-    // Walk the same stage sequence as the MMA; warp w serves the stage uses
-    // it with it % K4W == w: wait until the stage landed, copy this tile's
-    // units to registers, release the stage, split them.
-    if constexpr (K4W > 0) {
-      __shared__ K4sSlot k4s_slots[K4W][16];
-      const uint2* lut = k4_lut_init();
-      const int tn = shape.tiles_n < 8 ? shape.tiles_n : 8;
-      int stage = 0;
-      uint32_t phase = 0;
-      long long it = 0;
-      for (int iter = 0;; ++iter) {
-        const int u = dyn ? sched_take(iter, false) : cluster_id + iter * num_clusters;
-        if (u >= total_units) break;
-        int half;
-        const int t = unit_tile(u, half);
-        int mb, nb, kb0, kb1;
-        tile_coords(shape, t % mn_tiles, mb, nb);
-        kb_range(t, kb0, kb1);
-        const int m0 = (mb * MC + static_cast<int>(pair)) * Cfg::TILE_M + static_cast<int>(rank) * Cfg::BM;
-        const bool work = shape.has_fs && nb < tn && m0 < shape.fs.n;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          if (static_cast<int>(it % K4W) == warp) {
-            if (leader) {
-              mbar_wait(&full_bar[stage], phase);
-              if constexpr (CG == 2)
-                if (lane == 0) mbar_arrive_remote_release(&k4_ready[stage], leader_rank + 1);
-            } else {
-              mbar_wait_cluster(&k4_ready[stage], phase);
-            }
-            const uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-            const uint8_t* se = sa + Cfg::A_BYTES + Cfg::B_BYTES;
-            K4sRegs u;
-            int j = nb;
-            if (work) k4s_load(sa, se, j, static_cast<int>(lane), u);
-            if (work && j + tn < 8) {
-              // small N (fewer than 8 N tiles): this tile owns several units;
-              // all but the last are split while the stage is still held
-              for (; j + tn < 8; j += tn) {
-                k4s_compute(shape.fs, u, kb * 128 + j * 16, m0, static_cast<int>(lane), lut, k4s_slots[warp]);
-                k4s_load(sa, se, j + tn, static_cast<int>(lane), u);
-              }
-            }
-            // release the stage only once this warp's copies have landed in
-            // registers (the arrive depends on the loaded words) and are
-            // ordered before the TMA refill (generic -> async proxy)
-            uint32_t dep = 1u;
-            if (work) dep |= k4s_fold(u);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            dep = __reduce_or_sync(0xffffffffu, dep);
-            if (lane == 0 && dep != 0u) mbar_arrive(&empty_bar[stage]);
-            if (work) k4s_compute(shape.fs, u, kb * 128 + j * 16, m0, static_cast<int>(lane), lut, k4s_slots[warp]);
-          }
-          if (++stage == Cfg::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
   }
 
   tc_fence_before();

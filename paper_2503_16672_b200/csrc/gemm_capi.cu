@@ -67,29 +67,6 @@ int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t o
   return make_map_2d(map, base, true, inner, outer, ld * 2, box_inner, box_outer, true);
 }
 
-// ---------------------------------------------------------------------------
-// Dynamic tile scheduler counters: {next, done} int pairs in device memory,
-// zeroed once and reset by each launch's last cluster. Launches take pairs
-// round-robin, so concurrent launches on different streams never share one.
-static constexpr int kSchedSlots = 4096;
-
-static int* sched_counter() {
-  static std::mutex mu;
-  static int* pool[64] = {nullptr};
-  static unsigned next[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!pool[dev]) {
-    int* p = nullptr;
-    if (cudaMalloc(&p, sizeof(int) * 2 * kSchedSlots) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, sizeof(int) * 2 * kSchedSlots) != cudaSuccess) return nullptr;
-    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
-    pool[dev] = p;
-  }
-  return pool[dev] + 2 * (next[dev]++ % kSchedSlots);
-}
-
 // operands of one GEMM problem (the grouped launch takes two of equal shape)
 template <class Epi>
 struct GemmOperands {
@@ -153,8 +130,7 @@ static int make_operand_maps(const void* A, int64_t lda, const void* B, int64_t 
 template <class Cfg, class Epi>
 static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                        const uint8_t* meta, const typename Epi::Params& ep, cudaStream_t stream, int k_splits = 1,
-                       const K4Job* bg = nullptr, const GemmOperands<Epi>* second = nullptr,
-                       const K4Args* fs = nullptr) {
+                       const GemmOperands<Epi>* second = nullptr) {
   if (M <= 0 || N <= 0 || K <= 0) return S24_OK;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return fail(S24_ERR_DIMENSION, "GEMM dims too large");
   CUtensorMap ma, mb, me, ma2, mb2, me2;
@@ -174,39 +150,15 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   sh.M = static_cast<int>(M);
   sh.N = static_cast<int>(N);
   sh.K = static_cast<int>(K);
-  // work units cover MC vertically adjacent tiles (one per CTA pair)
-  sh.tiles_m = static_cast<int>((M + Cfg::TILE_M * Cfg::MC - 1) / (Cfg::TILE_M * Cfg::MC));
+  sh.tiles_m = static_cast<int>((M + Cfg::TILE_M - 1) / Cfg::TILE_M);
   sh.tiles_n = static_cast<int>((N + Cfg::BN - 1) / Cfg::BN);
   // raster: groups of 512 rows sweep N (measured best for the 2:4 GEMMs,
   // neutral for the dense ones; 2048-row groups cost up to 10%)
-  sh.group_m = Cfg::CLUSTER >= 4 ? 1 : 4 / Cfg::CLUSTER;
-  if (const char* g = std::getenv("S24_GROUP_M")) {  // experiments: raster group height in tiles
-    const int v = std::atoi(g);
-    if (v > 0) sh.group_m = v;
-  }
+  sh.group_m = 4 / Cfg::CLUSTER;
   sh.k_splits = k_splits < 1 ? 1 : k_splits;
   sh.groups = second ? 2 : 1;
-  sh.sched = nullptr;
-#ifndef S24_STATIC_SCHED
-  if constexpr (Cfg::MC == 1) {
-    // dynamic work units: clusters that start late (SMs still busy with a
-    // co-running kernel) or run slow simply take fewer units
-    sh.sched = sched_counter();
-    if (!sh.sched) return fail(S24_ERR_CUDA, "scheduler counters unavailable");
-  }
-#endif
-  sh.has_bg = bg != nullptr;
-  if (bg)
-    sh.bg = *bg;
-  else
-    std::memset(&sh.bg, 0, sizeof(sh.bg));
-  sh.has_fs = fs != nullptr;
-  if (fs)
-    sh.fs = *fs;
-  else
-    std::memset(&sh.fs, 0, sizeof(sh.fs));
-  if (fs && (k_splits > 1 || second)) return fail(S24_ERR_CONFIG, "the in-GEMM feature split needs one problem, no split-K");
   const int tiles = sh.tiles_m * sh.tiles_n * sh.k_splits * sh.groups;
+  if (static_cast<long long>(tiles) * 2 * Cfg::CLUSTER >= (1ll << 31)) return fail(S24_ERR_DIMENSION, "too many tiles");
 
   auto kern = gemm_kernel<Cfg, Epi>;
   cudaLaunchConfig_t cfg{};
@@ -220,74 +172,49 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // persistent grid: as many clusters as fit at once (clusters of 4 may not
-  // tile every GPC exactly, so ask the occupancy calculator)
+  // clusters resident at once (one CTA per SM: the stage ring fills smem)
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  static int max_clusters = 0;
   std::call_once(once, [&] {
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    max_clusters = num_sms() / Cfg::CLUSTER;
-    if (attr_err == cudaSuccess && Cfg::CLUSTER > 2) {
-      cfg.gridDim = dim3(static_cast<unsigned>(max_clusters * Cfg::CLUSTER));
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0 && n < max_clusters)
-        max_clusters = n;
-      cudaGetLastError();
-    }
   });
   if (attr_err != cudaSuccess) return fail(S24_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  const int clusters = tiles < max_clusters ? tiles : max_clusters;
+  const int resident = num_sms() / Cfg::CLUSTER;
   // L2 policies (see gemm.cuh): pin B when it fits, and only then let the
   // A panels stream through (measured: with a 64 MiB B, evict-first A panels
   // are lost before all N tiles of their row have read them)
   sh.b_keep = static_cast<long long>(K) * N * Cfg::EB * sh.groups <= (40ll << 20);
-  sh.a_stream = sh.b_keep && sh.group_m * sh.tiles_n <= clusters;
+  sh.a_stream = sh.b_keep && sh.group_m * sh.tiles_n <= resident;
   // a partial last wave of at most half the clusters: its tiles run as two
-  // N-halves each, so that wave takes half as long (dynamic scheduler only)
+  // N-halves each, so that wave takes half as long
   sh.tail_split = 0;
   if constexpr (Cfg::HALF_OK) {
-    const int rem = tiles % clusters;
-    const char* e = std::getenv("S24_TAIL_SPLIT");
-    if (sh.sched && !fs && !bg && tiles > clusters && rem > 0 && 2 * rem <= clusters && !(e && e[0] == '0'))
-      sh.tail_split = rem;
+    const int rem = tiles % resident;
+    if (tiles > resident && rem > 0 && 2 * rem <= resident) sh.tail_split = rem;
   }
-  cfg.gridDim = dim3(static_cast<unsigned>(clusters * Cfg::CLUSTER));
+  // one cluster per work unit; running clusters steal the units of the ones
+  // that have not started (cluster launch control, gemm.cuh)
+  const long long units = static_cast<long long>(tiles) + sh.tail_split;
+  cfg.gridDim = dim3(static_cast<unsigned>(units * Cfg::CLUSTER));
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, ma2, mb2, me2, sh, ep, second ? second->ep : ep);
   if (e != cudaSuccess) return fail(S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return check_launch("gemm_kernel");
 }
 
 // tile configurations
-// <sparse, A MN-major, B MN-major, BN, stages, CTA-group>
-#ifndef S24_DENSE_MC
-#define S24_DENSE_MC 1
-#endif
-#ifndef S24_DENSE_STAGES
-#define S24_DENSE_STAGES 6
-#endif
-using DenseKN = GemmCfg<false, false, true, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;   // A K-major, B MN-major
-using DenseKK = GemmCfg<false, false, false, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;  // A K-major, B K-major
-using DenseMM = GemmCfg<false, true, true, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;    // A MN-major, B MN-major
-using DenseMK = GemmCfg<false, true, false, 256, S24_DENSE_STAGES, 2, 8, S24_DENSE_MC>;   // A MN-major, B K-major
+// <sparse, A MN-major, B MN-major, BN, stages, CTA-group, epilogue warps, e4m3>
+using DenseKN = GemmCfg<false, false, true, 256, 6, 2, 8>;   // A K-major, B MN-major
+using DenseKK = GemmCfg<false, false, false, 256, 6, 2, 8>;  // A K-major, B K-major
+using DenseMM = GemmCfg<false, true, true, 256, 6, 2, 8>;    // A MN-major, B MN-major
+using DenseMK = GemmCfg<false, true, false, 256, 6, 2, 8>;   // A MN-major, B K-major
 // sparse: light epilogue, 4 epilogue warps and <= 128 registers/thread, leaving
 // room for a co-resident side-stream kernel (the feature-wise split K4)
-// (S24_SPARSE_MC = CTA pairs per cluster sharing B by TMA multicast)
-#ifndef S24_SPARSE_MC
-#define S24_SPARSE_MC 1
-#endif
-using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4, S24_SPARSE_MC>;   // sparse A, B MN-major
-using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, S24_SPARSE_MC>;  // sparse A, B K-major
-// ... plus warps that split the A stages feature-wise (k4s.cuh)
-#ifndef S24_FS_WARPS
-#define S24_FS_WARPS 4
-#endif
-using SparseN_FS = GemmCfg<true, false, true, 256, 4, 2, 4, 1, false, S24_FS_WARPS>;
-using SparseK_FS = GemmCfg<true, false, false, 256, 4, 2, 4, 1, false, S24_FS_WARPS>;
+using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4>;   // sparse A, B MN-major
+using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4>;  // sparse A, B K-major
 
 // e4m3 (kind::f8f6f4): same byte geometry per stage as the bf16 configs
-using F8DenseKK = GemmCfg<false, false, false, 256, S24_DENSE_STAGES, 2, 8, 1, true>;
-using F8SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, 1, true>;
+using F8DenseKK = GemmCfg<false, false, false, 256, 6, 2, 8, true>;
+using F8SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, true>;
 
 // wide dense tiles: 256 x 512 per CTA pair, one 512-column accumulator (see
 // gemm.cuh). A quarter fewer operand bytes per MAC than 256 x 256, but the
@@ -295,20 +222,13 @@ using F8SparseK = GemmCfg<true, false, false, 256, 4, 2, 4, 1, true>;
 // MN-major-A weight-gradient GEMMs (K = tokens = 16384) gain 6-9%; the
 // K-major-A GEMMs lose 1-6% (K1 0.400 -> 0.423 ms: its heavier epilogue is
 // what gets exposed). Default: wide for MN-major A only.
-#ifndef S24_DENSE_WIDE_STAGES
-#define S24_DENSE_WIDE_STAGES 4
-#endif
-using DenseKN_W = GemmCfg<false, false, true, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
-using DenseKK_W = GemmCfg<false, false, false, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
-using DenseMM_W = GemmCfg<false, true, true, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
-using DenseMK_W = GemmCfg<false, true, false, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1>;
-using F8DenseKK_W = GemmCfg<false, false, false, 512, S24_DENSE_WIDE_STAGES, 2, 8, 1, true>;
+using DenseKN_W = GemmCfg<false, false, true, 512, 4, 2, 8>;
+using DenseKK_W = GemmCfg<false, false, false, 512, 4, 2, 8>;
+using DenseMM_W = GemmCfg<false, true, true, 512, 4, 2, 8>;
+using DenseMK_W = GemmCfg<false, true, false, 512, 4, 2, 8>;
+using F8DenseKK_W = GemmCfg<false, false, false, 512, 4, 2, 8, true>;
 
-// S24_DENSE_BN=512 / 256 forces every dense GEMM wide / narrow (experiments)
-static bool dense_wide(bool a_mn) {
-  const char* e = std::getenv("S24_DENSE_BN");
-  return e ? std::atoi(e) == 512 : a_mn;
-}
+static bool dense_wide(bool a_mn) { return a_mn; }
 
 template <class Narrow, class Wide, class Epi>
 static int launch_dense(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
@@ -368,9 +288,9 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__
 template <class Epi>
 static int dispatch_sparse(int b_mn, const void* A, const uint8_t* meta, const void* B, int64_t ldb, int64_t M,
                            int64_t N, int64_t K, const typename Epi::Params& ep, cudaStream_t st,
-                           const K4Job* bg = nullptr, const GemmOperands<Epi>* second = nullptr) {
-  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg, second);
-  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, bg, second);
+                           const GemmOperands<Epi>* second = nullptr) {
+  if (b_mn) return launch_gemm<SparseN, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, second);
+  return launch_gemm<SparseK, Epi>(A, K / 2, B, ldb, M, N, K, meta, ep, st, 1, second);
 }
 
 static int check_common(int64_t M, int64_t N, int64_t K, int64_t lda, int a_mn, int64_t ldb, int b_mn) {
@@ -460,60 +380,6 @@ int s24_spmm(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_
   });
 }
 
-int s24_spmm_fs(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
-                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-                int64_t d_rows_valid, const int* d_row_valid, int64_t fs_n, const int* fs_feat_pos,
-                int64_t fs_n_sparse, int64_t fs_n_dense, void* fs_vs, uint8_t* fs_es, int fs_nonneg, void* stream) {
-  int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
-  if (rc) return rc;
-  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
-  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
-  if (fs_n % 128 != 0 || fs_n < M || fs_n > (M + 255) / 256 * 256)
-    return fail(S24_ERR_DIMENSION, "feature split tokens %lld must be pad128(M) for M = %lld", (long long)fs_n,
-                (long long)M);
-  if (!fs_vs || !fs_es || !fs_feat_pos) return fail(S24_ERR_DIMENSION, "feature split outputs required");
-  auto st = static_cast<cudaStream_t>(stream);
-  K4Args fs;
-  rc = k4_prepare(a_vals, a_meta, fs_n, K, fs_feat_pos, fs_n_sparse, fs_n_dense, fs_vs, fs_es, nullptr, st, &fs,
-                  2 * fs_n_dense);
-  if (rc) return rc;
-  fs.nonneg = fs_nonneg;
-  return with_out(out_dtype, [&](auto tag) {
-    using OutT = std::remove_pointer_t<decltype(tag)>;
-    using Epi = EpiStore<OutT>;
-    typename Epi::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
-                            static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
-    if (b_mn_major)
-      return launch_gemm<SparseN_FS, Epi>(a_vals, K / 2, B, ldb, M, N, K, a_meta, ep, st, 1, nullptr, nullptr, &fs);
-    return launch_gemm<SparseK_FS, Epi>(a_vals, K / 2, B, ldb, M, N, K, a_meta, ep, st, 1, nullptr, nullptr, &fs);
-  });
-}
-
-int s24_spmm_bg(const void* a_vals, const uint8_t* a_meta, const void* B, int b_mn_major, int64_t ldb, int64_t M,
-                int64_t N, int64_t K, void* D, int out_dtype, int64_t ldd, const int* d_row_map, int d_transposed,
-                int64_t d_rows_valid, const int* d_row_valid, const void* k4_vals, const uint8_t* k4_meta,
-                int64_t k4_n, int64_t k4_h, const int* k4_feat_pos, int64_t k4_n_sparse, int64_t k4_n_dense,
-                void* k4_vs, uint8_t* k4_es, void* k4_vd, int* k4_counter, void* stream) {
-  int rc = check_common(M, N, K, K, 0, ldb, b_mn_major);
-  if (rc) return rc;
-  if (K % 128 != 0) return fail(S24_ERR_DIMENSION, "sparse K = %lld must be a multiple of 128", (long long)K);
-  if (!d_transposed && ldd < N) return fail(S24_ERR_DIMENSION, "ldd too small");
-  auto st = static_cast<cudaStream_t>(stream);
-  K4Job job;
-  rc = k4_prepare(k4_vals, k4_meta, k4_n, k4_h, k4_feat_pos, k4_n_sparse, k4_n_dense, k4_vs, k4_es, k4_vd, st, &job.a);
-  if (rc) return rc;
-  if (!k4_counter) return fail(S24_ERR_DIMENSION, "background split needs a counter");
-  cudaMemsetAsync(k4_counter, 0, sizeof(int), st);
-  job.counter = k4_counter;
-  job.units = static_cast<int>((k4_n / 128) * (k4_h / 16));
-  return with_out(out_dtype, [&](auto tag) {
-    using OutT = std::remove_pointer_t<decltype(tag)>;
-    typename EpiStore<OutT>::Params ep{static_cast<OutT*>(D), ldd, d_row_map, d_transposed,
-                                       static_cast<int>(d_rows_valid < 0 ? M : d_rows_valid), d_row_valid, 0};
-    return dispatch_sparse<EpiStore<OutT>>(b_mn_major, a_vals, a_meta, B, ldb, M, N, K, ep, st, &job);
-  });
-}
-
 int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype, const void* a_vals0,
                   const uint8_t* a_meta0, const void* B0, int64_t ldb0, void* D0, int64_t ldd0, const int* d_row_map0,
                   int d_transposed0, const int* d_row_valid0, const void* a_vals1, const uint8_t* a_meta1,
@@ -535,46 +401,29 @@ int s24_spmm_pair(int b_mn_major, int64_t M, int64_t N, int64_t K, int out_dtype
                              typename Epi::Params{static_cast<OutT*>(D1), ldd1, d_row_map1, d_transposed1,
                                                   static_cast<int>(M), d_row_valid1, 0, pr}};
     return dispatch_sparse<Epi>(b_mn_major, a_vals0, a_meta0, B0, ldb0, M, N, K, ep0,
-                                static_cast<cudaStream_t>(stream), nullptr, &second);
+                                static_cast<cudaStream_t>(stream), &second);
   });
-}
-
-static int check_fw(void* fw_vals, const uint8_t* fw_meta, int64_t fw_kdim, int64_t M) {
-  if (!fw_vals) return S24_OK;
-  if (!fw_meta) return fail(S24_ERR_DIMENSION, "feature-wise output needs its metadata buffer");
-  if (fw_kdim % 128 != 0 || fw_kdim < M)
-    return fail(S24_ERR_DIMENSION, "feature-wise K (tokens) %lld must be a multiple of 128 covering M", (long long)fw_kdim);
-  return S24_OK;
 }
 
 int s24_fwd_gemm1_fused(const void* x, int64_t ldx, const void* w1, int64_t ldw1, int64_t M, int64_t N,
                         int64_t K, void* act_vals, uint8_t* act_meta, int* counts, unsigned long long* stats,
-                        float* y_dbg, void* fw_vals, uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim,
-                        const int* row_map, void* stream) {
+                        float* y_dbg, void* stream) {
   int rc = check_common(M, N, K, ldx, 0, ldw1, 1);
   if (rc) return rc;
   if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
-  if ((rc = check_fw(fw_vals, fw_meta, fw_kdim, M))) return rc;
-  if (row_map && fw_vals) return fail(S24_ERR_CONFIG, "the fused feature-wise output needs unmapped rows");
-  EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N),
-                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)},
-                     row_map};
+  if (!act_vals || !act_meta) return fail(S24_ERR_DIMENSION, "K1 needs the value and metadata buffers");
+  EpiFwd1::Params ep{static_cast<__nv_bfloat16*>(act_vals), act_meta, counts, stats, y_dbg, static_cast<int>(N)};
   return launch_dense<DenseKN, DenseKN_W, EpiFwd1>(x, ldx, w1, ldw1, M, N, K, ep, static_cast<cudaStream_t>(stream));
 }
 
 int s24_bwd_dact_fused(const void* g, int64_t ldg, const void* w2, int64_t ldw2, int64_t M, int64_t N,
-                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* fw_vals,
-                       uint8_t* fw_meta, unsigned long long* fw_counts, int64_t fw_kdim, const int* row_map,
-                       void* stream) {
+                       int64_t K, const void* act_vals, const uint8_t* act_meta, void* g_vals, void* stream) {
   int rc = check_common(M, N, K, ldg, 0, ldw2, 0);
   if (rc) return rc;
   if (N % 128 != 0) return fail(S24_ERR_DIMENSION, "hidden width %lld must be a multiple of 128", (long long)N);
-  if ((rc = check_fw(fw_vals, fw_meta, fw_kdim, M))) return rc;
+  if (!act_vals || !act_meta || !g_vals) return fail(S24_ERR_DIMENSION, "K3 needs act, metadata and g_pre buffers");
   EpiBwd1::Params ep{static_cast<const __nv_bfloat16*>(act_vals), act_meta, static_cast<__nv_bfloat16*>(g_vals),
-                     static_cast<int>(N),
-                     FwTarget{static_cast<__nv_bfloat16*>(fw_vals), fw_meta, fw_counts, static_cast<int>(fw_kdim)},
-                     row_map};
-  if (row_map && fw_vals) return fail(S24_ERR_CONFIG, "the fused feature-wise output needs unmapped rows");
+                     static_cast<int>(N)};
   return launch_gemm<DenseKK, EpiBwd1>(g, ldg, w2, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 
@@ -665,7 +514,7 @@ int s24_spmm_pair_f8(int64_t M, int64_t N, int64_t K, int out_dtype, const uint8
                              typename Epi::Params{static_cast<OutT*>(D1), ldd1, d_row_map1, d_transposed1,
                                                   static_cast<int>(M), d_row_valid1, 0, pr, rs1, cs1}};
     return launch_gemm<F8SparseK, Epi>(a0, K / 2, B0, ldb0, M, N, K, meta0, ep0, static_cast<cudaStream_t>(stream),
-                                       1, nullptr, &second);
+                                       1, &second);
   });
 }
 
@@ -679,8 +528,7 @@ int s24_fwd_gemm1_f8(const uint8_t* xq, int64_t ldx, const uint8_t* w1q, int64_t
   if (!x_scale || !w1_scale || !act_vals32 || !row_amax)
     return fail(S24_ERR_DIMENSION, "e4m3 K1 needs scales, the fp32 value buffer and the row maxima");
   using Epi = EpiFwd1T<true>;
-  Epi::Params ep{nullptr, act_meta, counts, stats, y_dbg, static_cast<int>(N), FwTarget{nullptr, nullptr, nullptr, 0},
-                 nullptr, x_scale, w1_scale, act_vals32, row_amax};
+  Epi::Params ep{nullptr, act_meta, counts, stats, y_dbg, static_cast<int>(N), x_scale, w1_scale, act_vals32, row_amax};
   return launch_dense<F8DenseKK, F8DenseKK_W, Epi>(xq, ldx, w1q, ldw1, M, N, K, ep, static_cast<cudaStream_t>(stream));
 }
 
@@ -694,7 +542,7 @@ int s24_bwd_dact_f8(const uint8_t* gq, int64_t ldg, const uint8_t* w2q, int64_t 
   if (!g_scale || !w2_scale) return fail(S24_ERR_DIMENSION, "e4m3 K3 needs row and column scales");
   using Epi = EpiBwd1T<true>;
   Epi::Params ep{static_cast<const __nv_bfloat16*>(act_vals), act_meta, static_cast<__nv_bfloat16*>(g_vals),
-                 static_cast<int>(N), FwTarget{nullptr, nullptr, nullptr, 0}, nullptr, g_scale, w2_scale};
+                 static_cast<int>(N), g_scale, w2_scale};
   return launch_gemm<F8DenseKK, Epi>(gq, ldg, w2q, ldw2, M, N, K, nullptr, ep, static_cast<cudaStream_t>(stream));
 }
 

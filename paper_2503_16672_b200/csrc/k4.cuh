@@ -1,7 +1,7 @@
 // K4 -- feature-wise (transposed) split of a token-wise compressed [n, h]
-// matrix, as one warp-sized unit of work (16 features x 128 tokens) so that it
-// can run either as a standalone grid (k_feature_split) or as background work
-// in the idle epilogue warps of a tensor-bound GEMM (gemm.cuh).
+// matrix, as one warp-sized unit of work (16 features x 128 tokens), run by
+// the standalone grid k_feature_split (any layout, optional drop counts; the
+// hot path's paired-layout split is the leaner k4x.cuh).
 //
 // The unit: lane l owns the token group 4l..4l+3 of the 128-token block and
 //   1. loads its 4 tokens' compressed 16-feature slices (16 B each) and their
@@ -41,23 +41,10 @@ struct K4Args {
 // computes both parts; its epilogue adds each pair (exact dense dot product,
 // summed in two halves), so the split weight gradient needs no dense GEMM.
 
-// background-job descriptor for the GEMM epilogue warps
-struct K4Job {
-  K4Args a;
-  int* counter;  // zeroed before the launch; next unit to take
-  int units;     // (n / 128) * (h / 16)
-};
-
 __device__ __forceinline__ void k4_warp_add(unsigned long long v, unsigned long long* dst) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
-}
-
-__device__ __forceinline__ void k4_unit_coords(const K4Args& a, int u, int& t0, int& fbase) {
-  const int per_block = a.h / 16;
-  t0 = (u / per_block) * 128;
-  fbase = (u % per_block) * 16;
 }
 
 // per-warp copy of the nibble -> PRMT selector table (static shared memory)

@@ -456,4 +456,41 @@ __device__ __forceinline__ void mma_sp_e4m3_cg2(uint32_t d_tmem, uint64_t adesc,
       : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Cluster launch control (sm_100): hardware work stealing. try_cancel asks the
+// grid scheduler to cancel one cluster of this launch that has not started
+// yet; the 16-byte response (written asynchronously into the same smem offset
+// of every CTA of the calling cluster, each completing 16 transaction bytes on
+// its same-offset mbarrier) says whether it succeeded and which cluster it
+// was, whose work the caller then does instead. No device memory is involved.
+__device__ __forceinline__ void clc_try_cancel_all(void* resp16, uint64_t* bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.multicast::cluster::all.b128"
+      " [%0], [%1];" ::"r"(smem_u32(resp16)),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void clc_try_cancel(void* resp16, uint64_t* bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+          smem_u32(resp16)),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+// decode a response: the canceled cluster's first CTA x index, or -1 when
+// nothing was left to cancel
+__device__ __forceinline__ int clc_query(const void* resp16) {
+  int x;
+  asm volatile(
+      "{\n\t.reg .b128 rr;\n\t.reg .pred p;\n\t.reg .b32 cx;\n\t"
+      "ld.shared.b128 rr, [%1];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, rr;\n\t"
+      "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 cx, rr;\n\t"
+      "selp.b32 %0, cx, -1, p;\n\t}"
+      : "=r"(x)
+      : "r"(smem_u32(resp16))
+      : "memory");
+  return x;
+}
+
 }  // namespace s24

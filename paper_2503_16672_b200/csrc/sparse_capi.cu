@@ -10,7 +10,6 @@
 #include "meta.cuh"
 #include "ptx.cuh"
 #include "k4.cuh"
-#include "k4id.cuh"
 #include "k4x.cuh"
 
 namespace s24 {
@@ -614,55 +613,22 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
   return check_launch("k_plan");
 }
 
-int s24_feature_split_x(const void* vals_a, const void* vals_b, const uint8_t* meta_hw, int64_t n, int64_t h,
-                        const int* feat_pos, int64_t n_sparse, int64_t n_dense, void* vs_a, uint8_t* es_a, void* vs_b,
-                        uint8_t* es_b, int a_nonneg, const int* row_map, void* stream) {
+int s24_feature_split_x(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
+                        int64_t n_sparse, int64_t n_dense, void* vs, uint8_t* es, int operand_nonneg,
+                        const unsigned long long* nan_flag, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
-  K4Args pa, pb;
-  int rc = k4_prepare(vals_a, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs_a, es_a, nullptr, st, &pa, 2 * n_dense);
+  K4Args pa;
+  int rc = k4_prepare(vals, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs, es, nullptr, st, &pa, 2 * n_dense);
   if (rc) return rc;
-  const bool two = vals_b != nullptr;
-  if (two && (rc = k4_prepare(vals_b, meta_hw, n, h, feat_pos, n_sparse, n_dense, vs_b, es_b, nullptr, st, &pb,
-                              2 * n_dense)))
-    return rc;
-  if (n == 0 || h == 0) return S24_OK;
-  K4xArgs a{{static_cast<const __nv_bfloat16*>(vals_a), static_cast<const __nv_bfloat16*>(vals_b)},
-            meta_hw,
-            static_cast<int>(n),
-            static_cast<int>(h),
-            feat_pos,
-            static_cast<int>(2 * n_dense),
-            {static_cast<__nv_bfloat16*>(vs_a), static_cast<__nv_bfloat16*>(vs_b)},
-            {es_a, es_b},
-            row_map};
-  dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
-  if (two)
-    (a_nonneg ? k_feature_split_x<2, true> : k_feature_split_x<2, false>)<<<grid, 256, 0, st>>>(a);
-  else
-    (a_nonneg ? k_feature_split_x<1, true> : k_feature_split_x<1, false>)<<<grid, 256, 0, st>>>(a);
-  return check_launch("k_feature_split_x");
-}
-
-int s24_feature_split_id(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
-                         int64_t n_dense, void* vs, uint8_t* es, unsigned long long* stats, int operand_nonneg,
-                         void* stream) {
-  if (n < 0 || h < 0 || n_dense < 0 || n_dense > h) return fail(S24_ERR_DIMENSION, "bad feature split shape");
-  if (n % 128 != 0 || h % 128 != 0) return fail(S24_ERR_DIMENSION, "feature split needs n, h multiples of 128");
-  if (!vals || !meta_hw || !feat_pos || !vs || !es) return fail(S24_ERR_DIMENSION, "null operand");
-  if (!aligned16(vals) || !aligned16(vs) || !aligned16(es) || !aligned16(meta_hw))
+  if (!vals || !meta_hw || !feat_pos) return fail(S24_ERR_DIMENSION, "null operand");
+  if (!aligned16(vals) || !aligned16(vs) || !aligned16(meta_hw))
     return fail(S24_ERR_DIMENSION, "operands must be 16-byte aligned");
   if (n == 0 || h == 0) return S24_OK;
-  auto st = static_cast<cudaStream_t>(stream);
-  K4IdArgs a{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
-             static_cast<int>(n_dense), static_cast<int>((2 * n_dense + 127) / 128 * 128),
-             static_cast<__nv_bfloat16*>(vs), es, stats};
+  K4xArgs a{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
+            static_cast<int>(2 * n_dense), static_cast<__nv_bfloat16*>(vs), es, nan_flag};
   dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
-  const bool nn = operand_nonneg != 0;
-  if (stats)
-    (nn ? k_feature_split_id<true, true> : k_feature_split_id<true, false>)<<<grid, 256, 0, st>>>(a);
-  else
-    (nn ? k_feature_split_id<false, true> : k_feature_split_id<false, false>)<<<grid, 256, 0, st>>>(a);
-  return check_launch("k_feature_split_id");
+  (operand_nonneg ? k_feature_split_x<true> : k_feature_split_x<false>)<<<grid, 256, 0, st>>>(a);
+  return check_launch("k_feature_split_x");
 }
 
 int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, const int* feat_pos,
@@ -676,11 +642,6 @@ int s24_feature_split(const void* vals, const uint8_t* meta_hw, int64_t n, int64
   a.stats = stats;
   a.nonneg = operand_nonneg ? 1 : 0;
   dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
-  static const int env_ctas = [] {
-    const char* e = std::getenv("S24_K4_CTAS");  // experiments: persistent CTA count
-    return e ? std::atoi(e) : 0;
-  }();
-  if (env_ctas > 0 && env_ctas < static_cast<long long>(grid.x) * grid.y) grid = dim3(env_ctas, 1);
   if (stats)
     (a.nonneg ? k_feature_split<true, true> : k_feature_split<true, false>)<<<grid, 256, 0, st>>>(a);
   else

@@ -3,21 +3,20 @@ for the reference's pkg/src/srelu24/ffn.py (ffn_forward / ffn_backward and
 their dataclasses; activation = squared_relu).
 
 Recipe forward (ref ffn.py:276-363), one device pass each:
-  K1  Y1 = x . W1 -> relu^2 -> token-wise 2:4          (tcgen05 GEMM, fused epilogue:
-      compressed act + hw metadata + per-feature counts + drop stats; input row
-      r is written as act row perm[r], i.e. permute_rows folded into the store)
+  K6  x_in = permute_rows(x, perm)                     (row gather, padded to 128 rows)
+  K1  Y1 = x_in . W1 -> relu^2 -> token-wise 2:4       (tcgen05 GEMM, fused epilogue:
+      compressed act + hw metadata + per-feature counts + drop stats)
   K2  out = inverse_permute_rows(act_sp . W2)          (tcgen05.mma.sp, row map epilogue)
   side stream, next to K2:
   K7  plan = partition_features(counts, ratio)         (device radix select)
-  K6  x_in = permute_rows(x, perm)                     (row gather, dW1 operand)
-  K4  feature-wise 2:4 split of act (sparse features) + dense columns
+  K4  feature-wise 2:4 split of act (sparse features) + dense features as row pairs
 Recipe backward (ref ffn.py:366-451):
-  K3  g_pre = (dY . W2^T) * 2 relu(y1) on the forward keep pattern (fused,
-      compressed, rows paired with act row perm[r])
+  K6  g_c = permute_rows(dY, perm)
+  K3  g_pre = (g_c . W2^T) * 2 relu(y1) on the forward keep pattern (fused, compressed)
   K2  dX = inverse_permute_rows(g_pre_sp . W1^T)       (exact: forward metadata)
-  side stream: K6 g_c = permute_rows(dY, perm); K4 split of g_pre (next to dX)
-  K5  dW2 = split(act)^T g_c ; dW1 = (split(g_pre)^T x_in)^T  (one grouped sparse
-      launch + dense remainders, feature-index scatter / transpose in the epilogue)
+      side stream, next to it: K4 split of g_pre
+  K5  dW2 = split(act)^T g_c ; dW1 = (split(g_pre)^T x_in)^T  (one grouped 2:4 launch,
+      feature-index scatter / transpose in the epilogue)
 Dense mode runs the same GEMM kernels with dense operands (the "dense twin").
 
 Tensors are bf16 on the device (numpy float32 inputs are uploaded and rounded
@@ -26,7 +25,6 @@ to bf16). Weight gradients are fp32, activations/outputs bf16.
 
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass, field, replace
 
 import torch
@@ -43,99 +41,20 @@ from .sparse24 import (
 )
 from .splitgemm import (
     FeatureSplit,
-    FusedFeatureOperand,
-    alloc_feature_split,
-    k4_job_args,
-    run_feature_split,
-    side_stream,
     SplitPlan,
+    alloc_feature_split,
     feature_split,
-    fused_weight_grad,
     pad_plan,
     partition_features,
     partition_features_padded,
+    run_feature_split,
+    side_stream,
     split_gemm_macs,
     split_weight_grad,
     split_weight_grad_pair,
-    run_feature_split_dual,
 )
 
 ACTIVATIONS = ("squared_relu", "swiglu")
-
-# Where the feature-wise 2:4 operands of the split weight-gradient GEMMs come
-# from: False (default) = the standalone K4 kernel after the plan is known;
-# True = fused into the K1 / K3 epilogues for every feature (csrc/fwsel.cuh).
-# Both are bit-identical; on B200 the fused variant currently makes the K1/K3
-# epilogues the bottleneck, so it is opt-in.
-FUSED_FEATURE_SPLIT = os.environ.get("S24_FUSED_FW", "0") == "1"
-
-# How the standalone K4 runs next to the sparse GEMM that precedes its use
-# (fwd.out for the activation split, bwd.d_x for the g_pre split):
-#   "side"       -- on a side stream, co-resident with the GEMM (the sparse
-#                   GEMMs cap their registers to leave room for it)  [default]
-#   "background" -- inside the GEMM, in its idle epilogue warps (s24_spmm_bg)
-#   "inline"     -- serialized on the main stream
-#   "gemm"       -- inside the GEMM, by extra warps that split its own A
-#                   pipeline stages (s24_spmm_fs, csrc/k4s.cuh)
-K4_MODE = os.environ.get("S24_K4_MODE", "side")
-# Both split weight gradients in one grouped sparse launch (s24_spmm_pair)
-# when no per-gradient hook needs dW2 early. S24_PAIRED_WGRAD=0 disables.
-PAIRED_WEIGHT_GRADS = os.environ.get("S24_PAIRED_WGRAD", "1") == "1"
-# Gather the permuted copies x_in / g_c (weight-gradient operands only) on the
-# side stream next to the GEMMs ("1") or on the main stream right before
-# their first use ("0").
-SIDE_GATHERS = os.environ.get("S24_SIDE_GATHERS", "1") == "1"
-# K1 / K3 read x / dY unpermuted and apply the permutation as an epilogue row
-# map ("1"), or read the gathered copies x_in / g_c ("0").
-ROWMAP_GEMMS = os.environ.get("S24_ROWMAP", "0") == "1"
-# K3 alone row-mapped (dY read as is; its epilogue reads / writes the act and
-# g_pre rows perm[r] with whole-sector stores): the g_c gather leaves the
-# critical path for the side stream (dW2's B operand only)
-ROWMAP_K3 = os.environ.get("S24_ROWMAP_K3", os.environ.get("S24_ROWMAP", "0")) == "1"
-# Feature-wise split in the paired layout: the dense features travel inside
-# the 2:4 weight-gradient operand as fixed-selector row pairs, so no dense
-# remainder GEMM / split-K reduction runs ("1"); "0": separate dense operand.
-PAIRED_DENSE = os.environ.get("S24_PAIRED_DENSE", "1") == "1"
-# ... and in the identity layout (coalesced K4, csrc/k4id.cuh): rows in
-# feature order after the dense pairs ("1"), or rank order ("0").
-IDENTITY_LAYOUT = os.environ.get("S24_IDENTITY_LAYOUT", "0") == "1"
-# Where the feature-wise split of act (K4) runs on the side stream: next to
-# fwd.out in the forward ("0"), or next to K3 at the start of the backward
-# ("1": K3 is tensor/epilogue-bound and leaves room for it, fwd.out is
-# operand-feed-bound).
-ACT_SPLIT_IN_BWD = os.environ.get("S24_ACT_SPLIT_IN_BWD", "0") == "1"
-# One K4 pass for the activation and g_pre together (shared metadata work),
-# next to the dX GEMM in the backward ("1"), instead of two passes.
-DUAL_K4 = os.environ.get("S24_DUAL_K4", "0") == "1"
-# Backward tail order: dW2 on the main stream next to K4(g_pre) on the side
-# stream, then dW1 (side, after K4) and dX (third stream, after K3), so each
-# persistent GEMM's last partial wave is filled by the next one's CTAs ("1");
-# or dX next to K4(g_pre), then both weight gradients in one grouped launch ("0").
-WGRAD_OVERLAP = os.environ.get("S24_WGRAD_OVERLAP", "0") == "1"
-# Token-order storage ("1"): the recipe's activations stay in the caller's
-# token order -- K1 reads x and fwd.out writes out without row maps, K3 reads
-# dY and dX is written without one -- and the compute frame's permutation is
-# applied only where the backward needs it: inside K4 (row-mapped reads) and
-# in the permuted copies x_in / g_c that feed the weight-gradient GEMMs, both
-# on the side stream. "0": gather x / dY into the permuted frame before K1 / K3.
-# Measured slower on B200 (2.06 vs 1.99 ms at c2: row-mapped K4 reads scatter
-# over the whole activation, and the overlapped gathers slow K1 / K3 more than
-# the serialized ones cost), so opt-in.
-TOKEN_ORDER_STORAGE = os.environ.get("S24_TOKEN_ORDER", "0") == "1"
-# Side-stream start in the forward: right after K1 ("0": K4(act) co-runs with
-# fwd.out, a 2:4 GEMM) or after fwd.out ("1": K4(act) co-runs with K3, dense).
-K4_AFTER_FWD_OUT = os.environ.get("S24_K4_LATE", "0") == "1"
-
-
-def _dual_k4() -> bool:
-    lay = _layout()
-    return DUAL_K4 and K4_MODE == "side" and lay["paired"] and not lay["identity"]
-
-
-def _layout() -> dict:
-    """Layout of the feature-wise split operands (see splitgemm.FeatureSplit)."""
-    paired = PAIRED_DENSE and K4_MODE != "background"  # the in-GEMM K4 job writes the separate layout
-    return {"paired": paired, "identity": paired and IDENTITY_LAYOUT}
 FORWARD_MODES = ("dense", "sparse24")
 BACKWARD_MODES = ("dense", "naive_sparse", "split_masked")
 
@@ -234,46 +153,65 @@ class FfnCache:
     act_meta  uint8 hw metadata of the forward keep pattern
     act_dense bf16 [n, h] activation (dense forward only)
     pre_act   fp32 [n, h] pre-activation, kept only when the backward needs
-              relu(y1) outside the keep mask (mask_grad_with_fwd=False)
-    perm / perm_dev / inv_dev : host permutation and its device copies
+              relu(y1) outside the keep mask (mask_grad_with_fwd=False) or the
+              caller asked for it (keep_pre_act, parity checks)
+    perm / inv_dev : the permutation and its inverse (int32 device tensors)
+
+    The split plan, x_in's permuted copy and the feature-wise split of act are
+    produced on a side stream next to fwd.out; `plan` and `x_in` make the
+    caller's current stream wait for that work before handing them out, so
+    reading them right after ffn_forward is safe. The backward uses the raw
+    fields and joins the side stream only where it consumes them.
     """
 
-    x_in: torch.Tensor
     n: int
-    act_vals: torch.Tensor | None
-    act_meta: torch.Tensor | None
-    act_dense: torch.Tensor | None
-    pre_act: torch.Tensor | None
-    perm: object
-    perm_dev: torch.Tensor | None
-    inv_dev: torch.Tensor | None
-    plan: SplitPlan | None
-    stats: SparsifyStats | None
-    counts: torch.Tensor | None
-    census: list[GemmEvent]
     config: FfnConfig
-    gate: torch.Tensor | None = None
-    act_fw: FusedFeatureOperand | None = None  # feature-wise 2:4 act of all features (from K1)
-    act_split: FeatureSplit | None = None  # feature-wise split of act (K4, run during fwd.out)
-    act_split_ready: object = None  # CUDA event after which act_split is complete (side-stream K4)
-    x_in_ready: object = None  # CUDA event after which x_in is complete (gathered on the side stream)
+    census: list[GemmEvent]
+    _x_in: torch.Tensor | None = None
+    act_vals: torch.Tensor | None = None
+    act_meta: torch.Tensor | None = None
+    act_dense: torch.Tensor | None = None
+    pre_act: torch.Tensor | None = None
+    perm_dev: torch.Tensor | None = None
+    inv_dev: torch.Tensor | None = None
+    _plan: SplitPlan | None = None
+    stats: SparsifyStats | None = None
+    counts: torch.Tensor | None = None
+    stats_dev: torch.Tensor | None = None  # int64 [3]: K1's nonzeros before / after, NaN-kept flag
+    act_split: FeatureSplit | None = None  # feature-wise split of act (K4, run next to fwd.out)
+    side_ready: object = None  # CUDA event after which the side-stream work of the forward is complete
     # fp8_emulation (fp8.py): act_vals holds the dequantized activation (the
     # reference's act_sparse); K3 recovers relu(y1) from the unquantized one
     act_raw: torch.Tensor | None = None
     act_meta8: torch.Tensor | None = None  # act metadata in the e4m3 operand-E layout
     act_f32: torch.Tensor | None = None  # dense fp8 forward: the fp32 activation
     f8: dict | None = None  # e4m3 backward operands prepared next to the forward GEMMs (fp8.py)
-    # token-order storage (TOKEN_ORDER_STORAGE): act_vals / act_meta rows are in
-    # the caller's token order; compute-frame token j is storage row row_frame[j]
-    row_frame: torch.Tensor | None = None
     # padded FFN (model dim % 32 or hidden width % 128 != 0, see ffn_forward):
     # this cache is the caller's view of d_valid x h_valid features; `core` is
     # the device cache of the zero-padded FFN the backward runs on. On a core
-    # cache, plan_valid is the plan of the real features (plan: the padded one).
+    # cache, plan_valid is the plan of the real features (_plan: the padded one).
     core: "FfnCache | None" = None
     d_valid: int | None = None
     h_valid: int | None = None
     plan_valid: SplitPlan | None = None
+
+    def _join(self) -> None:
+        if self.side_ready is not None:
+            torch.cuda.current_stream().wait_event(self.side_ready)
+
+    @property
+    def x_in(self) -> torch.Tensor | None:
+        self._join()
+        return self._x_in
+
+    @property
+    def plan(self) -> SplitPlan | None:
+        self._join()
+        return self._plan
+
+    @property
+    def perm(self) -> torch.Tensor | None:
+        return self.perm_dev
 
     # Side-stream work of the forward reads and writes tensors allocated on
     # the main stream (no record_stream: its deferred frees stall the caching
@@ -282,11 +220,15 @@ class FfnCache:
     # to new main-stream work while the side stream still uses it.
     def __del__(self):
         try:
-            ev = self.act_split_ready or self.x_in_ready
-            if ev is not None and torch.cuda.is_initialized():
-                torch.cuda.current_stream(self.act_vals.device if self.act_vals is not None else None).wait_event(ev)
+            if self.side_ready is not None and torch.cuda.is_initialized():
+                torch.cuda.current_stream(self.side_ready_device).wait_event(self.side_ready)
         except Exception:  # interpreter shutdown
             pass
+
+    @property
+    def side_ready_device(self):
+        t = self.act_vals if self.act_vals is not None else self._x_in
+        return t.device if t is not None else None
 
     @property
     def act_sparse(self) -> Sparse24Matrix | None:
@@ -300,14 +242,7 @@ class FfnCache:
             hv = self.h_valid
             return Sparse24Matrix(self.n, hv, TOKEN_WISE, full.data[:, : hv // 2].contiguous(), None,
                                   meta_ref_cache=full.meta[:, : hv // 4].contiguous())
-        stored = Sparse24Matrix(self.n, h, TOKEN_WISE, self.act_vals, self.act_meta)
-        if self.row_frame is None:
-            return stored
-        # token-order storage: gather the rows into the compute frame (API view only)
-        from .splitgemm import frame_rows_compressed
-
-        data, hw = frame_rows_compressed(self.act_vals, self.act_meta, self.row_frame, self.n, h)
-        return Sparse24Matrix(self.n, h, TOKEN_WISE, data, hw)
+        return Sparse24Matrix(self.n, h, TOKEN_WISE, self.act_vals, self.act_meta)
 
     @property
     def fwd_mask(self) -> torch.Tensor | None:
@@ -328,6 +263,11 @@ class FfnGrads:
     census: list[GemmEvent] = field(default_factory=list)
     stats_act: SparsifyStats | None = None  # feature-wise drops of the act split (dW2)
     stats_grad: SparsifyStats | None = None  # feature-wise drops of the g_pre split (dW1)
+    # diagnostic views (parity checks): g_pre as K3 stored it (token-wise, on
+    # the forward metadata, compute frame) and the feature-wise split of it
+    # the dW1 GEMM consumed (the act split is FfnCache.act_split)
+    g_pre_sparse: Sparse24Matrix | None = None
+    g_split: FeatureSplit | None = None
 
 
 def act_squared_relu(pre):
@@ -391,11 +331,17 @@ def _plan_split(counts, ratio: float, plan: SplitPlan | None, h: int, h_valid: i
 
 
 def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, keep_pre_act: bool = False,
-                for_backward: bool = True):
+                for_backward: bool = True, counts_hook=None):
     """Run the forward pass; returns (out [n, d] bf16, FfnCache) (ref ffn.py:276-363).
     keep_pre_act=True also stores the fp32 pre-activation in the cache (parity
     tests use it to replay the selection on identical inputs). for_backward=False
-    (inference prefill) skips the feature-wise split the backward would need.
+    (inference prefill) skips what only the backward needs: the token
+    permutation (every forward stage maps one token row to one output row, so
+    the output is the same bits), x_in and the feature-wise split.
+    counts_hook(counts): called on the current stream right after K1 with the
+    int32 per-feature nonzero counts, before the split plan is computed from
+    them (data parallelism all-reduces them here so that every rank uses the
+    plan of the global batch).
 
     Any d and h % 4 == 0 (the reference's shapes): the device GEMMs tile the
     model dim by 32 and the hidden width by 128, so other sizes run on the FFN
@@ -409,20 +355,21 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     d, h = p.model_dim, p.hidden_dim
     dp, hp = _pad_to(d, 32), _pad_to(h, 128)
     if (dp, hp) == (d, h):
-        return _ffn_forward(x, p, cfg, plan, keep_pre_act, for_backward)
+        return _ffn_forward(x, p, cfg, plan, keep_pre_act, for_backward, counts_hook=counts_hook)
     if x.shape[1] != d:
         raise DimensionError(f"input width {x.shape[1]} does not match w1 {tuple(p.w1.shape)}")
     if plan is not None and plan.hidden_dim != h:
         raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h}")
+    hook = None if counts_hook is None else (lambda c: counts_hook(c[:h]))
     out, core = _ffn_forward(_pad_cols(x, dp), _pad_params(p, dp, hp), cfg, plan, keep_pre_act, for_backward,
-                             h_valid=h)
+                             h_valid=h, counts_hook=hook)
     n = core.n
     view = replace(core, pre_act=core.pre_act[:, :h] if core.pre_act is not None else None,
                    counts=core.counts[:h] if core.counts is not None else None,
-                   plan=core.plan_valid if core.plan_valid is not None else core.plan,
+                   _plan=core.plan_valid if core.plan_valid is not None else core._plan,
                    stats=SparsifyStats(n * h, core.stats._dev) if core.stats is not None else None,
                    census=_census_real(core.census, n, d, h, core.plan_valid, cfg),
-                   act_split_ready=None, x_in_ready=None, core=core, d_valid=d, h_valid=h, plan_valid=None)
+                   core=core, d_valid=d, h_valid=h, plan_valid=None)
     return (out[:, :d].contiguous() if dp != d else out), view
 
 
@@ -439,8 +386,39 @@ def _census_real(events, n: int, d: int, h: int, plan: SplitPlan | None, cfg: Ff
     return out
 
 
+def _all_sparse_plan(h: int, dev) -> SplitPlan:
+    """naive_sparse: every feature feature-wise 2:4 (ref ffn.py:430-437)."""
+    pos = torch.arange(h, dtype=torch.int32, device=dev)
+    return SplitPlan(h, 1.0, torch.zeros(h, dtype=torch.int64, device=dev), pos,
+                     torch.empty(0, dtype=torch.int32, device=dev), pos)
+
+
+def _frame_rows(a: torch.Tensor, npad: int, src_rows, fill: bool = True) -> torch.Tensor:
+    """The compute-frame copy of a [n, d] input: rows permuted (out[i] =
+    a[src_rows[i]]) and zero-padded to npad rows. Returns `a` itself when
+    neither applies. fill=False only allocates (fill with _fill_frame_rows)."""
+    n = a.shape[0]
+    if src_rows is None and npad == n:
+        return a
+    out = torch.empty(npad, a.shape[1], dtype=a.dtype, device=a.device)
+    if fill:
+        _fill_frame_rows(out, a, src_rows)
+    return out
+
+
+def _fill_frame_rows(out: torch.Tensor, a: torch.Tensor, src_rows) -> None:
+    """Fill a _frame_rows buffer on the current stream (K6 gather or copy)."""
+    n = a.shape[0]
+    if out.shape[0] > n:
+        out[n:].zero_()
+    if src_rows is not None:
+        gather_rows(a, src_rows, out)
+    else:
+        out[:n].copy_(a)
+
+
 def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_pre_act: bool, for_backward: bool,
-                 h_valid: int | None = None):
+                 h_valid: int | None = None, counts_hook=None):
     """ffn_forward on device-tileable sizes (d % 32 == 0, h % 128 == 0).
     h_valid: the FFN is zero-padded beyond its first h_valid features."""
     require_cuda()
@@ -456,210 +434,93 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
         raise DimensionError(f"sparse modes need token count % 4 == 0, got {n}")
     h = p.hidden_dim
     _check_dims(n, d, h)
+    if plan is not None and plan.hidden_dim != (h_valid or h):
+        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h_valid or h}")
     if cfg.fp8_emulation:
         # e4m3 operands on the kind::f8f6f4 tensor cores (fp8.py)
         from .fp8 import ffn_forward_f8
 
-        return ffn_forward_f8(x, p, cfg, plan, keep_pre_act, for_backward, h_valid=h_valid)
+        return ffn_forward_f8(x, p, cfg, plan, keep_pre_act, for_backward, h_valid=h_valid,
+                              counts_hook=counts_hook)
     dev = x.device
     s = stream()
     npad = pad128(n)
     census: list[GemmEvent] = []
 
-    perm = perm_dev = inv_dev = None
-    # The token permutation only shapes the feature-wise groups of the
-    # backward; every forward stage maps one token row to one output row, so an
-    # inference forward (for_backward=False) skips it: same bits, no gathers.
-    permute = cfg.permute_tokens and sparse_fwd and for_backward
-    if permute:
-        perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
-        perm = perm_dev
-
     out = torch.empty(n, d, dtype=BF16, device=dev)
     if not sparse_fwd:
+        # ------------------------------------------------------------ dense twin
         act = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_gemm_relu2", ptr(x), d, ptr(p.w1), h, n, h, d, ptr(act), h, s)
         census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
         _lib.call("s24_gemm", ptr(act), 0, h, ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d, None, 0, -1, None, s)
         census.append(GemmEvent("fwd.out", False, gemm_macs(n, h, d)))
-        cache = FfnCache(x, n, None, None, act, None, None, None, None, None, None, None, census, cfg)
-        return out, cache
+        x_in = _frame_rows(x, npad, None) if for_backward else None
+        return out, FfnCache(n, cfg, census, _x_in=x_in, act_dense=act)
 
+    # The compute frame is the token-permuted order (ref ffn.py:297-303). The
+    # permutation only shapes the feature-wise groups of the backward, so an
+    # inference forward skips it.
+    perm_dev = inv_dev = None
+    if cfg.permute_tokens and for_backward:
+        perm_dev, inv_dev = device_permutation(cfg.permute_seed, n, dev)
     act_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
     act_meta = torch.empty(_lib.meta_hw_bytes(n, h), dtype=torch.uint8, device=dev)
     if npad > n:
         act_vals[n:].zero_()
         act_meta[(n // 128) * (h // 128) * 2048:].fill_(0x44)
     counts = torch.zeros(h, dtype=torch.int32, device=dev)
-    stats_dev = torch.zeros(2, dtype=torch.int64, device=dev)
+    stats_dev = torch.zeros(3, dtype=torch.int64, device=dev)
     need_pre = keep_pre_act or not cfg.mask_grad_with_fwd
     pre = torch.empty(n, h, dtype=F32, device=dev) if need_pre else None
-    # the split / naive weight-gradient GEMMs read the activation feature-wise
-    # 2:4 compressed; K1's epilogue produces that operand for every feature
-    act_fw = FusedFeatureOperand.alloc(h, npad, dev) if (FUSED_FEATURE_SPLIT and cfg.backward_mode != "dense") else None
-    fw_args = act_fw.args() if act_fw is not None else (None, None, None, 0)
-
-    # The compute frame is the token-permuted order (ref ffn.py:297-303). K1
-    # reads x as is and writes input row r as activation row perm[r] (row map
-    # in its epilogue); the permuted copy x_in (zero rows up to a multiple of
-    # 128) is only the B operand of the dW1 GEMM, so it is gathered off the
-    # critical path. The fused feature-wise epilogue needs permuted input rows.
-    side = side_stream(dev) if (for_backward and K4_MODE == "side") else None
-    # (inference prefill, for_backward=False, needs no x_in at all)
-    x_in = _frame_rows(x, npad, inv_dev if permute else None, defer=True) if for_backward else None
-    k1_in, k1_map = x, (perm_dev if permute else None)
-    row_frame = None
-    if (TOKEN_ORDER_STORAGE and permute and side is not None and cfg.mask_grad_with_fwd and act_fw is None
-            and cfg.backward_mode in ("split_masked", "naive_sparse") and _layout()["paired"]
-            and not _layout()["identity"] and not _dual_k4() and not ACT_SPLIT_IN_BWD):
-        # token-order storage: K1 on x as is; the permutation is applied by K4
-        # and by the side-stream gathers (see TOKEN_ORDER_STORAGE)
-        row_frame = inv_dev if npad == n else torch.cat(
-            [inv_dev, torch.arange(n, npad, dtype=inv_dev.dtype, device=dev)])
-        k1_map = None
-    elif (act_fw is not None or not ROWMAP_GEMMS) and permute:
-        if x_in is None:
-            x_in = _frame_rows(x, npad, inv_dev, defer=True)
-        _fill_frame_rows(x_in, x, inv_dev)
-        k1_in, k1_map = x_in, None
+    # K1 reads the permuted copy x_in (K6 gather on the main stream); without
+    # a permutation x itself, and the padded copy the dW1 GEMM reads is made on
+    # the side stream
+    x_in = None
+    k1_in = x
+    if perm_dev is not None:
+        x_in = k1_in = _frame_rows(x, npad, inv_dev)
+    elif for_backward:
+        x_in = _frame_rows(x, npad, None, fill=False)
     _lib.call("s24_fwd_gemm1_fused", ptr(k1_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta),
-              ptr(counts), ptr(stats_dev), ptr(pre), *fw_args, ptr(k1_map), s)
+              ptr(counts), ptr(stats_dev), ptr(pre), s)
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
-    if plan is not None and plan.hidden_dim != (h_valid or h):
-        raise DimensionError(f"plan built for {plan.hidden_dim} features, FFN has {h_valid or h}")
-    need_plan = cfg.backward_mode == "split_masked"
-    plan_api = plan
+    if counts_hook is not None:
+        counts_hook(counts)
 
     # fwd.out on tensor cores (inverse permutation as its epilogue row map).
-    # Next to it, on a side stream: the split plan (K7), x_in, and -- when the
-    # backward will need it -- K4, the feature-wise split of act.
-    act_split = None
-    split_ready = x_in_ready = None
-    plan_out = plan
-    want_split = for_backward and cfg.backward_mode != "dense" and act_fw is None
-    defer_split = want_split and side is not None and (ACT_SPLIT_IN_BWD or _dual_k4())
-    want_split = want_split and not defer_split
-
-    def fwd_out(st):
-        _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-                  ptr(inv_dev if row_frame is None else None), 0, -1, None, 0, st)
-
-    if side is not None:
-        main = torch.cuda.current_stream()
-        if not K4_AFTER_FWD_OUT:
-            side.wait_stream(main)  # K1's outputs are ready; the side work must not wait for fwd.out
-        fwd_out(s)
-        if K4_AFTER_FWD_OUT:
-            side.wait_stream(main)
-        if need_plan or plan is not None:
-            plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid, side)
-        bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
-        if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, row_map=row_frame, **_layout())
-        with torch.cuda.stream(side):
-            if SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
-                _fill_frame_rows(x_in, x, inv_dev)
-            if want_split:  # (relu^2: >= 0)
-                run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True, row_map=row_frame)
-                if act_split.pair_rows >= 0 and not act_split.identity:
-                    bg_plan.paired_row_map  # (the weight-gradient row map, built here off the main stream)
-            ev = torch.cuda.Event()
-            ev.record(side)
-        split_ready = x_in_ready = ev
-        if not SIDE_GATHERS and x_in is not None and x_in is not x and k1_in is not x_in:
-            _fill_frame_rows(x_in, x, inv_dev)
-    else:
-        if need_plan or plan is not None:
-            plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid)
-        if x_in is not None and x_in is not x and k1_in is not x_in:
-            _fill_frame_rows(x_in, x, inv_dev)
-        bg_plan = plan_out if need_plan else _all_sparse_plan(h, dev)
-        if want_split:
-            act_split = alloc_feature_split(act_vals, act_meta, npad, h, bg_plan, **_layout())
-        if want_split and K4_MODE == "gemm" and _layout()["paired"] and not _layout()["identity"]:
-            # fwd.out whose CTAs also split their act stages feature-wise
-            _lib.call("s24_spmm_fs", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
-                      ptr(inv_dev), 0, -1, None, npad, ptr(bg_plan.feat_pos), bg_plan.n_sparse, bg_plan.n_dense,
-                      ptr(act_split.vs), ptr(act_split.es), 1, s)
-        elif want_split and K4_MODE == "background":
-            counter = torch.empty(1, dtype=torch.int32, device=dev)
-            _lib.call("s24_spmm_bg", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16,
-                      d, ptr(inv_dev), 0, -1, None,
-                      *k4_job_args(act_vals, act_meta, npad, h, bg_plan, act_split, counter), s)
-        else:
-            fwd_out(s)
-            if want_split:
-                run_feature_split(act_split, act_vals, act_meta, npad, h, bg_plan, nonneg=True)
-    census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
-    if row_frame is not None and pre is not None:
-        pre = pre[row_frame[:n].long()]  # (debug / parity view: the compute frame)
-    cache = FfnCache(x_in, n, act_vals, act_meta, None, pre, perm, perm_dev, inv_dev, plan_out,
-                     SparsifyStats(n * h, stats_dev), counts, census, cfg, act_fw=act_fw, act_split=act_split,
-                     act_split_ready=split_ready, x_in_ready=x_in_ready, row_frame=row_frame,
-                     plan_valid=plan_api if h_valid is not None else None)
-    return out, cache
-
-
-def _frame_rows(a: torch.Tensor, npad: int, src_rows, defer: bool = False) -> torch.Tensor:
-    """The compute-frame copy of a [n, d] input: rows permuted (out[i] =
-    a[src_rows[i]]) and zero-padded to npad rows. Returns `a` itself when
-    neither applies. defer=True only allocates (fill with _fill_frame_rows)."""
-    n = a.shape[0]
-    if src_rows is None and npad == n:
-        return a
-    out = torch.empty(npad, a.shape[1], dtype=a.dtype, device=a.device)
-    if not defer:
-        _fill_frame_rows(out, a, src_rows)
-    return out
-
-
-def _fill_frame_rows(out: torch.Tensor, a: torch.Tensor, src_rows) -> None:
-    """Fill a _frame_rows buffer on the current stream."""
-    n = a.shape[0]
-    if out.shape[0] > n:
-        out[n:].zero_()
-    if src_rows is not None:
-        gather_rows(a, src_rows, out)
-    else:
-        out[:n].copy_(a)
-
-
-
-
-
-def _spmm_with_split(launch_gemm, k4_work):
-    """Launch a sparse GEMM on the current stream and the K4 job `k4_work()`
-    next to it (K4_MODE "side": side stream, co-resident; "inline": after it).
-    Returns the CUDA event after which the K4 outputs are complete (None if
-    inline)."""
+    # Next to it, on the side stream: the split plan (K7), x_in's padded copy
+    # and -- when the backward will need it -- K4, the feature-wise split of
+    # act. Their outputs are allocated here, on the main stream.
     main = torch.cuda.current_stream()
-    if K4_MODE != "side":
-        launch_gemm(main.cuda_stream)
-        k4_work()
-        return None
-    side = side_stream(main.device)
-    side.wait_stream(main)  # K4's inputs are ready; it must not wait for the GEMM
-    launch_gemm(main.cuda_stream)
+    side = side_stream(dev)
+    side.wait_stream(main)
+    _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
+              ptr(inv_dev), 0, -1, None, 0, s)
+    census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))
+    plan_api = plan_out = plan
+    if cfg.backward_mode == "split_masked" or plan is not None:
+        plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid, side)
+    act_split = None
+    split = for_backward and cfg.backward_mode != "dense"
+    bplan = plan_out if cfg.backward_mode == "split_masked" else _all_sparse_plan(h, dev)
+    if split:
+        act_split = alloc_feature_split(act_vals, act_meta, npad, h, bplan)
     with torch.cuda.stream(side):
-        k4_work()
+        if x_in is not None and x_in is not k1_in and x_in is not x:
+            _fill_frame_rows(x_in, x, None)
+        if split:  # (relu^2: >= 0; NaN-aware only if K1 kept a NaN)
+            run_feature_split(act_split, act_vals, act_meta, npad, h, bplan, nonneg=True, nan_flag=stats_dev[2:])
+            bplan.paired_row_map  # (the weight-gradient row map, built here off the main stream)
         ev = torch.cuda.Event()
         ev.record(side)
-    return ev
-
-
-def _act_split(cache: FfnCache, npad: int, h: int, plan: SplitPlan):
-    """The feature-wise split of the cached activation (made by the forward
-    next to fwd.out when K4 runs on the side stream, else here)."""
-    if cache.act_split is None:
-        if cache.row_frame is not None:
-            fs = alloc_feature_split(cache.act_vals, cache.act_meta, npad, h, plan, paired=True,
-                                     row_map=cache.row_frame)
-            run_feature_split(fs, cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, row_map=cache.row_frame)
-            return fs
-        return feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, **_layout())
-    if cache.act_split_ready is not None:
-        torch.cuda.current_stream().wait_event(cache.act_split_ready)
-    return cache.act_split
+    if x_in is None and for_backward:
+        x_in = x
+    cache = FfnCache(n, cfg, census, _x_in=x_in, act_vals=act_vals, act_meta=act_meta, pre_act=pre,
+                     perm_dev=perm_dev, inv_dev=inv_dev, _plan=plan_out, stats=SparsifyStats(n * h, stats_dev[:2]),
+                     counts=counts, stats_dev=stats_dev, act_split=act_split, side_ready=ev,
+                     plan_valid=plan_api if h_valid is not None else None)
+    return out, cache
 
 
 def weight_grad_buffers(d: int, h: int, dev, bucket: torch.Tensor | None = None):
@@ -671,30 +532,16 @@ def weight_grad_buffers(d: int, h: int, dev, bucket: torch.Tensor | None = None)
     return bucket[: d * h].view(d, h), bucket[d * h:].view(h, d)
 
 
-_third_streams: dict = {}
-
-
-def _third_stream(device) -> torch.cuda.Stream:
-    idx = device.index if device.index is not None else torch.cuda.current_device()
-    st = _third_streams.get(idx)
-    if st is None:
-        st = _third_streams[idx] = torch.cuda.Stream(device=device)
-    return st
-
-
-def _all_sparse_plan(h: int, dev) -> SplitPlan:
-    pos = torch.arange(h, dtype=torch.int32, device=dev)
-    return SplitPlan(h, 1.0, torch.zeros(h, dtype=torch.int64, device=dev), pos,
-                     torch.empty(0, dtype=torch.int32, device=dev), pos)
-
-
 def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_ready=None,
                  grad_bucket: torch.Tensor | None = None) -> FfnGrads:
     """Backward matching the cached forward (ref ffn.py:366-451).
 
     grad_ready(name, tensor), if given, is called as soon as d_w2 and then
-    d_w1 are final on the current stream (used by the data-parallel step to
-    launch their all-reduce while the rest of the backward runs).
+    d_w1 are final on the current stream (the data-parallel step launches
+    their all-reduce there). With a hook the recipe runs dW2 right after K3,
+    then dX and dW1, so that dW2's all-reduce overlaps the rest of the
+    backward; without one, both weight gradients run in one grouped launch
+    at the end.
     grad_bucket: optional fp32 buffer of 2*d*h elements; d_w1 and d_w2 are then
     written as views into it ([d_w1 | d_w2]), so one collective covers both.
     A padded forward (see ffn_forward) runs the padded backward and returns
@@ -720,7 +567,7 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     d_w1.copy_(gr.d_w1[:d, :h])
     notify("d_w1", d_w1)
     d_x = gr.d_x[:, :d].contiguous() if dp != d else gr.d_x
-    return FfnGrads(d_w1, d_w2, d_x, None, _census_real(gr.census, n, d, h, cache.plan, cfg),
+    return FfnGrads(d_w1, d_w2, d_x, None, _census_real(gr.census, n, d, h, cache._plan, cfg),
                     _token_total(gr.stats_act, n, hp - h), _token_total(gr.stats_grad, n, hp - h))
 
 
@@ -741,9 +588,10 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         raise StateError("cache was produced under a different configuration")
     _unsupported(cfg)
     n = cache.n
-    if cache.x_in is None:
+    x_in = cache._x_in
+    if x_in is None:
         raise StateError("cache comes from an inference forward (for_backward=False)")
-    d = cache.x_in.shape[1]
+    d = x_in.shape[1]
     g_out = as_matrix(g_out, "g_out", BF16)
     if tuple(g_out.shape) != (n, d):
         raise StateError(f"gradient shape {tuple(g_out.shape)} does not match cached input {(n, d)}")
@@ -752,7 +600,7 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         raise StateError("sparse forward cache is missing the compressed activation")
     if not sparse_fwd and cache.act_dense is None:
         raise StateError("dense forward cache is missing the activation")
-    if cfg.backward_mode == "split_masked" and cache.plan is None:
+    if cfg.backward_mode == "split_masked" and cache._plan is None:
         raise StateError("split backward needs the plan computed in forward")
     h = p.hidden_dim
     if cfg.fp8_backward:
@@ -764,13 +612,12 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
     npad = pad128(n)
     census: list[GemmEvent] = []
     notify = grad_ready or (lambda name, t: None)
-
     d_w1, d_w2 = weight_grad_buffers(d, h, dev, grad_bucket)
     d_x = torch.empty(n, d, dtype=BF16, device=dev)
-    stats_a = stats_g = None
+    main = torch.cuda.current_stream()
 
     if not sparse_fwd:
-        # ---------------------------------------------------------- dense twin
+        # ------------------------------------------------------------ dense twin
         act = cache.act_dense
         g_pre = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_gemm_dact", ptr(g_out), d, ptr(p.w2), d, n, h, d, ptr(act), h, ptr(g_pre), h, s)
@@ -778,7 +625,7 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_out), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, None, s)
         census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
         notify("d_w2", d_w2)
-        _lib.call("s24_gemm", ptr(g_pre), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
+        _lib.call("s24_gemm", ptr(g_pre), 1, h, ptr(x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
         _lib.call("s24_gemm", ptr(g_pre), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d, None, 0, -1, None, s)
@@ -786,225 +633,107 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         return FfnGrads(d_w1, d_w2, d_x, None, census)
 
     # -------------------------------------------------------------- sparse forward
-    # g_pre on the forward keep pattern, compressed (exact; ref ffn.py:415-417, 443)
+    # g_c = permute_rows(dY) padded to npad rows: K3's A operand and dW2's B
+    g_c = _frame_rows(g_out, npad, cache.inv_dev)
+    # K3: g_pre on the forward keep pattern, compressed (exact; ref ffn.py:415-417, 443)
     g_vals = torch.empty(npad, h // 2, dtype=BF16, device=dev)
     if npad > n:
         g_vals[n:].zero_()
-    # K3's epilogue also emits the feature-wise 2:4 g_pre operand of the dW1
-    # GEMM when the split path will consume it
-    fused_g = FUSED_FEATURE_SPLIT and (
-        cfg.backward_mode == "split_masked" or (cfg.backward_mode == "naive_sparse" and cfg.mask_grad_with_fwd))
-    raw_naive = cfg.backward_mode == "naive_sparse" and not cfg.mask_grad_with_fwd
-    g_fw = FusedFeatureOperand.alloc(h, npad, dev) if fused_g else None
-    fw_args = g_fw.args() if g_fw is not None else (None, None, None, 0)
-    # The permuted, padded copy g_c of dY is only an operand of the weight
-    # gradients (B of dW2) and of the unmasked-derivative path, so it is
-    # gathered on the side stream while K3 reads dY as is (row map).
-    main = torch.cuda.current_stream()
-    side = side_stream(dev) if K4_MODE == "side" else None
-    g_c = _frame_rows(g_out, npad, cache.inv_dev, defer=True)
-    g_ready = None
-    rowmap = ROWMAP_K3 and g_fw is None
-    stored = cache.row_frame is not None  # token-order storage: K3 / dX need no frame rows
-    if stored and (side is None or g_fw is not None or not cfg.mask_grad_with_fwd):
-        raise StateError("token-order storage needs the side-stream backward with mask_grad_with_fwd")
-    if g_c is not g_out:
-        if not rowmap and cache.perm_dev is not None and not stored:
-            _fill_frame_rows(g_c, g_out, cache.inv_dev)  # K3 reads g_c
-        elif side is not None and SIDE_GATHERS:
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                _fill_frame_rows(g_c, g_out, cache.inv_dev)
-                g_ready = torch.cuda.Event()
-                g_ready.record(side)
-        elif side is None:
-            _fill_frame_rows(g_c, g_out, cache.inv_dev)
-    late_g_c = g_c is not g_out and side is not None and not SIDE_GATHERS and rowmap
-
-    def need_frame_inputs():
-        """Main-stream consumers of g_c / x_in wait for their side-stream gathers."""
-        nonlocal g_ready, late_g_c
-        if late_g_c:
-            _fill_frame_rows(g_c, g_out, cache.inv_dev)
-            late_g_c = False
-        if g_ready is not None:
-            main.wait_event(g_ready)
-            g_ready = None
-        if cache.x_in_ready is not None:
-            main.wait_event(cache.x_in_ready)
-
-    # the feature-wise split of act, when the forward left it for here: on the
-    # side stream next to K3
-    if cache.act_split is None and cache.act_fw is None and side is not None and \
-            cfg.backward_mode != "dense" and ACT_SPLIT_IN_BWD and not _dual_k4():
-        plan_a = _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else cache.plan
-        fa_b = alloc_feature_split(cache.act_vals, cache.act_meta, npad, h, plan_a, **_layout())
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            run_feature_split(fa_b, cache.act_vals, cache.act_meta, npad, h, plan_a, nonneg=True)
-            ev_a = torch.cuda.Event()
-            ev_a.record(side)
-        cache.act_split, cache.act_split_ready = fa_b, ev_a
-
-    # K3 reads dY unpermuted and pairs input row r with act / g_pre row
-    # perm[r]; the fused feature-wise epilogue needs the permuted rows
-    k3_in, k3_map = g_out, cache.perm_dev
-    if stored:
-        k3_in, k3_map = g_out, None  # dY rows pair with the stored act rows as they are
-    elif not rowmap and cache.perm_dev is not None:
-        need_frame_inputs()
-        k3_in, k3_map = g_c, None
     # (fp8 forward: relu(y1) comes from the unquantized activation)
     k3_act = cache.act_raw if cache.act_raw is not None else cache.act_vals
-    _lib.call("s24_bwd_dact_fused", ptr(k3_in), d, ptr(p.w2), d, n, h, d, ptr(k3_act), ptr(cache.act_meta),
-              ptr(g_vals), *fw_args, ptr(k3_map), s)
+    _lib.call("s24_bwd_dact_fused", ptr(g_c), d, ptr(p.w2), d, n, h, d, ptr(k3_act), ptr(cache.act_meta),
+              ptr(g_vals), s)
     census.append(GemmEvent("bwd.d_act", False, gemm_macs(n, d, h)))
     g_pre_dense = None
     if not cfg.mask_grad_with_fwd:
         # unmasked derivative: needs relu(y1) everywhere (fp32 pre-activation kept by the forward)
-        need_frame_inputs()
         G = torch.empty(n, h, dtype=F32, device=dev)
         _lib.call("s24_gemm", ptr(g_c), 0, d, ptr(p.w2), 0, d, n, h, d, ptr(G), _lib.F32, h, None, 0, -1, None, s)
         g_pre_dense = (G * act_squared_relu_grad(cache.pre_act)).to(BF16)
 
     mode = cfg.backward_mode
-    ev_dx = None
-    if mode != "dense":
-        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache.plan
-        macs_w = sp_gemm_macs(n, h, d) if mode == "naive_sparse" else split_gemm_macs(n, d, plan)
-    fg = None
-    fg_ready = None
-    if (WGRAD_OVERLAP and side is not None and cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None
-            and not raw_naive and grad_ready is None and cache.act_fw is None and _layout()["paired"]
-            and not _dual_k4()):
-        # dW2 (main) || K4(g_pre) (side) ; then dW1 (side) || dX (third stream)
-        ev_k3 = torch.cuda.Event()
-        ev_k3.record(main)
-        fa = _act_split(cache, npad, h, plan)
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame, **_layout())
-        need_frame_inputs()
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame)
-        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
-        with torch.cuda.stream(side):
-            split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
-            ev_w1 = torch.cuda.Event()
-            ev_w1.record(side)
-        third = _third_stream(dev)
-        third.wait_event(ev_k3)
-        with torch.cuda.stream(third):
-            _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16,
-                      d, ptr(None if stored else cache.inv_dev), 0, -1, None, 0, third.cuda_stream)
-            ev_x = torch.cuda.Event()
-            ev_x.record(third)
-        main.wait_event(ev_w1)
-        main.wait_event(ev_x)
-        census.append(GemmEvent("bwd.d_w2", True, macs_w))
-        census.append(GemmEvent("bwd.d_w1", True, macs_w))
-        census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
-        return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, fg.stats)
-    if cfg.mask_grad_with_fwd and mode != "dense" and g_fw is None and not raw_naive:
-        # dX first: its sparse GEMM carries the feature-wise split of g_pre (K4)
-        # as background work in its idle epilogue warps
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame, **_layout())
-        if K4_MODE == "gemm" and fg.pair_rows >= 0 and not fg.identity:
-            # dX whose CTAs also split their g_pre stages feature-wise
-            _lib.call("s24_spmm_fs", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16,
-                      d, ptr(cache.inv_dev), 0, -1, None, npad, ptr(plan.feat_pos), plan.n_sparse, plan.n_dense,
-                      ptr(fg.vs), ptr(fg.es), 0, s)
-        elif K4_MODE == "background":
-            counter = torch.empty(1, dtype=torch.int32, device=dev)
-            _lib.call("s24_spmm_bg", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x),
-                      _lib.BF16, d, ptr(cache.inv_dev), 0, -1, None,
-                      *k4_job_args(g_vals, cache.act_meta, npad, h, plan, fg, counter), s)
-        else:
-            dual = cache.act_split is None and cache.act_fw is None and _dual_k4()
-            fa = alloc_feature_split(cache.act_vals, cache.act_meta, npad, h, plan, **_layout()) if dual else None
-
-            def k4_side():
-                if dual:  # act (>= 0) and g_pre share the keep pattern: one pass for both
-                    run_feature_split_dual(fa, fg, cache.act_vals, g_vals, cache.act_meta, npad, h, plan)
-                else:
-                    run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan, row_map=cache.row_frame)
-
-            fg_ready = _spmm_with_split(
-                lambda st: _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h,
-                                     ptr(d_x), _lib.BF16, d, ptr(None if stored else cache.inv_dev), 0, -1, None,
-                                     0, st),
-                k4_side)
-            if dual:
-                cache.act_split, cache.act_split_ready = fa, fg_ready
-        ev_dx = GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d))
-
-    need_frame_inputs()
     if mode == "dense":
+        if cache.side_ready is not None:
+            main.wait_event(cache.side_ready)
         act = torch.empty(n, h, dtype=BF16, device=dev)
         _lib.call("s24_decompress_token", ptr(cache.act_vals), None, ptr(cache.act_meta), n, h, ptr(act), _lib.BF16, h, s)
-        if g_pre_dense is None:
+        gp = g_pre_dense
+        if gp is None:
             gp = torch.empty(n, h, dtype=BF16, device=dev)
             _lib.call("s24_decompress_token", ptr(g_vals), None, ptr(cache.act_meta), n, h, ptr(gp), _lib.BF16, h, s)
-        else:
-            gp = g_pre_dense
+        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
         _lib.call("s24_gemm", ptr(act), 1, h, ptr(g_c), 1, d, h, d, n, ptr(d_w2), _lib.F32, d, None, 0, -1, None, s)
-        census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
+        census.insert(1, GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
         notify("d_w2", d_w2)
-        _lib.call("s24_gemm", ptr(gp), 1, h, ptr(cache.x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
-        census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
+        _lib.call("s24_gemm", ptr(gp), 1, h, ptr(x_in), 1, d, h, d, n, ptr(d_w1), _lib.F32, h, None, 1, -1, None, s)
+        census.insert(2, GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
-    elif (grad_ready is None and cache.act_fw is None and g_fw is None and not raw_naive
-          and PAIRED_WEIGHT_GRADS):
-        # both split weight gradients in one grouped launch: dW2 = split(act)^T g_c
-        # and dW1^T = split(g_pre)^T x_in share (M, N, K) = (|S|, d, n), so the
-        # second fills the first one's partial last wave (no per-gradient hook
-        # to serve, hence only without grad_ready)
-        fa = _act_split(cache, npad, h, plan)
-        if fg is None:
-            fg = feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
-        elif fg_ready is not None:
-            torch.cuda.current_stream().wait_event(fg_ready)
-        split_weight_grad_pair(fa, fg, plan, g_c, cache.x_in, npad, d_w2, d_w1)
-        stats_a, stats_g = fa.stats, fg.stats
-        census.append(GemmEvent("bwd.d_w2", True, macs_w))
-        census.append(GemmEvent("bwd.d_w1", True, macs_w))
+        return FfnGrads(d_w1, d_w2, d_x, None, census)
+
+    # split_masked / naive_sparse: the weight gradients are feature-wise 2:4
+    # GEMMs over the split operands (K4 in the paired layout)
+    plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache._plan
+    macs_w = sp_gemm_macs(n, h, d) if mode == "naive_sparse" else split_gemm_macs(n, d, plan)
+    fa = cache.act_split
+    if fa is None:
+        raise StateError("cache is missing the feature-wise split of the activation")
+    raw_naive = mode == "naive_sparse" and not cfg.mask_grad_with_fwd
+    side = side_stream(dev)
+    if raw_naive:
+        # naive_sparse without the mask sparsifies the raw g_pre feature-wise
+        # (ref ffn.py:430-437); the split path always sees the masked g_pre
+        from .sparse24 import sparsify_feature_wise
+
+        gpad = torch.zeros(npad, h, dtype=BF16, device=dev)
+        gpad[:n] = g_pre_dense
+        sg, _, stats_g = sparsify_feature_wise(gpad)
+        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
+        main.wait_event(cache.side_ready)
+        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
+        census.insert(1, GemmEvent("bwd.d_w2", True, macs_w))
+        notify("d_w2", d_w2)
+        _lib.call("s24_spmm", ptr(sg.data), ptr(sg.meta_hw), ptr(x_in), 1, d, h, d, npad, ptr(d_w1), _lib.F32, h,
+                  None, 1, -1, None, 0, s)
+        census.insert(2, GemmEvent("bwd.d_w1", True, macs_w))
+        notify("d_w1", d_w1)
+        return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, stats_g)
+
+    # K4 of g_pre on the side stream, next to the next main-stream GEMM
+    fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
+        ev_g = torch.cuda.Event()
+        ev_g.record(side)
+    if grad_ready is None:
+        # dX || K4(g_pre), then both split weight gradients in one grouped
+        # launch: dW2 = split(act)^T g_c and dW1^T = split(g_pre)^T x_in share
+        # (rows, d, n), so the second fills the first one's partial last wave
+        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
+        main.wait_event(cache.side_ready)
+        main.wait_event(ev_g)
+        split_weight_grad_pair(fa, fg, plan, g_c, x_in, npad, d_w2, d_w1)
     else:
-        # dW2 = split(act)^T g_c  (act is already restricted to the mask)
-        if cache.act_fw is not None:
-            fused_weight_grad(cache.act_fw, cache.act_vals, cache.act_meta, h, plan, g_c, d_w2, transposed=False)
-            stats_a = cache.act_fw.stats(plan)
-        else:
-            fa = _act_split(cache, npad, h, plan)
-            split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
-            stats_a = fa.stats
-        census.append(GemmEvent("bwd.d_w2", True, macs_w))
+        # data parallel: dW2 first (its all-reduce then overlaps dX and dW1),
+        # K4(g_pre) next to it
+        main.wait_event(cache.side_ready)
+        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
         notify("d_w2", d_w2)
-        # dW1 = (split(g_pre)^T x_in)^T. The split path always sees the masked
-        # g_pre (ref splitgemm.py:72, even with mask_grad_with_fwd off);
-        # naive_sparse without the mask sparsifies the raw g_pre feature-wise.
-        if raw_naive:
-            from .sparse24 import sparsify_feature_wise
-
-            gpad = torch.zeros(npad, h, dtype=BF16, device=dev)
-            gpad[:n] = g_pre_dense
-            sg, _, stats_g = sparsify_feature_wise(gpad)
-            _lib.call("s24_spmm", ptr(sg.data), ptr(sg.meta_hw), ptr(cache.x_in), 1, d, h, d, npad, ptr(d_w1),
-                      _lib.F32, h, None, 1, -1, None, 0, s)
-        elif g_fw is not None:
-            fused_weight_grad(g_fw, g_vals, cache.act_meta, h, plan, cache.x_in, d_w1, transposed=True)
-            stats_g = g_fw.stats(plan)
-        else:
-            if fg is None:
-                fg = feature_split(g_vals, cache.act_meta, npad, h, plan, **_layout())
-            elif fg_ready is not None:
-                torch.cuda.current_stream().wait_event(fg_ready)
-            split_weight_grad(fg, plan, cache.x_in, npad, d_w1, transposed=True)
-            stats_g = fg.stats
-        census.append(GemmEvent("bwd.d_w1", True, macs_w))
+        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
+        main.wait_event(ev_g)
+        split_weight_grad(fg, plan, x_in, npad, d_w1, transposed=True)
         notify("d_w1", d_w1)
+    census.insert(1, GemmEvent("bwd.d_w2", True, macs_w))
+    census.insert(2, GemmEvent("bwd.d_w1", True, macs_w))
+    return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, fg.stats,
+                    Sparse24Matrix(n, h, TOKEN_WISE, g_vals, cache.act_meta), fg)
 
-    if ev_dx is not None:
-        census.append(ev_dx)
-    elif cfg.mask_grad_with_fwd:
+
+def _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census) -> None:
+    """bwd.d_x: the 2:4 GEMM on g_pre's forward keep pattern (exact, ref
+    ffn.py:440-445), or dense on the unmasked derivative (:446-447); the
+    inverse permutation is its epilogue row map."""
+    if cfg.mask_grad_with_fwd:
         _lib.call("s24_spmm", ptr(g_vals), ptr(cache.act_meta), ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
                   ptr(cache.inv_dev), 0, -1, None, 0, s)
         census.append(GemmEvent("bwd.d_x", True, sp_gemm_macs(n, h, d)))
@@ -1012,4 +741,3 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         _lib.call("s24_gemm", ptr(g_pre_dense), 0, h, ptr(p.w1), 0, h, n, d, h, ptr(d_x), _lib.BF16, d,
                   ptr(cache.inv_dev), 0, -1, None, s)
         census.append(GemmEvent("bwd.d_x", False, gemm_macs(n, h, d)))
-    return FfnGrads(d_w1, d_w2, d_x, None, census, stats_a, stats_g)

@@ -114,10 +114,10 @@ def _t_codes(R: int, C: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 class _Overlap:
-    """Side-stream work next to the main-stream GEMMs (the bf16 path's K4_MODE
-    "side" scheme): outputs are allocated on the main stream before the side
-    stream is forked, temporaries are kept alive in `keep` until the main
-    stream has joined the side stream's event."""
+    """Side-stream work next to the main-stream GEMMs (as in the bf16 path):
+    outputs are allocated on the main stream before the side stream is
+    forked, temporaries are kept alive in `keep` until the main stream has
+    joined the side stream's event."""
 
     def __init__(self, dev, enabled: bool):
         from .splitgemm import side_stream
@@ -285,7 +285,8 @@ def fp8_gemm_rowwise(a: Fp8Rowwise, b: Fp8Rowwise) -> torch.Tensor:
 # ---------------------------------------------------------------- FFN
 
 
-def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backward: bool, h_valid=None):
+def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backward: bool, h_valid=None,
+                   counts_hook=None):
     """ffn_forward under fp8_emulation (ref ffn.py:276-363 with fp8=True): the
     two forward GEMMs on e4m3 operands. Sparse forward: K1 on e4m3 codes
     selects on the fp32 scaled pre-activation (selection before quantization,
@@ -318,14 +319,12 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
         aq, sa = quant_rows(act)
         gemm_f8(aq, sa, w2q, s2, n, d, h, out, rows_valid=n)
         census.append(GemmEvent("fwd.out", False, gemm_macs(n, h, d)))
-        cache = FfnCache(x_in, n, None, None, act.to(BF16), pre, None, None, None, None, None, None, census, cfg,
-                         act_f32=act)
-        return out, cache
+        return out, FfnCache(n, cfg, census, _x_in=x_in, act_dense=act.to(BF16), pre_act=pre, act_f32=act)
 
-    from .ffn import K4_MODE, _all_sparse_plan
+    from .ffn import _all_sparse_plan
     from .splitgemm import alloc_feature_split, run_feature_split
 
-    ov = _Overlap(dev, K4_MODE == "side")
+    ov = _Overlap(dev, True)
     fp8b = cfg.fp8_backward and for_backward
     split_bwd = for_backward and cfg.backward_mode != "dense"
     # W2 codes for fwd.out -- and the backward's weight codes -- on the side
@@ -357,12 +356,14 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
         aq[n:].zero_()
         act_meta[(n // 128) * (h // 128) * 2048:].fill_(0x44)
     counts = torch.zeros(h, dtype=torch.int32, device=dev)
-    stats_dev = torch.zeros(2, dtype=torch.int64, device=dev)
+    stats_dev = torch.zeros(3, dtype=torch.int64, device=dev)
     need_pre = keep_pre_act or not cfg.mask_grad_with_fwd
     pre = torch.empty(n, h, dtype=F32, device=dev) if need_pre else None
     _lib.call("s24_fwd_gemm1_f8", ptr(xq), xq.stride(0), ptr(w1q), w1q.stride(0), n, h, d, ptr(sx),
               ptr(s1), ptr(vals32), ptr(amax), ptr(act_meta), ptr(counts), ptr(stats_dev), ptr(pre), stream())
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
+    if counts_hook is not None:
+        counts_hook(counts)
     _, sa = quant_rows(vals32, rows=n, amax=amax, codes=aq, deq=act_vals, raw=act_raw)
     meta8 = meta_to_f8(act_meta, n, h)
     if plan is not None and plan.hidden_dim != (h_valid or h):
@@ -382,7 +383,7 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     bplan = naive_plan if naive_plan is not None else plan_out
     fa = f8 = None
     if split_bwd:
-        fa = alloc_feature_split(act_vals, act_meta, npad, h, bplan, paired=True)
+        fa = alloc_feature_split(act_vals, act_meta, npad, h, bplan)
     if split_bwd and fp8b:
         xt = torch.empty(d, npad, dtype=U8, device=dev)  # npad % 128 == 0: no padding columns
         f8 = dict(wb, vq_a=torch.empty(fa.vs.shape, dtype=U8, device=dev),
@@ -411,9 +412,10 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
         ev_side = None
     elif ev_side is None:
         ev_side = ev_w
-    cache = FfnCache(x_in if for_backward else None, n, act_vals, act_meta, None, pre, perm_dev, perm_dev, inv_dev,
-                     plan_out, SparsifyStats(n * h, stats_dev), counts, census, cfg, act_split=fa,
-                     act_split_ready=ev_side, act_raw=act_raw, act_meta8=meta8, f8=f8,
+    cache = FfnCache(n, cfg, census, _x_in=x_in if for_backward else None, act_vals=act_vals, act_meta=act_meta,
+                     pre_act=pre, perm_dev=perm_dev, inv_dev=inv_dev, _plan=plan_out,
+                     stats=SparsifyStats(n * h, stats_dev[:2]), counts=counts, stats_dev=stats_dev, act_split=fa,
+                     side_ready=ev_side, act_raw=act_raw, act_meta8=meta8, f8=f8,
                      plan_valid=plan_api if h_valid is not None else None)
     if ov.side is not None and not for_backward:
         ov.join(ev_side)
@@ -423,7 +425,7 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
 def _split_grad_f8(fs, plan, b: torch.Tensor, npad: int, out: torch.Tensor, transposed: bool) -> None:
     """split / naive weight gradient on e4m3 operands: the feature-wise split
     (paired layout) quantized per feature, b per column (ref ffn.py:258-270)."""
-    rows, rmap, valid = fs.gemm_rows(plan)
+    rows, rmap, valid = fs.rows(plan), plan.paired_row_map, None
     if not rows:
         return
     vq = torch.zeros(fs.vs.shape[0], fs.vs.shape[1], dtype=U8, device=b.device)
@@ -443,7 +445,8 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
     from .splitgemm import feature_split, split_gemm_macs
 
     n = cache.n
-    d = cache.x_in.shape[1]
+    x_in = cache._x_in
+    d = x_in.shape[1]
     h = p.hidden_dim
     dev = g_out.device
     npad = pad128(n)
@@ -461,7 +464,7 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
         mm_at_f8(cache.act_f32, g_c[:n], d_w2)
         census.append(GemmEvent("bwd.d_w2", False, gemm_macs(h, n, d)))
         notify("d_w2", d_w2)
-        mm_at_f8(cache.x_in[:n], g_pre, d_w1)
+        mm_at_f8(x_in[:n], g_pre, d_w1)
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
         mm_f8(g_pre, p.w1, d_x)
@@ -469,11 +472,10 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
         return FfnGrads(d_w1, d_w2, d_x, None, census)
 
     # ---------------------------------------------------------- sparse forward
-    from .ffn import K4_MODE
     from .splitgemm import alloc_feature_split, run_feature_split
 
     f8 = cache.f8 or {}
-    ov = _Overlap(dev, K4_MODE == "side")
+    ov = _Overlap(dev, True)
     mode = cfg.backward_mode
     raw_naive = mode == "naive_sparse" and not cfg.mask_grad_with_fwd
     split = mode != "dense" and not raw_naive and cache.act_split is not None
@@ -508,8 +510,8 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
     # K4 of g_pre and its codes on the side stream, next to the dX GEMM
     ev_g = None
     if split:
-        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache.plan
-        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan, paired=True)
+        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache._plan
+        fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan)
         rows_g = fg.rows(plan)
         vq_g = torch.empty(fg.vs.shape, dtype=U8, device=dev)
         sv_g = torch.empty(fg.vs.shape[0], dtype=F32, device=dev)
@@ -548,23 +550,24 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
             _lib.call("s24_decompress_token", ptr(g_vals), None, ptr(cache.act_meta), n, h, ptr(gp), _lib.BF16, h, s)
         else:
             gp = g_pre_dense
-        mm_at_f8(cache.x_in[:n], gp, d_w1)
+        ov.join(cache.side_ready)
+        mm_at_f8(x_in[:n], gp, d_w1)
         census.append(GemmEvent("bwd.d_w1", False, gemm_macs(d, n, h)))
         notify("d_w1", d_w1)
     else:
-        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache.plan
+        plan = _all_sparse_plan(h, dev) if mode == "naive_sparse" else cache._plan
         macs_w = sp_gemm_macs(n, h, d) if mode == "naive_sparse" else split_gemm_macs(n, d, plan)
         # the forward's side work (act split, its codes, x_in^T codes) and ours
-        if cache.act_split_ready is not None:
-            torch.cuda.current_stream().wait_event(cache.act_split_ready)
+        if cache.side_ready is not None:
+            torch.cuda.current_stream().wait_event(cache.side_ready)
         ov.join(ev_g)
         fa = cache.act_split
         if fa is None:
-            fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan, nonneg=True, paired=True)
+            fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)
         if "vq_a" in f8 and ev_g is not None and grad_ready is None and gt is not None and "xt" in f8:
             # both split weight gradients in one grouped e4m3 launch (no
             # per-gradient hook to serve): dW2 = split(act)^T g_c, dW1^T = split(g_pre)^T x_in
-            rows_a, rmap, valid = fa.gemm_rows(plan)
+            rows_a, rmap, valid = fa.rows(plan), plan.paired_row_map, None
             _lib.call("s24_spmm_pair_f8", rows_a, d, npad, _lib.F32,
                       ptr(f8["vq_a"]), ptr(f8["e8_a"]), ptr(gt), gt.stride(0), ptr(f8["sv_a"]), ptr(sgt), ptr(d_w2),
                       d_w2.stride(0), ptr(rmap), 0, ptr(valid),
@@ -577,7 +580,7 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
         if "vq_a" in f8:
             if gt is None:
                 gt, sgt = quant_cols_t(g_c)
-            rows_a, rmap, valid = fa.gemm_rows(plan)
+            rows_a, rmap, valid = fa.rows(plan), plan.paired_row_map, None
             spmm_f8(f8["vq_a"], f8["e8_a"], f8["sv_a"], gt, sgt, rows_a, d, npad, d_w2, row_map=rmap,
                     rows_valid=rows_a, row_valid=valid, pair_rows=max(fa.pair_rows, 0))
         else:
@@ -591,17 +594,17 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
             sgw, _, stats_g = sparsify_feature_wise(gpad)
             vq = torch.zeros(sgw.data.shape, dtype=U8, device=dev)
             _, sv = quant_rows(sgw.data, rows=h, codes=vq)
-            bq, sb = quant_cols_t(cache.x_in)
+            bq, sb = quant_cols_t(x_in)
             spmm_f8(vq, meta_to_f8(sgw.meta_hw, h, npad), sv, bq, sb, h, d, npad, d_w1, transposed=True, rows_valid=h)
         elif ev_g is not None:
-            _, rmap, valid = fg.gemm_rows(plan)
-            xt, sxt = (f8["xt"], f8["sxt"]) if "xt" in f8 else quant_cols_t(cache.x_in)
+            rmap, valid = plan.paired_row_map, None
+            xt, sxt = (f8["xt"], f8["sxt"]) if "xt" in f8 else quant_cols_t(x_in)
             spmm_f8(vq_g, e8_g, sv_g, xt, sxt, rows_g, d, npad, d_w1, row_map=rmap, transposed=True,
                     rows_valid=rows_g, row_valid=valid, pair_rows=max(fg.pair_rows, 0))
             stats_g = fg.stats
         else:
-            fg = feature_split(g_vals, cache.act_meta, npad, h, plan, paired=True)
-            _split_grad_f8(fg, plan, cache.x_in, npad, d_w1, transposed=True)
+            fg = feature_split(g_vals, cache.act_meta, npad, h, plan)
+            _split_grad_f8(fg, plan, x_in, npad, d_w1, transposed=True)
             stats_g = fg.stats
         census.append(GemmEvent("bwd.d_w1", True, macs_w))
         notify("d_w1", d_w1)

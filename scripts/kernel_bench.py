@@ -55,7 +55,7 @@ def main():
     act_vals = torch.zeros(n, h // 2, device="cuda", dtype=bf)
     meta = torch.zeros(_lib.meta_hw_bytes(n, h), device="cuda", dtype=torch.uint8)
     counts = torch.zeros(h, device="cuda", dtype=torch.int32)
-    stats = torch.zeros(2, device="cuda", dtype=torch.int64)
+    stats = torch.zeros(3, device="cuda", dtype=torch.int64)
     out = torch.empty(n, d, device="cuda", dtype=bf)
     act = torch.empty(n, h, device="cuda", dtype=bf)
     gv = torch.zeros_like(act_vals)
@@ -77,7 +77,7 @@ def main():
     f = 2.0 * n * d * h
     cb1 = timeit(lambda: torch.matmul(x, w1), args.iters, flush)
     rec("K1 fwd gemm1 fused", timeit(lambda: _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(act_vals),
-                                                          P(meta), P(counts), P(stats), None, None, None, None, 0, None, S()), args.iters, flush),
+                                                          P(meta), P(counts), P(stats), None, S()), args.iters, flush),
         f, cb1)
     rec("dense relu2 (twin of K1)", timeit(lambda: _lib.call("s24_gemm_relu2", P(x), d, P(w1), h, n, h, d, P(act), h,
                                                                 S()), args.iters, flush), f, cb1)
@@ -91,7 +91,7 @@ def main():
                                                           None, 0, -1, None, S()), args.iters, flush), f, cb2)
     cb3 = timeit(lambda: torch.matmul(g, w2.t()), args.iters, flush)
     rec("K3 bwd dact fused", timeit(lambda: _lib.call("s24_bwd_dact_fused", P(g), d, P(w2), d, n, h, d, P(act_vals),
-                                                         P(meta), P(gv), None, None, None, 0, None, S()), args.iters, flush), f, cb3)
+                                                         P(meta), P(gv), S()), args.iters, flush), f, cb3)
     rec("dense dact (twin of K3)", timeit(lambda: _lib.call("s24_gemm_dact", P(g), d, P(w2), d, n, h, d, P(act), h,
                                                                P(act), h, S()), args.iters, flush), f, cb3)
     cb4 = timeit(lambda: torch.matmul(act, w1.t()), args.iters, flush)
@@ -127,16 +127,9 @@ def main():
     esx = torch.empty(_lib.meta_hw_bytes((2 * nd + kcount + 127) // 128 * 128 + 128, n), device="cuda",
                       dtype=torch.uint8)
     k4x_bytes = n * h * 1.125 + (2 * nd + kcount) * n * 0.5625
-    rec("K4x paired (hot path)", timeit(lambda: _lib.call("s24_feature_split_x", P(act_vals), None, P(meta), n, h,
-                                                             P(pos), kcount, nd, P(vsx), P(esx), None, None, 1, None, S()),
+    rec("K4x paired (hot path)", timeit(lambda: _lib.call("s24_feature_split_x", P(act_vals), P(meta), n, h,
+                                                             P(pos), kcount, nd, P(vsx), P(esx), 1, None, S()),
                                          args.iters, flush), 1e-9, bytes_=k4x_bytes)
-    pad = (2 * nd + 127) // 128 * 128
-    vsi = torch.empty(pad + h, n // 2, device="cuda", dtype=bf)
-    esi = torch.empty(_lib.meta_hw_bytes(pad + h, n), device="cuda", dtype=torch.uint8)
-    k4i_bytes = n * h * 1.125 + (pad + h) * n * 0.5625 + 0.0
-    rec("K4 identity layout", timeit(lambda: _lib.call("s24_feature_split_id", P(act_vals), P(meta), n, h, P(pos), nd,
-                                                          P(vsi), P(esi), None, 1, S()), args.iters, flush),
-        1e-9, bytes_=k4i_bytes)
     src = torch.randperm(n, device="cuda").int()
     rec("K6 gather rows", timeit(lambda: _lib.call("s24_gather_rows", P(x), n, 2 * d, 2 * d, P(src), P(out), 2 * d,
                                                       S()), args.iters, flush), 1e-9, bytes_=2 * n * d * 2)

@@ -77,6 +77,12 @@ def test_recipe_selection_exact_and_outputs_within_tolerance(n, d, h):
     assert grads.stats_act.total_entries == fst["total_entries"]
     assert grads.stats_act.nonzeros_before == fst["nonzeros_before"]
     assert grads.stats_act.dropped == fst["dropped"]
+    # ... and of g_pre (the split of dW1), on the device's own stored g_pre
+    g_kept = s24.decompress(grads.g_pre_sparse).cpu().numpy()
+    _, _, _, gst = O.sparsify_feature(np.ascontiguousarray(g_kept[:, osp]))
+    assert grads.stats_grad.total_entries == gst["total_entries"]
+    assert grads.stats_grad.nonzeros_before == gst["nonzeros_before"]
+    assert grads.stats_grad.dropped == gst["dropped"]
 
     # end-to-end vs the oracle run independently on the same (bf16-rounded) inputs
     o_out, o_cache = O.ffn_forward(x, w1, w2, cfg_dict(cfg), ordered=False)
@@ -259,50 +265,45 @@ def test_nn_module_autograd_matches_api():
     assert m.w1.grad.dtype == torch.float32
 
 
-def test_wgrad_overlap_order_is_bitwise_identical(monkeypatch):
-    """S24_WGRAD_OVERLAP (dW2 || K4(g), then dW1 || dX on three streams) gives
-    the same bits as the default order (dX || K4(g), grouped dW launch)."""
-    from paper_2503_16672_b200 import ffn as F
-
+def test_grad_ready_order_is_bitwise_identical():
+    """With a grad_ready hook (data parallel) the backward runs dW2 right
+    after K3 and dW1 after dX, in two launches; without one, both weight
+    gradients run in one grouped launch after dX. Same bits, same census, and
+    the hook sees d_w2 then d_w1 with their final values."""
     n, d, h = 1024, 256, 1024
     x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=77)
     p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
     tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
-    runs = []
-    for flag in (False, True):
-        monkeypatch.setattr(F, "WGRAD_OVERLAP", flag)
-        out, cache = s24.ffn_forward(tx, p, s24.RECIPE)
-        g = s24.ffn_backward(tg, cache, p, s24.RECIPE)
-        torch.cuda.synchronize()
-        runs.append((out, g))
-    (o0, g0), (o1, g1) = runs
-    assert torch.equal(o0, o1)
+    out, cache = s24.ffn_forward(tx, p, s24.RECIPE)
+    g0 = s24.ffn_backward(tg, cache, p, s24.RECIPE)
+    seen = []
+    out1, cache = s24.ffn_forward(tx, p, s24.RECIPE)
+    g1 = s24.ffn_backward(tg, cache, p, s24.RECIPE, grad_ready=lambda name, t: seen.append((name, t.clone())))
+    torch.cuda.synchronize()
+    assert torch.equal(out, out1)
     for t in ("d_w1", "d_w2", "d_x"):
         assert torch.equal(getattr(g0, t), getattr(g1, t)), t
     assert [e.name for e in g0.census] == [e.name for e in g1.census]
+    assert [nm for nm, _ in seen] == ["d_w2", "d_w1"]
+    assert torch.equal(seen[0][1], g0.d_w2) and torch.equal(seen[1][1], g0.d_w1)
 
 
-@pytest.mark.parametrize("n,d,h", [(1024, 256, 1024), (640, 512, 512)])
-def test_k4_in_gemm_is_bitwise_identical(monkeypatch, n, d, h):
-    """S24_K4_MODE=gemm (the act / g_pre feature splits computed by extra
-    warps of fwd.out / dX from their own A stages, s24_spmm_fs) gives the same
-    bits as the side-stream K4 kernels."""
-    from paper_2503_16672_b200 import ffn as F
-
-    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=78)
+def test_public_side_stream_outputs_are_safe_to_read():
+    """The plan and x_in are produced on the side stream; reading them from
+    the cache right after ffn_forward (no synchronize, no backward) must see
+    the finished values (the properties make the caller's stream wait)."""
+    n, d, h = 4096, 512, 2048
+    x, w1, w2, _ = O.synthetic_ffn_inputs(n, d, h, sparsity=0.9, seed=5)
     p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
-    tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
-    runs = []
-    for mode in ("side", "gemm"):
-        monkeypatch.setattr(F, "K4_MODE", mode)
+    tx = torch.from_numpy(x).cuda()
+    ref_out, ref_cache = s24.ffn_forward(tx, p, s24.RECIPE)
+    torch.cuda.synchronize()
+    want_sp = ref_cache.plan.sparse_features.cpu()
+    want_x = ref_cache.x_in.cpu()
+    for _ in range(3):
         out, cache = s24.ffn_forward(tx, p, s24.RECIPE)
-        g = s24.ffn_backward(tg, cache, p, s24.RECIPE)
-        torch.cuda.synchronize()
-        runs.append((out, g))
-    (o0, g0), (o1, g1) = runs
-    assert torch.equal(o0, o1)
-    for t in ("d_w1", "d_w2", "d_x"):
-        assert torch.equal(getattr(g0, t), getattr(g1, t)), t
+        assert torch.equal(cache.plan.sparse_features.cpu(), want_sp)
+        assert torch.equal(cache.x_in.cpu(), want_x)
 
 
 @pytest.mark.parametrize("fp8", [False, True])
@@ -356,39 +357,6 @@ def test_inference_forward_skips_permutation_same_bits(fp8):
     assert c_train.stats.dropped == c_inf.stats.dropped
     assert torch.equal(c_train.plan.sparse_features, c_inf.plan.sparse_features)
     assert c_inf.perm is None and c_train.perm is not None
-
-
-@pytest.mark.parametrize("n,d,h,mode", [(1024, 256, 1024, "split_masked"), (600, 512, 512, "split_masked"),
-                                         (512, 256, 512, "naive_sparse")])
-def test_token_order_storage_is_bitwise_identical(monkeypatch, n, d, h, mode):
-    """TOKEN_ORDER_STORAGE (activations kept in the caller's token order, the
-    permutation applied inside K4 and by the side-stream gathers) gives the
-    same bits as gathering into the permuted frame first, and the cache's
-    compute-frame views (act_sparse, fwd_mask, pre_act) are unchanged."""
-    from dataclasses import replace
-
-    from paper_2503_16672_b200 import ffn as F
-
-    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=0.85, seed=81)
-    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
-    cfg = replace(s24.RECIPE, backward_mode=mode)
-    tx, tg = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
-    runs = []
-    for flag in (False, True):
-        monkeypatch.setattr(F, "TOKEN_ORDER_STORAGE", flag)
-        out, cache = s24.ffn_forward(tx, p, cfg, keep_pre_act=True)
-        views = (cache.act_sparse.values.clone(), cache.act_sparse.meta.clone(), cache.fwd_mask.clone(),
-                 cache.pre_act.clone())
-        g = s24.ffn_backward(tg, cache, p, cfg)
-        torch.cuda.synchronize()
-        assert (cache.row_frame is not None) == flag
-        runs.append((out, g, views))
-    (o0, g0, v0), (o1, g1, v1) = runs
-    assert torch.equal(o0, o1)
-    for t in ("d_w1", "d_w2", "d_x"):
-        assert torch.equal(getattr(g0, t), getattr(g1, t)), t
-    for a, b in zip(v0, v1):
-        assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("fp8", [False, True])

@@ -39,8 +39,8 @@ def test_feature_split_x_stays_in_bounds():
     rp = (rows + 127) // 128 * 128
     vb, vs = guarded(rp * (n // 2) * 2)
     eb, es = guarded(_lib.meta_hw_bytes(rp, n))
-    _lib.call("s24_feature_split_x", P(vals), None, P(meta_hw), n, h, P(torch.from_numpy(pos).cuda()), len(sp),
-              len(de), P(vs), P(es), None, None, 1, None, S())
+    _lib.call("s24_feature_split_x", P(vals), P(meta_hw), n, h, P(torch.from_numpy(pos).cuda()), len(sp),
+              len(de), P(vs), P(es), 1, None, S())
     torch.cuda.synchronize()
     assert intact(vb) and intact(eb)
 
@@ -73,9 +73,8 @@ def test_fwd_gemm1_and_spmm_stay_in_bounds(M):
     vb, vals = guarded(mp * (N // 2) * 2, 0)
     eb, meta = guarded(_lib.meta_hw_bytes(M, N), 0x44)
     cnt_b, counts = guarded(N * 4, 0)
-    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
-    _lib.call("s24_fwd_gemm1_fused", P(x), K, P(w1), N, M, N, K, P(vals), P(meta), P(counts), P(stats), None, None,
-              None, None, 0, None, S())
+    stats = torch.zeros(3, dtype=torch.int64, device="cuda")
+    _lib.call("s24_fwd_gemm1_fused", P(x), K, P(w1), N, M, N, K, P(vals), P(meta), P(counts), P(stats), None, S())
     torch.cuda.synchronize()
     assert intact(vb, 0) and intact(eb, 0x44) and intact(cnt_b, 0)
     # fwd.out over the same activation, output rows through a row map, bf16
