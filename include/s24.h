@@ -83,6 +83,14 @@ int s24_sparsify_feature(const void* a, int dtype, int64_t rows, int64_t cols, i
                          uint8_t* meta_ref, uint8_t* meta_hw, uint8_t* mask, unsigned long long* stats,
                          void* stream);
 
+/* Replaces sparsify_feature_wise_masked (sparse24.py:118-129): as
+ * s24_sparsify_feature, with every entry where fwd_mask (uint8 [rows, cols],
+ * 0/1, row-major) is 0 read as zero before the selection and before the
+ * counts, so masked-out values never count as dropped. */
+int s24_sparsify_feature_masked(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda,
+                                const uint8_t* fwd_mask, void* vals_t, uint8_t* meta_ref, uint8_t* meta_hw,
+                                uint8_t* mask, unsigned long long* stats, void* stream);
+
 /* Replaces compress_token_wise_with_mask (sparse24.py:138-154). bad_groups
  * (device int, caller-zeroed) counts groups whose mask does not have exactly 2
  * bits; the binding raises MaskError when it is non-zero. */

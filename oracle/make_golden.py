@@ -29,6 +29,13 @@ def bern(r, rows, cols, p):
     return ((r.random((rows, cols)) < p) * r.standard_normal((rows, cols))).astype(np.float32)
 
 
+def bf16(a):
+    """round to the nearest bfloat16 (ties to even), kept as float32"""
+    u = np.asarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32)
+
+
 def stats_arr(st):
     return np.array([st.total_entries, st.nonzeros_before, st.nonzeros_after, st.dropped], dtype=np.int64)
 
@@ -44,6 +51,9 @@ def main():
     OUT.mkdir(parents=True, exist_ok=True)
     if args.only == "fp8":
         make_fp8(R)
+        return
+    if args.only == "nonfinite":
+        make_nonfinite(R)
         return
 
     # ---------------------------------------------------------------- sparsifiers
@@ -193,8 +203,79 @@ def main():
             cases[f"bad_{k}_bytes"] = np.frombuffer(blob, dtype=np.uint8)
             cases[f"bad_{k}_error"] = np.array(err)
     np.savez_compressed(OUT / "formats.npz", **cases)
+    make_nonfinite(R)
     for f in sorted(OUT.glob("*.npz")):
         print(f, f.stat().st_size)
+
+
+def make_nonfinite(R):
+    """NaN / Inf through the reference (it accepts them: ffn_forward and the
+    sparsifiers check shape and dtype, not finiteness): numpy's maximum keeps
+    NaN, count_nonzero counts it, the stable argsort ranks it below zero.
+    Also the masked feature-wise sparsifier (sparse24.py:118-129) on random
+    masks, including the reference's all-ones / all-zeros KATs
+    (tests/test_sparse24.py:119-140)."""
+    cases = {}
+    r = rng(300)
+    for i, (rows, cols) in enumerate([(16, 32), (64, 64)]):
+        a = bern(r, rows, cols, 0.5)
+        a[r.random((rows, cols)) < 0.08] = np.nan
+        a[r.random((rows, cols)) < 0.03] = np.inf
+        a[r.random((rows, cols)) < 0.03] = -np.inf
+        a[0, :4] = [np.nan, 0.0, 0.0, 0.0]      # NaN ranks below zeros
+        a[0, 4:8] = [np.nan, np.nan, 1.0, np.nan]  # NaN kept only with < 2 others above it
+        a[1, :4] = [np.nan, np.nan, np.nan, np.nan]
+        s, m, st = R.sparsify_token_wise(a)
+        cases[f"tok{i}_a"] = a
+        cases[f"tok{i}_values"] = s.values
+        cases[f"tok{i}_meta"] = s.meta
+        cases[f"tok{i}_mask"] = m
+        cases[f"tok{i}_stats"] = stats_arr(st)
+        f, fm, fst = R.sparsify_feature_wise(a)
+        cases[f"feat{i}_values"] = f.values
+        cases[f"feat{i}_meta"] = f.meta
+        cases[f"feat{i}_stats"] = stats_arr(fst)
+        cases[f"counts{i}"] = R.column_nonzero_counts(a)
+        cases[f"plan{i}_sparse"] = R.partition_features(R.column_nonzero_counts(a), 0.75).sparse_features
+    # full FFN, recipe, with NaN / Inf in a few W1 columns (mixed groups) and
+    # one NaN input row
+    # (bf16-representable inputs: the device path computes on bf16 operands)
+    n, d, h = 32, 8, 16
+    rr = rng(301)
+    x = bf16(rr.standard_normal((n, d)))
+    w1 = bf16(rr.standard_normal((d, h)) / np.sqrt(d))
+    w2 = bf16(rr.standard_normal((h, d)) / np.sqrt(h))
+    g = bf16(rr.standard_normal((n, d)))
+    w1[:, 2] = np.nan
+    w1[0, 5] = np.inf
+    w1[3, 9] = np.nan
+    x[7, 3] = np.nan
+    cfg = R.FfnConfig(forward_mode="sparse24", backward_mode="split_masked", mask_grad_with_fwd=True,
+                      permute_tokens=True)
+    out, cache = R.ffn_forward(x, R.FfnParams(w1=w1, w2=w2), cfg)
+    grads = R.ffn_backward(g, cache, R.FfnParams(w1=w1, w2=w2), cfg)
+    cases.update(ffn_x=x, ffn_w1=w1, ffn_w2=w2, ffn_g=g, ffn_out=out, ffn_pre=cache.pre_act,
+                 ffn_mask=cache.fwd_mask, ffn_stats=stats_arr(cache.stats),
+                 ffn_plan_sparse=cache.plan.sparse_features, ffn_d_x=grads.d_x, ffn_d_w1=grads.d_w1,
+                 ffn_d_w2=grads.d_w2)
+    # masked feature-wise
+    a = rng(4).standard_normal((8, 8)).astype(np.float32)
+    for tag, mask in (("ones", np.ones((8, 8), bool)), ("zeros", np.zeros((8, 8), bool))):
+        sm, mm, st = R.sparsify_feature_wise_masked(a, mask)
+        cases[f"masked_{tag}_a"], cases[f"masked_{tag}_mask"] = a, mask
+        cases[f"masked_{tag}_values"], cases[f"masked_{tag}_meta"] = sm.values, sm.meta
+        cases[f"masked_{tag}_stats"] = stats_arr(st)
+    rm = rng(6)
+    for i in range(4):
+        a = rm.standard_normal((8 * (i + 1), 12)).astype(np.float32)
+        mask = rm.random(a.shape) < 0.5
+        sm, mm, st = R.sparsify_feature_wise_masked(a, mask)
+        cases[f"masked_r{i}_a"], cases[f"masked_r{i}_mask"] = a, mask
+        cases[f"masked_r{i}_values"], cases[f"masked_r{i}_meta"] = sm.values, sm.meta
+        cases[f"masked_r{i}_keep"] = mm
+        cases[f"masked_r{i}_stats"] = stats_arr(st)
+    with np.errstate(all="ignore"):
+        np.savez_compressed(OUT / "nonfinite.npz", **cases)
 
 
 def make_fp8(R):

@@ -45,6 +45,27 @@ def gemm_at(a: np.ndarray, b: np.ndarray, ordered: bool = True) -> np.ndarray:
     return acc
 
 
+def gemm_kept(a: np.ndarray, keep: np.ndarray, b: np.ndarray, ordered: bool = True) -> np.ndarray:
+    """sum over kept k of a[:, k] b[k] -- the reference's exact-skip sparse
+    product (sp_gemm, ref sparse24.py:170-192: entries outside the keep
+    pattern are never multiplied, so a non-finite b row meets only the kept
+    entries; kept zeros do multiply). Ascending k when ordered."""
+    if not ordered and np.all(np.isfinite(b)):
+        return np.matmul(np.where(keep, a, a.dtype.type(0)), b)
+    acc = np.zeros((a.shape[0], b.shape[1]), dtype=a.dtype)
+    with np.errstate(invalid="ignore", over="ignore"):
+        for k in range(a.shape[1]):
+            rows = keep[:, k]
+            if rows.any():
+                acc[rows] += np.multiply.outer(a[rows, k], b[k])
+    return acc
+
+
+def gemm_at_kept(a: np.ndarray, keep: np.ndarray, b: np.ndarray, ordered: bool = True) -> np.ndarray:
+    """a^T b over kept entries only (sp_gemm_t, ref sparse24.py:195-216)."""
+    return gemm_kept(np.ascontiguousarray(a.T), np.ascontiguousarray(keep.T), b, ordered)
+
+
 # ---------------------------------------------------------------- 2:4 selection
 
 _LOWER = np.arange(4)[:, None] < np.arange(4)[None, :]
@@ -109,6 +130,14 @@ def sparsify_feature(a: np.ndarray):
     vals = np.take_along_axis(g, meta.astype(np.int64), axis=2)
     mask = keep.transpose(0, 2, 1).reshape(r, c)
     return vals, meta, mask, _stats(a.size, int(np.count_nonzero(a)), int(np.count_nonzero(vals)))
+
+
+def sparsify_feature_masked(a: np.ndarray, fwd_mask: np.ndarray):
+    """Zero entries outside fwd_mask, then sparsify_feature (ref
+    sparse24.py:118-129): masked-out values are not counted as dropped."""
+    if fwd_mask.shape != a.shape:
+        raise ValueError("mask shape does not match matrix")
+    return sparsify_feature(np.where(fwd_mask, a, a.dtype.type(0)))
 
 
 def compress_with_mask(a: np.ndarray, mask: np.ndarray):
@@ -283,12 +312,17 @@ def split_gemm_t(a, mask, b, sparse, dense, ordered=True):
     the feature-wise sparsification)."""
     am = np.where(mask, a, a.dtype.type(0))
     comp = am.copy()
+    # dense features: every token multiplies (gemm_at over the masked column,
+    # ref splitgemm.py:78-80); sparse features: the feature-wise kept entries
+    # only (sp_gemm_t)
+    keep = np.ones(am.shape, dtype=bool)
     st = _stats(0, 0, 0)
     if len(sparse):
         sub = np.ascontiguousarray(am[:, sparse])
-        v, m, _, st = sparsify_feature(sub)
+        v, m, fmask, st = sparsify_feature(sub)
         comp[:, sparse] = decompress_feature(v, m, *sub.shape)
-    return gemm_at(comp, b, ordered), st
+        keep[:, sparse] = fmask
+    return gemm_at_kept(comp, keep, b, ordered), st
 
 
 # ---------------------------------------------------------------- permutation
@@ -358,7 +392,7 @@ def ffn_forward(x, w1, w2, cfg, plan=None, ordered=True):
             kept = decompress_token(vals, meta, *act.shape)
         else:
             kept = decompress_token(vals, meta, *act.shape)
-            out_c = gemm(kept, w2, ordered)
+            out_c = gemm_kept(kept, mask, w2, ordered)
         cache.update(mask=mask, vals=vals, meta=meta, act=kept, stats=st)
     else:
         out_c = mm_f8(act, w2, ordered) if fp8 else gemm(act, w2, ordered)
@@ -385,16 +419,20 @@ def ffn_backward(g_out, cache, w1, w2, cfg, ordered=True):
         d_w2 = gemm_at(act, g_c, ordered)
         d_w1 = gemm_at(cache["x_in"], g_pre, ordered)
     elif mode == "naive_sparse":
-        v, m, _, fst_a = sparsify_feature(act)
-        d_w2 = gemm_at(decompress_feature(v, m, *act.shape), g_c, ordered)
-        v, m, _, fst_g = sparsify_feature(g_pre)
-        d_w1 = gemm_at(decompress_feature(v, m, *g_pre.shape), cache["x_in"], ordered).T
+        v, m, km, fst_a = sparsify_feature(act)
+        d_w2 = gemm_at_kept(decompress_feature(v, m, *act.shape), km, g_c, ordered)
+        v, m, km, fst_g = sparsify_feature(g_pre)
+        d_w1 = gemm_at_kept(decompress_feature(v, m, *g_pre.shape), km, cache["x_in"], ordered).T
     else:
         sp, de = cache["plan"]
         d_w2, fst_a = split_gemm_t(act, cache["mask"], g_c, sp, de, ordered)
         d_w1t, fst_g = split_gemm_t(g_pre, cache["mask"], cache["x_in"], sp, de, ordered)
         d_w1 = d_w1t.T
-    d_x_c = gemm(g_pre, np.ascontiguousarray(w1.T), ordered)
+    if cfg["mask_grad_with_fwd"]:
+        # compress_token_wise_with_mask + sp_gemm: the mask's entries only (ref ffn.py:440-445)
+        d_x_c = gemm_kept(g_pre, cache["mask"], np.ascontiguousarray(w1.T), ordered)
+    else:
+        d_x_c = gemm(g_pre, np.ascontiguousarray(w1.T), ordered)
     d_x = inverse_permute_rows(d_x_c, perm) if perm is not None else d_x_c
     return dict(d_w1=np.ascontiguousarray(d_w1), d_w2=d_w2, d_x=d_x, g_pre=g_pre, fstats_act=fst_a,
                 fstats_g=fst_g)

@@ -29,6 +29,7 @@ INT = ctypes.c_int
 SIGNATURES: dict[str, list] = {
     "s24_sparsify_token": [P, INT, I64, I64, I64, P, P, P, P, P, P],
     "s24_sparsify_feature": [P, INT, I64, I64, I64, P, P, P, P, P, P],
+    "s24_sparsify_feature_masked": [P, INT, I64, I64, I64, P, P, P, P, P, P, P],
     "s24_compress_token_with_mask": [P, INT, I64, I64, I64, P, P, P, P, P, P],
     "s24_decompress_token": [P, P, P, I64, I64, P, INT, I64, P],
     "s24_decompress_feature": [P, P, P, I64, I64, P, INT, I64, P],

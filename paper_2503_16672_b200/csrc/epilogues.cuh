@@ -254,14 +254,15 @@ struct EpiFwd1T {
     float a[32], k[32];
     uint32_t nz = 0;
 #pragma unroll
-    // (rows >= M: TMA zero-fills the A rows, so acc = 0 and a = 0 there; the
-    // F8 row scale is 0 for them as well)
     for (int i = 0; i < 32; ++i) {
       const float r = relu_nan(v[i]);
       a[i] = __fmul_rn(r, r);
       k[i] = fmaxf(a[i], -1.f);
       nz |= (a[i] != 0.f ? 1u : 0u) << i;
     }
+    // rows >= M read TMA zero fill, so y = 0 there -- unless B holds NaN / Inf
+    // (0 * Inf = NaN): they never count
+    if (!row_ok) nz = 0u;
     // per-feature counts over the warp's 32 rows: transpose the nonzero bit
     // matrix so lane i holds column i, then popcount
     if (p.counts) {

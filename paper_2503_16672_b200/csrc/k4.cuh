@@ -67,7 +67,7 @@ __device__ __forceinline__ const uint2* k4_lut_init() {
 __device__ __forceinline__ uint32_t k4_key2(uint32_t x) {
   const uint32_t mag = x & 0x7FFF7FFFu;
   const __nv_bfloat162 m = *reinterpret_cast<const __nv_bfloat162*>(&mag);
-  const uint32_t nan = __hne2_mask(m, m);
+  const uint32_t nan = __hneu2_mask(m, m);  // (unordered: true exactly for NaN)
   return (mag & ~nan) | (0xBF80BF80u & nan);
 }
 
@@ -78,7 +78,8 @@ __device__ __forceinline__ uint32_t k4_ge(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t k4_nz(uint32_t x) {  // 1 per nonzero half, packed
   const uint32_t mag = x & 0x7FFF7FFFu;
   const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
-  return __hne2_mask(*reinterpret_cast<const __nv_bfloat162*>(&mag), z) & 0x00010001u;
+  // (unordered: NaN counts as a nonzero, numpy's count_nonzero)
+  return __hneu2_mask(*reinterpret_cast<const __nv_bfloat162*>(&mag), z) & 0x00010001u;
 }
 
 __device__ __forceinline__ uint32_t k4_sel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }

@@ -88,11 +88,14 @@ __global__ void k_sparsify_token(const T* __restrict__ a, long long rows, long l
 
 // ---------------------------------------------------------------------------
 // feature-wise sparsify: thread owns GPT consecutive row-groups of column j.
+// fwd_mask (nullable, uint8 [rows, cols]): entries outside it read as zero
+// before the selection and the counts (sparsify_feature_wise_masked,
+// ref sparse24.py:118-129: masked-out values are not "dropped").
 template <typename T, int GPT>
 __global__ void k_sparsify_feature(const T* __restrict__ a, long long rows, long long cols, long long lda,
                                    __nv_bfloat16* __restrict__ vals_t, uint8_t* __restrict__ meta_ref,
                                    uint8_t* __restrict__ meta_hw, uint8_t* __restrict__ mask,
-                                   unsigned long long* stats) {
+                                   unsigned long long* stats, const uint8_t* __restrict__ fwd_mask) {
   const long long chunks = rows / (4 * GPT);
   const long long total = chunks * cols;
   unsigned long long nb = 0, na = 0;
@@ -105,8 +108,14 @@ __global__ void k_sparsify_feature(const T* __restrict__ a, long long rows, long
     for (int g = 0; g < GPT; ++g) {
       const long long gi = ch * GPT + g;  // row group index
       const long long r0 = gi * 4;
-      const float x0 = ldf(a + r0 * lda + j), x1 = ldf(a + (r0 + 1) * lda + j), x2 = ldf(a + (r0 + 2) * lda + j),
-                  x3 = ldf(a + (r0 + 3) * lda + j);
+      float x0 = ldf(a + r0 * lda + j), x1 = ldf(a + (r0 + 1) * lda + j), x2 = ldf(a + (r0 + 2) * lda + j),
+            x3 = ldf(a + (r0 + 3) * lda + j);
+      if (fwd_mask) {
+        x0 = fwd_mask[r0 * cols + j] ? x0 : 0.f;
+        x1 = fwd_mask[(r0 + 1) * cols + j] ? x1 : 0.f;
+        x2 = fwd_mask[(r0 + 2) * cols + j] ? x2 : 0.f;
+        x3 = fwd_mask[(r0 + 3) * cols + j] ? x3 : 0.f;
+      }
       nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
       const uint32_t keep = top2_keep_mask(x0, x1, x2, x3);
       const uint32_t nib = keep_to_nibble(keep);
@@ -480,9 +489,9 @@ int s24_sparsify_token(const void* a, int dtype, int64_t rows, int64_t cols, int
   return check_launch("k_sparsify_token");
 }
 
-int s24_sparsify_feature(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda, void* vals_t,
-                         uint8_t* meta_ref, uint8_t* meta_hw, uint8_t* mask, unsigned long long* stats,
-                         void* stream) {
+int s24_sparsify_feature_masked(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda,
+                                const uint8_t* fwd_mask, void* vals_t, uint8_t* meta_ref, uint8_t* meta_hw,
+                                uint8_t* mask, unsigned long long* stats, void* stream) {
   if (rows < 0 || cols < 0) return fail(S24_ERR_DIMENSION, "negative shape");
   if (rows % 4 != 0) return fail(S24_ERR_DIMENSION, "feature-wise groups need rows %% 4 == 0, got %lld", (long long)rows);
   if (lda < cols) return fail(S24_ERR_DIMENSION, "lda < cols");
@@ -493,24 +502,30 @@ int s24_sparsify_feature(const void* a, int dtype, int64_t rows, int64_t cols, i
   const bool q = rows % 16 == 0;
   const long long work = rows * cols / (q ? 16 : 4);
   const int g = grid_for(work, 256);
+  auto vt = static_cast<__nv_bfloat16*>(vals_t);
   if (dtype == S24_F32) {
+    auto ap = static_cast<const float*>(a);
     if (q)
-      k_sparsify_feature<float, 4><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
-                                                       static_cast<__nv_bfloat16*>(vals_t), meta_ref, meta_hw, mask, stats);
+      k_sparsify_feature<float, 4><<<g, 256, 0, st>>>(ap, rows, cols, lda, vt, meta_ref, meta_hw, mask, stats, fwd_mask);
     else
-      k_sparsify_feature<float, 1><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
-                                                       static_cast<__nv_bfloat16*>(vals_t), meta_ref, nullptr, mask, stats);
+      k_sparsify_feature<float, 1><<<g, 256, 0, st>>>(ap, rows, cols, lda, vt, meta_ref, nullptr, mask, stats, fwd_mask);
   } else {
+    auto ap = static_cast<const __nv_bfloat16*>(a);
     if (q)
-      k_sparsify_feature<__nv_bfloat16, 4><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
-                                                               static_cast<__nv_bfloat16*>(vals_t), meta_ref, meta_hw,
-                                                               mask, stats);
+      k_sparsify_feature<__nv_bfloat16, 4><<<g, 256, 0, st>>>(ap, rows, cols, lda, vt, meta_ref, meta_hw, mask, stats,
+                                                               fwd_mask);
     else
-      k_sparsify_feature<__nv_bfloat16, 1><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
-                                                               static_cast<__nv_bfloat16*>(vals_t), meta_ref, nullptr,
-                                                               mask, stats);
+      k_sparsify_feature<__nv_bfloat16, 1><<<g, 256, 0, st>>>(ap, rows, cols, lda, vt, meta_ref, nullptr, mask, stats,
+                                                               fwd_mask);
   }
   return check_launch("k_sparsify_feature");
+}
+
+int s24_sparsify_feature(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda, void* vals_t,
+                         uint8_t* meta_ref, uint8_t* meta_hw, uint8_t* mask, unsigned long long* stats,
+                         void* stream) {
+  return s24_sparsify_feature_masked(a, dtype, rows, cols, lda, nullptr, vals_t, meta_ref, meta_hw, mask, stats,
+                                     stream);
 }
 
 int s24_compress_token_with_mask(const void* a, int dtype, int64_t rows, int64_t cols, int64_t lda,

@@ -364,10 +364,20 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     out, core = _ffn_forward(_pad_cols(x, dp), _pad_params(p, dp, hp), cfg, plan, keep_pre_act, for_backward,
                              h_valid=h, counts_hook=hook)
     n = core.n
+    stats = None
+    if core.stats is not None:
+        def real_feature_stats():
+            # nonzeros before / after over the real features (the padding
+            # features are zero unless the input carries NaN / Inf)
+            before = core.counts[:h].sum(dtype=torch.int64)
+            vals = core.act_vals[:n].view(n, hp // 4, 2)[:, : h // 4]
+            return torch.stack([before, (vals != 0).sum(dtype=torch.int64)])
+
+        stats = SparsifyStats(n * h, real_feature_stats if hp != h else core.stats._dev)
     view = replace(core, pre_act=core.pre_act[:, :h] if core.pre_act is not None else None,
                    counts=core.counts[:h] if core.counts is not None else None,
                    _plan=core.plan_valid if core.plan_valid is not None else core._plan,
-                   stats=SparsifyStats(n * h, core.stats._dev) if core.stats is not None else None,
+                   stats=stats,
                    census=_census_real(core.census, n, d, h, core.plan_valid, cfg),
                    core=core, d_valid=d, h_valid=h, plan_valid=None)
     return (out[:, :d].contiguous() if dp != d else out), view

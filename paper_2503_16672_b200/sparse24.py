@@ -161,8 +161,15 @@ def sparsify_token_wise(a):
 
 def sparsify_feature_wise(a):
     """Top-2-per-group down each column (ref sparse24.py:96-115)."""
+    return _sparsify_feature(a, None)
+
+
+def _sparsify_feature(a, fwd_mask):
     a = as_matrix(a, "a")
     rows, cols = a.shape
+    m8 = None
+    if fwd_mask is not None:
+        m8 = _as_mask(fwd_mask, a.shape, a.device).to(torch.uint8).contiguous()
     if rows % 4 != 0:
         raise DimensionError(f"feature-wise groups need rows % 4 == 0, got {rows}")
     with_hw = rows % 128 == 0
@@ -174,8 +181,8 @@ def sparsify_feature_wise(a):
     meta_ref = torch.empty(rows // 4, cols, 2, dtype=torch.uint8, device=a.device)
     mask = torch.empty(rows, cols, dtype=torch.uint8, device=a.device)
     cnt = _new_stats_counter(a.device)
-    _lib.call("s24_sparsify_feature", ptr(a), dtype_code(a), rows, cols, a.stride(0), ptr(data), ptr(meta_ref),
-              ptr(hw), ptr(mask), ptr(cnt), stream())
+    _lib.call("s24_sparsify_feature_masked", ptr(a), dtype_code(a), rows, cols, a.stride(0), ptr(m8), ptr(data),
+              ptr(meta_ref), ptr(hw), ptr(mask), ptr(cnt), stream())
     s = Sparse24Matrix(rows, cols, FEATURE_WISE, data, hw, meta_ref)
     return s, mask.bool(), SparsifyStats(rows * cols, cnt)
 
@@ -197,8 +204,9 @@ def apply_mask(a, mask) -> torch.Tensor:
 
 def sparsify_feature_wise_masked(a, fwd_mask):
     """Zero entries outside fwd_mask, then sparsify feature-wise; masked-out
-    values do not count as dropped (ref sparse24.py:118-129)."""
-    return sparsify_feature_wise(apply_mask(a, fwd_mask))
+    values do not count as dropped (ref sparse24.py:118-129). One device pass:
+    the mask is applied while the kernel reads the operand."""
+    return _sparsify_feature(a, fwd_mask)
 
 
 def compress_token_wise_with_mask(a, mask) -> Sparse24Matrix:

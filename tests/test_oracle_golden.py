@@ -188,3 +188,54 @@ def test_fp8_selects_before_quantizing(f8):
     eye = np.eye(4, dtype=np.float32)
     _, cache = O.ffn_forward(f8["kat_sel_x"], eye, eye, dict(O.DENSE, forward_mode="sparse24", fp8_emulation=True))
     assert np.array_equal(cache["meta"], f8["kat_sel_meta"])
+
+
+@pytest.fixture(scope="module")
+def nf():
+    return np.load(GOLD / "nonfinite.npz")
+
+
+def test_nonfinite_selection_counts_and_plan(nf):
+    """NaN / Inf as the reference treats them (fixtures from the reference
+    itself): NaN ranks below zero, counts as a nonzero, Inf ranks above all."""
+    for i in range(2):
+        a = nf[f"tok{i}_a"]
+        v, m, mask, st = O.sparsify_token(a)
+        assert np.array_equal(v, nf[f"tok{i}_values"], equal_nan=True)
+        assert np.array_equal(m, nf[f"tok{i}_meta"]) and np.array_equal(mask, nf[f"tok{i}_mask"])
+        assert _stats(st) == nf[f"tok{i}_stats"].tolist()
+        fv, fm, _, fst = O.sparsify_feature(a)
+        assert np.array_equal(fv, nf[f"feat{i}_values"], equal_nan=True)
+        assert np.array_equal(fm, nf[f"feat{i}_meta"]) and _stats(fst) == nf[f"feat{i}_stats"].tolist()
+        counts = O.column_counts(a)
+        assert np.array_equal(counts, nf[f"counts{i}"])
+        assert np.array_equal(O.partition(counts, 0.75)[0], nf[f"plan{i}_sparse"])
+
+
+def test_nonfinite_ffn(nf):
+    cfg = dict(O.RECIPE)
+    with np.errstate(all="ignore"):
+        out, cache = O.ffn_forward(nf["ffn_x"], nf["ffn_w1"], nf["ffn_w2"], cfg)
+        g = O.ffn_backward(nf["ffn_g"], cache, nf["ffn_w1"], nf["ffn_w2"], cfg)
+    assert np.array_equal(cache["mask"], nf["ffn_mask"])
+    assert np.array_equal(cache["plan"][0], nf["ffn_plan_sparse"])
+    assert np.array_equal(out, nf["ffn_out"], equal_nan=True)
+    for k in ("d_x", "d_w1", "d_w2"):
+        assert np.array_equal(g[k], nf[f"ffn_{k}"], equal_nan=True), k
+
+
+def test_masked_feature_wise_kats(nf):
+    """ref tests/test_sparse24.py:119-140: all-ones mask = plain feature-wise,
+    all-zeros mask removes everything and drops nothing, support stays inside
+    the mask; plus random masks against the reference's own outputs."""
+    for tag in ("ones", "zeros"):
+        v, m, _, st = O.sparsify_feature_masked(nf[f"masked_{tag}_a"], nf[f"masked_{tag}_mask"])
+        assert np.array_equal(v, nf[f"masked_{tag}_values"]) and np.array_equal(m, nf[f"masked_{tag}_meta"])
+        assert _stats(st) == nf[f"masked_{tag}_stats"].tolist()
+    assert nf["masked_zeros_stats"].tolist()[1:] == [0, 0, 0]
+    for i in range(4):
+        a, mask = nf[f"masked_r{i}_a"], nf[f"masked_r{i}_mask"]
+        v, m, keep, st = O.sparsify_feature_masked(a, mask)
+        assert np.array_equal(v, nf[f"masked_r{i}_values"]) and np.array_equal(m, nf[f"masked_r{i}_meta"])
+        assert np.array_equal(keep, nf[f"masked_r{i}_keep"]) and _stats(st) == nf[f"masked_r{i}_stats"].tolist()
+        assert not np.any(O.decompress_feature(v, m, *a.shape)[~mask] != 0)
