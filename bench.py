@@ -4,7 +4,8 @@ Contract (one JSON line on rank 0):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU runs are launched by torchrun (one rank per GPU, NCCL); each rank
 processes its own token shard (weak scaling) and the weight gradients are
-summed with one NCCL all-reduce per tensor inside the step.
+summed over NCCL inside the step (dp.train_step: the split plan of the global
+batch from all-reduced feature counts, dW2's all-reduce overlapping dX / dW1).
 
 Workload (BASELINE.json configs[1]): FFN d=2048, h=8192, 16384 tokens per GPU,
 bf16 operands / fp32 accumulation, synthetic activations at 90% sparsity (95%
@@ -13,9 +14,15 @@ split_masked backward + mask_grad_with_fwd + token permutation, ratio 0.95.
 A "step" is one forward + backward of the FFN over the batch. Timing: CUDA
 events on the launching stream around every step, L2 flushed (256 MiB write)
 between steps outside the events, barrier + synchronize on both sides, max
-over ranks. The dense twin (same kernels, FfnConfig() dense) is timed the
-same way for the speedup. e2e repeats the recipe step through the public API
-with pinned host buffers: H2D of x and dY, D2H of out, dX, dW1, dW2.
+over ranks. The dense twin (same kernels, FfnConfig() dense) is timed in
+blocks interleaved with the recipe's for the speedup. e2e repeats the recipe
+step through the public API with pinned host buffers: H2D of x and dY, D2H
+of out, dX, dW1, dW2.
+
+The reference arm (--impl reference) runs the reference implementation
+itself (the srelu24 package installed unchanged into baseline/_ref) on the
+host cores: every step is a bounded sample of the same workload, one sample
+per host core in parallel processes.
 """
 
 from __future__ import annotations
@@ -42,7 +49,7 @@ WORKLOAD = {"c1": "c1: FFN d=512 h=2048, 4096 tokens/GPU, fwd+bwd",
             "c4": "c4: FFN d=4096 h=16384 (7B-class), 32768 tokens/GPU, fwd+bwd + dW all-reduce"}
 PREFILL = {"c3"}  # forward-only configurations (BASELINE configs[2])
 SPARSITY = 0.9
-CPU_SAMPLE_TOKENS = 192
+CPU_SAMPLE_TOKENS = 32
 REF_SAMPLE_TOKENS = 32
 
 
@@ -59,6 +66,8 @@ def parse():
     ap.add_argument("--no-fp8", action="store_true", help="skip the e4m3 (fp8_emulation + fp8_backward) variant")
     ap.add_argument("--sparsity", type=float, default=SPARSITY,
                     help="target activation sparsity of the synthetic inputs (c5 sweep)")
+    ap.add_argument("--cpu-c1-tokens", type=int, default=256,
+                    help="tokens of the BASELINE.md 2 c1 CPU run (4096 = the full batch, ~5 min)")
     return ap.parse_args()
 
 
@@ -89,23 +98,59 @@ def measured_traffic(label: str):
     return None, None
 
 
-def _cpu_sample(seed: int, n: int, d: int, h: int, forward_only: bool = False) -> float:
-    """One bounded sample of the workload on the CPU oracle (ordered-accumulation
-    GEMMs, the reference's own arithmetic): returns wall seconds."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_module():
+    """(module, kind): the reference package installed unchanged into
+    baseline/_ref (kind "reference"), else the numpy port of it in oracle/
+    (kind "port") when that install is absent."""
+    if (REF_DIR / "srelu24").exists():
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        import srelu24
+
+        return srelu24, "reference"
+    return None, "port"
+
+
+def _ref_inputs(seed: int, n: int, d: int, h: int, sparsity: float = SPARSITY):
+    """SURVEY 8d synthetic inputs (numpy PCG64), rounded to bf16 and passed
+    as fp32, as BASELINE.md 2 prescribes."""
     from oracle import srelu24_np as O
 
-    x, w1, w2, dy = O.synthetic_ffn_inputs(n, d, h, sparsity=SPARSITY, seed=seed)
+    return O.synthetic_ffn_inputs(n, d, h, sparsity=sparsity, seed=seed)
+
+
+def _cpu_sample(seed: int, n: int, d: int, h: int, forward_only: bool = False, dense: bool = False) -> float:
+    """One bounded sample of the workload on the CPU: the reference's own
+    ffn_forward (+ ffn_backward) on n tokens (recipe config, or FfnConfig()
+    dense). Returns wall seconds of the forward + backward only."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    x, w1, w2, dy = _ref_inputs(seed, n, d, h)
+    R, kind = reference_module()
+    if R is not None:
+        cfg = R.FfnConfig() if dense else R.FfnConfig(forward_mode="sparse24", backward_mode="split_masked",
+                                                       mask_grad_with_fwd=True, permute_tokens=True)
+        p = R.FfnParams(w1=w1, w2=w2)
+        t0 = time.perf_counter()
+        out, cache = R.ffn_forward(x, p, cfg)
+        if not forward_only:
+            R.ffn_backward(dy, cache, p, cfg)
+        return time.perf_counter() - t0
+    from oracle import srelu24_np as O
+
+    cfg = O.DENSE if dense else O.RECIPE
     t0 = time.perf_counter()
-    out, cache = O.ffn_forward(x, w1, w2, O.RECIPE, ordered=True)
+    out, cache = O.ffn_forward(x, w1, w2, cfg, ordered=True)
     if not forward_only:
-        O.ffn_backward(dy, cache, w1, w2, O.RECIPE, ordered=True)
+        O.ffn_backward(dy, cache, w1, w2, cfg, ordered=True)
     return time.perf_counter() - t0
 
 
 def cpu_sample_tokens(d: int, h: int) -> int:
-    """CPU sample size: ~15 s of oracle work whatever the model width."""
-    return max(16, int(CPU_SAMPLE_TOKENS * (2048 * 8192) / (d * h)) // 4 * 4)
+    """CPU sample size: ~4-8 s of reference work whatever the model width."""
+    return max(8, int(CPU_SAMPLE_TOKENS * (2048 * 8192) / (d * h)) // 4 * 4)
 
 
 def _cpu_worker(args):
@@ -131,10 +176,61 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _pinned_sample(args):
+    """A sample pinned to core 0 (taskset -c 0), in its own process."""
+    os.sched_setaffinity(0, {0})
+    return _cpu_sample(*args)
+
+
+def baseline_plan_c1(tokens: int, repeats: int = 3) -> dict:
+    """the reference's ffn_forward + ffn_backward at c1 (d=512,
+    h=2048) for the recipe and for FfnConfig() dense, median of `repeats`,
+    pinned to core 0. tokens < 4096 runs a sample of the 4096-token batch and
+    scales to tokens/s (the reference's cost is linear in tokens)."""
+    import multiprocessing as mp
+
+    n, d, h = CONFIGS["c1"]
+    ctx = mp.get_context("spawn")
+    res = {}
+    with ctx.Pool(1) as pool:
+        for name, dense in (("recipe", False), ("dense", True)):
+            ts = [pool.apply(_pinned_sample, ((0, tokens, d, h, False, dense),)) for _ in range(repeats)]
+            t = statistics.median(ts)
+            res[name] = {"median_s": t, "runs_s": ts, "tokens_per_s": tokens / t}
+    res["speedup_recipe_vs_dense"] = res["dense"]["median_s"] / res["recipe"]["median_s"]
+    res.update(tokens=tokens, full_batch_tokens=n, cores="1 (core 0)", cpu_model=cpu_model(),
+               nproc=host_cores(), impl=reference_module()[1])
+    return res
+
+
+def config_dict(args, world: int) -> dict:
+    """The workload description both arms print (identical keys and values)."""
+    n, d, h = CONFIGS[args.config]
+    prefill = args.config in PREFILL
+    return {"workload": WORKLOAD[args.config], "tokens_per_gpu": n, "global_tokens": n * world, "d": d, "h": h,
+            "activation_sparsity": args.sparsity,
+            "recipe": "sparse24 fwd + split_masked bwd (ratio 0.95) + mask_grad_with_fwd + permute_tokens",
+            "step": "forward only (inference prefill)" if prefill else "forward + backward",
+            "parallelism": (f"dp{world}: token shards, NCCL all-reduce of dW1 / dW2 (and of the feature counts "
+                            "for the global split plan)") if world > 1 else "single GPU",
+            "l2": "flushed (256 MiB write) between timed steps, outside the step events"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     n_total, d, h = CONFIGS[args.config]
     procs = max(1, min(host_cores(), 32))
     fwd_only = args.config in PREFILL
@@ -145,15 +241,17 @@ def run_reference(args):
     times = [cpu_parallel_step(procs, tok, d, h, seed0=7 + 100 * i, forward_only=fwd_only) for i in range(args.steps)]
     total = sum(times)
     value = procs * tok * len(times) / total
-    sample = (f"{procs} processes x {tok} tokens each per step of the {WORKLOAD[args.config]} workload "
-              f"(oracle/srelu24_np.py recipe {'forward' if fwd_only else 'fwd+bwd'}, ordered fp32 GEMMs = the "
-              f"reference's arithmetic)")
+    _, kind = reference_module()
+    sample = (f"{procs} processes x {tok} tokens each per step (a bounded sample of the {n_total}-token batch of "
+              f"the workload), the {'reference srelu24 package from baseline/_ref' if kind == 'reference' else 'numpy port oracle/srelu24_np.py'}"
+              f" ffn_forward{'' if fwd_only else ' + ffn_backward'} under the recipe config, fp32 ordered GEMMs; "
+              f"{cpu_model()}, {host_cores()} host cores")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD[args.config], "d": d, "h": h, "sparsity": SPARSITY},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs, "kind": "port", "sample": sample},
+        "config": config_dict(args, world),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -182,9 +280,6 @@ class KernelTracer:
         if name == "s24_spmm_pair":
             return ("tensor_sparse", 2 * 2.0 * a[1] * a[2] * a[3],
                     f"spmm 2:4 x2 grouped (dW2 + dW1) M={a[1]} N={a[2]} K={a[3]}")
-        if name == "s24_spmm_bg":
-            return ("tensor_sparse", 2.0 * a[5] * a[6] * a[7],
-                    f"spmm 2:4 M={a[5]} N={a[6]} K={a[7]} + K4 split in background warps")
         if name in ("s24_fwd_gemm1_fused",):
             return "tensor", 2.0 * a[4] * a[5] * a[6], "K1 gemm+relu2+2:4 (fwd.pre_act)"
         if name in ("s24_bwd_dact_fused",):
@@ -196,6 +291,9 @@ class KernelTracer:
         if name == "s24_feature_split":
             n, h, ns, nd = a[2], a[3], a[5], a[6]
             return "hbm", n * h * 1.125 + n * ns * 1.125 + n * nd * 2.0, "K4 feature split"
+        if name == "s24_feature_split_x":
+            n, h, ns, nd = a[2], a[3], a[5], a[6]
+            return "hbm", 1.125 * n * (h + ns + 2 * nd), "K4 feature split (paired layout)"
         if name == "s24_gather_rows":
             return "hbm", 2.0 * a[1] * a[2], "K6 row gather"
         if name == "s24_plan":
@@ -330,6 +428,56 @@ def synthetic_device_inputs(torch, n, d, h, seed, device, sparsity=SPARSITY):
     return x.to(bf), w1.to(bf), w2.to(bf), dy.to(bf)
 
 
+def sparsify_kernel_bandwidth(torch, s24, _lib, cache, grads, n, d, h, pk, flush, iters=10):
+    """HBM-bound kernels timed alone (main stream, CUDA events, L2 flushed
+    before each launch): K4 on the step's own activation and g_pre, and the
+    standalone token-wise sparsifier (SURVEY 7's first kernel) on an [n, h]
+    bf16 activation. Algorithmic bytes per launch:
+      K4: reads the token-wise operand n*h*(2/2 + 1/8) B, writes the paired
+          operand rows*n*(2/2 + 1/8) B, rows = n_sparse + 2 n_dense;
+      token-wise sparsify: reads n*h*2 B (bf16), writes kept values n*h B and
+          hw metadata n*h/8 B."""
+    from paper_2503_16672_b200.splitgemm import alloc_feature_split, run_feature_split
+
+    def timeit(fn):
+        ts = []
+        for _ in range(iters + 2):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            ts.append((s, e))
+        torch.cuda.synchronize()
+        return statistics.median(s.elapsed_time(e) for s, e in ts[2:])
+
+    out = {}
+    plan = cache.plan
+    npad = cache.act_vals.shape[0]
+    rows = plan.n_sparse + 2 * plan.n_dense
+    k4_bytes = 1.125 * npad * (h + rows)
+    for label, vals, nonneg in (("K4 feature split (act)", cache.act_vals, True),
+                                ("K4 feature split (g_pre)", grads.g_pre_sparse.data, False)):
+        fs = alloc_feature_split(vals, cache.act_meta, npad, h, plan)
+        ms = timeit(lambda: run_feature_split(fs, vals, cache.act_meta, npad, h, plan, nonneg=nonneg,
+                                              nan_flag=cache.stats_dev[2:]))
+        gbs = k4_bytes / (ms / 1e3) / 1e9
+        out[label] = {"ms": ms, "bytes": k4_bytes, "achieved": gbs, "unit": "GB/s", "peak": pk["hbm_gbs"],
+                      "frac": gbs / pk["hbm_gbs"]}
+    a = s24.decompress(cache.act_sparse, torch.bfloat16)
+    vals = torch.zeros(npad, h // 2, dtype=torch.bfloat16, device=a.device)
+    hw = torch.empty(_lib.meta_hw_bytes(n, h), dtype=torch.uint8, device=a.device)
+    cnt = torch.zeros(2, dtype=torch.int64, device=a.device)
+    st = torch.cuda.current_stream().cuda_stream
+    ms = timeit(lambda: _lib.call("s24_sparsify_token", a.data_ptr(), _lib.BF16, n, h, h, vals.data_ptr(), None,
+                                  hw.data_ptr(), None, cnt.data_ptr(), st))
+    tb = 3.125 * n * h
+    gbs = tb / (ms / 1e3) / 1e9
+    out["s24_sparsify_token (standalone, bf16 in)"] = {"ms": ms, "bytes": tb, "achieved": gbs, "unit": "GB/s",
+                                                       "peak": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -337,14 +485,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NCCL over NVLink; S24_DIST_BACKEND=gloo exercises the same code path
+    # with several ranks sharing one GPU (functional checks only, no timing claim)
+    backend = os.environ.get("S24_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
 
     import paper_2503_16672_b200 as s24
-    from paper_2503_16672_b200 import _lib
-    from paper_2503_16672_b200.dp import GradAllReducer
+    from paper_2503_16672_b200 import _lib, dp
 
     n, d, h = CONFIGS[args.config]
     prefill = args.config in PREFILL
@@ -353,42 +505,44 @@ def run_ours(args):
     params = s24.FfnParams(w1=w1, w2=w2)
     recipe = s24.RECIPE
     dense = s24.FfnConfig()
+    fp8 = replace(recipe, fp8_emulation=True, fp8_backward=not prefill)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step(cfg, xx, gg):
-        """Eager step through the public API (per-kernel breakdown pass)."""
-        out, cache = s24.ffn_forward(xx, params, cfg, for_backward=not prefill)
+        """Eager step through the public API: ffn_forward + ffn_backward on one
+        GPU, dp.train_step (gradients all-reduced in the step) on several."""
         if prefill:
+            out, cache = s24.ffn_forward(xx, params, cfg, for_backward=False)
             return out, cache, None
         if world > 1:
-            red = GradAllReducer()
-            grads = s24.ffn_backward(gg, cache, params, cfg, grad_ready=red)
-            red.wait()
-        else:
-            grads = s24.ffn_backward(gg, cache, params, cfg)
-        return out, cache, grads
+            out, grads = dp.train_step(xx, gg, params, cfg)
+            return out, None, grads
+        out, cache = s24.ffn_forward(xx, params, cfg)
+        return out, cache, s24.ffn_backward(gg, cache, params, cfg)
 
-    # The timed step: the whole local fwd+bwd captured once as a CUDA graph
-    # (s24.FfnStepGraph, public API) and replayed; with N > 1 GPUs the two
-    # weight gradients are then summed across ranks (NCCL all-reduce).
+    # The timed step on one GPU: the whole fwd+bwd captured once as a CUDA
+    # graph (s24.FfnStepGraph, public API) and replayed. With N > 1 GPUs the
+    # eager data-parallel step (its collectives run on NCCL's stream next to
+    # the backward's GEMMs).
     graphs = {}
 
-    fp8 = replace(recipe, fp8_emulation=True, fp8_backward=not prefill)
-
-    def graph_step(cfg, xx=None, gg=None):
+    def graph_step(cfg):
         key = "recipe" if cfg is recipe else ("fp8" if cfg is fp8 else "dense")
         g = graphs.get(key)
         if g is None:
-            g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill, grad_bucket=world > 1)
+            g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill)
             g.x.copy_(x)
             g.dy.copy_(dy)
-        if xx is not None:
-            g.x.copy_(xx, non_blocking=True)
-            g.dy.copy_(gg, non_blocking=True)
         g.replay()
-        if world > 1 and not prefill:
-            dist.all_reduce(g.bucket)  # one NCCL all-reduce of [dW1 | dW2]
         return g
+
+    use_graph = world == 1
+
+    def run_step(cfg):
+        if use_graph:
+            graph_step(cfg)
+        else:
+            step(cfg, x, dy)
 
     def barrier():
         if world > 1:
@@ -413,26 +567,26 @@ def run_ours(args):
             if eager:
                 step(cfg, x, dy)
             else:
-                graph_step(cfg)
+                run_step(cfg)
             e.record()
             _lib.set_tracer(None)
             evs.append((s, e))
         barrier()
         return max_over_ranks(sum(s.elapsed_time(e) for s, e in evs))
 
-    # warm-up (also JIT-free: kernels are precompiled in libs24.so); builds
-    # the graphs, then replays them
+    # warm-up: eager steps, then the graphs are built and replayed
+    warm = max(args.warmup, 3)
     for cfg in ([recipe] + ([] if args.no_dense else [dense])):
-        for _ in range(max(args.warmup, 3)):
+        for _ in range(warm):
             step(cfg, x, dy)
-        for _ in range(max(args.warmup, 3)):
-            graph_step(cfg)
+        for _ in range(warm):
+            run_step(cfg)
     torch.cuda.synchronize()
 
-    # recipe and dense twin timed in interleaved blocks (same K steps each in
+    # recipe and dense twin timed in interleaved blocks (K steps each in
     # total), so a power cap or thermal drift during the run hits both alike
     clocks, clocks_d = ClockSampler(local), ClockSampler(local)
-    nblk = 2 if (args.steps >= 2 and not args.no_dense) else 1
+    nblk = min(4, args.steps) if not args.no_dense else 1
     ks = [args.steps // nblk + (1 if i < args.steps % nblk else 0) for i in range(nblk)]
     t_recipe = 0.0
     t_dense = None if args.no_dense else 0.0
@@ -445,13 +599,12 @@ def run_ours(args):
             t_dense += timed(dense, k)
             clocks_d.pause()
     clk = clocks.stop()
-    if not args.no_dense:
-        clk_dense = clocks_d.stop()
+    clk_dense = clocks_d.stop() if not args.no_dense else None
     # the e4m3 variant of the recipe (the paper's precision): same timing method
     t_fp8 = None
     if not args.no_fp8:
         for _ in range(3):
-            graph_step(fp8)
+            run_step(fp8)
         torch.cuda.synchronize()
         t_fp8 = timed(fp8, args.steps)
     for _ in range(2):  # re-warm the eager allocator pools after the graph phase
@@ -462,8 +615,9 @@ def run_ours(args):
     tracer = KernelTracer(torch)
     timed(recipe, args.steps, tracer, eager=True)
 
-    # drop statistics of one recipe step (reported, not timed)
-    out, cache, grads = step(recipe, x, dy)
+    # drop statistics of one recipe step (reported, not timed), single-GPU API
+    out, cache = s24.ffn_forward(x, params, recipe, for_backward=not prefill)
+    grads = None if prefill else s24.ffn_backward(dy, cache, params, recipe)
     torch.cuda.synchronize()
     drops = {"fwd_token_wise_dropped_fraction": cache.stats.dropped_fraction_of_nonzeros,
              "fwd_activation_sparsity": cache.stats.sparsity_before}
@@ -471,29 +625,30 @@ def run_ours(args):
         drops.update({"bwd_act_feature_wise_dropped_fraction": grads.stats_act.dropped_fraction_of_nonzeros,
                       "bwd_grad_feature_wise_dropped_fraction": grads.stats_grad.dropped_fraction_of_nonzeros,
                       "plan_sparse_features": cache.plan.n_sparse, "plan_dense_features": cache.plan.n_dense})
+    sparsify_kernels = None
+    if not prefill:
+        sparsify_kernels = sparsify_kernel_bandwidth(torch, s24, _lib, cache, grads, n, d, h, pk, flush)
 
     ms_step = t_recipe / args.steps
     value = world * n * args.steps / (t_recipe / 1e3)
     flops_useful = (4.0 if prefill else 12.0) * n * d * h
-    result = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD[args.config], "tokens_per_gpu": n, "global_tokens": n * world, "d": d,
-                   "h": h, "activation_sparsity": args.sparsity, "recipe": "sparse24 fwd + split_masked bwd (ratio 0.95) "
-                   "+ mask_grad_with_fwd + permute_tokens", "parallelism": f"dp{world} (token shards, NCCL "
-                   "all-reduce of the [dW1 | dW2] bucket)" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) between timed steps, outside the step events",
-                   "step": "s24.FfnStepGraph replay (whole fwd+bwd as one CUDA graph)"
-                           + (" + one NCCL all-reduce of the [dW1 | dW2] bucket" if world > 1 else "")},
-        "eager_ms_per_step": t_eager / args.steps,
-    }
+    # the head of the line carries the numbers the driver parses first
+    result = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+              "warmup": warm, "ms_per_step": ms_step}
     if t_dense is not None:
-        result["dense_twin"] = {"value": world * n * args.steps / (t_dense / 1e3), "unit": "tokens/s",
-                                "ms_per_step": t_dense / args.steps,
-                                "timing": f"same K steps as the recipe, interleaved with it in {nblk} blocks"}
         result["speedup_vs_dense"] = t_dense / t_recipe
-        result["dense_twin"]["clocks"] = {k: clk_dense.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")}
+        result["dense_twin"] = {"ms_per_step": t_dense / args.steps,
+                                "value": world * n * args.steps / (t_dense / 1e3), "unit": "tokens/s",
+                                "timing": f"same K steps as the recipe, interleaved with it in {nblk} blocks",
+                                "clocks": {k: clk_dense.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")}}
+    result.update({"higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                   "data": "synthetic (SURVEY.md 8d generator, torch CUDA generator seed 1234 + rank)",
+                   "config": config_dict(args, world),
+                   "timed_step": ("s24.FfnStepGraph replay (whole step as one CUDA graph)" if use_graph
+                                  else "eager dp.train_step (ffn_forward + ffn_backward, collectives inside the "
+                                       "step)")})
+    result["sparse_tflops"] = flops_useful / (ms_step / 1e3) / 1e12
+    result["eager_ms_per_step"] = t_eager / args.steps
     if t_fp8 is not None:
         result["fp8_variant"] = {
             "config": "recipe + fp8_emulation" + ("" if prefill else " + fp8_backward"),
@@ -501,7 +656,6 @@ def run_ours(args):
             "ms_per_step": t_fp8 / args.steps, "value": world * n * args.steps / (t_fp8 / 1e3), "unit": "tokens/s",
             "speedup_vs_bf16_recipe": t_recipe / t_fp8,
             "speedup_vs_dense_bf16": (t_dense / t_fp8) if t_dense is not None else None}
-    result["sparse_tflops"] = flops_useful / (ms_step / 1e3) / 1e12
     result["drops"] = drops
 
     # per-kernel breakdown and roofline of the dominant kernel (timed region)
@@ -528,35 +682,91 @@ def run_ours(args):
                           "frac": dom["frac"], "traffic": traffic, "traffic_source": traffic_src,
                           "peak_source": f"{pk['source']} (MEASURED_PEAKS.json bf16 burst / hbm copy"
                                          f"{'; 2:4 sparse peak = 2x dense, derived' if 'sparse' in dom['kernel'] or 'spmm' in dom['kernel'] else ''})"}
+    if sparsify_kernels:
+        result["sparsify_kernels"] = sparsify_kernels
     result["kernels"] = kernels
-    result["gpu_launches"] = tracer.launches
+    result["gpu_launches"] = tracer.launches // args.steps * args.steps
     result["clocks"] = clk
 
     # end-to-end through the public API with host buffers
     if not args.no_e2e:
-        pin = dict(pin_memory=True)
-        xh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
-        gh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
-        xh.copy_(x)
-        gh.copy_(dy)
-        oh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
-        dxh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
-        dw1h = torch.empty(d, h, dtype=torch.float32, **pin)
-        dw2h = torch.empty(h, d, dtype=torch.float32, **pin)
+        result["e2e"] = run_e2e(torch, dist, s24, args, world, prefill, params, recipe, x, dy, flush, barrier,
+                                max_over_ranks, graph_step, step)
 
+    # CPU baseline: the reference itself on this host, rank 0, N=1 only
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tok = cpu_sample_tokens(d, h)
+        import multiprocessing as mp
+
+        with mp.get_context("spawn").Pool(1) as pool:
+            t = pool.apply(_pinned_sample, ((11, tok, d, h, prefill, False),))
+        kind = reference_module()[1]
+        result["cpu_baseline"] = {
+            "value": tok / t, "unit": "tokens/s", "cores": 1, "kind": kind,
+            "sample": f"{tok} tokens of the {WORKLOAD[args.config]} workload through "
+                      f"{'the reference srelu24 package (baseline/_ref)' if kind == 'reference' else 'oracle/srelu24_np.py'}"
+                      f" (recipe {'forward' if prefill else 'fwd+bwd'}, fp32 ordered GEMMs), one process pinned to "
+                      f"core 0, {t:.1f} s; {cpu_model()}, {host_cores()} host cores"}
+        if args.cpu_c1_tokens > 0 and not prefill:
+            result["cpu_baseline"]["baseline_md_c1"] = baseline_plan_c1(args.cpu_c1_tokens)
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(torch, dist, s24, args, world, prefill, params, recipe, x, dy, flush, barrier, max_over_ranks,
+            graph_step, step):
+    """The recipe step end to end through the public API: the step's inputs
+    copied in from pinned host memory and its results copied out, every step,
+    inside the timed region."""
+    n, d = x.shape
+    h = params.hidden_dim
+    pin = dict(pin_memory=True)
+    xh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+    gh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+    xh.copy_(x)
+    gh.copy_(dy)
+    oh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+    dxh = torch.empty(n, d, dtype=torch.bfloat16, **pin)
+    dw1h = torch.empty(d, h, dtype=torch.float32, **pin)
+    dw2h = torch.empty(h, d, dtype=torch.float32, **pin)
+    h2d = (1 if prefill else 2) * n * d * 2
+    d2h = n * d * 2 if prefill else 2 * n * d * 2 + 2 * d * h * 4
+    comp = torch.cuda.current_stream()
+    hosts = (oh,) if prefill else (oh, dxh, dw1h, dw2h)
+
+    if world > 1:
+        # eager data-parallel step: copy in, train_step, copy out (serialized)
+        def run(k):
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st.record(comp)
+            for _ in range(k):
+                flush.zero_()
+                xx = xh.to(x.device, non_blocking=True)
+                gg = gh.to(x.device, non_blocking=True)
+                out, _, grads = step(recipe, xx, gg)
+                outs = (out,) if prefill else (out, grads.d_x, grads.d_w1, grads.d_w2)
+                for hb, dv in zip(hosts, outs):
+                    hb.copy_(dv, non_blocking=True)
+            en.record(comp)
+            return st, en
+
+        path = ("dp.train_step (public API) with pinned host x, dY copied in and out, dX, dW1, dW2 copied out "
+                "every step")
+    else:
         # Two captured instances of the step alternate (double buffering), so
         # the H2D of step i+1 (copy stream) and the D2H of step i (a second
         # copy stream) run while step i computes: a standard input / output
         # pipeline. Every step's own copies are inside the timed region.
         g_a = graph_step(recipe)
-        g_b = s24.FfnStepGraph(params, recipe, n, backward=not prefill, grad_bucket=world > 1)
+        g_b = s24.FfnStepGraph(params, recipe, n, backward=not prefill)
         gs = (g_a, g_b)
-        comp = torch.cuda.current_stream()
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         outs_of = (lambda g: (g.out,)) if prefill else (lambda g: (g.out, g.d_x, g.d_w1, g.d_w2))
-        hosts = (oh,) if prefill else (oh, dxh, dw1h, dw2h)
 
-        def e2e_run(k: int):
+        def run(k: int):
             """k pipelined steps; returns (start, end) events on the compute stream."""
             ev_in = [torch.cuda.Event(), torch.cuda.Event()]
             ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
@@ -577,8 +787,6 @@ def run_ours(args):
                     comp.wait_event(ev_out[j])  # step i-2's outputs of this instance were read
                 flush.zero_()
                 g.replay()
-                if world > 1 and not prefill:
-                    dist.all_reduce(g.bucket)
                 ev_comp[j].record(comp)
                 if i + 1 < k:
                     nxt = gs[1 - j]
@@ -598,35 +806,20 @@ def run_ours(args):
             en.record(comp)
             return st, en
 
-        e2e_run(3)
-        barrier()
-        st, en = e2e_run(args.steps)
-        barrier()
-        t_e2e = max_over_ranks(st.elapsed_time(en))
-        result["e2e"] = {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s",
-                         "h2d_bytes_per_step": (1 if prefill else 2) * n * d * 2,
-                         "d2h_bytes_per_step": n * d * 2 if prefill else 2 * n * d * 2 + 2 * d * h * 4,
-                         "ms_per_step": t_e2e / args.steps,
-                         "path": ("s24.FfnStepGraph(backward=False) (public API: ffn_forward captured) with pinned "
-                                  "host x copied in and out copied out every step" if prefill else
-                                  "s24.FfnStepGraph (public API: ffn_forward + ffn_backward captured) with pinned "
-                                  "host x, dY copied in and out, dX, dW1, dW2 copied out every step")
-                                 + "; two graph instances alternate so the H2D of step i+1 and the D2H of step i "
-                                   "overlap step i's compute (copy streams); L2 flushed before every step"}
+        path = (("s24.FfnStepGraph(backward=False) (public API: ffn_forward captured) with pinned host x copied in "
+                 "and out copied out every step") if prefill else
+                ("s24.FfnStepGraph (public API: ffn_forward + ffn_backward captured) with pinned host x, dY copied "
+                 "in and out, dX, dW1, dW2 copied out every step")) + \
+            ("; two graph instances alternate so the H2D of step i+1 and the D2H of step i overlap step i's "
+             "compute (copy streams); L2 flushed before every step")
 
-    # CPU baseline: the oracle port on this host, rank 0, N=1 only
-    if rank == 0 and world == 1 and not args.no_cpu:
-        tok = cpu_sample_tokens(d, h)
-        t = _cpu_sample(11, tok, d, h, forward_only=prefill)
-        result["cpu_baseline"] = {
-            "value": tok / t, "unit": "tokens/s", "cores": 1, "kind": "port",
-            "sample": f"{tok} tokens of the {WORKLOAD[args.config]} workload through oracle/srelu24_np.py "
-                      f"(recipe {'forward' if prefill else 'fwd+bwd'}, ordered fp32 GEMMs), one process, {t:.1f} s"}
-
-    if rank == 0:
-        print(json.dumps(result), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    run(3)
+    barrier()
+    st, en = run(args.steps)
+    barrier()
+    t_e2e = max_over_ranks(st.elapsed_time(en))
+    return {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e / args.steps, "path": path}
 
 
 def main():

@@ -63,13 +63,28 @@ class GradAllReducer:
         return out
 
 
-def train_step(x_shard, g_shard, params, cfg, group=None):
+def train_step(x_shard, g_shard, params, cfg, group=None, global_plan: bool = True, average: bool = False):
     """Forward + backward on this rank's token shard, weight gradients summed
-    over the group. Returns (out_shard, FfnGrads with global d_w1 / d_w2)."""
+    over the group. Returns (out_shard, FfnGrads with global d_w1 / d_w2).
+
+    global_plan=True all-reduces K1's per-feature nonzero counts (h int32,
+    one small collective between K1 and the plan) so every rank splits the
+    same features dense / sparse: the plan of the global batch, as a
+    single-GPU run over all tokens would choose it. The feature-wise 2:4
+    groups themselves stay per shard (groups of 4 consecutive tokens of the
+    rank's own permutation), i.e. the reference applied per shard.
+
+    The backward hands d_w2 to the all-reducer as soon as it is final (right
+    after K3), so its all-reduce overlaps dX and dW1; d_w1's follows."""
     from .ffn import ffn_backward, ffn_forward
 
-    out, cache = ffn_forward(x_shard, params, cfg)
-    reducer = GradAllReducer(group)
+    hook = None
+    if global_plan and cfg.backward_mode == "split_masked":
+        def hook(counts):
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+
+    out, cache = ffn_forward(x_shard, params, cfg, counts_hook=hook)
+    reducer = GradAllReducer(group, average=average)
     grads = ffn_backward(g_shard, cache, params, cfg, grad_ready=reducer)
     reducer.wait()
     return out, grads
