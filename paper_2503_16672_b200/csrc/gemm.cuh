@@ -46,6 +46,18 @@
 #include "meta.cuh"
 #include "ptx.cuh"
 
+// Work distribution (see the header): S24_STATIC_SCHED = 1 (default) runs a
+// persistent grid of the resident clusters, cluster c taking units c, c + C,
+// c + 2C, ...; 0 launches one cluster per unit and lets running clusters
+// steal the units of not-yet-started ones through cluster launch control.
+// Both need no device memory. Measured (scripts/ab_step.py, c2 step): the
+// pending clusters of a CLC launch keep the block scheduler from placing the
+// side-stream K4 CTAs next to the running GEMM, which starves K4 and stalls
+// the weight gradients that wait for it (1.95 vs 1.92 ms; K4 of act 688 vs
+// 254 us while co-running, scripts/timeline.py).
+#ifndef S24_STATIC_SCHED
+#define S24_STATIC_SCHED 1
+#endif
 #ifndef S24_CLC_PREFETCH
 #define S24_CLC_PREFETCH 1
 #endif
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   // consumer side of the ring (all lanes of the calling warp, or a single
   // thread with one_thread): wait, read, release
   auto sched_take = [&](int iter, bool one_thread) -> int {
-    if (iter == 0) return first_unit;
+    if (S24_STATIC_SCHED || iter == 0) return first_unit + iter * static_cast<int>(gridDim.x / Cfg::CLUSTER);
     const int slot = (iter - 1) % NS;
     mbar_wait(&sched_full[slot], static_cast<uint32_t>((iter - 1) / NS) & 1u);
     const int t = resp_unit(slot);
@@ -312,8 +324,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
       };
       for (int iter = 0;; ++iter) {
         int t;
-        if (iter == 0) {
-          t = first_unit;
+        if (S24_STATIC_SCHED || iter == 0) {
+          t = first_unit + iter * static_cast<int>(gridDim.x / Cfg::CLUSTER);
         } else if (leader) {
 #if S24_CLC_PREFETCH == 0
           request(iter);
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
           t = sched_take(iter, true);
         }
 #if S24_CLC_PREFETCH
-        if (leader && t < total_units) request(iter + 1);
+        if (!S24_STATIC_SCHED && leader && t < total_units) request(iter + 1);
 #endif
         if (t >= total_units) break;
         int half;

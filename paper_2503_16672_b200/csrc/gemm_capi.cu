@@ -165,13 +165,18 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = Cfg::CLUSTER;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // critical-path priority (host_util.h high_priority): when a GEMM becomes
+  // ready together with a side-stream kernel (K4), the block scheduler places
+  // the GEMM's CTA pairs first and K4 fills the registers / warps they leave
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = high_priority();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   // clusters resident at once (one CTA per SM: the stage ring fills smem)
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -194,7 +199,8 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
   }
   // one cluster per work unit; running clusters steal the units of the ones
   // that have not started (cluster launch control, gemm.cuh)
-  const long long units = static_cast<long long>(tiles) + sh.tail_split;
+  long long units = static_cast<long long>(tiles) + sh.tail_split;
+  if (S24_STATIC_SCHED && units > resident) units = resident;  // (persistent grid, static round robin)
   cfg.gridDim = dim3(static_cast<unsigned>(units * Cfg::CLUSTER));
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, me, ma2, mb2, me2, sh, ep, second ? second->ep : ep);
   if (e != cudaSuccess) return fail(S24_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));

@@ -41,6 +41,36 @@ int make_map_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t inner, u
 int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                   uint32_t box_inner, uint32_t box_outer);
 
+// The device's greatest (most urgent) launch priority. Every kernel of the
+// FFN's critical path launches at it (the GEMMs, the row gathers, the plan);
+// K4, which the recipe runs on side streams next to them, keeps the default,
+// so the block scheduler places critical-path CTAs first and K4 fills the
+// room they leave.
+inline int high_priority() {
+  static const int prio = [] {
+    int least = 0, greatest = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+    return greatest;
+  }();
+  return prio;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_high(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, size_t smem,
+                               Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = high_priority();
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct K4Args;

@@ -297,99 +297,134 @@ __global__ void k_gather_rows(const uint8_t* __restrict__ in, long long rows, lo
 // splitgemm.py:49). An 8-bit MSB radix select finds the key of rank
 // n_sparse-1; features with key <= it are sparse. A block scan then emits the
 // ascending index lists (splitgemm.py:50-51) and the per-feature positions.
-__global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts, int h, int n_sparse,
-                                               int* __restrict__ sparse_idx, int* __restrict__ dense_idx,
-                                               int* __restrict__ feat_pos) {
-  __shared__ unsigned int hist[256];
-  __shared__ unsigned long long sh_prefix;
-  __shared__ int sh_rank;
-  __shared__ int warp_tot[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (h + 1023) / 1024;
-  const int j0 = min(h, tid * per), j1 = min(h, j0 + per);
-
-  unsigned long long thr = 0;  // threshold key (inclusive); unused when n_sparse == 0
-  if (n_sparse > 0) {
-    if (tid == 0) {
-      sh_prefix = 0;
-      sh_rank = n_sparse - 1;
-    }
-    unsigned long long maskbits = 0;
-    for (int pass = 0; pass < 6; ++pass) {
-      const int shift = 40 - 8 * pass;
-      for (int b = tid; b < 256; b += 1024) hist[b] = 0;
-      __syncthreads();
-      const unsigned long long prefix = sh_prefix;
-      for (int j = j0; j < j1; ++j) {
-        const unsigned long long key = (static_cast<unsigned long long>(static_cast<unsigned>(counts[j])) << 16) | j;
-        if ((key & maskbits) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      if (wid == 0) {
-        unsigned int loc[8], s = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          loc[i] = hist[lane * 8 + i];
-          s += loc[i];
-        }
-        unsigned int inc = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += t;
-        }
-        const unsigned int exc = inc - s;
-        const int rank = sh_rank;
-        if (static_cast<unsigned>(rank) >= exc && static_cast<unsigned>(rank) < inc) {
-          unsigned int c = exc;
-          int b = 7;
-          for (int i = 0; i < 8; ++i) {
-            if (static_cast<unsigned>(rank) < c + loc[i]) {
-              b = i;
-              break;
-            }
-            c += loc[i];
-          }
-          sh_rank = rank - static_cast<int>(c);
-          sh_prefix = prefix | (static_cast<unsigned long long>(lane * 8 + b) << shift);
-        }
-      }
-      maskbits |= 255ull << shift;
-      __syncthreads();
-    }
-    thr = sh_prefix;
-  }
-
-  // flags and block-wide exclusive scan of sparse counts in index order
-  int my_sparse = 0;
-  for (int j = j0; j < j1; ++j) {
-    const unsigned long long key = (static_cast<unsigned long long>(static_cast<unsigned>(counts[j])) << 16) | j;
-    my_sparse += (n_sparse > 0 && key <= thr) ? 1 : 0;
-  }
-  int inc = my_sparse;
+// K7: partition_features (ref splitgemm.py:41-52) on the device. Stable
+// ascending order of (count, index): the n_sparse smallest keys are sparse.
+// Radix select on the count value (11-bit digits over the significant bits,
+// warp-aggregated shared-memory histograms), then the tie-break among the
+// threshold count's features by index (a block scan), then one block scan
+// that writes both ascending index lists and feat_pos. One CTA.
+__device__ __forceinline__ int block_excl_scan_1024(int v, int* warp_tot, int lane, int wid, int& total) {
+  int inc = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int t = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += t;
   }
+  __syncthreads();  // (warp_tot may still be read by a previous scan)
   if (lane == 31) warp_tot[wid] = inc;
   __syncthreads();
   if (wid == 0) {
-    int v = warp_tot[lane];
-    int vi = v;
+    const int w = warp_tot[lane];
+    int wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, vi, o);
-      if (lane >= o) vi += t;
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
     }
-    warp_tot[lane] = vi - v;
+    warp_tot[lane] = wi - w;
+    if (lane == 31) warp_tot[32] = wi;
   }
   __syncthreads();
-  int s_off = warp_tot[wid] + inc - my_sparse;
+  total = warp_tot[32];
+  return warp_tot[wid] + inc - v;
+}
+
+__global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts_g, int h, int n_sparse,
+                                               int* __restrict__ sparse_idx, int* __restrict__ dense_idx,
+                                               int* __restrict__ feat_pos, int counts_in_smem) {
+  constexpr int DIGIT = 11, BINS = 1 << DIGIT;
+  // the counts are read six times: staged in shared memory first (one
+  // coalesced pass) when they fit, so the passes do not wait on L2 / DRAM
+  // latency chains
+  extern __shared__ int s_counts[];
+  const int* __restrict__ counts = counts_g;
+  if (counts_in_smem) {
+    for (int j = threadIdx.x; j < h; j += 1024) s_counts[j] = __ldg(counts_g + j);
+    __syncthreads();
+    counts = s_counts;
+  }
+  __shared__ unsigned hist[BINS];
+  __shared__ int warp_tot[33];
+  __shared__ unsigned sh_max, sh_prefix;
+  __shared__ int sh_rank, sh_jstar;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (h + 1023) / 1024;
+  const int j0 = min(h, tid * per), j1 = min(h, j0 + per);
+
+  unsigned cstar = 0xFFFFFFFFu;  // threshold count; features with count < cstar are sparse
+  int jstar = -1;                // ... and those with count == cstar up to index jstar
+  if (n_sparse > 0) {
+    if (tid == 0) {
+      sh_max = 0;
+      sh_prefix = 0;
+      sh_rank = n_sparse - 1;
+    }
+    __syncthreads();
+    unsigned mx = 0;
+    for (int j = j0; j < j1; ++j) mx = max(mx, static_cast<unsigned>(counts[j]));
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) atomicMax(&sh_max, mx);
+    __syncthreads();
+    const int bits = 32 - __clz(static_cast<int>(sh_max | 1u));
+    // digits from the most significant one down
+    for (int hi = bits; hi > 0; hi -= DIGIT) {
+      const int shift = max(hi - DIGIT, 0), width = hi - shift;
+      for (int b = tid; b < BINS; b += 1024) hist[b] = 0;
+      __syncthreads();
+      const unsigned prefix = sh_prefix;  // the bits above `hi` of the threshold
+      for (int i = 0; i < per; ++i) {
+        const int j = j0 + i;
+        unsigned bin = 0xFFFFFFFFu;
+        if (j < j1) {
+          const unsigned c = static_cast<unsigned>(counts[j]);
+          if ((hi >= 32 ? 0u : (c >> hi)) == prefix) bin = (c >> shift) & ((1u << width) - 1u);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+      }
+      __syncthreads();
+      // locate the digit holding rank sh_rank: each thread scans 2 bins
+      const unsigned h0 = hist[2 * tid], h1 = hist[2 * tid + 1];
+      int total;
+      const int exc = block_excl_scan_1024(static_cast<int>(h0 + h1), warp_tot, lane, wid, total);
+      const int rank = sh_rank;
+      __syncthreads();
+      if (rank >= exc && rank < exc + static_cast<int>(h0 + h1)) {
+        const bool first = rank < exc + static_cast<int>(h0);
+        const unsigned digit = 2u * tid + (first ? 0u : 1u);
+        sh_rank = rank - exc - (first ? 0 : static_cast<int>(h0));
+        sh_prefix = (prefix << width) | digit;
+      }
+      __syncthreads();
+    }
+    cstar = sh_prefix;
+    // tie-break: the (sh_rank)-th feature (by index) with count == cstar
+    int my_eq = 0;
+    for (int j = j0; j < j1; ++j) my_eq += static_cast<unsigned>(counts[j]) == cstar ? 1 : 0;
+    int total;
+    const int exc = block_excl_scan_1024(my_eq, warp_tot, lane, wid, total);
+    const int r = sh_rank;
+    if (r >= exc && r < exc + my_eq) {
+      int seen = exc;
+      for (int j = j0; j < j1; ++j)
+        if (static_cast<unsigned>(counts[j]) == cstar && seen++ == r) sh_jstar = j;
+    }
+    __syncthreads();
+    jstar = sh_jstar;
+  }
+
+  // flags and block-wide exclusive scan of sparse counts in index order
+  auto is_sparse = [&](int j) {
+    const unsigned c = static_cast<unsigned>(counts[j]);
+    return n_sparse > 0 && (c < cstar || (c == cstar && j <= jstar));
+  };
+  int my_sparse = 0;
+  for (int j = j0; j < j1; ++j) my_sparse += is_sparse(j) ? 1 : 0;
+  int total;
+  int s_off = block_excl_scan_1024(my_sparse, warp_tot, lane, wid, total);
   int d_off = j0 - s_off;
   for (int j = j0; j < j1; ++j) {
-    const unsigned long long key = (static_cast<unsigned long long>(static_cast<unsigned>(counts[j])) << 16) | j;
-    if (n_sparse > 0 && key <= thr) {
+    if (is_sparse(j)) {
       sparse_idx[s_off] = j;
       feat_pos[j] = s_off;
       ++s_off;
@@ -612,9 +647,9 @@ int s24_gather_rows(const void* in, int64_t rows, int64_t row_bytes, int64_t ld_
     return fail(S24_ERR_DIMENSION, "row gather needs 16-byte aligned rows");
   if (rows == 0 || row_bytes == 0) return S24_OK;
   const int g = grid_for(rows * 32, 256);
-  k_gather_rows<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint8_t*>(in), rows, row_bytes,
-                                                                  ld_in_bytes, src, static_cast<uint8_t*>(out),
-                                                                  ld_out_bytes);
+  launch_high(k_gather_rows, dim3(g), dim3(256), static_cast<cudaStream_t>(stream), 0, static_cast<const uint8_t*>(in),
+              static_cast<long long>(rows), static_cast<long long>(row_bytes), static_cast<long long>(ld_in_bytes), src,
+              static_cast<uint8_t*>(out), static_cast<long long>(ld_out_bytes));
   return check_launch("k_gather_rows");
 }
 
@@ -623,8 +658,10 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
   if (h < 0 || h > 65536) return fail(S24_ERR_DIMENSION, "plan supports 0 <= h <= 65536");
   if (n_sparse < 0 || n_sparse > h) return fail(S24_ERR_CONFIG, "n_sparse out of range");
   if (h == 0) return S24_OK;
+  // (32 registers x 1024 threads and 8 KB of shared memory: the one CTA fits
+  // next to a running 2:4 GEMM CTA, so the plan can overlap fwd.out)
   k_plan<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(counts, static_cast<int>(h), static_cast<int>(n_sparse),
-                                                            sparse_idx, dense_idx, feat_pos);
+                                                            sparse_idx, dense_idx, feat_pos, 0);
   return check_launch("k_plan");
 }
 
@@ -641,8 +678,13 @@ int s24_feature_split_x(const void* vals, const uint8_t* meta_hw, int64_t n, int
   if (n == 0 || h == 0) return S24_OK;
   K4xArgs a{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
             static_cast<int>(2 * n_dense), static_cast<__nv_bfloat16*>(vs), es, nan_flag};
-  dim3 grid(static_cast<unsigned>(h / 128), static_cast<unsigned>(n / 128));
-  (operand_nonneg ? k_feature_split_x<true> : k_feature_split_x<false>)<<<grid, 256, 0, st>>>(a);
+  long long grid = (h / (16 * K4X_WARPS)) * (n / 128);
+#ifdef S24_K4X_CTAS_PER_SM
+  if (S24_K4X_CTAS_PER_SM > 0 && grid > static_cast<long long>(num_sms()) * S24_K4X_CTAS_PER_SM)
+    grid = static_cast<long long>(num_sms()) * S24_K4X_CTAS_PER_SM;
+#endif
+  (operand_nonneg ? k_feature_split_x<true> : k_feature_split_x<false>)<<<static_cast<unsigned>(grid), 32 * K4X_WARPS, 0,
+                                                                         st>>>(a);
   return check_launch("k_feature_split_x");
 }
 

@@ -51,7 +51,6 @@ from .splitgemm import (
     side_stream,
     split_gemm_macs,
     split_weight_grad,
-    split_weight_grad_pair,
 )
 
 ACTIVATIONS = ("squared_relu", "swiglu")
@@ -498,10 +497,11 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
     if counts_hook is not None:
         counts_hook(counts)
 
-    # fwd.out on tensor cores (inverse permutation as its epilogue row map).
-    # Next to it, on the side stream: the split plan (K7), x_in's padded copy
-    # and -- when the backward will need it -- K4, the feature-wise split of
-    # act. Their outputs are allocated here, on the main stream.
+    # fwd.out on tensor cores (inverse permutation as its epilogue row map)
+    # and next to it, on the side stream: the split plan (K7, one small CTA
+    # that fits beside a GEMM CTA), x_in's padded copy and -- when the
+    # backward will need it -- K4, the feature-wise split of act. Their
+    # outputs are allocated here, on the main stream.
     main = torch.cuda.current_stream()
     side = side_stream(dev)
     side.wait_stream(main)
@@ -517,11 +517,12 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
     if split:
         act_split = alloc_feature_split(act_vals, act_meta, npad, h, bplan)
     with torch.cuda.stream(side):
+        if split:
+            bplan.paired_row_map  # (the weight-gradient row map, built on the side stream)
         if x_in is not None and x_in is not k1_in and x_in is not x:
             _fill_frame_rows(x_in, x, None)
         if split:  # (relu^2: >= 0; NaN-aware only if K1 kept a NaN)
             run_feature_split(act_split, act_vals, act_meta, npad, h, bplan, nonneg=True, nan_flag=stats_dev[2:])
-            bplan.paired_row_map  # (the weight-gradient row map, built here off the main stream)
         ev = torch.cuda.Event()
         ev.record(side)
     if x_in is None and for_backward:
@@ -548,10 +549,8 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
 
     grad_ready(name, tensor), if given, is called as soon as d_w2 and then
     d_w1 are final on the current stream (the data-parallel step launches
-    their all-reduce there). With a hook the recipe runs dW2 right after K3,
-    then dX and dW1, so that dW2's all-reduce overlaps the rest of the
-    backward; without one, both weight gradients run in one grouped launch
-    at the end.
+    their all-reduce there). The recipe runs dW2 right after K3, then dX and
+    dW1, so that dW2's all-reduce overlaps the rest of the backward.
     grad_bucket: optional fp32 buffer of 2*d*h elements; d_w1 and d_w2 are then
     written as views into it ([d_w1 | d_w2]), so one collective covers both.
     A padded forward (see ffn_forward) runs the padded backward and returns
@@ -708,31 +707,26 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         notify("d_w1", d_w1)
         return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, stats_g)
 
-    # K4 of g_pre on the side stream, next to the next main-stream GEMM
+    # K4 of g_pre on a second side stream (not queued behind the forward's
+    # K4 of act), next to the next main-stream GEMM
     fg = alloc_feature_split(g_vals, cache.act_meta, npad, h, plan)
+    side = side_stream(dev, 1)
     side.wait_stream(main)
     with torch.cuda.stream(side):
         run_feature_split(fg, g_vals, cache.act_meta, npad, h, plan)
         ev_g = torch.cuda.Event()
         ev_g.record(side)
-    if grad_ready is None:
-        # dX || K4(g_pre), then both split weight gradients in one grouped
-        # launch: dW2 = split(act)^T g_c and dW1^T = split(g_pre)^T x_in share
-        # (rows, d, n), so the second fills the first one's partial last wave
-        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
-        main.wait_event(cache.side_ready)
-        main.wait_event(ev_g)
-        split_weight_grad_pair(fa, fg, plan, g_c, x_in, npad, d_w2, d_w1)
-    else:
-        # data parallel: dW2 first (its all-reduce then overlaps dX and dW1),
-        # K4(g_pre) next to it
-        main.wait_event(cache.side_ready)
-        split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
-        notify("d_w2", d_w2)
-        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
-        main.wait_event(ev_g)
-        split_weight_grad(fg, plan, x_in, npad, d_w1, transposed=True)
-        notify("d_w1", d_w1)
+    # dW2 first (it needs only the forward's split of act, ready long before),
+    # K4(g_pre) next to it and next to dX, then dW1: K4(g_pre) gets two GEMMs
+    # to hide under instead of one, and a data-parallel step's dW2 all-reduce
+    # overlaps dX and dW1
+    main.wait_event(cache.side_ready)
+    split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
+    notify("d_w2", d_w2)
+    _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
+    main.wait_event(ev_g)
+    split_weight_grad(fg, plan, x_in, npad, d_w1, transposed=True)
+    notify("d_w1", d_w1)
     census.insert(1, GemmEvent("bwd.d_w2", True, macs_w))
     census.insert(2, GemmEvent("bwd.d_w1", True, macs_w))
     return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, fg.stats,

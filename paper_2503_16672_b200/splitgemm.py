@@ -198,21 +198,24 @@ def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tenso
     """Fill preallocated K4 outputs on the current stream (no drop counting).
     nan_flag: K1's "a kept value is NaN" word; with nonneg it switches K4 back
     to NaN-aware ranking."""
+    import os
+    if os.environ.get("S24_EXP_SKIP_K4") == "1":
+        return
     _lib.call("s24_feature_split_x", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse,
               plan.n_dense, ptr(fs.vs), ptr(fs.es), int(nonneg), ptr(nan_flag), stream())
 
 
-def side_stream(device) -> torch.cuda.Stream:
-    """The per-device stream that carries K4, the plan and the permuted copies
-    next to the main-stream GEMMs."""
+def side_stream(device, which: int = 0) -> torch.cuda.Stream:
+    """Per-device streams that carry K4 and the permuted copies next to the
+    main-stream GEMMs (0: the forward's, 1: the backward's)."""
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    st = _side_streams.get(idx)
+    st = _side_streams.get((idx, which))
     if st is None:
-        st = _side_streams[idx] = torch.cuda.Stream(device=device)
+        st = _side_streams[(idx, which)] = torch.cuda.Stream(device=device)
     return st
 
 
-_side_streams: dict[int, torch.cuda.Stream] = {}
+_side_streams: dict[tuple[int, int], torch.cuda.Stream] = {}
 
 
 def split_weight_grad(fs: FeatureSplit, plan: SplitPlan, b: torch.Tensor, n: int, out: torch.Tensor,

@@ -3,6 +3,8 @@ builds of libs24.so, in one process so box-to-box and clock drift cancel out.
 
 usage: python scripts/ab_step.py --libs paper_2503_16672_b200/libs24.so,/tmp/alt.so [--blocks 8] [--steps 5]
        [--dense] [--n 16384 --d 2048 --h 8192]
+A variant may carry environment settings read by the Python layer while the
+graph is captured: --libs "a.so,a.so|S24_FOO=1".
 
 Each library is loaded side by side (ctypes) and the whole step is captured
 as a CUDA graph per library (FfnStepGraph), so a graph replays exactly that
@@ -53,14 +55,27 @@ def main():
     p = s24.FfnParams(w1=w1, w2=w2)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     variants = []
-    for i, path in enumerate(args.libs.split(",")):
-        variants.append((f"{i}:{Path(path).name}", load_lib(path), s24.RECIPE))
+    import os
+
+    envs = []
+    for i, spec in enumerate(args.libs.split(",")):
+        path, *kv = spec.split("|")
+        variants.append((f"{i}:{Path(path).name}" + ("|" + "|".join(kv) if kv else ""), load_lib(path), s24.RECIPE))
+        envs.append(dict(e.split("=", 1) for e in kv))
     if args.dense:
         variants.append(("dense_twin", variants[0][1], s24.FfnConfig()))
+        envs.append({})
     graphs = []
-    for name, lib, cfg in variants:
+    for (name, lib, cfg), env in zip(variants, envs):
         _lib._lib = lib
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
         g = s24.FfnStepGraph(p, cfg, n)
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
         g.x.copy_(x)
         g.dy.copy_(dy)
         graphs.append(g)

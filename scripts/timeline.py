@@ -1,0 +1,74 @@
+"""Per-launch timeline of one eager recipe step on both streams (CUDA events
+recorded around every libs24 call on the stream it is launched on, offsets
+from one start event). Shows which side-stream kernels overlap which
+main-stream GEMMs and how long each takes while co-running.
+
+usage: python scripts/timeline.py [--n 16384 --d 2048 --h 8192] [--steps 3]
+"""
+
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import paper_2503_16672_b200 as s24  # noqa: E402
+from paper_2503_16672_b200 import _lib  # noqa: E402
+
+
+class Timeline:
+    def __init__(self):
+        self.recs = []
+        self.main = torch.cuda.current_stream()
+
+    def before(self, name, args):
+        s = torch.cuda.Event(enable_timing=True)
+        s.record()
+        self._open = (name, s, torch.cuda.current_stream())
+
+    def after(self, name):
+        nm, s, st = self._open
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.recs.append((nm, "main" if st == self.main else "side", s, e))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--d", type=int, default=2048)
+    ap.add_argument("--h", type=int, default=8192)
+    ap.add_argument("--steps", type=int, default=3)
+    args = ap.parse_args()
+    import bench  # noqa: E402
+
+    x, w1, w2, dy = bench.synthetic_device_inputs(torch, args.n, args.d, args.h, seed=1234,
+                                                  device=torch.device("cuda"))
+    p = s24.FfnParams(w1=w1, w2=w2)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        out, cache = s24.ffn_forward(x, p, s24.RECIPE)
+        s24.ffn_backward(dy, cache, p, s24.RECIPE)
+    torch.cuda.synchronize()
+    for step in range(args.steps):
+        flush.zero_()
+        tl = Timeline()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        _lib.set_tracer(tl)
+        out, cache = s24.ffn_forward(x, p, s24.RECIPE)
+        g = s24.ffn_backward(dy, cache, p, s24.RECIPE)
+        _lib.set_tracer(None)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record()
+        torch.cuda.synchronize()
+        print(f"--- step {step}: {t0.elapsed_time(t1) * 1e3:.0f} us")
+        for nm, st, s, e in tl.recs:
+            a, b = t0.elapsed_time(s) * 1e3, t0.elapsed_time(e) * 1e3
+            print(f"  {st:4s} {nm:24s} {a:8.1f} -> {b:8.1f}  ({b - a:7.1f} us)")
+
+
+if __name__ == "__main__":
+    main()
