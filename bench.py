@@ -527,7 +527,7 @@ def run_ours(args):
     graphs = {}
 
     def graph_step(cfg):
-        key = "recipe" if cfg is recipe else ("fp8" if cfg is fp8 else "dense")
+        key = cfg
         g = graphs.get(key)
         if g is None:
             g = graphs[key] = s24.FfnStepGraph(params, cfg, n, backward=not prefill)
@@ -601,12 +601,16 @@ def run_ours(args):
     clk = clocks.stop()
     clk_dense = clocks_d.stop() if not args.no_dense else None
     # the e4m3 variant of the recipe (the paper's precision): same timing method
-    t_fp8 = None
+    t_fp8 = t_fp8_dense = None
     if not args.no_fp8:
-        for _ in range(3):
-            run_step(fp8)
+        fp8_dense = replace(dense, fp8_emulation=True, fp8_backward=not prefill)
+        for cfg in (fp8, fp8_dense):
+            for _ in range(3):
+                run_step(cfg)
         torch.cuda.synchronize()
         t_fp8 = timed(fp8, args.steps)
+        if not args.no_dense:
+            t_fp8_dense = timed(fp8_dense, args.steps)
     for _ in range(2):  # re-warm the eager allocator pools after the graph phase
         step(recipe, x, dy)
     t_eager = timed(recipe, args.steps, eager=True)
@@ -656,6 +660,11 @@ def run_ours(args):
             "ms_per_step": t_fp8 / args.steps, "value": world * n * args.steps / (t_fp8 / 1e3), "unit": "tokens/s",
             "speedup_vs_bf16_recipe": t_recipe / t_fp8,
             "speedup_vs_dense_bf16": (t_dense / t_fp8) if t_dense is not None else None}
+        if t_fp8_dense is not None:
+            result["fp8_variant"].update(
+                dense_fp8_ms_per_step=t_fp8_dense / args.steps, speedup_vs_dense_fp8=t_fp8_dense / t_fp8,
+                dense_fp8_path="FfnConfig(fp8_emulation, fp8_backward) dense: the same e4m3 GEMMs, dense operands "
+                               "(relu^2 / derivative and quantization between them unfused)")
     result["drops"] = drops
 
     # per-kernel breakdown and roofline of the dominant kernel (timed region)

@@ -10,17 +10,19 @@ rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
-want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+want = ["Kernel Name", "gpu__time_duration.sum", "gpc__cycles_elapsed.max.per_second", "dram__bytes_read.sum",
+        "dram__bytes_write.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-        "launch__registers_per_thread", "sm__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__occupancy_limit_registers",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__cycles_elapsed.avg"]
 for w in want:
     for i, h in enumerate(hdr):
-        if h == w or (w.startswith("sm__pipe_tensor") and "pipe_tensor" in h and "pct" in h and "active" in h):
-            print(f"{h:70s} {vals[i]} {units[i]}")
-            if not w.startswith("sm__pipe_tensor"):
-                break
+        if h == w:
+            print(f"{h:70s} {vals[i][:100]} {units[i]}")
+            break
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 srows = list(csv.reader(io.StringIO(src)))

@@ -1,12 +1,17 @@
-"""c5: activation-sparsity sweep at the 7B-class shape.
+"""c5 (BASELINE configs[4]): activation-sparsity sweep at the
+7B-class shape.
 
 For each target sparsity s: the recipe fwd+bwd step (graph) vs the dense twin
-(timed in interleaved blocks by bench.py, so both see the same clocks),
-the drop fractions (token-wise forward, feature-wise backward for act and
-g_pre) and the sparse TFLOPS. One bench.py process per point (c4 shape,
-32768 tokens, d=4096, h=16384). Writes a JSON list and prints a table.
+(timed by bench.py in interleaved blocks, so both see the same clocks), the
+drop fractions (token-wise forward, feature-wise backward for act and g_pre),
+the sparse TFLOPS, and the tensor-pipe utilisation of every GEMM of the step
+(achieved dense-equivalent TFLOP/s over the measured peak: 2:4 GEMMs against
+twice the dense bf16 peak, from bench.py's per-kernel CUDA-event pass). A
+point whose two arms ran at median SM clocks more than 5% apart is flagged
+"rejected" (its speedup is a clock artefact) and re-run once. One bench.py
+process per point (c4 shape: 32768 tokens, d=4096, h=16384).
 
-usage: python scripts/sweep_c5.py [--out profiles/r01/sweep_c5.json] [--config c4]
+usage: python scripts/sweep_c5.py [--out profiles/r02/sweep_c5.json] [--config c4]
 """
 
 import argparse
@@ -23,26 +28,37 @@ IID_DROP = {0.5: 0.1875, 0.6: 0.128, 0.7: 0.0765, 0.8: 0.036, 0.85: 0.0208, 0.9:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=str(ROOT / "profiles" / "r01" / "sweep_c5.json"))
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r02" / "sweep_c5.json"))
     ap.add_argument("--config", default="c4")
     ap.add_argument("--steps", type=int, default=5)
     args = ap.parse_args()
     rows = []
     for s in LEVELS:
-        cmd = [sys.executable, str(ROOT / "bench.py"), "--config", args.config, "--sparsity", str(s), "--steps",
-               str(args.steps), "--warmup", "3", "--no-e2e", "--no-cpu"]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
-        try:
-            d = json.loads(r.stdout.strip().splitlines()[-1])
-        except (IndexError, ValueError):
-            print(f"s={s}: failed\n{r.stderr[-2000:]}", file=sys.stderr)
+        for attempt in range(2):
+            cmd = [sys.executable, str(ROOT / "bench.py"), "--config", args.config, "--sparsity", str(s), "--steps",
+                   str(args.steps), "--warmup", "3", "--no-e2e", "--no-cpu"]
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+            try:
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+            except (IndexError, ValueError):
+                print(f"s={s}: failed\n{r.stderr[-2000:]}", file=sys.stderr)
+                d = None
+                break
+            mhz, dmhz = d["clocks"].get("sm_mhz") or 0, (d["dense_twin"].get("clocks") or {}).get("sm_mhz") or 0
+            rejected = not (mhz and dmhz) or abs(mhz - dmhz) > 0.05 * max(mhz, dmhz)
+            if not rejected:
+                break
+        if d is None:
             continue
+        tensor = {k["kernel"]: round(k["frac"], 3) for k in d["kernels"] if k["unit"] == "TFLOP/s"}
         row = {"sparsity": s, "ms_per_step": d["ms_per_step"], "dense_ms_per_step": d["dense_twin"]["ms_per_step"],
                "speedup_vs_dense": d["speedup_vs_dense"], "sparse_tflops": d["sparse_tflops"],
                "iid_token_wise_drop": IID_DROP[s], **d["drops"], "clocks": d["clocks"],
-               "dense_clocks": d["dense_twin"].get("clocks"),
+               "dense_clocks": d["dense_twin"].get("clocks"), "clock_mismatch_rejected": rejected,
+               "tensor_pipe_frac_per_gemm": tensor,
                "fp8_ms_per_step": (d.get("fp8_variant") or {}).get("ms_per_step"),
-               "fp8_speedup_vs_dense_bf16": (d.get("fp8_variant") or {}).get("speedup_vs_dense_bf16")}
+               "fp8_speedup_vs_dense_bf16": (d.get("fp8_variant") or {}).get("speedup_vs_dense_bf16"),
+               "fp8_speedup_vs_dense_fp8": (d.get("fp8_variant") or {}).get("speedup_vs_dense_fp8")}
         rows.append(row)
         print(json.dumps(row), flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)

@@ -89,3 +89,29 @@ def test_fwd_gemm1_and_spmm_stay_in_bounds(M):
     _lib.call("s24_spmm", P(vals), P(meta), P(w2), 1, K, M, K, N, P(outt), F32, M, None, 1, -1, None, 64, S())
     torch.cuda.synchronize()
     assert intact(tb)
+
+
+def test_plan_and_masked_sparsify_stay_in_bounds():
+    """K7 (h not a multiple of the 1024 threads) and the masked feature-wise
+    sparsifier (ragged column count) write only their declared outputs."""
+    h, k = 3000, 2850
+    counts = torch.randint(0, 5000, (h,), dtype=torch.int32, device="cuda")
+    sb, sp = guarded(k * 4)
+    db, de = guarded((h - k) * 4)
+    pb, pos = guarded(h * 4)
+    _lib.call("s24_plan", P(counts), h, k, P(sp), P(de), P(pos), S())
+    torch.cuda.synchronize()
+    assert intact(sb) and intact(db) and intact(pb)
+    rows, cols = 256, 200
+    a = torch.randn(rows, cols, device="cuda")
+    m = (torch.rand(rows, cols, device="cuda") < 0.5).to(torch.uint8)
+    cp = (cols + 127) // 128 * 128
+    vb, vals = guarded(cp * (rows // 2) * 2, 0)
+    mb, meta_ref = guarded((rows // 4) * cols * 2)
+    hb, meta_hw = guarded(_lib.meta_hw_bytes(cols, rows), 0x44)
+    kb, keep = guarded(rows * cols)
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.call("s24_sparsify_feature_masked", P(a), F32, rows, cols, cols, P(m), P(vals), P(meta_ref), P(meta_hw),
+              P(keep), P(stats), S())
+    torch.cuda.synchronize()
+    assert intact(vb, 0) and intact(mb) and intact(hb, 0x44) and intact(kb)
