@@ -11,6 +11,7 @@ stream (so it is bit-identical), then cached on the device.
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 
 import numpy as np
 import torch
@@ -81,18 +82,34 @@ def gemm_at(a, b, out_dtype: torch.dtype = F32) -> torch.Tensor:
 
 # ---------------------------------------------------------------- permutations
 
-_perm_cache: dict[tuple[int, int], np.ndarray] = {}
-_dev_cache: dict[tuple[int, int, int], tuple[torch.Tensor, torch.Tensor]] = {}
+_CACHE_ENTRIES = 16  # permutations kept per cache (LRU): distinct token counts are few in practice
+_perm_cache: "OrderedDict[tuple[int, int], np.ndarray]" = OrderedDict()
+_dev_cache: "OrderedDict[tuple[int, int, int], tuple[torch.Tensor, torch.Tensor]]" = OrderedDict()
 _cache_lock = threading.Lock()
+
+
+def _lru_get(cache: OrderedDict, key):
+    with _cache_lock:
+        hit = cache.get(key)
+        if hit is not None:
+            cache.move_to_end(key)
+        return hit
+
+
+def _lru_put(cache: OrderedDict, key, value) -> None:
+    with _cache_lock:
+        cache[key] = value
+        cache.move_to_end(key)
+        while len(cache) > _CACHE_ENTRIES:
+            cache.popitem(last=False)
 
 
 def make_permutation(seed: int, n: int) -> np.ndarray:
     """Fisher-Yates shuffle of [0, n) driven by numpy's PCG64(seed), swapping
     from the top with j = integers(0, i + 1) (ref matcore.py:269-280). Same
-    (seed, n) -> same permutation on every platform; cached per (seed, n)."""
+    (seed, n) -> same permutation on every platform; LRU-cached per (seed, n)."""
     key = (int(seed), int(n))
-    with _cache_lock:
-        hit = _perm_cache.get(key)
+    hit = _lru_get(_perm_cache, key)
     if hit is not None:
         return hit.copy()
     gen = np.random.Generator(np.random.PCG64(seed))
@@ -101,25 +118,22 @@ def make_permutation(seed: int, n: int) -> np.ndarray:
     for i in range(n - 1, 0, -1):
         j = int(draw(0, i + 1))
         perm[i], perm[j] = perm[j], perm[i]
-    with _cache_lock:
-        _perm_cache[key] = perm
+    _lru_put(_perm_cache, key, perm)
     return perm.copy()
 
 
 def device_permutation(seed: int, n: int, device=None) -> tuple[torch.Tensor, torch.Tensor]:
-    """(perm, inverse) as int32 device tensors, cached per (seed, n, device)."""
+    """(perm, inverse) as int32 device tensors, LRU-cached per (seed, n, device)."""
     dev = torch.device(device or "cuda")
     di = dev.index if dev.index is not None else torch.cuda.current_device()
     key = (int(seed), int(n), di)
-    with _cache_lock:
-        hit = _dev_cache.get(key)
+    hit = _lru_get(_dev_cache, key)
     if hit is None:
         p = make_permutation(seed, n)
         inv = np.empty_like(p)
         inv[p] = np.arange(n)
         hit = (torch.from_numpy(p.astype(np.int32)).to(dev), torch.from_numpy(inv.astype(np.int32)).to(dev))
-        with _cache_lock:
-            _dev_cache[key] = hit
+        _lru_put(_dev_cache, key, hit)
     return hit
 
 

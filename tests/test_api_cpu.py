@@ -106,3 +106,16 @@ def test_toy_schedule_and_config_validation():
     assert [k for k, _ in toy.ABLATION_ROWS][:3] == ["dense-swiglu", "dense-relu2", "recipe"]
     mc, tcr = toy.ablation_configs(toy.ToyModelConfig(), toy.TrainConfig(), "no-permute")
     assert tcr.ffn.forward_mode == "sparse24" and not tcr.ffn.permute_tokens
+
+
+def test_permutation_caches_are_bounded():
+    """one cache entry per distinct token count must not grow
+    without bound (LRU of _CACHE_ENTRIES)."""
+    from paper_2503_16672_b200 import matcore as M
+
+    for n in range(4, 4 + 4 * (M._CACHE_ENTRIES + 10), 4):
+        p = M.make_permutation(0, n)
+        assert sorted(p.tolist()) == list(range(n))
+    assert len(M._perm_cache) == M._CACHE_ENTRIES
+    again = M.make_permutation(0, 8)  # evicted long ago: recomputed, same stream
+    assert again.tolist() == M.make_permutation(0, 8).tolist()
