@@ -119,6 +119,11 @@ int s24_meta_ref_to_hw(const uint8_t* meta_ref, int64_t rows, int64_t cols, uint
 int s24_gather_rows(const void* in, int64_t rows, int64_t row_bytes, int64_t ld_in_bytes, const int* src,
                     void* out, int64_t ld_out_bytes, void* stream);
 
+/* diagnostics: one thread writes the GPU's global nanosecond timer to *out
+ * when the stream reaches it (per-kernel timelines inside CUDA graphs,
+ * scripts/timeline.py --graph) */
+int s24_timestamp(unsigned long long* out, void* stream);
+
 /* ---------------------------------------------------------------- split plan
  * Replaces partition_features (splitgemm.py:41-52) on device counts: stable
  * ascending (count, index) order, the first n_sparse features form the sparse

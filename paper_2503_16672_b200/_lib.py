@@ -37,6 +37,7 @@ SIGNATURES: dict[str, list] = {
     "s24_meta_ref_to_hw": [P, I64, I64, P, P],
     "s24_gather_rows": [P, I64, I64, I64, P, P, I64, P],
     "s24_plan": [P, I64, I64, P, P, P, P],
+    "s24_timestamp": [P, P],
     "s24_feature_split_x": [P, P, I64, I64, P, I64, I64, P, P, INT, P, P],
     "s24_feature_split": [P, P, I64, I64, P, I64, I64, P, P, P, P, INT, I64, P],
     "s24_gemm": [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],

@@ -36,12 +36,13 @@ struct K4xSlot {
 // K4X_WARPS warps per CTA (16 features each) at <= 64 registers: several CTAs
 // fit next to a running GEMM CTA, so the split runs on the side stream
 // co-resident with the GEMMs
-#ifndef S24_K4X_EXP
-#define S24_K4X_EXP 0
-#endif
 #ifndef S24_K4X_WARPS
 #define S24_K4X_WARPS 4
 #endif
+#ifndef S24_K4X_TB
+#define S24_K4X_TB 1
+#endif
+constexpr int K4X_TB = S24_K4X_TB;
 constexpr int K4X_WARPS = S24_K4X_WARPS;
 template <bool NONNEG>
 __global__ void __launch_bounds__(32 * K4X_WARPS, 32 / K4X_WARPS) k_feature_split_x(K4xArgs a) {
@@ -50,30 +51,33 @@ __global__ void __launch_bounds__(32 * K4X_WARPS, 32 / K4X_WARPS) k_feature_spli
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = a.n, h = a.h;
   const bool keys = !NONNEG || (a.nan_flag != nullptr && __ldg(a.nan_flag) != 0ull);
-  // blocks of K4X_WARPS x 16 features x 128 tokens, feature block fastest;
-  // a grid smaller than the block count strides over them
-  const int fblocks = h / (16 * K4X_WARPS), blocks = fblocks * (n / 128);
-  for (int b = blockIdx.x; b < blocks; b += gridDim.x) {
-    const int fb = b % fblocks, tb = b / fblocks;
-    __syncwarp();  // (the previous block's slot reads are done)
-    const int t0 = tb * 128, fbase = fb * (16 * K4X_WARPS) + warp * 16;
-    const uint32_t nw = static_cast<uint32_t>(n / 4);
-    if (lane < 16) {
-      const int pos = __ldg(a.feat_pos + fbase + lane);
-      const uint32_t row = pos >= 0 ? static_cast<uint32_t>(a.pair_rows + pos) : 2u * static_cast<uint32_t>(-pos - 1);
-      K4xSlot s;
-      s.ofs = row * nw + static_cast<uint32_t>(t0 / 4);
-      s.mb = static_cast<uint32_t>(meta_hw_halfword_offset(row, t0 / 16, n));
-      s.mb2 = static_cast<uint32_t>(meta_hw_halfword_offset(row + 1, t0 / 16, n));
-      s.dense = pos < 0 ? 1u : 0u;
-      slots[warp][lane] = s;
-    }
-    __syncwarp();
+  // CTA = K4X_WARPS x 16 features (blockIdx.x) x K4X_TB consecutive 128-token
+  // blocks (blockIdx.y): the per-feature output slots are computed once and
+  // advanced by one metadata atom / 32 value words per token block
+  const int fbase = blockIdx.x * (16 * K4X_WARPS) + warp * 16;
+  const int tblocks = n / 128;
+  const uint32_t nw = static_cast<uint32_t>(n / 4);
+  if (lane < 16) {
+    const int pos = __ldg(a.feat_pos + fbase + lane);
+    const uint32_t row = pos >= 0 ? static_cast<uint32_t>(a.pair_rows + pos) : 2u * static_cast<uint32_t>(-pos - 1);
+    const int t0 = blockIdx.y * K4X_TB * 128;
+    K4xSlot s;
+    s.ofs = row * nw + static_cast<uint32_t>(t0 / 4);
+    s.mb = static_cast<uint32_t>(meta_hw_halfword_offset(row, t0 / 16, n));
+    s.mb2 = static_cast<uint32_t>(meta_hw_halfword_offset(row + 1, t0 / 16, n));
+    s.dense = pos < 0 ? 1u : 0u;
+    slots[warp][lane] = s;
+  }
+  __syncwarp();
+  for (int bi = 0; bi < K4X_TB; ++bi) {
+    const int tb = blockIdx.y * K4X_TB + bi;
+    if (tb >= tblocks) break;
+    const int t0 = tb * 128;
+    const uint32_t dofs = 32u * bi, dmb = 2048u * bi;  // (slot offsets of token block bi)
     const int t = t0 + 4 * lane;
     const uint32_t qd = static_cast<uint32_t>(lane) >> 2;
     const uint32_t q_off = 4u * (qd >> 1) + 128u * (qd & 1u);
 
-    uint32_t exp_acc = 0;  // (experiment 1 only)
     // load + expand: X[token][feature pair] packed bf16x2
     uint32_t X[4][8];
   #pragma unroll
@@ -91,21 +95,16 @@ __global__ void __launch_bounds__(32 * K4X_WARPS, 32 / K4X_WARPS) k_feature_spli
 
   #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const K4xSlot s0 = slots[warp][2 * k], s1 = slots[warp][2 * k + 1];
+      K4xSlot s0 = slots[warp][2 * k], s1 = slots[warp][2 * k + 1];
+      s0.ofs += dofs;
+      s1.ofs += dofs;
+      s0.mb += dmb;
+      s1.mb += dmb;
+      s0.mb2 += dmb;
+      s1.mb2 += dmb;
       const uint32_t x0 = X[0][k], x1 = X[1][k], x2 = X[2][k], x3 = X[3][k];
       uint32_t* vs32 = reinterpret_cast<uint32_t*>(a.vs);
       uint8_t* es = a.es;
-#if S24_K4X_EXP == 2
-      if (true) {
-        const uint32_t v0 = x0 ^ x2, v1 = x1 ^ x3, hw = x0;
-        vs32[s0.ofs + lane] = __byte_perm(v0, v1, 0x5410);
-        if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + s0.mb + q_off) = static_cast<uint16_t>(hw);
-        vs32[s1.ofs + lane] = __byte_perm(v0, v1, 0x7632);
-        if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + s1.mb + q_off) = static_cast<uint16_t>(hw >> 16);
-        continue;
-      }
-#endif
-      const bool st_ok = S24_K4X_EXP != 1 || n < 0;  // (experiment 1: compute, no stores)
       if (!(s0.dense & s1.dense)) {
         uint32_t k0 = x0, k1 = x1, k2 = x2, k3 = x3;
         if (keys) {
@@ -125,18 +124,17 @@ __global__ void __launch_bounds__(32 * K4X_WARPS, 32 / K4X_WARPS) k_feature_spli
         uint32_t hw = nib << (4 * (lane & 3));
         hw |= __shfl_xor_sync(0xffffffffu, hw, 1);
         hw |= __shfl_xor_sync(0xffffffffu, hw, 2);
-        if (S24_K4X_EXP == 1) exp_acc ^= v0 ^ (v1 * 3u) ^ hw;
-        if (!s0.dense && st_ok) {
+        if (!s0.dense) {
           vs32[s0.ofs + lane] = __byte_perm(v0, v1, 0x5410);
           if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + s0.mb + q_off) = static_cast<uint16_t>(hw);
         }
-        if (!s1.dense && st_ok) {
+        if (!s1.dense) {
           vs32[s1.ofs + lane] = __byte_perm(v0, v1, 0x7632);
           if ((lane & 3) == 0) *reinterpret_cast<uint16_t*>(es + s1.mb + q_off) = static_cast<uint16_t>(hw >> 16);
         }
       }
       // paired dense features: (x0, x1) | selector 0x4, (x2, x3) | 0xE
-      if (s0.dense && st_ok) {
+      if (s0.dense) {
         vs32[s0.ofs + lane] = __byte_perm(x0, x1, 0x5410);
         vs32[s0.ofs + nw + lane] = __byte_perm(x2, x3, 0x5410);
         if ((lane & 3) == 0) {
@@ -144,7 +142,7 @@ __global__ void __launch_bounds__(32 * K4X_WARPS, 32 / K4X_WARPS) k_feature_spli
           *reinterpret_cast<uint16_t*>(es + s0.mb2 + q_off) = 0xEEEE;
         }
       }
-      if (s1.dense && st_ok) {
+      if (s1.dense) {
         vs32[s1.ofs + lane] = __byte_perm(x0, x1, 0x7632);
         vs32[s1.ofs + nw + lane] = __byte_perm(x2, x3, 0x7632);
         if ((lane & 3) == 0) {

@@ -485,6 +485,12 @@ int k4_prepare(const void* vals, const uint8_t* meta_hw, int64_t n, int64_t h, c
   return S24_OK;
 }
 
+__global__ void k_timestamp(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
 }  // namespace s24
 
 using namespace s24;
@@ -653,6 +659,12 @@ int s24_gather_rows(const void* in, int64_t rows, int64_t row_bytes, int64_t ld_
   return check_launch("k_gather_rows");
 }
 
+int s24_timestamp(unsigned long long* out, void* stream) {
+  if (!out) return fail(S24_ERR_DIMENSION, "null output");
+  k_timestamp<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out);
+  return check_launch("k_timestamp");
+}
+
 int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, int* dense_idx, int* feat_pos,
              void* stream) {
   if (h < 0 || h > 65536) return fail(S24_ERR_DIMENSION, "plan supports 0 <= h <= 65536");
@@ -678,13 +690,8 @@ int s24_feature_split_x(const void* vals, const uint8_t* meta_hw, int64_t n, int
   if (n == 0 || h == 0) return S24_OK;
   K4xArgs a{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
             static_cast<int>(2 * n_dense), static_cast<__nv_bfloat16*>(vs), es, nan_flag};
-  long long grid = (h / (16 * K4X_WARPS)) * (n / 128);
-#ifdef S24_K4X_CTAS_PER_SM
-  if (S24_K4X_CTAS_PER_SM > 0 && grid > static_cast<long long>(num_sms()) * S24_K4X_CTAS_PER_SM)
-    grid = static_cast<long long>(num_sms()) * S24_K4X_CTAS_PER_SM;
-#endif
-  (operand_nonneg ? k_feature_split_x<true> : k_feature_split_x<false>)<<<static_cast<unsigned>(grid), 32 * K4X_WARPS, 0,
-                                                                         st>>>(a);
+  const dim3 grid(static_cast<unsigned>(h / (16 * K4X_WARPS)), static_cast<unsigned>((n / 128 + K4X_TB - 1) / K4X_TB));
+  (operand_nonneg ? k_feature_split_x<true> : k_feature_split_x<false>)<<<grid, 32 * K4X_WARPS, 0, st>>>(a);
   return check_launch("k_feature_split_x");
 }
 

@@ -525,6 +525,9 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
             run_feature_split(act_split, act_vals, act_meta, npad, h, bplan, nonneg=True, nan_flag=stats_dev[2:])
         ev = torch.cuda.Event()
         ev.record(side)
+    if not for_backward:
+        main.wait_event(ev)  # (inference: no backward will join the side stream)
+        ev = None
     if x_in is None and for_backward:
         x_in = x
     cache = FfnCache(n, cfg, census, _x_in=x_in, act_vals=act_vals, act_meta=act_meta, pre_act=pre,

@@ -3,7 +3,11 @@ recorded around every libs24 call on the stream it is launched on, offsets
 from one start event). Shows which side-stream kernels overlap which
 main-stream GEMMs and how long each takes while co-running.
 
-usage: python scripts/timeline.py [--n 16384 --d 2048 --h 8192] [--steps 3]
+usage: python scripts/timeline.py [--n 16384 --d 2048 --h 8192] [--steps 3] [--graph]
+
+--graph: the step is captured as a CUDA graph with a one-thread timestamp
+kernel (s24_timestamp, %globaltimer) before and after every libs24 launch on
+its stream, and replayed; the stamps add ~1-2 us each.
 """
 
 import argparse
@@ -35,18 +39,72 @@ class Timeline:
         self.recs.append((nm, "main" if st == self.main else "side", s, e))
 
 
+class Stamps:
+    """tracer that brackets every launch with s24_timestamp kernels"""
+
+    def __init__(self, slots: int = 256):
+        self.buf = torch.zeros(slots, dtype=torch.int64, device="cuda")
+        self.recs = []
+        self.main = torch.cuda.current_stream()
+        self.i = 0
+
+    def _stamp(self):
+        st = torch.cuda.current_stream()
+        _lib.load().s24_timestamp(self.buf.data_ptr() + 8 * self.i, st.cuda_stream)
+        self.i += 1
+        return self.i - 1
+
+    def before(self, name, args):
+        self._open = (name, self._stamp(), torch.cuda.current_stream())
+
+    def after(self, name):
+        nm, a, st = self._open
+        self.recs.append((nm, "main" if st == self.main else "side", a, self._stamp()))
+
+
+def graph_timeline(args, p, x, dy):
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap):
+        for _ in range(2):
+            out, cache = s24.ffn_forward(x, p, s24.RECIPE)
+            s24.ffn_backward(dy, cache, p, s24.RECIPE)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        st = Stamps()
+        _lib.set_tracer(st)
+        out, cache = s24.ffn_forward(x, p, s24.RECIPE)
+        gr = s24.ffn_backward(dy, cache, p, s24.RECIPE)
+        _lib.set_tracer(None)
+    for step in range(args.steps):
+        flush.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        t = st.buf.cpu().tolist()
+        t0 = min(t[a] for _, _, a, _ in st.recs)
+        t1 = max(t[b] for _, _, _, b in st.recs)
+        print(f"--- graph replay {step}: {(t1 - t0) / 1e3:.0f} us from the first stamp to the last")
+        for nm, side, a, b in st.recs:
+            print(f"  {side:4s} {nm:24s} {(t[a] - t0) / 1e3:8.1f} -> {(t[b] - t0) / 1e3:8.1f}  ({(t[b] - t[a]) / 1e3:7.1f} us)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--d", type=int, default=2048)
     ap.add_argument("--h", type=int, default=8192)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--graph", action="store_true")
     args = ap.parse_args()
     import bench  # noqa: E402
 
     x, w1, w2, dy = bench.synthetic_device_inputs(torch, args.n, args.d, args.h, seed=1234,
                                                   device=torch.device("cuda"))
     p = s24.FfnParams(w1=w1, w2=w2)
+    if args.graph:
+        return graph_timeline(args, p, x, dy)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(3):
         out, cache = s24.ffn_forward(x, p, s24.RECIPE)

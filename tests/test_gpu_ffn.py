@@ -391,3 +391,23 @@ def test_minimum_and_degenerate_shapes(fp8):
                           (g.d_w2, o_g["d_w2"])):
             got = got.cpu().numpy().astype(np.float64)
             assert np.linalg.norm(got - want) <= tol * max(np.linalg.norm(want), 1e-30)
+
+
+@pytest.mark.parametrize("fp8", [False, True])
+def test_prefill_graph_capture(fp8):
+    """The inference forward (for_backward=False) joins its side-stream work
+    (plan) before returning, so it captures as a CUDA graph (the c3 prefill
+    bench) and replays to the eager output, bit for bit."""
+    from dataclasses import replace
+
+    n, d, h = 640, 256, 512
+    x, w1, w2, _ = O.synthetic_ffn_inputs(n, d, h, sparsity=0.9, seed=82)
+    p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
+    cfg = replace(s24.RECIPE, fp8_emulation=fp8)
+    tx = torch.from_numpy(x).cuda().bfloat16()
+    want, _ = s24.ffn_forward(tx, p, cfg, for_backward=False)
+    step = s24.FfnStepGraph(p, cfg, n, backward=False)
+    step.x.copy_(tx)
+    step.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(step.out, want)
