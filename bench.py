@@ -696,6 +696,24 @@ def run_ours(args):
     result["kernels"] = kernels
     result["gpu_launches"] = tracer.launches // args.steps * args.steps
     result["clocks"] = clk
+    # NVML's samples (every 2 ms) report the clock target, not what the SMs
+    # run at inside a power-limited GEMM: a separate, untimed pass replays
+    # the recipe step while one-warp probe CTAs on another stream compare
+    # %clock64 with %globaltimer over 20 us (scripts/clock_probe.py)
+    try:
+        probe = torch.zeros(16, dtype=torch.int64, device=dev)
+        side = torch.cuda.Stream(device=dev)
+        seen = []
+        for _ in range(6):
+            run_step(recipe)
+            _lib.call("s24_clock_probe", probe.data_ptr(), 8, 20000, side.cuda_stream)
+            run_step(recipe)
+            torch.cuda.synchronize()
+            v = probe.view(8, 2).tolist()
+            seen.append(statistics.median(c / t * 1e3 for c, t in v))
+        result["clocks"]["sm_mhz_in_step_probe"] = round(statistics.median(seen))
+    except Exception as e:  # diagnostics only
+        result["clocks"]["sm_mhz_in_step_probe"] = f"unavailable: {e}"
 
     # end-to-end through the public API with host buffers
     if not args.no_e2e:

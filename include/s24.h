@@ -123,6 +123,10 @@ int s24_gather_rows(const void* in, int64_t rows, int64_t row_bytes, int64_t ld_
  * when the stream reaches it (per-kernel timelines inside CUDA graphs,
  * scripts/timeline.py --graph) */
 int s24_timestamp(unsigned long long* out, void* stream);
+/* diagnostics: `ctas` one-warp CTAs busy-wait `ns` nanoseconds and write
+ * (SM clock cycles, nanoseconds) pairs to out[2*ctas]: the SM clock while
+ * other work runs (scripts/clock_probe.py) */
+int s24_clock_probe(unsigned long long* out, int ctas, int64_t ns, void* stream);
 
 /* ---------------------------------------------------------------- split plan
  * Replaces partition_features (splitgemm.py:41-52) on device counts: stable

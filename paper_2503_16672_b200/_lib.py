@@ -38,6 +38,7 @@ SIGNATURES: dict[str, list] = {
     "s24_gather_rows": [P, I64, I64, I64, P, P, I64, P],
     "s24_plan": [P, I64, I64, P, P, P, P],
     "s24_timestamp": [P, P],
+    "s24_clock_probe": [P, INT, I64, P],
     "s24_feature_split_x": [P, P, I64, I64, P, I64, I64, P, P, INT, P, P],
     "s24_feature_split": [P, P, I64, I64, P, I64, I64, P, P, P, P, INT, I64, P],
     "s24_gemm": [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, INT, I64, P, P],

@@ -491,6 +491,22 @@ __global__ void k_timestamp(unsigned long long* out) {
   *out = t;
 }
 
+// diagnostics: SM clock over a busy-wait of `ns` nanoseconds, one record
+// (clock64 delta, globaltimer delta) per CTA
+__global__ void k_clock_probe(unsigned long long* out, unsigned long long ns) {
+  unsigned long long c0, g0, c1, g1;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  } while (g1 - g0 < ns);
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1));
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = c1 - c0;
+    out[2 * blockIdx.x + 1] = g1 - g0;
+  }
+}
+
 }  // namespace s24
 
 using namespace s24;
@@ -663,6 +679,12 @@ int s24_timestamp(unsigned long long* out, void* stream) {
   if (!out) return fail(S24_ERR_DIMENSION, "null output");
   k_timestamp<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out);
   return check_launch("k_timestamp");
+}
+
+int s24_clock_probe(unsigned long long* out, int ctas, int64_t ns, void* stream) {
+  if (!out || ctas < 1) return fail(S24_ERR_DIMENSION, "bad probe arguments");
+  k_clock_probe<<<ctas, 32, 0, static_cast<cudaStream_t>(stream)>>>(out, static_cast<unsigned long long>(ns));
+  return check_launch("k_clock_probe");
 }
 
 int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, int* dense_idx, int* feat_pos,
