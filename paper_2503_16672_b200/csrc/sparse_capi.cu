@@ -86,6 +86,73 @@ __global__ void k_sparsify_token(const T* __restrict__ a, long long rows, long l
   }
 }
 
+// Fast path of the above for the operand the GEMMs consume (values + hw
+// metadata only): one thread per 16-column chunk, 16-byte vector loads and a
+// single 16-byte value store; needs cols % 16 == 0 and 16-byte aligned rows.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sparsify_token_hw(const T* __restrict__ a, long long rows, long long cols,
+                                                           long long lda, __nv_bfloat16* __restrict__ vals,
+                                                           uint8_t* __restrict__ meta_hw, unsigned long long* stats) {
+  constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte load
+  constexpr int NV = 16 / VEC;         // 16-byte loads per chunk
+  constexpr int U = 2;                 // chunks per thread per iteration (their loads in flight together)
+  const long long chunks_per_row = cols / 16;
+  const long long total = rows * chunks_per_row;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long nb = 0, na = 0;
+  for (long long w0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; w0 < total; w0 += U * stride) {
+    uint4 u[U][NV];
+#pragma unroll
+    for (int c = 0; c < U; ++c) {
+      const long long w = w0 + c * stride;
+      if (w < total) {
+        const long long r = w / chunks_per_row, q = w - r * chunks_per_row;
+        const uint4* src = reinterpret_cast<const uint4*>(a + r * lda + q * 16);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) u[c][v] = __ldcs(src + v);  // (streamed: read once)
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < U; ++c) {
+      const long long w = w0 + c * stride;
+      if (w >= total) break;
+      const long long r = w / chunks_per_row, q = w - r * chunks_per_row;
+      float x[16];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint32_t wv[4] = {u[c][v].x, u[c][v].y, u[c][v].z, u[c][v].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if constexpr (sizeof(T) == 4) {
+            x[v * 4 + i] = __uint_as_float(wv[i]);
+          } else {
+            x[v * 8 + 2 * i] = __uint_as_float(wv[i] << 16);
+            x[v * 8 + 2 * i + 1] = __uint_as_float(wv[i] & 0xFFFF0000u);
+          }
+        }
+      }
+      uint32_t packed[4];
+      uint32_t m16 = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const float x0 = x[4 * g], x1 = x[4 * g + 1], x2 = x[4 * g + 2], x3 = x[4 * g + 3];
+        nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
+        const uint32_t nib = keep_to_nibble(top2_keep_mask(x0, x1, x2, x3));
+        const float v0 = sel4(x0, x1, x2, x3, nib & 3u), v1 = sel4(x0, x1, x2, x3, nib >> 2);
+        na += (v0 != 0.f) + (v1 != 0.f);
+        packed[g] = pack_bf16x2(v0, v1);
+        m16 |= nib << (4 * g);
+      }
+      *reinterpret_cast<uint4*>(vals + r * (cols / 2) + q * 8) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      *reinterpret_cast<uint16_t*>(meta_hw + meta_hw_halfword_offset(r, q, cols)) = static_cast<uint16_t>(m16);
+    }
+  }
+  if (stats) {
+    block_sum_u64_to(nb, stats);
+    block_sum_u64_to(na, stats + 1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // feature-wise sparsify: thread owns GPT consecutive row-groups of column j.
 // fwd_mask (nullable, uint8 [rows, cols]): entries outside it read as zero
@@ -526,6 +593,16 @@ int s24_sparsify_token(const void* a, int dtype, int64_t rows, int64_t cols, int
   const bool q = cols % 16 == 0;
   const long long work = rows * cols / (q ? 16 : 4);
   const int g = grid_for(work, 256);
+  const int esz = dtype == S24_F32 ? 4 : 2;
+  if (meta_hw && !meta_ref && !mask && aligned16(a) && aligned16(vals) && (lda * esz) % 16 == 0) {
+    if (dtype == S24_F32)
+      k_sparsify_token_hw<float><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
+                                                    static_cast<__nv_bfloat16*>(vals), meta_hw, stats);
+    else
+      k_sparsify_token_hw<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
+                                                            static_cast<__nv_bfloat16*>(vals), meta_hw, stats);
+    return check_launch("k_sparsify_token_hw");
+  }
   if (dtype == S24_F32) {
     if (q)
       k_sparsify_token<float, 4><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,

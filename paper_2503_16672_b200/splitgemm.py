@@ -198,9 +198,6 @@ def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tenso
     """Fill preallocated K4 outputs on the current stream (no drop counting).
     nan_flag: K1's "a kept value is NaN" word; with nonneg it switches K4 back
     to NaN-aware ranking."""
-    import os
-    if os.environ.get("S24_EXP_SKIP_K4") == "1":
-        return
     _lib.call("s24_feature_split_x", ptr(vals), ptr(meta_hw), n, h, ptr(plan.feat_pos), plan.n_sparse,
               plan.n_dense, ptr(fs.vs), ptr(fs.es), int(nonneg), ptr(nan_flag), stream())
 

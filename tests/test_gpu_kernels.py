@@ -412,3 +412,25 @@ def test_feature_split_x_matches_reference_kernel(nan):
         _lib.call("s24_feature_split_x", P(v), P(meta_hw), n, h, P(tpos), ks, nd, P(gv_), P(ge), nn, P(flag), S())
         assert torch.equal(re_, ge)
         assert torch.equal(rv.view(torch.int16), gv_.view(torch.int16))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_sparsify_token_hw_fast_path_bitwise(dtype):
+    """s24_sparsify_token with only values + hw metadata requested takes the
+    vectorized one-chunk-per-thread kernel: bit-identical to the general
+    kernel (which also writes the reference metadata and the mask), NaN / Inf
+    included."""
+    rows, cols = 384, 1024
+    a = torch.randn(rows, cols, device="cuda") * (torch.rand(rows, cols, device="cuda") < 0.4)
+    a[torch.rand(rows, cols, device="cuda") < 0.01] = float("nan")
+    a[torch.rand(rows, cols, device="cuda") < 0.005] = float("inf")
+    a = a.to(dtype)
+    v0, _, m0, _, s0 = gpu_sparsify_token(a)
+    v1 = torch.zeros_like(v0)
+    m1 = torch.full_like(m0, 0x44)
+    s1 = torch.zeros(2, dtype=torch.int64, device="cuda")
+    dt = F32 if dtype == torch.float32 else BF16
+    _lib.call("s24_sparsify_token", P(a), dt, rows, cols, cols, P(v1), None, P(m1), None, P(s1), S())
+    torch.cuda.synchronize()
+    assert torch.equal(v0.view(torch.int16), v1.view(torch.int16))
+    assert torch.equal(m0, m1) and torch.equal(s0, s1)
