@@ -1,5 +1,5 @@
 """Run one c2-shaped GEMM of the step repeatedly (for ncu captures):
-usage: python scripts/gemm_probe.py {k1|k3|fwdout|dx|dw|dense|k4|gather|plan} [--iters 5]
+usage: python scripts/gemm_probe.py {k1|k3|relu2|dact|fwdout|dx|dw|dense|k4|gather|plan} [--iters 5]
 ncu: the step that builds the operands launches 6 gemm_kernel, 2 k_feature_split_x, 2 k_gather_rows and
 1 k_plan first (skip them with -s)."""
 import argparse
@@ -29,6 +29,9 @@ P = lambda t: t.data_ptr()  # noqa: E731
 o = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
 dw = torch.empty(h, d, device="cuda")
 gv = torch.empty_like(cache.act_vals)
+if args.which in ("relu2", "dact"):  # dense twin operands: act / g_pre [n, h]
+    gv = torch.randn(n, h, device="cuda").bfloat16().relu_()
+    gv2 = torch.empty_like(gv)
 stats = torch.zeros(3, dtype=torch.int64, device="cuda")
 cnt = torch.zeros(h, dtype=torch.int32, device="cuda")
 av = torch.empty_like(cache.act_vals)
@@ -44,6 +47,8 @@ calls = {
                             None, 0, -1, None, 0, S),
     "dw": lambda: _lib.call("s24_spmm", P(fa.vs), P(fa.es), P(dy), 1, d, fa.rows(plan), d, n, P(dw), 0, d,
                             P(plan.paired_row_map), 0, fa.rows(plan), None, fa.pair_rows, S),
+    "relu2": lambda: _lib.call("s24_gemm_relu2", P(x), d, P(w1), h, n, h, d, P(gv), h, S),
+    "dact": lambda: _lib.call("s24_gemm_dact", P(dy), d, P(w2), d, n, h, d, P(gv), h, P(gv2), h, S),
     "dense": lambda: _lib.call("s24_gemm", P(x), 0, d, P(w1), 1, h, n, h, d, P(gv), 1, h, None, 0, -1, None, S),
     "k4": lambda: _lib.call("s24_feature_split_x", P(cache.act_vals), P(cache.act_meta), n, h, P(plan.feat_pos),
                             plan.n_sparse, plan.n_dense, P(fa.vs), P(fa.es), 1, None, S),

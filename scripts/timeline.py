@@ -3,11 +3,13 @@ recorded around every libs24 call on the stream it is launched on, offsets
 from one start event). Shows which side-stream kernels overlap which
 main-stream GEMMs and how long each takes while co-running.
 
-usage: python scripts/timeline.py [--n 16384 --d 2048 --h 8192] [--steps 3] [--graph]
+usage: python scripts/timeline.py [--n 16384 --d 2048 --h 8192] [--steps 3] [--queued]
 
---graph: the step is captured as a CUDA graph with a one-thread timestamp
+--queued: a one-CTA busy-wait kernel (s24_clock_probe, 20 ms) holds the GPU
+while the whole eager step is queued behind it, with a one-thread timestamp
 kernel (s24_timestamp, %globaltimer) before and after every libs24 launch on
-its stream, and replayed; the stamps add ~1-2 us each.
+its stream; the GPU then runs the step back to back as a graph replay would
+(no host gaps). The stamps add ~1-2 us each.
 """
 
 import argparse
@@ -48,44 +50,44 @@ class Stamps:
         self.main = torch.cuda.current_stream()
         self.i = 0
 
-    def _stamp(self):
-        st = torch.cuda.current_stream()
-        _lib.load().s24_timestamp(self.buf.data_ptr() + 8 * self.i, st.cuda_stream)
+    def _stamp(self, handle):
+        _lib.load().s24_timestamp(self.buf.data_ptr() + 8 * self.i, handle)
         self.i += 1
         return self.i - 1
 
     def before(self, name, args):
-        self._open = (name, self._stamp(), torch.cuda.current_stream())
+        # every libs24 entry point takes its stream last
+        handle = args[-1] if isinstance(args[-1], int) else torch.cuda.current_stream().cuda_stream
+        self._open = (name, self._stamp(handle), handle)
 
     def after(self, name):
-        nm, a, st = self._open
-        self.recs.append((nm, "main" if st == self.main else "side", a, self._stamp()))
+        nm, a, handle = self._open
+        self.recs.append((nm, "main" if handle == self.main.cuda_stream else "side", a, self._stamp(handle)))
 
 
-def graph_timeline(args, p, x, dy):
+def queued_timeline(args, p, x, dy):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    cap = torch.cuda.Stream()
-    cap.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(cap):
-        for _ in range(2):
-            out, cache = s24.ffn_forward(x, p, s24.RECIPE)
-            s24.ffn_backward(dy, cache, p, s24.RECIPE)
+    probe = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        out, cache = s24.ffn_forward(x, p, s24.RECIPE)
+        s24.ffn_backward(dy, cache, p, s24.RECIPE)
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    for step in range(args.steps):
+        flush.zero_()
         st = Stamps()
+        torch.cuda.synchronize()
+        main = torch.cuda.current_stream().cuda_stream
+        _lib.call("s24_clock_probe", probe.data_ptr(), 1, 20_000_000, main)  # hold the GPU while we queue
         _lib.set_tracer(st)
         out, cache = s24.ffn_forward(x, p, s24.RECIPE)
         gr = s24.ffn_backward(dy, cache, p, s24.RECIPE)
         _lib.set_tracer(None)
-    for step in range(args.steps):
-        flush.zero_()
-        g.replay()
+        del cache, gr
         torch.cuda.synchronize()
         t = st.buf.cpu().tolist()
         t0 = min(t[a] for _, _, a, _ in st.recs)
         t1 = max(t[b] for _, _, _, b in st.recs)
-        print(f"--- graph replay {step}: {(t1 - t0) / 1e3:.0f} us from the first stamp to the last")
+        print(f"--- queued step {step}: {(t1 - t0) / 1e3:.0f} us from the first stamp to the last")
         for nm, side, a, b in st.recs:
             print(f"  {side:4s} {nm:24s} {(t[a] - t0) / 1e3:8.1f} -> {(t[b] - t0) / 1e3:8.1f}  ({(t[b] - t[a]) / 1e3:7.1f} us)")
 
@@ -96,15 +98,15 @@ def main():
     ap.add_argument("--d", type=int, default=2048)
     ap.add_argument("--h", type=int, default=8192)
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--queued", action="store_true")
     args = ap.parse_args()
     import bench  # noqa: E402
 
     x, w1, w2, dy = bench.synthetic_device_inputs(torch, args.n, args.d, args.h, seed=1234,
                                                   device=torch.device("cuda"))
     p = s24.FfnParams(w1=w1, w2=w2)
-    if args.graph:
-        return graph_timeline(args, p, x, dy)
+    if args.queued:
+        return queued_timeline(args, p, x, dy)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(3):
         out, cache = s24.ffn_forward(x, p, s24.RECIPE)
