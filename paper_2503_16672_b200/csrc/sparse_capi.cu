@@ -359,11 +359,6 @@ __global__ void k_gather_rows(const uint8_t* __restrict__ in, long long rows, lo
 }
 
 // ---------------------------------------------------------------------------
-// K7: split plan. One CTA of 1024 threads. Key of feature j = (count_j << 16)
-// | j (unique, orders by (count, index) exactly like the stable argsort in
-// splitgemm.py:49). An 8-bit MSB radix select finds the key of rank
-// n_sparse-1; features with key <= it are sparse. A block scan then emits the
-// ascending index lists (splitgemm.py:50-51) and the per-feature positions.
 // K7: partition_features (ref splitgemm.py:41-52) on the device. Stable
 // ascending order of (count, index): the n_sparse smallest keys are sparse.
 // Radix select on the count value (11-bit digits over the significant bits,
@@ -396,27 +391,33 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* warp_tot, int la
   return warp_tot[wid] + inc - v;
 }
 
-__global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts_g, int h, int n_sparse,
+// Each thread owns PER consecutive features (j0 = tid * PER) and keeps their
+// counts in registers, so the counts are read from memory once: the passes
+// below (max, two radix digits, tie-break, lists) only touch registers and the
+// 8 KB of shared memory (histogram, scan totals).
+template <int PER>
+__global__ void __launch_bounds__(1024, 2) k_plan(const int* __restrict__ counts_g, int h, int n_sparse,
                                                int* __restrict__ sparse_idx, int* __restrict__ dense_idx,
-                                               int* __restrict__ feat_pos, int counts_in_smem) {
+                                               int* __restrict__ feat_pos) {
   constexpr int DIGIT = 11, BINS = 1 << DIGIT;
-  // the counts are read six times: staged in shared memory first (one
-  // coalesced pass) when they fit, so the passes do not wait on L2 / DRAM
-  // latency chains
-  extern __shared__ int s_counts[];
-  const int* __restrict__ counts = counts_g;
-  if (counts_in_smem) {
-    for (int j = threadIdx.x; j < h; j += 1024) s_counts[j] = __ldg(counts_g + j);
-    __syncthreads();
-    counts = s_counts;
-  }
   __shared__ unsigned hist[BINS];
   __shared__ int warp_tot[33];
   __shared__ unsigned sh_max, sh_prefix;
   __shared__ int sh_rank, sh_jstar;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (h + 1023) / 1024;
-  const int j0 = min(h, tid * per), j1 = min(h, j0 + per);
+  const int j0 = tid * PER;
+  unsigned c[PER];
+  if (j0 + PER <= h && (h & 3) == 0 && PER % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < PER; i += 4) {
+      const int4 v = __ldg(reinterpret_cast<const int4*>(counts_g + j0 + i));
+      c[i] = v.x, c[i + 1] = v.y, c[i + 2] = v.z, c[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) c[i] = j0 + i < h ? static_cast<unsigned>(__ldg(counts_g + j0 + i)) : 0u;
+  }
+  auto valid = [&](int i) { return j0 + i < h; };
 
   unsigned cstar = 0xFFFFFFFFu;  // threshold count; features with count < cstar are sparse
   int jstar = -1;                // ... and those with count == cstar up to index jstar
@@ -426,10 +427,11 @@ __global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts_g,
       sh_prefix = 0;
       sh_rank = n_sparse - 1;
     }
-    __syncthreads();
     unsigned mx = 0;
-    for (int j = j0; j < j1; ++j) mx = max(mx, static_cast<unsigned>(counts[j]));
+#pragma unroll
+    for (int i = 0; i < PER; ++i) mx = max(mx, valid(i) ? c[i] : 0u);
     mx = __reduce_max_sync(0xffffffffu, mx);
+    __syncthreads();
     if (lane == 0) atomicMax(&sh_max, mx);
     __syncthreads();
     const int bits = 32 - __clz(static_cast<int>(sh_max | 1u));
@@ -439,13 +441,10 @@ __global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts_g,
       for (int b = tid; b < BINS; b += 1024) hist[b] = 0;
       __syncthreads();
       const unsigned prefix = sh_prefix;  // the bits above `hi` of the threshold
-      for (int i = 0; i < per; ++i) {
-        const int j = j0 + i;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
         unsigned bin = 0xFFFFFFFFu;
-        if (j < j1) {
-          const unsigned c = static_cast<unsigned>(counts[j]);
-          if ((hi >= 32 ? 0u : (c >> hi)) == prefix) bin = (c >> shift) & ((1u << width) - 1u);
-        }
+        if (valid(i) && (hi >= 32 ? 0u : (c[i] >> hi)) == prefix) bin = (c[i] >> shift) & ((1u << width) - 1u);
         const unsigned peers = __match_any_sync(0xffffffffu, bin);
         if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
       }
@@ -467,31 +466,34 @@ __global__ void __launch_bounds__(1024) k_plan(const int* __restrict__ counts_g,
     cstar = sh_prefix;
     // tie-break: the (sh_rank)-th feature (by index) with count == cstar
     int my_eq = 0;
-    for (int j = j0; j < j1; ++j) my_eq += static_cast<unsigned>(counts[j]) == cstar ? 1 : 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) my_eq += valid(i) && c[i] == cstar ? 1 : 0;
     int total;
     const int exc = block_excl_scan_1024(my_eq, warp_tot, lane, wid, total);
     const int r = sh_rank;
     if (r >= exc && r < exc + my_eq) {
       int seen = exc;
-      for (int j = j0; j < j1; ++j)
-        if (static_cast<unsigned>(counts[j]) == cstar && seen++ == r) sh_jstar = j;
+#pragma unroll
+      for (int i = 0; i < PER; ++i)
+        if (valid(i) && c[i] == cstar && seen++ == r) sh_jstar = j0 + i;
     }
     __syncthreads();
     jstar = sh_jstar;
   }
 
   // flags and block-wide exclusive scan of sparse counts in index order
-  auto is_sparse = [&](int j) {
-    const unsigned c = static_cast<unsigned>(counts[j]);
-    return n_sparse > 0 && (c < cstar || (c == cstar && j <= jstar));
-  };
-  int my_sparse = 0;
-  for (int j = j0; j < j1; ++j) my_sparse += is_sparse(j) ? 1 : 0;
+  unsigned long long sparse_bits = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (valid(i) && n_sparse > 0 && (c[i] < cstar || (c[i] == cstar && j0 + i <= jstar))) sparse_bits |= 1ull << i;
   int total;
-  int s_off = block_excl_scan_1024(my_sparse, warp_tot, lane, wid, total);
-  int d_off = j0 - s_off;
-  for (int j = j0; j < j1; ++j) {
-    if (is_sparse(j)) {
+  int s_off = block_excl_scan_1024(__popcll(sparse_bits), warp_tot, lane, wid, total);
+  int d_off = min(j0, h) - s_off;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    if (!valid(i)) break;
+    const int j = j0 + i;
+    if (sparse_bits >> i & 1ull) {
       sparse_idx[s_off] = j;
       feat_pos[j] = s_off;
       ++s_off;
@@ -771,8 +773,19 @@ int s24_plan(const int* counts, int64_t h, int64_t n_sparse, int* sparse_idx, in
   if (h == 0) return S24_OK;
   // (32 registers x 1024 threads and 8 KB of shared memory: the one CTA fits
   // next to a running 2:4 GEMM CTA, so the plan can overlap fwd.out)
-  k_plan<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(counts, static_cast<int>(h), static_cast<int>(n_sparse),
-                                                            sparse_idx, dense_idx, feat_pos, 0);
+  const int per = static_cast<int>((h + 1023) / 1024);
+  const auto st = static_cast<cudaStream_t>(stream);
+  const int hh = static_cast<int>(h), ns = static_cast<int>(n_sparse);
+  if (per <= 4)
+    k_plan<4><<<1, 1024, 0, st>>>(counts, hh, ns, sparse_idx, dense_idx, feat_pos);
+  else if (per <= 8)
+    k_plan<8><<<1, 1024, 0, st>>>(counts, hh, ns, sparse_idx, dense_idx, feat_pos);
+  else if (per <= 16)
+    k_plan<16><<<1, 1024, 0, st>>>(counts, hh, ns, sparse_idx, dense_idx, feat_pos);
+  else if (per <= 32)
+    k_plan<32><<<1, 1024, 0, st>>>(counts, hh, ns, sparse_idx, dense_idx, feat_pos);
+  else
+    k_plan<64><<<1, 1024, 0, st>>>(counts, hh, ns, sparse_idx, dense_idx, feat_pos);
   return check_launch("k_plan");
 }
 

@@ -210,7 +210,8 @@ def test_gather_rows():
 
 
 @pytest.mark.parametrize("h,ratio,hi", [(2048, 0.95, 4096), (8192, 0.95, 50), (16384, 0.95, 32768), (100, 0.5, 3),
-                                        (4096, 1.0, 10), (4096, 0.0, 10), (1, 0.95, 5)])
+                                        (4096, 1.0, 10), (4096, 0.0, 10), (1, 0.95, 5), (30002, 0.9, 7),
+                                        (65536, 0.95, 40000), (5000, 0.95, 1 << 20)])
 def test_plan_matches_oracle(h, ratio, hi):
     rng = np.random.Generator(np.random.PCG64(h))
     counts = rng.integers(0, hi, h).astype(np.int32)
