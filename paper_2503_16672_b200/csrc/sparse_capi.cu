@@ -802,7 +802,7 @@ int s24_feature_split_x(const void* vals, const uint8_t* meta_hw, int64_t n, int
   if (n == 0 || h == 0) return S24_OK;
   K4xArgs a{static_cast<const __nv_bfloat16*>(vals), meta_hw, static_cast<int>(n), static_cast<int>(h), feat_pos,
             static_cast<int>(2 * n_dense), static_cast<__nv_bfloat16*>(vs), es, nan_flag};
-  const dim3 grid(static_cast<unsigned>(h / (16 * K4X_WARPS)), static_cast<unsigned>((n / 128 + K4X_TB - 1) / K4X_TB));
+  const dim3 grid(static_cast<unsigned>(h / (16 * K4X_WARPS)), static_cast<unsigned>(n / 128));
   (operand_nonneg ? k_feature_split_x<true> : k_feature_split_x<false>)<<<grid, 32 * K4X_WARPS, 0, st>>>(a);
   return check_launch("k_feature_split_x");
 }

@@ -2,7 +2,7 @@
 builds of libs24.so, in one process so box-to-box and clock drift cancel out.
 
 usage: python scripts/ab_step.py --libs paper_2503_16672_b200/libs24.so,/tmp/alt.so [--blocks 8] [--steps 5]
-       [--dense] [--n 16384 --d 2048 --h 8192]
+       [--dense] [--k4] [--n 16384 --d 2048 --h 8192]
 A variant may carry environment settings read by the Python layer while the
 graph is captured: --libs "a.so,a.so|S24_FOO=1".
 
@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--d", type=int, default=2048)
     ap.add_argument("--h", type=int, default=8192)
+    ap.add_argument("--k4", action="store_true",
+                    help="time only the two feature-wise splits (K4 of act and g_pre, alone) per library")
     args = ap.parse_args()
     import bench  # noqa: E402
 
@@ -66,8 +68,34 @@ def main():
         variants.append(("dense_twin", variants[0][1], s24.FfnConfig()))
         envs.append({})
     graphs = []
+    if args.k4:
+        from paper_2503_16672_b200.splitgemm import alloc_feature_split, run_feature_split
+
+        _lib._lib = variants[0][1]
+        out, cache = s24.ffn_forward(x, p, s24.RECIPE)
+        grads = s24.ffn_backward(dy, cache, p, s24.RECIPE)
+        plan, npad = cache.plan, cache.act_vals.shape[0]
+        g_vals = grads.g_pre_sparse.data
+        torch.cuda.synchronize()
     for (name, lib, cfg), env in zip(variants, envs):
         _lib._lib = lib
+        if args.k4:
+            fa = alloc_feature_split(cache.act_vals, cache.act_meta, npad, args.h, plan)
+            fg = alloc_feature_split(g_vals, cache.act_meta, npad, args.h, plan)
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                run_feature_split(fa, cache.act_vals, cache.act_meta, npad, args.h, plan, nonneg=True,
+                                  nan_flag=cache.stats_dev[2:])
+                run_feature_split(fg, g_vals, cache.act_meta, npad, args.h, plan)
+            torch.cuda.current_stream().wait_stream(st)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                run_feature_split(fa, cache.act_vals, cache.act_meta, npad, args.h, plan, nonneg=True,
+                                  nan_flag=cache.stats_dev[2:])
+                run_feature_split(fg, g_vals, cache.act_meta, npad, args.h, plan)
+            graphs.append(g)
+            continue
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
         g = s24.FfnStepGraph(p, cfg, n)
