@@ -16,15 +16,6 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
-// bitwise 0 / 0xffffffff comparison mask (single FSET instruction)
-__device__ __forceinline__ uint32_t fge_mask(float a, float b) {
-  uint32_t r;
-  asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
-  return r;
-}
-
-__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
-__device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
 
 // e4m3 GEMMs: v = (sr * col_scale[j]) * acc (the reference's order), the 32
 // column scales of the chunk read as 8 broadcast 16-byte loads
@@ -45,12 +36,6 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
-// keep bits (4-bit mask with two bits set) -> nibble i0 | i1 << 2
-constexpr unsigned long long kKeepNibbleLut = 0x000E0DC009804000ull;
-
-__device__ __forceinline__ uint32_t keep_nibble(uint32_t kb) {
-  return static_cast<uint32_t>(kKeepNibbleLut >> (4u * kb)) & 0xFu;
-}
 
 // relu that keeps NaN (numpy's maximum(y, 0), ref ffn.py:167-169)
 __device__ __forceinline__ float relu_nan(float x) {

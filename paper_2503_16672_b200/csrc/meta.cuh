@@ -67,6 +67,26 @@ __device__ __forceinline__ uint32_t keep_to_nibble(uint32_t keep) {
   return i0 | (i1 << 2);
 }
 
+// The same rule on 0 / 0xffffffff masks (the fused epilogues' form): i beats
+// j (i < j) iff key_i >= key_j; kept iff it beats two of the other three
+// (a bitwise majority); the kept values are picked with bitwise selects.
+// fge_mask compiles to one compare (+ select) per pair.
+__device__ __forceinline__ uint32_t fge_mask(float a, float b) {
+  uint32_t r;
+  asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
+__device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
+
+// keep bits (4-bit mask with two bits set) -> nibble i0 | i1 << 2
+constexpr unsigned long long kKeepNibbleLut = 0x000E0DC009804000ull;
+
+__device__ __forceinline__ uint32_t keep_nibble(uint32_t kb) {
+  return static_cast<uint32_t>(kKeepNibbleLut >> (4u * kb)) & 0xFu;
+}
+
 __device__ __forceinline__ float sel4(float x0, float x1, float x2, float x3, uint32_t i) {
   float r = x0;
   r = (i == 1u) ? x1 : r;

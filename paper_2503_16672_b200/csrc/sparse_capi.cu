@@ -87,40 +87,90 @@ __global__ void k_sparsify_token(const T* __restrict__ a, long long rows, long l
 }
 
 // Fast path of the above for the operand the GEMMs consume (values + hw
-// metadata only): one thread per 16-column chunk, 16-byte vector loads and a
-// single 16-byte value store; needs cols % 16 == 0 and 16-byte aligned rows.
-template <typename T>
+// metadata only; cols % 128 == 0). A warp unit is 4 rows x 128 columns: rows
+// {2j, 2j+1, 2j+8, 2j+9} of a 16-row group, lane = (k1, row, k2) owning the
+// 16-column chunk q = k1 + 2 k2 of the atom column. That is exactly the
+// rows x chunks that share the hw layout's 32-byte metadata sectors (meta.cuh:
+// rows m0 = 2j, 2j+1 and m1 = 0, 1; chunks k2 = 0..3 at fixed k1), so each
+// half-warp's halfword stores fill one whole sector instead of scattering
+// halfwords that other warps complete much later. Per row the warp reads 256
+// contiguous input bytes and writes 128 contiguous value bytes.
+#ifndef S24_TOK_U
+#define S24_TOK_U 2
+#endif
+template <typename T, bool STATS>
 __global__ void __launch_bounds__(256) k_sparsify_token_hw(const T* __restrict__ a, long long rows, long long cols,
                                                            long long lda, __nv_bfloat16* __restrict__ vals,
-                                                           uint8_t* __restrict__ meta_hw, unsigned long long* stats) {
+                                                           uint8_t* __restrict__ meta_hw,
+                                                           unsigned long long* stats) {
   constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte load
   constexpr int NV = 16 / VEC;         // 16-byte loads per chunk
-  constexpr int U = 2;                 // chunks per thread per iteration (their loads in flight together)
-  const long long chunks_per_row = cols / 16;
-  const long long total = rows * chunks_per_row;
-  const long long stride = (long long)gridDim.x * blockDim.x;
+  constexpr int U = S24_TOK_U;         // warp units per iteration (their loads in flight together)
+  const int lane = threadIdx.x & 31;
+  const int k1 = lane >> 4, rho = (lane >> 2) & 3, k2 = lane & 3;
+  const long long kbs = cols / 128;                       // atom columns
+  const long long units = (rows + 15) / 16 * 4 * kbs;     // row quartets (4 per 16-row group) x atom columns
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
   unsigned long long nb = 0, na = 0;
-  for (long long w0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; w0 < total; w0 += U * stride) {
-    uint4 u[U][NV];
+  for (long long u0 = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); u0 < units; u0 += U * wstride) {
+    uint4 ld[U][NV];
+    long long rr[U], qq[U];
 #pragma unroll
     for (int c = 0; c < U; ++c) {
-      const long long w = w0 + c * stride;
-      if (w < total) {
-        const long long r = w / chunks_per_row, q = w - r * chunks_per_row;
-        const uint4* src = reinterpret_cast<const uint4*>(a + r * lda + q * 16);
+      const long long u = u0 + c * wstride;
+      const long long quartet = u / kbs, kb = u - quartet * kbs;
+      rr[c] = (quartet >> 2) * 16 + (quartet & 3) * 2 + (rho & 1) + 8 * (rho >> 1);
+      qq[c] = kb * 8 + k1 + 2 * k2;
+      if (u < units && rr[c] < rows) {
+        const uint4* src = reinterpret_cast<const uint4*>(a + rr[c] * lda + qq[c] * 16);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) u[c][v] = __ldcs(src + v);  // (streamed: read once)
+        for (int v = 0; v < NV; ++v) ld[c][v] = __ldcs(src + v);  // (streamed: read once)
       }
     }
 #pragma unroll
     for (int c = 0; c < U; ++c) {
-      const long long w = w0 + c * stride;
-      if (w >= total) break;
-      const long long r = w / chunks_per_row, q = w - r * chunks_per_row;
+      const long long u = u0 + c * wstride;
+      if (u >= units || rr[c] >= rows) continue;
+      const long long r = rr[c], q = qq[c];
+      if constexpr (sizeof(T) == 2) {
+        // bf16 in: two groups per bf16x2 word (the same in-group position of
+        // groups g and g + 1), ranked with K4x's packed compares (k4.cuh)
+        const uint32_t w[8] = {ld[c][0].x, ld[c][0].y, ld[c][0].z, ld[c][0].w,
+                               ld[c][1].x, ld[c][1].y, ld[c][1].z, ld[c][1].w};
+        uint32_t packed[4];
+        uint32_t m16 = 0;
+#pragma unroll
+        for (int g = 0; g < 4; g += 2) {
+          const uint32_t x0 = __byte_perm(w[2 * g], w[2 * g + 2], 0x5410);
+          const uint32_t x1 = __byte_perm(w[2 * g], w[2 * g + 2], 0x7632);
+          const uint32_t x2 = __byte_perm(w[2 * g + 1], w[2 * g + 3], 0x5410);
+          const uint32_t x3 = __byte_perm(w[2 * g + 1], w[2 * g + 3], 0x7632);
+          const uint32_t k0 = k4_key2(x0), k1 = k4_key2(x1), k2 = k4_key2(x2), k3 = k4_key2(x3);
+          const uint32_t b01 = k4_ge(k0, k1), b02 = k4_ge(k0, k2), b03 = k4_ge(k0, k3);
+          const uint32_t b12 = k4_ge(k1, k2), b13 = k4_ge(k1, k3), b23 = k4_ge(k2, k3);
+          const uint32_t K0 = k4_maj(b01, b02, b03), K1 = k4_maj(~b01, b12, b13);
+          const uint32_t K2 = k4_maj(~b02, ~b12, b23), K3 = k4_maj(~b03, ~b13, ~b23);
+          const uint32_t v0 = k4_sel(K0, x0, k4_sel(K1, x1, x2));
+          const uint32_t v1 = k4_sel(K3, x3, k4_sel(K2, x2, x1));
+          const uint32_t nib = ((~K0 & K1) & 0x00010001u) | ((~K0 & ~K1) & 0x00020002u) |
+                               ((K3 | ~K2) & 0x00040004u) | ((K3 | K2) & 0x00080008u);
+          packed[g] = __byte_perm(v0, v1, 0x5410);
+          packed[g + 1] = __byte_perm(v0, v1, 0x7632);
+          m16 |= ((nib & 0xFu) | ((nib >> 12) & 0xF0u)) << (4 * g);
+          if constexpr (STATS) {
+            nb += __popc(k4_nz(x0) | (k4_nz(x1) << 1) | (k4_nz(x2) << 2) | (k4_nz(x3) << 3));
+            na += __popc(k4_nz(v0) | (k4_nz(v1) << 1));
+          }
+        }
+        *reinterpret_cast<uint4*>(vals + r * (cols / 2) + q * 8) =
+            make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        *reinterpret_cast<uint16_t*>(meta_hw + meta_hw_halfword_offset(r, q, cols)) = static_cast<uint16_t>(m16);
+        continue;
+      }
       float x[16];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        const uint32_t wv[4] = {u[c][v].x, u[c][v].y, u[c][v].z, u[c][v].w};
+        const uint32_t wv[4] = {ld[c][v].x, ld[c][v].y, ld[c][v].z, ld[c][v].w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if constexpr (sizeof(T) == 4) {
@@ -136,18 +186,29 @@ __global__ void __launch_bounds__(256) k_sparsify_token_hw(const T* __restrict__
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const float x0 = x[4 * g], x1 = x[4 * g + 1], x2 = x[4 * g + 2], x3 = x[4 * g + 3];
-        nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
-        const uint32_t nib = keep_to_nibble(top2_keep_mask(x0, x1, x2, x3));
-        const float v0 = sel4(x0, x1, x2, x3, nib & 3u), v1 = sel4(x0, x1, x2, x3, nib >> 2);
-        na += (v0 != 0.f) + (v1 != 0.f);
+        // magnitude keys, NaN -> -1 (ranked below every number: max(NaN, -1) = -1)
+        const float k0 = fmaxf(fabsf(x0), -1.f), k1 = fmaxf(fabsf(x1), -1.f);
+        const float k2 = fmaxf(fabsf(x2), -1.f), k3 = fmaxf(fabsf(x3), -1.f);
+        const uint32_t b01 = fge_mask(k0, k1), b02 = fge_mask(k0, k2), b03 = fge_mask(k0, k3);
+        const uint32_t b12 = fge_mask(k1, k2), b13 = fge_mask(k1, k3), b23 = fge_mask(k2, k3);
+        const uint32_t K0 = maj3(b01, b02, b03), K1 = maj3(~b01, b12, b13);
+        const uint32_t K2 = maj3(~b02, ~b12, b23), K3 = maj3(~b03, ~b13, ~b23);
+        const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1), u2 = __float_as_uint(x2),
+                       u3 = __float_as_uint(x3);
+        const float v0 = __uint_as_float(bsel(K0, u0, bsel(K1, u1, u2)));  // first kept
+        const float v1 = __uint_as_float(bsel(K3, u3, bsel(K2, u2, u1)));  // second kept
+        if constexpr (STATS) {
+          nb += (x0 != 0.f) + (x1 != 0.f) + (x2 != 0.f) + (x3 != 0.f);
+          na += (v0 != 0.f) + (v1 != 0.f);
+        }
         packed[g] = pack_bf16x2(v0, v1);
-        m16 |= nib << (4 * g);
+        m16 |= keep_nibble((K0 & 1u) | (K1 & 2u) | (K2 & 4u) | (K3 & 8u)) << (4 * g);
       }
       *reinterpret_cast<uint4*>(vals + r * (cols / 2) + q * 8) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
       *reinterpret_cast<uint16_t*>(meta_hw + meta_hw_halfword_offset(r, q, cols)) = static_cast<uint16_t>(m16);
     }
   }
-  if (stats) {
+  if constexpr (STATS) {
     block_sum_u64_to(nb, stats);
     block_sum_u64_to(na, stats + 1);
   }
@@ -597,12 +658,20 @@ int s24_sparsify_token(const void* a, int dtype, int64_t rows, int64_t cols, int
   const int g = grid_for(work, 256);
   const int esz = dtype == S24_F32 ? 4 : 2;
   if (meta_hw && !meta_ref && !mask && aligned16(a) && aligned16(vals) && (lda * esz) % 16 == 0) {
-    if (dtype == S24_F32)
-      k_sparsify_token_hw<float><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
-                                                    static_cast<__nv_bfloat16*>(vals), meta_hw, stats);
+    auto run = [&](auto stats_tag) {
+      constexpr bool ST = decltype(stats_tag)::value;
+      if (dtype == S24_F32)
+        k_sparsify_token_hw<float, ST><<<g, 256, 0, st>>>(static_cast<const float*>(a), rows, cols, lda,
+                                                          static_cast<__nv_bfloat16*>(vals), meta_hw, stats);
+      else
+        k_sparsify_token_hw<__nv_bfloat16, ST><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols,
+                                                                  lda, static_cast<__nv_bfloat16*>(vals), meta_hw,
+                                                                  stats);
+    };
+    if (stats)
+      run(std::true_type{});
     else
-      k_sparsify_token_hw<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a), rows, cols, lda,
-                                                            static_cast<__nv_bfloat16*>(vals), meta_hw, stats);
+      run(std::false_type{});
     return check_launch("k_sparsify_token_hw");
   }
   if (dtype == S24_F32) {

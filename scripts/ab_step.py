@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--h", type=int, default=8192)
     ap.add_argument("--k4", action="store_true",
                     help="time only the two feature-wise splits (K4 of act and g_pre, alone) per library")
+    ap.add_argument("--sparsify", action="store_true",
+                    help="time only the standalone token-wise sparsifier on an [n, h] bf16 activation per library")
     args = ap.parse_args()
     import bench  # noqa: E402
 
@@ -77,8 +79,25 @@ def main():
         plan, npad = cache.plan, cache.act_vals.shape[0]
         g_vals = grads.g_pre_sparse.data
         torch.cuda.synchronize()
+    if args.sparsify:
+        act = (torch.randn(n, args.h, device="cuda") * (torch.rand(n, args.h, device="cuda") < 0.1)).bfloat16()
+        sv = torch.zeros(n, args.h // 2, dtype=torch.bfloat16, device="cuda")
+        sm = torch.empty(_lib.meta_hw_bytes(n, args.h), dtype=torch.uint8, device="cuda")
     for (name, lib, cfg), env in zip(variants, envs):
         _lib._lib = lib
+        if args.sparsify:
+            g = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                _lib.call("s24_sparsify_token", act.data_ptr(), _lib.BF16, n, args.h, args.h, sv.data_ptr(), None,
+                          sm.data_ptr(), None, None, st.cuda_stream)
+            torch.cuda.current_stream().wait_stream(st)
+            with torch.cuda.graph(g):
+                _lib.call("s24_sparsify_token", act.data_ptr(), _lib.BF16, n, args.h, args.h, sv.data_ptr(), None,
+                          sm.data_ptr(), None, None, torch.cuda.current_stream().cuda_stream)
+            graphs.append(g)
+            continue
         if args.k4:
             fa = alloc_feature_split(cache.act_vals, cache.act_meta, npad, args.h, plan)
             fg = alloc_feature_split(g_vals, cache.act_meta, npad, args.h, plan)

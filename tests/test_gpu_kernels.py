@@ -416,12 +416,12 @@ def test_feature_split_x_matches_reference_kernel(nan):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_sparsify_token_hw_fast_path_bitwise(dtype):
+@pytest.mark.parametrize("rows,cols", [(384, 1024), (100, 256), (4, 128)])
+def test_sparsify_token_hw_fast_path_bitwise(dtype, rows, cols):
     """s24_sparsify_token with only values + hw metadata requested takes the
-    vectorized one-chunk-per-thread kernel: bit-identical to the general
-    kernel (which also writes the reference metadata and the mask), NaN / Inf
-    included."""
-    rows, cols = 384, 1024
+    sector-mapped fast kernel: bit-identical to the general kernel (which also
+    writes the reference metadata and the mask), NaN / Inf and ragged row
+    counts included."""
     a = torch.randn(rows, cols, device="cuda") * (torch.rand(rows, cols, device="cuda") < 0.4)
     a[torch.rand(rows, cols, device="cuda") < 0.01] = float("nan")
     a[torch.rand(rows, cols, device="cuda") < 0.005] = float("inf")
@@ -432,6 +432,8 @@ def test_sparsify_token_hw_fast_path_bitwise(dtype):
     s1 = torch.zeros(2, dtype=torch.int64, device="cuda")
     dt = F32 if dtype == torch.float32 else BF16
     _lib.call("s24_sparsify_token", P(a), dt, rows, cols, cols, P(v1), None, P(m1), None, P(s1), S())
+    v2, m2 = torch.zeros_like(v0), torch.full_like(m0, 0x44)
+    _lib.call("s24_sparsify_token", P(a), dt, rows, cols, cols, P(v2), None, P(m2), None, None, S())  # (no statistics)
     torch.cuda.synchronize()
-    assert torch.equal(v0.view(torch.int16), v1.view(torch.int16))
-    assert torch.equal(m0, m1) and torch.equal(s0, s1)
+    assert torch.equal(v0.view(torch.int16), v1.view(torch.int16)) and torch.equal(v0.view(torch.int16), v2.view(torch.int16))
+    assert torch.equal(m0, m1) and torch.equal(m0, m2) and torch.equal(s0, s1)
