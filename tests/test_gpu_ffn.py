@@ -288,20 +288,24 @@ def test_grad_ready_order_is_bitwise_identical():
     assert torch.equal(seen[0][1], g0.d_w2) and torch.equal(seen[1][1], g0.d_w1)
 
 
-def test_public_side_stream_outputs_are_safe_to_read():
+@pytest.mark.parametrize("fp8", [False, True])
+def test_public_side_stream_outputs_are_safe_to_read(fp8):
     """The plan and x_in are produced on the side stream; reading them from
     the cache right after ffn_forward (no synchronize, no backward) must see
     the finished values (the properties make the caller's stream wait)."""
+    from dataclasses import replace
+
     n, d, h = 4096, 512, 2048
+    cfg = replace(s24.RECIPE, fp8_emulation=True, fp8_backward=True) if fp8 else s24.RECIPE
     x, w1, w2, _ = O.synthetic_ffn_inputs(n, d, h, sparsity=0.9, seed=5)
     p = s24.FfnParams(w1=torch.from_numpy(w1).cuda(), w2=torch.from_numpy(w2).cuda())
     tx = torch.from_numpy(x).cuda()
-    ref_out, ref_cache = s24.ffn_forward(tx, p, s24.RECIPE)
+    ref_out, ref_cache = s24.ffn_forward(tx, p, cfg)
     torch.cuda.synchronize()
     want_sp = ref_cache.plan.sparse_features.cpu()
     want_x = ref_cache.x_in.cpu()
     for _ in range(3):
-        out, cache = s24.ffn_forward(tx, p, s24.RECIPE)
+        out, cache = s24.ffn_forward(tx, p, cfg)
         assert torch.equal(cache.plan.sparse_features.cpu(), want_sp)
         assert torch.equal(cache.x_in.cpu(), want_x)
 
