@@ -248,3 +248,27 @@ def test_recipe_at_7b_class_size(sparsity):
     import bench
 
     full_parity(*bench.CONFIGS["c4"], sparsity=sparsity, seed=11)
+
+
+def test_prefill_at_7b_class_size():
+    """BASELINE configs[2] (c3: the 7B-class FFN forward, inference prefill):
+    the forward without the permutation / plan / split (for_backward=False)
+    returns the bits of the training forward, and its selection, values,
+    counts and statistics follow the rank rule on its own pre-activation."""
+    import bench
+
+    n, d, h = bench.CONFIGS["c3"]
+    x, w1, w2, _ = bench.synthetic_device_inputs(torch, n, d, h, seed=13, device=torch.device("cuda"))
+    p = s24.FfnParams(w1=w1, w2=w2)
+    out_inf, c_inf = s24.ffn_forward(x, p, s24.RECIPE, for_backward=False, keep_pre_act=True)
+    out_tr, c_tr = s24.ffn_forward(x, p, s24.RECIPE)
+    torch.cuda.synchronize()
+    assert torch.equal(out_inf, out_tr)
+    assert c_inf.perm is None and c_inf.act_split is None
+    act = torch.clamp_min(c_inf.pre_act, 0) ** 2
+    m_rule = top2_mask(act.reshape(n, h // 4, 4)).reshape(n, h)
+    assert torch.equal(c_inf.fwd_mask, m_rule)
+    assert torch.equal(c_inf.act_sparse.values.reshape(n, h // 2), act[m_rule].reshape(n, h // 2).bfloat16())
+    counts = (act != 0).sum(dim=0)
+    assert torch.equal(c_inf.counts.long(), counts) and torch.equal(c_tr.counts, c_inf.counts)
+    assert c_inf.stats.nonzeros_after == int((act * m_rule != 0).sum())
