@@ -661,7 +661,8 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         # unmasked derivative: needs relu(y1) everywhere (fp32 pre-activation kept by the forward)
         G = torch.empty(n, h, dtype=F32, device=dev)
         _lib.call("s24_gemm", ptr(g_c), 0, d, ptr(p.w2), 0, d, n, h, d, ptr(G), _lib.F32, h, None, 0, -1, None, s)
-        g_pre_dense = (G * act_squared_relu_grad(cache.pre_act)).to(BF16)
+        G *= act_squared_relu_grad(cache.pre_act)  # g_pre in fp32 (the reference's precision)
+        g_pre_dense = G.to(BF16)
 
     mode = cfg.backward_mode
     if mode == "dense":
@@ -696,8 +697,10 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         # (ref ffn.py:430-437); the split path always sees the masked g_pre
         from .sparse24 import sparsify_feature_wise
 
-        gpad = torch.zeros(npad, h, dtype=BF16, device=dev)
-        gpad[:n] = g_pre_dense
+        # (the selection ranks the fp32 g_pre, as the reference does; a bf16
+        # copy would turn near-ties into ties that break toward lower tokens)
+        gpad = torch.zeros(npad, h, dtype=F32, device=dev)
+        gpad[:n] = G
         sg, _, stats_g = sparsify_feature_wise(gpad)
         _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
         main.wait_event(cache.side_ready)
