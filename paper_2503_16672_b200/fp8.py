@@ -342,6 +342,19 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     ev_w = ov.record()
 
     x_in = _frame_rows(x, npad, inv_dev)
+    # x_in^T codes (the dW1 GEMM's B operand) on a stream of their own, from
+    # here on: off the chain of plan / K4(act) / split codes of the side stream,
+    # so neither waits for the other (their events are merged into side_ready)
+    xt = sxt = ev_xt = None
+    if split_bwd and fp8b:
+        from .splitgemm import side_stream
+
+        xt = torch.empty(d, npad, dtype=U8, device=dev)  # npad % 128 == 0: no padding columns
+        sxt = torch.empty(d, dtype=F32, device=dev)
+        st_x = side_stream(dev, 2)
+        st_x.wait_stream(ov.main)
+        quant_cols_t(x_in, xt, sxt, st=st_x, keep=ov.keep)
+        ev_xt = ov.record(st_x)
     xq, sx = quant_rows(x_in)
     w1q, s1 = quant_cols_t(p.w1)  # [h, d] (d % 32 == 0)
     vals32 = torch.empty(npad, h // 2, dtype=F32, device=dev)
@@ -385,10 +398,9 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     if split_bwd:
         fa = alloc_feature_split(act_vals, act_meta, npad, h, bplan)
     if split_bwd and fp8b:
-        xt = torch.empty(d, npad, dtype=U8, device=dev)  # npad % 128 == 0: no padding columns
         f8 = dict(wb, vq_a=torch.empty(fa.vs.shape, dtype=U8, device=dev),
                   sv_a=torch.empty(fa.vs.shape[0], dtype=F32, device=dev), e8_a=torch.empty_like(fa.es),
-                  rows_a=fa.rows(bplan), xt=xt, sxt=torch.empty(d, dtype=F32, device=dev), keep=ov.keep)
+                  rows_a=fa.rows(bplan), xt=xt, sxt=sxt, keep=ov.keep)
     elif wb is not None:
         f8 = dict(wb, keep=ov.keep)
     ov.join(ev_w)
@@ -404,7 +416,8 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
             quant_rows(fa.vs, rows=f8["rows_a"], pair_rows=fa.pair_rows, codes=f8["vq_a"], scales=f8["sv_a"],
                        st=ov.st)
             meta_to_f8(fa.es, f8["rows_a"], npad, out=f8["e8_a"], st=ov.st)
-            quant_cols_t(x_in, f8["xt"], f8["sxt"], st=ov.st, keep=ov.keep)
+        if ev_xt is not None:
+            ov.st.wait_event(ev_xt)  # (side_ready covers the x_in^T codes too)
         ev_side = ov.record()
     elif ov.side is not None and plan_out is not None and plan_out is not plan:
         ev_side = ov.record()
@@ -486,13 +499,18 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
     else:
         w2q, s2 = quant_rows(p.w2)  # w2t per column = w2 per row: [h, d]
         w1r, s1r = quant_rows(p.w1)  # w1t per column = w1 per row: [d, h]
-    gt = sgt = None
+    gt = sgt = ev_gt = None
     if split:
-        # g_c^T codes (dW2's B operand) on the side stream, next to K3
+        # g_c^T codes (dW2's B operand) on a stream of their own (not queued
+        # behind the forward's side work), next to K3
+        from .splitgemm import side_stream
+
         gt = torch.empty(d, npad, dtype=U8, device=dev)
         sgt = torch.empty(d, dtype=F32, device=dev)
-        ov.fork()
-        quant_cols_t(g_c, gt, sgt, st=ov.st, keep=ov.keep)
+        st_g = side_stream(dev, 3)
+        st_g.wait_stream(ov.main)
+        quant_cols_t(g_c, gt, sgt, st=st_g, keep=ov.keep)
+        ev_gt = ov.record(st_g)
     # K3 on e4m3 codes: g_pre on the forward keep pattern (relu from the
     # unquantized activation), compressed
     gq, sg = quant_rows(g_c)
@@ -561,6 +579,7 @@ def ffn_backward_f8(g_out: torch.Tensor, cache, p, cfg, grad_ready=None, grad_bu
         if cache.side_ready is not None:
             torch.cuda.current_stream().wait_event(cache.side_ready)
         ov.join(ev_g)
+        ov.join(ev_gt)
         fa = cache.act_split
         if fa is None:
             fa = feature_split(cache.act_vals, cache.act_meta, npad, h, plan)

@@ -204,7 +204,8 @@ def run_feature_split(fs: FeatureSplit, vals: torch.Tensor, meta_hw: torch.Tenso
 
 def side_stream(device, which: int = 0) -> torch.cuda.Stream:
     """Per-device streams that carry K4 and the permuted copies next to the
-    main-stream GEMMs (0: the forward's, 1: the backward's)."""
+    main-stream GEMMs (0: the forward's, 1: the backward's; the e4m3 path also
+    quantizes the weight gradients' B operands on 2: x_in^T, 3: g_c^T)."""
     idx = device.index if device.index is not None else torch.cuda.current_device()
     st = _side_streams.get((idx, which))
     if st is None:

@@ -99,12 +99,17 @@ def main():
     ap.add_argument("--h", type=int, default=8192)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--queued", action="store_true")
+    ap.add_argument("--fp8", action="store_true", help="the recipe with fp8_emulation + fp8_backward")
     args = ap.parse_args()
     import bench  # noqa: E402
 
     x, w1, w2, dy = bench.synthetic_device_inputs(torch, args.n, args.d, args.h, seed=1234,
                                                   device=torch.device("cuda"))
     p = s24.FfnParams(w1=w1, w2=w2)
+    if args.fp8:
+        from dataclasses import replace
+
+        s24.RECIPE = replace(s24.RECIPE, fp8_emulation=True, fp8_backward=True)
     if args.queued:
         return queued_timeline(args, p, x, dy)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
