@@ -263,10 +263,17 @@ class FfnGrads:
     stats_act: SparsifyStats | None = None  # feature-wise drops of the act split (dW2)
     stats_grad: SparsifyStats | None = None  # feature-wise drops of the g_pre split (dW1)
     # diagnostic views (parity checks): g_pre as K3 stored it (token-wise, on
-    # the forward metadata, compute frame) and the feature-wise split of it
-    # the dW1 GEMM consumed (the act split is FfnCache.act_split)
-    g_pre_sparse: Sparse24Matrix | None = None
+    # the forward metadata, compute frame; built on first read for a padded
+    # FFN) and the feature-wise split of it the dW1 GEMM consumed (the act
+    # split is FfnCache.act_split)
+    _g_pre: object = None
     g_split: FeatureSplit | None = None
+
+    @property
+    def g_pre_sparse(self) -> Sparse24Matrix | None:
+        if callable(self._g_pre):
+            self._g_pre = self._g_pre()
+        return self._g_pre
 
 
 def act_squared_relu(pre):
@@ -579,8 +586,18 @@ def ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_read
     d_w1.copy_(gr.d_w1[:d, :h])
     notify("d_w1", d_w1)
     d_x = gr.d_x[:, :d].contiguous() if dp != d else gr.d_x
+
+    def g_pre_view():  # (diagnostic: the real features of the padded FFN's stored g_pre)
+        full = gr.g_pre_sparse
+        if full is None:
+            return None
+        if hp == h:
+            return full
+        return Sparse24Matrix(n, h, TOKEN_WISE, full.data[:, : h // 2].contiguous(), None,
+                              meta_ref_cache=full.meta[:, : h // 4].contiguous())
+
     return FfnGrads(d_w1, d_w2, d_x, None, _census_real(gr.census, n, d, h, cache._plan, cfg),
-                    _token_total(gr.stats_act, n, hp - h), _token_total(gr.stats_grad, n, hp - h))
+                    _token_total(gr.stats_act, n, hp - h), _token_total(gr.stats_grad, n, hp - h), g_pre_view)
 
 
 def _token_total(st: SparsifyStats | None, n: int, pad_features: int) -> SparsifyStats | None:

@@ -11,6 +11,8 @@ device stores bf16); GEMMs within 1e-5 relative of the oracle's fp32
 reduction over the same (bf16-valued) kept operands.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -19,6 +21,9 @@ import paper_2503_16672_b200 as s24
 from oracle import srelu24_np as O
 
 pytestmark = pytest.mark.gpu
+
+# S24_FUZZ_SCALE=k runs k times as many seeded cases (ad-hoc campaigns)
+SCALE = int(os.environ.get("S24_FUZZ_SCALE", "1"))
 
 
 def rel(a, b):
@@ -49,7 +54,7 @@ def shape(rng):
     return int(rng.integers(1, 80)) * 4, int(rng.integers(1, 80)) * 4
 
 
-@pytest.mark.parametrize("i", range(16))
+@pytest.mark.parametrize("i", range(16 * SCALE))
 def test_sparsifiers_and_compression(i):
     rng = np.random.Generator(np.random.PCG64(300 + i))
     rows, cols = shape(rng)
@@ -87,7 +92,7 @@ def test_sparsifiers_and_compression(i):
     assert np.array_equal(back, O.bf16_round(np.where(omask, a, np.float32(0))), equal_nan=True)
 
 
-@pytest.mark.parametrize("i", range(12))
+@pytest.mark.parametrize("i", range(12 * SCALE))
 def test_sparse_gemms_split_gemm_and_plan(i):
     rng = np.random.Generator(np.random.PCG64(500 + i))
     rows, cols = shape(rng)
@@ -126,7 +131,7 @@ def test_sparse_gemms_split_gemm_and_plan(i):
     assert rel(got, want) < 1e-5
 
 
-@pytest.mark.parametrize("i", range(6))
+@pytest.mark.parametrize("i", range(6 * SCALE))
 def test_permutations(i):
     rng = np.random.Generator(np.random.PCG64(700 + i))
     n, d = int(rng.integers(1, 300)), int(rng.choice([8, 16, 40, 64]))
