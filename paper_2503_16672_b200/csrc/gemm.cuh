@@ -58,6 +58,12 @@
 #ifndef S24_STATIC_SCHED
 #define S24_STATIC_SCHED 1
 #endif
+// S24_PROBE (experiments only): 1 = MMA issue without operand loads (stale
+// shared memory), 2 = operand loads without MMAs, 3 = as 1 without the 2:4
+// metadata copies into TMEM. Results are garbage.
+#ifndef S24_PROBE
+#define S24_PROBE 0
+#endif
 #ifndef S24_CLC_PREFETCH
 #define S24_CLC_PREFETCH 1
 #endif
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
         const int n0 = nb * Cfg::BN + static_cast<int>(rank) * Cfg::SUB_CTA;
         // half unit: this CTA's B_CTA/2 columns of the half (box 0 .. BN_CTA/128 - 1)
         const int n0h = nb * Cfg::BN + half * (Cfg::BN / 2) + static_cast<int>(rank) * (Cfg::BN_CTA / 2);
-        const uint32_t stage_tx = half < 0 ? Cfg::STAGE_BYTES : Cfg::STAGE_BYTES - Cfg::B_BYTES / 2;
+        const uint32_t stage_tx = (S24_PROBE == 1 || S24_PROBE == 3) ? 0u : half < 0 ? Cfg::STAGE_BYTES : Cfg::STAGE_BYTES - Cfg::B_BYTES / 2;
         const int atom_row = mb * CG + static_cast<int>(rank);  // 128-row metadata block
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -365,6 +371,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             mbar_arrive_expect_tx(&full_bar[stage], CG * stage_tx);
           else
             mbar_arrive_remote(&full_bar[stage], 0);
+          if (S24_PROBE == 1 || S24_PROBE == 3) {
+            if (++stage == Cfg::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if constexpr (Cfg::A_MN) {
             tma_load<CG>(sa, mapA, &full_bar[stage], m0, kb * Cfg::BK, pol_a);
             tma_load<CG>(sa + Cfg::A_BYTES / 2, mapA, &full_bar[stage], m0 + 64, kb * Cfg::BK, pol_a);
@@ -432,6 +445,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             e_tmem = tmem_base + Cfg::E_COL + stage * (4 * Cfg::E_ATOMS);
 #pragma unroll
             for (int a = 0; a < Cfg::E_ATOMS; ++a) {
+              if (S24_PROBE == 2 || S24_PROBE == 3) break;
               const uint64_t edesc = make_sdesc(sb + Cfg::B_BYTES + 2048 * a, 0, 128, kLayoutNone);
               if constexpr (CG == 2)
                 tmem_cp_128x128b_cg2(e_tmem + 4 * a, edesc);
@@ -461,6 +475,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
               bdesc = make_sdesc(sbs + j * 32, 16, 1024, kLayoutSw128);
             }
             const uint32_t accum = (kb > kb0 || j > 0) ? 1u : 0u;
+            if (S24_PROBE == 2) continue;
             if constexpr (Cfg::SPARSE && Cfg::F8) {
               // e4m3: one K=64 step reads 64 metadata bits per row = TMEM
               // columns 2j, 2j+1 of the stage

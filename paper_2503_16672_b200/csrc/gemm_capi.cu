@@ -45,7 +45,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 int make_map_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
-                uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+                uint32_t box_inner, uint32_t box_outer, int swizzle) {
   auto fn = encode_fn();
   if (!fn) return fail(S24_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (!aligned16(base) || ld_bytes % 16 != 0)
@@ -56,15 +56,17 @@ int make_map_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t inner, u
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(S24_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return S24_OK;
 }
 
 int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                  uint32_t box_inner, uint32_t box_outer) {
-  return make_map_2d(map, base, true, inner, outer, ld * 2, box_inner, box_outer, true);
+                  uint32_t box_inner, uint32_t box_outer, int swizzle) {
+  return make_map_2d(map, base, true, inner, outer, ld * 2, box_inner, box_outer, swizzle);
 }
 
 // operands of one GEMM problem (the grouped launch takes two of equal shape)
@@ -86,42 +88,42 @@ static int make_operand_maps(const void* A, int64_t lda, const void* B, int64_t 
     // e4m3 codes, both operands K-major (uint8 maps, 128-element boxes)
     if constexpr (Cfg::SPARSE) {
       const int64_t mpad = (M + 127) / 128 * 128;
-      rc = make_map_2d(ma, A, false, K / 2, mpad, K / 2, 128, Cfg::BM, true);
+      rc = make_map_2d(ma, A, false, K / 2, mpad, K / 2, 128, Cfg::BM, 128);
     } else {
-      rc = make_map_2d(ma, A, false, K, M, lda, 128, Cfg::BM, true);
+      rc = make_map_2d(ma, A, false, K, M, lda, 128, Cfg::BM, 128);
     }
     if (rc) return rc;
-    rc = make_map_2d(mb, B, false, K, N, ldb, 128, Cfg::B_BOX_ROWS, true);
+    rc = make_map_2d(mb, B, false, K, N, ldb, 128, Cfg::B_BOX_ROWS, 128);
     if (rc) return rc;
     std::memset(me, 0, sizeof(*me));
     if constexpr (Cfg::SPARSE) {
       const int64_t atoms = (M + 127) / 128 * (K / 128);
-      rc = make_map_2d(me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16 * Cfg::E_ATOMS, false);
+      rc = make_map_2d(me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16 * Cfg::E_ATOMS, 0);
     }
     return rc;
   }
   // A
   if constexpr (Cfg::A_MN) {
-    rc = make_map_bf16(ma, A, M, K, lda, 64, Cfg::BK);
+    rc = make_map_bf16(ma, A, M, K, lda, 64, Cfg::BK, 128);
   } else if constexpr (Cfg::SPARSE) {
     const int64_t mpad = (M + 127) / 128 * 128;
-    rc = make_map_bf16(ma, A, K / 2, mpad, K / 2, 64, Cfg::BM);
+    rc = make_map_bf16(ma, A, K / 2, mpad, K / 2, 64, Cfg::BM, 128);
   } else {
-    rc = make_map_bf16(ma, A, K, M, lda, 64, Cfg::BM);
+    rc = make_map_bf16(ma, A, K, M, lda, 64, Cfg::BM, 128);
   }
   if (rc) return rc;
   // B
   if constexpr (Cfg::B_MN) {
-    rc = make_map_bf16(mb, B, N, K, ldb, 64, Cfg::BK);
+    rc = make_map_bf16(mb, B, N, K, ldb, 64, Cfg::BK, 128);
   } else {
-    rc = make_map_bf16(mb, B, K, N, ldb, 64, Cfg::B_BOX_ROWS);
+    rc = make_map_bf16(mb, B, K, N, ldb, 64, Cfg::B_BOX_ROWS, 128);
   }
   if (rc) return rc;
   std::memset(me, 0, sizeof(*me));
   if constexpr (Cfg::SPARSE) {
     // metadata atoms viewed as [atoms * 16 rows, 128 bytes]; one box = one atom
     const int64_t atoms = (M + 127) / 128 * (K / 128);
-    rc = make_map_2d(me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16, false);
+    rc = make_map_2d(me, meta, false, 128, static_cast<uint64_t>(atoms) * 16, 128, 128, 16, 0);
     if (rc) return rc;
   }
   return S24_OK;
@@ -209,14 +211,22 @@ static int launch_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, i
 
 // tile configurations
 // <sparse, A MN-major, B MN-major, BN, stages, CTA-group, epilogue warps, e4m3>
-using DenseKN = GemmCfg<false, false, true, 256, 6, 2, 8>;   // A K-major, B MN-major
-using DenseKK = GemmCfg<false, false, false, 256, 6, 2, 8>;  // A K-major, B K-major
-using DenseMM = GemmCfg<false, true, true, 256, 6, 2, 8>;    // A MN-major, B MN-major
-using DenseMK = GemmCfg<false, true, false, 256, 6, 2, 8>;   // A MN-major, B K-major
+#ifndef S24_DN_STAGES
+#define S24_DN_STAGES 6
+#endif
+using DenseKN = GemmCfg<false, false, true, 256, S24_DN_STAGES, 2, 8>;   // A K-major, B MN-major
+using DenseKK = GemmCfg<false, false, false, 256, S24_DN_STAGES, 2, 8>;  // A K-major, B K-major
+using DenseMM = GemmCfg<false, true, true, 256, S24_DN_STAGES, 2, 8>;    // A MN-major, B MN-major
+using DenseMK = GemmCfg<false, true, false, 256, S24_DN_STAGES, 2, 8>;   // A MN-major, B K-major
 // sparse: light epilogue, 4 epilogue warps and <= 128 registers/thread, leaving
 // room for a co-resident side-stream kernel (the feature-wise split K4)
-using SparseN = GemmCfg<true, false, true, 256, 4, 2, 4>;   // sparse A, B MN-major
-using SparseK = GemmCfg<true, false, false, 256, 4, 2, 4>;  // sparse A, B K-major
+// (4 stages of 50 KB: 3 measured 18% slower; 8 half-K stages of 26 KB with
+// SWIZZLE_64B A rows 25-37% slower)
+#ifndef S24_SP_STAGES
+#define S24_SP_STAGES 4
+#endif
+using SparseN = GemmCfg<true, false, true, 256, S24_SP_STAGES, 2, 4>;   // sparse A, B MN-major
+using SparseK = GemmCfg<true, false, false, 256, S24_SP_STAGES, 2, 4>;  // sparse A, B K-major
 
 // e4m3 (kind::f8f6f4): same byte geometry per stage as the bf16 configs
 using F8DenseKK = GemmCfg<false, false, false, 256, 6, 2, 8, true>;

@@ -35,11 +35,12 @@ inline int check_launch(const char* what) {
 int num_sms();
 
 // 2-D bf16 tensor map: inner dim (contiguous) `inner` elements, `outer` rows,
-// row pitch `ld` elements; box {box_inner, box_outer}; 128B swizzle.
+// row pitch `ld` elements; box {box_inner, box_outer}; `swizzle` = 128, 64
+// (bytes) or 0 for none.
 int make_map_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
-                uint32_t box_inner, uint32_t box_outer, bool swizzle128);
+                uint32_t box_inner, uint32_t box_outer, int swizzle);
 int make_map_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                  uint32_t box_inner, uint32_t box_outer);
+                  uint32_t box_inner, uint32_t box_outer, int swizzle);
 
 // The device's greatest (most urgent) launch priority. Every kernel of the
 // FFN's critical path launches at it (the GEMMs, the row gathers, the plan);

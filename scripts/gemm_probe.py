@@ -1,5 +1,5 @@
 """Run one c2-shaped GEMM of the step repeatedly (for ncu captures):
-usage: python scripts/gemm_probe.py {k1|k3|relu2|dact|fwdout|dx|dw|dense|k4|gather|plan} [--iters 5]
+usage: python scripts/gemm_probe.py {k1|k3|relu2|dact|fwdout|dx|dw|dense|k4|gather|plan}[,...] [--iters 5]
 ncu: the step that builds the operands launches 6 gemm_kernel, 2 k_feature_split_x, 2 k_gather_rows and
 1 k_plan first (skip them with -s)."""
 import argparse
@@ -15,6 +15,7 @@ from paper_2503_16672_b200 import _lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("which")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--time", action="store_true", help="print the median CUDA-event time per call")
 args = ap.parse_args()
 import bench  # noqa: E402
 
@@ -56,7 +57,20 @@ calls = {
     "plan": lambda: _lib.call("s24_plan", P(cache.counts), h, plan.n_sparse, P(plan.sparse_features),
                               P(plan.dense_features), P(plan.feat_pos), S),
 }
-for _ in range(args.iters):
-    calls[args.which]()
+for which in args.which.split(","):
+    if args.time:
+        ts = []
+        for _ in range(args.iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            calls[which]()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        print(f"{which} median_ms {ts[len(ts) // 2]:.4f} min_ms {ts[0]:.4f}")
+        continue
+    for _ in range(args.iters):
+        calls[which]()
 torch.cuda.synchronize()
 print("ok", args.which)
