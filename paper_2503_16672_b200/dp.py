@@ -6,8 +6,9 @@ The FFN is per-token, so both inference prefill and training shard tokens:
   * training: each rank runs the full recipe on its shard (its own permutation
     of n/G tokens and its own split plan, i.e. the reference applied per shard)
     and the weight gradients are summed with ONE all-reduce bucket per tensor
-    over NCCL / NVLink. d_w2 is final first, so its all-reduce is launched
-    (async, NCCL's own stream) while d_w1 and d_x are still being computed.
+    over NCCL / NVLink. With the hook the backward runs dW2, dW1, then dX:
+    each all-reduce is launched (async, NCCL's own stream) as soon as its
+    gradient is final, dW2's overlapping dW1 and dX, dW1's overlapping dX.
 
 Nothing here is in the reference (distributed training is a reference
 non-goal, ref SPEC.md:486); it is the multi-GPU plumbing the north star asks
@@ -75,7 +76,8 @@ def train_step(x_shard, g_shard, params, cfg, group=None, global_plan: bool = Tr
     rank's own permutation), i.e. the reference applied per shard.
 
     The backward hands d_w2 to the all-reducer as soon as it is final (right
-    after K3), so its all-reduce overlaps dX and dW1; d_w1's follows."""
+    after K3) and computes dW1 before dX, so both all-reduces overlap compute
+    (dW2's overlaps dW1 and dX, dW1's overlaps dX)."""
     from .ffn import ffn_backward, ffn_forward
 
     hook = None

@@ -740,16 +740,26 @@ def _ffn_backward(g_out, cache: FfnCache, p: FfnParams, cfg: FfnConfig, grad_rea
         ev_g = torch.cuda.Event()
         ev_g.record(side)
     # dW2 first (it needs only the forward's split of act, ready long before),
-    # K4(g_pre) next to it and next to dX, then dW1: K4(g_pre) gets two GEMMs
-    # to hide under instead of one, and a data-parallel step's dW2 all-reduce
-    # overlaps dX and dW1
+    # with K4(g_pre) next to it. Alone: dX, then dW1, so K4(g_pre) has two
+    # GEMMs to hide under. With a grad_ready hook (data parallel): dW1 before
+    # dX, so both weight-gradient all-reduces overlap compute (dW2's overlaps
+    # dW1 and dX, dW1's overlaps dX) instead of dW1's trailing the step. On one
+    # GPU the two orders take the same time (1.837 vs 1.844 ms median, 1.814
+    # both min, 16 interleaved blocks, scripts/ab_step.py); K4(g_pre) ends
+    # before dW2 does (profiles/r02/timeline_queued_c2.txt).
     main.wait_event(cache.side_ready)
     split_weight_grad(fa, plan, g_c, npad, d_w2, transposed=False)
     notify("d_w2", d_w2)
-    _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
-    main.wait_event(ev_g)
-    split_weight_grad(fg, plan, x_in, npad, d_w1, transposed=True)
-    notify("d_w1", d_w1)
+    if grad_ready is not None:
+        main.wait_event(ev_g)
+        split_weight_grad(fg, plan, x_in, npad, d_w1, transposed=True)
+        notify("d_w1", d_w1)
+        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
+    else:
+        _dx(cfg, g_vals, g_pre_dense, cache, p, d_x, n, d, h, s, census)
+        main.wait_event(ev_g)
+        split_weight_grad(fg, plan, x_in, npad, d_w1, transposed=True)
+        notify("d_w1", d_w1)
     census.insert(1, GemmEvent("bwd.d_w2", True, macs_w))
     census.insert(2, GemmEvent("bwd.d_w1", True, macs_w))
     return FfnGrads(d_w1, d_w2, d_x, None, census, fa.stats, fg.stats,
