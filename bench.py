@@ -845,8 +845,34 @@ def run_e2e(torch, dist, s24, args, world, prefill, params, recipe, x, dy, flush
     st, en = run(args.steps)
     barrier()
     t_e2e = max_over_ranks(st.elapsed_time(en))
-    return {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e / args.steps, "path": path}
+    res = {"value": world * n * args.steps / (t_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e / args.steps, "path": path}
+    if world == 1:
+        # the same copies with no compute: the PCIe floor of this e2e step
+        devs = (g_a.x,) if prefill else (g_a.x, g_a.dy)
+        ins = (xh,) if prefill else (xh, gh)
+        outs = outs_of(g_a)
+        s_out.wait_stream(comp)
+        s_in.wait_stream(comp)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(comp)
+        s_in.wait_event(c0)
+        s_out.wait_event(c0)
+        for _ in range(args.steps):
+            with torch.cuda.stream(s_in):
+                for dv, hb in zip(devs, ins):
+                    dv.copy_(hb, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for hb, dv in zip(hosts, outs):
+                    hb.copy_(dv, non_blocking=True)
+        comp.wait_stream(s_in)
+        comp.wait_stream(s_out)
+        c1.record(comp)
+        torch.cuda.synchronize()
+        floor = c0.elapsed_time(c1) / args.steps
+        res["copy_floor_ms_per_step"] = floor
+        res["frac_of_copy_floor"] = floor / res["ms_per_step"]
+    return res
 
 
 def main():
