@@ -40,6 +40,7 @@ am = torch.empty_like(cache.act_meta)
 fa, plan = cache.act_split, cache.plan
 calls = {
     "k1": lambda: _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(av), P(am), P(cnt), P(stats), None, S),
+    "k1nc": lambda: _lib.call("s24_fwd_gemm1_fused", P(x), d, P(w1), h, n, h, d, P(av), P(am), None, None, None, S),
     "k3": lambda: _lib.call("s24_bwd_dact_fused", P(dy), d, P(w2), d, n, h, d, P(cache.act_vals), P(cache.act_meta),
                             P(gv), S),
     "fwdout": lambda: _lib.call("s24_spmm", P(cache.act_vals), P(cache.act_meta), P(w2), 1, d, n, d, h, P(o), 1, d,
