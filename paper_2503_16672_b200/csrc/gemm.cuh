@@ -60,7 +60,8 @@
 #endif
 // S24_PROBE (experiments only): 1 = MMA issue without operand loads (stale
 // shared memory), 2 = operand loads without MMAs, 3 = as 1 without the 2:4
-// metadata copies into TMEM. Results are garbage.
+// metadata copies into TMEM, 5 = the full kernel without those copies.
+// Results are garbage.
 #ifndef S24_PROBE
 #define S24_PROBE 0
 #endif
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
             e_tmem = tmem_base + Cfg::E_COL + stage * (4 * Cfg::E_ATOMS);
 #pragma unroll
             for (int a = 0; a < Cfg::E_ATOMS; ++a) {
-              if (S24_PROBE == 2 || S24_PROBE == 3) break;
+              if (S24_PROBE == 2 || S24_PROBE == 3 || S24_PROBE == 5) break;
               const uint64_t edesc = make_sdesc(sb + Cfg::B_BYTES + 2048 * a, 0, 128, kLayoutNone);
               if constexpr (CG == 2)
                 tmem_cp_128x128b_cg2(e_tmem + 4 * a, edesc);
