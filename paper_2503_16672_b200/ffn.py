@@ -344,10 +344,11 @@ def ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None = None, 
     (inference prefill) skips what only the backward needs: the token
     permutation (every forward stage maps one token row to one output row, so
     the output is the same bits), x_in and the feature-wise split.
-    counts_hook(counts): called on the current stream right after K1 with the
-    int32 per-feature nonzero counts, before the split plan is computed from
-    them (data parallelism all-reduces them here so that every rank uses the
-    plan of the global batch).
+    counts_hook(counts): called right after K1 with the int32 per-feature
+    nonzero counts, before the split plan is computed from them, with the
+    side stream that computes the plan current: data parallelism all-reduces
+    them here (every rank then uses the plan of the global batch) while fwd.out
+    runs on the caller's stream.
 
     Any d and h % 4 == 0 (the reference's shapes): the device GEMMs tile the
     model dim by 32 and the hidden width by 128, so other sizes run on the FFN
@@ -501,8 +502,6 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
     _lib.call("s24_fwd_gemm1_fused", ptr(k1_in), d, ptr(p.w1), h, n, h, d, ptr(act_vals), ptr(act_meta),
               ptr(counts), ptr(stats_dev), ptr(pre), s)
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
-    if counts_hook is not None:
-        counts_hook(counts)
 
     # fwd.out on tensor cores (inverse permutation as its epilogue row map)
     # and next to it, on the side stream: the split plan (K7, one small CTA
@@ -512,6 +511,9 @@ def _ffn_forward(x, p: FfnParams, cfg: FfnConfig, plan: SplitPlan | None, keep_p
     main = torch.cuda.current_stream()
     side = side_stream(dev)
     side.wait_stream(main)
+    if counts_hook is not None:
+        with torch.cuda.stream(side):  # (a collective here overlaps fwd.out)
+            counts_hook(counts)
     _lib.call("s24_spmm", ptr(act_vals), ptr(act_meta), ptr(p.w2), 1, d, n, d, h, ptr(out), _lib.BF16, d,
               ptr(inv_dev), 0, -1, None, 0, s)
     census.append(GemmEvent("fwd.out", True, sp_gemm_macs(n, h, d)))

@@ -375,8 +375,6 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     _lib.call("s24_fwd_gemm1_f8", ptr(xq), xq.stride(0), ptr(w1q), w1q.stride(0), n, h, d, ptr(sx),
               ptr(s1), ptr(vals32), ptr(amax), ptr(act_meta), ptr(counts), ptr(stats_dev), ptr(pre), stream())
     census.append(GemmEvent("fwd.pre_act", False, gemm_macs(n, d, h)))
-    if counts_hook is not None:
-        counts_hook(counts)
     _, sa = quant_rows(vals32, rows=n, amax=amax, codes=aq, deq=act_vals, raw=act_raw)
     meta8 = meta_to_f8(act_meta, n, h)
     if plan is not None and plan.hidden_dim != (h_valid or h):
@@ -390,6 +388,9 @@ def ffn_forward_f8(x: torch.Tensor, p, cfg, plan, keep_pre_act: bool, for_backwa
     naive_plan = _all_sparse_plan(h, dev) if cfg.backward_mode == "naive_sparse" else None
     ev_k1 = ov.record(ov.main)
     ov.fork(ev_k1)
+    if counts_hook is not None:
+        with torch.cuda.stream(ov.st):  # (a collective here overlaps fwd.out, as in ffn.py)
+            counts_hook(counts)
     plan_api = plan_out = plan
     if cfg.backward_mode == "split_masked" or plan is not None:  # (allocations only here)
         plan_api, plan_out = _plan_split(counts, cfg.split_ratio, plan, h, h_valid, ov.st)
