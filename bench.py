@@ -83,9 +83,8 @@ def peaks():
 # --------------------------------------------------------------------------- CPU reference (oracle port)
 
 
-def measured_traffic(label: str):
-    """DRAM bytes (read + write) per launch of a kernel, from the newest
-    committed ncu --set full capture (profiles/rNN/traffic.json), or None."""
+def traffic_entry(label: str):
+    """The newest committed ncu figures for a kernel (profiles/rNN/traffic.json), or None."""
     for f in sorted(Path(__file__).resolve().parent.glob("profiles/r*/traffic.json"), reverse=True):
         try:
             table = json.loads(f.read_text())
@@ -94,8 +93,30 @@ def measured_traffic(label: str):
         # keys are label prefixes (shapes may follow in the live label)
         t = next((v for k, v in table.items() if label.startswith(k)), None)
         if t:
-            return t["traffic_bytes"], f"{t['profile']} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
+            return t
+    return None
+
+
+def measured_traffic(label: str):
+    """DRAM bytes (read + write) per launch of a kernel, from the newest
+    committed ncu --set full capture (profiles/rNN/traffic.json), or None."""
+    t = traffic_entry(label)
+    if t:
+        return t["traffic_bytes"], f"{t['profile']} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
     return None, None
+
+
+def operand_feed(label: str, avg_launch_s: float):
+    """The L2 -> SM operand bytes of one launch (ncu) against the same kernel's
+    feed-only rate (its TMA operand ring run without MMAs, S24_PROBE=2): the
+    resource that bounds the 2:4 GEMMs. None if not captured."""
+    t = traffic_entry(label)
+    if not t or "l2_to_sm_bytes" not in t or avg_launch_s <= 0:
+        return None
+    b = t["l2_to_sm_bytes"]
+    ach, cap = b / avg_launch_s / 1e12, b / t["feed_only_s"] / 1e12
+    return {"bytes_per_launch": b, "achieved": ach, "feed_only": cap, "unit": "TB/s", "frac": ach / cap,
+            "source": f"{t['l2_to_sm_source']}; {t['feed_only_source']}"}
 
 
 REF_DIR = ROOT / "baseline" / "_ref"
@@ -691,6 +712,9 @@ def run_ours(args):
                           "frac": dom["frac"], "traffic": traffic, "traffic_source": traffic_src,
                           "peak_source": f"{pk['source']} (MEASURED_PEAKS.json bf16 burst / hbm copy"
                                          f"{'; 2:4 sparse peak = 2x dense, derived' if 'sparse' in dom['kernel'] or 'spmm' in dom['kernel'] else ''})"}
+    feed = operand_feed(dom["kernel"], dom["ms_per_step"] / max(dom["launches_per_step"], 1e-9) / 1e3)
+    if feed:
+        result["roofline"]["operand_feed"] = feed
     if sparsify_kernels:
         result["sparsify_kernels"] = sparsify_kernels
     result["kernels"] = kernels
