@@ -1,5 +1,5 @@
 """Run one c2-shaped GEMM of the step repeatedly (for ncu captures):
-usage: python scripts/gemm_probe.py {k1|k3|relu2|dact|fwdout|dx|dw|dense|k4|gather|plan}[,...] [--iters 5]
+usage: python scripts/gemm_probe.py {k1|k1nc|k3|relu2|dact|fwdout|dx|dw|dense|k4|gather|plan}[,...] [--iters 5]
 --time prints the median CUDA-event time per call instead; with S24_LIB pointing at an
 S24_PROBE build (MMA-only / feed-only, csrc/gemm.cuh) it gives profiles/r02/gemm_ceilings_c2.txt.
 ncu: the step that builds the operands launches 6 gemm_kernel, 2 k_feature_split_x, 2 k_gather_rows and
